@@ -1,0 +1,97 @@
+/*
+ * fvv.h — C ABI of the B200 free-viewpoint-video hot path (libfvv.so).
+ *
+ * Plain pointers and sizes only: no torch types cross this boundary. All
+ * array arguments named *_dev are device pointers owned by the caller; all
+ * other pointers are host memory read during the call (camera and grid
+ * tables are copied into the kernel parameter block, so the call is CUDA
+ * graph capturable). `stream` is a cudaStream_t (NULL = legacy default).
+ * Every entry point returns 0 on success or a nonzero FVV_E_* code;
+ * fvv_last_error() then describes the failure (thread-local).
+ *
+ * Each function names the reference interface it replaces
+ * (/root/reference/pkg/src/freeview/<file>:<line>). The reference is a
+ * Python library with no FFI; INTEGRATION.md shows the ctypes binding a
+ * freeview maintainer would add for each entry point.
+ *
+ * Layouts
+ *   occupancy bits : grid g's voxel l = i + nx*(j + ny*k) (voxels.py:74-96)
+ *                    is bit (l & 31) of word occ_dev[word_off[g] + (l >> 5)].
+ *   silhouette bits: camera c's pixel (row y, column x) is bit (x & 31) of
+ *                    word sil_dev[sil_word_off[c] + y*ceil(W/32) + (x >> 5)].
+ *   meshes         : vertices float64 (V,3); triangles int32 (T,3).
+ */
+#ifndef FVV_H
+#define FVV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FVV_MAX_CAMS 64   /* kernels keep the rig in the parameter block */
+#define FVV_MAX_GRIDS 128 /* grids per batched carve / polygonize launch */
+
+#define FVV_OK 0
+#define FVV_E_ARG 1   /* invalid argument (message says which) */
+#define FVV_E_CUDA 2  /* CUDA launch / runtime error */
+#define FVV_E_LIMIT 3 /* exceeds FVV_MAX_CAMS / FVV_MAX_GRIDS / capacity */
+
+/* camera.py:28-101 CameraModel, flattened. R maps world -> camera
+ * (x_c = R x_w + t), row-major; dist order k1 k2 p1 p2 k3 (camera.py:156).
+ * has_distortion = any(dist != 0) (camera.py:67-68). 192 bytes. */
+typedef struct fvv_camera {
+    double R[9];
+    double t[3];
+    double fx, fy, cx, cy, skew;
+    double k1, k2, p1, p2, k3;
+    int32_t width, height, id, has_distortion;
+} fvv_camera;
+
+/* voxels.py:18-71 GridSpec: voxel centre = origin + spacing*(ijk + 0.5). */
+typedef struct fvv_grid {
+    double origin[3];
+    double spacing;
+    int64_t dims[3];
+} fvv_grid;
+
+/* hull.py:23-28 Component; bbox inclusive voxel indices. */
+typedef struct fvv_component {
+    int64_t id, voxel_count;
+    int64_t bbox_min[3], bbox_max[3];
+} fvv_component;
+
+const char *fvv_last_error(void);
+int fvv_version(void);
+/* Bytes of device workspace the *_workspace arguments below need. */
+size_t fvv_ccl_workspace_bytes(int64_t num_voxels);
+
+/* camera.py:164-201 project(cam, p, use_distortion) for n points (float64
+ * (n,3)); writes pixel (n,2), camera-frame z (n,), in_frustum (n,) 0/1.
+ * single_point selects numpy's 1-row BLAS order. */
+int fvv_project(const fvv_camera *cam, const double *pts_dev, int64_t n, int use_distortion,
+                int single_point, double *pixel_dev, double *z_dev, uint8_t *in_dev,
+                void *stream);
+
+/* Input side of hull.py:63-75 (_check_sils): uint8/bool masks, camera c's
+ * (H,W) row-major mask at masks_dev + mask_off[c], -> silhouette bits. */
+int fvv_pack_silhouettes(const fvv_camera *cams, int ncam, const uint8_t *masks_dev,
+                         const int64_t *mask_off, uint32_t *sil_dev, const int64_t *sil_word_off,
+                         void *stream);
+
+/* hull.py:78-119 carve / hull.py:287-302 dense_carve: one launch carves
+ * ngrid grids (the coarse stage grid, or every ROI grid) against the rig.
+ * Voxel ON iff in-frustum for >= min_views cameras and every camera that
+ * sees it hits foreground. Also writes per-grid ON counts (int64 [ngrid])
+ * to count_dev when non-NULL (zeroed by the call). */
+int fvv_carve(const fvv_camera *cams, int ncam, const uint32_t *sil_dev,
+              const int64_t *sil_word_off, const fvv_grid *grids, int ngrid,
+              const int64_t *word_off, int min_views, uint32_t *occ_dev,
+              int64_t *count_dev, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FVV_H */

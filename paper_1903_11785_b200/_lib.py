@@ -1,0 +1,88 @@
+"""ctypes binding of libfvv.so (the C ABI declared in include/fvv.h).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+present, every hot-path call raises. The library is built in-tree by
+``__graft_entry__.build()`` (``make -C paper_1903_11785_b200/csrc``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfvv.so")
+
+FVV_MAX_CAMS = 64
+FVV_MAX_GRIDS = 128
+FVV_OK, FVV_E_ARG, FVV_E_CUDA, FVV_E_LIMIT = 0, 1, 2, 3
+
+# include/fvv.h fvv_camera (192 bytes)
+CAM_DTYPE = np.dtype(
+    [
+        ("R", "<f8", (9,)), ("t", "<f8", (3,)),
+        ("fx", "<f8"), ("fy", "<f8"), ("cx", "<f8"), ("cy", "<f8"), ("skew", "<f8"),
+        ("k1", "<f8"), ("k2", "<f8"), ("p1", "<f8"), ("p2", "<f8"), ("k3", "<f8"),
+        ("width", "<i4"), ("height", "<i4"), ("id", "<i4"), ("has_distortion", "<i4"),
+    ]
+)
+# include/fvv.h fvv_grid (56 bytes)
+GRID_DTYPE = np.dtype([("origin", "<f8", (3,)), ("spacing", "<f8"), ("dims", "<i8", (3,))])
+# include/fvv.h fvv_component (64 bytes)
+COMP_DTYPE = np.dtype([("id", "<i8"), ("voxel_count", "<i8"), ("bbox_min", "<i8", (3,)),
+                       ("bbox_max", "<i8", (3,))])
+assert CAM_DTYPE.itemsize == 192 and GRID_DTYPE.itemsize == 56 and COMP_DTYPE.itemsize == 64
+
+# exported symbols; tests check the .so exports every one of them
+SYMBOLS = (
+    "fvv_last_error", "fvv_version", "fvv_ccl_workspace_bytes", "fvv_project",
+    "fvv_pack_silhouettes", "fvv_carve",
+)
+
+
+class FvvError(RuntimeError):
+    """A CUDA-side failure reported through the C ABI."""
+
+
+_lib = None
+
+
+def load():
+    """Load libfvv.so once; raise loudly if it was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                "g.build()'` (there is no CPU fallback for the hot path)"
+            )
+        lib = ctypes.CDLL(LIB_PATH)
+        lib.fvv_last_error.restype = ctypes.c_char_p
+        lib.fvv_ccl_workspace_bytes.restype = ctypes.c_size_t
+        lib.fvv_ccl_workspace_bytes.argtypes = [ctypes.c_int64]
+        _lib = lib
+    return _lib
+
+
+def call(name: str, *args) -> None:
+    """Invoke an fvv_* entry point and map its status to an exception."""
+    rc = getattr(load(), name)(*args)
+    if rc != FVV_OK:
+        msg = load().fvv_last_error().decode(errors="replace")
+        if rc in (FVV_E_ARG, FVV_E_LIMIT):
+            raise ValueError(msg)
+        raise FvvError(msg)
+
+
+def host_ptr(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def dev_ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def i64(v):
+    return ctypes.c_int64(int(v))

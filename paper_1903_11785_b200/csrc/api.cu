@@ -1,0 +1,126 @@
+// C-ABI plumbing (errors, version) plus the small camera kernels:
+// fvv_project (camera.py:164-201) and fvv_pack_silhouettes (hull.py:63-75).
+#include <cstdarg>
+#include <cstring>
+
+#include "fvv_common.cuh"
+
+namespace fvv {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_check(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return FVV_E_CUDA;
+  }
+  return FVV_OK;
+}
+
+__global__ void project_kernel(fvv_camera cam, const double *__restrict__ pts, int64_t n,
+                               bool use_dist, bool gemv, double *__restrict__ pix,
+                               double *__restrict__ zo, uint8_t *__restrict__ ino) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double u, v, z;
+    bool in = project_exact(cam, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], use_dist, gemv, u,
+                            v, z);
+    pix[2 * i] = u;
+    pix[2 * i + 1] = v;
+    zo[i] = z;
+    ino[i] = in;
+  }
+}
+
+struct PackParams {
+  int ncam;
+  const uint8_t *masks;
+  uint32_t *sil;
+  int64_t mask_off[FVV_MAX_CAMS];
+  int64_t sil_off[FVV_MAX_CAMS];
+  int32_t width[FVV_MAX_CAMS];
+  int32_t height[FVV_MAX_CAMS];
+  int64_t word_start[FVV_MAX_CAMS + 1];  // cumulative words over cameras
+};
+
+// One warp builds one 32-pixel word from 32 coalesced mask bytes (ballot).
+__global__ void pack_kernel(const __grid_constant__ PackParams p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * blockDim.x / 32;
+  const int64_t total = p.word_start[p.ncam];
+  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; w < total; w += warps) {
+    int c = 0;
+    while (w >= p.word_start[c + 1]) ++c;
+    int64_t local = w - p.word_start[c];
+    int stride = (p.width[c] + 31) >> 5;
+    int64_t row = local / stride;
+    int x = (int)(local - row * stride) * 32 + lane;
+    bool fg = false;
+    if (x < p.width[c]) fg = p.masks[p.mask_off[c] + row * p.width[c] + x] != 0;
+    uint32_t bits = __ballot_sync(0xffffffffu, fg);
+    if (lane == 0) p.sil[p.sil_off[c] + local] = bits;
+  }
+}
+
+}  // namespace fvv
+
+using namespace fvv;
+
+extern "C" {
+
+const char *fvv_last_error(void) { return g_err; }
+
+int fvv_version(void) { return 1; }
+
+int fvv_project(const fvv_camera *cam, const double *pts_dev, int64_t n, int use_distortion,
+                int single_point, double *pixel_dev, double *z_dev, uint8_t *in_dev,
+                void *stream) {
+  if (!cam || n < 0) {
+    set_error("fvv_project: bad arguments");
+    return FVV_E_ARG;
+  }
+  if (n == 0) return FVV_OK;
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  project_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(*cam, pts_dev, n, use_distortion != 0,
+                                                           single_point != 0, pixel_dev, z_dev,
+                                                           in_dev);
+  return cuda_check("fvv_project");
+}
+
+int fvv_pack_silhouettes(const fvv_camera *cams, int ncam, const uint8_t *masks_dev,
+                         const int64_t *mask_off, uint32_t *sil_dev, const int64_t *sil_word_off,
+                         void *stream) {
+  if (ncam < 1 || ncam > FVV_MAX_CAMS) {
+    set_error("fvv_pack_silhouettes: %d cameras (limit %d)", ncam, FVV_MAX_CAMS);
+    return ncam < 1 ? FVV_E_ARG : FVV_E_LIMIT;
+  }
+  PackParams p;
+  memset(&p, 0, sizeof(p));
+  p.ncam = ncam;
+  p.masks = masks_dev;
+  p.sil = sil_dev;
+  p.word_start[0] = 0;
+  for (int c = 0; c < ncam; ++c) {
+    p.mask_off[c] = mask_off[c];
+    p.sil_off[c] = sil_word_off[c];
+    p.width[c] = cams[c].width;
+    p.height[c] = cams[c].height;
+    p.word_start[c + 1] = p.word_start[c] + (int64_t)sil_stride_words(cams[c].width) * cams[c].height;
+  }
+  int64_t warps = p.word_start[ncam];
+  int64_t blocks = (warps * 32 + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  pack_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(p);
+  return cuda_check("fvv_pack_silhouettes");
+}
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+// Shared device helpers: the reference's float64 projection chain, bit
+// lookups, error plumbing. Every kernel TU is compiled with -fmad=false, so
+// `a*b + c` below rounds twice exactly like numpy; fma() is written out
+// only where the reference goes through OpenBLAS.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+
+#include "../../include/fvv.h"
+
+namespace fvv {
+
+constexpr int kCarveChunk = 1 << 20;  // hull.py:20 CARVE_CHUNK
+constexpr double kNearClip = 1.0;     // visibility.py:19 NEAR_CLIP_MM
+constexpr double kDegenerateArea = 1e-9;  // mesh.py:22
+
+void set_error(const char *fmt, ...);
+int cuda_check(const char *what);
+
+// camera.py:177 `pts @ R.T + t`: OpenBLAS gemm (>= 2 rows) accumulates
+// fma(z,R2, fma(y,R1, x*R0)); the 1-row gemv kernel fma(z,R2, fma(x,R0, y*R1)).
+__device__ __forceinline__ void world_to_cam(const fvv_camera &c, double x, double y, double z,
+                                             bool gemv, double &X, double &Y, double &Z) {
+  double a0 = gemv ? fma(x, c.R[0], y * c.R[1]) : fma(y, c.R[1], x * c.R[0]);
+  double a1 = gemv ? fma(x, c.R[3], y * c.R[4]) : fma(y, c.R[4], x * c.R[3]);
+  double a2 = gemv ? fma(x, c.R[6], y * c.R[7]) : fma(y, c.R[7], x * c.R[6]);
+  X = fma(z, c.R[2], a0) + c.t[0];
+  Y = fma(z, c.R[5], a1) + c.t[1];
+  Z = fma(z, c.R[8], a2) + c.t[2];
+}
+
+// camera.py:164-201 project() + camera.py:154-161 distort(), float64, in the
+// reference's evaluation order. Returns in_frustum; u, v unrounded pixel.
+__device__ __forceinline__ bool project_exact(const fvv_camera &c, double x, double y, double z,
+                                              bool use_dist, bool gemv, double &u, double &v,
+                                              double &zc) {
+  double X, Y, Z;
+  world_to_cam(c, x, y, z, gemv, X, Y, Z);
+  double sz = (Z != 0.0) ? Z : 1.0;
+  double xn = X / sz;
+  double yn = Y / sz;
+  double xd = xn, yd = yn;
+  if (use_dist && c.has_distortion) {
+    double r2 = xn * xn + yn * yn;
+    double radial = 1.0 + r2 * (c.k1 + r2 * (c.k2 + r2 * c.k3));
+    xd = xn * radial + 2.0 * c.p1 * xn * yn + c.p2 * (r2 + 2.0 * xn * xn);
+    yd = yn * radial + c.p1 * (r2 + 2.0 * yn * yn) + 2.0 * c.p2 * xn * yn;
+  }
+  u = c.fx * (xd + c.skew * yd) + c.cx;
+  v = c.fy * yd + c.cy;
+  zc = Z;
+  double iu = rint(u), iv = rint(v);  // np.rint: round half to even
+  return (Z > 0.0) && (iu >= 0.0) && (iu <= (double)(c.width - 1)) && (iv >= 0.0) &&
+         (iv <= (double)(c.height - 1));
+}
+
+// voxels.py:52-56 voxel centre.
+__device__ __forceinline__ void voxel_center(const fvv_grid &g, int64_t i, int64_t j, int64_t k,
+                                             double &x, double &y, double &z) {
+  x = g.origin[0] + g.spacing * ((double)i + 0.5);
+  y = g.origin[1] + g.spacing * ((double)j + 0.5);
+  z = g.origin[2] + g.spacing * ((double)k + 0.5);
+}
+
+__device__ __forceinline__ bool sil_bit(const uint32_t *__restrict__ plane, int stride_words,
+                                        int x, int y) {
+  uint32_t w = __ldg(plane + (int64_t)y * stride_words + (x >> 5));
+  return (w >> (x & 31)) & 1u;
+}
+
+inline int sil_stride_words(int width) { return (width + 31) >> 5; }
+
+}  // namespace fvv
