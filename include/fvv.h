@@ -65,8 +65,6 @@ typedef struct fvv_component {
 
 const char *fvv_last_error(void);
 int fvv_version(void);
-/* Bytes of device workspace the *_workspace arguments below need. */
-size_t fvv_ccl_workspace_bytes(int64_t num_voxels);
 
 /* camera.py:164-201 project(cam, p, use_distortion) for n points (float64
  * (n,3)); writes pixel (n,2), camera-frame z (n,), in_frustum (n,) 0/1.

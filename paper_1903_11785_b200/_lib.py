@@ -37,7 +37,7 @@ assert CAM_DTYPE.itemsize == 192 and GRID_DTYPE.itemsize == 56 and COMP_DTYPE.it
 
 # exported symbols; tests check the .so exports every one of them
 SYMBOLS = (
-    "fvv_last_error", "fvv_version", "fvv_ccl_workspace_bytes", "fvv_project",
+    "fvv_last_error", "fvv_version", "fvv_project",
     "fvv_pack_silhouettes", "fvv_carve",
 )
 
@@ -60,8 +60,6 @@ def load():
             )
         lib = ctypes.CDLL(LIB_PATH)
         lib.fvv_last_error.restype = ctypes.c_char_p
-        lib.fvv_ccl_workspace_bytes.restype = ctypes.c_size_t
-        lib.fvv_ccl_workspace_bytes.argtypes = [ctypes.c_int64]
         _lib = lib
     return _lib
 
