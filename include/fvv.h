@@ -89,6 +89,41 @@ int fvv_carve(const fvv_camera *cams, int ncam, const uint32_t *sil_dev,
               const int64_t *word_off, int min_views, uint32_t *occ_dev,
               int64_t *count_dev, void *stream);
 
+/* ---- B-2: hull.py:122-269 ------------------------------------------------ */
+
+/* Device workspace fvv_ccl26 needs for `grid` (compacted ON-voxel ranks,
+ * union-find forest, per-component stats). */
+size_t fvv_ccl_workspace_bytes(const fvv_grid *grid);
+
+/* hull.py:218-254 label_components: 26-connected labelling of occ_dev.
+ * Labels 1..n ascend with each component's minimum linear index (the
+ * reference's canonical numbering). Writes min(n, comp_cap) component
+ * records (id, count, inclusive bbox) to comps_dev and {n_on, n} to
+ * counts_dev[0..1]; the labelling itself stays in the workspace. */
+int fvv_ccl26(const uint32_t *occ_dev, const fvv_grid *grid, void *ws_dev, size_t ws_bytes,
+              fvv_component *comps_dev, int64_t comp_cap, int64_t *counts_dev, void *stream);
+
+/* Re-export component records from a labelled workspace (larger buffer). */
+int fvv_ccl_components(const fvv_grid *grid, const void *ws_dev, fvv_component *comps_dev,
+                       int64_t comp_cap, void *stream);
+
+/* Dense int32 labels (0 = background) of a labelled workspace: the
+ * reference's Labeling.labels (hull.py:31-34). */
+int fvv_ccl_labels(const fvv_grid *grid, const void *ws_dev, int32_t *labels_dev, void *stream);
+
+/* hull.py:257-269 filter_noise on a labelled workspace: keep_dev[label]
+ * (uint8, indexed 0..n) selects survivors, ids unchanged. Writes the
+ * filtered dense labels and/or occupancy bits (either may be NULL) and the
+ * surviving voxel count. */
+int fvv_filter_labels(const fvv_grid *grid, const void *ws_dev, const uint8_t *keep_dev,
+                      int32_t *labels_dev, uint32_t *occ_dev, int64_t *kept_dev, void *stream);
+
+/* The same filter for a caller-supplied dense label array (nkeep entries
+ * in keep_dev). */
+int fvv_filter_dense(const int32_t *labels_in_dev, int64_t nvox, const uint8_t *keep_dev,
+                     int64_t nkeep, int32_t *labels_dev, uint32_t *occ_dev, int64_t *kept_dev,
+                     void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -38,7 +38,8 @@ assert CAM_DTYPE.itemsize == 192 and GRID_DTYPE.itemsize == 56 and COMP_DTYPE.it
 # exported symbols; tests check the .so exports every one of them
 SYMBOLS = (
     "fvv_last_error", "fvv_version", "fvv_project",
-    "fvv_pack_silhouettes", "fvv_carve",
+    "fvv_pack_silhouettes", "fvv_carve", "fvv_ccl_workspace_bytes", "fvv_ccl26",
+    "fvv_ccl_components", "fvv_ccl_labels", "fvv_filter_labels", "fvv_filter_dense",
 )
 
 
@@ -60,6 +61,7 @@ def load():
             )
         lib = ctypes.CDLL(LIB_PATH)
         lib.fvv_last_error.restype = ctypes.c_char_p
+        lib.fvv_ccl_workspace_bytes.restype = ctypes.c_size_t
         _lib = lib
     return _lib
 

@@ -1,0 +1,371 @@
+// B-2: 26-connected component labelling, noise filter support
+// (hull.py:122-269).
+//
+// Works on the compacted set of ON voxels instead of the whole grid (the
+// coarse stage grid is ~0.6% ON): an ordered popcount scan over the
+// occupancy words gives every ON voxel its rank r (ranks ascend with the
+// linear index), so a union-find forest over ranks keeps the reference's
+// canonical numbering:
+//   1. rank scan      : word_prefix[w], on_list[r] = l, parent[r] = r
+//   2. union          : each ON voxel unites with its 13 lexicographically
+//                       negative 26-neighbours (hull.py:124-133); roots are
+//                       linked by atomicMin, so every root ends as its
+//                       component's minimum rank = minimum linear index
+//   3. flatten        : parent[r] = find(r)
+//   4. root scan      : label(root) = 1 + #roots before it — ascending
+//                       minimum linear index, as hull.py:195-197 numbers them
+//   5. stats          : per-label count and inclusive bbox with
+//                       warp-aggregated integer atomics (hull.py:201-214)
+// Integer-only and order independent; results are bit-identical to the
+// reference for every launch configuration (its block_dims independence,
+// tests/test_hull.py:159-168, holds trivially).
+#include <cstring>
+
+#include "scan.cuh"
+
+namespace fvv {
+
+struct CclWs {
+  int64_t *counts;     // [0] n_on, [1] ncomp
+  int64_t *sums;       // scan chunk sums
+  int32_t *word_prefix;
+  int32_t *on_list;
+  int32_t *parent;
+  int32_t *rank_label;
+  int32_t *stats;      // [ncomp][8]: count, min ijk, max ijk, pad
+  int64_t words, nvox, comp_cap;
+};
+
+static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+// Most components a 26-connected grid can hold: one per 2x2x2 block.
+static int64_t max_components(const int64_t *dims) {
+  return ((dims[0] + 1) / 2) * ((dims[1] + 1) / 2) * ((dims[2] + 1) / 2);
+}
+
+static CclWs ccl_layout(void *base, const int64_t *dims) {
+  CclWs w;
+  char *p = (char *)base;
+  const int64_t nvox = dims[0] * dims[1] * dims[2];
+  w.nvox = nvox;
+  w.words = (nvox + 31) / 32;
+  w.comp_cap = max_components(dims);
+  w.counts = (int64_t *)p;
+  p += align256(4 * sizeof(int64_t));
+  w.sums = (int64_t *)p;
+  p += align256(sizeof(int64_t) * scan_chunks(nvox > w.words ? nvox : w.words));
+  w.word_prefix = (int32_t *)p;
+  p += align256(sizeof(int32_t) * w.words);
+  w.on_list = (int32_t *)p;
+  p += align256(sizeof(int32_t) * nvox);
+  w.parent = (int32_t *)p;
+  p += align256(sizeof(int32_t) * nvox);
+  w.rank_label = (int32_t *)p;
+  p += align256(sizeof(int32_t) * nvox);
+  w.stats = (int32_t *)p;
+  p += align256(sizeof(int32_t) * 8 * w.comp_cap);
+  return w;
+}
+
+static size_t ccl_bytes(const int64_t *dims) {
+  CclWs w = ccl_layout(nullptr, dims);
+  return (size_t)((char *)w.stats - (char *)nullptr) + align256(sizeof(int32_t) * 8 * w.comp_cap);
+}
+
+// -- 1. rank scan over occupancy words --------------------------------------
+struct WordRank {
+  const uint32_t *occ;
+  int32_t *word_prefix, *on_list, *parent;
+  int64_t words, nvox;
+  __device__ uint32_t word(int64_t w) const {
+    uint32_t v = occ[w];
+    if (w == words - 1 && (nvox & 31)) v &= (1u << (nvox & 31)) - 1u;
+    return v;
+  }
+  __device__ int64_t value(int64_t w) const { return __popc(word(w)); }
+  __device__ void emit(int64_t w, int64_t prefix, int64_t) const {
+    word_prefix[w] = (int32_t)prefix;
+    uint32_t v = word(w);
+    int32_t r = (int32_t)prefix;
+    while (v) {
+      int b = __ffs(v) - 1;
+      v &= v - 1;
+      on_list[r] = (int32_t)(w * 32 + b);
+      parent[r] = r;
+      ++r;
+    }
+  }
+};
+
+__device__ __forceinline__ int32_t uf_find(const int32_t *parent, int32_t x) {
+  int32_t p = __ldcg(parent + x);
+  while (p != x) {
+    x = p;
+    p = __ldcg(parent + x);
+  }
+  return x;
+}
+
+// Link the two trees; the smaller root wins (hull.py:146-153 links likewise).
+__device__ __forceinline__ void uf_unite(int32_t *parent, int32_t a, int32_t b) {
+  bool done;
+  do {
+    a = uf_find(parent, a);
+    b = uf_find(parent, b);
+    if (a < b) {
+      int32_t old = atomicMin(parent + b, a);
+      done = (old == b);
+      b = old;
+    } else if (b < a) {
+      int32_t old = atomicMin(parent + a, b);
+      done = (old == a);
+      a = old;
+    } else {
+      done = true;
+    }
+  } while (!done);
+}
+
+__device__ __forceinline__ bool occ_bit(const uint32_t *occ, int64_t l) {
+  return (__ldg(occ + (l >> 5)) >> (l & 31)) & 1u;
+}
+
+__device__ __forceinline__ int32_t rank_of(const uint32_t *occ, const int32_t *word_prefix,
+                                           int64_t l) {
+  uint32_t w = __ldg(occ + (l >> 5));
+  return word_prefix[l >> 5] + __popc(w & ((1u << (l & 31)) - 1u));
+}
+
+// -- 2. union over the 13 negative neighbours --------------------------------
+__global__ void ccl_union_kernel(const uint32_t *__restrict__ occ, CclWs w, int64_t nx, int64_t ny,
+                                 int64_t nz) {
+  const int64_t n_on = *(volatile int64_t *)w.counts;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_on;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = w.on_list[r];
+    const int64_t i = l % nx, j = (l / nx) % ny, k = l / (nx * ny);
+#pragma unroll
+    for (int o = 0; o < 13; ++o) {
+      // offsets with (dk, dj, di) lexicographically negative (hull.py:124-133)
+      const int dk = o < 9 ? -1 : 0;
+      const int rem = o < 9 ? o : o - 9;
+      const int dj = rem / 3 - 1;
+      const int di = rem % 3 - 1;
+      const int64_t ii = i + di, jj = j + dj, kk = k + dk;
+      if (ii < 0 || jj < 0 || kk < 0 || ii >= nx || jj >= ny || kk >= nz) continue;
+      const int64_t m = ii + nx * (jj + ny * kk);
+      if (!occ_bit(occ, m)) continue;
+      uf_unite(w.parent, (int32_t)r, rank_of(occ, w.word_prefix, m));
+    }
+  }
+}
+
+// -- 3. flatten ----------------------------------------------------------------
+__global__ void ccl_flatten_kernel(CclWs w) {
+  const int64_t n_on = *(volatile int64_t *)w.counts;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_on;
+       r += (int64_t)gridDim.x * blockDim.x)
+    w.parent[r] = uf_find(w.parent, (int32_t)r);
+}
+
+// -- 4. label roots in rank order --------------------------------------------
+struct RootLabel {
+  const int32_t *parent;
+  int32_t *rank_label;
+  __device__ int64_t value(int64_t r) const { return parent[r] == (int32_t)r; }
+  __device__ void emit(int64_t r, int64_t prefix, int64_t v) const {
+    if (v) rank_label[r] = (int32_t)(prefix + 1);
+  }
+};
+
+__global__ void ccl_stats_init_kernel(CclWs w) {
+  const int64_t ncomp = *(volatile int64_t *)(w.counts + 1);
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ncomp;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    int32_t *s = w.stats + 8 * c;
+    s[0] = 0;
+    s[1] = s[2] = s[3] = 0x7fffffff;
+    s[4] = s[5] = s[6] = -1;
+    s[7] = 0;
+  }
+}
+
+// -- 5. per-rank label + component count/bbox ----------------------------------
+__global__ void ccl_stats_kernel(CclWs w, int64_t nx, int64_t ny) {
+  const int64_t n_on = *(volatile int64_t *)w.counts;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; r0 < n_on;
+       r0 += stride) {
+    const int64_t r = r0 + lane;
+    const bool act = r < n_on;
+    int32_t lab = 0;
+    unsigned i = 0, j = 0, k = 0;
+    if (act) {
+      const int32_t root = w.parent[r];
+      lab = w.rank_label[root];
+      if (root != (int32_t)r) w.rank_label[r] = lab;
+      const int64_t l = w.on_list[r];
+      i = (unsigned)(l % nx);
+      j = (unsigned)((l / nx) % ny);
+      k = (unsigned)(l / (nx * ny));
+    }
+    const unsigned grp = __match_any_sync(0xffffffffu, act ? lab : -1);
+    const unsigned mn_i = __reduce_min_sync(grp, i), mx_i = __reduce_max_sync(grp, i);
+    const unsigned mn_j = __reduce_min_sync(grp, j), mx_j = __reduce_max_sync(grp, j);
+    const unsigned mn_k = __reduce_min_sync(grp, k), mx_k = __reduce_max_sync(grp, k);
+    if (act && lane == __ffs(grp) - 1) {
+      int32_t *s = w.stats + 8 * (int64_t)(lab - 1);
+      atomicAdd(s + 0, __popc(grp));
+      atomicMin(s + 1, (int32_t)mn_i);
+      atomicMin(s + 2, (int32_t)mn_j);
+      atomicMin(s + 3, (int32_t)mn_k);
+      atomicMax(s + 4, (int32_t)mx_i);
+      atomicMax(s + 5, (int32_t)mx_j);
+      atomicMax(s + 6, (int32_t)mx_k);
+    }
+  }
+}
+
+__global__ void ccl_export_kernel(CclWs w, fvv_component *out, int64_t cap) {
+  const int64_t ncomp = *(volatile int64_t *)(w.counts + 1);
+  const int64_t n = ncomp < cap ? ncomp : cap;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t *s = w.stats + 8 * c;
+    fvv_component rec;
+    rec.id = c + 1;
+    rec.voxel_count = s[0];
+    for (int d = 0; d < 3; ++d) {
+      rec.bbox_min[d] = s[1 + d];
+      rec.bbox_max[d] = s[4 + d];
+    }
+    out[c] = rec;
+  }
+}
+
+__global__ void ccl_expand_kernel(CclWs w, int32_t *labels) {
+  const int64_t n_on = *(volatile int64_t *)w.counts;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_on;
+       r += (int64_t)gridDim.x * blockDim.x)
+    labels[w.on_list[r]] = w.rank_label[r];
+}
+
+// hull.py:257-269: keep[label] selects survivors; ids are not renumbered.
+__global__ void ccl_filter_kernel(CclWs w, const uint8_t *__restrict__ keep, int32_t *labels,
+                                  uint32_t *occ_out, int64_t *kept) {
+  const int64_t n_on = *(volatile int64_t *)w.counts;
+  int64_t mine = 0;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_on;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t lab = w.rank_label[r];
+    if (!keep[lab]) continue;
+    const int64_t l = w.on_list[r];
+    if (labels) labels[l] = lab;
+    if (occ_out) atomicOr(occ_out + (l >> 5), 1u << (l & 31));
+    ++mine;
+  }
+  if (kept && mine) atomicAdd((unsigned long long *)kept, (unsigned long long)mine);
+}
+
+// Same filter for a caller-supplied dense label array (no CCL workspace).
+__global__ void dense_filter_kernel(const int32_t *__restrict__ in, int64_t nvox, int64_t nkeep,
+                                    const uint8_t *__restrict__ keep, int32_t *out,
+                                    uint32_t *occ_out, int64_t *kept) {
+  const int lane = threadIdx.x & 31;
+  int64_t mine = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t l0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; l0 < nvox;
+       l0 += stride) {
+    const int64_t l = l0 + lane;
+    int32_t lab = l < nvox ? in[l] : 0;
+    const bool on = lab > 0 && lab < nkeep && keep[lab];
+    if (l < nvox && out) out[l] = on ? lab : 0;
+    const uint32_t bits = __ballot_sync(0xffffffffu, on);
+    if (lane == 0) {
+      if (occ_out) occ_out[l0 >> 5] = bits;
+      mine += __popc(bits);
+    }
+  }
+  if (kept && mine) atomicAdd((unsigned long long *)kept, (unsigned long long)mine);
+}
+
+constexpr int kCclGrid = 148 * 8;
+
+}  // namespace fvv
+
+using namespace fvv;
+
+extern "C" {
+
+size_t fvv_ccl_workspace_bytes(const fvv_grid *grid) { return ccl_bytes(grid->dims); }
+
+int fvv_ccl26(const uint32_t *occ_dev, const fvv_grid *grid, void *ws_dev, size_t ws_bytes,
+              fvv_component *comps_dev, int64_t comp_cap, int64_t *counts_dev, void *stream) {
+  const int64_t nx = grid->dims[0], ny = grid->dims[1], nz = grid->dims[2];
+  const int64_t nvox = nx * ny * nz;
+  if (nvox <= 0 || nvox >= (1ll << 31)) {
+    set_error("fvv_ccl26: grid of %lld voxels (need 1 .. 2^31-1)", (long long)nvox);
+    return FVV_E_ARG;
+  }
+  if (ws_bytes < ccl_bytes(grid->dims)) {
+    set_error("fvv_ccl26: workspace %zu < %zu bytes", ws_bytes, ccl_bytes(grid->dims));
+    return FVV_E_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  CclWs w = ccl_layout(ws_dev, grid->dims);
+  cudaMemsetAsync(w.counts, 0, 4 * sizeof(int64_t), st);
+  WordRank wr{occ_dev, w.word_prefix, w.on_list, w.parent, w.words, nvox};
+  ordered_scan(wr, nullptr, w.words, w.sums, w.counts + 0, st);
+  ccl_union_kernel<<<kCclGrid, 256, 0, st>>>(occ_dev, w, nx, ny, nz);
+  ccl_flatten_kernel<<<kCclGrid, 256, 0, st>>>(w);
+  RootLabel rl{w.parent, w.rank_label};
+  ordered_scan(rl, w.counts + 0, 0, w.sums, w.counts + 1, st);
+  ccl_stats_init_kernel<<<kCclGrid, 256, 0, st>>>(w);
+  ccl_stats_kernel<<<kCclGrid, 256, 0, st>>>(w, nx, ny);
+  if (comps_dev) ccl_export_kernel<<<kCclGrid, 256, 0, st>>>(w, comps_dev, comp_cap);
+  if (counts_dev) cudaMemcpyAsync(counts_dev, w.counts, 2 * sizeof(int64_t),
+                                  cudaMemcpyDeviceToDevice, st);
+  return cuda_check("fvv_ccl26");
+}
+
+int fvv_ccl_components(const fvv_grid *grid, const void *ws_dev, fvv_component *comps_dev,
+                       int64_t comp_cap, void *stream) {
+  const int64_t nvox = grid->dims[0] * grid->dims[1] * grid->dims[2];
+  CclWs w = ccl_layout((void *)ws_dev, grid->dims);
+  ccl_export_kernel<<<kCclGrid, 256, 0, (cudaStream_t)stream>>>(w, comps_dev, comp_cap);
+  return cuda_check("fvv_ccl_components");
+}
+
+int fvv_ccl_labels(const fvv_grid *grid, const void *ws_dev, int32_t *labels_dev, void *stream) {
+  const int64_t nvox = grid->dims[0] * grid->dims[1] * grid->dims[2];
+  CclWs w = ccl_layout((void *)ws_dev, grid->dims);
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaMemsetAsync(labels_dev, 0, sizeof(int32_t) * nvox, st);
+  ccl_expand_kernel<<<kCclGrid, 256, 0, st>>>(w, labels_dev);
+  return cuda_check("fvv_ccl_labels");
+}
+
+int fvv_filter_labels(const fvv_grid *grid, const void *ws_dev, const uint8_t *keep_dev,
+                      int32_t *labels_dev, uint32_t *occ_dev, int64_t *kept_dev, void *stream) {
+  const int64_t nvox = grid->dims[0] * grid->dims[1] * grid->dims[2];
+  CclWs w = ccl_layout((void *)ws_dev, grid->dims);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (labels_dev) cudaMemsetAsync(labels_dev, 0, sizeof(int32_t) * nvox, st);
+  if (occ_dev) cudaMemsetAsync(occ_dev, 0, sizeof(uint32_t) * ((nvox + 31) / 32), st);
+  if (kept_dev) cudaMemsetAsync(kept_dev, 0, sizeof(int64_t), st);
+  ccl_filter_kernel<<<kCclGrid, 256, 0, st>>>(w, keep_dev, labels_dev, occ_dev, kept_dev);
+  return cuda_check("fvv_filter_labels");
+}
+
+int fvv_filter_dense(const int32_t *labels_in_dev, int64_t nvox, const uint8_t *keep_dev,
+                     int64_t nkeep, int32_t *labels_dev, uint32_t *occ_dev, int64_t *kept_dev,
+                     void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (kept_dev) cudaMemsetAsync(kept_dev, 0, sizeof(int64_t), st);
+  dense_filter_kernel<<<kCclGrid, 256, 0, st>>>(labels_in_dev, nvox, nkeep, keep_dev, labels_dev,
+                                                occ_dev, kept_dev);
+  return cuda_check("fvv_filter_dense");
+}
+
+}  // extern "C"

@@ -32,12 +32,47 @@ class Component:
     bbox_max: tuple
 
 
-@dataclass
 class Labeling:
-    """hull.py:31-34; ``labels`` is materialised from the GPU on first read."""
+    """hull.py:31-34: flat int32 ``labels`` (0 = background) and the
+    ``components`` list (ascending id).
 
-    labels: np.ndarray
-    components: list
+    A labelling produced on the GPU keeps its labels in device memory (the
+    CCL workspace, or a dense device array after filtering) and copies them
+    to the host only when ``labels`` is read."""
+
+    def __init__(self, labels=None, components=None, *, spec=None, ws=None, dense=None):
+        self.components = list(components or [])
+        self._labels = None if labels is None else np.asarray(labels, dtype=np.int32)
+        self._spec = spec
+        self._ws = ws
+        self._dense = dense
+
+    @property
+    def labels(self) -> np.ndarray:
+        if self._labels is None:
+            self._labels = self.device_labels().cpu().numpy()
+        return self._labels
+
+    @labels.setter
+    def labels(self, value) -> None:
+        self._labels = np.asarray(value, dtype=np.int32)
+        self._ws = self._dense = None
+
+    def device_labels(self) -> torch.Tensor:
+        """Dense int32 labels on the GPU."""
+        if self._dense is None:
+            if self._ws is not None:
+                n = self._spec.num_voxels
+                dense = torch.empty(n, dtype=torch.int32, device=self._ws.device)
+                _lib.call("fvv_ccl_labels", _lib.host_ptr(grid_table([self._spec])),
+                          _lib.dev_ptr(self._ws), _lib.dev_ptr(dense), stream_handle())
+                self._dense = dense
+            else:
+                self._dense = torch.from_numpy(self._labels).to(require_cuda())
+        return self._dense
+
+    def __repr__(self) -> str:
+        return f"Labeling(components={self.components!r})"
 
 
 @dataclass
@@ -120,6 +155,81 @@ def dense_carve(rig, sils, rois, fine_spacing: float, min_views: int = 1, worker
     if not specs:
         return []
     return carve_grids(_as_device_sils(rig, sils), specs, min_views)
+
+
+def _comps_from_records(rec) -> list:
+    return [Component(id=int(r["id"]), voxel_count=int(r["voxel_count"]),
+                      bbox_min=tuple(int(v) for v in r["bbox_min"]),
+                      bbox_max=tuple(int(v) for v in r["bbox_max"])) for r in rec]
+
+
+_COMP_PREFETCH = 4096  # component records copied back with the counts (one sync)
+
+
+def label_grid_async(grid: VoxelGrid):
+    """Launch fvv_ccl26 on ``grid``; returns (workspace, comps_dev, counts_dev)
+    without synchronising."""
+    dev = require_cuda()
+    tab = grid_table([grid.spec])
+    nbytes = int(_lib.load().fvv_ccl_workspace_bytes(_lib.host_ptr(tab)))
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    comps = torch.empty((_COMP_PREFETCH, _lib.COMP_DTYPE.itemsize), dtype=torch.uint8, device=dev)
+    counts = torch.zeros(2, dtype=torch.int64, device=dev)
+    _lib.call("fvv_ccl26", _lib.dev_ptr(grid.device_bits(dev)), _lib.host_ptr(tab),
+              _lib.dev_ptr(ws), ctypes.c_size_t(nbytes), _lib.dev_ptr(comps),
+              _lib.i64(_COMP_PREFETCH), _lib.dev_ptr(counts), stream_handle())
+    return ws, comps, counts
+
+
+def finish_labels(grid: VoxelGrid, ws, comps, counts) -> Labeling:
+    """Read the component table back (one sync) and wrap the labelling."""
+    n_on, ncomp = (int(v) for v in counts.cpu().tolist())
+    if ncomp > _COMP_PREFETCH:
+        comps = torch.empty((ncomp, _lib.COMP_DTYPE.itemsize), dtype=torch.uint8,
+                            device=ws.device)
+        _lib.call("fvv_ccl_components", _lib.host_ptr(grid_table([grid.spec])),
+                  _lib.dev_ptr(ws), _lib.dev_ptr(comps), _lib.i64(ncomp), stream_handle())
+    rec = comps[:ncomp].cpu().numpy().view(_lib.COMP_DTYPE).reshape(-1)
+    return Labeling(components=_comps_from_records(rec), spec=grid.spec, ws=ws)
+
+
+def label_components(grid: VoxelGrid, block_dims=(16, 16, 16)) -> Labeling:
+    """26-connected components labelling on the GPU (hull.py:218-254).
+
+    Ids 1..n ascend with each component's minimum linear voxel index, as in
+    the reference. ``block_dims`` is validated for API parity; the GPU
+    union-find's result does not depend on any decomposition (nor does the
+    reference's)."""
+    bx, by, bz = (int(b) for b in block_dims)
+    if min(bx, by, bz) < 1:
+        raise ValueError("block dims must be >= 1")
+    return finish_labels(grid, *label_grid_async(grid))
+
+
+def filter_noise(grid: VoxelGrid, lab: Labeling, params: NoiseFilterParams):
+    """Drop components whose voxel count is outside [t_small, t_large]
+    (hull.py:257-269); survivors keep their ids and voxels. Runs the
+    fvv_filter kernel over the device labelling."""
+    dev = require_cuda()
+    kept = [c for c in lab.components if params.keeps(c.voxel_count)]
+    keep = np.zeros(len(lab.components) + 1, dtype=np.uint8)
+    keep[[c.id for c in kept]] = 1
+    keep_d = torch.from_numpy(keep).to(dev)
+    n = grid.spec.num_voxels
+    labels = torch.empty(n, dtype=torch.int32, device=dev)
+    bits = torch.empty(max(words_for(n), 1), dtype=torch.int32, device=dev)
+    count = torch.zeros(1, dtype=torch.int64, device=dev)
+    if lab._ws is not None and lab._spec is not None and lab._spec.num_voxels == n:
+        _lib.call("fvv_filter_labels", _lib.host_ptr(grid_table([grid.spec])),
+                  _lib.dev_ptr(lab._ws), _lib.dev_ptr(keep_d), _lib.dev_ptr(labels),
+                  _lib.dev_ptr(bits), _lib.dev_ptr(count), stream_handle())
+    else:
+        src = lab.device_labels()
+        _lib.call("fvv_filter_dense", _lib.dev_ptr(src), _lib.i64(n), _lib.dev_ptr(keep_d),
+                  _lib.i64(len(keep)), _lib.dev_ptr(labels), _lib.dev_ptr(bits),
+                  _lib.dev_ptr(count), stream_handle())
+    return (VoxelGrid(grid.spec, bits=bits, count=count[0]),
+            Labeling(components=kept, spec=grid.spec, dense=labels))
 
 
 def extract_rois(lab: Labeling, spec: GridSpec, margin: float) -> list:
