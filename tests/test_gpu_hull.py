@@ -94,3 +94,83 @@ def test_carve_errors_match_reference_messages(gpu):
         carve(rig, [np.ones((8, 8), dtype=bool) for _ in rig], sp)
     with pytest.raises(ValueError, match="silhouettes for"):
         carve(rig, [], sp)
+
+
+def _comp_rows(comps):
+    return np.array([[c.id, c.voxel_count, *c.bbox_min, *c.bbox_max] for c in comps],
+                    dtype=np.int64).reshape(-1, 8)
+
+
+def test_ccl_matches_reference_golden(gpu):
+    from paper_1903_11785_b200.hull import NoiseFilterParams, filter_noise, label_components
+    from paper_1903_11785_b200.voxels import GridSpec, VoxelGrid
+
+    z = G.load("ccl")
+    for i in range(8):
+        dims = tuple(int(d) for d in z[f"g{i}_dims"])
+        spec = GridSpec(origin=(0, 0, 0), spacing=10.0, dims=dims)
+        grid = VoxelGrid(spec, G.unpack(z[f"g{i}_occ"], spec.num_voxels))
+        lab = label_components(grid)
+        assert np.array_equal(_comp_rows(lab.components), z[f"g{i}_comps"]), i
+        assert np.array_equal(lab.labels, z[f"g{i}_labels"]), i
+        fgrid, flab = filter_noise(grid, lab, NoiseFilterParams(t_small=3, t_large=40))
+        assert np.array_equal(flab.labels, z[f"g{i}_flabels"]), i
+        assert np.array_equal(fgrid.occ, z[f"g{i}_flabels"] > 0), i
+        assert fgrid.occupied_count == int((z[f"g{i}_flabels"] > 0).sum())
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_ccl_random_vs_oracle(gpu, seed):
+    from paper_1903_11785_b200.hull import label_components
+    from paper_1903_11785_b200.voxels import GridSpec, VoxelGrid
+
+    rng = np.random.default_rng(100 + seed)
+    for _ in range(5):
+        dims = tuple(int(d) for d in rng.integers(1, 70, 3))
+        dens = float(rng.choice([0.02, 0.1, 0.3, 0.6, 0.9]))
+        spec = GridSpec(origin=(0, 0, 0), spacing=1.0, dims=dims)
+        occ = rng.random(spec.num_voxels) < dens
+        lab = label_components(VoxelGrid(spec, occ))
+        ref_labels, ref_comps = O.label(occ, dims)
+        assert np.array_equal(lab.labels, ref_labels), (dims, dens)
+        assert np.array_equal(_comp_rows(lab.components), _comp_rows(ref_comps))
+
+
+def test_ccl_reference_kats(gpu):
+    """tests/test_hull.py:119-149 known answers."""
+    from paper_1903_11785_b200.hull import label_components
+    from paper_1903_11785_b200.voxels import GridSpec, VoxelGrid
+
+    spec = GridSpec(origin=(0, 0, 0), spacing=1.0, dims=(4, 4, 4))
+    lab = label_components(VoxelGrid(spec, np.zeros(64, dtype=bool)))
+    assert lab.components == [] and not lab.labels.any()
+    spec = GridSpec(origin=(0, 0, 0), spacing=1.0, dims=(3, 3, 3))
+    occ = np.zeros(27, dtype=bool)
+    occ[spec.linear_index(0, 0, 0)] = occ[spec.linear_index(1, 1, 1)] = True
+    lab = label_components(VoxelGrid(spec, occ))
+    assert len(lab.components) == 1 and lab.components[0].voxel_count == 2
+    spec = GridSpec(origin=(0, 0, 0), spacing=1.0, dims=(5, 1, 1))
+    lab = label_components(VoxelGrid(spec, np.array([True, False, True, True, False])))
+    assert [c.voxel_count for c in lab.components] == [1, 2]
+    assert lab.labels[0] == 1 and lab.labels[2] == 2
+    spec = GridSpec(origin=(0, 0, 0), spacing=1.0, dims=(6, 6, 6))
+    occ = np.zeros(spec.num_voxels, dtype=bool)
+    for ijk in [(1, 2, 3), (2, 2, 3), (2, 3, 4)]:
+        occ[spec.linear_index(*ijk)] = True
+    lab = label_components(VoxelGrid(spec, occ))
+    assert lab.components[0].bbox_min == (1, 2, 3) and lab.components[0].bbox_max == (2, 3, 4)
+    with pytest.raises(ValueError):
+        label_components(VoxelGrid(spec, occ), block_dims=(0, 1, 1))
+
+
+def test_coarse_labels_of_full_frames(gpu):
+    from paper_1903_11785_b200.hull import carve, label_components
+
+    for name in ("tiny_cli", "figures"):
+        z = G.load(name)
+        rig, sils = G.rig(z), G.sils(z)
+        spec = G.spec(z["coarse_spec"])
+        grid = carve(rig, sils, spec)
+        lab = label_components(grid)
+        assert np.array_equal(_comp_rows(lab.components), z["comps"])
+        assert np.array_equal(lab.labels, z["labels"])
