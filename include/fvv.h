@@ -124,6 +124,49 @@ int fvv_filter_dense(const int32_t *labels_in_dev, int64_t nvox, const uint8_t *
                      int64_t nkeep, int32_t *labels_dev, uint32_t *occ_dev, int64_t *kept_dev,
                      void *stream);
 
+/* ---- C: mesh.py:131-374 --------------------------------------------------- */
+
+/* Workspace of fvv_mesh_prepare / fvv_mesh_emit for a batch of grids. */
+size_t fvv_mesh_workspace_bytes(const fvv_grid *grids, int ngrid);
+
+/* Phase A of mesh.py:275-374 polygonize, batched over ngrid grids (their
+ * occupancy bits at occ_dev + word_off[g]): transposes occupancy into
+ * k-rows and scans intersected grid edges (vertices, in the reference's
+ * (axis, i, j, k) order) and surface cells. Grids with a dimension < 2
+ * yield empty meshes (mesh.py:298-299). Counts are read with
+ * fvv_mesh_counts. */
+int fvv_mesh_prepare(const fvv_grid *grids, int ngrid, const uint32_t *occ_dev,
+                     const int64_t *word_off, void *ws_dev, size_t ws_bytes, void *stream);
+
+/* Copies totals {V, S, T} (int64[3]) and per-grid info int64[ngrid][8] =
+ * {vbase, V, sbase, S, tbase, T, fallback_edges, inconsistent_starts}
+ * (IsovalueStats, mesh.py:225-228) out of the workspace. T fields are valid
+ * after fvv_mesh_emit. */
+int fvv_mesh_counts(const fvv_grid *grids, int ngrid, const void *ws_dev, int64_t *totals_dev,
+                    int64_t *info_dev, void *stream);
+
+/* Scratch fvv_mesh_emit needs for V vertices and S surface cells. */
+size_t fvv_mesh_emit_scratch_bytes(int64_t num_vertices, int64_t num_cells);
+
+/* Phase B: per-edge isovalues (exact: mesh.py:231-272 with cameras given in
+ * ascending id order; else fixed_iso), vertices p_on + lam*(p_off - p_on)
+ * (float64 [V][3], grid-major), triangles (int32 [<=5S][3], indices into
+ * verts_dev, slot-major per grid, winding reversed, area <= 1e-9 dropped). */
+int fvv_mesh_emit(const fvv_camera *cams_by_id, int ncam, const uint32_t *sil_dev,
+                  const int64_t *sil_word_off, const fvv_grid *grids, int ngrid,
+                  const uint32_t *occ_dev, const int64_t *word_off, int exact, double fixed_iso,
+                  void *ws_dev, size_t ws_bytes, int64_t num_vertices, int64_t num_cells,
+                  void *scratch_dev, size_t scratch_bytes, double *verts_dev, int32_t *tris_dev,
+                  void *stream);
+
+/* mesh.py:231-272 _edge_isovalues_batch on explicit endpoints (n,3):
+ * lam (n,), contributing camera id (n,) (-1 = fallback 0.5), stats int64[2]
+ * = {fallback_edges, inconsistent_starts}. */
+int fvv_edge_isovalues(const fvv_camera *cams_by_id, int ncam, const uint32_t *sil_dev,
+                       const int64_t *sil_word_off, const double *p_on_dev,
+                       const double *p_off_dev, int64_t n, double *lam_dev, int32_t *cam_dev,
+                       int64_t *stats_dev, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

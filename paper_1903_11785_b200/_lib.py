@@ -40,6 +40,8 @@ SYMBOLS = (
     "fvv_last_error", "fvv_version", "fvv_project",
     "fvv_pack_silhouettes", "fvv_carve", "fvv_ccl_workspace_bytes", "fvv_ccl26",
     "fvv_ccl_components", "fvv_ccl_labels", "fvv_filter_labels", "fvv_filter_dense",
+    "fvv_mesh_workspace_bytes", "fvv_mesh_prepare", "fvv_mesh_counts",
+    "fvv_mesh_emit_scratch_bytes", "fvv_mesh_emit", "fvv_edge_isovalues",
 )
 
 
@@ -62,6 +64,9 @@ def load():
         lib = ctypes.CDLL(LIB_PATH)
         lib.fvv_last_error.restype = ctypes.c_char_p
         lib.fvv_ccl_workspace_bytes.restype = ctypes.c_size_t
+        lib.fvv_mesh_workspace_bytes.restype = ctypes.c_size_t
+        lib.fvv_mesh_emit_scratch_bytes.restype = ctypes.c_size_t
+        lib.fvv_mesh_emit_scratch_bytes.argtypes = [ctypes.c_int64, ctypes.c_int64]
         _lib = lib
     return _lib
 

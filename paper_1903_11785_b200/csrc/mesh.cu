@@ -1,0 +1,791 @@
+// Stage C: marching cubes with silhouette-exact edge isovalues
+// (mesh.py:131-374), batched over every ROI grid of a frame.
+//
+// Layout: each grid's occupancy is first transposed into "rows" (one row
+// per (i, j), row index q = i*ny + j, C order) of ceil(nz/32) words holding
+// consecutive k. In that layout the reference's orderings become word
+// scans:
+//   * vertices: one per sign-changing grid edge, ordered by (axis, i, j, k)
+//     with k fastest (mesh.py:315-327 argwhere order). Edge-flag words
+//     along axis 0/1 are XORs of neighbouring rows, along axis 2 an XOR
+//     with the row shifted by one bit; an ordered popcount scan over
+//     (grid, axis, row, word) gives every vertex its index.
+//   * triangles: slot-major (TRI_TABLE triangle 0 of every surface cell in
+//     C order, then triangle 1, ...) (mesh.py:351-359), winding reversed
+//     (mesh.py:365), degenerate ones (area <= 1e-9 mm^2) dropped in place
+//     (mesh.py:372-373): a 5-lane ordered scan over surface cells.
+// Phase A (fvv_mesh_prepare) counts vertices and surface cells; the host
+// sizes the outputs from those counts; phase B (fvv_mesh_emit) computes
+// isovalues, vertices and triangles. All float64 work uses the reference's
+// operation order (fvv_common.cuh, -fmad=false).
+#include <cstring>
+
+#include "mc_cases.cuh"
+#include "scan.cuh"
+
+namespace fvv {
+
+__constant__ unsigned long long c_mc_edges[256];
+__constant__ unsigned char c_mc_ntri[256];
+
+// mesh.py:31-38 edge -> (base corner offset, axis), packed (di,dj,dk,axis)
+__constant__ unsigned char c_edge_base[12][4] = {
+    {0, 0, 0, 0}, {1, 0, 0, 1}, {0, 1, 0, 0}, {0, 0, 0, 1}, {0, 0, 1, 0}, {1, 0, 1, 1},
+    {0, 1, 1, 0}, {0, 0, 1, 1}, {0, 0, 0, 2}, {1, 0, 0, 2}, {1, 1, 0, 2}, {0, 1, 0, 2}};
+
+struct MeshGridInfo {
+  fvv_grid g;
+  int64_t occ_word_off;  // F-order occupancy words of this grid
+  int64_t rows, nzw;     // rows = nx*ny (0 when a dim < 2: empty mesh, mesh.py:298-299)
+  int64_t tw_off;        // transposed-word offset (S space); V space offset = 3*tw_off
+};
+
+struct MeshGrids {
+  int ngrid, exact;
+  double fixed_iso;
+  int64_t tw_total;
+  int64_t tw_start[FVV_MAX_GRIDS + 1];  // prefix of rows*nzw
+  MeshGridInfo gi[FVV_MAX_GRIDS];
+};
+
+struct MeshBufs {
+  const uint32_t *occ;
+  uint32_t *tw;        // transposed words [tw_total]
+  uint32_t *eflags;    // [3*tw_total]
+  int32_t *vprefix;    // [3*tw_total]
+  uint32_t *sflags;    // [tw_total]
+  int32_t *sprefix;    // [tw_total]
+  int64_t *sums;       // scan chunk sums
+  int64_t *totals;     // [0] V, [1] S, [2] T
+  int64_t *info;       // [ngrid][8]: vbase V sbase S tbase T fallback inconsistent
+  // phase B
+  int64_t *vert_key;   // [V] V-element*32 + bit
+  int64_t *cell_key;   // [S] S-element*32 + bit
+  int32_t *cell_mask;  // [S] case | keep<<8
+  int32_t *cprefix;    // [S][5]
+  int64_t *slot_base;  // [ngrid][5]
+  int64_t *cell_sums;
+  double *verts;       // [V][3]
+  int32_t *tris;       // [T][3] global vertex indices
+};
+
+enum { kInfoVbase, kInfoV, kInfoSbase, kInfoS, kInfoTbase, kInfoT, kInfoFallback, kInfoIncons };
+
+__device__ __forceinline__ int grid_of(const MeshGrids &G, int64_t e) {
+  // last g with tw_start[g] <= e < tw_start[g+1]
+  int lo = 0, hi = G.ngrid - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (G.tw_start[mid] <= e) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ uint32_t kmask(int64_t w, int64_t limit) {
+  // bits b of word w with 32*w + b < limit
+  const int64_t lo = w * 32;
+  if (limit <= lo) return 0u;
+  if (limit >= lo + 32) return 0xffffffffu;
+  return (1u << (limit - lo)) - 1u;
+}
+
+__device__ __forceinline__ uint32_t row_word(const uint32_t *tw, const MeshGridInfo &gi, int64_t q,
+                                             int64_t w) {
+  return (w < gi.nzw) ? tw[gi.tw_off + q * gi.nzw + w] : 0u;
+}
+
+// row word shifted so bit b holds k+1
+__device__ __forceinline__ uint32_t row_next(const uint32_t *tw, const MeshGridInfo &gi, int64_t q,
+                                             int64_t w) {
+  return (row_word(tw, gi, q, w) >> 1) | (row_word(tw, gi, q, w + 1) << 31);
+}
+
+// ---- A1: transpose F-order occupancy into k-rows --------------------------
+__global__ void mesh_transpose_kernel(const __grid_constant__ MeshGrids G, MeshBufs B) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < G.tw_total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int g = grid_of(G, e);
+    const MeshGridInfo &gi = G.gi[g];
+    const int64_t local = e - G.tw_start[g];
+    const int64_t q = local / gi.nzw, w = local - q * gi.nzw;
+    const int64_t nx = gi.g.dims[0], ny = gi.g.dims[1], nz = gi.g.dims[2];
+    const int64_t i = q / ny, j = q - i * ny;
+    uint32_t out = 0;
+    const int64_t kend = (w * 32 + 32 < nz) ? w * 32 + 32 : nz;
+    for (int64_t k = w * 32; k < kend; ++k) {
+      const int64_t l = i + nx * (j + ny * k);
+      const uint32_t word = __ldg(B.occ + gi.occ_word_off + (l >> 5));
+      out |= ((word >> (l & 31)) & 1u) << (k - w * 32);
+    }
+    B.tw[e] = out;
+  }
+}
+
+// ---- A2: vertex (edge-flag) scan over (grid, axis, row, word) ---------------
+struct EdgeFlags {
+  MeshGrids G;
+  const uint32_t *tw;
+  uint32_t *eflags;
+  int32_t *vprefix;
+  __device__ uint32_t compute(int64_t e) const {
+    // V space: grid g occupies [3*tw_start[g], 3*tw_start[g+1]), axis-major
+    const MeshGrids &g_ = G;
+    int lo = 0, hi = g_.ngrid - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (3 * g_.tw_start[mid] <= e) lo = mid; else hi = mid - 1;
+    }
+    const MeshGridInfo &gi = g_.gi[lo];
+    const int64_t per_axis = gi.rows * gi.nzw;
+    const int64_t local = e - 3 * g_.tw_start[lo];
+    const int axis = (int)(local / per_axis);
+    const int64_t rw = local - axis * per_axis;
+    const int64_t q = rw / gi.nzw, w = rw - q * gi.nzw;
+    const int64_t nx = gi.g.dims[0], ny = gi.g.dims[1], nz = gi.g.dims[2];
+    const int64_t i = q / ny, j = q - i * ny;
+    const uint32_t x = row_word(tw, gi, q, w);
+    uint32_t f;
+    if (axis == 0) {
+      f = (i < nx - 1) ? (x ^ row_word(tw, gi, q + ny, w)) & kmask(w, nz) : 0u;
+    } else if (axis == 1) {
+      f = (j < ny - 1) ? (x ^ row_word(tw, gi, q + 1, w)) & kmask(w, nz) : 0u;
+    } else {
+      f = (x ^ row_next(tw, gi, q, w)) & kmask(w, nz - 1);
+    }
+    return f;
+  }
+  __device__ int64_t value(int64_t e) const { return __popc(compute(e)); }
+  __device__ void emit(int64_t e, int64_t prefix, int64_t) const {
+    eflags[e] = compute(e);
+    vprefix[e] = (int32_t)prefix;
+  }
+};
+
+// ---- A3: surface-cell scan over (grid, row, word) ---------------------------
+struct CellFlags {
+  MeshGrids G;
+  const uint32_t *tw;
+  uint32_t *sflags;
+  int32_t *sprefix;
+  __device__ uint32_t compute(int64_t e) const {
+    const MeshGrids &g_ = G;
+    int lo = 0, hi = g_.ngrid - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (g_.tw_start[mid] <= e) lo = mid; else hi = mid - 1;
+    }
+    const MeshGridInfo &gi = g_.gi[lo];
+    const int64_t rw = e - g_.tw_start[lo];
+    const int64_t q = rw / gi.nzw, w = rw - q * gi.nzw;
+    const int64_t nx = gi.g.dims[0], ny = gi.g.dims[1], nz = gi.g.dims[2];
+    const int64_t i = q / ny, j = q - i * ny;
+    if (i >= nx - 1 || j >= ny - 1) return 0u;
+    const int64_t rows[4] = {q, q + ny, q + ny + 1, q + 1};
+    uint32_t any = 0u, all = 0xffffffffu;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const uint32_t a = row_word(tw, gi, rows[r], w), b = row_next(tw, gi, rows[r], w);
+      any |= a | b;
+      all &= a & b;
+    }
+    return (any & ~all) & kmask(w, nz - 1);
+  }
+  __device__ int64_t value(int64_t e) const { return __popc(compute(e)); }
+  __device__ void emit(int64_t e, int64_t prefix, int64_t) const {
+    sflags[e] = compute(e);
+    sprefix[e] = (int32_t)prefix;
+  }
+};
+
+// per-grid vertex / surface-cell bases and counts (prefix at grid starts)
+__global__ void mesh_grid_counts_kernel(const __grid_constant__ MeshGrids G, MeshBufs B) {
+  for (int g = threadIdx.x; g < G.ngrid; g += blockDim.x) {
+    const int64_t s0 = G.tw_start[g], s1 = G.tw_start[g + 1];
+    const int64_t vb = (3 * s0 < 3 * G.tw_total) ? B.vprefix[3 * s0] : B.totals[0];
+    const int64_t ve = (3 * s1 < 3 * G.tw_total) ? B.vprefix[3 * s1] : B.totals[0];
+    const int64_t sb = (s0 < G.tw_total) ? B.sprefix[s0] : B.totals[1];
+    const int64_t se = (s1 < G.tw_total) ? B.sprefix[s1] : B.totals[1];
+    int64_t *inf = B.info + 8 * g;
+    inf[kInfoVbase] = vb;
+    inf[kInfoV] = ve - vb;
+    inf[kInfoSbase] = sb;
+    inf[kInfoS] = se - sb;
+    inf[kInfoTbase] = 0;
+    inf[kInfoT] = 0;
+    inf[kInfoFallback] = 0;
+    inf[kInfoIncons] = 0;
+  }
+}
+
+// ---- B0: vertex list ----------------------------------------------------------
+__global__ void mesh_vertex_list_kernel(const __grid_constant__ MeshGrids G, MeshBufs B) {
+  const int64_t n = 3 * G.tw_total;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t f = B.eflags[e];
+    int64_t v = B.vprefix[e];
+    while (f) {
+      const int b = __ffs(f) - 1;
+      f &= f - 1;
+      B.vert_key[v++] = e * 32 + b;
+    }
+  }
+}
+
+
+// decode a V-space key -> grid, axis, (i, j, k)
+__device__ __forceinline__ int decode_vkey(const MeshGrids &G, int64_t key, int &axis, int64_t &i,
+                                           int64_t &j, int64_t &k) {
+  const int64_t e = key >> 5;
+  int lo = 0, hi = G.ngrid - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (3 * G.tw_start[mid] <= e) lo = mid; else hi = mid - 1;
+  }
+  const MeshGridInfo &gi = G.gi[lo];
+  const int64_t per_axis = gi.rows * gi.nzw;
+  const int64_t local = e - 3 * G.tw_start[lo];
+  axis = (int)(local / per_axis);
+  const int64_t rw = local - axis * per_axis;
+  const int64_t q = rw / gi.nzw, w = rw - q * gi.nzw;
+  const int64_t ny = gi.g.dims[1];
+  i = q / ny;
+  j = q - i * ny;
+  k = w * 32 + (key & 31);
+  return lo;
+}
+
+
+struct MeshCams {
+  int ncam;
+  int32_t sil_stride[FVV_MAX_CAMS];
+  int64_t sil_off[FVV_MAX_CAMS];
+  fvv_camera cams[FVV_MAX_CAMS];  // ascending camera id (mesh.py:165-167)
+};
+
+// mesh.py:131-162 closed-form Bresenham: pixel t of the segment a -> b.
+__device__ __forceinline__ void bresenham_px(int ax, int ay, int bx, int by, int t, int &x,
+                                             int &y) {
+  const int dx = abs(bx - ax), dy = abs(by - ay);
+  const int sx = bx >= ax ? 1 : -1, sy = by >= ay ? 1 : -1;
+  const int major = dx > dy ? dx : dy;
+  const bool xmajor = dx >= dy;
+  const long long dmaj = major > 1 ? major : 1;
+  const long long dmin = xmajor ? dy : dx;
+  const int tc = t < major ? t : major;
+  const int smin = (int)((2ll * tc * dmin + dmaj) / (2ll * dmaj));
+  x = ax + sx * (xmajor ? tc : smin);
+  y = ay + sy * (xmajor ? smin : tc);
+}
+
+// mesh.py:231-272 for one edge: cameras in ascending id order, only those
+// seeing both endpoints; Bresenham walk from rint(p_on) to rint(p_off);
+// lam_i = |last fg pixel - px_on| / |px_off - px_on| clipped to [0,1], 1 if
+// unconstrained, 0 if the start pixel is background; min over cameras
+// (strict <: ties keep the lower id). sel = camera slot or -1 (lam = 0.5).
+__device__ __forceinline__ double edge_lambda(const MeshCams &C, const uint32_t *__restrict__ sil,
+                                              const double *pon, const double *poff, bool gemv,
+                                              int &sel, int &incons) {
+  double lam = INFINITY;
+  sel = -1;
+  incons = 0;
+  for (int c = 0; c < C.ncam; ++c) {
+    const fvv_camera &cam = C.cams[c];
+    double uo, vo, zo, uf, vf, zf;
+    const bool ino = project_exact(cam, pon[0], pon[1], pon[2], true, gemv, uo, vo, zo);
+    const bool inf = project_exact(cam, poff[0], poff[1], poff[2], true, gemv, uf, vf, zf);
+    if (!(ino && inf)) continue;
+    const int ax = (int)rint(uo), ay = (int)rint(vo), bx = (int)rint(uf), by = (int)rint(vf);
+    const int len = max(abs(bx - ax), abs(by - ay)) + 1;
+    const uint32_t *plane = sil + C.sil_off[c];
+    int first_bg = -1;
+    for (int t = 0; t < len; ++t) {
+      int x, y;
+      bresenham_px(ax, ay, bx, by, t, x, y);
+      if (!sil_bit(plane, C.sil_stride[c], x, y)) {
+        first_bg = t;
+        break;
+      }
+    }
+    const double ddx = uf - uo, ddy = vf - vo;
+    const double denom = sqrt(ddx * ddx + ddy * ddy);
+    double lam_i = 1.0;
+    if (first_bg == 0) {
+      ++incons;
+      lam_i = 0.0;
+    } else if (first_bg > 0 && denom > 1e-12) {
+      int lx, ly;
+      bresenham_px(ax, ay, bx, by, first_bg - 1, lx, ly);
+      const double ex = (double)lx - uo, ey = (double)ly - vo;
+      const double qv = sqrt(ex * ex + ey * ey) / denom;
+      lam_i = qv > 1.0 ? 1.0 : qv;
+    }
+    if (lam_i < lam) {
+      lam = lam_i;
+      sel = c;
+    }
+  }
+  return sel < 0 ? 0.5 : lam;
+}
+
+// _edge_isovalues_batch (mesh.py:231-272) on explicit endpoint arrays.
+__global__ void __launch_bounds__(128)
+    edge_isovalues_kernel(const __grid_constant__ MeshCams C, const uint32_t *__restrict__ sil,
+                          const double *__restrict__ pon, const double *__restrict__ poff, int64_t n,
+                          double *lam_out, int32_t *cam_out, int64_t *stats) {
+  const bool gemv = (n == 1);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int sel, incons;
+    const double lam = edge_lambda(C, sil, pon + 3 * e, poff + 3 * e, gemv, sel, incons);
+    lam_out[e] = lam;
+    cam_out[e] = sel < 0 ? -1 : C.cams[sel].id;
+    if (sel < 0) atomicAdd((unsigned long long *)stats, 1ull);
+    if (incons) atomicAdd((unsigned long long *)(stats + 1), (unsigned long long)incons);
+  }
+}
+
+// ---- B1: isovalues + vertices (mesh.py:231-272, 332-337) --------------------
+__global__ void __launch_bounds__(128)
+    mesh_lambda_kernel(const __grid_constant__ MeshGrids G, const __grid_constant__ MeshCams C,
+                       MeshBufs B, const uint32_t *__restrict__ sil) {
+  const int64_t nv = *(volatile int64_t *)B.totals;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    int axis;
+    int64_t i, j, k;
+    const int g = decode_vkey(G, B.vert_key[v], axis, i, j, k);
+    const MeshGridInfo &gi = G.gi[g];
+    const int64_t q = i * gi.g.dims[1] + j;
+    const bool on = (row_word(B.tw, gi, q, k >> 5) >> (k & 31)) & 1u;
+    double p0[3], p1[3];
+    voxel_center(gi.g, i, j, k, p0[0], p0[1], p0[2]);
+    for (int d = 0; d < 3; ++d) p1[d] = p0[d] + gi.g.spacing * (double)(d == axis);
+    const double *pon = on ? p0 : p1, *poff = on ? p1 : p0;
+    double lam;
+    if (G.exact) {
+      const bool gemv = B.info[8 * g + kInfoV] == 1;  // one-edge batch: numpy gemv order
+      int sel, incons;
+      lam = edge_lambda(C, sil, pon, poff, gemv, sel, incons);
+      if (sel < 0)
+        atomicAdd((unsigned long long *)(B.info + 8 * g + kInfoFallback), 1ull);
+      if (incons)
+        atomicAdd((unsigned long long *)(B.info + 8 * g + kInfoIncons),
+                  (unsigned long long)incons);
+    } else {
+      lam = G.fixed_iso;
+    }
+    for (int d = 0; d < 3; ++d) B.verts[3 * v + d] = pon[d] + lam * (poff[d] - pon[d]);
+  }
+}
+
+// global vertex index of cell-edge `edge` of cell (i, j, k) in grid gi
+__device__ __forceinline__ int64_t edge_vertex(const MeshGrids &G, const MeshBufs &B, int g,
+                                               int64_t i, int64_t j, int64_t k, int edge) {
+  const MeshGridInfo &gi = G.gi[g];
+  const int64_t bi = i + c_edge_base[edge][0], bj = j + c_edge_base[edge][1],
+                bk = k + c_edge_base[edge][2];
+  const int axis = c_edge_base[edge][3];
+  const int64_t e = 3 * G.tw_start[g] + axis * gi.rows * gi.nzw + (bi * gi.g.dims[1] + bj) * gi.nzw +
+                    (bk >> 5);
+  return B.vprefix[e] + __popc(B.eflags[e] & ((1u << (bk & 31)) - 1u));
+}
+
+__device__ __forceinline__ int cell_case(const MeshBufs &B, const MeshGridInfo &gi, int64_t q,
+                                         int64_t k) {
+  const int64_t ny = gi.g.dims[1];
+  const int64_t rows[4] = {q, q + ny, q + ny + 1, q + 1};  // corners v0..v3 (mesh.py:26-29)
+  int ci = 0;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const uint32_t lo = row_word(B.tw, gi, rows[r], k >> 5);
+    const uint32_t hi = row_word(B.tw, gi, rows[r], (k + 1) >> 5);
+    ci |= ((lo >> (k & 31)) & 1u) << r;
+    ci |= ((hi >> ((k + 1) & 31)) & 1u) << (r + 4);
+  }
+  return ci;
+}
+
+// ---- B2: surface-cell list, per-slot keep bits (mesh.py:339-373) ------------
+__global__ void mesh_cells_kernel(const __grid_constant__ MeshGrids G, MeshBufs B) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < G.tw_total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t f = B.sflags[e];
+    if (!f) continue;
+    int lo = 0, hi = G.ngrid - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (G.tw_start[mid] <= e) lo = mid; else hi = mid - 1;
+    }
+    const int g = lo;
+    const MeshGridInfo &gi = G.gi[g];
+    const int64_t rw = e - G.tw_start[g];
+    const int64_t q = rw / gi.nzw, w = rw - q * gi.nzw;
+    const int64_t ny = gi.g.dims[1];
+    const int64_t i = q / ny, j = q - i * ny;
+    int64_t c = B.sprefix[e];
+    while (f) {
+      const int b = __ffs(f) - 1;
+      f &= f - 1;
+      const int64_t k = w * 32 + b;
+      const int ci = cell_case(B, gi, q, k);
+      const int ntri = c_mc_ntri[ci];
+      const unsigned long long edges = c_mc_edges[ci];
+      int keep = 0;
+      for (int t = 0; t < ntri; ++t) {
+        const int64_t v0 = edge_vertex(G, B, g, i, j, k, (int)((edges >> (12 * t)) & 15));
+        const int64_t v1 = edge_vertex(G, B, g, i, j, k, (int)((edges >> (12 * t + 4)) & 15));
+        const int64_t v2 = edge_vertex(G, B, g, i, j, k, (int)((edges >> (12 * t + 8)) & 15));
+        // reversed winding (v2, v1, v0); area as numpy: 0.5*|cross(B-A, C-A)|
+        const double *A = B.verts + 3 * v2, *Bv = B.verts + 3 * v1, *Cv = B.verts + 3 * v0;
+        const double a0 = Bv[0] - A[0], a1 = Bv[1] - A[1], a2 = Bv[2] - A[2];
+        const double b0 = Cv[0] - A[0], b1 = Cv[1] - A[1], b2 = Cv[2] - A[2];
+        const double c0 = a1 * b2 - a2 * b1;
+        const double c1 = a2 * b0 - a0 * b2;
+        const double c2 = a0 * b1 - a1 * b0;
+        const double area = 0.5 * sqrt((c0 * c0 + c1 * c1) + c2 * c2);
+        if (area > kDegenerateArea) keep |= 1 << t;
+      }
+      B.cell_key[c] = e * 32 + b;
+      B.cell_mask[c] = ci | (keep << 8);
+      ++c;
+    }
+  }
+}
+
+struct Slot5 {
+  int32_t v[5];
+  __host__ __device__ Slot5() {}
+  __host__ __device__ Slot5(int x) {
+    for (int t = 0; t < 5; ++t) v[t] = x;
+  }
+  __host__ __device__ Slot5 operator+(const Slot5 &o) const {
+    Slot5 r;
+    for (int t = 0; t < 5; ++t) r.v[t] = v[t] + o.v[t];
+    return r;
+  }
+  __host__ __device__ Slot5 &operator+=(const Slot5 &o) {
+    for (int t = 0; t < 5; ++t) v[t] += o.v[t];
+    return *this;
+  }
+};
+
+// ---- B3: 5-lane triangle scan over cells ------------------------------------
+struct TriScan {
+  const int32_t *cell_mask;
+  int32_t *cprefix;
+  __device__ Slot5 value(int64_t c) const {
+    const int keep = cell_mask[c] >> 8;
+    Slot5 s;
+    for (int t = 0; t < 5; ++t) s.v[t] = (keep >> t) & 1;
+    return s;
+  }
+  __device__ void emit(int64_t c, Slot5 prefix, Slot5) const {
+    for (int t = 0; t < 5; ++t) cprefix[5 * c + t] = prefix.v[t];
+  }
+};
+
+// ---- B4: per-grid slot bases (one thread; <= 128 grids) --------------------
+__global__ void mesh_slot_bases_kernel(const __grid_constant__ MeshGrids G, MeshBufs B,
+                                       const Slot5 *total) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int64_t S = B.totals[1];
+  int64_t tbase = 0;
+  for (int g = 0; g < G.ngrid; ++g) {
+    int64_t *inf = B.info + 8 * g;
+    const int64_t s0 = inf[kInfoSbase], s1 = s0 + inf[kInfoS];
+    int64_t p0[5], p1[5];
+    for (int t = 0; t < 5; ++t) {
+      p0[t] = s0 < S ? B.cprefix[5 * s0 + t] : total->v[t];
+      p1[t] = s1 < S ? B.cprefix[5 * s1 + t] : total->v[t];
+    }
+    inf[kInfoTbase] = tbase;
+    int64_t run = tbase;
+    for (int t = 0; t < 5; ++t) {
+      // slot_base[g][t] = first triangle index of slot t minus the prefix at the grid start
+      B.slot_base[5 * g + t] = run - p0[t];
+      run += p1[t] - p0[t];
+    }
+    inf[kInfoT] = run - tbase;
+    tbase = run;
+  }
+  B.totals[2] = tbase;
+}
+
+// ---- B5: triangle emission ----------------------------------------------------
+__global__ void mesh_emit_kernel(const __grid_constant__ MeshGrids G, MeshBufs B) {
+  const int64_t S = *(volatile int64_t *)(B.totals + 1);
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < S;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const int m = B.cell_mask[c];
+    const int keep = m >> 8;
+    if (!keep) continue;
+    const int ci = m & 255;
+    const int64_t key = B.cell_key[c];
+    const int64_t e = key >> 5;
+    int lo = 0, hi = G.ngrid - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (G.tw_start[mid] <= e) lo = mid; else hi = mid - 1;
+    }
+    const int g = lo;
+    const MeshGridInfo &gi = G.gi[g];
+    const int64_t rw = e - G.tw_start[g];
+    const int64_t q = rw / gi.nzw, w = rw - q * gi.nzw;
+    const int64_t ny = gi.g.dims[1];
+    const int64_t i = q / ny, j = q - i * ny, k = w * 32 + (key & 31);
+    const unsigned long long edges = c_mc_edges[ci];
+    for (int t = 0; t < 5; ++t) {
+      if (!((keep >> t) & 1)) continue;
+      const int64_t idx = B.slot_base[5 * g + t] + B.cprefix[5 * c + t];
+      const int64_t v0 = edge_vertex(G, B, g, i, j, k, (int)((edges >> (12 * t)) & 15));
+      const int64_t v1 = edge_vertex(G, B, g, i, j, k, (int)((edges >> (12 * t + 4)) & 15));
+      const int64_t v2 = edge_vertex(G, B, g, i, j, k, (int)((edges >> (12 * t + 8)) & 15));
+      B.tris[3 * idx] = (int32_t)v2;
+      B.tris[3 * idx + 1] = (int32_t)v1;
+      B.tris[3 * idx + 2] = (int32_t)v0;
+    }
+  }
+}
+
+constexpr int kMeshGrid = 148 * 8;
+
+static size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+struct PrepLayout {
+  size_t tw, eflags, vprefix, sflags, sprefix, sums, totals, info, slot5, cell_sums, total;
+};
+
+static PrepLayout prep_layout(int64_t tw_total, int ngrid) {
+  PrepLayout L;
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    size_t o = off;
+    off += al256(b);
+    return o;
+  };
+  L.tw = take(4 * (size_t)tw_total);
+  L.eflags = take(12 * (size_t)tw_total);
+  L.vprefix = take(12 * (size_t)tw_total);
+  L.sflags = take(4 * (size_t)tw_total);
+  L.sprefix = take(4 * (size_t)tw_total);
+  L.sums = take(8 * (size_t)scan_chunks(3 * tw_total + 1));
+  L.totals = take(8 * 4);
+  L.info = take(8 * 8 * (size_t)(ngrid > 0 ? ngrid : 1));
+  L.slot5 = take(sizeof(int64_t) * 5 * (size_t)(ngrid > 0 ? ngrid : 1) + sizeof(Slot5));
+  L.cell_sums = 0;
+  L.total = off;
+  return L;
+}
+
+static thread_local MeshGrids h_grids;
+
+static int fill_grids(const fvv_grid *grids, int ngrid, const int64_t *word_off, int exact,
+                      double fixed_iso) {
+  if (ngrid < 1 || ngrid > FVV_MAX_GRIDS) {
+    set_error("mesh: %d grids (1..%d)", ngrid, FVV_MAX_GRIDS);
+    return FVV_E_LIMIT;
+  }
+  memset(&h_grids, 0, sizeof(h_grids));
+  h_grids.ngrid = ngrid;
+  h_grids.exact = exact;
+  h_grids.fixed_iso = fixed_iso;
+  int64_t acc = 0;
+  for (int g = 0; g < ngrid; ++g) {
+    MeshGridInfo &gi = h_grids.gi[g];
+    gi.g = grids[g];
+    gi.occ_word_off = word_off[g];
+    const int64_t nx = grids[g].dims[0], ny = grids[g].dims[1], nz = grids[g].dims[2];
+    const bool meshable = nx >= 2 && ny >= 2 && nz >= 2;  // mesh.py:298-299
+    gi.rows = meshable ? nx * ny : 0;
+    gi.nzw = meshable ? (nz + 31) / 32 : 1;
+    gi.tw_off = acc;
+    h_grids.tw_start[g] = acc;
+    acc += gi.rows * gi.nzw;
+  }
+  for (int g = ngrid; g <= FVV_MAX_GRIDS; ++g) h_grids.tw_start[g] = acc;
+  h_grids.tw_total = acc;
+  return FVV_OK;
+}
+
+static MeshBufs bufs_from(void *ws, const PrepLayout &L) {
+  char *p = (char *)ws;
+  MeshBufs B;
+  memset(&B, 0, sizeof(B));
+  B.tw = (uint32_t *)(p + L.tw);
+  B.eflags = (uint32_t *)(p + L.eflags);
+  B.vprefix = (int32_t *)(p + L.vprefix);
+  B.sflags = (uint32_t *)(p + L.sflags);
+  B.sprefix = (int32_t *)(p + L.sprefix);
+  B.sums = (int64_t *)(p + L.sums);
+  B.totals = (int64_t *)(p + L.totals);
+  B.info = (int64_t *)(p + L.info);
+  B.slot_base = (int64_t *)(p + L.slot5);
+  return B;
+}
+
+}  // namespace fvv
+
+using namespace fvv;
+
+static bool g_tables_ready = false;
+
+static int ensure_tables() {
+  if (g_tables_ready) return FVV_OK;
+  if (cudaMemcpyToSymbol(c_mc_edges, FVV_MC_EDGES, sizeof(FVV_MC_EDGES)) != cudaSuccess ||
+      cudaMemcpyToSymbol(c_mc_ntri, FVV_MC_NTRI, sizeof(FVV_MC_NTRI)) != cudaSuccess) {
+    return cuda_check("mesh tables");
+  }
+  g_tables_ready = true;
+  return FVV_OK;
+}
+
+extern "C" {
+
+size_t fvv_mesh_workspace_bytes(const fvv_grid *grids, int ngrid) {
+  int64_t acc = 0;
+  for (int g = 0; g < ngrid; ++g) {
+    const int64_t nx = grids[g].dims[0], ny = grids[g].dims[1], nz = grids[g].dims[2];
+    if (nx >= 2 && ny >= 2 && nz >= 2) acc += nx * ny * ((nz + 31) / 32);
+  }
+  return prep_layout(acc, ngrid).total;
+}
+
+int fvv_mesh_prepare(const fvv_grid *grids, int ngrid, const uint32_t *occ_dev,
+                     const int64_t *word_off, void *ws_dev, size_t ws_bytes, void *stream) {
+  int rc = ensure_tables();
+  if (rc) return rc;
+  rc = fill_grids(grids, ngrid, word_off, 1, 0.5);
+  if (rc) return rc;
+  const PrepLayout L = prep_layout(h_grids.tw_total, ngrid);
+  if (ws_bytes < L.total) {
+    set_error("fvv_mesh_prepare: workspace %zu < %zu bytes", ws_bytes, L.total);
+    return FVV_E_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  MeshBufs B = bufs_from(ws_dev, L);
+  B.occ = occ_dev;
+  cudaMemsetAsync(B.totals, 0, 32, st);
+  if (h_grids.tw_total > 0) {
+    mesh_transpose_kernel<<<kMeshGrid, 256, 0, st>>>(h_grids, B);
+    EdgeFlags ef{h_grids, B.tw, B.eflags, B.vprefix};
+    ordered_scan(ef, nullptr, 3 * h_grids.tw_total, B.sums, B.totals + 0, st);
+    CellFlags cf{h_grids, B.tw, B.sflags, B.sprefix};
+    ordered_scan(cf, nullptr, h_grids.tw_total, B.sums, B.totals + 1, st);
+  }
+  mesh_grid_counts_kernel<<<1, 128, 0, st>>>(h_grids, B);
+  return cuda_check("fvv_mesh_prepare");
+}
+
+// Reads the counts fvv_mesh_prepare left in the workspace: totals[3] = {V, S, T}
+// and info[ngrid][8] (vbase V sbase S tbase T fallback inconsistent).
+int fvv_mesh_counts(const fvv_grid *grids, int ngrid, const void *ws_dev, int64_t *totals_dev,
+                    int64_t *info_dev, void *stream) {
+  int64_t acc = 0;
+  for (int g = 0; g < ngrid; ++g) {
+    const int64_t nx = grids[g].dims[0], ny = grids[g].dims[1], nz = grids[g].dims[2];
+    if (nx >= 2 && ny >= 2 && nz >= 2) acc += nx * ny * ((nz + 31) / 32);
+  }
+  const PrepLayout L = prep_layout(acc, ngrid);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (totals_dev)
+    cudaMemcpyAsync(totals_dev, (const char *)ws_dev + L.totals, 3 * sizeof(int64_t),
+                    cudaMemcpyDeviceToDevice, st);
+  if (info_dev)
+    cudaMemcpyAsync(info_dev, (const char *)ws_dev + L.info, 8 * sizeof(int64_t) * ngrid,
+                    cudaMemcpyDeviceToDevice, st);
+  return cuda_check("fvv_mesh_counts");
+}
+
+size_t fvv_mesh_emit_scratch_bytes(int64_t num_vertices, int64_t num_cells) {
+  return al256(8 * (size_t)num_vertices) + al256(8 * (size_t)num_cells) +
+         al256(4 * (size_t)num_cells) + al256(20 * (size_t)num_cells) +
+         al256(sizeof(Slot5) * (size_t)scan_chunks(num_cells + 1));
+}
+
+int fvv_mesh_emit(const fvv_camera *cams_by_id, int ncam, const uint32_t *sil_dev,
+                  const int64_t *sil_word_off, const fvv_grid *grids, int ngrid,
+                  const uint32_t *occ_dev, const int64_t *word_off, int exact, double fixed_iso,
+                  void *ws_dev, size_t ws_bytes, int64_t num_vertices, int64_t num_cells,
+                  void *scratch_dev, size_t scratch_bytes, double *verts_dev, int32_t *tris_dev,
+                  void *stream) {
+  int rc = ensure_tables();
+  if (rc) return rc;
+  if (exact && (ncam < 1 || ncam > FVV_MAX_CAMS)) {
+    set_error("fvv_mesh_emit: %d cameras (1..%d)", ncam, FVV_MAX_CAMS);
+    return FVV_E_LIMIT;
+  }
+  rc = fill_grids(grids, ngrid, word_off, exact, fixed_iso);
+  if (rc) return rc;
+  const PrepLayout L = prep_layout(h_grids.tw_total, ngrid);
+  if (ws_bytes < L.total || scratch_bytes < fvv_mesh_emit_scratch_bytes(num_vertices, num_cells)) {
+    set_error("fvv_mesh_emit: workspace/scratch too small");
+    return FVV_E_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  MeshBufs B = bufs_from(ws_dev, L);
+  B.occ = occ_dev;
+  char *s = (char *)scratch_dev;
+  B.vert_key = (int64_t *)s;
+  s += al256(8 * (size_t)num_vertices);
+  B.cell_key = (int64_t *)s;
+  s += al256(8 * (size_t)num_cells);
+  B.cell_mask = (int32_t *)s;
+  s += al256(4 * (size_t)num_cells);
+  B.cprefix = (int32_t *)s;
+  s += al256(20 * (size_t)num_cells);
+  Slot5 *cell_sums = (Slot5 *)s;
+  B.verts = verts_dev;
+  B.tris = tris_dev;
+  static thread_local MeshCams h_cams;
+  memset(&h_cams, 0, sizeof(h_cams));
+  h_cams.ncam = exact ? ncam : 0;
+  for (int c = 0; c < h_cams.ncam; ++c) {
+    h_cams.cams[c] = cams_by_id[c];
+    h_cams.sil_off[c] = sil_word_off[c];
+    h_cams.sil_stride[c] = sil_stride_words(cams_by_id[c].width);
+  }
+  Slot5 *d_total = (Slot5 *)((char *)ws_dev + L.slot5 + sizeof(int64_t) * 5 * ngrid);
+  if (num_vertices > 0) {
+    mesh_vertex_list_kernel<<<kMeshGrid, 256, 0, st>>>(h_grids, B);
+    mesh_lambda_kernel<<<kMeshGrid, 128, 0, st>>>(h_grids, h_cams, B, sil_dev);
+  }
+  if (num_cells > 0) {
+    mesh_cells_kernel<<<kMeshGrid, 256, 0, st>>>(h_grids, B);
+    TriScan ts{B.cell_mask, B.cprefix};
+    ordered_scan(ts, B.totals + 1, 0, cell_sums, d_total, st);
+  } else {
+    cudaMemsetAsync(d_total, 0, sizeof(Slot5), st);
+  }
+  mesh_slot_bases_kernel<<<1, 32, 0, st>>>(h_grids, B, d_total);
+  if (num_cells > 0) mesh_emit_kernel<<<kMeshGrid, 256, 0, st>>>(h_grids, B);
+  return cuda_check("fvv_mesh_emit");
+}
+
+int fvv_edge_isovalues(const fvv_camera *cams_by_id, int ncam, const uint32_t *sil_dev,
+                       const int64_t *sil_word_off, const double *p_on_dev,
+                       const double *p_off_dev, int64_t n, double *lam_dev, int32_t *cam_dev,
+                       int64_t *stats_dev, void *stream) {
+  if (ncam < 1 || ncam > FVV_MAX_CAMS) {
+    set_error("fvv_edge_isovalues: %d cameras (1..%d)", ncam, FVV_MAX_CAMS);
+    return FVV_E_LIMIT;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaMemsetAsync(stats_dev, 0, 2 * sizeof(int64_t), st);
+  if (n <= 0) return cuda_check("fvv_edge_isovalues");
+  static thread_local MeshCams h_cams;
+  memset(&h_cams, 0, sizeof(h_cams));
+  h_cams.ncam = ncam;
+  for (int c = 0; c < ncam; ++c) {
+    h_cams.cams[c] = cams_by_id[c];
+    h_cams.sil_off[c] = sil_word_off[c];
+    h_cams.sil_stride[c] = sil_stride_words(cams_by_id[c].width);
+  }
+  int64_t blocks = (n + 127) / 128;
+  if (blocks > kMeshGrid) blocks = kMeshGrid;
+  edge_isovalues_kernel<<<(int)blocks, 128, 0, st>>>(h_cams, sil_dev, p_on_dev, p_off_dev, n,
+                                                      lam_dev, cam_dev, stats_dev);
+  return cuda_check("fvv_edge_isovalues");
+}
+
+}  // extern "C"

@@ -28,7 +28,7 @@ __device__ __forceinline__ int64_t scan_len(const int64_t *n_dev, int64_t n_host
 
 template <class F, typename T>
 __global__ void __launch_bounds__(kScanThreads)
-    chunk_reduce_kernel(F f, const int64_t *n_dev, int64_t n_host, T *sums) {
+    chunk_reduce_kernel(const __grid_constant__ F f, const int64_t *n_dev, int64_t n_host, T *sums) {
   using Reduce = cub::BlockReduce<T, kScanThreads>;
   __shared__ typename Reduce::TempStorage tmp;
   const int64_t n = scan_len(n_dev, n_host);
@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(1024)
 
 template <class F, typename T>
 __global__ void __launch_bounds__(kScanThreads)
-    chunk_emit_kernel(F f, const int64_t *n_dev, int64_t n_host, const T *bases) {
+    chunk_emit_kernel(const __grid_constant__ F f, const int64_t *n_dev, int64_t n_host, const T *bases) {
   using Scan = cub::BlockScan<T, kScanThreads>;
   __shared__ typename Scan::TempStorage tmp;
   const int64_t n = scan_len(n_dev, n_host);
