@@ -455,7 +455,9 @@ __global__ void mesh_cells_kernel(const __grid_constant__ MeshGrids G, MeshBufs 
 
 struct Slot5 {
   int32_t v[5];
-  __host__ __device__ Slot5() {}
+  __host__ __device__ Slot5() {  // cub value-initialises scan seeds with T{}
+    for (int t = 0; t < 5; ++t) v[t] = 0;
+  }
   __host__ __device__ Slot5(int x) {
     for (int t = 0; t < 5; ++t) v[t] = x;
   }
