@@ -167,6 +167,55 @@ int fvv_edge_isovalues(const fvv_camera *cams_by_id, int ncam, const uint32_t *s
                        const double *p_off_dev, int64_t n, double *lam_dev, int32_t *cam_dev,
                        int64_t *stats_dev, void *stream);
 
+/* ---- D-1 / D-2: visibility.py:34-140 --------------------------------------- */
+
+/* Scratch for fvv_rasterize (queue of large-bbox triangles). */
+size_t fvv_raster_workspace_bytes(int64_t num_triangles, int ncam);
+
+/* visibility.py:34-98 rasterize for ncam cameras at once (zero-distortion
+ * projection, near clip 1 mm, top-left rule, perspective-correct depth).
+ * Camera c's float64 depth plane (+inf background) is depth_dev +
+ * plane_off[c]; when tri_id_dev is non-NULL its int32 winning-triangle
+ * plane (-1 background; lowest id on exact depth ties) is tri_id_dev +
+ * plane_off[c]. The triangle count is *nt_dev when nt_dev is non-NULL
+ * (nt is then an upper bound), else nt. */
+int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int64_t nv,
+                  const int32_t *tris_dev, int64_t nt, const int64_t *nt_dev, double *depth_dev,
+                  const int64_t *plane_off, int32_t *tri_id_dev, void *ws_dev, size_t ws_bytes,
+                  void *stream);
+
+/* visibility.py:106-129 classify_visibility for ncam cameras: triangle t
+ * visible in camera c iff its centroid projects in-frustum and
+ * z - depth[rint v, rint u] <= t_v. Bit t of vis_dev + c*vis_stride_words. */
+int fvv_classify(const fvv_camera *cams, int ncam, const double *verts_dev,
+                 const int32_t *tris_dev, int64_t nt, const int64_t *nt_dev,
+                 const double *depth_dev, const int64_t *plane_off, double t_v,
+                 uint32_t *vis_dev, int64_t vis_stride_words, void *stream);
+
+/* ---- E: render.py:29-113, camera.py:204-220 --------------------------------- */
+
+/* render.py:35-43 triangle_sources: first ranked camera (rig position
+ * rank_pos[r], id rank_id[r]) whose visibility bit is set; -1 if none. */
+int fvv_triangle_sources(const int32_t *rank_pos, const int32_t *rank_id, int nrank,
+                         const uint32_t *vis_dev, int64_t vis_stride_words, int64_t nt,
+                         const int64_t *nt_dev, int32_t *src_dev, void *stream);
+
+/* render.py:64-113 render_view colour pass, given the virtual view's depth /
+ * triangle-id planes (fvv_rasterize) and per-triangle source ids: back-
+ * projects each covered pixel, projects it (with distortion) into its source
+ * camera and samples that camera's (H,W,3) uint8 frame (frames_dev +
+ * frame_off[c], rig order) bilinearly; fallback colour where no camera sees
+ * the triangle. counts_dev: int64[1 + ncam] scratch. */
+int fvv_render_view(const fvv_camera *rig, int ncam, const uint8_t *frames_dev,
+                    const int64_t *frame_off, const fvv_camera *virt, const double *depth_dev,
+                    const int32_t *tri_id_dev, const int32_t *tri_src_dev, const uint8_t *fallback,
+                    uint8_t *color_dev, int32_t *source_dev, uint8_t *covered_dev,
+                    int64_t *counts_dev, void *stream);
+
+/* camera.py:204-220 back_project for n pixels (n,2) at depths (n,) -> (n,3). */
+int fvv_back_project(const fvv_camera *cam, const double *pixel_dev, const double *depth_dev,
+                     int64_t n, double *out_dev, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -42,6 +42,8 @@ SYMBOLS = (
     "fvv_ccl_components", "fvv_ccl_labels", "fvv_filter_labels", "fvv_filter_dense",
     "fvv_mesh_workspace_bytes", "fvv_mesh_prepare", "fvv_mesh_counts",
     "fvv_mesh_emit_scratch_bytes", "fvv_mesh_emit", "fvv_edge_isovalues",
+    "fvv_raster_workspace_bytes", "fvv_rasterize", "fvv_classify", "fvv_triangle_sources",
+    "fvv_render_view", "fvv_back_project",
 )
 
 
@@ -67,6 +69,8 @@ def load():
         lib.fvv_mesh_workspace_bytes.restype = ctypes.c_size_t
         lib.fvv_mesh_emit_scratch_bytes.restype = ctypes.c_size_t
         lib.fvv_mesh_emit_scratch_bytes.argtypes = [ctypes.c_int64, ctypes.c_int64]
+        lib.fvv_raster_workspace_bytes.restype = ctypes.c_size_t
+        lib.fvv_raster_workspace_bytes.argtypes = [ctypes.c_int64, ctypes.c_int]
         _lib = lib
     return _lib
 

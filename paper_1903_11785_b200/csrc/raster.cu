@@ -1,0 +1,534 @@
+// D-1 depth images, D-2 visibility, E view-dependent colour
+// (visibility.py:34-140, render.py:35-113, camera.py:204-220).
+//
+// Rasterisation: one thread per (camera, triangle) sets the triangle up
+// exactly as visibility.py:48-78 does (zero-distortion projection, near
+// clip, clamped bbox, signed area / swap, top-left flags) and walks its
+// bbox when it is small (the norm at C3: ~1-4 px); triangles with a larger
+// bbox go to a queue that whole blocks sweep pixel-parallel. The reference
+// keeps, per pixel, the first triangle (ascending id) reaching the minimum
+// depth (strict `<`): lexicographic min of (depth, id). Depth is positive,
+// so its IEEE bits order like the value: pass 1 is a 64-bit atomicMin of
+// the depth bits; pass 2 (only when ids are wanted) re-evaluates the
+// identical depth and atomicMin's the id where it equals the stored depth.
+// Integer atomics only; results do not depend on scheduling.
+#include <cstring>
+
+#include "fvv_common.cuh"
+
+namespace fvv {
+
+constexpr int kSmallBBox = 64;       // pixels walked by one thread
+constexpr int kRasterThreads = 128;
+constexpr int kBigThreads = 256;
+
+struct RasterCams {
+  int ncam;
+  int64_t depth_off[FVV_MAX_CAMS];  // element offset of camera c's (H, W) planes
+  fvv_camera cams[FVV_MAX_CAMS];
+};
+
+struct TriSetup {
+  double x0, y0, x1, y1, x2, y2, za, zb, zc, area;
+  int lox, loy, hix, hiy;
+  bool tl0, tl1, tl2;
+};
+
+__device__ __forceinline__ bool top_left(double ax, double ay, double bx, double by) {
+  const double dy = by - ay, dx = bx - ax;  // visibility.py:28-31
+  return dy < 0.0 || (dy == 0.0 && dx < 0.0);
+}
+
+// visibility.py:48-78 for triangle t in camera `cam`. False = skipped.
+__device__ __forceinline__ bool tri_setup(const fvv_camera &cam, const double *__restrict__ V,
+                                          const int32_t *__restrict__ T, int64_t t, bool gemv,
+                                          TriSetup &s) {
+  const int32_t ia = T[3 * t], ib = T[3 * t + 1], ic = T[3 * t + 2];
+  double u[3], v[3], z[3];
+  const int32_t idx[3] = {ia, ib, ic};
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const double *p = V + 3 * (int64_t)idx[q];
+    project_exact(cam, p[0], p[1], p[2], false, gemv, u[q], v[q], z[q]);
+  }
+  if (!(z[0] > kNearClip && z[1] > kNearClip && z[2] > kNearClip)) return false;
+  if (isnan(u[0]) || isnan(u[1]) || isnan(u[2]) || isnan(v[0]) || isnan(v[1]) || isnan(v[2]))
+    return false;
+  const double mnx = fmin(fmin(u[0], u[1]), u[2]), mxx = fmax(fmax(u[0], u[1]), u[2]);
+  const double mny = fmin(fmin(v[0], v[1]), v[2]), mxy = fmax(fmax(v[0], v[1]), v[2]);
+  const double flx = floor(mnx), fly = floor(mny), chx = ceil(mxx), chy = ceil(mxy);
+  const double W1 = (double)(cam.width - 1), H1 = (double)(cam.height - 1);
+  if (flx > W1 || fly > H1 || chx < 0.0 || chy < 0.0) return false;
+  s.lox = flx > 0.0 ? (int)flx : 0;
+  s.loy = fly > 0.0 ? (int)fly : 0;
+  s.hix = chx < W1 ? (int)chx : cam.width - 1;
+  s.hiy = chy < H1 ? (int)chy : cam.height - 1;
+  if (s.hix < s.lox || s.hiy < s.loy) return false;
+  double x0 = u[0], y0 = v[0], x1 = u[1], y1 = v[1], x2 = u[2], y2 = v[2];
+  double za = z[0], zb = z[1], zc = z[2];
+  double area = (x1 - x0) * (y2 - y0) - (y1 - y0) * (x2 - x0);
+  if (area == 0.0) return false;
+  if (area < 0.0) {  // swap v1 <-> v2 (visibility.py:63-66)
+    double tx = x1, ty = y1;
+    x1 = x2; y1 = y2; x2 = tx; y2 = ty;
+    double tz = zb; zb = zc; zc = tz;
+    area = -area;
+  }
+  s.x0 = x0; s.y0 = y0; s.x1 = x1; s.y1 = y1; s.x2 = x2; s.y2 = y2;
+  s.za = za; s.zb = zb; s.zc = zc; s.area = area;
+  s.tl0 = top_left(x1, y1, x2, y2);
+  s.tl1 = top_left(x2, y2, x0, y0);
+  s.tl2 = top_left(x0, y0, x1, y1);
+  return true;
+}
+
+// visibility.py:67-91 at pixel (x, y): inside test and perspective depth.
+__device__ __forceinline__ bool tri_depth(const TriSetup &s, int x, int y, double &d) {
+  const double gx = (double)x, gy = (double)y;
+  const double w0 = (s.x2 - s.x1) * (gy - s.y1) - (s.y2 - s.y1) * (gx - s.x1);
+  const double w1 = (s.x0 - s.x2) * (gy - s.y2) - (s.y0 - s.y2) * (gx - s.x2);
+  const double w2 = (s.x1 - s.x0) * (gy - s.y0) - (s.y1 - s.y0) * (gx - s.x0);
+  const bool in = (w0 > 0.0 || (w0 == 0.0 && s.tl0)) && (w1 > 0.0 || (w1 == 0.0 && s.tl1)) &&
+                  (w2 > 0.0 || (w2 == 0.0 && s.tl2));
+  if (!in) return false;
+  const double b0 = w0 / s.area, b1 = w1 / s.area, b2 = w2 / s.area;
+  const double zinv = b0 / s.za + b1 / s.zb + b2 / s.zc;
+  d = 1.0 / zinv;
+  return d < INFINITY;  // only finite depths can beat the +inf background
+}
+
+__device__ __forceinline__ void pixel_update(int pass, double d, int64_t t,
+                                             unsigned long long *depth, unsigned *ids) {
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(d);
+  if (pass == 0) {
+    if (bits < *(volatile unsigned long long *)depth) atomicMin(depth, bits);
+  } else if (bits == *depth) {
+    atomicMin(ids, (unsigned)t);
+  }
+}
+
+struct RasterArgs {
+  const double *V;
+  const int32_t *T;
+  int64_t nt;
+  const int64_t *nt_dev;
+  int64_t nv;
+  double *depth;
+  int32_t *ids;
+  int64_t *queue;     // big (camera, triangle) entries
+  int64_t *qcount;
+  int64_t qcap;
+  int pass;
+};
+
+__global__ void __launch_bounds__(kRasterThreads)
+    raster_small_kernel(const __grid_constant__ RasterCams C, RasterArgs A) {
+  const int64_t nt = A.nt_dev ? *(volatile const int64_t *)A.nt_dev : A.nt;
+  const int64_t total = nt * C.ncam;
+  const bool gemv = A.nv == 1;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(w / nt);
+    const int64_t t = w - (int64_t)c * nt;
+    const fvv_camera &cam = C.cams[c];
+    TriSetup s;
+    if (!tri_setup(cam, A.V, A.T, t, gemv, s)) continue;
+    const int64_t npx = (int64_t)(s.hix - s.lox + 1) * (s.hiy - s.loy + 1);
+    if (npx > kSmallBBox) {
+      if (A.pass == 0) {
+        const unsigned long long slot = atomicAdd((unsigned long long *)A.qcount, 1ull);
+        if ((int64_t)slot < A.qcap) {
+          A.queue[slot] = w;
+          continue;
+        }
+      } else if (*(volatile int64_t *)A.qcount <= A.qcap) {
+        continue;  // pass 1: the big kernel replays the queue
+      }
+      // queue overflowed: walk it here (atomicMin is idempotent, so a queued
+      // triangle walked twice in pass 1 is harmless)
+    }
+    unsigned long long *dp = (unsigned long long *)(A.depth + C.depth_off[c]);
+    unsigned *ip = (unsigned *)(A.ids ? A.ids + C.depth_off[c] : nullptr);
+    for (int y = s.loy; y <= s.hiy; ++y)
+      for (int x = s.lox; x <= s.hix; ++x) {
+        double d;
+        if (!tri_depth(s, x, y, d)) continue;
+        const int64_t p = (int64_t)y * cam.width + x;
+        pixel_update(A.pass, d, t, dp + p, ip ? ip + p : nullptr);
+      }
+  }
+}
+
+__global__ void __launch_bounds__(kBigThreads)
+    raster_big_kernel(const __grid_constant__ RasterCams C, RasterArgs A) {
+  const int64_t nt = A.nt_dev ? *(volatile const int64_t *)A.nt_dev : A.nt;
+  int64_t nq = *(volatile int64_t *)A.qcount;
+  if (nq > A.qcap) nq = A.qcap;
+  const bool gemv = A.nv == 1;
+  for (int64_t q = blockIdx.x; q < nq; q += gridDim.x) {
+    const int64_t w = A.queue[q];
+    const int c = (int)(w / nt);
+    const int64_t t = w - (int64_t)c * nt;
+    const fvv_camera &cam = C.cams[c];
+    TriSetup s;
+    if (!tri_setup(cam, A.V, A.T, t, gemv, s)) continue;  // uniform per block
+    const int bw = s.hix - s.lox + 1;
+    const int64_t npx = (int64_t)bw * (s.hiy - s.loy + 1);
+    unsigned long long *dp = (unsigned long long *)(A.depth + C.depth_off[c]);
+    unsigned *ip = (unsigned *)(A.ids ? A.ids + C.depth_off[c] : nullptr);
+    for (int64_t k = threadIdx.x; k < npx; k += blockDim.x) {
+      const int y = s.loy + (int)(k / bw), x = s.lox + (int)(k % bw);
+      double d;
+      if (!tri_depth(s, x, y, d)) continue;
+      const int64_t p = (int64_t)y * cam.width + x;
+      pixel_update(A.pass, d, t, dp + p, ip ? ip + p : nullptr);
+    }
+  }
+}
+
+__global__ void fill_u64_kernel(unsigned long long *p, int64_t n, unsigned long long v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+// ---- D-2: visibility.py:106-129 ------------------------------------------------
+struct ClassifyArgs {
+  const double *V;
+  const int32_t *T;
+  int64_t nt;
+  const int64_t *nt_dev;
+  const double *depth;
+  double t_v;
+  uint32_t *vis;       // [ncam][stride] bits
+  int64_t vis_stride;  // words per camera
+};
+
+__global__ void classify_kernel(const __grid_constant__ RasterCams C, ClassifyArgs A) {
+  const int64_t nt = A.nt_dev ? *(volatile const int64_t *)A.nt_dev : A.nt;
+  const bool gemv = nt == 1;
+  const int lane = threadIdx.x & 31;
+  const int64_t words = (nt + 31) / 32;
+  const int64_t total = words * C.ncam * 32;
+  for (int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; w0 < total;
+       w0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t word = w0 >> 5;
+    const int c = (int)(word / words);
+    const int64_t wi = word - (int64_t)c * words;
+    const int64_t t = wi * 32 + lane;
+    bool vis = false;
+    if (t < nt) {
+      const fvv_camera &cam = C.cams[c];
+      const double *a = A.V + 3 * (int64_t)A.T[3 * t], *b = A.V + 3 * (int64_t)A.T[3 * t + 1],
+                   *cc = A.V + 3 * (int64_t)A.T[3 * t + 2];
+      const double mx = ((a[0] + b[0]) + cc[0]) / 3.0;  // mesh.py:84-85 mean
+      const double my = ((a[1] + b[1]) + cc[1]) / 3.0;
+      const double mz = ((a[2] + b[2]) + cc[2]) / 3.0;
+      double u, v, z;
+      if (project_exact(cam, mx, my, mz, false, gemv, u, v, z)) {
+        const int64_t p = (int64_t)rint(v) * cam.width + (int64_t)rint(u);
+        vis = (z - A.depth[C.depth_off[c] + p]) <= A.t_v;
+      }
+    }
+    const uint32_t bits = __ballot_sync(0xffffffffu, vis);
+    if (lane == 0) A.vis[(int64_t)c * A.vis_stride + wi] = bits;
+  }
+}
+
+// ---- E: render.py:35-43 triangle_sources ------------------------------------
+struct SourceArgs {
+  int nrank;
+  int32_t rank_pos[FVV_MAX_CAMS];  // rig position of the r-th ranked camera
+  int32_t rank_id[FVV_MAX_CAMS];
+  const uint32_t *vis;
+  int64_t vis_stride;
+  int64_t nt;
+  const int64_t *nt_dev;
+  int32_t *src;
+};
+
+__global__ void sources_kernel(const __grid_constant__ SourceArgs A) {
+  const int64_t nt = A.nt_dev ? *(volatile const int64_t *)A.nt_dev : A.nt;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nt;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int32_t s = -1;
+    for (int r = 0; r < A.nrank; ++r) {
+      const uint32_t w = A.vis[(int64_t)A.rank_pos[r] * A.vis_stride + (t >> 5)];
+      if ((w >> (t & 31)) & 1u) {
+        s = A.rank_id[r];
+        break;
+      }
+    }
+    A.src[t] = s;
+  }
+}
+
+// camera.py:204-220 back_project (zero distortion) of one pixel at depth d.
+// `(pc - t) @ R`: OpenBLAS gemm (>= 2 rows) fuses fma(q2,R2c, fma(q1,R1c, q0*R0c));
+// one row goes through gemv, whose Haswell kernel sums unfused.
+__device__ __forceinline__ void back_project1(const fvv_camera &c, double px, double py, double d,
+                                              bool gemv, double &X, double &Y, double &Z) {
+  const double yn = (py - c.cy) / c.fy;
+  const double xn = (px - c.cx) / c.fx - c.skew * yn;
+  const double q0 = xn * d - c.t[0], q1 = yn * d - c.t[1], q2 = d - c.t[2];
+  double out[3];
+#pragma unroll
+  for (int col = 0; col < 3; ++col) {
+    const double r0 = c.R[col], r1 = c.R[3 + col], r2 = c.R[6 + col];
+    out[col] = gemv ? (q0 * r0 + q1 * r1) + q2 * r2 : fma(q2, r2, fma(q1, r1, q0 * r0));
+  }
+  X = out[0];
+  Y = out[1];
+  Z = out[2];
+}
+
+struct RenderArgs {
+  fvv_camera virt;
+  int ncam;
+  int32_t cam_id[FVV_MAX_CAMS];
+  int64_t frame_off[FVV_MAX_CAMS];
+  fvv_camera cams[FVV_MAX_CAMS];
+  const uint8_t *frames;
+  const double *depth;
+  const int32_t *ids;
+  const int32_t *tri_src;
+  uint8_t fallback[4];
+  uint8_t *color;
+  int32_t *source;
+  uint8_t *covered;
+  int64_t *counts;  // [0] covered pixels, [1 + pos] pixels sourced from camera pos
+};
+
+__device__ __forceinline__ int cam_pos(const RenderArgs &A, int32_t id) {
+  for (int c = 0; c < A.ncam; ++c)
+    if (A.cam_id[c] == id) return c;
+  return -1;
+}
+
+// covered pixels and pixels per source camera (numpy's one-row gemv rule
+// applies when a count is 1); warp-aggregated atomics.
+__global__ void render_count_kernel(const __grid_constant__ RenderArgs A) {
+  const int64_t np = (int64_t)A.virt.width * A.virt.height;
+  const int lane = threadIdx.x & 31;
+  for (int64_t p0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; p0 < np;
+       p0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = p0 + lane;
+    const int32_t t = p < np ? A.ids[p] : -1;
+    int c = -1;
+    if (t >= 0) {
+      const int32_t s = A.tri_src[t];
+      if (s >= 0) c = cam_pos(A, s);
+    }
+    const unsigned cov = __ballot_sync(0xffffffffu, t >= 0);
+    if (lane == 0 && cov) atomicAdd((unsigned long long *)A.counts, (unsigned long long)__popc(cov));
+    const unsigned grp = __match_any_sync(0xffffffffu, c);
+    if (c >= 0 && lane == __ffs(grp) - 1)
+      atomicAdd((unsigned long long *)(A.counts + 1 + c), (unsigned long long)__popc(grp));
+  }
+}
+
+// render.py:46-61 sample_bilinear, render.py:104-113 rint/clip.
+__global__ void render_color_kernel(const __grid_constant__ RenderArgs A) {
+  const int W = A.virt.width;
+  const int64_t np = (int64_t)W * A.virt.height;
+  const bool bp_gemv = A.counts[0] == 1;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < np;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t t = A.ids[p];
+    uint8_t rgb[3] = {0, 0, 0};
+    int32_t src = -1;
+    if (t >= 0) {
+      src = A.tri_src[t];
+      const int c = src >= 0 ? cam_pos(A, src) : -1;
+      if (c < 0) {
+        rgb[0] = A.fallback[0];
+        rgb[1] = A.fallback[1];
+        rgb[2] = A.fallback[2];
+      } else {
+        double X, Y, Z;
+        back_project1(A.virt, (double)(p % W), (double)(p / W), A.depth[p], bp_gemv, X, Y, Z);
+        const fvv_camera &cam = A.cams[c];
+        double u, v, zc;
+        project_exact(cam, X, Y, Z, true, A.counts[1 + c] == 1, u, v, zc);
+        const int w = cam.width, h = cam.height;
+        u = fmin(fmax(u, 0.0), (double)w - 1.0);
+        v = fmin(fmax(v, 0.0), (double)h - 1.0);
+        const int x0 = (int)floor(u), y0 = (int)floor(v);
+        const int x1 = min(x0 + 1, w - 1), y1 = min(y0 + 1, h - 1);
+        const double fx = u - (double)x0, fy = v - (double)y0;
+        const uint8_t *img = A.frames + A.frame_off[c];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+          const double a = img[((int64_t)y0 * w + x0) * 3 + ch];
+          const double b = img[((int64_t)y0 * w + x1) * 3 + ch];
+          const double cc = img[((int64_t)y1 * w + x0) * 3 + ch];
+          const double d = img[((int64_t)y1 * w + x1) * 3 + ch];
+          const double top = a * (1.0 - fx) + b * fx;
+          const double bot = cc * (1.0 - fx) + d * fx;
+          double q = rint(top * (1.0 - fy) + bot * fy);
+          q = q < 0.0 ? 0.0 : (q > 255.0 ? 255.0 : q);
+          rgb[ch] = (uint8_t)q;
+        }
+      }
+    }
+    A.color[3 * p] = rgb[0];
+    A.color[3 * p + 1] = rgb[1];
+    A.color[3 * p + 2] = rgb[2];
+    A.source[p] = src;
+    if (A.covered) A.covered[p] = t >= 0;
+  }
+}
+
+__global__ void back_project_kernel(fvv_camera cam, const double *__restrict__ px,
+                                    const double *__restrict__ d, int64_t n, double *out) {
+  const bool gemv = n == 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    back_project1(cam, px[2 * i], px[2 * i + 1], d[i], gemv, out[3 * i], out[3 * i + 1],
+                  out[3 * i + 2]);
+}
+
+constexpr int kRasterGrid = 148 * 16;
+
+static int fill_cams(RasterCams &C, const fvv_camera *cams, int ncam, const int64_t *off) {
+  if (ncam < 1 || ncam > FVV_MAX_CAMS) {
+    set_error("raster: %d cameras (1..%d)", ncam, FVV_MAX_CAMS);
+    return FVV_E_LIMIT;
+  }
+  memset(&C, 0, sizeof(C));
+  C.ncam = ncam;
+  for (int c = 0; c < ncam; ++c) {
+    C.cams[c] = cams[c];
+    C.depth_off[c] = off[c];
+  }
+  return FVV_OK;
+}
+
+}  // namespace fvv
+
+using namespace fvv;
+
+extern "C" {
+
+size_t fvv_raster_workspace_bytes(int64_t num_triangles, int ncam) {
+  int64_t cap = num_triangles * (int64_t)ncam;
+  if (cap > (4ll << 20)) cap = 4ll << 20;
+  return 256 + 8 * (size_t)(cap > 0 ? cap : 1);
+}
+
+int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int64_t nv,
+                  const int32_t *tris_dev, int64_t nt, const int64_t *nt_dev, double *depth_dev,
+                  const int64_t *plane_off, int32_t *tri_id_dev, void *ws_dev, size_t ws_bytes,
+                  void *stream) {
+  static thread_local RasterCams C;
+  int rc = fill_cams(C, cams, ncam, plane_off);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  // background: depth +inf, id -1 (visibility.py:44-45)
+  for (int c = 0; c < ncam; ++c) {
+    const int64_t n = (int64_t)cams[c].width * cams[c].height;
+    fill_u64_kernel<<<256, 256, 0, st>>>((unsigned long long *)(depth_dev + plane_off[c]), n,
+                                         0x7ff0000000000000ull);
+    if (tri_id_dev) cudaMemsetAsync(tri_id_dev + plane_off[c], 0xff, 4 * n, st);
+  }
+  if (nt <= 0) return cuda_check("fvv_rasterize");
+  RasterArgs A;
+  A.V = verts_dev;
+  A.T = tris_dev;
+  A.nt = nt;
+  A.nt_dev = nt_dev;
+  A.nv = nv;
+  A.depth = depth_dev;
+  A.ids = tri_id_dev;
+  A.qcount = (int64_t *)ws_dev;
+  A.queue = (int64_t *)((char *)ws_dev + 256);
+  A.qcap = (int64_t)((ws_bytes - 256) / 8);
+  cudaMemsetAsync(A.qcount, 0, 8, st);
+  for (int pass = 0; pass < (tri_id_dev ? 2 : 1); ++pass) {
+    A.pass = pass;
+    raster_small_kernel<<<kRasterGrid, kRasterThreads, 0, st>>>(C, A);
+    raster_big_kernel<<<148 * 4, kBigThreads, 0, st>>>(C, A);
+  }
+  return cuda_check("fvv_rasterize");
+}
+
+int fvv_classify(const fvv_camera *cams, int ncam, const double *verts_dev,
+                 const int32_t *tris_dev, int64_t nt, const int64_t *nt_dev,
+                 const double *depth_dev, const int64_t *plane_off, double t_v,
+                 uint32_t *vis_dev, int64_t vis_stride_words, void *stream) {
+  static thread_local RasterCams C;
+  int rc = fill_cams(C, cams, ncam, plane_off);
+  if (rc) return rc;
+  ClassifyArgs A{verts_dev, tris_dev, nt, nt_dev, depth_dev, t_v, vis_dev, vis_stride_words};
+  classify_kernel<<<kRasterGrid, 256, 0, (cudaStream_t)stream>>>(C, A);
+  return cuda_check("fvv_classify");
+}
+
+int fvv_triangle_sources(const int32_t *rank_pos, const int32_t *rank_id, int nrank,
+                         const uint32_t *vis_dev, int64_t vis_stride_words, int64_t nt,
+                         const int64_t *nt_dev, int32_t *src_dev, void *stream) {
+  if (nrank < 0 || nrank > FVV_MAX_CAMS) {
+    set_error("fvv_triangle_sources: %d cameras", nrank);
+    return FVV_E_LIMIT;
+  }
+  static thread_local SourceArgs A;
+  memset(&A, 0, sizeof(A));
+  A.nrank = nrank;
+  for (int r = 0; r < nrank; ++r) {
+    A.rank_pos[r] = rank_pos[r];
+    A.rank_id[r] = rank_id[r];
+  }
+  A.vis = vis_dev;
+  A.vis_stride = vis_stride_words;
+  A.nt = nt;
+  A.nt_dev = nt_dev;
+  A.src = src_dev;
+  sources_kernel<<<kRasterGrid, 256, 0, (cudaStream_t)stream>>>(A);
+  return cuda_check("fvv_triangle_sources");
+}
+
+int fvv_render_view(const fvv_camera *rig, int ncam, const uint8_t *frames_dev,
+                    const int64_t *frame_off, const fvv_camera *virt, const double *depth_dev,
+                    const int32_t *tri_id_dev, const int32_t *tri_src_dev, const uint8_t *fallback,
+                    uint8_t *color_dev, int32_t *source_dev, uint8_t *covered_dev,
+                    int64_t *counts_dev, void *stream) {
+  if (ncam < 1 || ncam > FVV_MAX_CAMS) {
+    set_error("fvv_render_view: %d cameras", ncam);
+    return FVV_E_LIMIT;
+  }
+  static thread_local RenderArgs A;
+  memset(&A, 0, sizeof(A));
+  A.virt = *virt;
+  A.ncam = ncam;
+  for (int c = 0; c < ncam; ++c) {
+    A.cams[c] = rig[c];
+    A.cam_id[c] = rig[c].id;
+    A.frame_off[c] = frame_off[c];
+  }
+  A.frames = frames_dev;
+  A.depth = depth_dev;
+  A.ids = tri_id_dev;
+  A.tri_src = tri_src_dev;
+  for (int ch = 0; ch < 3; ++ch) A.fallback[ch] = fallback[ch];
+  A.color = color_dev;
+  A.source = source_dev;
+  A.covered = covered_dev;
+  A.counts = counts_dev;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaMemsetAsync(counts_dev, 0, sizeof(int64_t) * (1 + ncam), st);
+  render_count_kernel<<<kRasterGrid, 256, 0, st>>>(A);
+  render_color_kernel<<<kRasterGrid, 256, 0, st>>>(A);
+  return cuda_check("fvv_render_view");
+}
+
+int fvv_back_project(const fvv_camera *cam, const double *pixel_dev, const double *depth_dev,
+                     int64_t n, double *out_dev, void *stream) {
+  if (n <= 0) return FVV_OK;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > kRasterGrid) blocks = kRasterGrid;
+  back_project_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(*cam, pixel_dev, depth_dev,
+                                                                      n, out_dev);
+  return cuda_check("fvv_back_project");
+}
+
+}  // extern "C"

@@ -1,0 +1,351 @@
+"""Per-frame orchestration on the GPU (drop-in for freeview.pipeline).
+
+``run_frame`` keeps the reference's signature, stage names, stats and
+errors (pipeline.py:34-220). Inside, every stage runs on the current CUDA
+stream with its inputs resident on the device:
+
+  B-1 fvv_carve (stage grid)      -> occupancy bits
+  B-2 fvv_ccl26 -> component table (host sync #1: the ROI table is host
+      bookkeeping, hull.py:272-284, computed with numpy like the reference)
+  B-3 fvv_carve (all ROI grids in one launch)
+  C   fvv_mesh_prepare / fvv_mesh_emit (host sync #2: output sizes)
+  D-1 fvv_rasterize (all cameras in one launch; triangle count read on device)
+  D-2 fvv_classify  (all cameras, visibility as bits)
+
+Stage timings are CUDA-event device times. Host views (meshes, visibility
+flags, depth images) are materialised when the bundle is read.
+"""
+
+from __future__ import annotations
+
+import json
+from dataclasses import asdict, dataclass, replace
+
+import numpy as np
+import torch
+
+from ._device import DeviceSilhouettes, require_cuda
+from .bundle import SceneBundle, StageTimings
+from .hull import NoiseFilterParams, Roi, carve_grids, finish_labels, label_grid_async
+from .mesh import TriangleMesh, polygonize_grids
+from .visibility import bits_to_flags, classify_bits, raster_planes
+from .voxels import GridSpec
+
+
+class StageError(RuntimeError):
+    """A pipeline stage failed; ``stage`` names it (pipeline.py:34-38)."""
+
+    def __init__(self, stage: str, cause: Exception):
+        super().__init__(f"[{stage}] {cause}")
+        self.stage = stage
+        self.cause = cause
+
+
+@dataclass
+class AdaptiveParams:
+    """Silhouette-extraction thresholds (silhouette.py); carried for config
+    parity - extraction itself is upstream of this hot path."""
+
+    theta_near: float = 3.0
+    theta_far: float = 8.0
+    d_max: float = 32.0
+
+
+@dataclass
+class PipelineConfig:
+    """pipeline.py:41-101, same fields, defaults, validation and JSON form."""
+
+    stage_lo: tuple = (-9000.0, -9000.0, 0.0)
+    stage_hi: tuple = (9000.0, 9000.0, 9000.0)
+    coarse_spacing: float = 50.0
+    fine_spacing: float = 20.0
+    min_views: int = 1
+    t_small: int = 5
+    t_large: float = float("inf")
+    roi_margin: float = None  # default: one coarse voxel
+    t_v: float = None  # default: 3 * fine_spacing
+    iso_mode: str = "exact"
+    fixed_isovalue: float = 0.5
+    theta_near: float = 3.0
+    theta_far: float = 8.0
+    d_max: float = 32.0
+    block_dims: tuple = (16, 16, 16)
+    workers: int = 1
+
+    def __post_init__(self) -> None:
+        self.stage_lo = tuple(float(v) for v in self.stage_lo)
+        self.stage_hi = tuple(float(v) for v in self.stage_hi)
+        if self.fine_spacing > self.coarse_spacing:
+            raise ValueError("fine_spacing must be <= coarse_spacing")
+        if any(hi <= lo for lo, hi in zip(self.stage_lo, self.stage_hi)):
+            raise ValueError("stage volume must be nonempty")
+        if self.t_small < 0 or self.t_v is not None and self.t_v < 0:
+            raise ValueError("thresholds must be nonnegative")
+        if self.roi_margin is None:
+            self.roi_margin = self.coarse_spacing
+        if self.t_v is None:
+            self.t_v = 3.0 * self.fine_spacing
+        if self.iso_mode not in ("exact", "fixed"):
+            raise ValueError(f"unknown isovalue mode {self.iso_mode!r}")
+
+    @property
+    def adaptive_params(self) -> AdaptiveParams:
+        return AdaptiveParams(self.theta_near, self.theta_far, self.d_max)
+
+    @property
+    def noise_params(self) -> NoiseFilterParams:
+        return NoiseFilterParams(self.t_small, self.t_large)
+
+    def coarse_spec(self) -> GridSpec:
+        return GridSpec.from_aabb(self.stage_lo, self.stage_hi, self.coarse_spacing)
+
+    def to_json(self, path) -> None:
+        d = asdict(self)
+        d["t_large"] = None if np.isinf(self.t_large) else self.t_large
+        with open(path, "w", encoding="utf-8") as fh:
+            json.dump(d, fh, indent=2)
+            fh.write("\n")
+
+    @classmethod
+    def from_json(cls, path) -> "PipelineConfig":
+        with open(path, "r", encoding="utf-8") as fh:
+            d = json.load(fh)
+        if d.get("t_large") is None:
+            d["t_large"] = float("inf")
+        return cls(**{k: (tuple(v) if isinstance(v, list) else v) for k, v in d.items()})
+
+
+class _StageClock:
+    """CUDA events at stage boundaries on the current stream."""
+
+    def __init__(self):
+        self.marks = []
+
+    def mark(self, name):
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        self.marks.append((name, ev))
+
+    def timings(self) -> StageTimings:
+        t = StageTimings()
+        for (_, a), (name, b) in zip(self.marks, self.marks[1:]):
+            setattr(t, name, a.elapsed_time(b))
+        return t
+
+
+class FrameResult:
+    """Device-side outputs of B-1 .. D-2 for one frame."""
+
+    def __init__(self):
+        self.stats = {}
+
+
+def reconstruct(cfg: PipelineConfig, rig, dsils: DeviceSilhouettes, clock=None) -> FrameResult:
+    """B-1 .. D-2 on the GPU for one frame; outputs stay on the device."""
+    r = FrameResult()
+    clock = clock or _StageClock()
+    cams = list(rig)
+
+    def stage(name, fn):
+        try:
+            return fn()
+        except StageError:
+            raise
+        except Exception as exc:  # noqa: BLE001  (reference wraps every failure)
+            raise StageError(name, exc) from exc
+
+    spec = cfg.coarse_spec()
+    r.spec = spec
+    r.stats["sparse_tests"] = spec.num_voxels
+    clock.mark("start")
+    r.coarse = stage("B-1 sparse carve", lambda: carve_grids(dsils, [spec], cfg.min_views)[0])
+    clock.mark("sparse_carve")
+
+    def b2():
+        lab = finish_labels(r.coarse, *label_grid_async(r.coarse))
+        params = cfg.noise_params
+        comps = [c for c in lab.components if params.keeps(c.voxel_count)]
+        rois = []
+        for c in comps:  # hull.py:272-284 with the reference's numpy expressions
+            lo = spec.origin + spec.spacing * np.asarray(c.bbox_min, dtype=np.float64) - \
+                cfg.roi_margin
+            hi = spec.origin + spec.spacing * (np.asarray(c.bbox_max, dtype=np.float64) + 1.0) \
+                + cfg.roi_margin
+            rois.append(Roi(np.maximum(lo, spec.origin), np.minimum(hi, spec.extent), c.id))
+        return lab, comps, rois
+
+    r.labeling, r.components, r.rois = stage("B-2 noise filter/ROI", b2)
+    r.stats["sparse_occupied"] = r.coarse.occupied_count  # synced by B-2 already
+    r.stats["components"] = len(r.components)
+    clock.mark("noise_filter_roi")
+
+    def b3():
+        specs = [GridSpec.from_aabb(roi.lo, roi.hi, cfg.fine_spacing) for roi in r.rois]
+        return carve_grids(dsils, specs, cfg.min_views) if specs else []
+
+    r.fine = stage("B-3 dense carve", b3)
+    r.stats["dense_tests"] = sum(g.spec.num_voxels for g in r.fine)
+    clock.mark("dense_carve")
+
+    def c():
+        if not r.fine:
+            return None
+        return polygonize_grids(r.fine, rig, dsils, cfg.iso_mode, cfg.fixed_isovalue,
+                                [roi.component_id for roi in r.rois])
+
+    r.batch = stage("C polygonize", c)
+    clock.mark("polygonize")
+    if r.batch is not None and r.batch.verts.shape[0] > 0:
+        verts, tris = r.batch.verts, r.batch.tris
+        nt_dev = r.batch.num_triangles_dev
+        r.planes = stage("D-1 depth images",
+                         lambda: raster_planes(verts, tris, cams, want_ids=False, nt_dev=nt_dev))
+        clock.mark("depth_images")
+        r.vis_bits = stage("D-2 visibility",
+                           lambda: classify_bits(verts, tris, r.planes, cfg.t_v, nt_dev=nt_dev))
+        clock.mark("visibility")
+    else:
+        r.planes = None
+        r.vis_bits = None
+        clock.mark("depth_images")
+        clock.mark("visibility")
+    r.clock = clock
+    return r
+
+
+def _finish_stats(r: FrameResult):
+    """Read the device-side counts (one sync) into the reference's stats keys."""
+    dense_counts = [g._count for g in r.fine]
+    if dense_counts:
+        occ = torch.stack([c.reshape(()) for c in dense_counts]).cpu().numpy()
+        r.stats["dense_occupied"] = int(occ.sum())
+    else:
+        r.stats["dense_occupied"] = 0
+    if r.batch is not None:
+        totals, _ = r.batch.host_info()
+        st = [r.batch.stats(g) for g in range(len(r.fine))]
+        r.stats["fallback_edges"] = sum(s.fallback_edges for s in st)
+        r.stats["inconsistent_edge_starts"] = sum(s.inconsistent_starts for s in st)
+        r.stats["triangles"] = int(totals[2])
+    else:
+        r.stats["fallback_edges"] = 0
+        r.stats["inconsistent_edge_starts"] = 0
+        r.stats["triangles"] = 0
+
+
+class _LazyVisibility(dict):
+    """camera id -> (T,) bool, unpacked from the device bit rows on first read."""
+
+    def __init__(self, ids, bits_host, n):
+        super().__init__()
+        self._ids = list(ids)
+        self._bits = bits_host
+        self._n = n
+        for i in self._ids:
+            dict.__setitem__(self, i, None)
+
+    def __getitem__(self, key):
+        v = dict.__getitem__(self, key)
+        if v is None:
+            row = self._ids.index(key)
+            v = bits_to_flags(self._bits[row], self._n) if self._n else np.zeros(0, dtype=bool)
+            dict.__setitem__(self, key, v)
+        return v
+
+    def values(self):
+        return [self[k] for k in self._ids]
+
+    def items(self):
+        return [(k, self[k]) for k in self._ids]
+
+    def get(self, key, default=None):
+        return self[key] if key in self else default
+
+
+def compute_silhouettes(cfg, rig, frames, proposals, background):
+    """Adaptive silhouette extraction (silhouette.py) sits upstream of this
+    hot path and is not rebuilt yet."""
+    raise NotImplementedError("silhouette extraction is not part of the B200 hot path yet; "
+                              "pass sils=")
+
+
+def run_frame(cfg: PipelineConfig, rig, frames: dict, sils=None, proposals: dict = None,
+              background: dict = None, frame_id: int = 0, keep_depths: bool = False) -> SceneBundle:
+    """Reconstruct one frame into a SceneBundle (pipeline.py:115-220) on the GPU.
+
+    ``sils`` may be the reference's list of (H, W) bool arrays, a stacked
+    (N, H, W) uint8/bool tensor (pinned host or device), or a
+    DeviceSilhouettes already resident on the GPU."""
+    if sils is None:
+        if proposals is None or background is None:
+            raise StageError("silhouette", ValueError("need sils or proposals+background"))
+        try:
+            sils = compute_silhouettes(cfg, rig, frames, proposals, background)
+        except Exception as exc:
+            raise StageError("silhouette", exc) from exc
+    try:
+        require_cuda()
+        dsils = sils if isinstance(sils, DeviceSilhouettes) else DeviceSilhouettes(rig, sils)
+    except Exception as exc:
+        raise StageError("B-1 sparse carve", exc) from exc
+    r = reconstruct(cfg, rig, dsils)
+    return bundle_from(r, cfg, rig, frames, frame_id, keep_depths)
+
+
+def bundle_from(r: FrameResult, cfg, rig, frames, frame_id=0, keep_depths=False) -> SceneBundle:
+    """Host-side SceneBundle over a device FrameResult (one sync)."""
+    _finish_stats(r)
+    timings = r.clock.timings()
+    cams = list(rig)
+    meshes = r.batch.meshes() if r.batch is not None else []
+    nt = r.stats["triangles"]
+    if r.vis_bits is not None:
+        vis = _LazyVisibility([c.id for c in cams], r.vis_bits.cpu().numpy(), nt)
+    else:
+        vis = {c.id: np.zeros(0, dtype=bool) for c in cams}
+    depths = {}
+    if keep_depths:
+        for i, c in enumerate(cams):
+            depths[c.id] = (r.planes.depth_of(i).cpu().numpy() if r.planes is not None
+                            else np.full((c.image_height, c.image_width), np.inf))
+    stats = {k: r.stats[k] for k in ("sparse_tests", "sparse_occupied", "components", "dense_tests",
+                                     "dense_occupied", "fallback_edges",
+                                     "inconsistent_edge_starts", "triangles")}
+    bundle = SceneBundle(frame_id=frame_id, rig=rig, meshes=meshes,
+                         textures=dict(frames) if frames is not None else {}, visibility=vis,
+                         timings=timings, stats=stats, stage_lo=np.array(cfg.stage_lo),
+                         stage_hi=np.array(cfg.stage_hi), depths=depths)
+    bundle._merged = r.batch.merged() if r.batch is not None else TriangleMesh.empty()
+    bundle._result = r
+    return bundle
+
+
+def sweep(cfg: PipelineConfig, rig, sils, axis: str, values) -> list:
+    """run_frame per spacing value on fixed inputs (pipeline.py:223-243)."""
+    if axis not in ("coarse_spacing", "fine_spacing"):
+        raise ValueError(f"unknown sweep axis {axis!r}")
+    if list(values) != sorted(values):
+        raise ValueError("sweep values must be ascending")
+    dsils = DeviceSilhouettes(rig, sils)
+    rows = []
+    for v in values:
+        if axis == "coarse_spacing":
+            run_cfg = replace(cfg, coarse_spacing=float(v), roi_margin=None, t_v=cfg.t_v)
+            if run_cfg.fine_spacing > run_cfg.coarse_spacing:
+                raise ValueError(f"coarse value {v} below fine_spacing")
+        else:
+            run_cfg = replace(cfg, fine_spacing=float(v), t_v=None)
+        bundle = run_frame(run_cfg, rig, frames={c.id: None for c in rig}, sils=dsils)
+        rows.append((float(v), bundle.timings))
+    return rows
+
+
+def sweep_csv(rows, path) -> None:
+    import csv
+
+    with open(path, "w", newline="", encoding="utf-8") as fh:
+        w = csv.writer(fh)
+        w.writerow(["value"] + [label for _, label in StageTimings.LABELS] + ["total"])
+        for value, t in rows:
+            w.writerow([value] + [f"{getattr(t, k):.3f}" for k, _ in StageTimings.LABELS]
+                       + [f"{t.total:.3f}"])
