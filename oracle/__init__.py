@@ -73,7 +73,9 @@ def lib():
 
 
 def _p(a):
-    return ctypes.c_void_p(a.ctypes.data)
+    p = ctypes.c_void_p(a.ctypes.data)
+    p._keep = a  # inline temporaries must outlive the call
+    return p
 
 
 def cam_struct(cams) -> np.ndarray:

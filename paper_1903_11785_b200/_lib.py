@@ -86,11 +86,18 @@ def call(name: str, *args) -> None:
 
 
 def host_ptr(a: np.ndarray):
-    return ctypes.c_void_p(a.ctypes.data)
+    """Pointer to a host array that keeps the array alive for the call
+    (arguments are often temporaries built inline)."""
+    p = ctypes.c_void_p(a.ctypes.data)
+    p._keep = a
+    return p
 
 
 def dev_ptr(t):
-    return ctypes.c_void_p(t.data_ptr())
+    """Device pointer of a tensor, holding a reference to it."""
+    p = ctypes.c_void_p(t.data_ptr())
+    p._keep = t
+    return p
 
 
 def i64(v):
