@@ -139,7 +139,7 @@ __device__ __forceinline__ int32_t rank_of(const uint32_t *occ, const int32_t *w
 // -- 2. union over the 13 negative neighbours --------------------------------
 __global__ void ccl_union_kernel(const uint32_t *__restrict__ occ, CclWs w, int64_t nx, int64_t ny,
                                  int64_t nz) {
-  const int64_t n_on = *(volatile int64_t *)w.counts;
+  const int64_t n_on = __ldcg(w.counts);
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_on;
        r += (int64_t)gridDim.x * blockDim.x) {
     const int64_t l = w.on_list[r];
@@ -162,7 +162,7 @@ __global__ void ccl_union_kernel(const uint32_t *__restrict__ occ, CclWs w, int6
 
 // -- 3. flatten ----------------------------------------------------------------
 __global__ void ccl_flatten_kernel(CclWs w) {
-  const int64_t n_on = *(volatile int64_t *)w.counts;
+  const int64_t n_on = __ldcg(w.counts);
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_on;
        r += (int64_t)gridDim.x * blockDim.x)
     w.parent[r] = uf_find(w.parent, (int32_t)r);
@@ -179,7 +179,7 @@ struct RootLabel {
 };
 
 __global__ void ccl_stats_init_kernel(CclWs w) {
-  const int64_t ncomp = *(volatile int64_t *)(w.counts + 1);
+  const int64_t ncomp = __ldcg(w.counts + 1);
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ncomp;
        c += (int64_t)gridDim.x * blockDim.x) {
     int32_t *s = w.stats + 8 * c;
@@ -192,7 +192,7 @@ __global__ void ccl_stats_init_kernel(CclWs w) {
 
 // -- 5. per-rank label + component count/bbox ----------------------------------
 __global__ void ccl_stats_kernel(CclWs w, int64_t nx, int64_t ny) {
-  const int64_t n_on = *(volatile int64_t *)w.counts;
+  const int64_t n_on = __ldcg(w.counts);
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t r0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; r0 < n_on;
@@ -228,7 +228,7 @@ __global__ void ccl_stats_kernel(CclWs w, int64_t nx, int64_t ny) {
 }
 
 __global__ void ccl_export_kernel(CclWs w, fvv_component *out, int64_t cap) {
-  const int64_t ncomp = *(volatile int64_t *)(w.counts + 1);
+  const int64_t ncomp = __ldcg(w.counts + 1);
   const int64_t n = ncomp < cap ? ncomp : cap;
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
        c += (int64_t)gridDim.x * blockDim.x) {
@@ -245,7 +245,7 @@ __global__ void ccl_export_kernel(CclWs w, fvv_component *out, int64_t cap) {
 }
 
 __global__ void ccl_expand_kernel(CclWs w, int32_t *labels) {
-  const int64_t n_on = *(volatile int64_t *)w.counts;
+  const int64_t n_on = __ldcg(w.counts);
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_on;
        r += (int64_t)gridDim.x * blockDim.x)
     labels[w.on_list[r]] = w.rank_label[r];
@@ -254,7 +254,7 @@ __global__ void ccl_expand_kernel(CclWs w, int32_t *labels) {
 // hull.py:257-269: keep[label] selects survivors; ids are not renumbered.
 __global__ void ccl_filter_kernel(CclWs w, const uint8_t *__restrict__ keep, int32_t *labels,
                                   uint32_t *occ_out, int64_t *kept) {
-  const int64_t n_on = *(volatile int64_t *)w.counts;
+  const int64_t n_on = __ldcg(w.counts);
   int64_t mine = 0;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_on;
        r += (int64_t)gridDim.x * blockDim.x) {

@@ -71,4 +71,13 @@ __device__ __forceinline__ bool sil_bit(const uint32_t *__restrict__ plane, int 
 
 inline int sil_stride_words(int width) { return (width + 31) >> 5; }
 
+// Element count produced on the device by an earlier launch, else the host
+// value. (A `p ? *p : fallback` select on a __grid_constant__ member makes
+// nvcc form a generic pointer into parameter space; keep it a value select.)
+__device__ __forceinline__ int64_t device_count(const int64_t *p, int64_t fallback) {
+  int64_t v = fallback;
+  if (p != nullptr) v = __ldcg(p);
+  return v;
+}
+
 }  // namespace fvv

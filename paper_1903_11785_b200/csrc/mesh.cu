@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(128)
 __global__ void __launch_bounds__(128)
     mesh_lambda_kernel(const __grid_constant__ MeshGrids G, const __grid_constant__ MeshCams C,
                        MeshBufs B, const uint32_t *__restrict__ sil) {
-  const int64_t nv = *(volatile int64_t *)B.totals;
+  const int64_t nv = __ldcg(B.totals);
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv;
        v += (int64_t)gridDim.x * blockDim.x) {
     int axis;
@@ -516,7 +516,7 @@ __global__ void mesh_slot_bases_kernel(const __grid_constant__ MeshGrids G, Mesh
 
 // ---- B5: triangle emission ----------------------------------------------------
 __global__ void mesh_emit_kernel(const __grid_constant__ MeshGrids G, MeshBufs B) {
-  const int64_t S = *(volatile int64_t *)(B.totals + 1);
+  const int64_t S = __ldcg(B.totals + 1);
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < S;
        c += (int64_t)gridDim.x * blockDim.x) {
     const int m = B.cell_mask[c];

@@ -123,7 +123,7 @@ struct RasterArgs {
 
 __global__ void __launch_bounds__(kRasterThreads)
     raster_small_kernel(const __grid_constant__ RasterCams C, RasterArgs A) {
-  const int64_t nt = A.nt_dev ? *(volatile const int64_t *)A.nt_dev : A.nt;
+  const int64_t nt = device_count(A.nt_dev, A.nt);
   const int64_t total = nt * C.ncam;
   const bool gemv = A.nv == 1;
   for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(kRasterThreads)
           A.queue[slot] = w;
           continue;
         }
-      } else if (*(volatile int64_t *)A.qcount <= A.qcap) {
+      } else if (__ldcg(A.qcount) <= A.qcap) {
         continue;  // pass 1: the big kernel replays the queue
       }
       // queue overflowed: walk it here (atomicMin is idempotent, so a queued
@@ -161,8 +161,8 @@ __global__ void __launch_bounds__(kRasterThreads)
 
 __global__ void __launch_bounds__(kBigThreads)
     raster_big_kernel(const __grid_constant__ RasterCams C, RasterArgs A) {
-  const int64_t nt = A.nt_dev ? *(volatile const int64_t *)A.nt_dev : A.nt;
-  int64_t nq = *(volatile int64_t *)A.qcount;
+  const int64_t nt = device_count(A.nt_dev, A.nt);
+  int64_t nq = __ldcg(A.qcount);
   if (nq > A.qcap) nq = A.qcap;
   const bool gemv = A.nv == 1;
   for (int64_t q = blockIdx.x; q < nq; q += gridDim.x) {
@@ -205,7 +205,7 @@ struct ClassifyArgs {
 };
 
 __global__ void classify_kernel(const __grid_constant__ RasterCams C, ClassifyArgs A) {
-  const int64_t nt = A.nt_dev ? *(volatile const int64_t *)A.nt_dev : A.nt;
+  const int64_t nt = device_count(A.nt_dev, A.nt);
   const bool gemv = nt == 1;
   const int lane = threadIdx.x & 31;
   const int64_t words = (nt + 31) / 32;
@@ -248,7 +248,7 @@ struct SourceArgs {
 };
 
 __global__ void sources_kernel(const __grid_constant__ SourceArgs A) {
-  const int64_t nt = A.nt_dev ? *(volatile const int64_t *)A.nt_dev : A.nt;
+  const int64_t nt = device_count(A.nt_dev, A.nt);
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nt;
        t += (int64_t)gridDim.x * blockDim.x) {
     int32_t s = -1;

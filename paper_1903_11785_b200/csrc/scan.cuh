@@ -23,7 +23,7 @@ constexpr int kScanChunk = kScanThreads * kScanItems;  // 1024 elements per chun
 constexpr int kScanGrid = 148 * 4;
 
 __device__ __forceinline__ int64_t scan_len(const int64_t *n_dev, int64_t n_host) {
-  return n_dev ? *(volatile const int64_t *)n_dev : n_host;
+  return device_count(n_dev, n_host);
 }
 
 template <class F, typename T>
