@@ -1,0 +1,465 @@
+#!/usr/bin/env python
+"""FVV frames/s benchmark (BASELINE.json metric) on the C3 volleyball workload.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+One step = one synthetic frame through B-1 sparse carve, B-2 CCL/filter/ROI,
+B-3 ROI carve, C exact polygonisation, D-1 depth images, D-2 visibility and
+one 1920x1080 virtual-view colour pass. Frames are sharded
+across ranks (frame f -> rank f mod N, no collective on the data path:
+weak scaling). Rank 0 prints one JSON line.
+
+  value : frames/s, inputs resident in HBM, device time (CUDA events,
+          barrier + synchronize on both sides, max over ranks)
+  e2e   : frames/s through the public API (pipeline.run_frame +
+          render.render_view) from pinned host buffers, H2D of every
+          frame's silhouettes and colour frames and D2H of the mesh,
+          visibility flags and rendered image inside the timed region
+  --impl reference : the CPU oracle port of the reference pipeline
+          (oracle/, C + OpenMP, all host threads), same workload and metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
+METRIC = "FVV frames/sec (carve+CCL+mesh+color) at 1/2/4/8 B200; Gvoxel-projections/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="C3")
+    ap.add_argument("--frames", type=int, default=4, help="distinct input frames per rank")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--stage-json", default=None, help="write per-stage ms here (rank 0)")
+    return ap.parse_args()
+
+
+def dist_setup(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([float(x)], device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([float(x)], device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100", "-f", self.path],
+                stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except Exception:  # noqa: BLE001
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+        rows = []
+        with open(self.path) as fh:
+            for line in fh:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = sorted(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None,
+                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def peaks():
+    try:
+        with open(MEASURED_PEAKS) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)", p
+    except Exception:  # noqa: BLE001
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)", {}
+
+
+# ---------------------------------------------------------------- inputs
+def make_inputs(wl, frame_ids):
+    """Silhouettes (N,H,W) uint8 and colour frames (N,H,W,3) uint8 on the GPU."""
+    from paper_1903_11785_b200 import synthetic as S
+
+    out = []
+    for f in frame_ids:
+        masks, frames = S.render_scene_device(wl.rig, wl.objects(f), shade=True)
+        out.append((f, masks, frames))
+    return out
+
+
+def algorithmic_work(result, ncam):
+    """Voxel-camera projections of one frame: every voxel of the stage grid
+    and of every ROI grid against every camera (hull.py:83-90)."""
+    coarse = result.spec.num_voxels
+    fine = sum(g.spec.num_voxels for g in result.fine)
+    return (coarse + fine) * ncam
+
+
+# ---------------------------------------------------------------- b200 arm
+def run_b200(args):
+    import numpy as np
+    import torch
+
+    from paper_1903_11785_b200 import _lib, workloads
+    from paper_1903_11785_b200._device import DeviceSilhouettes
+    from paper_1903_11785_b200.pipeline import _StageClock, reconstruct, run_frame
+    from paper_1903_11785_b200.render import frames_device, render_device, render_view
+
+    rank, world, local = dist_setup(args)
+    wl = workloads.get(args.workload)
+    rig, cfg, virt = wl.rig, wl.cfg, wl.virtual
+    cams = list(rig)
+    ncam = len(cams)
+    frame_ids = [rank + world * i for i in range(args.frames)]
+    inputs = make_inputs(wl, frame_ids)
+    torch.cuda.synchronize()
+
+    dev_frames = []
+    for f, masks, frames in inputs:
+        fb = frames.reshape(-1)
+        foff = np.arange(ncam, dtype=np.int64) * (frames.shape[1] * frames.shape[2] * 3)
+        dev_frames.append((masks, fb, foff))
+
+    stage_sum = {}
+    work = {"proj": 0, "tris": 0, "frames": 0}
+
+    def device_step(i, timed):
+        masks, fb, foff = dev_frames[i % len(dev_frames)]
+        clock = _StageClock()
+        dsils = DeviceSilhouettes(rig, masks)
+        r = reconstruct(cfg, rig, dsils, clock)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        if r.batch is not None and r.vis_bits is not None:
+            render_device(r.batch.verts, r.batch.tris, int(r.batch.tris.shape[0]), cams, fb, foff,
+                          r.vis_bits, int(r.vis_bits.shape[1]), virt,
+                          nt_dev=r.batch.num_triangles_dev)
+        e1.record()
+        if timed:
+            r._render_events = (e0, e1)
+            r._clock = clock
+            work["proj"] += algorithmic_work(r, ncam)
+            work["frames"] += 1
+        return r
+
+    for i in range(args.warmup):
+        device_step(i, False)
+    torch.cuda.synchronize()
+    lib = _lib.load()
+    barrier(world)
+    sampler = ClockSampler(local if "CUDA_VISIBLE_DEVICES" not in os.environ else
+                           os.environ["CUDA_VISIBLE_DEVICES"].split(",")[local])
+    sampler.start()
+    launches0 = lib.fvv_launch_count()
+    torch.cuda.synchronize()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record()
+    results = [device_step(i, True) for i in range(args.steps)]
+    t_end.record()
+    torch.cuda.synchronize()
+    launches = lib.fvv_launch_count() - launches0
+    barrier(world)
+    clocks = sampler.stop()
+    ms_local = t_start.elapsed_time(t_end)
+    ms = max_over_ranks(ms_local, world)
+
+    for r in results:
+        for k, v in r._clock.timings().to_dict().items():
+            stage_sum[k] = stage_sum.get(k, 0.0) + v
+        stage_sum["render"] = stage_sum.get("render", 0.0) + r._render_events[0].elapsed_time(
+            r._render_events[1])
+        work["tris"] += int(r.batch.host_info()[0][2]) if r.batch is not None else 0
+    stage_ms = {k: v / args.steps for k, v in stage_sum.items()}
+
+    total_frames = sum_over_ranks(args.steps, world)
+    total_proj = sum_over_ranks(work["proj"], world)
+    value = total_frames / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel ----
+    hbm_peak, peak_src, _ = peaks()
+    H, W = cams[0].image_height, cams[0].image_width
+    top = max(stage_ms, key=stage_ms.get)
+    roof = roofline_for(top, stage_ms[top], results, ncam, H, W, hbm_peak, peak_src)
+
+    # ---- e2e through the public API from pinned host memory ----
+    e2e = None
+    if not args.no_e2e:
+        host = []
+        for f, masks, frames in inputs:
+            m_h = masks.cpu().pin_memory()
+            f_h = frames.cpu().pin_memory()
+            host.append((m_h, {c.id: f_h[k] for k, c in enumerate(cams)}))
+        h2d = int(host[0][0].numel() + sum(t.numel() for t in host[0][1].values()))
+
+        def e2e_step(i):
+            m_h, f_h = host[i % len(host)]
+            bundle = run_frame(cfg, rig, f_h, sils=m_h)
+            merged = bundle.merged_mesh
+            img = render_view(merged, rig, f_h, bundle.visibility, virt)
+            v, t = merged.vertices, merged.triangles  # D2H of the mesh
+            vis_bytes = bundle.visibility._bits.nbytes if hasattr(bundle.visibility, "_bits") \
+                else 0
+            return (v.nbytes + t.nbytes + vis_bytes + img.color.nbytes + img.source.nbytes +
+                    img.covered.nbytes)
+
+        for i in range(min(args.warmup, 2)):
+            e2e_step(i)
+        torch.cuda.synchronize()
+        barrier(world)
+        t0 = time.perf_counter()
+        d2h = 0
+        for i in range(args.steps):
+            d2h += e2e_step(i)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        barrier(world)
+        e2e_ms = max_over_ranks((t1 - t0) * 1e3, world)
+        e2e = {"value": round(total_frames / (e2e_ms / 1e3), 3), "unit": "frames/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(d2h / args.steps),
+               "ms_per_step": round(e2e_ms / args.steps, 3),
+               "api": "pipeline.run_frame + render.render_view, pinned host inputs"}
+
+    # ---- CPU baseline: the oracle port on this box's host cores, rank 0, N=1 ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(wl, inputs[0])
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": round(value, 3),
+            "unit": "frames/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms / args.steps, 4),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (GPU ray-cast ellipsoid figures, BASELINE C3)",
+            "config": {"workload": f"{wl.name}: {wl.description}", "cameras": ncam,
+                       "image": f"{W}x{H}", "coarse_mm": cfg.coarse_spacing,
+                       "fine_mm": cfg.fine_spacing, "virtual_view": "1920x1080",
+                       "frames_cycled": args.frames,
+                       "l2": f"inputs cycle over {args.frames} frames x "
+                             f"{(ncam * H * W * 4) / 1e6:.0f} MB (> 126 MB L2)",
+                       "parallelism": f"frame-sharded x{world}"},
+            "gvoxel_proj_per_s": round(total_proj / (ms / 1e3) / 1e9, 2),
+            "triangles_per_frame": int(work["tris"] / max(args.steps, 1)),
+            "stage_ms": {k: round(v, 4) for k, v in stage_ms.items()},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+        }
+        print(json.dumps(line))
+        if args.stage_json:
+            with open(args.stage_json, "w") as fh:
+                json.dump(line, fh, indent=2)
+
+
+def roofline_for(stage, ms, results, ncam, H, W, hbm_peak, peak_src):
+    """Algorithmic bytes of the dominant stage's kernels per launch / time."""
+    r = results[0]
+    nvox_c = r.spec.num_voxels
+    nvox_f = sum(g.spec.num_voxels for g in r.fine)
+    tris = int(r.batch.host_info()[0][2]) if r.batch is not None else 0
+    verts = int(r.batch.verts.shape[0]) if r.batch is not None else 0
+    sil_bytes = ncam * H * ((W + 31) // 32) * 4
+    per_stage = {
+        # silhouette planes read once + occupancy bits written
+        "sparse_carve": ("fvv_carve (B-1)", sil_bytes + nvox_c / 8),
+        "dense_carve": ("fvv_carve (B-3)", sil_bytes + nvox_f / 8),
+        # occupancy bits + int32 label per voxel
+        "noise_filter_roi": ("fvv_ccl26", nvox_c / 8 + 4 * nvox_c),
+        # occupancy bits read, vertices + triangles written, silhouettes read
+        "polygonize": ("fvv_mesh_prepare+emit", nvox_f / 8 + 24 * verts + 12 * tris + sil_bytes),
+        # every camera's float64 depth plane written once, mesh read once per camera
+        "depth_images": ("fvv_rasterize (16 cams)", ncam * H * W * 8 + ncam * (24 * verts +
+                                                                             12 * tris)),
+        # centroid depth lookups + visibility bits
+        "visibility": ("fvv_classify", ncam * tris * 8 + ncam * tris / 8 + 24 * verts +
+                       12 * tris),
+        # virtual view depth + id planes, colour/source written, 4 texel reads per pixel
+        "render": ("fvv_rasterize+fvv_render_view (virtual)", 1920 * 1080 * (8 + 4 + 3 + 4 + 1)),
+    }
+    kernel, nbytes = per_stage.get(stage, (stage, 0.0))
+    achieved = nbytes / (ms / 1e3) / 1e9
+    return {"bound": "hbm", "kernel": kernel, "stage": stage, "achieved": round(achieved, 2),
+            "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
+            "frac": round(achieved / hbm_peak, 5), "traffic": None,
+            "algorithmic_bytes": int(nbytes), "ms_per_launch": round(ms, 4)}
+
+
+# ---------------------------------------------------------------- CPU arm
+def cpu_frame(wl, masks_np, frames_np):
+    """One frame through the CPU oracle (B-1..D-2 + virtual colour pass)."""
+    import oracle as O
+
+    cfg = wl.cfg
+    cams = list(wl.rig)
+    out = O.run_frame(cams, masks_np, cfg.stage_lo, cfg.stage_hi, cfg.coarse_spacing,
+                      cfg.fine_spacing, cfg.min_views, cfg.t_small, cfg.t_large, cfg.roi_margin,
+                      cfg.t_v)
+    v, t, _ = out["merged"]
+    if len(t):
+        O.render_view(v, t, cams, frames_np, out["visibility"], wl.virtual)
+    return out
+
+
+def cpu_baseline(wl, inp):
+    _, masks, frames = inp
+    masks_np = [m.cpu().numpy().astype(bool) for m in masks]
+    fr = frames.cpu().numpy()
+    frames_np = {c.id: fr[k] for k, c in enumerate(wl.rig)}
+    t0 = time.perf_counter()
+    cpu_frame(wl, masks_np, frames_np)
+    dt = time.perf_counter() - t0
+    return {"value": round(1.0 / dt, 5), "unit": "frames/s", "cores": os.cpu_count(),
+            "kind": "port",
+            "sample": f"1 {wl.name} frame (B-1..D-2 + 1080p colour pass) through oracle/ "
+                      f"(C restatement of the reference, OpenMP {os.cpu_count()} threads), "
+                      f"{dt:.2f} s"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    import numpy as np
+
+    from paper_1903_11785_b200 import synthetic as S
+    from paper_1903_11785_b200 import workloads
+
+    wl = workloads.get(args.workload)
+    ids = list(range(max(1, min(args.frames, 2))))
+    inputs = []
+    for f in ids:
+        try:
+            import torch
+
+            if not torch.cuda.is_available():
+                raise RuntimeError
+            masks, frames = S.render_scene_device(wl.rig, wl.objects(f))
+            masks_np = [m.cpu().numpy().astype(bool) for m in masks]
+            fr = frames.cpu().numpy()
+            frames_np = {c.id: fr[k] for k, c in enumerate(wl.rig)}
+        except Exception:  # noqa: BLE001  (no GPU: generate on the host)
+            sils, frames_np = S.render_scene(wl.rig, wl.objects(f))
+            masks_np = sils
+        inputs.append((masks_np, frames_np))
+    for i in range(args.warmup):
+        cpu_frame(wl, *inputs[i % len(inputs)])
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        cpu_frame(wl, *inputs[i % len(inputs)])
+    dt = time.perf_counter() - t0
+    value = args.steps / dt
+    print(json.dumps({
+        "metric": METRIC, "value": round(value, 5), "unit": "frames/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 2),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (ellipsoid figures, BASELINE C3)", "impl": "reference",
+        "config": {"workload": f"{wl.name}: {wl.description}"},
+        "cpu_baseline": {"value": round(value, 5), "unit": "frames/s", "cores": os.cpu_count(),
+                         "kind": "port",
+                         "sample": "every step = 1 full frame (B-1..D-2 + 1080p colour pass) "
+                                   "through oracle/ (C restatement of the reference pipeline)"},
+        "e2e": {"value": round(value, 5), "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -65,6 +65,8 @@ typedef struct fvv_component {
 
 const char *fvv_last_error(void);
 int fvv_version(void);
+/* Number of kernels this library has launched (all entry points). */
+long long fvv_launch_count(void);
 
 /* camera.py:164-201 project(cam, p, use_distortion) for n points (float64
  * (n,3)); writes pixel (n,2), camera-frame z (n,), in_frustum (n,) 0/1.
@@ -215,6 +217,17 @@ int fvv_render_view(const fvv_camera *rig, int ncam, const uint8_t *frames_dev,
 /* camera.py:204-220 back_project for n pixels (n,2) at depths (n,) -> (n,3). */
 int fvv_back_project(const fvv_camera *cam, const double *pixel_dev, const double *depth_dev,
                      int64_t n, double *out_dev, void *stream);
+
+/* ---- harness (not hot path): synthetic scene inputs ------------------------- */
+
+/* Ray-cast nparts ellipsoids (float64 records: centre[3], orientation[9]
+ * row-major (columns = ellipsoid axes), semi-axes[3], rgb[3]) into camera
+ * `cam`: silhouette uint8 (H,W) and Lambertian frame uint8 (H,W,3); either
+ * output may be NULL. shading = {ambient, light dir xyz, background rgb}.
+ * GPU twin of synthetic.py render_camera (reference synthetic.py:165-218). */
+int fvv_render_ellipsoids(const fvv_camera *cam, const double *parts_dev, int nparts,
+                          uint8_t *sil_dev, uint8_t *rgb_dev, const double *shading,
+                          void *stream);
 
 #ifdef __cplusplus
 }

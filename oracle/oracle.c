@@ -445,11 +445,12 @@ static inline int or_top_left(double ax, double ay, double bx, double by) {
 
 /* visibility.py:34-98 (rasterize). Rows [row0, row1) only, so callers can
  * split the image across threads without changing any pixel's result. */
-static void or_raster_rows(const double *px, const double *pz, const int32_t *tris, int64_t nt,
-                           const or_cam *cam, double *depth, int32_t *tri_id, int64_t row0,
-                           int64_t row1) {
+static void or_raster_rows(const double *px, const double *pz, const int32_t *tris,
+                           const int64_t *list, int64_t nlist, const or_cam *cam, double *depth,
+                           int32_t *tri_id, int64_t row0, int64_t row1) {
     int64_t W = cam->width, H = cam->height;
-    for (int64_t t = 0; t < nt; ++t) {
+    for (int64_t li = 0; li < nlist; ++li) {
+        int64_t t = list[li];
         const int32_t *tv = tris + 3 * t;
         double x0 = px[2 * tv[0]], y0 = px[2 * tv[0] + 1];
         double x1 = px[2 * tv[1]], y1 = px[2 * tv[1] + 1];
@@ -516,10 +517,45 @@ OR_HOT void or_rasterize(const double *verts, int64_t nv, const int32_t *tris, i
         or_project1(cam, verts[3 * i], verts[3 * i + 1], verts[3 * i + 2], 0, gemv, &px[2 * i],
                     &px[2 * i + 1], &pz[i], &in);
     }
-    int64_t band = 16;
+    /* bin triangles into 16-row bands (ascending id inside each band), so
+     * bands rasterise independently; a pixel's result only depends on the
+     * triangles covering it, visited in ascending id exactly as before. */
+    const int64_t band = 16, nband = (H + band - 1) / band;
+    int64_t *cnt = (int64_t *)calloc((size_t)nband + 1, sizeof(int64_t));
+    int64_t *b0 = (int64_t *)malloc((size_t)nt * sizeof(int64_t));
+    int64_t *b1 = (int64_t *)malloc((size_t)nt * sizeof(int64_t));
+    for (int64_t t = 0; t < nt; ++t) {
+        const int32_t *tv = tris + 3 * t;
+        double y0 = px[2 * tv[0] + 1], y1 = px[2 * tv[1] + 1], y2 = px[2 * tv[2] + 1];
+        double mny = fmin(fmin(y0, y1), y2), mxy = fmax(fmax(y0, y1), y2);
+        b0[t] = 1;
+        b1[t] = 0; /* empty unless the row span meets the image */
+        if (isnan(mny) || isnan(mxy)) continue;
+        double fly = floor(mny), chy = ceil(mxy);
+        if (fly > (double)(H - 1) || chy < 0.0) continue;
+        int64_t lo = fly > 0.0 ? (int64_t)fly : 0;
+        int64_t hi = chy < (double)(H - 1) ? (int64_t)chy : H - 1;
+        b0[t] = lo / band;
+        b1[t] = hi / band;
+        for (int64_t b = b0[t]; b <= b1[t]; ++b) cnt[b + 1] += 1;
+    }
+    for (int64_t b = 0; b < nband; ++b) cnt[b + 1] += cnt[b];
+    int64_t *lists = (int64_t *)malloc((size_t)(cnt[nband] > 0 ? cnt[nband] : 1) * sizeof(int64_t));
+    int64_t *fill = (int64_t *)malloc((size_t)nband * sizeof(int64_t));
+    for (int64_t b = 0; b < nband; ++b) fill[b] = cnt[b];
+    for (int64_t t = 0; t < nt; ++t)
+        for (int64_t b = b0[t]; b <= b1[t]; ++b) lists[fill[b]++] = t;
 #pragma omp parallel for schedule(dynamic, 1)
-    for (int64_t r0 = 0; r0 < H; r0 += band)
-        or_raster_rows(px, pz, tris, nt, cam, depth, tri_id, r0, r0 + band < H ? r0 + band : H);
+    for (int64_t b = 0; b < nband; ++b) {
+        int64_t r0 = b * band;
+        or_raster_rows(px, pz, tris, lists + cnt[b], cnt[b + 1] - cnt[b], cam, depth, tri_id, r0,
+                       r0 + band < H ? r0 + band : H);
+    }
+    free(cnt);
+    free(b0);
+    free(b1);
+    free(lists);
+    free(fill);
     free(px);
     free(pz);
 }

@@ -37,13 +37,13 @@ assert CAM_DTYPE.itemsize == 192 and GRID_DTYPE.itemsize == 56 and COMP_DTYPE.it
 
 # exported symbols; tests check the .so exports every one of them
 SYMBOLS = (
-    "fvv_last_error", "fvv_version", "fvv_project",
+    "fvv_last_error", "fvv_version", "fvv_launch_count", "fvv_project",
     "fvv_pack_silhouettes", "fvv_carve", "fvv_ccl_workspace_bytes", "fvv_ccl26",
     "fvv_ccl_components", "fvv_ccl_labels", "fvv_filter_labels", "fvv_filter_dense",
     "fvv_mesh_workspace_bytes", "fvv_mesh_prepare", "fvv_mesh_counts",
     "fvv_mesh_emit_scratch_bytes", "fvv_mesh_emit", "fvv_edge_isovalues",
     "fvv_raster_workspace_bytes", "fvv_rasterize", "fvv_classify", "fvv_triangle_sources",
-    "fvv_render_view", "fvv_back_project",
+    "fvv_render_view", "fvv_back_project", "fvv_render_ellipsoids",
 )
 
 
@@ -65,6 +65,7 @@ def load():
             )
         lib = ctypes.CDLL(LIB_PATH)
         lib.fvv_last_error.restype = ctypes.c_char_p
+        lib.fvv_launch_count.restype = ctypes.c_longlong
         lib.fvv_ccl_workspace_bytes.restype = ctypes.c_size_t
         lib.fvv_mesh_workspace_bytes.restype = ctypes.c_size_t
         lib.fvv_mesh_emit_scratch_bytes.restype = ctypes.c_size_t

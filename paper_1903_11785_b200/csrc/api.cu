@@ -1,5 +1,6 @@
 // C-ABI plumbing (errors, version) plus the small camera kernels:
 // fvv_project (camera.py:164-201) and fvv_pack_silhouettes (hull.py:63-75).
+#include <atomic>
 #include <cstdarg>
 #include <cstring>
 
@@ -8,6 +9,9 @@
 namespace fvv {
 
 static thread_local char g_err[512] = "";
+static std::atomic<long long> g_launches{0};
+
+void note_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 void set_error(const char *fmt, ...) {
   va_list ap;
@@ -80,6 +84,8 @@ const char *fvv_last_error(void) { return g_err; }
 
 int fvv_version(void) { return 1; }
 
+long long fvv_launch_count(void) { return g_launches.load(); }
+
 int fvv_project(const fvv_camera *cam, const double *pts_dev, int64_t n, int use_distortion,
                 int single_point, double *pixel_dev, double *z_dev, uint8_t *in_dev,
                 void *stream) {
@@ -93,6 +99,7 @@ int fvv_project(const fvv_camera *cam, const double *pts_dev, int64_t n, int use
   project_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(*cam, pts_dev, n, use_distortion != 0,
                                                            single_point != 0, pixel_dev, z_dev,
                                                            in_dev);
+  note_launches(1);
   return cuda_check("fvv_project");
 }
 
@@ -120,6 +127,7 @@ int fvv_pack_silhouettes(const fvv_camera *cams, int ncam, const uint8_t *masks_
   int64_t blocks = (warps * 32 + 255) / 256;
   if (blocks > 148 * 32) blocks = 148 * 32;
   pack_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(p);
+  note_launches(1);
   return cuda_check("fvv_pack_silhouettes");
 }
 

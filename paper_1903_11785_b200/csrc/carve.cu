@@ -138,5 +138,6 @@ extern "C" int fvv_carve(const fvv_camera *cams, int ncam, const uint32_t *sil_d
     return FVV_E_LIMIT;
   }
   carve_kernel<<<(unsigned)blocks, kCarveThreads, 0, st>>>(p);
+  note_launches(1);
   return cuda_check("fvv_carve");
 }

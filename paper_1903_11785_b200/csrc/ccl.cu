@@ -324,6 +324,7 @@ int fvv_ccl26(const uint32_t *occ_dev, const fvv_grid *grid, void *ws_dev, size_
   ccl_stats_init_kernel<<<kCclGrid, 256, 0, st>>>(w);
   ccl_stats_kernel<<<kCclGrid, 256, 0, st>>>(w, nx, ny);
   if (comps_dev) ccl_export_kernel<<<kCclGrid, 256, 0, st>>>(w, comps_dev, comp_cap);
+  note_launches(4 + (comps_dev ? 1 : 0));
   if (counts_dev) cudaMemcpyAsync(counts_dev, w.counts, 2 * sizeof(int64_t),
                                   cudaMemcpyDeviceToDevice, st);
   return cuda_check("fvv_ccl26");
@@ -334,6 +335,7 @@ int fvv_ccl_components(const fvv_grid *grid, const void *ws_dev, fvv_component *
   const int64_t nvox = grid->dims[0] * grid->dims[1] * grid->dims[2];
   CclWs w = ccl_layout((void *)ws_dev, grid->dims);
   ccl_export_kernel<<<kCclGrid, 256, 0, (cudaStream_t)stream>>>(w, comps_dev, comp_cap);
+  note_launches(1);
   return cuda_check("fvv_ccl_components");
 }
 
@@ -343,6 +345,7 @@ int fvv_ccl_labels(const fvv_grid *grid, const void *ws_dev, int32_t *labels_dev
   cudaStream_t st = (cudaStream_t)stream;
   cudaMemsetAsync(labels_dev, 0, sizeof(int32_t) * nvox, st);
   ccl_expand_kernel<<<kCclGrid, 256, 0, st>>>(w, labels_dev);
+  note_launches(1);
   return cuda_check("fvv_ccl_labels");
 }
 
@@ -355,6 +358,7 @@ int fvv_filter_labels(const fvv_grid *grid, const void *ws_dev, const uint8_t *k
   if (occ_dev) cudaMemsetAsync(occ_dev, 0, sizeof(uint32_t) * ((nvox + 31) / 32), st);
   if (kept_dev) cudaMemsetAsync(kept_dev, 0, sizeof(int64_t), st);
   ccl_filter_kernel<<<kCclGrid, 256, 0, st>>>(w, keep_dev, labels_dev, occ_dev, kept_dev);
+  note_launches(1);
   return cuda_check("fvv_filter_labels");
 }
 
@@ -365,6 +369,7 @@ int fvv_filter_dense(const int32_t *labels_in_dev, int64_t nvox, const uint8_t *
   if (kept_dev) cudaMemsetAsync(kept_dev, 0, sizeof(int64_t), st);
   dense_filter_kernel<<<kCclGrid, 256, 0, st>>>(labels_in_dev, nvox, nkeep, keep_dev, labels_dev,
                                                 occ_dev, kept_dev);
+  note_launches(1);
   return cuda_check("fvv_filter_dense");
 }
 

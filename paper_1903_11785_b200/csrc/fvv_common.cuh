@@ -17,6 +17,8 @@ constexpr double kDegenerateArea = 1e-9;  // mesh.py:22
 
 void set_error(const char *fmt, ...);
 int cuda_check(const char *what);
+// kernels launched by this library (bench.py reports the timed-region delta)
+void note_launches(long long n);
 
 // camera.py:177 `pts @ R.T + t`: OpenBLAS gemm (>= 2 rows) accumulates
 // fma(z,R2, fma(y,R1, x*R0)); the 1-row gemv kernel fma(z,R2, fma(x,R0, y*R1)).

@@ -670,12 +670,14 @@ int fvv_mesh_prepare(const fvv_grid *grids, int ngrid, const uint32_t *occ_dev,
   cudaMemsetAsync(B.totals, 0, 32, st);
   if (h_grids.tw_total > 0) {
     mesh_transpose_kernel<<<kMeshGrid, 256, 0, st>>>(h_grids, B);
+    note_launches(1);
     EdgeFlags ef{h_grids, B.tw, B.eflags, B.vprefix};
     ordered_scan(ef, nullptr, 3 * h_grids.tw_total, B.sums, B.totals + 0, st);
     CellFlags cf{h_grids, B.tw, B.sflags, B.sprefix};
     ordered_scan(cf, nullptr, h_grids.tw_total, B.sums, B.totals + 1, st);
   }
   mesh_grid_counts_kernel<<<1, 128, 0, st>>>(h_grids, B);
+  note_launches(1);
   return cuda_check("fvv_mesh_prepare");
 }
 
@@ -751,9 +753,11 @@ int fvv_mesh_emit(const fvv_camera *cams_by_id, int ncam, const uint32_t *sil_de
   if (num_vertices > 0) {
     mesh_vertex_list_kernel<<<kMeshGrid, 256, 0, st>>>(h_grids, B);
     mesh_lambda_kernel<<<kMeshGrid, 128, 0, st>>>(h_grids, h_cams, B, sil_dev);
+    note_launches(2);
   }
   if (num_cells > 0) {
     mesh_cells_kernel<<<kMeshGrid, 256, 0, st>>>(h_grids, B);
+    note_launches(1);
     TriScan ts{B.cell_mask, B.cprefix};
     ordered_scan(ts, B.totals + 1, 0, cell_sums, d_total, st);
   } else {
@@ -761,6 +765,7 @@ int fvv_mesh_emit(const fvv_camera *cams_by_id, int ncam, const uint32_t *sil_de
   }
   mesh_slot_bases_kernel<<<1, 32, 0, st>>>(h_grids, B, d_total);
   if (num_cells > 0) mesh_emit_kernel<<<kMeshGrid, 256, 0, st>>>(h_grids, B);
+  note_launches(1 + (num_cells > 0 ? 1 : 0));
   return cuda_check("fvv_mesh_emit");
 }
 
@@ -787,6 +792,7 @@ int fvv_edge_isovalues(const fvv_camera *cams_by_id, int ncam, const uint32_t *s
   if (blocks > kMeshGrid) blocks = kMeshGrid;
   edge_isovalues_kernel<<<(int)blocks, 128, 0, st>>>(h_cams, sil_dev, p_on_dev, p_off_dev, n,
                                                       lam_dev, cam_dev, stats_dev);
+  note_launches(1);
   return cuda_check("fvv_edge_isovalues");
 }
 

@@ -429,6 +429,7 @@ int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int
     const int64_t n = (int64_t)cams[c].width * cams[c].height;
     fill_u64_kernel<<<256, 256, 0, st>>>((unsigned long long *)(depth_dev + plane_off[c]), n,
                                          0x7ff0000000000000ull);
+    note_launches(1);
     if (tri_id_dev) cudaMemsetAsync(tri_id_dev + plane_off[c], 0xff, 4 * n, st);
   }
   if (nt <= 0) return cuda_check("fvv_rasterize");
@@ -448,6 +449,7 @@ int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int
     A.pass = pass;
     raster_small_kernel<<<kRasterGrid, kRasterThreads, 0, st>>>(C, A);
     raster_big_kernel<<<148 * 4, kBigThreads, 0, st>>>(C, A);
+    note_launches(2);
   }
   return cuda_check("fvv_rasterize");
 }
@@ -461,6 +463,7 @@ int fvv_classify(const fvv_camera *cams, int ncam, const double *verts_dev,
   if (rc) return rc;
   ClassifyArgs A{verts_dev, tris_dev, nt, nt_dev, depth_dev, t_v, vis_dev, vis_stride_words};
   classify_kernel<<<kRasterGrid, 256, 0, (cudaStream_t)stream>>>(C, A);
+  note_launches(1);
   return cuda_check("fvv_classify");
 }
 
@@ -484,6 +487,7 @@ int fvv_triangle_sources(const int32_t *rank_pos, const int32_t *rank_id, int nr
   A.nt_dev = nt_dev;
   A.src = src_dev;
   sources_kernel<<<kRasterGrid, 256, 0, (cudaStream_t)stream>>>(A);
+  note_launches(1);
   return cuda_check("fvv_triangle_sources");
 }
 
@@ -518,6 +522,7 @@ int fvv_render_view(const fvv_camera *rig, int ncam, const uint8_t *frames_dev,
   cudaMemsetAsync(counts_dev, 0, sizeof(int64_t) * (1 + ncam), st);
   render_count_kernel<<<kRasterGrid, 256, 0, st>>>(A);
   render_color_kernel<<<kRasterGrid, 256, 0, st>>>(A);
+  note_launches(2);
   return cuda_check("fvv_render_view");
 }
 
@@ -528,6 +533,7 @@ int fvv_back_project(const fvv_camera *cam, const double *pixel_dev, const doubl
   if (blocks > kRasterGrid) blocks = kRasterGrid;
   back_project_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(*cam, pixel_dev, depth_dev,
                                                                       n, out_dev);
+  note_launches(1);
   return cuda_check("fvv_back_project");
 }
 

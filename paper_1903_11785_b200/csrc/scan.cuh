@@ -103,6 +103,7 @@ inline void ordered_scan(const F &f, const int64_t *n_dev, int64_t n_host, T *su
   chunk_reduce_kernel<F, T><<<kScanGrid, kScanThreads, 0, st>>>(f, n_dev, n_host, sums);
   chunk_scan_kernel<T><<<1, 1024, 0, st>>>(sums, n_dev, n_host, total);
   chunk_emit_kernel<F, T><<<kScanGrid, kScanThreads, 0, st>>>(f, n_dev, n_host, sums);
+  note_launches(3);
 }
 
 inline int64_t scan_chunks(int64_t n_max) { return (n_max + kScanChunk - 1) / kScanChunk + 1; }

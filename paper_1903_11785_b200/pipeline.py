@@ -301,6 +301,7 @@ def bundle_from(r: FrameResult, cfg, rig, frames, frame_id=0, keep_depths=False)
     nt = r.stats["triangles"]
     if r.vis_bits is not None:
         vis = _LazyVisibility([c.id for c in cams], r.vis_bits.cpu().numpy(), nt)
+        vis._device_bits = r.vis_bits  # render_view reads these directly (rig order)
     else:
         vis = {c.id: np.zeros(0, dtype=bool) for c in cams}
     depths = {}

@@ -149,7 +149,11 @@ def render_view(mesh, rig, frames: dict, vis: dict, virtual, fallback_color=FALL
                              np.zeros((h, w), bool))
     verts, tris = mesh.device_arrays()
     n = mesh.num_triangles
-    bits, stride = _vis_bits_from_dict(vis, rig, n, dev)
+    dbits = getattr(vis, "_device_bits", None)
+    if dbits is not None and getattr(vis, "_n", -1) == n and list(vis) == [c.id for c in rig]:
+        bits, stride = dbits, int(dbits.shape[1])  # run_frame's bits, still on the GPU
+    else:
+        bits, stride = _vis_bits_from_dict(vis, rig, n, dev)
     fbuf, foff = frames_device(rig, frames, dev)
     color, source, covered, counts = render_device(verts, tris, n, rig, fbuf, foff, bits, stride,
                                                    virtual, fallback_color)

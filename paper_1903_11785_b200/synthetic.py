@@ -285,3 +285,43 @@ def place_figures(n, area_lo, area_hi, seed=0, t=0.0, min_gap=1200.0):
                            phase=float(rng.uniform(0, 2 * np.pi)), t=t,
                            color=palette[i % len(palette)]))
     return figs
+
+
+def parts_table(objects) -> np.ndarray:
+    """(P, 18) float64 records for fvv_render_ellipsoids."""
+    parts = scene_parts(objects)
+    tab = np.zeros((len(parts), 18))
+    for i, p in enumerate(parts):
+        tab[i, 0:3] = p.center
+        tab[i, 3:12] = p.orient.reshape(9)
+        tab[i, 12:15] = p.semi_axes
+        tab[i, 15:18] = p.color
+    return tab
+
+
+def render_scene_device(rig, objects, shade=True):
+    """GPU ray cast of the scene into every rig camera (harness kernel
+    fvv_render_ellipsoids). Returns (masks uint8 (N,H,W), frames uint8
+    (N,H,W,3) or None) as CUDA tensors; all cameras must share one size."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    from ._device import cam_table, require_cuda, stream_handle
+
+    dev = require_cuda()
+    cams = list(rig)
+    h, w = cams[0].image_height, cams[0].image_width
+    if any((c.image_height, c.image_width) != (h, w) for c in cams):
+        raise ValueError("render_scene_device needs equal image sizes")
+    tab = torch.from_numpy(np.ascontiguousarray(parts_table(objects))).to(dev)
+    masks = torch.empty((len(cams), h, w), dtype=torch.uint8, device=dev)
+    frames = torch.empty((len(cams), h, w, 3), dtype=torch.uint8, device=dev) if shade else None
+    shading = np.array([AMBIENT, *LIGHT_DIR, *BG_COLOR], dtype=np.float64)
+    for i, c in enumerate(cams):
+        _lib.call("fvv_render_ellipsoids", _lib.host_ptr(cam_table([c])), _lib.dev_ptr(tab),
+                  ctypes.c_int(len(tab)), _lib.dev_ptr(masks[i]),
+                  _lib.dev_ptr(frames[i]) if shade else ctypes.c_void_p(0),
+                  _lib.host_ptr(shading), stream_handle())
+    return masks, frames
