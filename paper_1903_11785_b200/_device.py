@@ -23,9 +23,34 @@ def stream_handle():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+_CAM_CACHE = {}
+
+
+def _cam_key(c):
+    return (int(c.id), int(c.image_width), int(c.image_height), float(c.fx), float(c.fy),
+            float(c.cx), float(c.cy), float(c.skew),
+            np.asarray(c.dist, dtype=np.float64).tobytes(),
+            np.asarray(c.rotation, dtype=np.float64).tobytes(),
+            np.asarray(c.translation, dtype=np.float64).tobytes())
+
+
 def cam_table(cams) -> np.ndarray:
-    """CameraModel-like objects -> fvv_camera records (include/fvv.h)."""
+    """CameraModel-like objects -> fvv_camera records (include/fvv.h),
+    memoised on the cameras' parameter values (rigs are reused every frame)."""
     cams = list(cams)
+    key = tuple(_cam_key(c) for c in cams)
+    hit = _CAM_CACHE.get(key)
+    if hit is not None:
+        return hit
+    out = _build_cam_table(cams)
+    if len(_CAM_CACHE) > 256:
+        _CAM_CACHE.clear()
+    out.setflags(write=False)
+    _CAM_CACHE[key] = out
+    return out
+
+
+def _build_cam_table(cams) -> np.ndarray:
     out = np.zeros(len(cams), dtype=_lib.CAM_DTYPE)
     for i, c in enumerate(cams):
         dist = np.asarray(c.dist, dtype=np.float64).reshape(5)
