@@ -171,8 +171,9 @@ int fvv_edge_isovalues(const fvv_camera *cams_by_id, int ncam, const uint32_t *s
 
 /* ---- D-1 / D-2: visibility.py:34-140 --------------------------------------- */
 
-/* Scratch for fvv_rasterize (queue of large-bbox triangles). */
-size_t fvv_raster_workspace_bytes(int64_t num_triangles, int ncam);
+/* Scratch for fvv_rasterize: projected vertices of every camera and the
+ * queue of large-bbox triangles. */
+size_t fvv_raster_workspace_bytes(int64_t num_vertices, int64_t num_triangles, int ncam);
 
 /* visibility.py:34-98 rasterize for ncam cameras at once (zero-distortion
  * projection, near clip 1 mm, top-left rule, perspective-correct depth).

@@ -71,7 +71,7 @@ def load():
         lib.fvv_mesh_emit_scratch_bytes.restype = ctypes.c_size_t
         lib.fvv_mesh_emit_scratch_bytes.argtypes = [ctypes.c_int64, ctypes.c_int64]
         lib.fvv_raster_workspace_bytes.restype = ctypes.c_size_t
-        lib.fvv_raster_workspace_bytes.argtypes = [ctypes.c_int64, ctypes.c_int]
+        lib.fvv_raster_workspace_bytes.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int]
         _lib = lib
     return _lib
 

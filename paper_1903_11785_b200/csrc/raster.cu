@@ -39,30 +39,41 @@ __device__ __forceinline__ bool top_left(double ax, double ay, double bx, double
   return dy < 0.0 || (dy == 0.0 && dx < 0.0);
 }
 
-// visibility.py:48-78 for triangle t in camera `cam`. False = skipped.
-__device__ __forceinline__ bool tri_setup(const fvv_camera &cam, const double *__restrict__ V,
-                                          const int32_t *__restrict__ T, int64_t t, bool gemv,
-                                          TriSetup &s) {
-  const int32_t ia = T[3 * t], ib = T[3 * t + 1], ic = T[3 * t + 2];
-  double u[3], v[3], z[3];
-  const int32_t idx[3] = {ia, ib, ic};
-#pragma unroll
-  for (int q = 0; q < 3; ++q) {
-    const double *p = V + 3 * (int64_t)idx[q];
-    project_exact(cam, p[0], p[1], p[2], false, gemv, u[q], v[q], z[q]);
+// visibility.py:50: every vertex projected once per camera (zero distortion,
+// gemm order; gemv when the mesh has one vertex) -> (u, v, z, pad) records.
+__global__ void raster_vertex_kernel(const __grid_constant__ RasterCams C,
+                                     const double *__restrict__ V, int64_t nv,
+                                     double4 *__restrict__ proj) {
+  const bool gemv = nv == 1;
+  const int64_t total = nv * C.ncam;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(w / nv);
+    const int64_t i = w - (int64_t)c * nv;
+    double u, v, z;
+    project_exact(C.cams[c], V[3 * i], V[3 * i + 1], V[3 * i + 2], false, gemv, u, v, z);
+    proj[w] = make_double4(u, v, z, 0.0);
   }
+}
+
+// visibility.py:48-78 for triangle t from its projected vertices. False = skipped.
+__device__ __forceinline__ bool tri_setup(int width, int height, const double4 *__restrict__ P,
+                                          const int32_t *__restrict__ T, int64_t t,
+                                          TriSetup &s) {
+  const double4 pa = P[T[3 * t]], pb = P[T[3 * t + 1]], pc = P[T[3 * t + 2]];
+  const double u[3] = {pa.x, pb.x, pc.x}, v[3] = {pa.y, pb.y, pc.y}, z[3] = {pa.z, pb.z, pc.z};
   if (!(z[0] > kNearClip && z[1] > kNearClip && z[2] > kNearClip)) return false;
   if (isnan(u[0]) || isnan(u[1]) || isnan(u[2]) || isnan(v[0]) || isnan(v[1]) || isnan(v[2]))
     return false;
   const double mnx = fmin(fmin(u[0], u[1]), u[2]), mxx = fmax(fmax(u[0], u[1]), u[2]);
   const double mny = fmin(fmin(v[0], v[1]), v[2]), mxy = fmax(fmax(v[0], v[1]), v[2]);
   const double flx = floor(mnx), fly = floor(mny), chx = ceil(mxx), chy = ceil(mxy);
-  const double W1 = (double)(cam.width - 1), H1 = (double)(cam.height - 1);
+  const double W1 = (double)(width - 1), H1 = (double)(height - 1);
   if (flx > W1 || fly > H1 || chx < 0.0 || chy < 0.0) return false;
   s.lox = flx > 0.0 ? (int)flx : 0;
   s.loy = fly > 0.0 ? (int)fly : 0;
-  s.hix = chx < W1 ? (int)chx : cam.width - 1;
-  s.hiy = chy < H1 ? (int)chy : cam.height - 1;
+  s.hix = chx < W1 ? (int)chx : width - 1;
+  s.hiy = chy < H1 ? (int)chy : height - 1;
   if (s.hix < s.lox || s.hiy < s.loy) return false;
   double x0 = u[0], y0 = v[0], x1 = u[1], y1 = v[1], x2 = u[2], y2 = v[2];
   double za = z[0], zb = z[1], zc = z[2];
@@ -101,14 +112,14 @@ __device__ __forceinline__ void pixel_update(int pass, double d, int64_t t,
                                              unsigned long long *depth, unsigned *ids) {
   const unsigned long long bits = (unsigned long long)__double_as_longlong(d);
   if (pass == 0) {
-    if (bits < *(volatile unsigned long long *)depth) atomicMin(depth, bits);
-  } else if (bits == *depth) {
+    atomicMin(depth, bits);  // result unused -> RED.MIN (no round trip)
+  } else if (bits == __ldcg(depth)) {
     atomicMin(ids, (unsigned)t);
   }
 }
 
 struct RasterArgs {
-  const double *V;
+  const double4 *P;  // [ncam][nv] projected vertices
   const int32_t *T;
   int64_t nt;
   const int64_t *nt_dev;
@@ -121,18 +132,17 @@ struct RasterArgs {
   int pass;
 };
 
-__global__ void __launch_bounds__(kRasterThreads)
+__global__ void __launch_bounds__(kRasterThreads, 6)
     raster_small_kernel(const __grid_constant__ RasterCams C, RasterArgs A) {
   const int64_t nt = device_count(A.nt_dev, A.nt);
   const int64_t total = nt * C.ncam;
-  const bool gemv = A.nv == 1;
   for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
        w += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(w / nt);
     const int64_t t = w - (int64_t)c * nt;
-    const fvv_camera &cam = C.cams[c];
+    const int width = C.cams[c].width, height = C.cams[c].height;
     TriSetup s;
-    if (!tri_setup(cam, A.V, A.T, t, gemv, s)) continue;
+    if (!tri_setup(width, height, A.P + (int64_t)c * A.nv, A.T, t, s)) continue;
     const int64_t npx = (int64_t)(s.hix - s.lox + 1) * (s.hiy - s.loy + 1);
     if (npx > kSmallBBox) {
       if (A.pass == 0) {
@@ -153,7 +163,7 @@ __global__ void __launch_bounds__(kRasterThreads)
       for (int x = s.lox; x <= s.hix; ++x) {
         double d;
         if (!tri_depth(s, x, y, d)) continue;
-        const int64_t p = (int64_t)y * cam.width + x;
+        const int64_t p = (int64_t)y * width + x;
         pixel_update(A.pass, d, t, dp + p, ip ? ip + p : nullptr);
       }
   }
@@ -164,14 +174,13 @@ __global__ void __launch_bounds__(kBigThreads)
   const int64_t nt = device_count(A.nt_dev, A.nt);
   int64_t nq = __ldcg(A.qcount);
   if (nq > A.qcap) nq = A.qcap;
-  const bool gemv = A.nv == 1;
   for (int64_t q = blockIdx.x; q < nq; q += gridDim.x) {
     const int64_t w = A.queue[q];
     const int c = (int)(w / nt);
     const int64_t t = w - (int64_t)c * nt;
-    const fvv_camera &cam = C.cams[c];
+    const int width = C.cams[c].width, height = C.cams[c].height;
     TriSetup s;
-    if (!tri_setup(cam, A.V, A.T, t, gemv, s)) continue;  // uniform per block
+    if (!tri_setup(width, height, A.P + (int64_t)c * A.nv, A.T, t, s)) continue;  // uniform
     const int bw = s.hix - s.lox + 1;
     const int64_t npx = (int64_t)bw * (s.hiy - s.loy + 1);
     unsigned long long *dp = (unsigned long long *)(A.depth + C.depth_off[c]);
@@ -180,7 +189,7 @@ __global__ void __launch_bounds__(kBigThreads)
       const int y = s.loy + (int)(k / bw), x = s.lox + (int)(k % bw);
       double d;
       if (!tri_depth(s, x, y, d)) continue;
-      const int64_t p = (int64_t)y * cam.width + x;
+      const int64_t p = (int64_t)y * width + x;
       pixel_update(A.pass, d, t, dp + p, ip ? ip + p : nullptr);
     }
   }
@@ -410,10 +419,15 @@ using namespace fvv;
 
 extern "C" {
 
-size_t fvv_raster_workspace_bytes(int64_t num_triangles, int ncam) {
+static int64_t raster_queue_cap(int64_t num_triangles, int ncam) {
   int64_t cap = num_triangles * (int64_t)ncam;
   if (cap > (4ll << 20)) cap = 4ll << 20;
-  return 256 + 8 * (size_t)(cap > 0 ? cap : 1);
+  return cap > 0 ? cap : 1;
+}
+
+size_t fvv_raster_workspace_bytes(int64_t num_vertices, int64_t num_triangles, int ncam) {
+  return 256 + 8 * (size_t)raster_queue_cap(num_triangles, ncam) +
+         sizeof(double4) * (size_t)(num_vertices > 0 ? num_vertices : 1) * (size_t)ncam;
 }
 
 int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int64_t nv,
@@ -433,8 +447,12 @@ int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int
     if (tri_id_dev) cudaMemsetAsync(tri_id_dev + plane_off[c], 0xff, 4 * n, st);
   }
   if (nt <= 0) return cuda_check("fvv_rasterize");
+  if (ws_bytes < fvv_raster_workspace_bytes(nv, nt, ncam)) {
+    set_error("fvv_rasterize: workspace %zu < %zu bytes", ws_bytes,
+              fvv_raster_workspace_bytes(nv, nt, ncam));
+    return FVV_E_ARG;
+  }
   RasterArgs A;
-  A.V = verts_dev;
   A.T = tris_dev;
   A.nt = nt;
   A.nt_dev = nt_dev;
@@ -443,8 +461,16 @@ int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int
   A.ids = tri_id_dev;
   A.qcount = (int64_t *)ws_dev;
   A.queue = (int64_t *)((char *)ws_dev + 256);
-  A.qcap = (int64_t)((ws_bytes - 256) / 8);
+  A.qcap = raster_queue_cap(nt, ncam);
+  double4 *proj = (double4 *)((char *)ws_dev + 256 + 8 * (size_t)A.qcap);
+  A.P = proj;
   cudaMemsetAsync(A.qcount, 0, 8, st);
+  {
+    int64_t blocks = (nv * ncam + 255) / 256;
+    if (blocks > kRasterGrid) blocks = kRasterGrid;
+    raster_vertex_kernel<<<(int)(blocks > 0 ? blocks : 1), 256, 0, st>>>(C, verts_dev, nv, proj);
+    note_launches(1);
+  }
   for (int pass = 0; pass < (tri_id_dev ? 2 : 1); ++pass) {
     A.pass = pass;
     raster_small_kernel<<<kRasterGrid, kRasterThreads, 0, st>>>(C, A);

@@ -74,7 +74,7 @@ def raster_planes(verts, tris, cams, want_ids=False, nt_dev=None) -> DevicePlane
     depth = torch.empty(total, dtype=torch.float64, device=dev)
     ids = torch.empty(total, dtype=torch.int32, device=dev) if want_ids else None
     nt = int(tris.shape[0]) if tris.numel() else 0
-    wsb = int(_lib.load().fvv_raster_workspace_bytes(nt, len(cams)))
+    wsb = int(_lib.load().fvv_raster_workspace_bytes(int(verts.shape[0]), nt, len(cams)))
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
     _lib.call("fvv_rasterize", _lib.host_ptr(tab), ctypes.c_int(len(cams)), _lib.dev_ptr(verts),
               _lib.i64(verts.shape[0]), _lib.dev_ptr(tris), _lib.i64(nt),
