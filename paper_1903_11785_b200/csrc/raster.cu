@@ -425,8 +425,12 @@ static int64_t raster_queue_cap(int64_t num_triangles, int ncam) {
   return cap > 0 ? cap : 1;
 }
 
+static size_t raster_proj_offset(int64_t num_triangles, int ncam) {
+  return (256 + 8 * (size_t)raster_queue_cap(num_triangles, ncam) + 255) & ~(size_t)255;
+}
+
 size_t fvv_raster_workspace_bytes(int64_t num_vertices, int64_t num_triangles, int ncam) {
-  return 256 + 8 * (size_t)raster_queue_cap(num_triangles, ncam) +
+  return raster_proj_offset(num_triangles, ncam) +
          sizeof(double4) * (size_t)(num_vertices > 0 ? num_vertices : 1) * (size_t)ncam;
 }
 
@@ -462,7 +466,7 @@ int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int
   A.qcount = (int64_t *)ws_dev;
   A.queue = (int64_t *)((char *)ws_dev + 256);
   A.qcap = raster_queue_cap(nt, ncam);
-  double4 *proj = (double4 *)((char *)ws_dev + 256 + 8 * (size_t)A.qcap);
+  double4 *proj = (double4 *)((char *)ws_dev + raster_proj_offset(nt, ncam));
   A.P = proj;
   cudaMemsetAsync(A.qcount, 0, 8, st);
   {
