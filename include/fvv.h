@@ -203,17 +203,26 @@ int fvv_triangle_sources(const int32_t *rank_pos, const int32_t *rank_id, int nr
                          const uint32_t *vis_dev, int64_t vis_stride_words, int64_t nt,
                          const int64_t *nt_dev, int32_t *src_dev, void *stream);
 
+/* render.py:96-110 bookkeeping of render_view: int64 counts_dev[1 + ncam] =
+ * {covered pixels, pixels sourced from rig camera c ...} of the virtual view
+ * (tri_id_dev from fvv_rasterize, tri_src_dev from fvv_triangle_sources).
+ * A count of 1 selects numpy's one-row BLAS order downstream, and the
+ * non-zero entries say which cameras' frames the colour pass reads. */
+int fvv_render_count(const fvv_camera *rig, int ncam, const fvv_camera *virt,
+                     const int32_t *tri_id_dev, const int32_t *tri_src_dev, int64_t *counts_dev,
+                     void *stream);
+
 /* render.py:64-113 render_view colour pass, given the virtual view's depth /
- * triangle-id planes (fvv_rasterize) and per-triangle source ids: back-
- * projects each covered pixel, projects it (with distortion) into its source
- * camera and samples that camera's (H,W,3) uint8 frame (frames_dev +
- * frame_off[c], rig order) bilinearly; fallback colour where no camera sees
- * the triangle. counts_dev: int64[1 + ncam] scratch. */
+ * triangle-id planes, per-triangle source ids and fvv_render_count's counts:
+ * back-projects each covered pixel, projects it (with distortion) into its
+ * source camera and samples that camera's (H,W,3) uint8 frame (frames_dev +
+ * frame_off[c], rig order; only cameras with a non-zero count are read)
+ * bilinearly; fallback colour where no camera sees the triangle. */
 int fvv_render_view(const fvv_camera *rig, int ncam, const uint8_t *frames_dev,
                     const int64_t *frame_off, const fvv_camera *virt, const double *depth_dev,
                     const int32_t *tri_id_dev, const int32_t *tri_src_dev, const uint8_t *fallback,
                     uint8_t *color_dev, int32_t *source_dev, uint8_t *covered_dev,
-                    int64_t *counts_dev, void *stream);
+                    const int64_t *counts_dev, void *stream);
 
 /* camera.py:204-220 back_project for n pixels (n,2) at depths (n,) -> (n,3). */
 int fvv_back_project(const fvv_camera *cam, const double *pixel_dev, const double *depth_dev,

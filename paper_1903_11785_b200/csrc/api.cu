@@ -55,6 +55,32 @@ struct PackParams {
   int64_t word_start[FVV_MAX_CAMS + 1];  // cumulative words over cameras
 };
 
+// Rows whose width is a multiple of 32 (1080p, 4K): each thread turns 32
+// mask bytes (two 16-byte loads) into one word, so a warp streams 1 KB.
+__global__ void pack_wide_kernel(const __grid_constant__ PackParams p) {
+  const int64_t total = p.word_start[p.ncam];
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    int c = 0;
+    while (w >= p.word_start[c + 1]) ++c;
+    const int64_t local = w - p.word_start[c];
+    const uint4 *src = reinterpret_cast<const uint4 *>(p.masks + p.mask_off[c] + local * 32);
+    const uint4 a = __ldcs(src), b = __ldcs(src + 1);
+    const uint32_t q[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint32_t bits = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      // byte j of q[k] nonzero -> bit 4k + j
+      const uint32_t v = q[k];
+      bits |= (uint32_t)((v & 0x000000ffu) != 0) << (4 * k);
+      bits |= (uint32_t)((v & 0x0000ff00u) != 0) << (4 * k + 1);
+      bits |= (uint32_t)((v & 0x00ff0000u) != 0) << (4 * k + 2);
+      bits |= (uint32_t)((v & 0xff000000u) != 0) << (4 * k + 3);
+    }
+    p.sil[p.sil_off[c] + local] = bits;
+  }
+}
+
 // One warp builds one 32-pixel word from 32 coalesced mask bytes (ballot).
 __global__ void pack_kernel(const __grid_constant__ PackParams p) {
   const int lane = threadIdx.x & 31;
@@ -123,10 +149,19 @@ int fvv_pack_silhouettes(const fvv_camera *cams, int ncam, const uint8_t *masks_
     p.height[c] = cams[c].height;
     p.word_start[c + 1] = p.word_start[c] + (int64_t)sil_stride_words(cams[c].width) * cams[c].height;
   }
-  int64_t warps = p.word_start[ncam];
-  int64_t blocks = (warps * 32 + 255) / 256;
-  if (blocks > 148 * 32) blocks = 148 * 32;
-  pack_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(p);
+  bool wide = ((uintptr_t)masks_dev & 15) == 0;
+  for (int c = 0; c < ncam; ++c)
+    wide = wide && (cams[c].width % 32 == 0) && (mask_off[c] % 16 == 0);
+  int64_t words = p.word_start[ncam];
+  if (wide) {
+    int64_t blocks = (words + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    pack_wide_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(p);
+  } else {
+    int64_t blocks = (words * 32 + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    pack_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(p);
+  }
   note_launches(1);
   return cuda_check("fvv_pack_silhouettes");
 }

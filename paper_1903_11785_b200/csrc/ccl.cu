@@ -106,12 +106,28 @@ __device__ __forceinline__ int32_t uf_find(const int32_t *parent, int32_t x) {
   return x;
 }
 
+// find with path halving: every visited node is re-pointed at its
+// grandparent. Plain stores are safe: they only ever replace a parent by one
+// of its ancestors (smaller index), never touch a root, and the atomicMin
+// linking in uf_unite re-checks roots, so connectivity and the min-root
+// invariant are preserved (the forest only gets shallower).
+__device__ __forceinline__ int32_t uf_find_halving(int32_t *parent, int32_t x) {
+  int32_t p = __ldcg(parent + x);
+  while (p != x) {
+    const int32_t g = __ldcg(parent + p);
+    if (g != p) __stcg(parent + x, g);
+    x = p;
+    p = g;
+  }
+  return x;
+}
+
 // Link the two trees; the smaller root wins (hull.py:146-153 links likewise).
 __device__ __forceinline__ void uf_unite(int32_t *parent, int32_t a, int32_t b) {
   bool done;
   do {
-    a = uf_find(parent, a);
-    b = uf_find(parent, b);
+    a = uf_find_halving(parent, a);
+    b = uf_find_halving(parent, b);
     if (a < b) {
       int32_t old = atomicMin(parent + b, a);
       done = (old == b);

@@ -521,38 +521,61 @@ int fvv_triangle_sources(const int32_t *rank_pos, const int32_t *rank_id, int nr
   return cuda_check("fvv_triangle_sources");
 }
 
-int fvv_render_view(const fvv_camera *rig, int ncam, const uint8_t *frames_dev,
-                    const int64_t *frame_off, const fvv_camera *virt, const double *depth_dev,
-                    const int32_t *tri_id_dev, const int32_t *tri_src_dev, const uint8_t *fallback,
-                    uint8_t *color_dev, int32_t *source_dev, uint8_t *covered_dev,
-                    int64_t *counts_dev, void *stream) {
+static int fill_render(RenderArgs &A, const fvv_camera *rig, int ncam, const uint8_t *frames_dev,
+                       const int64_t *frame_off, const fvv_camera *virt, const double *depth_dev,
+                       const int32_t *tri_id_dev, const int32_t *tri_src_dev,
+                       const uint8_t *fallback, uint8_t *color_dev, int32_t *source_dev,
+                       uint8_t *covered_dev, int64_t *counts_dev) {
   if (ncam < 1 || ncam > FVV_MAX_CAMS) {
-    set_error("fvv_render_view: %d cameras", ncam);
+    set_error("render: %d cameras", ncam);
     return FVV_E_LIMIT;
   }
-  static thread_local RenderArgs A;
   memset(&A, 0, sizeof(A));
   A.virt = *virt;
   A.ncam = ncam;
   for (int c = 0; c < ncam; ++c) {
     A.cams[c] = rig[c];
     A.cam_id[c] = rig[c].id;
-    A.frame_off[c] = frame_off[c];
+    A.frame_off[c] = frame_off ? frame_off[c] : 0;
   }
   A.frames = frames_dev;
   A.depth = depth_dev;
   A.ids = tri_id_dev;
   A.tri_src = tri_src_dev;
-  for (int ch = 0; ch < 3; ++ch) A.fallback[ch] = fallback[ch];
+  for (int ch = 0; ch < 3; ++ch) A.fallback[ch] = fallback ? fallback[ch] : 0;
   A.color = color_dev;
   A.source = source_dev;
   A.covered = covered_dev;
   A.counts = counts_dev;
+  return FVV_OK;
+}
+
+int fvv_render_count(const fvv_camera *rig, int ncam, const fvv_camera *virt,
+                     const int32_t *tri_id_dev, const int32_t *tri_src_dev, int64_t *counts_dev,
+                     void *stream) {
+  static thread_local RenderArgs A;
+  int rc = fill_render(A, rig, ncam, nullptr, nullptr, virt, nullptr, tri_id_dev, tri_src_dev,
+                       nullptr, nullptr, nullptr, nullptr, counts_dev);
+  if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   cudaMemsetAsync(counts_dev, 0, sizeof(int64_t) * (1 + ncam), st);
   render_count_kernel<<<kRasterGrid, 256, 0, st>>>(A);
-  render_color_kernel<<<kRasterGrid, 256, 0, st>>>(A);
-  note_launches(2);
+  note_launches(1);
+  return cuda_check("fvv_render_count");
+}
+
+int fvv_render_view(const fvv_camera *rig, int ncam, const uint8_t *frames_dev,
+                    const int64_t *frame_off, const fvv_camera *virt, const double *depth_dev,
+                    const int32_t *tri_id_dev, const int32_t *tri_src_dev, const uint8_t *fallback,
+                    uint8_t *color_dev, int32_t *source_dev, uint8_t *covered_dev,
+                    const int64_t *counts_dev, void *stream) {
+  static thread_local RenderArgs A;
+  int rc = fill_render(A, rig, ncam, frames_dev, frame_off, virt, depth_dev, tri_id_dev,
+                       tri_src_dev, fallback, color_dev, source_dev, covered_dev,
+                       const_cast<int64_t *>(counts_dev));
+  if (rc) return rc;
+  render_color_kernel<<<kRasterGrid, 256, 0, (cudaStream_t)stream>>>(A);
+  note_launches(1);
   return cuda_check("fvv_render_view");
 }
 

@@ -321,6 +321,87 @@ def bundle_from(r: FrameResult, cfg, rig, frames, frame_id=0, keep_depths=False)
     return bundle
 
 
+def _prefetch(rig, frames, sils, virtual, copy_stream, compute_stream, k_frames):
+    """Queue the H2D copies of one frame's inputs on ``copy_stream``."""
+    dev = require_cuda()
+    cams = list(rig)
+    with torch.cuda.stream(copy_stream):
+        if isinstance(sils, torch.Tensor):
+            d_masks = sils.to(dev, non_blocking=True)
+        else:
+            d_masks = torch.stack([torch.from_numpy(np.ascontiguousarray(s, dtype=bool))
+                                   for s in sils]).to(dev, non_blocking=True)
+        d_masks.record_stream(compute_stream)
+        pre = {}
+        if virtual is not None and frames is not None and k_frames > 0:
+            from .render import H2D_BYTES, _frame_tensor, rank_cameras
+
+            pos = {c.id: i for i, c in enumerate(cams)}
+            for cid in rank_cameras(virtual, cams)[:k_frames]:
+                t = _frame_tensor(frames[cid]).to(dev, non_blocking=True)
+                H2D_BYTES["frames"] += t.numel()
+                t.record_stream(compute_stream)
+                pre[pos[cid]] = t
+        ev = torch.cuda.Event()
+        ev.record(copy_stream)
+    return d_masks, pre, ev
+
+
+def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
+                 fallback_color=None, prefetch_frames: int = 4, frame_id0: int = 0):
+    """Reconstruct (and, given ``virtual``, colour) a sequence of frames.
+
+    The production form of run_frame + render_view for video: while frame f
+    computes, frame f+1's silhouettes and the colour frames of the cameras
+    ranked nearest to ``virtual`` are copied host->device on a second stream
+    (the paper overlaps upload and compute with two CPU threads,
+    PAPER.md:561). Inputs should be pinned host tensors for the copies to be
+    asynchronous. Yields (SceneBundle, RenderedImage or None) per frame, with
+    the mesh, visibility flags and rendered image already on the host."""
+    from .render import FALLBACK_COLOR, RenderedImage, render_device
+
+    fallback_color = FALLBACK_COLOR if fallback_color is None else fallback_color
+    require_cuda()
+    cams = list(rig)
+    compute = torch.cuda.current_stream()
+    copy = torch.cuda.Stream()
+    it = iter(zip(frames_seq, sils_seq))
+    try:
+        nxt = next(it)
+    except StopIteration:
+        return
+    staged = _prefetch(cams, nxt[0], nxt[1], virtual, copy, compute, prefetch_frames)
+    fid = frame_id0
+    while nxt is not None:
+        frames, _ = nxt
+        d_masks, pre, ev = staged
+        compute.wait_event(ev)
+        try:
+            nxt = next(it)
+            staged = _prefetch(cams, nxt[0], nxt[1], virtual, copy, compute, prefetch_frames)
+        except StopIteration:
+            nxt = None
+        dsils = DeviceSilhouettes(cams, d_masks)
+        r = reconstruct(cfg, cams, dsils)
+        bundle = bundle_from(r, cfg, rig, frames, fid)
+        merged = bundle.merged_mesh
+        img = None
+        if virtual is not None:
+            h, w = virtual.image_height, virtual.image_width
+            if r.vis_bits is None or merged.num_triangles == 0:
+                img = RenderedImage(np.zeros((h, w, 3), np.uint8), np.full((h, w), -1, np.int32),
+                                    np.zeros((h, w), bool))
+            else:
+                color, source, covered, _ = render_device(
+                    r.batch.verts, r.batch.tris, merged.num_triangles, cams, frames, r.vis_bits,
+                    int(r.vis_bits.shape[1]), virtual, fallback_color, prefetched=pre)
+                img = RenderedImage(color.cpu().numpy(), source.cpu().numpy(),
+                                    covered.cpu().numpy().astype(bool))
+        merged.vertices  # noqa: B018  (materialise the mesh on the host)
+        yield bundle, img
+        fid += 1
+
+
 def sweep(cfg: PipelineConfig, rig, sils, axis: str, values) -> list:
     """run_frame per spacing value on fixed inputs (pipeline.py:223-243)."""
     if axis not in ("coarse_spacing", "fine_spacing"):

@@ -22,6 +22,9 @@ from .visibility import classify_bits, raster_planes  # noqa: F401  (re-exported
 
 FALLBACK_COLOR = np.array([128, 128, 128], dtype=np.uint8)  # render.py:19
 
+# host->device bytes of colour frames moved by the render path (bench.py reads it)
+H2D_BYTES = {"frames": 0}
+
 
 @dataclass
 class RenderedImage:
@@ -109,9 +112,21 @@ def frames_device(rig, frames, dev):
     return buf, off
 
 
-def render_device(verts, tris, nt, rig, frames_buf, frame_off, vis_bits, stride, virtual,
-                  fallback_color=FALLBACK_COLOR, nt_dev=None):
-    """Device-side render_view: returns (color, source, covered) GPU tensors."""
+def _frame_tensor(f):
+    if isinstance(f, torch.Tensor):
+        return f
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(f, dtype=np.uint8)))
+
+
+def render_device(verts, tris, nt, rig, frames, vis_bits, stride, virtual,
+                  fallback_color=FALLBACK_COLOR, nt_dev=None, frame_buf=None, prefetched=None):
+    """Device-side render_view -> (color, source, covered, counts) GPU tensors.
+
+    Colour frames come either as ``frame_buf = (device buffer, offsets)``
+    holding every rig camera, or as the reference's ``frames`` dict of host
+    (H, W, 3) arrays; then only the cameras that actually source a pixel are
+    copied to the GPU (after fvv_render_count), reusing ``prefetched``
+    {rig position: device tensor} when given."""
     dev = verts.device
     rig = list(rig)
     h, w = virtual.image_height, virtual.image_width
@@ -119,17 +134,38 @@ def render_device(verts, tris, nt, rig, frames_buf, frame_off, vis_bits, stride,
                            want_ids=True, nt_dev=nt_dev)
     ranking = rank_cameras(virtual, rig)
     src = sources_device(ranking, rig, vis_bits, stride, max(nt, 1), nt_dev)
+    tab = cam_table(rig)
+    vtab = cam_table([virtual])
+    counts = torch.empty(1 + len(rig), dtype=torch.int64, device=dev)
+    _lib.call("fvv_render_count", _lib.host_ptr(tab), ctypes.c_int(len(rig)),
+              _lib.host_ptr(vtab), _lib.dev_ptr(planes.tri_id), _lib.dev_ptr(src),
+              _lib.dev_ptr(counts), stream_handle())
+    if frame_buf is not None:
+        buf, off = frame_buf
+    else:
+        used = np.flatnonzero(counts[1:].cpu().numpy() > 0)  # sync: which frames are read
+        prefetched = prefetched or {}
+        sizes = [rig[c].image_height * rig[c].image_width * 3 for c in used]
+        off = np.zeros(len(rig), dtype=np.int64)
+        buf = torch.empty(max(int(sum(sizes)), 1), dtype=torch.uint8, device=dev)
+        o = 0
+        for c, sz in zip(used, sizes):
+            off[c] = o
+            t = prefetched.get(int(c))
+            if t is None:
+                t = _frame_tensor(frames[rig[c].id])
+                H2D_BYTES["frames"] += sz
+            buf[o:o + sz].copy_(t.reshape(-1), non_blocking=True)
+            o += sz
     color = torch.empty((h, w, 3), dtype=torch.uint8, device=dev)
     source = torch.empty((h, w), dtype=torch.int32, device=dev)
     covered = torch.empty((h, w), dtype=torch.uint8, device=dev)
-    counts = torch.zeros(1 + len(rig), dtype=torch.int64, device=dev)
     fb = np.ascontiguousarray(np.asarray(fallback_color, dtype=np.uint8).reshape(3))
-    _lib.call("fvv_render_view", _lib.host_ptr(cam_table(rig)), ctypes.c_int(len(rig)),
-              _lib.dev_ptr(frames_buf), _lib.host_ptr(frame_off),
-              _lib.host_ptr(cam_table([virtual])), _lib.dev_ptr(planes.depth),
-              _lib.dev_ptr(planes.tri_id), _lib.dev_ptr(src), _lib.host_ptr(fb),
-              _lib.dev_ptr(color), _lib.dev_ptr(source), _lib.dev_ptr(covered),
-              _lib.dev_ptr(counts), stream_handle())
+    _lib.call("fvv_render_view", _lib.host_ptr(tab), ctypes.c_int(len(rig)),
+              _lib.dev_ptr(buf), _lib.host_ptr(off), _lib.host_ptr(vtab),
+              _lib.dev_ptr(planes.depth), _lib.dev_ptr(planes.tri_id), _lib.dev_ptr(src),
+              _lib.host_ptr(fb), _lib.dev_ptr(color), _lib.dev_ptr(source),
+              _lib.dev_ptr(covered), _lib.dev_ptr(counts), stream_handle())
     return color, source, covered, counts
 
 
@@ -154,8 +190,7 @@ def render_view(mesh, rig, frames: dict, vis: dict, virtual, fallback_color=FALL
         bits, stride = dbits, int(dbits.shape[1])  # run_frame's bits, still on the GPU
     else:
         bits, stride = _vis_bits_from_dict(vis, rig, n, dev)
-    fbuf, foff = frames_device(rig, frames, dev)
-    color, source, covered, counts = render_device(verts, tris, n, rig, fbuf, foff, bits, stride,
+    color, source, covered, counts = render_device(verts, tris, n, rig, frames, bits, stride,
                                                    virtual, fallback_color)
     cov = covered.cpu().numpy().astype(bool)
     if virtual.has_distortion and cov.any():

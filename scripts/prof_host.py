@@ -12,8 +12,9 @@ fb = frames.reshape(-1); foff = np.arange(16, dtype=np.int64) * (1080 * 1920 * 3
 def step():
     d = DeviceSilhouettes(wl.rig, masks)
     r = reconstruct(wl.cfg, wl.rig, d)
-    render_device(r.batch.verts, r.batch.tris, int(r.batch.tris.shape[0]), cams, fb, foff, r.vis_bits,
-                  int(r.vis_bits.shape[1]), wl.virtual, nt_dev=r.batch.num_triangles_dev)
+    render_device(r.batch.verts, r.batch.tris, int(r.batch.tris.shape[0]), cams, None, r.vis_bits,
+                  int(r.vis_bits.shape[1]), wl.virtual, nt_dev=r.batch.num_triangles_dev,
+                  frame_buf=(fb, foff))
 for _ in range(3): step()
 torch.cuda.synchronize()
 t = time.perf_counter()

@@ -180,3 +180,32 @@ def test_run_frame_empty_scene_and_errors(gpu):
     with pytest.raises(StageError) as ei:
         run_frame(cfg, rig, {}, sils=bad)
     assert "B-1" in str(ei.value)
+
+
+def test_run_sequence_matches_golden_frames(gpu):
+    """pipeline.run_sequence (overlapped uploads, pinned inputs, only the
+    needed colour frames copied) returns the same bundles and images as the
+    reference for a sequence mixing the two golden scenes' inputs."""
+    import torch
+
+    from paper_1903_11785_b200.pipeline import PipelineConfig, run_sequence
+
+    z = G.load("figures")
+    rig, sils = G.rig(z), G.sils(z)
+    cfg_d = json.loads(str(z["cfg"]))
+    cfg_d["t_large"] = float("inf")
+    cfg = PipelineConfig(**{k: (tuple(v) if isinstance(v, list) else v) for k, v in cfg_d.items()})
+    frames = {c.id: torch.from_numpy(z["frames"][i]).pin_memory() for i, c in enumerate(rig)}
+    masks = torch.from_numpy(np.stack(sils).astype(np.uint8)).pin_memory()
+    virtual = G.camera(z, "virtual")
+    out = list(run_sequence(cfg, rig, [frames, frames, frames], [masks, masks, sils], virtual))
+    assert len(out) == 3
+    for bundle, img in out:
+        assert bundle.stats == json.loads(str(z["stats"]))
+        assert np.array_equal(bundle.merged_mesh.triangles, z["merged_tris"])
+        assert np.array_equal(bundle.merged_mesh.vertices, z["merged_verts"])
+        for i, c in enumerate(rig):
+            assert np.array_equal(bundle.visibility[c.id],
+                                  G.unpack(z["vis"][i], bundle.merged_mesh.num_triangles))
+        assert np.array_equal(img.color, z["render_color"])
+        assert np.array_equal(img.source, z["render_source"])
