@@ -317,6 +317,20 @@ class MeshBatch:
             return IsovalueStats()
         return IsovalueStats(int(info[_INFO_FB]), int(info[_INFO_INC]))
 
+    def host_arrays(self):
+        """All vertices (V,3) and triangles (T,3) (indices into the batch's
+        vertex array) copied to the host in two transfers, cached."""
+        if getattr(self, "_host_arrays", None) is None:
+            totals, _ = self.host_info()
+            nt = int(totals[2])
+            v = torch.empty(self.verts.shape, dtype=torch.float64, pin_memory=True)
+            t = torch.empty((nt, 3), dtype=torch.int32, pin_memory=True)
+            v.copy_(self.verts, non_blocking=True)
+            t.copy_(self.tris[:nt], non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            self._host_arrays = (v.numpy(), t.numpy())
+        return self._host_arrays
+
     def mesh(self, g) -> TriangleMesh:
         info = self.host_info()[1][g]
         vb, nv, tb, nt = (int(info[k]) for k in (_INFO_VBASE, _INFO_V, _INFO_TBASE, _INFO_T))
@@ -325,9 +339,8 @@ class MeshBatch:
             return TriangleMesh.empty()
 
         def load():
-            v = self.verts[vb:vb + nv].cpu().numpy()
-            t = self.tris[tb:tb + nt].cpu().numpy() - np.int32(vb)
-            return v, t, np.full(nt, oid, dtype=np.int32)
+            v, t = self.host_arrays()
+            return v[vb:vb + nv], t[tb:tb + nt] - np.int32(vb), np.full(nt, oid, dtype=np.int32)
 
         return TriangleMesh._lazy(nt, load)
 
@@ -335,14 +348,20 @@ class MeshBatch:
         return [self.mesh(g) for g in range(len(self.grids))]
 
     def merged(self) -> TriangleMesh:
-        """TriangleMesh.concatenate(meshes) with device arrays attached: the
-        device triangles index the batch's full vertex array (same
-        positions, same triangle order as the concatenation)."""
+        """TriangleMesh.concatenate(meshes) (mesh.py:92-105) with device arrays
+        attached; the device triangles index the batch's full vertex array
+        (same positions, same triangle order as the concatenation)."""
         totals, info = self.host_info()
         nt = int(totals[2])
         meshes = self.meshes()
 
         def load():
+            # grids with vertices but no surviving triangle are dropped by
+            # concatenate; when there are none, the batch arrays ARE the merge
+            if np.all((info[:, _INFO_V] == 0) | (info[:, _INFO_T] > 0)):
+                v, t = self.host_arrays()
+                oids = np.repeat(np.asarray(self.object_ids, dtype=np.int32), info[:, _INFO_T])
+                return v, t, oids
             m = TriangleMesh.concatenate(meshes)
             return m.vertices, m.triangles, m.object_ids
 

@@ -216,7 +216,9 @@ def reconstruct(cfg: PipelineConfig, rig, dsils: DeviceSilhouettes, clock=None) 
 def _finish_stats(r: FrameResult):
     """Read the device-side counts (one sync) into the reference's stats keys."""
     dense_counts = [g._count for g in r.fine]
-    if dense_counts:
+    if getattr(r, "_dense_occ", None) is not None:
+        r.stats["dense_occupied"] = int(r._dense_occ)
+    elif dense_counts:
         occ = torch.stack([c.reshape(()) for c in dense_counts]).cpu().numpy()
         r.stats["dense_occupied"] = int(occ.sum())
     else:
@@ -300,7 +302,9 @@ def bundle_from(r: FrameResult, cfg, rig, frames, frame_id=0, keep_depths=False)
     meshes = r.batch.meshes() if r.batch is not None else []
     nt = r.stats["triangles"]
     if r.vis_bits is not None:
-        vis = _LazyVisibility([c.id for c in cams], r.vis_bits.cpu().numpy(), nt)
+        vbits = r._vis_host if getattr(r, "_vis_host", None) is not None else \
+            r.vis_bits.cpu().numpy()
+        vis = _LazyVisibility([c.id for c in cams], vbits, nt)
         vis._device_bits = r.vis_bits  # render_view reads these directly (rig order)
     else:
         vis = {c.id: np.zeros(0, dtype=bool) for c in cams}
@@ -321,10 +325,13 @@ def bundle_from(r: FrameResult, cfg, rig, frames, frame_id=0, keep_depths=False)
     return bundle
 
 
-def _prefetch(rig, frames, sils, virtual, copy_stream, compute_stream, k_frames):
-    """Queue the H2D copies of one frame's inputs on ``copy_stream``."""
+def _prefetch(rig, frames, sils, want_frames, copy_stream, compute_stream):
+    """Queue the H2D copies of one frame's inputs on ``copy_stream``:
+    silhouette masks and (when rendering) every camera's colour frame into
+    one device buffer."""
     dev = require_cuda()
     cams = list(rig)
+    fbuf = foff = None
     with torch.cuda.stream(copy_stream):
         if isinstance(sils, torch.Tensor):
             d_masks = sils.to(dev, non_blocking=True)
@@ -332,32 +339,69 @@ def _prefetch(rig, frames, sils, virtual, copy_stream, compute_stream, k_frames)
             d_masks = torch.stack([torch.from_numpy(np.ascontiguousarray(s, dtype=bool))
                                    for s in sils]).to(dev, non_blocking=True)
         d_masks.record_stream(compute_stream)
-        pre = {}
-        if virtual is not None and frames is not None and k_frames > 0:
-            from .render import H2D_BYTES, _frame_tensor, rank_cameras
+        if want_frames and frames is not None:
+            from .render import H2D_BYTES, _frame_tensor
 
-            pos = {c.id: i for i, c in enumerate(cams)}
-            for cid in rank_cameras(virtual, cams)[:k_frames]:
-                t = _frame_tensor(frames[cid]).to(dev, non_blocking=True)
-                H2D_BYTES["frames"] += t.numel()
-                t.record_stream(compute_stream)
-                pre[pos[cid]] = t
+            sizes = [c.image_height * c.image_width * 3 for c in cams]
+            foff = np.zeros(len(cams), dtype=np.int64)
+            foff[1:] = np.cumsum(sizes)[:-1]
+            fbuf = torch.empty(int(sum(sizes)), dtype=torch.uint8, device=dev)
+            for c, o, sz in zip(cams, foff, sizes):
+                fbuf[int(o):int(o) + sz].copy_(_frame_tensor(frames[c.id]).reshape(-1),
+                                               non_blocking=True)
+            H2D_BYTES["frames"] += int(sum(sizes))
+            fbuf.record_stream(compute_stream)
         ev = torch.cuda.Event()
         ev.record(copy_stream)
-    return d_masks, pre, ev
+    return d_masks, (fbuf, foff), ev
+
+
+def _readback(r, image):
+    """Copy every host-facing result of a frame back with two syncs: the
+    small counters first (they size the rest), then the mesh, visibility
+    bits and rendered image in one batch of async copies."""
+    small = [torch.zeros(1, dtype=torch.int64, device=r.coarse.device_bits().device)]
+    if r.fine:
+        small.append(torch.stack([g._count.reshape(()) for g in r.fine]))
+    if r.batch is not None:
+        small += [r.batch._totals, r.batch._info.reshape(-1)]
+    host = torch.cat(small).cpu().numpy()
+    nf = len(r.fine)
+    r._dense_occ = int(host[1:1 + nf].sum())
+    if r.batch is None:
+        return None
+    totals = host[1 + nf:4 + nf].copy()
+    info = host[4 + nf:].reshape(len(r.fine), 8).copy()
+    r.batch._host = (totals, info)
+    nt = int(totals[2])
+    pinned = []
+
+    def fetch(t):
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t, non_blocking=True)
+        pinned.append(h)
+        return h
+
+    hv, ht = fetch(r.batch.verts), fetch(r.batch.tris[:nt])
+    hb = fetch(r.vis_bits) if r.vis_bits is not None else None
+    himg = [fetch(x) for x in image] if image is not None else None
+    torch.cuda.current_stream().synchronize()
+    r.batch._host_arrays = (hv.numpy(), ht.numpy())
+    r._vis_host = hb.numpy() if hb is not None else None
+    return [x.numpy() for x in himg] if himg is not None else None
 
 
 def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
-                 fallback_color=None, prefetch_frames: int = 4, frame_id0: int = 0):
+                 fallback_color=None, frame_id0: int = 0):
     """Reconstruct (and, given ``virtual``, colour) a sequence of frames.
 
     The production form of run_frame + render_view for video: while frame f
-    computes, frame f+1's silhouettes and the colour frames of the cameras
-    ranked nearest to ``virtual`` are copied host->device on a second stream
-    (the paper overlaps upload and compute with two CPU threads,
+    computes, frame f+1's silhouettes and colour frames are copied
+    host->device on a second stream (the paper overlaps upload and compute with two CPU threads,
     PAPER.md:561). Inputs should be pinned host tensors for the copies to be
-    asynchronous. Yields (SceneBundle, RenderedImage or None) per frame, with
-    the mesh, visibility flags and rendered image already on the host."""
+    asynchronous. Results come back in two transfers per frame. Yields
+    (SceneBundle, RenderedImage or None) per frame, with the mesh, visibility
+    flags and rendered image already on the host."""
     from .render import FALLBACK_COLOR, RenderedImage, render_device
 
     fallback_color = FALLBACK_COLOR if fallback_color is None else fallback_color
@@ -370,34 +414,37 @@ def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
         nxt = next(it)
     except StopIteration:
         return
-    staged = _prefetch(cams, nxt[0], nxt[1], virtual, copy, compute, prefetch_frames)
+    staged = _prefetch(cams, nxt[0], nxt[1], virtual is not None, copy, compute)
     fid = frame_id0
     while nxt is not None:
         frames, _ = nxt
-        d_masks, pre, ev = staged
+        d_masks, frame_buf, ev = staged
         compute.wait_event(ev)
         try:
             nxt = next(it)
-            staged = _prefetch(cams, nxt[0], nxt[1], virtual, copy, compute, prefetch_frames)
+            staged = _prefetch(cams, nxt[0], nxt[1], virtual is not None, copy, compute)
         except StopIteration:
             nxt = None
         dsils = DeviceSilhouettes(cams, d_masks)
         r = reconstruct(cfg, cams, dsils)
+        image = None
+        if virtual is not None and r.batch is not None and r.vis_bits is not None:
+            color, source, covered, _ = render_device(
+                r.batch.verts, r.batch.tris, int(r.batch.tris.shape[0]), cams, frames,
+                r.vis_bits, int(r.vis_bits.shape[1]), virtual, fallback_color,
+                nt_dev=r.batch.num_triangles_dev, frame_buf=frame_buf)
+            image = (color, source, covered)
+        himg = _readback(r, image)
         bundle = bundle_from(r, cfg, rig, frames, fid)
-        merged = bundle.merged_mesh
         img = None
         if virtual is not None:
             h, w = virtual.image_height, virtual.image_width
-            if r.vis_bits is None or merged.num_triangles == 0:
+            if himg is None or bundle.stats["triangles"] == 0:
                 img = RenderedImage(np.zeros((h, w, 3), np.uint8), np.full((h, w), -1, np.int32),
                                     np.zeros((h, w), bool))
             else:
-                color, source, covered, _ = render_device(
-                    r.batch.verts, r.batch.tris, merged.num_triangles, cams, frames, r.vis_bits,
-                    int(r.vis_bits.shape[1]), virtual, fallback_color, prefetched=pre)
-                img = RenderedImage(color.cpu().numpy(), source.cpu().numpy(),
-                                    covered.cpu().numpy().astype(bool))
-        merged.vertices  # noqa: B018  (materialise the mesh on the host)
+                img = RenderedImage(himg[0], himg[1], himg[2].astype(bool))
+        bundle.merged_mesh.vertices  # noqa: B018  (host arrays are already cached)
         yield bundle, img
         fid += 1
 
