@@ -74,25 +74,15 @@ def barrier(world):
 
 
 def max_over_ranks(x, world):
-    if world == 1:
-        return x
-    import torch
-    import torch.distributed as dist
+    from paper_1903_11785_b200.sharding import reduce_max
 
-    t = torch.tensor([float(x)], device="cuda" if torch.cuda.is_available() else "cpu")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    return reduce_max(x) if world > 1 else x
 
 
 def sum_over_ranks(x, world):
-    if world == 1:
-        return x
-    import torch
-    import torch.distributed as dist
+    from paper_1903_11785_b200.sharding import reduce_sum
 
-    t = torch.tensor([float(x)], device="cuda" if torch.cuda.is_available() else "cpu")
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    return float(t.item())
+    return reduce_sum(x) if world > 1 else x
 
 
 class ClockSampler:
@@ -203,7 +193,9 @@ def run_b200(args):
     rig, cfg, virt = wl.rig, wl.cfg, wl.virtual
     cams = list(rig)
     ncam = len(cams)
-    frame_ids = [rank + world * i for i in range(args.frames)]
+    from paper_1903_11785_b200.sharding import frames_for_rank
+
+    frame_ids = frames_for_rank(rank, world, world * args.frames)  # frame f -> rank f mod N
     inputs = make_inputs(wl, frame_ids)
     torch.cuda.synchronize()
 
