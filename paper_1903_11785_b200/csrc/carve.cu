@@ -19,6 +19,14 @@ namespace fvv {
 constexpr int kCarveThreads = 256;
 constexpr int kCarveWordsPerBlock = 32;  // 1024 voxels per block
 
+// FP32 image of a camera for the certified fast path (see project_fast).
+struct Cam32 {
+  float R[9], t[3];
+  float fx, fy, cx, cy, skew, askew;
+  float eX, eY, eZ;  // bounds on |X32 - X64| etc. over the batch's voxel centres
+  int fast;          // 0 when the camera has distortion: always the exact path
+};
+
 struct CarveParams {
   int ncam, ngrid, min_views, pad;
   const uint32_t *sil;
@@ -30,7 +38,48 @@ struct CarveParams {
   fvv_grid grids[FVV_MAX_GRIDS];
   int64_t word_off[FVV_MAX_GRIDS];
   int64_t blk_start[FVV_MAX_GRIDS + 1];
+  Cam32 c32[FVV_MAX_CAMS];
 };
+
+constexpr float kU32 = 5.9604645e-8f;  // 2^-24
+
+// Certified FP32 filter for one (voxel, camera) test. Returns 0 when the
+// voxel is certainly outside the camera's frustum, 1 when it is certainly
+// inside with rounded pixel (iu, iv), and 2 when the float64 reference chain
+// must decide (u or v within the error bound of a half-integer, z near 0).
+// The bound: the float32 camera coordinates differ from the float64 ones by
+// at most eX/eY/eZ (6 roundings of |R||p| + |t|, host-computed with margin);
+// division, scaling and the rounding of fx, cx add <= 7 u32 relative; the
+// result is doubled. rint(u) is decided iff u stays farther than the bound
+// from every half-integer, which also settles the image-bound tests (the
+// bounds -0.5 and W-0.5 are half-integers).
+__device__ __forceinline__ int project_fast(const Cam32 &c, float x, float y, float z, int W,
+                                            int H, int &iu, int &iv) {
+  const float X = fmaf(z, c.R[2], fmaf(y, c.R[1], x * c.R[0])) + c.t[0];
+  const float Y = fmaf(z, c.R[5], fmaf(y, c.R[4], x * c.R[3])) + c.t[1];
+  const float Z = fmaf(z, c.R[8], fmaf(y, c.R[7], x * c.R[6])) + c.t[2];
+  if (Z < -c.eZ) return 0;  // z64 < 0: never in frustum
+  if (!(Z > 4.0f * c.eZ + 1e-3f)) return 2;
+  const float inv = __frcp_rn(Z);
+  const float xn = X * inv, yn = Y * inv;
+  const float u = fmaf(c.fx, fmaf(c.skew, yn, xn), c.cx);
+  const float v = fmaf(c.fy, yn, c.cy);
+  const float axn = fabsf(xn), ayn = fabsf(yn);
+  const float exn = (c.eX + axn * c.eZ) * inv + 3.0f * kU32 * axn;
+  const float eyn = (c.eY + ayn * c.eZ) * inv + 3.0f * kU32 * ayn;
+  const float eu = 2.0f * (c.fx * (exn + c.askew * eyn) +
+                           7.0f * kU32 * (c.fx * (axn + c.askew * ayn) + fabsf(u) + fabsf(c.cx))) +
+                   1e-6f;
+  const float ev = 2.0f * (c.fy * eyn + 7.0f * kU32 * (c.fy * ayn + fabsf(v) + fabsf(c.cy))) +
+                   1e-6f;
+  if (!(fabsf(u) < 4.0e6f && fabsf(v) < 4.0e6f)) return 2;
+  const float ru = (u + 12582912.0f) - 12582912.0f;  // round half to even (1.5 * 2^23)
+  const float rv = (v + 12582912.0f) - 12582912.0f;
+  if (fabsf(u - ru) > 0.5f - eu || fabsf(v - rv) > 0.5f - ev) return 2;
+  iu = (int)ru;
+  iv = (int)rv;
+  return (iu >= 0 && iu <= W - 1 && iv >= 0 && iv <= H - 1) ? 1 : 0;
+}
 
 __global__ void __launch_bounds__(kCarveThreads)
     carve_kernel(const __grid_constant__ CarveParams p) {
@@ -57,14 +106,24 @@ __global__ void __launch_bounds__(kCarveThreads)
       double x, y, z;
       voxel_center(G, i, j, k, x, y, z);
       const bool gemv = (l == gemv_voxel);
+      const float xf = (float)x, yf = (float)y, zf = (float)z;
       int seen = 0;
       bool keep = true;
       for (int c = 0; c < p.ncam; ++c) {
         const fvv_camera &cam = p.cams[c];
-        double u, v, zc;
-        if (!project_exact(cam, x, y, z, true, gemv, u, v, zc)) continue;
+        int iu = 0, iv = 0;
+        int r = 2;
+        if (p.c32[c].fast && !gemv) r = project_fast(p.c32[c], xf, yf, zf, cam.width, cam.height,
+                                                     iu, iv);
+        if (r == 0) continue;
+        if (r == 2) {  // the reference's float64 chain decides
+          double u, v, zc;
+          if (!project_exact(cam, x, y, z, true, gemv, u, v, zc)) continue;
+          iu = (int)rint(u);
+          iv = (int)rint(v);
+        }
         ++seen;
-        if (!sil_bit(p.sil + p.sil_off[c], p.sil_stride[c], (int)rint(u), (int)rint(v))) {
+        if (!sil_bit(p.sil + p.sil_off[c], p.sil_stride[c], iu, iv)) {
           keep = false;
           break;
         }
@@ -132,6 +191,39 @@ extern "C" int fvv_carve(const fvv_camera *cams, int ncam, const uint32_t *sil_d
     p.blk_start[g + 1] = p.blk_start[g] + (words + kCarveWordsPerBlock - 1) / kCarveWordsPerBlock;
   }
   for (int g = ngrid; g < FVV_MAX_GRIDS; ++g) p.blk_start[g + 1] = p.blk_start[ngrid];
+  // FP32 filter constants: P_j bounds |voxel centre coordinate j| over the batch
+  double P[3] = {0, 0, 0};
+  for (int g = 0; g < ngrid; ++g)
+    for (int j = 0; j < 3; ++j) {
+      const double a = fabs(grids[g].origin[j]);
+      const double b = fabs(grids[g].origin[j] + grids[g].spacing * (double)grids[g].dims[j]);
+      P[j] = fmax(P[j], fmax(a, b));
+    }
+  for (int c = 0; c < ncam; ++c) {
+    const fvv_camera &k = cams[c];
+    Cam32 &f = p.c32[c];
+    for (int q = 0; q < 9; ++q) f.R[q] = (float)k.R[q];
+    for (int q = 0; q < 3; ++q) f.t[q] = (float)k.t[q];
+    f.fx = (float)k.fx;
+    f.fy = (float)k.fy;
+    f.cx = (float)k.cx;
+    f.cy = (float)k.cy;
+    f.skew = (float)k.skew;
+    f.askew = fabsf((float)k.skew);
+    float e[3];
+    for (int r = 0; r < 3; ++r) {
+      const double S = fabs(k.R[3 * r]) * P[0] + fabs(k.R[3 * r + 1]) * P[1] +
+                       fabs(k.R[3 * r + 2]) * P[2] + fabs(k.t[r]);
+      e[r] = (float)(8.0 * 5.9604645e-8 * S);
+    }
+    f.eX = e[0];
+    f.eY = e[1];
+    f.eZ = e[2];
+    // exact path for distorted cameras and for parameters float32 cannot hold
+    f.fast = !k.has_distortion && k.fx > 0 && k.fy > 0 && k.fx < 1e7 && k.fy < 1e7 &&
+             fabs(k.cx) < 1e6 && fabs(k.cy) < 1e6 && fabs(k.skew) < 1e3 &&
+             (P[0] + P[1] + P[2]) < 1e7 && k.width < (1 << 22) && k.height < (1 << 22);
+  }
   int64_t blocks = p.blk_start[ngrid];
   if (blocks > 0x7fffffff) {
     set_error("fvv_carve: %lld blocks", (long long)blocks);

@@ -174,3 +174,28 @@ def test_coarse_labels_of_full_frames(gpu):
         lab = label_components(grid)
         assert np.array_equal(_comp_rows(lab.components), z["comps"])
         assert np.array_equal(lab.labels, z["labels"])
+
+
+def test_carve_fp32_filter_on_exact_half_pixels(gpu):
+    """Voxel centres that project exactly onto pixel boundaries (u, v =
+    k + 0.5) and onto the image borders: the certified float32 filter must
+    hand every such test to the float64 chain (round-half-to-even)."""
+    from paper_1903_11785_b200.camera import CameraModel, CameraRig
+    from paper_1903_11785_b200.hull import carve
+    from paper_1903_11785_b200.voxels import GridSpec
+
+    rng = np.random.default_rng(3)
+    cams = [CameraModel(id=0, image_width=200, image_height=100, fx=100.0, fy=100.0, cx=99.5,
+                        cy=49.5),
+            CameraModel(id=1, image_width=201, image_height=101, fx=50.0, fy=50.0, cx=100.0,
+                        cy=50.0, skew=0.25)]
+    rig = CameraRig(cams)
+    sils = [rng.random((c.image_height, c.image_width)) < 0.5 for c in cams]
+    for origin, spacing, dims in [((-1205.0, -605.0, 995.0), 10.0, (241, 121, 3)),
+                                  ((-2010.0, -1010.0, 1990.0), 20.0, (202, 102, 2)),
+                                  ((-40.0, -40.0, 2.0), 0.5, (160, 160, 4))]:
+        spec = GridSpec(origin=origin, spacing=spacing, dims=dims)
+        got = carve(rig, sils, spec).occ
+        ref = O.carve(rig, sils, spec.origin, spec.spacing, spec.dims)
+        assert np.array_equal(got, ref), origin
+        assert got.any() and not got.all()
