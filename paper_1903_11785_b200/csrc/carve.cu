@@ -109,24 +109,36 @@ __global__ void __launch_bounds__(kCarveThreads)
       const float xf = (float)x, yf = (float)y, zf = (float)z;
       int seen = 0;
       bool keep = true;
+      // pass 1: certified float32 tests; undecided cameras are deferred so a
+      // rare float64 fallback does not serialise the whole warp every camera
+      unsigned long long pending = 0ull;
       for (int c = 0; c < p.ncam; ++c) {
-        const fvv_camera &cam = p.cams[c];
         int iu = 0, iv = 0;
-        int r = 2;
-        if (p.c32[c].fast && !gemv) r = project_fast(p.c32[c], xf, yf, zf, cam.width, cam.height,
-                                                     iu, iv);
+        const int r = (p.c32[c].fast && !gemv)
+                          ? project_fast(p.c32[c], xf, yf, zf, p.cams[c].width,
+                                         p.cams[c].height, iu, iv)
+                          : 2;
         if (r == 0) continue;
-        if (r == 2) {  // the reference's float64 chain decides
-          double u, v, zc;
-          if (!project_exact(cam, x, y, z, true, gemv, u, v, zc)) continue;
-          iu = (int)rint(u);
-          iv = (int)rint(v);
+        if (r == 2) {
+          pending |= 1ull << c;
+          continue;
         }
         ++seen;
         if (!sil_bit(p.sil + p.sil_off[c], p.sil_stride[c], iu, iv)) {
           keep = false;
           break;
         }
+      }
+      // pass 2: the reference's float64 chain for the deferred cameras (only
+      // voxels still ON need them: one background camera already decides)
+      while (keep && pending) {
+        const int c = __ffsll((long long)pending) - 1;
+        pending &= pending - 1;
+        double u, v, zc;
+        if (!project_exact(p.cams[c], x, y, z, true, gemv, u, v, zc)) continue;
+        ++seen;
+        if (!sil_bit(p.sil + p.sil_off[c], p.sil_stride[c], (int)rint(u), (int)rint(v)))
+          keep = false;
       }
       on = keep && seen >= p.min_views;
     }
