@@ -81,6 +81,79 @@ __device__ __forceinline__ int project_fast(const Cam32 &c, float x, float y, fl
   return (iu >= 0 && iu <= W - 1 && iv >= 0 && iv <= H - 1) ? 1 : 0;
 }
 
+enum { kSegMixed = 0, kSegFg = 1, kSegBg = 2, kSegOut = 3 };
+
+// Certified float32 projection of a point, with its error bounds (see
+// project_fast). False when z is not certainly > 0.
+__device__ __forceinline__ bool project_bounds(const Cam32 &c, float x, float y, float z,
+                                               float &u, float &v, float &eu, float &ev,
+                                               bool &behind) {
+  const float X = fmaf(z, c.R[2], fmaf(y, c.R[1], x * c.R[0])) + c.t[0];
+  const float Y = fmaf(z, c.R[5], fmaf(y, c.R[4], x * c.R[3])) + c.t[1];
+  const float Z = fmaf(z, c.R[8], fmaf(y, c.R[7], x * c.R[6])) + c.t[2];
+  behind = Z < -c.eZ;
+  if (!(Z > 4.0f * c.eZ + 1e-3f)) return false;
+  const float inv = __frcp_rn(Z);
+  const float xn = X * inv, yn = Y * inv;
+  u = fmaf(c.fx, fmaf(c.skew, yn, xn), c.cx);
+  v = fmaf(c.fy, yn, c.cy);
+  const float axn = fabsf(xn), ayn = fabsf(yn);
+  const float exn = (c.eX + axn * c.eZ) * inv + 3.0f * kU32 * axn;
+  const float eyn = (c.eY + ayn * c.eZ) * inv + 3.0f * kU32 * ayn;
+  eu = 2.0f * (c.fx * (exn + c.askew * eyn) +
+               7.0f * kU32 * (c.fx * (axn + c.askew * ayn) + fabsf(u) + fabsf(c.cx))) +
+       1e-5f;
+  ev = 2.0f * (c.fy * eyn + 7.0f * kU32 * (c.fy * ayn + fabsf(v) + fabsf(c.cy))) + 1e-5f;
+  return fabsf(u) < 4.0e6f && fabsf(v) < 4.0e6f;
+}
+
+// Status of one camera for a run of voxels along i (same j, k) whose first
+// and last centres are a and b. The projection of a segment in front of the
+// camera is the segment between the projected endpoints (u, v are monotone
+// along it), so every voxel's rounded pixel lies in the bounding rectangle
+// of the two projections widened by their error bounds:
+//   kSegFg  : rectangle inside the image and all foreground -> every voxel
+//             is seen by this camera and passes it;
+//   kSegBg  : rectangle inside the image and all background -> every voxel
+//             is seen and fails (the whole run is OFF);
+//   kSegOut : run entirely behind the camera or entirely off one image side
+//             -> no voxel is seen by this camera;
+//   kSegMixed: anything else -> per-voxel tests.
+__device__ __forceinline__ int segment_status(const Cam32 &c, int W, int H,
+                                              const uint32_t *__restrict__ plane, int stride,
+                                              const float *a, const float *b) {
+  if (!c.fast) return kSegMixed;
+  float ua, va, eua, eva, ub, vb, eub, evb;
+  bool behind_a, behind_b;
+  const bool ok_a = project_bounds(c, a[0], a[1], a[2], ua, va, eua, eva, behind_a);
+  const bool ok_b = project_bounds(c, b[0], b[1], b[2], ub, vb, eub, evb, behind_b);
+  if (behind_a && behind_b) return kSegOut;  // z affine along the run: all behind
+  if (!(ok_a && ok_b)) return kSegMixed;
+  const float eu = fmaxf(eua, eub), ev = fmaxf(eva, evb);
+  const float fx0 = floorf(fminf(ua, ub) - eu), fx1 = ceilf(fmaxf(ua, ub) + eu);
+  const float fy0 = floorf(fminf(va, vb) - ev), fy1 = ceilf(fmaxf(va, vb) + ev);
+  if (fx1 < 0.0f || fy1 < 0.0f || fx0 > (float)(W - 1) || fy0 > (float)(H - 1)) return kSegOut;
+  if (fx0 < 0.0f || fy0 < 0.0f || fx1 > (float)(W - 1) || fy1 > (float)(H - 1)) return kSegMixed;
+  const int x0 = (int)fx0, x1 = (int)fx1, y0 = (int)fy0, y1 = (int)fy1;
+  if ((int64_t)(x1 - x0 + 1) * (y1 - y0 + 1) > 4096) return kSegMixed;
+  bool any_fg = false, any_bg = false;
+  const int w0 = x0 >> 5, w1 = x1 >> 5;
+  for (int y = y0; y <= y1 && !(any_fg && any_bg); ++y) {
+    const uint32_t *row = plane + (int64_t)y * stride;
+    for (int w = w0; w <= w1; ++w) {
+      uint32_t m = 0xffffffffu;
+      if (w == w0) m &= 0xffffffffu << (x0 & 31);
+      if (w == w1) m &= 0xffffffffu >> (31 - (x1 & 31));
+      const uint32_t bits = __ldg(row + w);
+      any_fg |= (bits & m) != 0u;
+      any_bg |= (~bits & m) != 0u;
+    }
+  }
+  if (!any_bg) return kSegFg;
+  if (!any_fg) return kSegBg;
+  return kSegMixed;
+}
+
 __global__ void __launch_bounds__(kCarveThreads)
     carve_kernel(const __grid_constant__ CarveParams p) {
   __shared__ int block_on;
@@ -101,18 +174,57 @@ __global__ void __launch_bounds__(kCarveThreads)
     const int64_t word = word0 + it * (kCarveThreads / 32) + warp;
     const int64_t l = word * 32 + lane;
     bool on = false;
+    // ---- warp-level camera classification of this word's voxel runs ----
+    // the 32 voxels of a word form <= 2 runs along i (nx >= 32); lane L
+    // classifies camera L & 15 for run L >> 4
+    uint32_t seg_fg = 0u, seg_bg = 0u, seg_out = 0u;  // bit (16*run + cam)
+    const int64_t lw = word * 32;
+    const bool seg_ok = nx >= 32 && p.ncam <= 16 && lw < nvox &&
+                        !(gemv_voxel >= lw && gemv_voxel < lw + 32);
+    if (seg_ok) {
+      const int64_t key0 = lw / nx;
+      const int64_t llast = (lw + 31 < nvox ? lw + 31 : nvox - 1);
+      const int run = lane >> 4, cam = lane & 15;
+      int st = kSegMixed;
+      const int64_t rkey = key0 + run;
+      if (cam < p.ncam && rkey <= llast / nx) {
+        // run endpoints: linear range [max(lw, rkey*nx), min(llast, rkey*nx + nx - 1)]
+        const int64_t la = lw > rkey * nx ? lw : rkey * nx;
+        const int64_t lb = llast < rkey * nx + nx - 1 ? llast : rkey * nx + nx - 1;
+        const int64_t jj = rkey % ny, kk = rkey / ny;
+        double ax, ay, az, bx, by, bz;
+        voxel_center(G, la - rkey * nx, jj, kk, ax, ay, az);
+        voxel_center(G, lb - rkey * nx, jj, kk, bx, by, bz);
+        const float a[3] = {(float)ax, (float)ay, (float)az};
+        const float bb[3] = {(float)bx, (float)by, (float)bz};
+        st = segment_status(p.c32[cam], p.cams[cam].width, p.cams[cam].height,
+                            p.sil + p.sil_off[cam], p.sil_stride[cam], a, bb);
+      }
+      seg_fg = __ballot_sync(0xffffffffu, st == kSegFg);
+      seg_bg = __ballot_sync(0xffffffffu, st == kSegBg);
+      seg_out = __ballot_sync(0xffffffffu, st == kSegOut);
+    }
     if (l < nvox) {
       const int64_t i = l % nx, j = (l / nx) % ny, k = l / (nx * ny);
+      uint32_t my_fg = 0u, my_bg = 0u, my_done = 0u;
+      if (seg_ok) {
+        const int run = (int)(l / nx - lw / nx);
+        my_fg = (seg_fg >> (16 * run)) & 0xffffu;
+        my_bg = (seg_bg >> (16 * run)) & 0xffffu;
+        my_done = my_fg | my_bg | ((seg_out >> (16 * run)) & 0xffffu);
+      }
       double x, y, z;
       voxel_center(G, i, j, k, x, y, z);
       const bool gemv = (l == gemv_voxel);
       const float xf = (float)x, yf = (float)y, zf = (float)z;
-      int seen = 0;
-      bool keep = true;
-      // pass 1: certified float32 tests; undecided cameras are deferred so a
-      // rare float64 fallback does not serialise the whole warp every camera
+      int seen = __popc(my_fg | my_bg);
+      bool keep = my_bg == 0u;
+      // pass 1: certified float32 tests for the cameras the run left undecided;
+      // undecided voxels are deferred so a rare float64 fallback does not
+      // serialise the whole warp every camera
       unsigned long long pending = 0ull;
-      for (int c = 0; c < p.ncam; ++c) {
+      for (int c = 0; c < p.ncam && keep; ++c) {
+        if (c < 32 && ((my_done >> c) & 1u)) continue;
         int iu = 0, iv = 0;
         const int r = (p.c32[c].fast && !gemv)
                           ? project_fast(p.c32[c], xf, yf, zf, p.cams[c].width,
