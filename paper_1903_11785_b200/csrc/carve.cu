@@ -135,7 +135,7 @@ __device__ __forceinline__ int segment_status(const Cam32 &c, int W, int H,
   if (fx1 < 0.0f || fy1 < 0.0f || fx0 > (float)(W - 1) || fy0 > (float)(H - 1)) return kSegOut;
   if (fx0 < 0.0f || fy0 < 0.0f || fx1 > (float)(W - 1) || fy1 > (float)(H - 1)) return kSegMixed;
   const int x0 = (int)fx0, x1 = (int)fx1, y0 = (int)fy0, y1 = (int)fy1;
-  if ((int64_t)(x1 - x0 + 1) * (y1 - y0 + 1) > 4096) return kSegMixed;
+  if ((x1 - x0 + 1) * (y1 - y0 + 1) > 192 || y1 - y0 > 15) return kSegMixed;
   bool any_fg = false, any_bg = false;
   const int w0 = x0 >> 5, w1 = x1 >> 5;
   for (int y = y0; y <= y1 && !(any_fg && any_bg); ++y) {
@@ -175,43 +175,44 @@ __global__ void __launch_bounds__(kCarveThreads)
     const int64_t l = word * 32 + lane;
     bool on = false;
     // ---- warp-level camera classification of this word's voxel runs ----
-    // the 32 voxels of a word form <= 2 runs along i (nx >= 32); lane L
-    // classifies camera L & 15 for run L >> 4
-    uint32_t seg_fg = 0u, seg_bg = 0u, seg_out = 0u;  // bit (16*run + cam)
+    // lanes 8q..8q+7 (run q) are consecutive voxels along i; a run that
+    // crosses a row end is left unclassified. Task t = 16*q + cam (64 tasks,
+    // two per lane) classifies one camera for one run.
+    unsigned long long seg_fg = 0ull, seg_bg = 0ull, seg_out = 0ull;
     const int64_t lw = word * 32;
-    const bool seg_ok = nx >= 32 && p.ncam <= 16 && lw < nvox &&
-                        !(gemv_voxel >= lw && gemv_voxel < lw + 32);
+    const bool seg_ok = p.ncam <= 16 && lw < nvox && !(gemv_voxel >= lw && gemv_voxel < lw + 32);
     if (seg_ok) {
-      const int64_t key0 = lw / nx;
-      const int64_t llast = (lw + 31 < nvox ? lw + 31 : nvox - 1);
-      const int run = lane >> 4, cam = lane & 15;
-      int st = kSegMixed;
-      const int64_t rkey = key0 + run;
-      if (cam < p.ncam && rkey <= llast / nx) {
-        // run endpoints: linear range [max(lw, rkey*nx), min(llast, rkey*nx + nx - 1)]
-        const int64_t la = lw > rkey * nx ? lw : rkey * nx;
-        const int64_t lb = llast < rkey * nx + nx - 1 ? llast : rkey * nx + nx - 1;
-        const int64_t jj = rkey % ny, kk = rkey / ny;
-        double ax, ay, az, bx, by, bz;
-        voxel_center(G, la - rkey * nx, jj, kk, ax, ay, az);
-        voxel_center(G, lb - rkey * nx, jj, kk, bx, by, bz);
-        const float a[3] = {(float)ax, (float)ay, (float)az};
-        const float bb[3] = {(float)bx, (float)by, (float)bz};
-        st = segment_status(p.c32[cam], p.cams[cam].width, p.cams[cam].height,
-                            p.sil + p.sil_off[cam], p.sil_stride[cam], a, bb);
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int task = lane + 32 * half;
+        const int q = task >> 4, cam = task & 15;
+        const int64_t la = lw + 8 * q;
+        int64_t lb = la + 7;
+        if (lb >= nvox) lb = nvox - 1;
+        int st = kSegMixed;
+        if (cam < p.ncam && la < nvox && la / nx == lb / nx) {
+          const int64_t key = la / nx, jj = key % ny, kk = key / ny;
+          double ax, ay, az, bx, by, bz;
+          voxel_center(G, la - key * nx, jj, kk, ax, ay, az);
+          voxel_center(G, lb - key * nx, jj, kk, bx, by, bz);
+          const float a[3] = {(float)ax, (float)ay, (float)az};
+          const float bb[3] = {(float)bx, (float)by, (float)bz};
+          st = segment_status(p.c32[cam], p.cams[cam].width, p.cams[cam].height,
+                              p.sil + p.sil_off[cam], p.sil_stride[cam], a, bb);
+        }
+        seg_fg |= (unsigned long long)__ballot_sync(0xffffffffu, st == kSegFg) << (32 * half);
+        seg_bg |= (unsigned long long)__ballot_sync(0xffffffffu, st == kSegBg) << (32 * half);
+        seg_out |= (unsigned long long)__ballot_sync(0xffffffffu, st == kSegOut) << (32 * half);
       }
-      seg_fg = __ballot_sync(0xffffffffu, st == kSegFg);
-      seg_bg = __ballot_sync(0xffffffffu, st == kSegBg);
-      seg_out = __ballot_sync(0xffffffffu, st == kSegOut);
     }
     if (l < nvox) {
       const int64_t i = l % nx, j = (l / nx) % ny, k = l / (nx * ny);
       uint32_t my_fg = 0u, my_bg = 0u, my_done = 0u;
       if (seg_ok) {
-        const int run = (int)(l / nx - lw / nx);
-        my_fg = (seg_fg >> (16 * run)) & 0xffffu;
-        my_bg = (seg_bg >> (16 * run)) & 0xffffu;
-        my_done = my_fg | my_bg | ((seg_out >> (16 * run)) & 0xffffu);
+        const int sh = 16 * (lane >> 3);
+        my_fg = (uint32_t)(seg_fg >> sh) & 0xffffu;
+        my_bg = (uint32_t)(seg_bg >> sh) & 0xffffu;
+        my_done = my_fg | my_bg | ((uint32_t)(seg_out >> sh) & 0xffffu);
       }
       double x, y, z;
       voxel_center(G, i, j, k, x, y, z);
