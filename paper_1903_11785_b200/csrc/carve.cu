@@ -27,6 +27,15 @@ struct Cam32 {
   int fast;          // 0 when the camera has distortion: always the exact path
 };
 
+// per-camera constants staged in shared memory (lanes index different
+// cameras in the run classification; divergent parameter-space loads would
+// serialise)
+struct CamShared {
+  Cam32 f;
+  int W, H, stride, pad;
+  int64_t sil_off;
+};
+
 struct CarveParams {
   int ncam, ngrid, min_views, pad;
   const uint32_t *sil;
@@ -157,7 +166,16 @@ __device__ __forceinline__ int segment_status(const Cam32 &c, int W, int H,
 __global__ void __launch_bounds__(kCarveThreads)
     carve_kernel(const __grid_constant__ CarveParams p) {
   __shared__ int block_on;
+  __shared__ CamShared cs[16];
   const int64_t b = blockIdx.x;
+  if (threadIdx.x < 16 && threadIdx.x < p.ncam) {
+    const int c = threadIdx.x;
+    cs[c].f = p.c32[c];
+    cs[c].W = p.cams[c].width;
+    cs[c].H = p.cams[c].height;
+    cs[c].stride = p.sil_stride[c];
+    cs[c].sil_off = p.sil_off[c];
+  }
   int g = 0;
   while (b >= p.blk_start[g + 1]) ++g;  // uniform across the block
   const fvv_grid &G = p.grids[g];
@@ -197,8 +215,8 @@ __global__ void __launch_bounds__(kCarveThreads)
           voxel_center(G, lb - key * nx, jj, kk, bx, by, bz);
           const float a[3] = {(float)ax, (float)ay, (float)az};
           const float bb[3] = {(float)bx, (float)by, (float)bz};
-          st = segment_status(p.c32[cam], p.cams[cam].width, p.cams[cam].height,
-                              p.sil + p.sil_off[cam], p.sil_stride[cam], a, bb);
+          const CamShared &k = cs[cam];
+          st = segment_status(k.f, k.W, k.H, p.sil + k.sil_off, k.stride, a, bb);
         }
         seg_fg |= (unsigned long long)__ballot_sync(0xffffffffu, st == kSegFg) << (32 * half);
         seg_bg |= (unsigned long long)__ballot_sync(0xffffffffu, st == kSegBg) << (32 * half);
