@@ -132,40 +132,106 @@ struct RasterArgs {
   int pass;
 };
 
-__global__ void __launch_bounds__(kRasterThreads, 6)
+// Triangle setup as kept in shared memory for the warp's pixel sweep.
+struct TriSmem {
+  double x0, y0, x1, y1, x2, y2, za, zb, zc, area;
+  int t, cam, lox, loy, bw, tl;  // tl: top-left flags bits 0..2
+};
+
+__device__ __forceinline__ void setup_to_smem(const TriSetup &s, int64_t t, int cam, TriSmem &m) {
+  m.x0 = s.x0; m.y0 = s.y0; m.x1 = s.x1; m.y1 = s.y1; m.x2 = s.x2; m.y2 = s.y2;
+  m.za = s.za; m.zb = s.zb; m.zc = s.zc; m.area = s.area;
+  m.t = (int)t;
+  m.cam = cam;
+  m.lox = s.lox;
+  m.loy = s.loy;
+  m.bw = s.hix - s.lox + 1;
+  m.tl = (int)s.tl0 | ((int)s.tl1 << 1) | ((int)s.tl2 << 2);
+}
+
+__device__ __forceinline__ void smem_to_setup(const TriSmem &m, TriSetup &s) {
+  s.x0 = m.x0; s.y0 = m.y0; s.x1 = m.x1; s.y1 = m.y1; s.x2 = m.x2; s.y2 = m.y2;
+  s.za = m.za; s.zb = m.zb; s.zc = m.zc; s.area = m.area;
+  s.tl0 = m.tl & 1; s.tl1 = (m.tl >> 1) & 1; s.tl2 = (m.tl >> 2) & 1;
+}
+
+// Warp-cooperative small-triangle raster: the 32 lanes set up 32 (camera,
+// triangle) items, publish them in shared memory, then sweep the union of
+// their bounding-box pixels 32 at a time (each lane finds its pixel's owner
+// by a shuffle binary search over the warp's inclusive pixel-count scan), so
+// uneven bounding boxes and culled triangles do not leave lanes idle.
+__global__ void __launch_bounds__(kRasterThreads)
     raster_small_kernel(const __grid_constant__ RasterCams C, RasterArgs A) {
+  __shared__ TriSmem sm[kRasterThreads];
+  const int lane = threadIdx.x & 31;
+  TriSmem *wsm = sm + (threadIdx.x & ~31);
   const int64_t nt = device_count(A.nt_dev, A.nt);
   const int64_t total = nt * C.ncam;
-  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
-       w += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(w / nt);
-    const int64_t t = w - (int64_t)c * nt;
-    const int width = C.cams[c].width, height = C.cams[c].height;
-    TriSetup s;
-    if (!tri_setup(width, height, A.P + (int64_t)c * A.nv, A.T, t, s)) continue;
-    const int64_t npx = (int64_t)(s.hix - s.lox + 1) * (s.hiy - s.loy + 1);
-    if (npx > kSmallBBox) {
-      if (A.pass == 0) {
-        const unsigned long long slot = atomicAdd((unsigned long long *)A.qcount, 1ull);
-        if ((int64_t)slot < A.qcap) {
-          A.queue[slot] = w;
-          continue;
+  const bool overflow = A.pass == 1 && __ldcg(A.qcount) > A.qcap;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; w0 < total;
+       w0 += stride) {
+    const int64_t w = w0 + lane;
+    int npx = 0;
+    if (w < total) {
+      const int c = (int)(w / nt);
+      const int64_t t = w - (int64_t)c * nt;
+      TriSetup s;
+      if (tri_setup(C.cams[c].width, C.cams[c].height, A.P + (int64_t)c * A.nv, A.T, t, s)) {
+        const int64_t n = (int64_t)(s.hix - s.lox + 1) * (s.hiy - s.loy + 1);
+        bool mine = true;
+        if (n > kSmallBBox) {
+          if (A.pass == 0) {
+            const unsigned long long slot = atomicAdd((unsigned long long *)A.qcount, 1ull);
+            mine = (int64_t)slot >= A.qcap;  // queue full: sweep it here
+            if (!mine) A.queue[slot] = w;
+          } else {
+            mine = overflow;  // pass 1: the big kernel replays the queue
+          }
         }
-      } else if (__ldcg(A.qcount) <= A.qcap) {
-        continue;  // pass 1: the big kernel replays the queue
+        if (mine) {
+          setup_to_smem(s, t, c, wsm[lane]);
+          npx = (int)n;
+        }
       }
-      // queue overflowed: walk it here (atomicMin is idempotent, so a queued
-      // triangle walked twice in pass 1 is harmless)
     }
-    unsigned long long *dp = (unsigned long long *)(A.depth + C.depth_off[c]);
-    unsigned *ip = (unsigned *)(A.ids ? A.ids + C.depth_off[c] : nullptr);
-    for (int y = s.loy; y <= s.hiy; ++y)
-      for (int x = s.lox; x <= s.hix; ++x) {
-        double d;
-        if (!tri_depth(s, x, y, d)) continue;
-        const int64_t p = (int64_t)y * width + x;
-        pixel_update(A.pass, d, t, dp + p, ip ? ip + p : nullptr);
+    // inclusive scan of the pixel counts across the warp
+    int incl = npx;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int sum = __shfl_sync(0xffffffffu, incl, 31);
+    __syncwarp();
+    for (int base = 0; base < sum; base += 32) {
+      const int idx = base + lane;
+      // owner = number of lanes whose inclusive count is <= idx
+      int own = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const int v = __shfl_sync(0xffffffffu, incl, own + step - 1);
+        if (v <= idx) own += step;
       }
+      const int own_incl = __shfl_sync(0xffffffffu, incl, own);
+      const int own_cnt = __shfl_sync(0xffffffffu, npx, own);
+      if (idx < sum) {
+        const TriSmem &m = wsm[own];
+        const int k = idx - (own_incl - own_cnt);
+        const int y = m.loy + k / m.bw, x = m.lox + k % m.bw;
+        TriSetup s;
+        smem_to_setup(m, s);
+        double d;
+        if (tri_depth(s, x, y, d)) {
+          const int W = C.cams[m.cam].width;
+          unsigned long long *dp = (unsigned long long *)(A.depth + C.depth_off[m.cam]);
+          unsigned *ip = (unsigned *)(A.ids ? A.ids + C.depth_off[m.cam] : nullptr);
+          const int64_t pxl = (int64_t)y * W + x;
+          pixel_update(A.pass, d, m.t, dp + pxl, ip ? ip + pxl : nullptr);
+        }
+      }
+    }
+    __syncwarp();
   }
 }
 
