@@ -218,7 +218,11 @@ __global__ void __launch_bounds__(kRasterThreads)
       if (idx < sum) {
         const TriSmem &m = wsm[own];
         const int k = idx - (own_incl - own_cnt);
-        const int y = m.loy + k / m.bw, x = m.lox + k % m.bw;
+        // k / bw without an integer divide: exact for k < 2^12 (the fraction
+        // of (k + 0.5) / bw is >= 0.5 / bw, far above the float error)
+        int qy = (k < 4096) ? __float2int_rz(((float)k + 0.5f) * __frcp_rn((float)m.bw))
+                            : k / m.bw;
+        const int y = m.loy + qy, x = m.lox + (k - qy * m.bw);
         TriSetup s;
         smem_to_setup(m, s);
         double d;
