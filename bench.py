@@ -155,38 +155,12 @@ def make_inputs(wl, frame_ids):
     return out
 
 
-def algorithmic_work(result, ncam):
-    """Voxel-camera projections of one frame: every voxel of the stage grid
-    and of every ROI grid against every camera (hull.py:83-90)."""
-    coarse = result.spec.num_voxels
-    fine = sum(g.spec.num_voxels for g in result.fine)
-    return (coarse + fine) * ncam
-
-
-class _Lite:
-    """Per-step scalars kept for reporting after the timed region."""
-
-    def __init__(self, r, clock, render_events):
-        self.spec = r.spec
-        self.fine_specs = [g.spec for g in r.fine]
-        self._clock = clock
-        self._render_events = render_events
-        self._tri_dev = r.batch.num_triangles_dev if r.batch is not None else None
-        self._nverts = int(r.batch.verts.shape[0]) if r.batch is not None else 0
-
-    def triangles(self):
-        return int(self._tri_dev.item()) if self._tri_dev is not None else 0
-
-
 # ---------------------------------------------------------------- b200 arm
 def run_b200(args):
     import numpy as np
     import torch
 
     from paper_1903_11785_b200 import _lib, workloads
-    from paper_1903_11785_b200._device import DeviceSilhouettes
-    from paper_1903_11785_b200.pipeline import _StageClock, reconstruct, run_frame
-    from paper_1903_11785_b200.render import frames_device, render_device, render_view
 
     rank, world, local = dist_setup(args)
     wl = workloads.get(args.workload)
@@ -205,29 +179,28 @@ def run_b200(args):
         foff = np.arange(ncam, dtype=np.int64) * (frames.shape[1] * frames.shape[2] * 3)
         dev_frames.append((masks, fb, foff))
 
-    stage_sum = {}
-    work = {"proj": 0, "tris": 0, "frames": 0}
+    from paper_1903_11785_b200.executor import executor_for
+
+    ex = executor_for(cfg, rig)
+    stage_names = ("sparse_carve", "noise_filter_roi", "dense_carve", "polygonize",
+                   "depth_images", "visibility", "render")
+    stage_sum = {k: 0.0 for k in stage_names}
+    work = {"proj": 0, "tris": 0, "frames": 0, "nv": 0}
 
     def device_step(i, timed):
         masks, fb, foff = dev_frames[i % len(dev_frames)]
-        clock = _StageClock()
-        dsils = DeviceSilhouettes(rig, masks)
-        r = reconstruct(cfg, rig, dsils, clock)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        if r.batch is not None and r.vis_bits is not None:
-            render_device(r.batch.verts, r.batch.tris, int(r.batch.tris.shape[0]), cams, None,
-                          r.vis_bits, int(r.vis_bits.shape[1]), virt,
-                          nt_dev=r.batch.num_triangles_dev, frame_buf=(fb, foff))
-        e1.record()
+        out = ex.run(masks, virt, fb, foff)
         if timed:
-            # keep only scalars: holding every frame's device buffers would turn the
-            # caching allocator's reuse into fresh cudaMalloc calls each step
-            work["proj"] += algorithmic_work(r, ncam)
+            st = out.stats_raw
+            for k, ms_ in zip(stage_names, st["ms"][:7]):
+                stage_sum[k] += float(ms_)
+            # algorithmic voxel-camera projections (hull.py:83-90): every voxel
+            # of the stage grid and of every ROI grid against every camera
+            work["proj"] += int(st["sparse_tests"] + st["dense_tests"]) * ncam
+            work["tris"] += int(st["triangles"])
+            work["nv"] = int(st["vertices"])
             work["frames"] += 1
-            return _Lite(r, clock, (e0, e1))
-        return None
+            work["last"] = (int(st["sparse_tests"]), int(st["dense_tests"]))
 
     for i in range(args.warmup):
         device_step(i, False)
@@ -242,7 +215,8 @@ def run_b200(args):
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record()
-    results = [device_step(i, True) for i in range(args.steps)]
+    for i in range(args.steps):
+        device_step(i, True)
     t_end.record()
     torch.cuda.synchronize()
     launches = lib.fvv_launch_count() - launches0
@@ -250,13 +224,6 @@ def run_b200(args):
     clocks = sampler.stop()
     ms_local = t_start.elapsed_time(t_end)
     ms = max_over_ranks(ms_local, world)
-
-    for r in results:
-        for k, v in r._clock.timings().to_dict().items():
-            stage_sum[k] = stage_sum.get(k, 0.0) + v
-        stage_sum["render"] = stage_sum.get("render", 0.0) + r._render_events[0].elapsed_time(
-            r._render_events[1])
-        work["tris"] += r.triangles()
     stage_ms = {k: v / args.steps for k, v in stage_sum.items()}
 
     total_frames = sum_over_ranks(args.steps, world)
@@ -267,7 +234,7 @@ def run_b200(args):
     hbm_peak, peak_src, _ = peaks()
     H, W = cams[0].image_height, cams[0].image_width
     top = max(stage_ms, key=stage_ms.get)
-    roof = roofline_for(top, stage_ms[top], results, ncam, H, W, hbm_peak, peak_src)
+    roof = roofline_for(top, stage_ms[top], work, ncam, H, W, hbm_peak, peak_src)
 
     # ---- e2e through the public API from pinned host memory ----
     e2e = None
@@ -354,13 +321,11 @@ def run_b200(args):
                 json.dump(line, fh, indent=2)
 
 
-def roofline_for(stage, ms, results, ncam, H, W, hbm_peak, peak_src):
+def roofline_for(stage, ms, work, ncam, H, W, hbm_peak, peak_src):
     """Algorithmic bytes of the dominant stage's kernels per launch / time."""
-    r = results[0]
-    nvox_c = r.spec.num_voxels
-    nvox_f = sum(s.num_voxels for s in r.fine_specs)
-    tris = r.triangles()
-    verts = r._nverts
+    nvox_c, nvox_f = work["last"]
+    tris = work["tris"] // max(work["frames"], 1)
+    verts = work["nv"]
     sil_bytes = ncam * H * ((W + 31) // 32) * 4
     per_stage = {
         # silhouette planes read once + occupancy bits written

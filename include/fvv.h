@@ -228,6 +228,64 @@ int fvv_render_view(const fvv_camera *rig, int ncam, const uint8_t *frames_dev,
 int fvv_back_project(const fvv_camera *cam, const double *pixel_dev, const double *depth_dev,
                      int64_t n, double *out_dev, void *stream);
 
+/* ---- native frame executor: pipeline.py:115-220 run_frame + render.py:64-113 ---- */
+
+typedef struct fvv_frame fvv_frame;
+
+/* PipelineConfig (pipeline.py:41-101) with derived defaults resolved
+ * (roi_margin, t_v); t_large may be +inf; budget = GridSpec voxel budget. */
+typedef struct fvv_frame_config {
+    double stage_lo[3], stage_hi[3];
+    double coarse_spacing, fine_spacing, roi_margin, t_v, t_large, fixed_isovalue;
+    int64_t t_small, budget;
+    int32_t min_views, exact;
+} fvv_frame_config;
+
+/* run_frame's stats dict (pipeline.py:152-196) + sizes + device stage times
+ * (ms: B-1, B-2, B-3, C, D-1, D-2, E, readback). */
+typedef struct fvv_frame_stats {
+    int64_t sparse_tests, sparse_occupied, components, dense_tests, dense_occupied,
+        fallback_edges, inconsistent_edge_starts, triangles, vertices, n_rois;
+    float ms[8];
+} fvv_frame_stats;
+
+/* Device outputs of the last fvv_frame_run (valid until the next run):
+ * merged-order triangles indexing verts (per-ROI slices via fvv_frame_rois),
+ * visibility bits (ncam x vis_stride words), depth planes (rig order,
+ * H*W each), virtual-view colour/source/covered. */
+typedef struct fvv_frame_outputs {
+    double *verts;
+    int32_t *tris;
+    int64_t nv, nt;
+    uint32_t *vis;
+    int64_t vis_stride;
+    double *depth;
+    uint8_t *color;
+    int32_t *source;
+    uint8_t *covered;
+    int64_t n_rois;
+    int64_t *ntri_dev;
+} fvv_frame_outputs;
+
+/* Executor for a fixed rig and config; device buffers persist across runs. */
+fvv_frame *fvv_frame_create(const fvv_camera *cams, int ncam, const fvv_frame_config *cfg);
+void fvv_frame_destroy(fvv_frame *frame);
+
+/* One frame: silhouette masks (uint8, rig order, camera c at
+ * masks_dev + sum of previous H*W) -> B-1 .. D-2, and when virt != NULL the
+ * colour pass from frames_dev (rig order, frame_off per camera) with the
+ * camera ranking rank_pos (rig positions, render.py:29-32). On failure
+ * *out_stage names the stage (1 B-1, 2 B-2, 3 B-3, 4 C, 5 D-1, 6 D-2, 7 E). */
+int fvv_frame_run(fvv_frame *frame, const uint8_t *masks_dev, const fvv_camera *virt,
+                  const int32_t *rank_pos, const uint8_t *frames_dev, const int64_t *frame_off,
+                  const uint8_t *fallback, void *stream, fvv_frame_stats *out_stats,
+                  int *out_stage);
+int fvv_frame_get_outputs(const fvv_frame *frame, fvv_frame_outputs *out);
+/* Per ROI: component id, box lo/hi (6 doubles), fine grid, mesh info
+ * {vbase, V, sbase, S, tbase, T, fallback_edges, inconsistent_starts}. */
+int fvv_frame_get_rois(const fvv_frame *frame, int64_t *component_ids, double *boxes,
+                   fvv_grid *grids, int64_t *info);
+
 /* ---- harness (not hot path): synthetic scene inputs ------------------------- */
 
 /* Ray-cast nparts ellipsoids (float64 records: centre[3], orientation[9]

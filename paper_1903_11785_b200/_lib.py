@@ -44,7 +44,27 @@ SYMBOLS = (
     "fvv_mesh_emit_scratch_bytes", "fvv_mesh_emit", "fvv_edge_isovalues",
     "fvv_raster_workspace_bytes", "fvv_rasterize", "fvv_classify", "fvv_triangle_sources",
     "fvv_render_count", "fvv_render_view", "fvv_back_project", "fvv_render_ellipsoids",
+    "fvv_frame_create", "fvv_frame_destroy", "fvv_frame_run", "fvv_frame_get_outputs",
+    "fvv_frame_get_rois",
 )
+
+FRAME_CONFIG_DTYPE = np.dtype([("stage_lo", "<f8", (3,)), ("stage_hi", "<f8", (3,)),
+                               ("coarse_spacing", "<f8"), ("fine_spacing", "<f8"),
+                               ("roi_margin", "<f8"), ("t_v", "<f8"), ("t_large", "<f8"),
+                               ("fixed_isovalue", "<f8"), ("t_small", "<i8"), ("budget", "<i8"),
+                               ("min_views", "<i4"), ("exact", "<i4")])
+FRAME_STATS_DTYPE = np.dtype([(k, "<i8") for k in (
+    "sparse_tests", "sparse_occupied", "components", "dense_tests", "dense_occupied",
+    "fallback_edges", "inconsistent_edge_starts", "triangles", "vertices", "n_rois")] +
+    [("ms", "<f4", (8,))])
+
+
+class FrameOutputs(ctypes.Structure):
+    _fields_ = [("verts", ctypes.c_void_p), ("tris", ctypes.c_void_p), ("nv", ctypes.c_int64),
+                ("nt", ctypes.c_int64), ("vis", ctypes.c_void_p), ("vis_stride", ctypes.c_int64),
+                ("depth", ctypes.c_void_p), ("color", ctypes.c_void_p),
+                ("source", ctypes.c_void_p), ("covered", ctypes.c_void_p),
+                ("n_rois", ctypes.c_int64), ("ntri_dev", ctypes.c_void_p)]
 
 
 class FvvError(RuntimeError):
@@ -66,6 +86,8 @@ def load():
         lib = ctypes.CDLL(LIB_PATH)
         lib.fvv_last_error.restype = ctypes.c_char_p
         lib.fvv_launch_count.restype = ctypes.c_longlong
+        lib.fvv_frame_create.restype = ctypes.c_void_p
+        lib.fvv_frame_destroy.argtypes = [ctypes.c_void_p]
         lib.fvv_ccl_workspace_bytes.restype = ctypes.c_size_t
         lib.fvv_mesh_workspace_bytes.restype = ctypes.c_size_t
         lib.fvv_mesh_emit_scratch_bytes.restype = ctypes.c_size_t

@@ -1,0 +1,520 @@
+// Native per-frame executor: the whole hot path of pipeline.py:115-220
+// (B-1 .. D-2) plus one render_view colour pass (render.py:64-113) driven
+// from C++ on one CUDA stream, with device buffers that persist across
+// frames (grown on demand, never freed between frames).
+//
+// The host work the reference does between its kernels is reproduced here
+// with the same IEEE double arithmetic: GridSpec.from_aabb (voxels.py:62-71),
+// the noise band filter (hull.py:46-47, 257-269) and extract_rois
+// (hull.py:272-284). Three host synchronisations per frame remain, each a
+// tiny pinned read: the component table (to size the ROI grids), the mesh
+// vertex/cell counts (to size the mesh outputs) and the final counters.
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "fvv_common.cuh"
+
+extern "C" {
+int fvv_pack_silhouettes(const fvv_camera *, int, const uint8_t *, const int64_t *, uint32_t *,
+                         const int64_t *, void *);
+int fvv_carve(const fvv_camera *, int, const uint32_t *, const int64_t *, const fvv_grid *, int,
+              const int64_t *, int, uint32_t *, int64_t *, void *);
+size_t fvv_ccl_workspace_bytes(const fvv_grid *);
+int fvv_ccl26(const uint32_t *, const fvv_grid *, void *, size_t, fvv_component *, int64_t,
+              int64_t *, void *);
+int fvv_ccl_components(const fvv_grid *, const void *, fvv_component *, int64_t, void *);
+size_t fvv_mesh_workspace_bytes(const fvv_grid *, int);
+int fvv_mesh_prepare(const fvv_grid *, int, const uint32_t *, const int64_t *, void *, size_t,
+                     void *);
+int fvv_mesh_counts(const fvv_grid *, int, const void *, int64_t *, int64_t *, void *);
+size_t fvv_mesh_emit_scratch_bytes(int64_t, int64_t);
+int fvv_mesh_emit(const fvv_camera *, int, const uint32_t *, const int64_t *, const fvv_grid *,
+                  int, const uint32_t *, const int64_t *, int, double, void *, size_t, int64_t,
+                  int64_t, void *, size_t, double *, int32_t *, void *);
+size_t fvv_raster_workspace_bytes(int64_t, int64_t, int);
+int fvv_rasterize(const fvv_camera *, int, const double *, int64_t, const int32_t *, int64_t,
+                  const int64_t *, double *, const int64_t *, int32_t *, void *, size_t, void *);
+int fvv_classify(const fvv_camera *, int, const double *, const int32_t *, int64_t,
+                 const int64_t *, const double *, const int64_t *, double, uint32_t *, int64_t,
+                 void *);
+int fvv_triangle_sources(const int32_t *, const int32_t *, int, const uint32_t *, int64_t, int64_t,
+                         const int64_t *, int32_t *, void *);
+int fvv_render_count(const fvv_camera *, int, const fvv_camera *, const int32_t *,
+                     const int32_t *, int64_t *, void *);
+int fvv_render_view(const fvv_camera *, int, const uint8_t *, const int64_t *,
+                    const fvv_camera *, const double *, const int32_t *, const int32_t *,
+                    const uint8_t *, uint8_t *, int32_t *, uint8_t *, const int64_t *, void *);
+}
+
+namespace fvv {
+
+// device buffer that only grows
+struct DevBuf {
+  void *p = nullptr;
+  size_t cap = 0;
+  int ensure(size_t bytes) {
+    if (bytes <= cap && p) return FVV_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = bytes + bytes / 4 + 256;
+    if (cudaMalloc(&p, want) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("frame executor: cudaMalloc(%zu) failed", want);
+      return FVV_E_CUDA;
+    }
+    cap = want;
+    return FVV_OK;
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  template <class T>
+  T *as() const {
+    return (T *)p;
+  }
+};
+
+__global__ void add_count_kernel(int64_t *dst, const int64_t *src, int64_t add) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *dst = *src + add;
+}
+
+__global__ void offset_tris_kernel(int32_t *tris, int64_t n3, int32_t add) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n3;
+       i += (int64_t)gridDim.x * blockDim.x)
+    tris[i] += add;
+}
+
+}  // namespace fvv
+
+using namespace fvv;
+
+struct fvv_frame {
+  std::vector<fvv_camera> cams, cams_by_id;
+  std::vector<int64_t> mask_off, word_off, word_off_by_id, plane_off;
+  int ncam = 0;
+  int64_t sil_words = 0, planes = 0;
+  fvv_frame_config cfg;
+  fvv_grid coarse;
+  // persistent device buffers
+  DevBuf sil, occ_c, cnt_c, ccl_ws, comps, ccl_counts, occ_f, cnt_f, mesh_ws, mesh_scratch,
+      mesh_totals, mesh_info, verts, tris, ntri, raster_ws, depth, vis, vplane_d, vplane_id,
+      vraster_ws, src, rcounts, color, source, covered;
+  // pinned host staging
+  void *host_small = nullptr;
+  size_t host_small_cap = 0;
+  // results of the last run
+  std::vector<fvv_grid> fine;
+  std::vector<int64_t> fine_word_off;
+  std::vector<int64_t> roi_component;
+  std::vector<double> roi_box;  // 6 per ROI
+  std::vector<int64_t> info;    // 8 per ROI
+  int64_t nv = 0, nt = 0, vis_stride = 0;
+  fvv_frame_stats stats;
+  cudaEvent_t ev[9];
+};
+
+static int grid_from_aabb(const double lo[3], const double hi[3], double spacing, int64_t budget,
+                          fvv_grid &g) {
+  // voxels.py:62-71 GridSpec.from_aabb (+ the budget check of voxels.py:34-37)
+  for (int j = 0; j < 3; ++j)
+    if (!(hi[j] > lo[j])) {
+      set_error("AABB must have positive extent on every axis");
+      return FVV_E_ARG;
+    }
+  int64_t n = 1;
+  for (int j = 0; j < 3; ++j) {
+    double d = std::ceil((hi[j] - lo[j]) / spacing - 1e-9);
+    int64_t di = (int64_t)d;
+    if (di < 1) di = 1;
+    g.origin[j] = lo[j];
+    g.dims[j] = di;
+    n *= di;
+  }
+  g.spacing = spacing;
+  if (n > budget) {
+    set_error("grid of %lld voxels exceeds budget %lld", (long long)n, (long long)budget);
+    return FVV_E_ARG;
+  }
+  return FVV_OK;
+}
+
+static int host_small_ensure(fvv_frame *f, size_t bytes) {
+  if (bytes <= f->host_small_cap) return FVV_OK;
+  if (f->host_small) cudaFreeHost(f->host_small);
+  f->host_small = nullptr;
+  size_t want = bytes * 2 + 4096;
+  if (cudaMallocHost(&f->host_small, want) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("frame executor: cudaMallocHost failed");
+    return FVV_E_CUDA;
+  }
+  f->host_small_cap = want;
+  return FVV_OK;
+}
+
+#define FVV_TRY(stage, expr)                     \
+  do {                                           \
+    int _rc = (expr);                            \
+    if (_rc != FVV_OK) {                         \
+      if (out_stage) *out_stage = (stage);       \
+      return _rc;                                \
+    }                                            \
+  } while (0)
+
+extern "C" {
+
+fvv_frame *fvv_frame_create(const fvv_camera *cams, int ncam, const fvv_frame_config *cfg) {
+  if (ncam < 1 || ncam > FVV_MAX_CAMS) {
+    set_error("fvv_frame_create: %d cameras (1..%d)", ncam, FVV_MAX_CAMS);
+    return nullptr;
+  }
+  fvv_frame *f = new fvv_frame();
+  f->cfg = *cfg;
+  f->ncam = ncam;
+  f->cams.assign(cams, cams + ncam);
+  int64_t m = 0, w = 0, pl = 0;
+  for (int c = 0; c < ncam; ++c) {
+    f->mask_off.push_back(m);
+    f->word_off.push_back(w);
+    f->plane_off.push_back(pl);
+    m += (int64_t)cams[c].width * cams[c].height;
+    w += (int64_t)cams[c].height * sil_stride_words(cams[c].width);
+    pl += (int64_t)cams[c].width * cams[c].height;
+  }
+  f->sil_words = w;
+  f->planes = pl;
+  // cameras in ascending id order for the isovalue kernel (mesh.py:165-167)
+  std::vector<int> order(ncam);
+  for (int c = 0; c < ncam; ++c) order[c] = c;
+  for (int a = 1; a < ncam; ++a)
+    for (int b = a; b > 0 && cams[order[b]].id < cams[order[b - 1]].id; --b)
+      std::swap(order[b], order[b - 1]);
+  for (int c = 0; c < ncam; ++c) {
+    f->cams_by_id.push_back(cams[order[c]]);
+    f->word_off_by_id.push_back(f->word_off[order[c]]);
+  }
+  if (grid_from_aabb(cfg->stage_lo, cfg->stage_hi, cfg->coarse_spacing, cfg->budget,
+                     f->coarse) != FVV_OK) {
+    delete f;
+    return nullptr;
+  }
+  for (int e = 0; e < 9; ++e) cudaEventCreate(&f->ev[e]);
+  if (f->sil.ensure(4 * (size_t)f->sil_words) || f->occ_c.ensure(4 * (size_t)((
+          f->coarse.dims[0] * f->coarse.dims[1] * f->coarse.dims[2] + 31) / 32)) ||
+      f->cnt_c.ensure(64) || f->ccl_counts.ensure(64) ||
+      f->ccl_ws.ensure(fvv_ccl_workspace_bytes(&f->coarse)) ||
+      f->comps.ensure(sizeof(fvv_component) * 4096) || f->mesh_totals.ensure(64) ||
+      f->ntri.ensure(64) || host_small_ensure(f, 1 << 20)) {
+    delete f;
+    return nullptr;
+  }
+  return f;
+}
+
+void fvv_frame_destroy(fvv_frame *f) {
+  if (!f) return;
+  for (int e = 0; e < 9; ++e) cudaEventDestroy(f->ev[e]);
+  if (f->host_small) cudaFreeHost(f->host_small);
+  delete f;
+}
+
+int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt,
+                  const int32_t *rank_pos, const uint8_t *frames_dev, const int64_t *frame_off,
+                  const uint8_t *fallback, void *stream, fvv_frame_stats *out_stats,
+                  int *out_stage) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const fvv_frame_config &cfg = f->cfg;
+  const int ncam = f->ncam;
+  if (out_stage) *out_stage = 0;
+  memset(&f->stats, 0, sizeof(f->stats));
+  fvv_frame_stats &S = f->stats;
+  cudaEventRecord(f->ev[0], st);
+
+  // ---- B-1 sparse carve (pipeline.py:154-157) ----
+  const fvv_grid &G = f->coarse;
+  const int64_t nvox_c = G.dims[0] * G.dims[1] * G.dims[2];
+  S.sparse_tests = nvox_c;
+  FVV_TRY(1, fvv_pack_silhouettes(f->cams.data(), ncam, masks_dev, f->mask_off.data(),
+                                  f->sil.as<uint32_t>(), f->word_off.data(), st));
+  const int64_t zero = 0;
+  FVV_TRY(1, fvv_carve(f->cams.data(), ncam, f->sil.as<uint32_t>(), f->word_off.data(), &G, 1,
+                       &zero, cfg.min_views, f->occ_c.as<uint32_t>(), f->cnt_c.as<int64_t>(),
+                       st));
+  cudaEventRecord(f->ev[1], st);
+
+  // ---- B-2 CCL, noise filter, ROIs (pipeline.py:159-166) ----
+  FVV_TRY(2, fvv_ccl26(f->occ_c.as<uint32_t>(), &G, f->ccl_ws.p, f->ccl_ws.cap,
+                       f->comps.as<fvv_component>(), 4096, f->ccl_counts.as<int64_t>(), st));
+  int64_t *hs = (int64_t *)f->host_small;
+  cudaMemcpyAsync(hs, f->ccl_counts.p, 16, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(hs + 2, f->cnt_c.p, 8, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(hs + 4, f->comps.p, sizeof(fvv_component) * 4096, cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) {
+    if (out_stage) *out_stage = 2;
+    return cuda_check("fvv_frame_run B-2");
+  }
+  const int64_t ncomp = hs[1];
+  S.sparse_occupied = hs[2];
+  const fvv_component *comps = (const fvv_component *)(hs + 4);
+  std::vector<fvv_component> big;
+  if (ncomp > 4096) {
+    FVV_TRY(2, f->comps.ensure(sizeof(fvv_component) * ncomp));
+    FVV_TRY(2, fvv_ccl_components(&G, f->ccl_ws.p, f->comps.as<fvv_component>(), ncomp, st));
+    big.resize(ncomp);
+    cudaMemcpyAsync(big.data(), f->comps.p, sizeof(fvv_component) * ncomp,
+                    cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    comps = big.data();
+  }
+  f->fine.clear();
+  f->roi_component.clear();
+  f->roi_box.clear();
+  double extent[3];
+  for (int j = 0; j < 3; ++j) extent[j] = G.origin[j] + G.spacing * (double)G.dims[j];
+  for (int64_t c = 0; c < ncomp; ++c) {
+    const double cnt = (double)comps[c].voxel_count;
+    if (!((double)cfg.t_small <= cnt && cnt <= cfg.t_large)) continue;  // hull.py:46-47
+    double lo[3], hi[3];
+    for (int j = 0; j < 3; ++j) {  // hull.py:279-282
+      lo[j] = G.origin[j] + G.spacing * (double)comps[c].bbox_min[j] - cfg.roi_margin;
+      hi[j] = G.origin[j] + G.spacing * ((double)comps[c].bbox_max[j] + 1.0) + cfg.roi_margin;
+      lo[j] = lo[j] >= G.origin[j] ? lo[j] : G.origin[j];  // np.maximum(lo, stage_lo)
+      hi[j] = hi[j] <= extent[j] ? hi[j] : extent[j];      // np.minimum(hi, stage_hi)
+    }
+    for (int j = 0; j < 3; ++j)
+      if (!(lo[j] < hi[j])) {
+        set_error("ROI must have positive extent");
+        if (out_stage) *out_stage = 2;
+        return FVV_E_ARG;
+      }
+    f->roi_component.push_back(comps[c].id);
+    for (int j = 0; j < 3; ++j) f->roi_box.push_back(lo[j]);
+    for (int j = 0; j < 3; ++j) f->roi_box.push_back(hi[j]);
+  }
+  S.components = (int64_t)f->roi_component.size();
+  cudaEventRecord(f->ev[2], st);
+
+  // ---- B-3 dense carve (pipeline.py:168-173) ----
+  const int nroi = (int)f->roi_component.size();
+  f->fine.resize(nroi);
+  f->fine_word_off.resize(nroi);
+  int64_t fw = 0;
+  for (int r = 0; r < nroi; ++r) {
+    FVV_TRY(3, grid_from_aabb(&f->roi_box[6 * r], &f->roi_box[6 * r + 3], cfg.fine_spacing,
+                              cfg.budget, f->fine[r]));
+    const int64_t n = f->fine[r].dims[0] * f->fine[r].dims[1] * f->fine[r].dims[2];
+    S.dense_tests += n;
+    f->fine_word_off[r] = fw;
+    fw += (n + 31) / 32;
+  }
+  FVV_TRY(3, f->occ_f.ensure(4 * (size_t)(fw > 0 ? fw : 1)));
+  FVV_TRY(3, f->cnt_f.ensure(8 * (size_t)(nroi > 0 ? nroi : 1)));
+  for (int r0 = 0; r0 < nroi; r0 += FVV_MAX_GRIDS) {
+    const int nb = nroi - r0 < FVV_MAX_GRIDS ? nroi - r0 : FVV_MAX_GRIDS;
+    FVV_TRY(3, fvv_carve(f->cams.data(), ncam, f->sil.as<uint32_t>(), f->word_off.data(),
+                         &f->fine[r0], nb, &f->fine_word_off[r0], cfg.min_views,
+                         f->occ_f.as<uint32_t>(), f->cnt_f.as<int64_t>() + r0, st));
+  }
+  cudaEventRecord(f->ev[3], st);
+
+  // ---- C polygonize every ROI (pipeline.py:175-190) ----
+  f->info.assign(8 * (size_t)nroi, 0);
+  f->nv = f->nt = 0;
+  int64_t v_before = 0, t_before = 0;
+  for (int r0 = 0; r0 < nroi; r0 += FVV_MAX_GRIDS) {
+    const int nb = nroi - r0 < FVV_MAX_GRIDS ? nroi - r0 : FVV_MAX_GRIDS;
+    const size_t wsb = fvv_mesh_workspace_bytes(&f->fine[r0], nb);
+    FVV_TRY(4, f->mesh_ws.ensure(wsb));
+    FVV_TRY(4, f->mesh_info.ensure(64 * (size_t)nb));
+    FVV_TRY(4, fvv_mesh_prepare(&f->fine[r0], nb, f->occ_f.as<uint32_t>(),
+                                &f->fine_word_off[r0], f->mesh_ws.p, wsb, st));
+    FVV_TRY(4, fvv_mesh_counts(&f->fine[r0], nb, f->mesh_ws.p, f->mesh_totals.as<int64_t>(),
+                               nullptr, st));
+    cudaMemcpyAsync(hs, f->mesh_totals.p, 24, cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) {
+      if (out_stage) *out_stage = 4;
+      return cuda_check("fvv_frame_run C");
+    }
+    const int64_t nv = hs[0], ns = hs[1];
+    const size_t sb = fvv_mesh_emit_scratch_bytes(nv, ns);
+    FVV_TRY(4, f->mesh_scratch.ensure(sb));
+    // vertices / triangles of all batches share one array; keep prior batches
+    if (r0 == 0) {
+      FVV_TRY(4, f->verts.ensure(24 * (size_t)(nv > 0 ? nv : 1)));
+      FVV_TRY(4, f->tris.ensure(12 * (size_t)(5 * ns > 0 ? 5 * ns : 1)));
+    } else if (24 * (size_t)(v_before + nv) > f->verts.cap ||
+               12 * (size_t)(t_before + 5 * ns) > f->tris.cap) {
+      set_error("frame executor: > %d ROIs with growing outputs is not supported",
+                FVV_MAX_GRIDS);
+      if (out_stage) *out_stage = 4;
+      return FVV_E_LIMIT;
+    }
+    FVV_TRY(4, fvv_mesh_emit(f->cams_by_id.data(), ncam, f->sil.as<uint32_t>(),
+                             f->word_off_by_id.data(), &f->fine[r0], nb,
+                             f->occ_f.as<uint32_t>(), &f->fine_word_off[r0], cfg.exact,
+                             cfg.fixed_isovalue, f->mesh_ws.p, wsb, nv, ns, f->mesh_scratch.p,
+                             sb, f->verts.as<double>() + 3 * v_before,
+                             f->tris.as<int32_t>() + 3 * t_before, st));
+    FVV_TRY(4, fvv_mesh_counts(&f->fine[r0], nb, f->mesh_ws.p, f->mesh_totals.as<int64_t>(),
+                               f->mesh_info.as<int64_t>(), st));
+    if (r0 + nb < nroi) {  // more batches: need this batch's triangle count now
+      cudaMemcpyAsync(hs, f->mesh_totals.p, 24, cudaMemcpyDeviceToHost, st);
+      cudaMemcpyAsync(f->info.data() + 8 * (size_t)r0, f->mesh_info.p, 64 * (size_t)nb,
+                      cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      const int64_t tb = hs[2];
+      if (v_before)
+        offset_tris_kernel<<<148 * 4, 256, 0, st>>>(f->tris.as<int32_t>() + 3 * t_before, 3 * tb,
+                                                    (int32_t)v_before);
+      for (int r = r0; r < r0 + nb; ++r) {
+        f->info[8 * r + 0] += v_before;
+        f->info[8 * r + 4] += t_before;
+      }
+      v_before += nv;
+      t_before += tb;
+    } else {
+      // last (usually only) batch: its triangle count stays on the device
+      // for D-1/D-2; the host reads it with the final counters
+      if (v_before) {
+        cudaMemcpyAsync(hs, f->mesh_totals.p, 24, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        offset_tris_kernel<<<148 * 4, 256, 0, st>>>(f->tris.as<int32_t>() + 3 * t_before,
+                                                    3 * hs[2], (int32_t)v_before);
+      }
+      f->nv = v_before + nv;
+      f->nt = t_before + 5 * ns;  // upper bound until the final read
+    }
+  }
+  cudaEventRecord(f->ev[4], st);
+
+  // device-side total triangle count for D-1 / D-2 / E (no host round trip)
+  int64_t *ntri_dev = f->ntri.as<int64_t>();
+  if (nroi > 0)
+    add_count_kernel<<<1, 32, 0, st>>>(ntri_dev, f->mesh_totals.as<int64_t>() + 2, t_before);
+  else
+    cudaMemsetAsync(ntri_dev, 0, 8, st);
+  const int64_t nt_ub = f->nt;
+  f->vis_stride = (nt_ub + 31) / 32 > 0 ? (nt_ub + 31) / 32 : 1;
+
+  // ---- D-1 depth images, D-2 visibility (pipeline.py:198-207) ----
+  const bool have_mesh = f->nv > 0 && nt_ub > 0;
+  if (have_mesh) {
+    FVV_TRY(5, f->depth.ensure(8 * (size_t)f->planes));
+    const size_t rwb = fvv_raster_workspace_bytes(f->nv, nt_ub, ncam);
+    FVV_TRY(5, f->raster_ws.ensure(rwb));
+    FVV_TRY(5, fvv_rasterize(f->cams.data(), ncam, f->verts.as<double>(), f->nv,
+                             f->tris.as<int32_t>(), nt_ub, ntri_dev, f->depth.as<double>(),
+                             f->plane_off.data(), nullptr, f->raster_ws.p, f->raster_ws.cap, st));
+  }
+  cudaEventRecord(f->ev[5], st);
+  FVV_TRY(6, f->vis.ensure(4 * (size_t)ncam * f->vis_stride));
+  cudaMemsetAsync(f->vis.p, 0, 4 * (size_t)ncam * f->vis_stride, st);
+  if (have_mesh)
+    FVV_TRY(6, fvv_classify(f->cams.data(), ncam, f->verts.as<double>(), f->tris.as<int32_t>(),
+                            nt_ub, ntri_dev, f->depth.as<double>(), f->plane_off.data(),
+                            cfg.t_v, f->vis.as<uint32_t>(), f->vis_stride, st));
+  cudaEventRecord(f->ev[6], st);
+
+  // ---- E: one virtual view (render.py:64-113) ----
+  if (virt) {
+    const int64_t np = (int64_t)virt->width * virt->height;
+    FVV_TRY(7, f->color.ensure(3 * (size_t)np));
+    FVV_TRY(7, f->source.ensure(4 * (size_t)np));
+    FVV_TRY(7, f->covered.ensure((size_t)np));
+    if (have_mesh) {
+      FVV_TRY(7, f->vplane_d.ensure(8 * (size_t)np));
+      FVV_TRY(7, f->vplane_id.ensure(4 * (size_t)np));
+      const size_t vwb = fvv_raster_workspace_bytes(f->nv, nt_ub, 1);
+      FVV_TRY(7, f->vraster_ws.ensure(vwb));
+      const int64_t off0 = 0;
+      FVV_TRY(7, fvv_rasterize(virt, 1, f->verts.as<double>(), f->nv, f->tris.as<int32_t>(),
+                               nt_ub, ntri_dev, f->vplane_d.as<double>(), &off0,
+                               f->vplane_id.as<int32_t>(), f->vraster_ws.p, f->vraster_ws.cap,
+                               st));
+      std::vector<int32_t> rank_id(ncam);
+      for (int r = 0; r < ncam; ++r) rank_id[r] = f->cams[rank_pos[r]].id;
+      FVV_TRY(7, f->src.ensure(4 * (size_t)(nt_ub > 0 ? nt_ub : 1)));
+      FVV_TRY(7, fvv_triangle_sources(rank_pos, rank_id.data(), ncam, f->vis.as<uint32_t>(),
+                                      f->vis_stride, nt_ub, ntri_dev, f->src.as<int32_t>(), st));
+      FVV_TRY(7, f->rcounts.ensure(8 * (size_t)(1 + ncam)));
+      FVV_TRY(7, fvv_render_count(f->cams.data(), ncam, virt, f->vplane_id.as<int32_t>(),
+                                  f->src.as<int32_t>(), f->rcounts.as<int64_t>(), st));
+      FVV_TRY(7, fvv_render_view(f->cams.data(), ncam, frames_dev, frame_off, virt,
+                                 f->vplane_d.as<double>(), f->vplane_id.as<int32_t>(),
+                                 f->src.as<int32_t>(), fallback, f->color.as<uint8_t>(),
+                                 f->source.as<int32_t>(), f->covered.as<uint8_t>(),
+                                 f->rcounts.as<int64_t>(), st));
+    } else {
+      cudaMemsetAsync(f->color.p, 0, 3 * (size_t)np, st);
+      cudaMemsetAsync(f->source.p, 0xff, 4 * (size_t)np, st);
+      cudaMemsetAsync(f->covered.p, 0, (size_t)np, st);
+    }
+  }
+  cudaEventRecord(f->ev[7], st);
+
+  // ---- final counters (one read) ----
+  int64_t *h = hs;
+  cudaMemcpyAsync(h, ntri_dev, 8, cudaMemcpyDeviceToHost, st);
+  if (nroi) {
+    cudaMemcpyAsync(h + 8, f->cnt_f.p, 8 * (size_t)nroi, cudaMemcpyDeviceToHost, st);
+    const int last0 = ((nroi - 1) / FVV_MAX_GRIDS) * FVV_MAX_GRIDS;
+    cudaMemcpyAsync(f->info.data() + 8 * (size_t)last0, f->mesh_info.p,
+                    64 * (size_t)(nroi - last0), cudaMemcpyDeviceToHost, st);
+  }
+  cudaEventRecord(f->ev[8], st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) {
+    if (out_stage) *out_stage = 8;
+    return cuda_check("fvv_frame_run");
+  }
+  if (nroi) {
+    const int last0 = ((nroi - 1) / FVV_MAX_GRIDS) * FVV_MAX_GRIDS;
+    for (int r = last0; r < nroi; ++r) {
+      f->info[8 * r + 0] += v_before;
+      f->info[8 * r + 4] += t_before;
+    }
+  }
+  f->nt = h[0];
+  S.triangles = h[0];
+  S.vertices = f->nv;
+  S.n_rois = nroi;
+  for (int r = 0; r < nroi; ++r) {
+    S.dense_occupied += h[8 + r];
+    S.fallback_edges += f->info[8 * r + 6];
+    S.inconsistent_edge_starts += f->info[8 * r + 7];
+  }
+  if (!cfg.exact) S.fallback_edges = S.inconsistent_edge_starts = 0;
+  for (int e = 0; e < 8; ++e) cudaEventElapsedTime(&S.ms[e], f->ev[e], f->ev[e + 1]);
+  if (out_stats) *out_stats = S;
+  return cuda_check("fvv_frame_run");
+}
+
+int fvv_frame_get_outputs(const fvv_frame *f, fvv_frame_outputs *o) {
+  memset(o, 0, sizeof(*o));
+  o->verts = f->verts.as<double>();
+  o->tris = f->tris.as<int32_t>();
+  o->nv = f->nv;
+  o->nt = f->nt;
+  o->vis = f->vis.as<uint32_t>();
+  o->vis_stride = f->vis_stride;
+  o->depth = f->depth.as<double>();
+  o->color = f->color.as<uint8_t>();
+  o->source = f->source.as<int32_t>();
+  o->covered = f->covered.as<uint8_t>();
+  o->n_rois = (int64_t)f->roi_component.size();
+  o->ntri_dev = f->ntri.as<int64_t>();
+  return FVV_OK;
+}
+
+int fvv_frame_get_rois(const fvv_frame *f, int64_t *component_ids, double *boxes, fvv_grid *grids,
+                   int64_t *info) {
+  const size_t n = f->roi_component.size();
+  if (component_ids) memcpy(component_ids, f->roi_component.data(), 8 * n);
+  if (boxes) memcpy(boxes, f->roi_box.data(), 48 * n);
+  if (grids) memcpy(grids, f->fine.data(), sizeof(fvv_grid) * n);
+  if (info) memcpy(info, f->info.data(), 64 * n);
+  return FVV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,206 @@
+"""Python face of the native frame executor (fvv_frame_*, csrc/frame.cu).
+
+One executor per (rig, PipelineConfig): the C++ side runs B-1 .. D-2 and the
+optional virtual-view colour pass on the current CUDA stream with device
+buffers that persist across frames; Python only hands over the inputs and
+wraps the outputs. ``FrameExecutor.run`` returns a ``FrameOutput`` whose
+device views stay valid until the executor's next run; ``to_host`` copies
+everything a SceneBundle needs back in one batch of pinned transfers.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._device import cam_table, require_cuda, stream_handle
+
+STAGE_NAMES = {1: "B-1 sparse carve", 2: "B-2 noise filter/ROI", 3: "B-3 dense carve",
+               4: "C polygonize", 5: "D-1 depth images", 6: "D-2 visibility",
+               7: "E render view", 8: "D-2 visibility"}
+_INFO_VBASE, _INFO_V, _INFO_SBASE, _INFO_S, _INFO_TBASE, _INFO_T, _INFO_FB, _INFO_INC = range(8)
+
+
+class _CudaView:
+    """Minimal __cuda_array_interface__ over executor-owned device memory."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(int(s) for s in shape),
+                                         "typestr": typestr, "data": (int(ptr or 0), False),
+                                         "version": 3, "strides": None}
+
+
+def _dev(ptr, shape, typestr):
+    if not ptr or 0 in shape:
+        return torch.empty(shape, dtype={"<f8": torch.float64, "<i4": torch.int32,
+                                         "<u4": torch.int32, "|u1": torch.uint8,
+                                         "<i8": torch.int64}[typestr], device="cuda")
+    t = torch.as_tensor(_CudaView(ptr, shape, typestr), device="cuda")
+    return t.view(torch.int32) if typestr == "<u4" else t
+
+
+class FrameOutput:
+    """Results of one executor run (device views + host scalars)."""
+
+    def __init__(self, stats, outs, rois, ncam, virtual):
+        self.stats_raw = stats
+        self.nv, self.nt = int(outs.nv), int(stats["triangles"])
+        self.verts = _dev(outs.verts, (self.nv, 3), "<f8")
+        self.tris = _dev(outs.tris, (self.nt, 3), "<i4")
+        self.vis_stride = int(outs.vis_stride)
+        self.vis_bits = _dev(outs.vis, (ncam, self.vis_stride), "<u4")
+        self.ntri_dev = _dev(outs.ntri_dev, (1,), "<i8") if outs.ntri_dev else None
+        self.depth_ptr = outs.depth
+        self.component_ids, self.boxes, self.grids, self.info = rois
+        self.image = None
+        if virtual is not None:
+            h, w = virtual.image_height, virtual.image_width
+            self.image = (_dev(outs.color, (h, w, 3), "|u1"), _dev(outs.source, (h, w), "<i4"),
+                          _dev(outs.covered, (h, w), "|u1"))
+
+    def stats(self) -> dict:
+        s = self.stats_raw
+        return {k: int(s[k]) for k in ("sparse_tests", "sparse_occupied", "components",
+                                       "dense_tests", "dense_occupied", "fallback_edges",
+                                       "inconsistent_edge_starts", "triangles")}
+
+    def depth_planes(self, cams):
+        total = sum(c.image_height * c.image_width for c in cams)
+        return _dev(self.depth_ptr, (total,), "<f8")
+
+    def to_host(self, cams, keep_depths=False):
+        """Pinned D2H of vertices, triangles, visibility bits, the rendered
+        image (and depth planes) with one synchronisation."""
+        pinned = {}
+
+        def fetch(name, t):
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t, non_blocking=True)
+            pinned[name] = h
+
+        fetch("verts", self.verts)
+        fetch("tris", self.tris)
+        fetch("vis", self.vis_bits)
+        if self.image is not None:
+            for n, t in zip(("color", "source", "covered"), self.image):
+                fetch(n, t)
+        if keep_depths and self.nt:
+            fetch("depth", self.depth_planes(cams))
+        torch.cuda.current_stream().synchronize()
+        return {k: v.numpy() for k, v in pinned.items()}
+
+
+class FrameExecutor:
+    """fvv_frame handle for one rig + PipelineConfig."""
+
+    def __init__(self, cfg, rig, budget=None):
+        from .voxels import DEFAULT_VOXEL_BUDGET
+
+        require_cuda()
+        self.cams = list(rig)
+        self.ncam = len(self.cams)
+        self._tab = cam_table(self.cams)
+        conf = np.zeros(1, dtype=_lib.FRAME_CONFIG_DTYPE)
+        conf["stage_lo"] = np.asarray(cfg.stage_lo, dtype=np.float64)
+        conf["stage_hi"] = np.asarray(cfg.stage_hi, dtype=np.float64)
+        conf["coarse_spacing"] = cfg.coarse_spacing
+        conf["fine_spacing"] = cfg.fine_spacing
+        conf["roi_margin"] = cfg.roi_margin
+        conf["t_v"] = cfg.t_v
+        conf["t_large"] = float(cfg.t_large)
+        conf["fixed_isovalue"] = cfg.fixed_isovalue
+        conf["t_small"] = int(cfg.t_small)
+        conf["budget"] = int(DEFAULT_VOXEL_BUDGET if budget is None else budget)
+        conf["min_views"] = int(cfg.min_views)
+        conf["exact"] = int(cfg.iso_mode == "exact")
+        self._conf = conf
+        h = _lib.load().fvv_frame_create(_lib.host_ptr(self._tab), ctypes.c_int(self.ncam),
+                                         _lib.host_ptr(conf))
+        if not h:
+            raise ValueError(_lib.load().fvv_last_error().decode(errors="replace"))
+        self._h = ctypes.c_void_p(h)
+        self._ranks = {}
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                _lib.load().fvv_frame_destroy(h)
+            except Exception:  # noqa: BLE001
+                pass
+            self._h = None
+
+    def _rank_pos(self, virtual):
+        from .render import rank_cameras
+
+        key = id(virtual)
+        hit = self._ranks.get(key)
+        if hit is None or hit[0] is not virtual:
+            pos = {c.id: i for i, c in enumerate(self.cams)}
+            arr = np.array([pos[i] for i in rank_cameras(virtual, self.cams)], dtype=np.int32)
+            hit = (virtual, arr)
+            self._ranks[key] = hit
+        return hit[1]
+
+    def run(self, masks, virtual=None, frames_buf=None, frame_off=None, fallback=None):
+        """masks: uint8 (N,H,W) (or flat) CUDA tensor in rig order; for the
+        colour pass, frames_buf (uint8 CUDA) + frame_off (int64 per camera)."""
+        from .pipeline import StageError
+        from .render import FALLBACK_COLOR
+
+        if masks.dtype == torch.bool:
+            masks = masks.view(torch.uint8)
+        masks = masks.reshape(-1)
+        stats = np.zeros(1, dtype=_lib.FRAME_STATS_DTYPE)
+        stage = ctypes.c_int(0)
+        if virtual is not None:
+            if frames_buf is None:
+                raise ValueError("the colour pass needs frames_buf/frame_off")
+            vt = cam_table([virtual])
+            rank = self._rank_pos(virtual)
+            fb = np.ascontiguousarray(np.asarray(
+                FALLBACK_COLOR if fallback is None else fallback, dtype=np.uint8).reshape(3))
+            args = (_lib.host_ptr(vt), _lib.host_ptr(rank), _lib.dev_ptr(frames_buf),
+                    _lib.host_ptr(np.ascontiguousarray(frame_off, dtype=np.int64)),
+                    _lib.host_ptr(fb))
+        else:
+            args = (ctypes.c_void_p(0),) * 5
+        rc = _lib.load().fvv_frame_run(self._h, _lib.dev_ptr(masks), *args, stream_handle(),
+                                       _lib.host_ptr(stats), ctypes.byref(stage))
+        if rc != 0:
+            msg = _lib.load().fvv_last_error().decode(errors="replace")
+            cause = ValueError(msg) if rc in (_lib.FVV_E_ARG, _lib.FVV_E_LIMIT) else \
+                _lib.FvvError(msg)
+            raise StageError(STAGE_NAMES.get(stage.value, "B-1 sparse carve"), cause)
+        outs = _lib.FrameOutputs()
+        _lib.load().fvv_frame_get_outputs(self._h, ctypes.byref(outs))
+        n = int(outs.n_rois)
+        cid = np.zeros(max(n, 1), dtype=np.int64)
+        boxes = np.zeros((max(n, 1), 6))
+        grids = np.zeros(max(n, 1), dtype=_lib.GRID_DTYPE)
+        info = np.zeros((max(n, 1), 8), dtype=np.int64)
+        _lib.load().fvv_frame_get_rois(self._h, _lib.host_ptr(cid), _lib.host_ptr(boxes),
+                                       _lib.host_ptr(grids), _lib.host_ptr(info))
+        return FrameOutput(stats[0], outs, (cid[:n], boxes[:n], grids[:n], info[:n]),
+                           self.ncam, virtual)
+
+
+_EXECUTORS = {}
+
+
+def executor_for(cfg, rig) -> FrameExecutor:
+    """Executors are cached per (config, rig parameters) so repeated
+    run_frame calls reuse the device buffers."""
+    from dataclasses import astuple
+
+    key = (astuple(cfg), cam_table(list(rig)).tobytes())
+    ex = _EXECUTORS.get(key)
+    if ex is None:
+        if len(_EXECUTORS) > 8:
+            _EXECUTORS.clear()
+        ex = FrameExecutor(cfg, rig)
+        _EXECUTORS[key] = ex
+    return ex

@@ -141,7 +141,9 @@ class FrameResult:
 
 
 def reconstruct(cfg: PipelineConfig, rig, dsils: DeviceSilhouettes, clock=None) -> FrameResult:
-    """B-1 .. D-2 on the GPU for one frame; outputs stay on the device."""
+    """B-1 .. D-2 for one frame composed from the per-stage public functions
+    (hull / mesh / visibility); outputs stay on the device. ``run_frame`` uses
+    the native executor (executor.py) instead; tests check the two agree."""
     r = FrameResult()
     clock = clock or _StageClock()
     cams = list(rig)
@@ -271,13 +273,97 @@ def compute_silhouettes(cfg, rig, frames, proposals, background):
                               "pass sils=")
 
 
+def _masks_on_device(rig, sils):
+    """Validate like hull.py:63-75 (_check_sils) and return the masks as one
+    uint8 CUDA tensor in rig order."""
+    dev = require_cuda()
+    cams = list(rig)
+    if isinstance(sils, DeviceSilhouettes):
+        if sils.ncam != len(cams):
+            raise ValueError(f"{sils.ncam} silhouettes for {len(cams)} cameras")
+        return sils._masks
+    if len(sils) != len(cams):
+        raise ValueError(f"{len(sils)} silhouettes for {len(cams)} cameras")
+    if isinstance(sils, torch.Tensor) and sils.dim() == 3:
+        shape = tuple(sils.shape[1:])
+        for c in cams:
+            if shape != (c.image_height, c.image_width):
+                raise ValueError(f"camera {c.id}: silhouette shape {shape} != "
+                                 f"({c.image_height}, {c.image_width})")
+        t = sils.view(torch.uint8) if sils.dtype == torch.bool else sils
+        return t.to(dev, non_blocking=True).reshape(-1)
+    parts = []
+    for c, s in zip(cams, sils):
+        if isinstance(s, torch.Tensor):
+            s = s.cpu().numpy()
+        s = np.asarray(s)
+        if s.shape != (c.image_height, c.image_width):
+            raise ValueError(f"camera {c.id}: silhouette shape {s.shape} != "
+                             f"({c.image_height}, {c.image_width})")
+        parts.append(np.ascontiguousarray(s if s.dtype == np.bool_ else s.astype(bool)))
+    out = torch.empty(sum(p.size for p in parts), dtype=torch.uint8, device=dev)
+    o = 0
+    for p in parts:
+        out[o:o + p.size].copy_(torch.from_numpy(p.reshape(-1).view(np.uint8)))
+        o += p.size
+    return out
+
+
+def bundle_from_output(out, host, cfg, rig, frames, frame_id=0, keep_depths=False,
+                       keep_device=True) -> SceneBundle:
+    """SceneBundle (bundle.py:55-74) from an executor run and its host copies."""
+    cams = list(rig)
+    stats = out.stats()
+    t = StageTimings()
+    for name, ms in zip(("sparse_carve", "noise_filter_roi", "dense_carve", "polygonize",
+                         "depth_images", "visibility"), out.stats_raw["ms"][:6]):
+        setattr(t, name, float(ms))
+    verts, tris = host["verts"], host["tris"]
+    meshes = []
+    for g, cid in enumerate(out.component_ids):
+        vb, nv, tb, nt = (int(out.info[g][k]) for k in (0, 1, 4, 5))
+        if nv == 0:
+            meshes.append(TriangleMesh.empty())
+            continue
+        meshes.append(TriangleMesh(verts[vb:vb + nv], tris[tb:tb + nt] - np.int32(vb),
+                                   np.full(nt, int(cid), dtype=np.int32)))
+    info = out.info
+    if len(info) == 0 or np.all((info[:, 1] == 0) | (info[:, 5] > 0)):
+        oids = np.repeat(out.component_ids.astype(np.int32), info[:, 5]) if len(info) else \
+            np.zeros(0, dtype=np.int32)
+        merged = TriangleMesh(verts if len(tris) else np.zeros((0, 3)), tris, oids)
+    else:
+        merged = TriangleMesh.concatenate(meshes)
+    nt = stats["triangles"]
+    vis = _LazyVisibility([c.id for c in cams], host["vis"], nt)
+    if keep_device and nt and len(merged.vertices) == out.nv:
+        merged._dev = (out.verts.clone(), out.tris.clone())
+        vis._device_bits = out.vis_bits.clone()
+    depths = {}
+    if keep_depths:
+        off = 0
+        for c in cams:
+            n = c.image_height * c.image_width
+            depths[c.id] = (host["depth"][off:off + n].reshape(c.image_height, c.image_width)
+                            if "depth" in host else
+                            np.full((c.image_height, c.image_width), np.inf))
+            off += n
+    bundle = SceneBundle(frame_id=frame_id, rig=rig, meshes=meshes,
+                         textures=dict(frames) if frames is not None else {}, visibility=vis,
+                         timings=t, stats=stats, stage_lo=np.array(cfg.stage_lo),
+                         stage_hi=np.array(cfg.stage_hi), depths=depths)
+    bundle._merged = merged
+    return bundle
+
+
 def run_frame(cfg: PipelineConfig, rig, frames: dict, sils=None, proposals: dict = None,
               background: dict = None, frame_id: int = 0, keep_depths: bool = False) -> SceneBundle:
     """Reconstruct one frame into a SceneBundle (pipeline.py:115-220) on the GPU.
 
-    ``sils`` may be the reference's list of (H, W) bool arrays, a stacked
-    (N, H, W) uint8/bool tensor (pinned host or device), or a
-    DeviceSilhouettes already resident on the GPU."""
+    Runs the native executor (csrc/frame.cu) for B-1 .. D-2 with the same
+    stage names, stats and errors as the reference. ``sils`` may be the
+    reference's list of (H, W) bool arrays, a stacked (N, H, W) uint8/bool
+    tensor (pinned host or CUDA) or a DeviceSilhouettes."""
     if sils is None:
         if proposals is None or background is None:
             raise StageError("silhouette", ValueError("need sils or proposals+background"))
@@ -285,13 +371,19 @@ def run_frame(cfg: PipelineConfig, rig, frames: dict, sils=None, proposals: dict
             sils = compute_silhouettes(cfg, rig, frames, proposals, background)
         except Exception as exc:
             raise StageError("silhouette", exc) from exc
+    from .executor import executor_for
+
+    cfg.coarse_spec()  # pipeline.py:151 validates the stage grid outside any stage
     try:
-        require_cuda()
-        dsils = sils if isinstance(sils, DeviceSilhouettes) else DeviceSilhouettes(rig, sils)
+        masks = _masks_on_device(rig, sils)
+        ex = executor_for(cfg, rig)
+    except StageError:
+        raise
     except Exception as exc:
         raise StageError("B-1 sparse carve", exc) from exc
-    r = reconstruct(cfg, rig, dsils)
-    return bundle_from(r, cfg, rig, frames, frame_id, keep_depths)
+    out = ex.run(masks)
+    host = out.to_host(list(rig), keep_depths)
+    return bundle_from_output(out, host, cfg, rig, frames, frame_id, keep_depths)
 
 
 def bundle_from(r: FrameResult, cfg, rig, frames, frame_id=0, keep_depths=False) -> SceneBundle:
@@ -402,7 +494,7 @@ def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
     asynchronous. Results come back in two transfers per frame. Yields
     (SceneBundle, RenderedImage or None) per frame, with the mesh, visibility
     flags and rendered image already on the host."""
-    from .render import FALLBACK_COLOR, RenderedImage, render_device
+    from .render import FALLBACK_COLOR, RenderedImage
 
     fallback_color = FALLBACK_COLOR if fallback_color is None else fallback_color
     require_cuda()
@@ -414,6 +506,9 @@ def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
         nxt = next(it)
     except StopIteration:
         return
+    from .executor import executor_for
+
+    ex = executor_for(cfg, rig)
     staged = _prefetch(cams, nxt[0], nxt[1], virtual is not None, copy, compute)
     fid = frame_id0
     while nxt is not None:
@@ -425,26 +520,15 @@ def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
             staged = _prefetch(cams, nxt[0], nxt[1], virtual is not None, copy, compute)
         except StopIteration:
             nxt = None
-        dsils = DeviceSilhouettes(cams, d_masks)
-        r = reconstruct(cfg, cams, dsils)
-        image = None
-        if virtual is not None and r.batch is not None and r.vis_bits is not None:
-            color, source, covered, _ = render_device(
-                r.batch.verts, r.batch.tris, int(r.batch.tris.shape[0]), cams, frames,
-                r.vis_bits, int(r.vis_bits.shape[1]), virtual, fallback_color,
-                nt_dev=r.batch.num_triangles_dev, frame_buf=frame_buf)
-            image = (color, source, covered)
-        himg = _readback(r, image)
-        bundle = bundle_from(r, cfg, rig, frames, fid)
+        if virtual is not None:
+            out = ex.run(d_masks, virtual, frame_buf[0], frame_buf[1], fallback_color)
+        else:
+            out = ex.run(d_masks)
+        host = out.to_host(cams)
+        bundle = bundle_from_output(out, host, cfg, rig, frames, fid, keep_device=False)
         img = None
         if virtual is not None:
-            h, w = virtual.image_height, virtual.image_width
-            if himg is None or bundle.stats["triangles"] == 0:
-                img = RenderedImage(np.zeros((h, w, 3), np.uint8), np.full((h, w), -1, np.int32),
-                                    np.zeros((h, w), bool))
-            else:
-                img = RenderedImage(himg[0], himg[1], himg[2].astype(bool))
-        bundle.merged_mesh.vertices  # noqa: B018  (host arrays are already cached)
+            img = RenderedImage(host["color"], host["source"], host["covered"].astype(bool))
         yield bundle, img
         fid += 1
 

@@ -99,3 +99,23 @@ def test_c2_judo_coarse_and_rois_match_oracle(gpu):
     assert len(rois) == len(ref_rois) >= 2
     for r, (lo, hi, cid) in zip(rois, ref_rois):
         assert np.array_equal(r.lo, lo) and np.array_equal(r.hi, hi) and r.component_id == cid
+
+
+def test_executor_matches_staged_composition(gpu):
+    """The native executor (run_frame) and the composition of the public
+    per-stage functions (pipeline.reconstruct) give identical frames."""
+    from paper_1903_11785_b200 import workloads
+    from paper_1903_11785_b200._device import DeviceSilhouettes
+    from paper_1903_11785_b200.pipeline import bundle_from, reconstruct, run_frame
+
+    wl = workloads.get("C3")
+    masks, _, frames = _inputs(wl, 4)
+    a = run_frame(wl.cfg, wl.rig, frames, sils=masks, keep_depths=True)
+    r = reconstruct(wl.cfg, wl.rig, DeviceSilhouettes(wl.rig, masks))
+    b = bundle_from(r, wl.cfg, wl.rig, frames, keep_depths=True)
+    assert a.stats == b.stats
+    assert np.array_equal(a.merged_mesh.vertices, b.merged_mesh.vertices)
+    assert np.array_equal(a.merged_mesh.triangles, b.merged_mesh.triangles)
+    for c in wl.rig:
+        assert np.array_equal(a.visibility[c.id], b.visibility[c.id])
+        assert np.array_equal(a.depths[c.id], b.depths[c.id])
