@@ -78,6 +78,17 @@ class TriangleMesh:
         self._nt = len(t)
 
     @classmethod
+    def _trusted(cls, vertices, triangles, object_ids, dev=None):
+        """Wrap kernel outputs without re-validating them (they come from
+        the mesh kernels, whose indices are in range by construction)."""
+        m = cls.__new__(cls)
+        m._v, m._t, m._o = vertices, triangles, object_ids
+        m._nt = len(triangles)
+        m._loader = None
+        m._dev = dev
+        return m
+
+    @classmethod
     def _lazy(cls, num_triangles, loader, dev=None):
         m = cls.__new__(cls)
         m._v = m._t = m._o = None

@@ -325,13 +325,17 @@ def bundle_from_output(out, host, cfg, rig, frames, frame_id=0, keep_depths=Fals
         if nv == 0:
             meshes.append(TriangleMesh.empty())
             continue
-        meshes.append(TriangleMesh(verts[vb:vb + nv], tris[tb:tb + nt] - np.int32(vb),
-                                   np.full(nt, int(cid), dtype=np.int32)))
+
+        def load(vb=vb, nv=nv, tb=tb, nt=nt, cid=cid):  # per-ROI views, built on access
+            return (verts[vb:vb + nv], tris[tb:tb + nt] - np.int32(vb),
+                    np.full(nt, int(cid), dtype=np.int32))
+
+        meshes.append(TriangleMesh._lazy(nt, load))
     info = out.info
     if len(info) == 0 or np.all((info[:, 1] == 0) | (info[:, 5] > 0)):
         oids = np.repeat(out.component_ids.astype(np.int32), info[:, 5]) if len(info) else \
             np.zeros(0, dtype=np.int32)
-        merged = TriangleMesh(verts if len(tris) else np.zeros((0, 3)), tris, oids)
+        merged = TriangleMesh._trusted(verts if len(tris) else np.zeros((0, 3)), tris, oids)
     else:
         merged = TriangleMesh.concatenate(meshes)
     nt = stats["triangles"]

@@ -16,13 +16,5 @@ def run(n):
         b.merged_mesh.triangles
 run(3); torch.cuda.synchronize()
 t = time.perf_counter(); run(20); torch.cuda.synchronize(); print("e2e ms/frame", (time.perf_counter() - t) / 20 * 1e3)
-# raw copy bandwidth
-x = host[0][0]; d = torch.empty_like(x, device="cuda")
-torch.cuda.synchronize(); t = time.perf_counter()
-for _ in range(10): d.copy_(x, non_blocking=True)
-torch.cuda.synchronize(); print("H2D GB/s", 10 * x.numel() / (time.perf_counter() - t) / 1e9)
-y = torch.empty(x.numel(), dtype=torch.uint8).pin_memory(); torch.cuda.synchronize(); t = time.perf_counter()
-for _ in range(10): y.copy_(d.reshape(-1), non_blocking=True)
-torch.cuda.synchronize(); print("D2H GB/s", 10 * x.numel() / (time.perf_counter() - t) / 1e9)
 pr = cProfile.Profile(); pr.enable(); run(10); torch.cuda.synchronize(); pr.disable()
-pstats.Stats(pr).sort_stats("tottime").print_stats(22)
+pstats.Stats(pr).sort_stats("tottime").print_stats(15)
