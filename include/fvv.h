@@ -228,6 +228,29 @@ int fvv_render_view(const fvv_camera *rig, int ncam, const uint8_t *frames_dev,
 int fvv_back_project(const fvv_camera *cam, const double *pixel_dev, const double *depth_dev,
                      int64_t n, double *out_dev, void *stream);
 
+/* ---- silhouettes: silhouette.py:59-109 (upstream of the hot path) ---- */
+
+/* silhouette.py:59-69 distance_map of one (H, W) uint8 proposal: exact
+ * squared Euclidean distance to the nearest proposal pixel (int32,
+ * INT32_MAX when the proposal is empty) and, when dm_dev != NULL, its
+ * float64 sqrt (+inf when empty) = scipy distance_transform_edt(~prop).
+ * ws_dev: int32 scratch of H*W. */
+int fvv_distance_map(const uint8_t *prop_dev, int64_t H, int64_t W, int32_t *sqdist_dev,
+                     double *dm_dev, int32_t *ws_dev, void *stream);
+
+/* silhouette.py:72-87 build_background: per element of n = H*W*C, mean and
+ * population std (floor 2.0) over K uint8 frames stacked frame-major. */
+int fvv_background(const uint8_t *frames_dev, int64_t K, int64_t n, double *mean_dev,
+                   double *std_dev, void *stream);
+
+/* silhouette.py:90-109 extract_silhouette with AdaptiveParams.threshold:
+ * uint8 mask = max_c |frame - mean| / std > theta(distance). Distances from
+ * dm_dev (float64) when non-NULL, else from fvv_distance_map's sqdist_dev. */
+int fvv_extract_silhouette(const uint8_t *frame_dev, const double *mean_dev,
+                           const double *std_dev, int64_t npx, int C, const int32_t *sqdist_dev,
+                           const double *dm_dev, double theta_near, double theta_far,
+                           double d_max, uint8_t *mask_dev, void *stream);
+
 /* ---- native frame executor: pipeline.py:115-220 run_frame + render.py:64-113 ---- */
 
 typedef struct fvv_frame fvv_frame;

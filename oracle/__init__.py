@@ -396,3 +396,49 @@ def run_frame(rig, sils, stage_lo, stage_hi, coarse_spacing, fine_spacing, min_v
     if keep_depths:
         out["depths"] = depths
     return out
+
+
+# -------------------------------------------------------------- silhouette
+STD_FLOOR = 2.0  # silhouette.py:18
+
+
+def distance_map(proposal):
+    """silhouette.py:59-69."""
+    prop = np.ascontiguousarray(np.asarray(proposal, dtype=bool)).view(np.uint8)
+    if prop.ndim != 2:
+        raise ValueError("proposal mask must be 2D")
+    out = np.empty(prop.shape)
+    if lib().or_distance_map(_p(prop), ctypes.c_int64(prop.shape[0]),
+                             ctypes.c_int64(prop.shape[1]), _p(out)):
+        return np.full(prop.shape, np.inf)
+    return out
+
+
+def build_background(frames):
+    """silhouette.py:72-87 -> (mean, std) float64 (H, W, C)."""
+    if len(frames) < 2:
+        raise ValueError("need at least 2 background frames")
+    stack = [np.asarray(f) for f in frames]
+    stack = [f[:, :, None] if f.ndim == 2 else f for f in stack]
+    arr = np.ascontiguousarray(np.stack(stack).astype(np.uint8))
+    n = arr[0].size
+    mean = np.empty(arr[0].shape)
+    std = np.empty(arr[0].shape)
+    lib().or_background(_p(arr), ctypes.c_int64(len(arr)), ctypes.c_int64(n), _p(mean), _p(std))
+    return mean, std
+
+
+def extract_silhouette(frame, mean, std, dm, theta_near=3.0, theta_far=8.0, d_max=32.0):
+    """silhouette.py:90-109."""
+    img = np.asarray(frame)
+    if img.ndim == 2:
+        img = img[:, :, None]
+    img = np.ascontiguousarray(img.astype(np.uint8))
+    h, w, c = img.shape
+    out = np.zeros((h, w), dtype=np.uint8)
+    lib().or_extract(_p(img), _p(np.ascontiguousarray(mean, dtype=np.float64)),
+                     _p(np.ascontiguousarray(std, dtype=np.float64)),
+                     _p(np.ascontiguousarray(dm, dtype=np.float64)), ctypes.c_int64(h * w),
+                     ctypes.c_int64(c), ctypes.c_double(theta_near), ctypes.c_double(theta_far),
+                     ctypes.c_double(d_max), _p(out))
+    return out.astype(bool)

@@ -679,3 +679,87 @@ OR_HOT void or_render(const double *verts, int64_t nv, const int32_t *tris, int6
     free(depth);
     free(tid);
 }
+
+/* ------------------------------------------------------------ silhouette */
+
+/* silhouette.py:59-69 distance_map: exact Euclidean distance to the nearest
+ * proposal pixel (scipy.ndimage.distance_transform_edt(~prop)), computed as
+ * sqrt of the exact integer squared distance. Independent algorithm from the
+ * GPU kernels: per-column nearest feature, then per row the brute-force
+ * minimum over candidate columns pruned by the running best. Returns 0, or 1
+ * when the proposal is empty (caller fills +inf, silhouette.py:67-68). */
+OR_HOT int or_distance_map(const uint8_t *prop, int64_t H, int64_t W, double *out) {
+    int64_t nfg = 0;
+    for (int64_t p = 0; p < H * W; ++p) nfg += prop[p] != 0;
+    if (!nfg) return 1;
+    const int64_t INF = (int64_t)1 << 40;
+    int64_t *g = (int64_t *)malloc((size_t)(H * W) * sizeof(int64_t)); /* squared vertical */
+#pragma omp parallel for schedule(static)
+    for (int64_t x = 0; x < W; ++x) {
+        int64_t last = -1;
+        for (int64_t y = 0; y < H; ++y) {
+            if (prop[y * W + x]) last = y;
+            g[y * W + x] = last < 0 ? INF : (y - last) * (y - last);
+        }
+        last = -1;
+        for (int64_t y = H - 1; y >= 0; --y) {
+            if (prop[y * W + x]) last = y;
+            if (last >= 0) {
+                int64_t d = (last - y) * (last - y);
+                if (d < g[y * W + x]) g[y * W + x] = d;
+            }
+        }
+    }
+#pragma omp parallel for schedule(dynamic, 8)
+    for (int64_t y = 0; y < H; ++y) {
+        const int64_t *gr = g + y * W;
+        for (int64_t x = 0; x < W; ++x) {
+            int64_t best = gr[x];
+            for (int64_t r = 1; r < W && r * r < best; ++r) {
+                if (x - r >= 0 && gr[x - r] + r * r < best) best = gr[x - r] + r * r;
+                if (x + r < W && gr[x + r] + r * r < best) best = gr[x + r] + r * r;
+            }
+            out[y * W + x] = sqrt((double)best);
+        }
+    }
+    free(g);
+    return 0;
+}
+
+/* silhouette.py:72-87 build_background: numpy reduces axis 0 of the
+ * (K, H, W, C) float64 stack sequentially; population std, floor 2.0. */
+OR_HOT void or_background(const uint8_t *frames, int64_t K, int64_t n, double *mean, double *std_) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        double s = (double)frames[i];
+        for (int64_t k = 1; k < K; ++k) s = s + (double)frames[k * n + i];
+        const double m = s / (double)K;
+        double v = 0.0;
+        for (int64_t k = 0; k < K; ++k) {
+            const double d = (double)frames[k * n + i] - m;
+            v = (k == 0) ? d * d : v + d * d;
+        }
+        const double sd = sqrt(v / (double)K);
+        mean[i] = m;
+        std_[i] = sd > 2.0 ? sd : 2.0; /* silhouette.py:86 np.maximum(std, STD_FLOOR) */
+    }
+}
+
+/* silhouette.py:90-109 extract_silhouette. */
+OR_HOT void or_extract(const uint8_t *frame, const double *mean, const double *std_,
+                       const double *dm, int64_t npx, int64_t C, double theta_near,
+                       double theta_far, double d_max, uint8_t *out) {
+#pragma omp parallel for schedule(static)
+    for (int64_t p = 0; p < npx; ++p) {
+        double dev = -INFINITY;
+        for (int64_t c = 0; c < C; ++c) {
+            const double x = (double)frame[p * C + c];
+            const double d = fabs(x - mean[p * C + c]) / std_[p * C + c];
+            if (d > dev || isnan(d)) dev = d;
+        }
+        double t = dm[p] / d_max;
+        t = t < 1.0 ? t : 1.0; /* np.minimum(d / d_max, 1.0) */
+        const double thr = theta_near + (theta_far - theta_near) * t;
+        out[p] = dev > thr;
+    }
+}

@@ -45,7 +45,7 @@ SYMBOLS = (
     "fvv_raster_workspace_bytes", "fvv_rasterize", "fvv_classify", "fvv_triangle_sources",
     "fvv_render_count", "fvv_render_view", "fvv_back_project", "fvv_render_ellipsoids",
     "fvv_frame_create", "fvv_frame_destroy", "fvv_frame_run", "fvv_frame_get_outputs",
-    "fvv_frame_get_rois",
+    "fvv_frame_get_rois", "fvv_distance_map", "fvv_background", "fvv_extract_silhouette",
 )
 
 FRAME_CONFIG_DTYPE = np.dtype([("stage_lo", "<f8", (3,)), ("stage_hi", "<f8", (3,)),

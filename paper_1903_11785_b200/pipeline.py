@@ -28,6 +28,7 @@ from ._device import DeviceSilhouettes, require_cuda
 from .bundle import SceneBundle, StageTimings
 from .hull import NoiseFilterParams, Roi, carve_grids, finish_labels, label_grid_async
 from .mesh import TriangleMesh, polygonize_grids
+from .silhouette import AdaptiveParams, silhouettes_device
 from .visibility import bits_to_flags, classify_bits, raster_planes
 from .voxels import GridSpec
 
@@ -39,16 +40,6 @@ class StageError(RuntimeError):
         super().__init__(f"[{stage}] {cause}")
         self.stage = stage
         self.cause = cause
-
-
-@dataclass
-class AdaptiveParams:
-    """Silhouette-extraction thresholds (silhouette.py); carried for config
-    parity - extraction itself is upstream of this hot path."""
-
-    theta_near: float = 3.0
-    theta_far: float = 8.0
-    d_max: float = 32.0
 
 
 @dataclass
@@ -267,10 +258,17 @@ class _LazyVisibility(dict):
 
 
 def compute_silhouettes(cfg, rig, frames, proposals, background):
-    """Adaptive silhouette extraction (silhouette.py) sits upstream of this
-    hot path and is not rebuilt yet."""
-    raise NotImplementedError("silhouette extraction is not part of the B200 hot path yet; "
-                              "pass sils=")
+    """Adaptive silhouette extraction for every camera (pipeline.py:104-112),
+    on the GPU (silhouette.py kernels); returns the reference's list of
+    (H, W) bool masks in rig order."""
+    masks = silhouettes_device(rig, frames, proposals, background, cfg.adaptive_params).cpu()
+    out, off = [], 0
+    for cam in rig:
+        n = cam.image_height * cam.image_width
+        out.append(masks[off:off + n].numpy().astype(bool).reshape(cam.image_height,
+                                                                   cam.image_width))
+        off += n
+    return out
 
 
 def _masks_on_device(rig, sils):
@@ -282,6 +280,10 @@ def _masks_on_device(rig, sils):
         if sils.ncam != len(cams):
             raise ValueError(f"{sils.ncam} silhouettes for {len(cams)} cameras")
         return sils._masks
+    if isinstance(sils, torch.Tensor) and sils.dim() == 1:  # flat, rig order (internal)
+        if sils.numel() != sum(c.image_height * c.image_width for c in cams):
+            raise ValueError("flat silhouette buffer does not match the rig's image sizes")
+        return sils.to(dev, non_blocking=True)
     if len(sils) != len(cams):
         raise ValueError(f"{len(sils)} silhouettes for {len(cams)} cameras")
     if isinstance(sils, torch.Tensor) and sils.dim() == 3:
@@ -371,8 +373,8 @@ def run_frame(cfg: PipelineConfig, rig, frames: dict, sils=None, proposals: dict
     if sils is None:
         if proposals is None or background is None:
             raise StageError("silhouette", ValueError("need sils or proposals+background"))
-        try:
-            sils = compute_silhouettes(cfg, rig, frames, proposals, background)
+        try:  # silhouettes stay on the GPU (flat, rig order) and feed the carve
+            sils = silhouettes_device(rig, frames, proposals, background, cfg.adaptive_params)
         except Exception as exc:
             raise StageError("silhouette", exc) from exc
     from .executor import executor_for

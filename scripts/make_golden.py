@@ -316,7 +316,53 @@ def fixture_raster():
          tri_id=ras.tri_id, vis=vis, one_verts=tris[0], one_vis=vis1)
 
 
+def fixture_silhouette():
+    """silhouette.py (distance_map, build_background, extract_silhouette) and
+    run_frame's proposal path (pipeline.py:104-112, 130-137) on a small
+    scene generated by the reference's own scenes.generate_scene."""
+    from freeview import silhouette as fsil
+
+    objects = fscenes.objects_from_spec([
+        {"type": "sphere", "center": [-250, 0, 450], "radius": 220},
+        {"type": "box", "lo": [150, -150, 250], "hi": [450, 150, 650]},
+    ])
+    rig = fscenes.default_rig_from_spec({"n_cameras": 4, "target": [0, 0, 450],
+                                         "ring_radius": 3200, "height": 1200, "width": 128,
+                                         "image_height": 96, "focal": 110})
+    cfg = fpipe.PipelineConfig(stage_lo=(-1000, -1000, 0), stage_hi=(1000, 1000, 1000),
+                               coarse_spacing=80.0, fine_spacing=40.0, t_small=3)
+    _, frames, proposals, _, bg_frames = fscenes.generate_scene(objects, rig, cfg,
+                                                                noise_sigma=2.0, seed=5)
+    arrays = dict(rig=rig_json(rig), cfg=json.dumps({k: (None if (k == "t_large" and np.isinf(v))
+                                                         else v) for k, v in cfg.__dict__.items()}))
+    for i, c in enumerate(rig):
+        bg = fsil.build_background(bg_frames[c.id])
+        dm = fsil.distance_map(proposals[c.id])
+        sil = fsil.extract_silhouette(frames[c.id], bg, dm, cfg.adaptive_params)
+        arrays[f"frame{i}"] = frames[c.id]
+        arrays[f"prop{i}"] = pack(proposals[c.id])
+        arrays[f"bgframes{i}"] = np.stack(bg_frames[c.id])
+        arrays[f"dm{i}"] = dm
+        arrays[f"sil{i}"] = pack(sil)
+        if i < 2:
+            arrays[f"bgmean{i}"], arrays[f"bgstd{i}"] = bg.mean, bg.std
+    # edge cases: empty proposal, full proposal, single pixel
+    arrays["dm_empty"] = fsil.distance_map(np.zeros((5, 7), dtype=bool))
+    one = np.zeros((40, 50), dtype=bool)
+    one[3, 47] = True
+    arrays["dm_one"] = fsil.distance_map(one)
+    rng = np.random.default_rng(9)
+    rnd = rng.random((61, 83)) < 0.03
+    arrays["rnd_prop"] = pack(rnd)
+    arrays["dm_rnd"] = fsil.distance_map(rnd)
+    background = {c.id: fsil.build_background(bg_frames[c.id]) for c in rig}
+    bundle = fpipe.run_frame(cfg, rig, frames, proposals=proposals, background=background)
+    arrays["stats"] = json.dumps(bundle.stats)
+    save("silhouette", **arrays)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["tiny_cli", "spheres", "distorted", "ccl", "raster", "figures"]
+    which = sys.argv[1:] or ["tiny_cli", "spheres", "distorted", "ccl", "raster", "figures",
+                             "silhouette"]
     for w in which:
         globals()[f"fixture_{w}"]()

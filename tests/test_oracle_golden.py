@@ -156,3 +156,27 @@ def test_raster_ties_winding_and_visibility():
     one = z["one_verts"]
     d1, _ = O.rasterize(one, [[0, 1, 2]], cam)
     assert np.array_equal(O.classify(one, [[0, 1, 2]], cam, d1, 10.0), z["one_vis"])
+
+
+def test_silhouette_extraction_matches_reference():
+    """silhouette.py: exact EDT, background statistics, adaptive threshold."""
+    z = G.load("silhouette")
+    rig = G.rig(z)
+    cfg = json.loads(str(z["cfg"]))
+    for i, c in enumerate(rig):
+        h, w = c.image_height, c.image_width
+        prop = G.unpack(z[f"prop{i}"], h * w).reshape(h, w)
+        dm = O.distance_map(prop)
+        assert np.array_equal(dm, z[f"dm{i}"]), i
+        mean, std = O.build_background(list(z[f"bgframes{i}"]))
+        if i < 2:
+            assert np.array_equal(mean, z[f"bgmean{i}"]) and np.array_equal(std, z[f"bgstd{i}"])
+        sil = O.extract_silhouette(z[f"frame{i}"], mean, std, dm, cfg["theta_near"],
+                                   cfg["theta_far"], cfg["d_max"])
+        assert np.array_equal(sil, G.unpack(z[f"sil{i}"], h * w).reshape(h, w)), i
+    assert np.all(np.isinf(O.distance_map(np.zeros((5, 7), bool))))
+    one = np.zeros((40, 50), dtype=bool)
+    one[3, 47] = True
+    assert np.array_equal(O.distance_map(one), z["dm_one"])
+    rnd = G.unpack(z["rnd_prop"], 61 * 83).reshape(61, 83)
+    assert np.array_equal(O.distance_map(rnd), z["dm_rnd"])
