@@ -316,6 +316,40 @@ def fixture_raster():
          tri_id=ras.tri_id, vis=vis, one_verts=tris[0], one_vis=vis1)
 
 
+def fixture_bundle():
+    """write_bundle (bundle.py:77-136, meshio.py, imgio.py) of the TINY_SPEC
+    frame: sha256 of every file except the non-deterministic timings.json."""
+    import hashlib
+
+    from freeview.bundle import write_bundle
+
+    z = np.load(os.path.join(OUT, "tiny_cli.npz"))
+    rig = fcam.CameraRig([fcam.CameraModel.from_dict(d)
+                          for d in json.loads(str(z["rig"]))["cameras"]])
+    shapes = z["sil_shapes"]
+    sils = [np.unpackbits(z["sils"][i], bitorder="little")[:h * w].astype(bool).reshape(h, w)
+            for i, (h, w) in enumerate(shapes)]
+    d = json.loads(str(z["cfg"]))
+    d["t_large"] = float("inf") if d["t_large"] is None else d["t_large"]
+    cfg = fpipe.PipelineConfig(**{k: (tuple(v) if isinstance(v, list) else v) for k, v in d.items()})
+    frames = {c.id: z["frames"][i] for i, c in enumerate(rig)}
+    bundle = fpipe.run_frame(cfg, rig, frames, sils=sils, frame_id=7, keep_depths=True)
+    hashes = {}
+    with tempfile.TemporaryDirectory() as tmp:
+        write_bundle(bundle, tmp, export_depth=True)
+        for root, _, files in os.walk(tmp):
+            for fn in files:
+                rel = os.path.relpath(os.path.join(root, fn), tmp)
+                if rel == "timings.json":
+                    continue
+                with open(os.path.join(root, fn), "rb") as fh:
+                    hashes[rel] = hashlib.sha256(fh.read()).hexdigest()
+    with open(os.path.join(OUT, "bundle_sha256.json"), "w") as fh:
+        json.dump(dict(sorted(hashes.items())), fh, indent=1)
+        fh.write("\n")
+    print(f"bundle hashes: {len(hashes)} files")
+
+
 def fixture_silhouette():
     """silhouette.py (distance_map, build_background, extract_silhouette) and
     run_frame's proposal path (pipeline.py:104-112, 130-137) on a small
@@ -363,6 +397,6 @@ def fixture_silhouette():
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["tiny_cli", "spheres", "distorted", "ccl", "raster", "figures",
-                             "silhouette"]
+                             "silhouette", "bundle"]
     for w in which:
         globals()[f"fixture_{w}"]()
