@@ -71,25 +71,38 @@ class FrameOutput:
         total = sum(c.image_height * c.image_width for c in cams)
         return _dev(self.depth_ptr, (total,), "<f8")
 
-    def to_host(self, cams, keep_depths=False):
-        """Pinned D2H of vertices, triangles, visibility bits, the rendered
-        image (and depth planes) with one synchronisation."""
+    def to_host_async(self, cams, keep_depths=False, stream=None):
+        """Queue pinned D2H copies of vertices, triangles, visibility bits,
+        the rendered image (and depth planes) on ``stream`` (default: the
+        current stream, after this frame's work). Returns (pinned dict,
+        completion event)."""
         pinned = {}
+        cur = torch.cuda.current_stream()
+        stream = stream or cur
+        if stream is not cur:
+            stream.wait_stream(cur)
+        with torch.cuda.stream(stream):
+            def fetch(name, t):
+                h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+                h.copy_(t, non_blocking=True)
+                pinned[name] = h
 
-        def fetch(name, t):
-            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-            h.copy_(t, non_blocking=True)
-            pinned[name] = h
+            fetch("verts", self.verts)
+            fetch("tris", self.tris)
+            fetch("vis", self.vis_bits)
+            if self.image is not None:
+                for n, t in zip(("color", "source", "covered"), self.image):
+                    fetch(n, t)
+            if keep_depths and self.nt:
+                fetch("depth", self.depth_planes(cams))
+            ev = torch.cuda.Event()
+            ev.record(stream)
+        return pinned, ev
 
-        fetch("verts", self.verts)
-        fetch("tris", self.tris)
-        fetch("vis", self.vis_bits)
-        if self.image is not None:
-            for n, t in zip(("color", "source", "covered"), self.image):
-                fetch(n, t)
-        if keep_depths and self.nt:
-            fetch("depth", self.depth_planes(cams))
-        torch.cuda.current_stream().synchronize()
+    def to_host(self, cams, keep_depths=False):
+        """Pinned D2H of every host-facing output, one synchronisation."""
+        pinned, ev = self.to_host_async(cams, keep_depths)
+        ev.synchronize()
         return {k: v.numpy() for k, v in pinned.items()}
 
 

@@ -512,11 +512,26 @@ def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
         nxt = next(it)
     except StopIteration:
         return
-    from .executor import executor_for
+    from .executor import FrameExecutor, executor_for
 
-    ex = executor_for(cfg, rig)
+    # two executors alternate, so frame f's results can stream back on the
+    # copy stream while frame f+1 computes into the other one's buffers
+    exs = [executor_for(cfg, rig), FrameExecutor(cfg, rig)]
     staged = _prefetch(cams, nxt[0], nxt[1], virtual is not None, copy, compute)
     fid = frame_id0
+    pending = None  # (frames, output, pinned, event, frame id) of the previous frame
+
+    def finish(p):
+        p_frames, p_out, p_pinned, p_ev, p_fid = p
+        p_ev.synchronize()
+        host = {k: v.numpy() for k, v in p_pinned.items()}
+        bundle = bundle_from_output(p_out, host, cfg, rig, p_frames, p_fid, keep_device=False)
+        img = None
+        if virtual is not None:
+            img = RenderedImage(host["color"], host["source"], host["covered"].astype(bool))
+        return bundle, img
+
+    k = 0
     while nxt is not None:
         frames, _ = nxt
         d_masks, frame_buf, ev = staged
@@ -526,17 +541,19 @@ def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
             staged = _prefetch(cams, nxt[0], nxt[1], virtual is not None, copy, compute)
         except StopIteration:
             nxt = None
+        ex = exs[k % 2]
         if virtual is not None:
             out = ex.run(d_masks, virtual, frame_buf[0], frame_buf[1], fallback_color)
         else:
             out = ex.run(d_masks)
-        host = out.to_host(cams)
-        bundle = bundle_from_output(out, host, cfg, rig, frames, fid, keep_device=False)
-        img = None
-        if virtual is not None:
-            img = RenderedImage(host["color"], host["source"], host["covered"].astype(bool))
-        yield bundle, img
+        pinned, dev_ev = out.to_host_async(cams, stream=copy)
+        if pending is not None:
+            yield finish(pending)
+        pending = (frames, out, pinned, dev_ev, fid)
         fid += 1
+        k += 1
+    if pending is not None:
+        yield finish(pending)
 
 
 def sweep(cfg: PipelineConfig, rig, sils, axis: str, values) -> list:
