@@ -68,6 +68,13 @@ int fvv_version(void);
 /* Number of kernels this library has launched (all entry points). */
 long long fvv_launch_count(void);
 
+/* Stage n host (or device) buffers back to back into dst on `stream`
+ * (cudaMemcpyAsync per piece, direction inferred through UVA): one frame's
+ * silhouettes or colour frames in a single call (pipeline.py:150-200 hands
+ * the reference per-camera arrays). Pinned sources copy asynchronously. */
+int fvv_copy_gather(const void *const *src, const int64_t *bytes, int64_t n, void *dst,
+                    void *stream);
+
 /* camera.py:164-201 project(cam, p, use_distortion) for n points (float64
  * (n,3)); writes pixel (n,2), camera-frame z (n,), in_frustum (n,) 0/1.
  * single_point selects numpy's 1-row BLAS order. */

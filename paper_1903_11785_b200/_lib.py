@@ -37,7 +37,7 @@ assert CAM_DTYPE.itemsize == 192 and GRID_DTYPE.itemsize == 56 and COMP_DTYPE.it
 
 # exported symbols; tests check the .so exports every one of them
 SYMBOLS = (
-    "fvv_last_error", "fvv_version", "fvv_launch_count", "fvv_project",
+    "fvv_last_error", "fvv_version", "fvv_launch_count", "fvv_copy_gather", "fvv_project",
     "fvv_pack_silhouettes", "fvv_carve", "fvv_ccl_workspace_bytes", "fvv_ccl26",
     "fvv_ccl_components", "fvv_ccl_labels", "fvv_filter_labels", "fvv_filter_dense",
     "fvv_mesh_workspace_bytes", "fvv_mesh_prepare", "fvv_mesh_counts",

@@ -112,6 +112,27 @@ int fvv_version(void) { return 1; }
 
 long long fvv_launch_count(void) { return g_launches.load(); }
 
+int fvv_copy_gather(const void *const *src, const int64_t *bytes, int64_t n, void *dst,
+                    void *stream) {
+  if (n < 0 || (n > 0 && (!src || !bytes || !dst))) {
+    set_error("fvv_copy_gather: bad arguments");
+    return FVV_E_ARG;
+  }
+  char *d = static_cast<char *>(dst);
+  for (int64_t i = 0; i < n; ++i) {
+    if (bytes[i] < 0 || (bytes[i] > 0 && !src[i])) {
+      set_error("fvv_copy_gather: piece %lld has no data", (long long)i);
+      return FVV_E_ARG;
+    }
+    if (bytes[i] &&
+        cudaMemcpyAsync(d, src[i], (size_t)bytes[i], cudaMemcpyDefault,
+                        (cudaStream_t)stream) != cudaSuccess)
+      return cuda_check("fvv_copy_gather");
+    d += bytes[i];
+  }
+  return FVV_OK;
+}
+
 int fvv_project(const fvv_camera *cam, const double *pts_dev, int64_t n, int use_distortion,
                 int single_point, double *pixel_dev, double *z_dev, uint8_t *in_dev,
                 void *stream) {

@@ -11,6 +11,7 @@
 // vertex/cell counts (to size the mesh outputs) and the final counters.
 #include <cmath>
 #include <cstring>
+#include <initializer_list>
 #include <vector>
 
 #include "fvv_common.cuh"
@@ -86,9 +87,45 @@ __global__ void offset_tris_kernel(int32_t *tris, int64_t n3, int32_t add) {
     tris[i] += add;
 }
 
+// Small results reach the host without a copy engine: one kernel stores
+// them straight into mapped pinned memory. (A cudaMemcpyAsync would queue
+// behind the multi-MB frame transfers run_sequence keeps on the copy
+// engines, stalling every host synchronisation of the next frame.)
+struct ReadPiece {
+  const int64_t *src;
+  int64_t *dst;          // device alias of mapped host memory
+  const int64_t *count;  // optional device element count (clamped to max_elems)
+  int64_t words;         // words to copy when count == nullptr
+  int64_t elem_words, max_elems;
+};
+struct ReadBatch {
+  ReadPiece p[4];
+};
+
+__global__ void readback_kernel(ReadBatch B) {
+  const int y = blockIdx.y;
+  const int64_t *src = B.p[y].src;
+  int64_t *dst = B.p[y].dst;
+  int64_t w = B.p[y].words;
+  if (B.p[y].count) {
+    int64_t c = __ldcg(B.p[y].count);
+    c = c < 0 ? 0 : (c > B.p[y].max_elems ? B.p[y].max_elems : c);
+    w = c * B.p[y].elem_words;
+  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < w;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __ldcg(src + i);
+}
+
 }  // namespace fvv
 
 using namespace fvv;
+
+// byte offsets inside the mapped host block
+constexpr size_t kHsComps = 32;           // up to 4096 components (256 KB)
+constexpr size_t kHsInfo = 512 * 1024;    // mesh_info of one ROI batch (64 B x 128)
+constexpr size_t kHsCntF = 640 * 1024;    // per-ROI dense counts
+constexpr int64_t kHsMaxCntF = 8192;
 
 struct fvv_frame {
   std::vector<fvv_camera> cams, cams_by_id;
@@ -102,7 +139,8 @@ struct fvv_frame {
       mesh_totals, mesh_info, verts, tris, ntri, raster_ws, depth, vis, vplane_d, vplane_id,
       vraster_ws, src, rcounts, color, source, covered;
   // pinned host staging
-  void *host_small = nullptr;
+  void *host_small = nullptr;  // mapped pinned block (kHs* layout)
+  void *host_small_dev = nullptr;
   size_t host_small_cap = 0;
   // results of the last run
   std::vector<fvv_grid> fine;
@@ -145,13 +183,45 @@ static int host_small_ensure(fvv_frame *f, size_t bytes) {
   if (f->host_small) cudaFreeHost(f->host_small);
   f->host_small = nullptr;
   size_t want = bytes * 2 + 4096;
-  if (cudaMallocHost(&f->host_small, want) != cudaSuccess) {
+  if (cudaHostAlloc(&f->host_small, want, cudaHostAllocMapped | cudaHostAllocPortable) !=
+          cudaSuccess ||
+      cudaHostGetDevicePointer(&f->host_small_dev, f->host_small, 0) != cudaSuccess) {
     cudaGetLastError();
-    set_error("frame executor: cudaMallocHost failed");
+    set_error("frame executor: mapped host allocation failed");
     return FVV_E_CUDA;
   }
   f->host_small_cap = want;
   return FVV_OK;
+}
+
+// Queue up to four device->host pieces (dst given as offsets into the
+// mapped block) in one launch.
+struct HostPiece {
+  const void *src;
+  size_t dst_off;
+  int64_t bytes;            // fixed size, or
+  const int64_t *count;     // device element count ...
+  int64_t elem_bytes, max;  // ... of elem_bytes each, at most max
+};
+static void readback(fvv_frame *f, cudaStream_t st, std::initializer_list<HostPiece> pieces) {
+  ReadBatch b{};
+  int n = 0;
+  int64_t most = 0;
+  for (const HostPiece &h : pieces) {
+    ReadPiece &r = b.p[n++];
+    r.src = (const int64_t *)h.src;
+    r.dst = (int64_t *)((char *)f->host_small_dev + h.dst_off);
+    r.count = h.count;
+    r.words = h.bytes / 8;
+    r.elem_words = h.elem_bytes / 8;
+    r.max_elems = h.max;
+    const int64_t w = h.count ? h.max * r.elem_words : r.words;
+    most = w > most ? w : most;
+  }
+  int64_t bx = (most + 255) / 256;
+  bx = bx < 1 ? 1 : (bx > 32 ? 32 : bx);
+  readback_kernel<<<dim3((unsigned)bx, (unsigned)n), 256, 0, st>>>(b);
+  note_launches(1);
 }
 
 #define FVV_TRY(stage, expr)                     \
@@ -248,9 +318,10 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
   FVV_TRY(2, fvv_ccl26(f->occ_c.as<uint32_t>(), &G, f->ccl_ws.p, f->ccl_ws.cap,
                        f->comps.as<fvv_component>(), 4096, f->ccl_counts.as<int64_t>(), st));
   int64_t *hs = (int64_t *)f->host_small;
-  cudaMemcpyAsync(hs, f->ccl_counts.p, 16, cudaMemcpyDeviceToHost, st);
-  cudaMemcpyAsync(hs + 2, f->cnt_c.p, 8, cudaMemcpyDeviceToHost, st);
-  cudaMemcpyAsync(hs + 4, f->comps.p, sizeof(fvv_component) * 4096, cudaMemcpyDeviceToHost, st);
+  readback(f, st, {{f->ccl_counts.p, 0, 16, nullptr, 0, 0},
+                   {f->cnt_c.p, 16, 8, nullptr, 0, 0},
+                   {f->comps.p, kHsComps, 0, f->ccl_counts.as<int64_t>() + 1,
+                    (int64_t)sizeof(fvv_component), 4096}});
   if (cudaStreamSynchronize(st) != cudaSuccess) {
     if (out_stage) *out_stage = 2;
     return cuda_check("fvv_frame_run B-2");
@@ -332,7 +403,7 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
                                 &f->fine_word_off[r0], f->mesh_ws.p, wsb, st));
     FVV_TRY(4, fvv_mesh_counts(&f->fine[r0], nb, f->mesh_ws.p, f->mesh_totals.as<int64_t>(),
                                nullptr, st));
-    cudaMemcpyAsync(hs, f->mesh_totals.p, 24, cudaMemcpyDeviceToHost, st);
+    readback(f, st, {{f->mesh_totals.p, 0, 24, nullptr, 0, 0}});
     if (cudaStreamSynchronize(st) != cudaSuccess) {
       if (out_stage) *out_stage = 4;
       return cuda_check("fvv_frame_run C");
@@ -360,10 +431,10 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
     FVV_TRY(4, fvv_mesh_counts(&f->fine[r0], nb, f->mesh_ws.p, f->mesh_totals.as<int64_t>(),
                                f->mesh_info.as<int64_t>(), st));
     if (r0 + nb < nroi) {  // more batches: need this batch's triangle count now
-      cudaMemcpyAsync(hs, f->mesh_totals.p, 24, cudaMemcpyDeviceToHost, st);
-      cudaMemcpyAsync(f->info.data() + 8 * (size_t)r0, f->mesh_info.p, 64 * (size_t)nb,
-                      cudaMemcpyDeviceToHost, st);
+      readback(f, st, {{f->mesh_totals.p, 0, 24, nullptr, 0, 0},
+                       {f->mesh_info.p, kHsInfo, 64 * (int64_t)nb, nullptr, 0, 0}});
       cudaStreamSynchronize(st);
+      memcpy(f->info.data() + 8 * (size_t)r0, (char *)f->host_small + kHsInfo, 64 * (size_t)nb);
       const int64_t tb = hs[2];
       if (v_before)
         offset_tris_kernel<<<148 * 4, 256, 0, st>>>(f->tris.as<int32_t>() + 3 * t_before, 3 * tb,
@@ -378,7 +449,7 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
       // last (usually only) batch: its triangle count stays on the device
       // for D-1/D-2; the host reads it with the final counters
       if (v_before) {
-        cudaMemcpyAsync(hs, f->mesh_totals.p, 24, cudaMemcpyDeviceToHost, st);
+        readback(f, st, {{f->mesh_totals.p, 0, 24, nullptr, 0, 0}});
         cudaStreamSynchronize(st);
         offset_tris_kernel<<<148 * 4, 256, 0, st>>>(f->tris.as<int32_t>() + 3 * t_before,
                                                     3 * hs[2], (int32_t)v_before);
@@ -456,20 +527,29 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
 
   // ---- final counters (one read) ----
   int64_t *h = hs;
-  cudaMemcpyAsync(h, ntri_dev, 8, cudaMemcpyDeviceToHost, st);
-  if (nroi) {
-    cudaMemcpyAsync(h + 8, f->cnt_f.p, 8 * (size_t)nroi, cudaMemcpyDeviceToHost, st);
-    const int last0 = ((nroi - 1) / FVV_MAX_GRIDS) * FVV_MAX_GRIDS;
-    cudaMemcpyAsync(f->info.data() + 8 * (size_t)last0, f->mesh_info.p,
-                    64 * (size_t)(nroi - last0), cudaMemcpyDeviceToHost, st);
+  const int last0 = nroi ? ((nroi - 1) / FVV_MAX_GRIDS) * FVV_MAX_GRIDS : 0;
+  std::vector<int64_t> cnt_big;
+  if (nroi > kHsMaxCntF) {  // rare: more ROIs than the mapped block holds
+    cnt_big.resize(nroi);
+    cudaMemcpyAsync(cnt_big.data(), f->cnt_f.p, 8 * (size_t)nroi, cudaMemcpyDeviceToHost, st);
   }
+  if (nroi)
+    readback(f, st, {{ntri_dev, 0, 8, nullptr, 0, 0},
+                     {f->cnt_f.p, kHsCntF, 8 * (nroi > kHsMaxCntF ? 0 : (int64_t)nroi), nullptr,
+                      0, 0},
+                     {f->mesh_info.p, kHsInfo, 64 * (int64_t)(nroi - last0), nullptr, 0, 0}});
+  else
+    readback(f, st, {{ntri_dev, 0, 8, nullptr, 0, 0}});
   cudaEventRecord(f->ev[8], st);
   if (cudaStreamSynchronize(st) != cudaSuccess) {
     if (out_stage) *out_stage = 8;
     return cuda_check("fvv_frame_run");
   }
+  const int64_t *cnt_f = nroi > kHsMaxCntF ? cnt_big.data()
+                                           : (const int64_t *)((char *)f->host_small + kHsCntF);
   if (nroi) {
-    const int last0 = ((nroi - 1) / FVV_MAX_GRIDS) * FVV_MAX_GRIDS;
+    memcpy(f->info.data() + 8 * (size_t)last0, (char *)f->host_small + kHsInfo,
+           64 * (size_t)(nroi - last0));
     for (int r = last0; r < nroi; ++r) {
       f->info[8 * r + 0] += v_before;
       f->info[8 * r + 4] += t_before;
@@ -480,7 +560,7 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
   S.vertices = f->nv;
   S.n_rois = nroi;
   for (int r = 0; r < nroi; ++r) {
-    S.dense_occupied += h[8 + r];
+    S.dense_occupied += cnt_f[r];
     S.fallback_edges += f->info[8 * r + 6];
     S.inconsistent_edge_starts += f->info[8 * r + 7];
   }

@@ -204,12 +204,13 @@ class FrameExecutor:
 _EXECUTORS = {}
 
 
-def executor_for(cfg, rig) -> FrameExecutor:
-    """Executors are cached per (config, rig parameters) so repeated
-    run_frame calls reuse the device buffers."""
+def executor_for(cfg, rig, slot: int = 0) -> FrameExecutor:
+    """Executors are cached per (config, rig parameters, slot) so repeated
+    run_frame / run_sequence calls reuse the device buffers; run_sequence
+    alternates slots 0 and 1 so one frame's D2H overlaps the next frame."""
     from dataclasses import astuple
 
-    key = (astuple(cfg), cam_table(list(rig)).tobytes())
+    key = (astuple(cfg), cam_table(list(rig)).tobytes(), int(slot))
     ex = _EXECUTORS.get(key)
     if ex is None:
         if len(_EXECUTORS) > 8:

@@ -18,12 +18,14 @@ flags, depth images) are materialised when the bundle is read.
 
 from __future__ import annotations
 
+import ctypes
 import json
 from dataclasses import asdict, dataclass, replace
 
 import numpy as np
 import torch
 
+from . import _lib
 from ._device import DeviceSilhouettes, require_cuda
 from .bundle import SceneBundle, StageTimings
 from .hull import NoiseFilterParams, Roi, carve_grids, finish_labels, label_grid_async
@@ -423,35 +425,77 @@ def bundle_from(r: FrameResult, cfg, rig, frames, frame_id=0, keep_depths=False)
     return bundle
 
 
+def _host_piece(a, keep):
+    """(pointer, bytes) of one host input, converted to contiguous uint8 if
+    needed (the converted array is kept alive in ``keep``)."""
+    if isinstance(a, torch.Tensor):
+        if a.dtype == torch.bool:
+            a = a.view(torch.uint8)
+        if a.dtype != torch.uint8:
+            a = a.to(torch.uint8)
+        a = a.contiguous()
+        keep.append(a)
+        return a.data_ptr(), a.numel()
+    arr = np.asarray(a)
+    if arr.dtype == bool:
+        arr = arr.view(np.uint8)
+    arr = np.ascontiguousarray(arr, dtype=np.uint8)
+    keep.append(arr)
+    return arr.ctypes.data, arr.size
+
+
+def _gather_to_device(pieces, dst, stream, keep):
+    ptrs = np.array([p for p, _ in pieces], dtype=np.uint64)
+    sizes = np.array([n for _, n in pieces], dtype=np.int64)
+    _lib.call("fvv_copy_gather", _lib.host_ptr(ptrs), _lib.host_ptr(sizes),
+              _lib.i64(len(pieces)), _lib.dev_ptr(dst), ctypes.c_void_p(stream.cuda_stream))
+    keep.append(ptrs)
+
+
 def _prefetch(rig, frames, sils, want_frames, copy_stream, compute_stream):
     """Queue the H2D copies of one frame's inputs on ``copy_stream``:
-    silhouette masks and (when rendering) every camera's colour frame into
-    one device buffer."""
+    silhouette masks and (when rendering) every camera's colour frame, each
+    into one device buffer with one fvv_copy_gather call."""
     dev = require_cuda()
     cams = list(rig)
     fbuf = foff = None
+    keep = []
+    if isinstance(sils, torch.Tensor):
+        m_pieces = [_host_piece(sils, keep)]
+    else:
+        sl = [sils[c.id] for c in cams] if isinstance(sils, dict) else list(sils)
+        m_pieces = [_host_piece(s, keep) for s in sl]
+    npx = sum(c.image_height * c.image_width for c in cams)
+    if sum(n for _, n in m_pieces) != npx:
+        raise ValueError("silhouettes do not match the rig's image sizes")
     with torch.cuda.stream(copy_stream):
-        if isinstance(sils, torch.Tensor):
-            d_masks = sils.to(dev, non_blocking=True)
-        else:
-            d_masks = torch.stack([torch.from_numpy(np.ascontiguousarray(s, dtype=bool))
-                                   for s in sils]).to(dev, non_blocking=True)
-        d_masks.record_stream(compute_stream)
-        if want_frames and frames is not None:
-            from .render import H2D_BYTES, _frame_tensor
+        d_masks = torch.empty(npx, dtype=torch.uint8, device=dev)
+    if isinstance(sils, torch.Tensor) and sils.is_cuda:
+        with torch.cuda.stream(copy_stream):
+            d_masks.copy_(keep[0].reshape(-1), non_blocking=True)
+    else:
+        _gather_to_device(m_pieces, d_masks, copy_stream, keep)
+    d_masks.record_stream(compute_stream)
+    if want_frames and frames is not None:
+        from .render import H2D_BYTES
 
-            sizes = [c.image_height * c.image_width * 3 for c in cams]
-            foff = np.zeros(len(cams), dtype=np.int64)
-            foff[1:] = np.cumsum(sizes)[:-1]
+        sizes = [c.image_height * c.image_width * 3 for c in cams]
+        foff = np.zeros(len(cams), dtype=np.int64)
+        foff[1:] = np.cumsum(sizes)[:-1]
+        with torch.cuda.stream(copy_stream):
             fbuf = torch.empty(int(sum(sizes)), dtype=torch.uint8, device=dev)
-            for c, o, sz in zip(cams, foff, sizes):
-                fbuf[int(o):int(o) + sz].copy_(_frame_tensor(frames[c.id]).reshape(-1),
-                                               non_blocking=True)
-            H2D_BYTES["frames"] += int(sum(sizes))
-            fbuf.record_stream(compute_stream)
-        ev = torch.cuda.Event()
-        ev.record(copy_stream)
-    return d_masks, (fbuf, foff), ev
+        f_pieces = [_host_piece(frames[c.id], keep) for c in cams]
+        for (_, n), sz, c in zip(f_pieces, sizes, cams):
+            if n != sz:
+                raise ValueError(f"camera {c.id}: colour frame has {n} bytes, expected {sz}")
+        _gather_to_device(f_pieces, fbuf, copy_stream, keep)
+        H2D_BYTES["frames"] += int(sum(sizes))
+        fbuf.record_stream(compute_stream)
+    ev = torch.cuda.Event()
+    ev.record(copy_stream)
+    # pinned sources must outlive the copies: the caller holds ``keep`` until
+    # the frame has run
+    return d_masks, (fbuf, foff), ev, keep
 
 
 def _readback(r, image):
@@ -493,67 +537,129 @@ def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
                  fallback_color=None, frame_id0: int = 0):
     """Reconstruct (and, given ``virtual``, colour) a sequence of frames.
 
-    The production form of run_frame + render_view for video: while frame f
-    computes, frame f+1's silhouettes and colour frames are copied
-    host->device on a second stream (the paper overlaps upload and compute with two CPU threads,
-    PAPER.md:561). Inputs should be pinned host tensors for the copies to be
-    asynchronous. Results come back in two transfers per frame. Yields
-    (SceneBundle, RenderedImage or None) per frame, with the mesh, visibility
-    flags and rendered image already on the host."""
+    The production form of run_frame + render_view for video, pipelined over
+    two CPU threads like the paper's system: a worker thread
+    drives the native executor frame after frame on the compute stream (the
+    ctypes calls release the GIL), while the caller's thread stages frame
+    f+1's silhouettes and colour frames host->device on a copy stream and
+    turns frame f-1's results, streamed back on a third (readback) stream,
+    into a SceneBundle. Two executors alternate so a frame's readback never
+    races the next frame's writes. Inputs should be pinned host tensors for
+    the copies to be asynchronous. Yields (SceneBundle, RenderedImage or
+    None) per frame, in order, with the mesh, visibility flags and rendered
+    image on the host."""
+    import queue
+    import threading
+
+    from .executor import executor_for
     from .render import FALLBACK_COLOR, RenderedImage
 
     fallback_color = FALLBACK_COLOR if fallback_color is None else fallback_color
     require_cuda()
+    dev_index = torch.cuda.current_device()
     cams = list(rig)
     compute = torch.cuda.current_stream()
-    copy = torch.cuda.Stream()
-    it = iter(zip(frames_seq, sils_seq))
-    try:
-        nxt = next(it)
-    except StopIteration:
-        return
-    from .executor import FrameExecutor, executor_for
+    copy = torch.cuda.Stream()      # H2D of the next frame's inputs
+    readback = torch.cuda.Stream()  # D2H of finished frames (PCIe is full duplex)
+    exs = [executor_for(cfg, rig, 0), executor_for(cfg, rig, 1)]
+    staged_q = queue.Queue(maxsize=1)   # uploads at most one frame ahead
+    done_q = queue.Queue()
+    stop = threading.Event()
+    _END = object()
 
-    # two executors alternate, so frame f's results can stream back on the
-    # copy stream while frame f+1 computes into the other one's buffers
-    exs = [executor_for(cfg, rig), FrameExecutor(cfg, rig)]
-    staged = _prefetch(cams, nxt[0], nxt[1], virtual is not None, copy, compute)
-    fid = frame_id0
-    pending = None  # (frames, output, pinned, event, frame id) of the previous frame
+    def worker():
+        slot_free = [None, None]  # readback event of the frame each executor last produced
+        k = 0
+        try:
+            torch.cuda.set_device(dev_index)
+            with torch.cuda.stream(compute):
+                while True:
+                    item = staged_q.get()
+                    if item is _END or stop.is_set():
+                        break
+                    frames, d_masks, (fbuf, foff), ev, _keep = item
+                    compute.wait_event(ev)
+                    if slot_free[k % 2] is not None:
+                        compute.wait_event(slot_free[k % 2])
+                    ex = exs[k % 2]
+                    if virtual is not None:
+                        out = ex.run(d_masks, virtual, fbuf, foff, fallback_color)
+                    else:
+                        out = ex.run(d_masks)
+                    pinned, r_ev = out.to_host_async(cams, stream=readback)
+                    slot_free[k % 2] = r_ev
+                    done_q.put((frames, out, pinned, r_ev))
+                    k += 1
+        except BaseException as exc:  # noqa: BLE001  (re-raised on the caller's thread)
+            done_q.put(exc)
+            return
+        done_q.put(_END)
 
-    def finish(p):
-        p_frames, p_out, p_pinned, p_ev, p_fid = p
+    def finish(item, fid):
+        if isinstance(item, BaseException):
+            raise item
+        p_frames, p_out, p_pinned, p_ev = item
         p_ev.synchronize()
         host = {k: v.numpy() for k, v in p_pinned.items()}
-        bundle = bundle_from_output(p_out, host, cfg, rig, p_frames, p_fid, keep_device=False)
+        bundle = bundle_from_output(p_out, host, cfg, rig, p_frames, fid, keep_device=False)
         img = None
         if virtual is not None:
             img = RenderedImage(host["color"], host["source"], host["covered"].astype(bool))
         return bundle, img
 
-    k = 0
-    while nxt is not None:
-        frames, _ = nxt
-        d_masks, frame_buf, ev = staged
-        compute.wait_event(ev)
+    def submit(item):
+        while True:
+            try:
+                staged_q.put(item, timeout=0.05)
+                return
+            except queue.Full:
+                if not th.is_alive():  # the worker failed: surface its exception
+                    while True:
+                        got = done_q.get()
+                        if isinstance(got, BaseException):
+                            raise got
+                        if got is _END:
+                            raise RuntimeError("run_sequence worker stopped early")
+
+    th = threading.Thread(target=worker, name="fvv-run-sequence", daemon=True)
+    th.start()
+    fid = frame_id0
+    in_flight = 0
+    try:
+        for frames, sils in zip(frames_seq, sils_seq):
+            d_masks, fb, ev, keep = _prefetch(cams, frames, sils, virtual is not None, copy,
+                                              compute)
+            submit((frames, d_masks, fb, ev, keep))
+            in_flight += 1
+            while True:  # hand back every frame that is already done
+                try:
+                    item = done_q.get_nowait()
+                except queue.Empty:
+                    break
+                in_flight -= 1
+                if item is _END:
+                    raise RuntimeError("run_sequence worker stopped early")
+                yield finish(item, fid)
+                fid += 1
+            if in_flight >= 3:  # bound the pinned readbacks held in flight
+                item = done_q.get()
+                in_flight -= 1
+                yield finish(item, fid)
+                fid += 1
+        submit(_END)
+        while True:
+            item = done_q.get()
+            if item is _END:
+                break
+            yield finish(item, fid)
+            fid += 1
+    finally:
+        stop.set()
         try:
-            nxt = next(it)
-            staged = _prefetch(cams, nxt[0], nxt[1], virtual is not None, copy, compute)
-        except StopIteration:
-            nxt = None
-        ex = exs[k % 2]
-        if virtual is not None:
-            out = ex.run(d_masks, virtual, frame_buf[0], frame_buf[1], fallback_color)
-        else:
-            out = ex.run(d_masks)
-        pinned, dev_ev = out.to_host_async(cams, stream=copy)
-        if pending is not None:
-            yield finish(pending)
-        pending = (frames, out, pinned, dev_ev, fid)
-        fid += 1
-        k += 1
-    if pending is not None:
-        yield finish(pending)
+            staged_q.put_nowait(_END)
+        except queue.Full:
+            pass
+        th.join()
 
 
 def sweep(cfg: PipelineConfig, rig, sils, axis: str, values) -> list:
