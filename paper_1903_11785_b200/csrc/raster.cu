@@ -135,10 +135,50 @@ struct RasterArgs {
 // Triangle setup as kept in shared memory for the warp's pixel sweep.
 struct TriSmem {
   double x0, y0, x1, y1, x2, y2, za, zb, zc, area;
+  unsigned long long mask;       // candidate bbox pixels (bit k = pixel k), 0 = all
   int t, cam, lox, loy, bw, tl;  // tl: top-left flags bits 0..2
 };
 
-__device__ __forceinline__ void setup_to_smem(const TriSetup &s, int64_t t, int cam, TriSmem &m) {
+// Candidate filter for a bbox of <= 64 pixels: a pixel centre is kept unless
+// an FP32 evaluation of some edge function, in bbox-local coordinates, is
+// below minus an error margin that dominates the FP32 error by orders of
+// magnitude. A rejected pixel therefore has a strictly negative real-valued
+// edge function, and the exact float64 test (tri_depth) would reject it too:
+// the filter changes how many pixels are tested, never the result. At C3 the
+// bboxes sweep ~8 pixel centres per triangle for ~0.25 inside.
+__device__ __forceinline__ unsigned long long candidate_mask(const TriSetup &s) {
+  const int bw = s.hix - s.lox + 1, bh = s.hiy - s.loy + 1;
+  const double ox = (double)s.lox, oy = (double)s.loy;
+  const float X0 = (float)(s.x0 - ox), Y0 = (float)(s.y0 - oy);
+  const float X1 = (float)(s.x1 - ox), Y1 = (float)(s.y1 - oy);
+  const float X2 = (float)(s.x2 - ox), Y2 = (float)(s.y2 - oy);
+  // w = a (gy - Y) - b (gx - X) = a gy - b gx + c   (edge order of tri_depth)
+  const float a0 = X2 - X1, b0 = Y2 - Y1, c0 = b0 * X1 - a0 * Y1;
+  const float a1 = X0 - X2, b1 = Y0 - Y2, c1 = b1 * X2 - a1 * Y2;
+  const float a2 = X1 - X0, b2 = Y1 - Y0, c2 = b2 * X0 - a2 * Y0;
+  const float ext = (float)(bw + bh + 2);
+  const float k = 1.0f / 16384.0f;
+  const float m0 = ((fabsf(a0) + fabsf(b0)) * ext + fabsf(c0) + 1.0f) * k;
+  const float m1 = ((fabsf(a1) + fabsf(b1)) * ext + fabsf(c1) + 1.0f) * k;
+  const float m2 = ((fabsf(a2) + fabsf(b2)) * ext + fabsf(c2) + 1.0f) * k;
+  unsigned long long mask = 0;
+  int bit = 0;
+  for (int yy = 0; yy < bh; ++yy) {
+    const float gy = (float)yy;
+    const float r0 = fmaf(a0, gy, c0), r1 = fmaf(a1, gy, c1), r2 = fmaf(a2, gy, c2);
+    for (int xx = 0; xx < bw; ++xx, ++bit) {
+      const float gx = (float)xx;
+      const bool keep = fmaf(-b0, gx, r0) >= -m0 && fmaf(-b1, gx, r1) >= -m1 &&
+                        fmaf(-b2, gx, r2) >= -m2;
+      mask |= (unsigned long long)keep << bit;
+    }
+  }
+  return mask;
+}
+
+__device__ __forceinline__ void setup_to_smem(const TriSetup &s, int64_t t, int cam, TriSmem &m,
+                                              unsigned long long mask) {
+  m.mask = mask;
   m.x0 = s.x0; m.y0 = s.y0; m.x1 = s.x1; m.y1 = s.y1; m.x2 = s.x2; m.y2 = s.y2;
   m.za = s.za; m.zb = s.zb; m.zc = s.zc; m.area = s.area;
   m.t = (int)t;
@@ -190,8 +230,14 @@ __global__ void __launch_bounds__(kRasterThreads)
           }
         }
         if (mine) {
-          setup_to_smem(s, t, c, wsm[lane]);
-          npx = (int)n;
+          unsigned long long mask = 0;
+          if (n <= 64) {
+            mask = candidate_mask(s);
+            npx = __popcll(mask);
+          } else {
+            npx = (int)n;  // (queue overflow) sweep the whole bbox
+          }
+          if (npx) setup_to_smem(s, t, c, wsm[lane], mask);
         }
       }
     }
@@ -217,7 +263,12 @@ __global__ void __launch_bounds__(kRasterThreads)
       const int own_cnt = __shfl_sync(0xffffffffu, npx, own);
       if (idx < sum) {
         const TriSmem &m = wsm[own];
-        const int k = idx - (own_incl - own_cnt);
+        int k = idx - (own_incl - own_cnt);
+        unsigned long long mk = m.mask;
+        if (mk) {  // k-th candidate -> its bbox pixel index
+          for (int j = 0; j < k; ++j) mk &= mk - 1;
+          k = __ffsll((long long)mk) - 1;
+        }
         // k / bw without an integer divide: exact for k < 2^12 (the fraction
         // of (k + 0.5) / bw is >= 0.5 / bw, far above the float error)
         int qy = (k < 4096) ? __float2int_rz(((float)k + 0.5f) * __frcp_rn((float)m.bw))
