@@ -277,8 +277,10 @@ def run_b200(args):
         e2e = {"value": round(total_frames / (e2e_ms / 1e3), 3), "unit": "frames/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(d2h / args.steps),
                "ms_per_step": round(e2e_ms / args.steps, 3),
-               "api": "pipeline.run_sequence (run_frame + render_view per frame, next frame's "
-                      "upload overlapped), pinned host inputs"}
+               "api": "pipeline.run_sequence (run_frame + render_view per frame; silhouettes "
+                      "uploaded one frame ahead, pinned colour frames sampled in place "
+                      "(zero-copy: h2d counts the 12 B of bilinear taps per sourced pixel), "
+                      "results read back on a third stream), pinned host inputs"}
 
     # ---- CPU baseline: the oracle port on this box's host cores, rank 0, N=1 ----
     cpu = None

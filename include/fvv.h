@@ -75,6 +75,12 @@ long long fvv_launch_count(void);
 int fvv_copy_gather(const void *const *src, const int64_t *bytes, int64_t n, void *dst,
                     void *stream);
 
+/* 1 if kernels can dereference host pointer p at the same address (pinned,
+ * mapped host memory under unified addressing), else 0. Colour frames that
+ * pass this test are sampled in place by the colour pass (zero-copy: only
+ * the bilinear taps cross PCIe) instead of being uploaded whole. */
+int fvv_host_mapped(const void *p);
+
 /* camera.py:164-201 project(cam, p, use_distortion) for n points (float64
  * (n,3)); writes pixel (n,2), camera-frame z (n,), in_frustum (n,) 0/1.
  * single_point selects numpy's 1-row BLAS order. */
@@ -277,6 +283,8 @@ typedef struct fvv_frame_stats {
     int64_t sparse_tests, sparse_occupied, components, dense_tests, dense_occupied,
         fallback_edges, inconsistent_edge_starts, triangles, vertices, n_rois;
     float ms[8];
+    /* colour pass: covered virtual pixels, pixels sampled from a rig camera */
+    int64_t covered_px, sourced_px;
 } fvv_frame_stats;
 
 /* Device outputs of the last fvv_frame_run (valid until the next run):
@@ -303,7 +311,8 @@ void fvv_frame_destroy(fvv_frame *frame);
 
 /* One frame: silhouette masks (uint8, rig order, camera c at
  * masks_dev + sum of previous H*W) -> B-1 .. D-2, and when virt != NULL the
- * colour pass from frames_dev (rig order, frame_off per camera) with the
+ * colour pass from frames_dev + frame_off[c] (bytes; device memory or
+ * mapped pinned host memory, see fvv_host_mapped) with the
  * camera ranking rank_pos (rig positions, render.py:29-32). On failure
  * *out_stage names the stage (1 B-1, 2 B-2, 3 B-3, 4 C, 5 D-1, 6 D-2, 7 E). */
 int fvv_frame_run(fvv_frame *frame, const uint8_t *masks_dev, const fvv_camera *virt,

@@ -37,7 +37,7 @@ assert CAM_DTYPE.itemsize == 192 and GRID_DTYPE.itemsize == 56 and COMP_DTYPE.it
 
 # exported symbols; tests check the .so exports every one of them
 SYMBOLS = (
-    "fvv_last_error", "fvv_version", "fvv_launch_count", "fvv_copy_gather", "fvv_project",
+    "fvv_last_error", "fvv_version", "fvv_launch_count", "fvv_copy_gather", "fvv_host_mapped", "fvv_project",
     "fvv_pack_silhouettes", "fvv_carve", "fvv_ccl_workspace_bytes", "fvv_ccl26",
     "fvv_ccl_components", "fvv_ccl_labels", "fvv_filter_labels", "fvv_filter_dense",
     "fvv_mesh_workspace_bytes", "fvv_mesh_prepare", "fvv_mesh_counts",
@@ -56,7 +56,7 @@ FRAME_CONFIG_DTYPE = np.dtype([("stage_lo", "<f8", (3,)), ("stage_hi", "<f8", (3
 FRAME_STATS_DTYPE = np.dtype([(k, "<i8") for k in (
     "sparse_tests", "sparse_occupied", "components", "dense_tests", "dense_occupied",
     "fallback_edges", "inconsistent_edge_starts", "triangles", "vertices", "n_rois")] +
-    [("ms", "<f4", (8,))])
+    [("ms", "<f4", (8,)), ("covered_px", "<i8"), ("sourced_px", "<i8")])
 
 
 class FrameOutputs(ctypes.Structure):

@@ -112,6 +112,15 @@ int fvv_version(void) { return 1; }
 
 long long fvv_launch_count(void) { return g_launches.load(); }
 
+int fvv_host_mapped(const void *p) {
+  cudaPointerAttributes a;
+  if (!p || cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return a.type == cudaMemoryTypeHost && a.devicePointer == p;
+}
+
 int fvv_copy_gather(const void *const *src, const int64_t *bytes, int64_t n, void *dst,
                     void *stream) {
   if (n < 0 || (n > 0 && (!src || !bytes || !dst))) {

@@ -126,6 +126,7 @@ constexpr size_t kHsComps = 32;           // up to 4096 components (256 KB)
 constexpr size_t kHsInfo = 512 * 1024;    // mesh_info of one ROI batch (64 B x 128)
 constexpr size_t kHsCntF = 640 * 1024;    // per-ROI dense counts
 constexpr int64_t kHsMaxCntF = 8192;
+constexpr size_t kHsRCounts = 768 * 1024;  // colour-pass pixel counts
 
 struct fvv_frame {
   std::vector<fvv_camera> cams, cams_by_id;
@@ -533,13 +534,17 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
     cnt_big.resize(nroi);
     cudaMemcpyAsync(cnt_big.data(), f->cnt_f.p, 8 * (size_t)nroi, cudaMemcpyDeviceToHost, st);
   }
+  const bool counted = virt && have_mesh;  // rcounts: [covered, per rig camera]
+  const HostPiece rc_piece{counted ? f->rcounts.p : ntri_dev, kHsRCounts,
+                           counted ? 8 * (int64_t)(1 + ncam) : 0, nullptr, 0, 0};
   if (nroi)
     readback(f, st, {{ntri_dev, 0, 8, nullptr, 0, 0},
                      {f->cnt_f.p, kHsCntF, 8 * (nroi > kHsMaxCntF ? 0 : (int64_t)nroi), nullptr,
                       0, 0},
-                     {f->mesh_info.p, kHsInfo, 64 * (int64_t)(nroi - last0), nullptr, 0, 0}});
+                     {f->mesh_info.p, kHsInfo, 64 * (int64_t)(nroi - last0), nullptr, 0, 0},
+                     rc_piece});
   else
-    readback(f, st, {{ntri_dev, 0, 8, nullptr, 0, 0}});
+    readback(f, st, {{ntri_dev, 0, 8, nullptr, 0, 0}, rc_piece});
   cudaEventRecord(f->ev[8], st);
   if (cudaStreamSynchronize(st) != cudaSuccess) {
     if (out_stage) *out_stage = 8;
@@ -557,6 +562,11 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
   }
   f->nt = h[0];
   S.triangles = h[0];
+  if (counted) {
+    const int64_t *rcn = (const int64_t *)((char *)f->host_small + kHsRCounts);
+    S.covered_px = rcn[0];
+    for (int c = 0; c < ncam; ++c) S.sourced_px += rcn[1 + c];
+  }
   S.vertices = f->nv;
   S.n_rois = nroi;
   for (int r = 0; r < nroi; ++r) {

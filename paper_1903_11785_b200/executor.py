@@ -160,7 +160,9 @@ class FrameExecutor:
 
     def run(self, masks, virtual=None, frames_buf=None, frame_off=None, fallback=None):
         """masks: uint8 (N,H,W) (or flat) CUDA tensor in rig order; for the
-        colour pass, frames_buf (uint8 CUDA) + frame_off (int64 per camera)."""
+        colour pass, frames_buf (uint8 CUDA tensor, or the int base address of
+        mapped pinned host frames, see fvv_host_mapped) + frame_off (int64
+        byte offset of each camera's (H, W, 3) frame from that base)."""
         from .pipeline import StageError
         from .render import FALLBACK_COLOR
 
@@ -176,7 +178,9 @@ class FrameExecutor:
             rank = self._rank_pos(virtual)
             fb = np.ascontiguousarray(np.asarray(
                 FALLBACK_COLOR if fallback is None else fallback, dtype=np.uint8).reshape(3))
-            args = (_lib.host_ptr(vt), _lib.host_ptr(rank), _lib.dev_ptr(frames_buf),
+            fptr = ctypes.c_void_p(int(frames_buf)) if isinstance(frames_buf, int) else \
+                _lib.dev_ptr(frames_buf)
+            args = (_lib.host_ptr(vt), _lib.host_ptr(rank), fptr,
                     _lib.host_ptr(np.ascontiguousarray(frame_off, dtype=np.int64)),
                     _lib.host_ptr(fb))
         else:

@@ -452,6 +452,26 @@ def _gather_to_device(pieces, dst, stream, keep):
     keep.append(ptrs)
 
 
+def _zero_copy_frames(cams, frames, keep):
+    """(base address, byte offsets) when every camera's colour frame is a
+    contiguous uint8 (H, W, 3) tensor in mapped pinned host memory, else None."""
+    ptrs = []
+    lib = _lib.load()
+    for c in cams:
+        f = frames[c.id]
+        if not (isinstance(f, torch.Tensor) and f.device.type == "cpu" and
+                f.dtype == torch.uint8 and f.is_contiguous() and
+                tuple(f.shape) == (c.image_height, c.image_width, 3)):
+            return None
+        p = f.data_ptr()
+        if not lib.fvv_host_mapped(ctypes.c_void_p(p)):
+            return None
+        ptrs.append(p)
+        keep.append(f)
+    base = min(ptrs)
+    return base, np.array([p - base for p in ptrs], dtype=np.int64)
+
+
 def _prefetch(rig, frames, sils, want_frames, copy_stream, compute_stream):
     """Queue the H2D copies of one frame's inputs on ``copy_stream``:
     silhouette masks and (when rendering) every camera's colour frame, each
@@ -479,6 +499,11 @@ def _prefetch(rig, frames, sils, want_frames, copy_stream, compute_stream):
     if want_frames and frames is not None:
         from .render import H2D_BYTES
 
+        zc = _zero_copy_frames(cams, frames, keep)
+        if zc is not None:  # sampled in place by the colour pass
+            ev = torch.cuda.Event()
+            ev.record(copy_stream)
+            return d_masks, zc, ev, keep
         sizes = [c.image_height * c.image_width * 3 for c in cams]
         foff = np.zeros(len(cams), dtype=np.int64)
         foff[1:] = np.cumsum(sizes)[:-1]
@@ -552,7 +577,7 @@ def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
     import threading
 
     from .executor import executor_for
-    from .render import FALLBACK_COLOR, RenderedImage
+    from .render import FALLBACK_COLOR, H2D_BYTES, RenderedImage
 
     fallback_color = FALLBACK_COLOR if fallback_color is None else fallback_color
     require_cuda()
@@ -584,6 +609,8 @@ def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
                     ex = exs[k % 2]
                     if virtual is not None:
                         out = ex.run(d_masks, virtual, fbuf, foff, fallback_color)
+                        if isinstance(fbuf, int):  # zero-copy: the bilinear taps crossed PCIe
+                            H2D_BYTES["frames"] += 12 * int(out.stats_raw["sourced_px"])
                     else:
                         out = ex.run(d_masks)
                     pinned, r_ev = out.to_host_async(cams, stream=readback)

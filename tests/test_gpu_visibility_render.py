@@ -183,8 +183,8 @@ def test_run_frame_empty_scene_and_errors(gpu):
 
 
 def test_run_sequence_matches_golden_frames(gpu):
-    """pipeline.run_sequence (overlapped uploads, pinned inputs, only the
-    needed colour frames copied) returns the same bundles and images as the
+    """pipeline.run_sequence (overlapped uploads; pinned colour frames sampled
+    in place, pageable ones uploaded) returns the same bundles and images as the
     reference for a sequence mixing the two golden scenes' inputs."""
     import torch
 
@@ -198,7 +198,13 @@ def test_run_sequence_matches_golden_frames(gpu):
     frames = {c.id: torch.from_numpy(z["frames"][i]).pin_memory() for i, c in enumerate(rig)}
     masks = torch.from_numpy(np.stack(sils).astype(np.uint8)).pin_memory()
     virtual = G.camera(z, "virtual")
-    out = list(run_sequence(cfg, rig, [frames, frames, frames], [masks, masks, sils], virtual))
+    np_frames = {c.id: z["frames"][i] for i, c in enumerate(rig)}  # pageable: uploaded
+    from paper_1903_11785_b200.pipeline import _zero_copy_frames
+
+    assert _zero_copy_frames(rig, frames, []) is not None  # pinned: sampled in place
+    assert _zero_copy_frames(rig, np_frames, []) is None
+    out = list(run_sequence(cfg, rig, [frames, np_frames, frames], [masks, masks, sils],
+                            virtual))
     assert len(out) == 3
     for bundle, img in out:
         assert bundle.stats == json.loads(str(z["stats"]))
