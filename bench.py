@@ -11,10 +11,11 @@ weak scaling). Rank 0 prints one JSON line.
 
   value : frames/s, inputs resident in HBM, device time (CUDA events,
           barrier + synchronize on both sides, max over ranks)
-  e2e   : frames/s through the public API (pipeline.run_frame +
-          render.render_view) from pinned host buffers, H2D of every
-          frame's silhouettes and colour frames and D2H of the mesh,
-          visibility flags and rendered image inside the timed region
+  e2e   : frames/s through the public API (pipeline.run_sequence =
+          run_frame + render_view per frame) from pinned host buffers: H2D
+          of every frame's silhouettes, the colour pass's zero-copy reads of
+          the pinned colour frames, and D2H of the mesh, visibility flags
+          and rendered image all inside the timed region
   --impl reference : the CPU oracle port of the reference pipeline
           (oracle/, C + OpenMP, all host threads), same workload and metric.
 """
