@@ -320,6 +320,13 @@ int fvv_frame_run(fvv_frame *frame, const uint8_t *masks_dev, const fvv_camera *
                   const uint8_t *fallback, void *stream, fvv_frame_stats *out_stats,
                   int *out_stage);
 int fvv_frame_get_outputs(const fvv_frame *frame, fvv_frame_outputs *out);
+/* Host copy of the last run's outputs in one pinned block: layout[0..6] =
+ * byte offsets of verts, tris, visibility bits, colour, source, covered,
+ * depth planes (depth only when want_depth), layout[8..14] their sizes,
+ * layout[7] the total; returns the total. fvv_frame_readback queues the
+ * device->host copies into host_dst (pinned, >= total bytes) on stream. */
+int64_t fvv_frame_readback_layout(const fvv_frame *frame, int want_depth, int64_t *layout);
+int fvv_frame_readback(const fvv_frame *frame, void *host_dst, int want_depth, void *stream);
 /* Per ROI: component id, box lo/hi (6 doubles), fine grid, mesh info
  * {vbase, V, sbase, S, tbase, T, fallback_edges, inconsistent_starts}. */
 int fvv_frame_get_rois(const fvv_frame *frame, int64_t *component_ids, double *boxes,

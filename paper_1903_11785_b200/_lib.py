@@ -45,7 +45,7 @@ SYMBOLS = (
     "fvv_raster_workspace_bytes", "fvv_rasterize", "fvv_classify", "fvv_triangle_sources",
     "fvv_render_count", "fvv_render_view", "fvv_back_project", "fvv_render_ellipsoids",
     "fvv_frame_create", "fvv_frame_destroy", "fvv_frame_run", "fvv_frame_get_outputs",
-    "fvv_frame_get_rois", "fvv_distance_map", "fvv_background", "fvv_extract_silhouette",
+    "fvv_frame_get_rois", "fvv_frame_readback_layout", "fvv_frame_readback", "fvv_distance_map", "fvv_background", "fvv_extract_silhouette",
 )
 
 FRAME_CONFIG_DTYPE = np.dtype([("stage_lo", "<f8", (3,)), ("stage_hi", "<f8", (3,)),
@@ -87,6 +87,7 @@ def load():
         lib.fvv_last_error.restype = ctypes.c_char_p
         lib.fvv_launch_count.restype = ctypes.c_longlong
         lib.fvv_frame_create.restype = ctypes.c_void_p
+        lib.fvv_frame_readback_layout.restype = ctypes.c_int64
         lib.fvv_frame_destroy.argtypes = [ctypes.c_void_p]
         lib.fvv_ccl_workspace_bytes.restype = ctypes.c_size_t
         lib.fvv_mesh_workspace_bytes.restype = ctypes.c_size_t

@@ -140,6 +140,7 @@ struct fvv_frame {
       mesh_totals, mesh_info, verts, tris, ntri, raster_ws, depth, vis, vplane_d, vplane_id,
       vraster_ws, src, rcounts, color, source, covered;
   // pinned host staging
+  int64_t virt_px = 0;         // pixels of the last colour pass (0: none)
   void *host_small = nullptr;  // mapped pinned block (kHs* layout)
   void *host_small_dev = nullptr;
   size_t host_small_cap = 0;
@@ -490,8 +491,10 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
   cudaEventRecord(f->ev[6], st);
 
   // ---- E: one virtual view (render.py:64-113) ----
+  f->virt_px = 0;
   if (virt) {
     const int64_t np = (int64_t)virt->width * virt->height;
+    f->virt_px = np;
     FVV_TRY(7, f->color.ensure(3 * (size_t)np));
     FVV_TRY(7, f->source.ensure(4 * (size_t)np));
     FVV_TRY(7, f->covered.ensure((size_t)np));
@@ -595,6 +598,44 @@ int fvv_frame_get_outputs(const fvv_frame *f, fvv_frame_outputs *o) {
   o->n_rois = (int64_t)f->roi_component.size();
   o->ntri_dev = f->ntri.as<int64_t>();
   return FVV_OK;
+}
+
+static void readback_layout(const fvv_frame *f, int want_depth, int64_t *lay) {
+  const int64_t sz[7] = {24 * f->nv,
+                         12 * f->nt,
+                         4 * (int64_t)f->ncam * f->vis_stride,
+                         3 * f->virt_px,
+                         4 * f->virt_px,
+                         f->virt_px,
+                         (want_depth && f->nt > 0) ? 8 * f->planes : 0};
+  int64_t off = 0;
+  for (int i = 0; i < 7; ++i) {
+    lay[i] = off;
+    lay[8 + i] = sz[i];
+    off += (sz[i] + 255) & ~255ll;
+  }
+  lay[7] = off;  // total bytes
+  lay[15] = 0;
+}
+
+int64_t fvv_frame_readback_layout(const fvv_frame *f, int want_depth, int64_t *layout) {
+  int64_t lay[16];
+  readback_layout(f, want_depth, lay);
+  if (layout) memcpy(layout, lay, sizeof(lay));
+  return lay[7];
+}
+
+int fvv_frame_readback(const fvv_frame *f, void *host_dst, int want_depth, void *stream) {
+  int64_t lay[16];
+  readback_layout(f, want_depth, lay);
+  const void *src[7] = {f->verts.p, f->tris.p, f->vis.p, f->color.p,
+                        f->source.p, f->covered.p, f->depth.p};
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int i = 0; i < 7; ++i)
+    if (lay[8 + i] > 0)
+      cudaMemcpyAsync((char *)host_dst + lay[i], src[i], (size_t)lay[8 + i],
+                      cudaMemcpyDeviceToHost, st);
+  return cuda_check("fvv_frame_readback");
 }
 
 int fvv_frame_get_rois(const fvv_frame *f, int64_t *component_ids, double *boxes, fvv_grid *grids,

@@ -42,24 +42,48 @@ def _dev(ptr, shape, typestr):
     return t.view(torch.int32) if typestr == "<u4" else t
 
 
-class FrameOutput:
-    """Results of one executor run (device views + host scalars)."""
+_READBACK_NAMES = ("verts", "tris", "vis", "color", "source", "covered", "depth")
 
-    def __init__(self, stats, outs, rois, ncam, virtual):
+
+class FrameOutput:
+    """Results of one executor run: host scalars, and device views (built on
+    first access) that stay valid until the executor's next run."""
+
+    def __init__(self, stats, outs, rois, ncam, virtual, handle=None):
         self.stats_raw = stats
+        self._outs = outs
+        self._h = handle
+        self.ncam = ncam
+        self.virtual = virtual
         self.nv, self.nt = int(outs.nv), int(stats["triangles"])
-        self.verts = _dev(outs.verts, (self.nv, 3), "<f8")
-        self.tris = _dev(outs.tris, (self.nt, 3), "<i4")
         self.vis_stride = int(outs.vis_stride)
-        self.vis_bits = _dev(outs.vis, (ncam, self.vis_stride), "<u4")
-        self.ntri_dev = _dev(outs.ntri_dev, (1,), "<i8") if outs.ntri_dev else None
         self.depth_ptr = outs.depth
         self.component_ids, self.boxes, self.grids, self.info = rois
-        self.image = None
-        if virtual is not None:
-            h, w = virtual.image_height, virtual.image_width
-            self.image = (_dev(outs.color, (h, w, 3), "|u1"), _dev(outs.source, (h, w), "<i4"),
-                          _dev(outs.covered, (h, w), "|u1"))
+
+    @property
+    def verts(self):
+        return _dev(self._outs.verts, (self.nv, 3), "<f8")
+
+    @property
+    def tris(self):
+        return _dev(self._outs.tris, (self.nt, 3), "<i4")
+
+    @property
+    def vis_bits(self):
+        return _dev(self._outs.vis, (self.ncam, self.vis_stride), "<u4")
+
+    @property
+    def ntri_dev(self):
+        return _dev(self._outs.ntri_dev, (1,), "<i8") if self._outs.ntri_dev else None
+
+    @property
+    def image(self):
+        if self.virtual is None:
+            return None
+        h, w = self.virtual.image_height, self.virtual.image_width
+        o = self._outs
+        return (_dev(o.color, (h, w, 3), "|u1"), _dev(o.source, (h, w), "<i4"),
+                _dev(o.covered, (h, w), "|u1"))
 
     def stats(self) -> dict:
         s = self.stats_raw
@@ -72,38 +96,57 @@ class FrameOutput:
         return _dev(self.depth_ptr, (total,), "<f8")
 
     def to_host_async(self, cams, keep_depths=False, stream=None):
-        """Queue pinned D2H copies of vertices, triangles, visibility bits,
-        the rendered image (and depth planes) on ``stream`` (default: the
-        current stream, after this frame's work). Returns (pinned dict,
-        completion event)."""
-        pinned = {}
+        """Queue the D2H copy of vertices, triangles, visibility bits, the
+        rendered image (and depth planes) into ONE pinned block on ``stream``
+        (default: the current stream, after this frame's work) with one
+        fvv_frame_readback call. Must be called before the executor's next
+        run. Returns (HostBlock, completion event)."""
         cur = torch.cuda.current_stream()
         stream = stream or cur
         if stream is not cur:
             stream.wait_stream(cur)
-        with torch.cuda.stream(stream):
-            def fetch(name, t):
-                h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-                h.copy_(t, non_blocking=True)
-                pinned[name] = h
-
-            fetch("verts", self.verts)
-            fetch("tris", self.tris)
-            fetch("vis", self.vis_bits)
-            if self.image is not None:
-                for n, t in zip(("color", "source", "covered"), self.image):
-                    fetch(n, t)
-            if keep_depths and self.nt:
-                fetch("depth", self.depth_planes(cams))
-            ev = torch.cuda.Event()
-            ev.record(stream)
-        return pinned, ev
+        lib = _lib.load()
+        lay = np.zeros(16, dtype=np.int64)
+        total = int(lib.fvv_frame_readback_layout(self._h, ctypes.c_int(int(keep_depths)),
+                                                  _lib.host_ptr(lay)))
+        buf = torch.empty(max(total, 1), dtype=torch.uint8, pin_memory=True)
+        _lib.call("fvv_frame_readback", self._h, ctypes.c_void_p(buf.data_ptr()),
+                  ctypes.c_int(int(keep_depths)), ctypes.c_void_p(stream.cuda_stream))
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        return HostBlock(self, buf, lay, keep_depths), ev
 
     def to_host(self, cams, keep_depths=False):
         """Pinned D2H of every host-facing output, one synchronisation."""
-        pinned, ev = self.to_host_async(cams, keep_depths)
+        block, ev = self.to_host_async(cams, keep_depths)
         ev.synchronize()
-        return {k: v.numpy() for k, v in pinned.items()}
+        return block.arrays()
+
+
+class HostBlock:
+    """One frame's outputs in a pinned host block (executor readback layout)."""
+
+    def __init__(self, out, buf, lay, keep_depths):
+        self.buf, self.lay = buf, lay
+        self.shapes = {"verts": ((out.nv, 3), np.float64), "tris": ((out.nt, 3), np.int32),
+                       "vis": ((out.ncam, out.vis_stride), np.uint32)}
+        if out.virtual is not None:
+            h, w = out.virtual.image_height, out.virtual.image_width
+            self.shapes.update(color=((h, w, 3), np.uint8), source=((h, w), np.int32),
+                               covered=((h, w), np.uint8))
+        if keep_depths and out.nt:
+            self.shapes["depth"] = ((int(lay[14]) // 8,), np.float64)
+
+    def arrays(self) -> dict:
+        raw = self.buf.numpy()
+        out = {}
+        for i, name in enumerate(_READBACK_NAMES):
+            if name not in self.shapes:
+                continue
+            shape, dt = self.shapes[name]
+            off, n = int(self.lay[i]), int(self.lay[8 + i])
+            out[name] = raw[off:off + n].view(dt).reshape(shape)
+        return out
 
 
 class FrameExecutor:
@@ -202,7 +245,7 @@ class FrameExecutor:
         _lib.load().fvv_frame_get_rois(self._h, _lib.host_ptr(cid), _lib.host_ptr(boxes),
                                        _lib.host_ptr(grids), _lib.host_ptr(info))
         return FrameOutput(stats[0], outs, (cid[:n], boxes[:n], grids[:n], info[:n]),
-                           self.ncam, virtual)
+                           self.ncam, virtual, self._h)
 
 
 _EXECUTORS = {}

@@ -558,21 +558,36 @@ def _readback(r, image):
     return [x.numpy() for x in himg] if himg is not None else None
 
 
+_SEQ_STREAMS = {}
+
+
+def _sequence_streams(dev_index, lanes):
+    """(copy, readback, [compute per lane]) streams reused across calls."""
+    key = (dev_index, lanes)
+    hit = _SEQ_STREAMS.get(key)
+    if hit is None:
+        hit = (torch.cuda.Stream(), torch.cuda.Stream(),
+               [torch.cuda.Stream() for _ in range(lanes)])
+        _SEQ_STREAMS[key] = hit
+    return hit
+
+
 def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
-                 fallback_color=None, frame_id0: int = 0):
+                 fallback_color=None, frame_id0: int = 0, lanes: int = 2):
     """Reconstruct (and, given ``virtual``, colour) a sequence of frames.
 
     The production form of run_frame + render_view for video, pipelined over
-    two CPU threads like the paper's system: a worker thread
-    drives the native executor frame after frame on the compute stream (the
-    ctypes calls release the GIL), while the caller's thread stages frame
-    f+1's silhouettes and colour frames host->device on a copy stream and
-    turns frame f-1's results, streamed back on a third (readback) stream,
-    into a SceneBundle. Two executors alternate so a frame's readback never
-    races the next frame's writes. Inputs should be pinned host tensors for
-    the copies to be asynchronous. Yields (SceneBundle, RenderedImage or
-    None) per frame, in order, with the mesh, visibility flags and rendered
-    image on the host."""
+    CPU threads like the paper's system. Frame f goes to lane
+    f mod ``lanes``; each lane is a worker thread driving its own native
+    executor on its own CUDA stream (the ctypes calls release the GIL), so
+    one lane's host synchronisations and small kernels overlap the other
+    lane's work. The caller's thread stages each frame's silhouettes
+    host->device on a copy stream one frame ahead (pinned colour frames are
+    sampled in place by the colour pass), and turns finished frames, streamed
+    back on a readback stream, into SceneBundles. Inputs should be pinned
+    host tensors for the copies to be asynchronous. Yields (SceneBundle,
+    RenderedImage or None) per frame, in input order, with the mesh,
+    visibility flags and rendered image on the host."""
     import queue
     import threading
 
@@ -581,112 +596,114 @@ def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
 
     fallback_color = FALLBACK_COLOR if fallback_color is None else fallback_color
     require_cuda()
+    lanes = max(1, int(lanes))
     dev_index = torch.cuda.current_device()
     cams = list(rig)
-    compute = torch.cuda.current_stream()
-    copy = torch.cuda.Stream()      # H2D of the next frame's inputs
-    readback = torch.cuda.Stream()  # D2H of finished frames (PCIe is full duplex)
-    exs = [executor_for(cfg, rig, 0), executor_for(cfg, rig, 1)]
-    staged_q = queue.Queue(maxsize=1)   # uploads at most one frame ahead
-    done_q = queue.Queue()
+    caller = torch.cuda.current_stream()
+    # persistent streams: the caching allocator keeps blocks per stream, so
+    # fresh streams on every call would re-allocate (and, under memory
+    # pressure, synchronise) at the start of each sequence
+    copy, readback, computes = _sequence_streams(dev_index, lanes)
+    copy.wait_stream(caller)
+    for st in computes:
+        st.wait_stream(caller)
+    exs = [executor_for(cfg, rig, k) for k in range(lanes)]
+    in_qs = [queue.Queue(maxsize=1) for _ in range(lanes)]
+    out_qs = [queue.Queue() for _ in range(lanes)]
     stop = threading.Event()
     _END = object()
 
-    def worker():
-        slot_free = [None, None]  # readback event of the frame each executor last produced
-        k = 0
+    def worker(lane):
+        compute, ex, in_q, out_q = computes[lane], exs[lane], in_qs[lane], out_qs[lane]
+        slot_free = None  # readback event of this lane's previous frame
         try:
             torch.cuda.set_device(dev_index)
             with torch.cuda.stream(compute):
                 while True:
-                    item = staged_q.get()
+                    item = in_q.get()
                     if item is _END or stop.is_set():
                         break
                     frames, d_masks, (fbuf, foff), ev, _keep = item
                     compute.wait_event(ev)
-                    if slot_free[k % 2] is not None:
-                        compute.wait_event(slot_free[k % 2])
-                    ex = exs[k % 2]
+                    if slot_free is not None:  # executor buffers still being read back
+                        compute.wait_event(slot_free)
                     if virtual is not None:
                         out = ex.run(d_masks, virtual, fbuf, foff, fallback_color)
                         if isinstance(fbuf, int):  # zero-copy: the bilinear taps crossed PCIe
                             H2D_BYTES["frames"] += 12 * int(out.stats_raw["sourced_px"])
                     else:
                         out = ex.run(d_masks)
-                    pinned, r_ev = out.to_host_async(cams, stream=readback)
-                    slot_free[k % 2] = r_ev
-                    done_q.put((frames, out, pinned, r_ev))
-                    k += 1
+                    pinned, slot_free = out.to_host_async(cams, stream=readback)
+                    out_q.put((frames, out, pinned, slot_free))
         except BaseException as exc:  # noqa: BLE001  (re-raised on the caller's thread)
-            done_q.put(exc)
+            out_q.put(exc)
             return
-        done_q.put(_END)
+        out_q.put(_END)
 
     def finish(item, fid):
         if isinstance(item, BaseException):
             raise item
+        if item is _END:
+            raise RuntimeError("run_sequence worker stopped early")
         p_frames, p_out, p_pinned, p_ev = item
         p_ev.synchronize()
-        host = {k: v.numpy() for k, v in p_pinned.items()}
+        host = p_pinned.arrays()
         bundle = bundle_from_output(p_out, host, cfg, rig, p_frames, fid, keep_device=False)
         img = None
         if virtual is not None:
             img = RenderedImage(host["color"], host["source"], host["covered"].astype(bool))
         return bundle, img
 
-    def submit(item):
+    threads = [threading.Thread(target=worker, args=(k,), name=f"fvv-lane{k}", daemon=True)
+               for k in range(lanes)]
+
+    def submit(lane, item):
         while True:
             try:
-                staged_q.put(item, timeout=0.05)
+                in_qs[lane].put(item, timeout=0.05)
                 return
             except queue.Full:
-                if not th.is_alive():  # the worker failed: surface its exception
+                if not threads[lane].is_alive():  # the lane failed: surface its exception
                     while True:
-                        got = done_q.get()
-                        if isinstance(got, BaseException):
-                            raise got
-                        if got is _END:
-                            raise RuntimeError("run_sequence worker stopped early")
+                        finish(out_qs[lane].get(), 0)
 
-    th = threading.Thread(target=worker, name="fvv-run-sequence", daemon=True)
-    th.start()
-    fid = frame_id0
-    in_flight = 0
+    for th in threads:
+        th.start()
+    n_in = n_out = 0
     try:
         for frames, sils in zip(frames_seq, sils_seq):
+            lane = n_in % lanes
             d_masks, fb, ev, keep = _prefetch(cams, frames, sils, virtual is not None, copy,
-                                              compute)
-            submit((frames, d_masks, fb, ev, keep))
-            in_flight += 1
-            while True:  # hand back every frame that is already done
-                try:
-                    item = done_q.get_nowait()
-                except queue.Empty:
-                    break
-                in_flight -= 1
-                if item is _END:
-                    raise RuntimeError("run_sequence worker stopped early")
-                yield finish(item, fid)
-                fid += 1
-            if in_flight >= 3:  # bound the pinned readbacks held in flight
-                item = done_q.get()
-                in_flight -= 1
-                yield finish(item, fid)
-                fid += 1
-        submit(_END)
-        while True:
-            item = done_q.get()
-            if item is _END:
-                break
-            yield finish(item, fid)
-            fid += 1
+                                              computes[lane])
+            submit(lane, (frames, d_masks, fb, ev, keep))
+            n_in += 1
+            while n_out < n_in:  # hand back, in order, every frame already done
+                q = out_qs[n_out % lanes]
+                if n_in - n_out > 2 * lanes:  # bound the pinned readbacks in flight
+                    item = q.get()
+                else:
+                    try:
+                        item = q.get_nowait()
+                    except queue.Empty:
+                        break
+                yield finish(item, frame_id0 + n_out)
+                n_out += 1
+        for k in range(lanes):
+            submit(k, _END)
+        while n_out < n_in:
+            yield finish(out_qs[n_out % lanes].get(), frame_id0 + n_out)
+            n_out += 1
     finally:
         stop.set()
-        try:
-            staged_q.put_nowait(_END)
-        except queue.Full:
-            pass
-        th.join()
+        for k in range(lanes):
+            try:
+                in_qs[k].put_nowait(_END)
+            except queue.Full:
+                pass
+        for th in threads:
+            th.join()
+        for st in computes:
+            caller.wait_stream(st)
 
 
 def sweep(cfg: PipelineConfig, rig, sils, axis: str, values) -> list:

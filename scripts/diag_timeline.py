@@ -2,6 +2,8 @@
 import sys, os, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
+import numpy as np
+STG = []
 from paper_1903_11785_b200 import workloads, synthetic as S, pipeline as P
 wl = workloads.get("C3"); cams = list(wl.rig)
 host = []
@@ -33,9 +35,15 @@ def wrap(name, fn):
         t = time.perf_counter(); r = fn(*a, **k); T[name] += time.perf_counter() - t; return r
     return g
 T["gpu_ms"] = 0.0
+from paper_1903_11785_b200 import _lib as L
+_lib_h = L.load(); _orig_fr = _lib_h.fvv_frame_run; T["c_run"] = 0.0
+def _fr(*a):
+    t = time.perf_counter(); r = _orig_fr(*a); T["c_run"] += time.perf_counter() - t; return r
+_lib_h.fvv_frame_run = _fr
 def run_w(*a, **k):
     t = time.perf_counter(); r = orig_run(*a, **k); T["run"] += time.perf_counter() - t
     T["gpu_ms"] += float(r.stats_raw["ms"][:8].sum()) / 1e3
+    STG.append(np.array(r.stats_raw["ms"][:8], dtype=np.float64))
     return r
 E.FrameExecutor.run = run_w; E.FrameOutput.to_host_async = wrap("to_host", orig_th)
 P._prefetch = wrap("prefetch", orig_pf)
@@ -53,4 +61,5 @@ for rep in range(2):
     for b, img in g:
         b.merged_mesh.triangles
     torch.cuda.synchronize(); el = time.perf_counter() - t0
+    print("stage ms:", np.round(np.mean(STG[-25:], axis=0), 3))
     print(f"rep {rep}: {el/30*1e3:.2f} ms/frame; " + " ".join(f"{k}={v/30*1e3:.2f}" for k, v in T.items()))
