@@ -20,7 +20,8 @@ extern "C" {
 int fvv_pack_silhouettes(const fvv_camera *, int, const uint8_t *, const int64_t *, uint32_t *,
                          const int64_t *, void *);
 int fvv_carve(const fvv_camera *, int, const uint32_t *, const int64_t *, const fvv_grid *, int,
-              const int64_t *, int, uint32_t *, int64_t *, void *);
+              const int64_t *, int, uint32_t *, int64_t *, void *, size_t, void *);
+size_t fvv_carve_workspace_bytes(void);
 size_t fvv_ccl_workspace_bytes(const fvv_grid *);
 int fvv_ccl26(const uint32_t *, const fvv_grid *, void *, size_t, fvv_component *, int64_t,
               int64_t *, void *);
@@ -136,6 +137,7 @@ struct fvv_frame {
   fvv_frame_config cfg;
   fvv_grid coarse;
   // persistent device buffers
+  DevBuf carve_ws;
   DevBuf sil, occ_c, cnt_c, ccl_ws, comps, ccl_counts, occ_f, cnt_f, mesh_ws, mesh_scratch,
       mesh_totals, mesh_info, verts, tris, ntri, raster_ws, depth, vis, vplane_d, vplane_id,
       vraster_ws, src, rcounts, color, source, covered;
@@ -278,7 +280,8 @@ fvv_frame *fvv_frame_create(const fvv_camera *cams, int ncam, const fvv_frame_co
       f->cnt_c.ensure(64) || f->ccl_counts.ensure(64) ||
       f->ccl_ws.ensure(fvv_ccl_workspace_bytes(&f->coarse)) ||
       f->comps.ensure(sizeof(fvv_component) * 4096) || f->mesh_totals.ensure(64) ||
-      f->ntri.ensure(64) || host_small_ensure(f, 1 << 20)) {
+      f->ntri.ensure(64) || f->carve_ws.ensure(fvv_carve_workspace_bytes()) ||
+      host_small_ensure(f, 1 << 20)) {
     delete f;
     return nullptr;
   }
@@ -313,7 +316,7 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
   const int64_t zero = 0;
   FVV_TRY(1, fvv_carve(f->cams.data(), ncam, f->sil.as<uint32_t>(), f->word_off.data(), &G, 1,
                        &zero, cfg.min_views, f->occ_c.as<uint32_t>(), f->cnt_c.as<int64_t>(),
-                       st));
+                       f->carve_ws.p, f->carve_ws.cap, st));
   cudaEventRecord(f->ev[1], st);
 
   // ---- B-2 CCL, noise filter, ROIs (pipeline.py:159-166) ----
@@ -388,7 +391,8 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
     const int nb = nroi - r0 < FVV_MAX_GRIDS ? nroi - r0 : FVV_MAX_GRIDS;
     FVV_TRY(3, fvv_carve(f->cams.data(), ncam, f->sil.as<uint32_t>(), f->word_off.data(),
                          &f->fine[r0], nb, &f->fine_word_off[r0], cfg.min_views,
-                         f->occ_f.as<uint32_t>(), f->cnt_f.as<int64_t>() + r0, st));
+                         f->occ_f.as<uint32_t>(), f->cnt_f.as<int64_t>() + r0, f->carve_ws.p,
+                         f->carve_ws.cap, st));
   }
   cudaEventRecord(f->ev[3], st);
 

@@ -125,6 +125,8 @@ def carve_grids(dsils: DeviceSilhouettes, specs, min_views: int = 1):
         word_off[1:] = np.cumsum(words)[:-1]
     bits = torch.empty(max(int(sum(words)), 1), dtype=torch.int32, device=dev)
     counts = torch.zeros(max(len(specs), 1), dtype=torch.int64, device=dev)
+    ws_bytes = int(_lib.load().fvv_carve_workspace_bytes())
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)  # stream-ordered reuse
     for b0 in range(0, len(specs), _lib.FVV_MAX_GRIDS):
         chunk = specs[b0:b0 + _lib.FVV_MAX_GRIDS]
         tab = grid_table(chunk)
@@ -132,7 +134,8 @@ def carve_grids(dsils: DeviceSilhouettes, specs, min_views: int = 1):
         _lib.call("fvv_carve", _lib.host_ptr(dsils.cams), ctypes.c_int(dsils.ncam),
                   _lib.dev_ptr(dsils.bits), _lib.host_ptr(dsils.word_off), _lib.host_ptr(tab),
                   ctypes.c_int(len(chunk)), _lib.host_ptr(off), ctypes.c_int(int(min_views)),
-                  _lib.dev_ptr(bits), _lib.dev_ptr(counts[b0:]), stream_handle())
+                  _lib.dev_ptr(bits), _lib.dev_ptr(counts[b0:]), _lib.dev_ptr(ws),
+                  ctypes.c_size_t(ws_bytes), stream_handle())
     return [VoxelGrid(s, bits=bits[int(o):int(o) + w], count=counts[g])
             for g, (s, o, w) in enumerate(zip(specs, word_off, words))]
 
