@@ -103,10 +103,10 @@ int fvv_carve(const fvv_camera *cams, int ncam, const uint32_t *sil_dev,
               const int64_t *sil_word_off, const fvv_grid *grids, int ngrid,
               const int64_t *word_off, int min_views, uint32_t *occ_dev,
               int64_t *count_dev, void *workspace, size_t ws_bytes, void *stream);
-/* Workspace fvv_carve uses to defer the (voxel, camera) tests its certified
- * FP32 pass cannot decide to a float64 pass; workspace may be NULL (they
- * are then decided inline). Word 0 holds the number of deferred voxels. */
-size_t fvv_carve_workspace_bytes(void);
+/* Device workspace fvv_carve needs for these cameras: per-(grid, camera)
+ * FP32 projection coefficients, 8x8-pixel silhouette cell maps, and the
+ * queue of voxels its certified FP32 pass leaves to the float64 chain. */
+size_t fvv_carve_workspace_bytes(const fvv_camera *cams, int ncam);
 
 /* ---- B-2: hull.py:122-269 ------------------------------------------------ */
 

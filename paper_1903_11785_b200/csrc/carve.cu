@@ -12,6 +12,7 @@
 // stops at the first camera that sees it on background: it is OFF whatever
 // the remaining cameras say (hull.py:91 ANDs them), so the early exit
 // cannot change the result.
+#include <algorithm>
 #include <cstring>
 
 #include "fvv_common.cuh"
@@ -29,6 +30,15 @@ struct CarveParams {
   int64_t *count;
   unsigned long long *amb;  // [0] = queued voxels, then (grid << 40 | voxel) entries
   int64_t amb_cap;
+  const struct CamAffine *affine;  // [ngrid][ncam] (carve_affine_kernel)
+  unsigned long long *tile_stats;  // culled tiles, sum of fg cameras, sum of mixed cameras
+  int tile_log2;                   // tile edge 1 << tile_log2 voxels
+  uint32_t tiles_x[FVV_MAX_GRIDS], tiles_y[FVV_MAX_GRIDS];
+  // 8x8-pixel cell maps per camera (carve_cells_kernel): bit = some / every
+  // pixel of the cell is foreground; rows of cell_words[c] words
+  uint32_t *cell_any, *cell_all;
+  int64_t cell_off[FVV_MAX_CAMS], cell_total;
+  int32_t cell_words[FVV_MAX_CAMS];
   int k1;                    // cameras order[0 .. k1) are tested in phase 1
   int order[FVV_MAX_CAMS];   // camera test order (a permutation of 0 .. ncam-1)
   int64_t sil_off[FVV_MAX_CAMS];
@@ -52,10 +62,12 @@ struct CarveParams {
 // Bound: with eps = 2^-24 and S = |U0| + i|Ui| + j|Uj| + k|Uk| (bounded by
 // its value at the far grid corner), coefficient rounding plus the three
 // fmaf roundings give |U32 - U| <= 4 eps S_U (same for Z); then
-// |U32/Z32 - U/Z| <= 4 eps (S_U + |u| S_Z) / Z32, plus 8.5 eps |u| for the
-// approximate reciprocal (__fdividef: <= 2 ulp) and the product; the float64
-// chain's own error (< 1e-9 px at these magnitudes) is covered by an
-// absolute 2^-12; the whole bound is doubled (and the per-camera constants
+// |U32/Z32 - U/Z| <= 4 eps (S_U + |u| S_Z) / Z32 to first order, plus
+// 3 eps |u| for the reciprocal (MUFU.RCP refined by one Newton step: within
+// ~1 ulp) and the product; the float64 chain's own error (< 1e-9 px at these
+// magnitudes) is covered by an absolute 2^-20; the whole bound is scaled by
+// 1.25 for second-order terms and the rounding of E itself (and the
+// per-camera constants
 // inflated by 1%). The sign of Z is certain once |Z32| > ez; when every
 // voxel of the grid has Z beyond that (Z is affine, its minimum is at a
 // grid corner) the sign checks are skipped. A |u32| beyond ulim lies outside
@@ -64,7 +76,7 @@ struct CarveParams {
 struct __align__(16) CamAffine {
   float u[4], v[4], z[4];  // constant, i, j, k coefficients
   float su, sv, sz, ez;    // magnitude sums at the far corner; |Z32 - Z| bound
-  float zsafe, ulim, bu, bv;  // fast path (Z32 >= zsafe): eu = (|u|+1)(A rz + C) + bu rz + 2^-12
+  float zsafe, ulim, bu, bv;  // E_u = (|u|+1)(A rz + C) + bu rz + 2^-20
   float A;                 // 8 eps sz
   int w, h, pad0;
 };
@@ -119,12 +131,18 @@ __device__ __forceinline__ void cam_affine(const fvv_camera &c, const fvv_grid &
   // sign checks run first
   const double zsafe = (zmin - 2.0 * ez) * (1.0 - 1e-6);
   a.zsafe = (!c.has_distortion && zsafe > ez) ? (float)zsafe : INFINITY;
-  a.A = (float)(8.0 * (double)kEps * sz * 1.01);
-  a.bu = (float)(8.0 * (double)kEps * su * 1.01);
-  a.bv = (float)(8.0 * (double)kEps * sv * 1.01);
+  a.A = (float)(5.0 * (double)kEps * sz * 1.01);  // 1.25 * 4 eps
+  a.bu = (float)(5.0 * (double)kEps * su * 1.01);
+  a.bv = (float)(5.0 * (double)kEps * sv * 1.01);
 }
 
 enum : int { kOut = 0, kIn = 1, kAmb = 2 };
+
+// 1/z to ~1 ulp: MUFU.RCP (<= 2 ulp) refined by one Newton step.
+__device__ __forceinline__ float recip(float z) {
+  const float r = __fdividef(1.0f, z);
+  return fmaf(r, fmaf(-z, r, 1.0f), r);
+}
 
 // FP32 classification of one (voxel, camera): kOut (not in frustum), kIn
 // (in frustum at pixel (px, py)), kAmb (undecided in FP32).
@@ -133,15 +151,15 @@ __device__ __forceinline__ int classify32(const CamAffine &a, float fi, float fj
   const float Z = fmaf(fk, a.z[3], fmaf(fj, a.z[2], fmaf(fi, a.z[1], a.z[0])));
   const float U = fmaf(fk, a.u[3], fmaf(fj, a.u[2], fmaf(fi, a.u[1], a.u[0])));
   const float V = fmaf(fk, a.v[3], fmaf(fj, a.v[2], fmaf(fi, a.v[1], a.v[0])));
-  // E = 2 (4 eps (|u| S_Z + S_U) / Z + 8.5 eps |u|) + 2^-12, |u| -> |u32| + 1
+  // E = 1.25 (4 eps (|u| S_Z + S_U) / Z + 3 eps |u|) + 2^-20, |u| -> |u32| + 1
   if (!(Z >= a.zsafe)) {
     if (Z <= -a.ez) return kOut;  // Z < 0 for certain
     if (Z < a.ez) return kAmb;
   }
-  const float rz = __fdividef(1.0f, Z);
-  const float k = fmaf(a.A, rz, 17.0f * kEps);
-  const float eu = fmaf(fabsf(U * rz) + 1.0f, k, fmaf(a.bu, rz, 2.44140625e-4f));
-  const float ev = fmaf(fabsf(V * rz) + 1.0f, k, fmaf(a.bv, rz, 2.44140625e-4f));
+  const float rz = recip(Z);
+  const float k = fmaf(a.A, rz, 3.75f * kEps);
+  const float eu = fmaf(fabsf(U * rz) + 1.0f, k, fmaf(a.bu, rz, 9.5367432e-7f));
+  const float ev = fmaf(fabsf(V * rz) + 1.0f, k, fmaf(a.bv, rz, 9.5367432e-7f));
   const float u = U * rz, v = V * rz;
   const float ru = rintf(u), rv = rintf(v);
   px = (int)ru;
@@ -225,97 +243,266 @@ __device__ __forceinline__ bool settle(const CarveParams &p, const fvv_grid &G, 
   return carve_exact(p, G, l);
 }
 
-// Two phases per block of 4096 voxels. Phase 1: every voxel against the
-// first p.k1 cameras of p.order (spread around the rig, so most voxels
-// outside the hull are rejected here); survivors are compacted into a
-// shared-memory queue with their partial view count. Phase 2: the block's
-// threads take the queue densely against the remaining cameras, so a few ON
-// voxels no longer hold whole warps for all cameras. The AND over cameras
-// and the view count do not depend on the order cameras are tested in.
-__global__ void __launch_bounds__(kCarveThreads)
-    carve_kernel(const __grid_constant__ CarveParams p) {
-  constexpr int kVox = kCarveWordsPerBlock * 32;
-  __shared__ CamAffine aff[FVV_MAX_CAMS];
-  __shared__ uint32_t occw[kCarveWordsPerBlock];
-  __shared__ uint32_t queue[kVox];  // local index | seen << 12 | amb << 19
-  __shared__ int qn, block_on;
-  const int64_t b = blockIdx.x;
-  int g = 0;
-  while (b >= p.blk_start[g + 1]) ++g;  // uniform across the block
-  const fvv_grid &G = p.grids[g];
-  const int64_t nx = G.dims[0], ny = G.dims[1];
-  const int64_t nvox = nx * ny * G.dims[2];
-  const bool small = nvox < (int64_t)0xffffffff;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int kWarps = kCarveThreads / 32;
-  if (threadIdx.x == 0) {
-    qn = 0;
-    block_on = 0;
+// ---- tile culling ---------------------------------------------------------
+// A block carves one tile of T^3 voxels (T = 8, or 16 for large grids). For each camera it first bounds,
+// in FP32 with the same certified error terms, the pixels the tile's voxel
+// centres can round to: u = U/Z is linear-fractional, so over the tile (a
+// box of voxel centres, Z > 0) its extrema are at the 8 corner centres. If
+// that pixel rectangle lies inside the image, every voxel of the tile is in
+// the camera's frustum, and then
+//   - all rectangle pixels background -> every voxel is OFF (hull.py:91),
+//   - all foreground -> the camera passes every voxel (one more view each),
+//   - otherwise the camera is tested per voxel.
+// Per-voxel work is thus confined to the cameras whose silhouette boundary
+// crosses the tile; empty space and hull interiors cost a few word loads.
+constexpr int kRectMaxPx = 4096;        // larger rectangles: test per voxel
+enum : int { kTileBg = 0, kTileFg = 1, kTileMixed = 2 };
+
+__device__ __forceinline__ void corner_bound(const CamAffine &a, float fi, float fj, float fk,
+                                             bool &zok, float &u0, float &u1, float &v0,
+                                             float &v1) {
+  const float Z = fmaf(fk, a.z[3], fmaf(fj, a.z[2], fmaf(fi, a.z[1], a.z[0])));
+  const float U = fmaf(fk, a.u[3], fmaf(fj, a.u[2], fmaf(fi, a.u[1], a.u[0])));
+  const float V = fmaf(fk, a.v[3], fmaf(fj, a.v[2], fmaf(fi, a.v[1], a.v[0])));
+  zok = Z >= a.ez;  // Z > 0 for certain
+  const float rz = recip(zok ? Z : 1.0f);
+  const float u = U * rz, v = V * rz;
+  const float k = fmaf(a.A, rz, 3.75f * kEps);
+  // + 1e-3 covers the rounding of these few float operations
+  const float eu = fmaf(fabsf(u) + 1.0f, k, fmaf(a.bu, rz, 9.5367432e-7f)) + 1e-3f;
+  const float ev = fmaf(fabsf(v) + 1.0f, k, fmaf(a.bv, rz, 9.5367432e-7f)) + 1e-3f;
+  u0 = u - eu;
+  u1 = u + eu;
+  v0 = v - ev;
+  v1 = v + ev;
+}
+
+// Eight lanes (one group of a warp; g8 = lane & 7) classify camera c for
+// the tile [i0, i1] x [j0, j1] x [k0, k1]; every lane of the warp calls this
+// (c < 0: idle group) and gets its own group's result.
+__device__ int tile_camera(const CarveParams &p, const CamAffine *aff, int c, int i0, int i1,
+                           int j0, int j1, int k0, int k1, int lane) {
+  const int g8 = lane & 7, grp = lane >> 3;
+  float u0 = INFINITY, u1 = -INFINITY, v0 = INFINITY, v1 = -INFINITY;
+  bool zok = false;
+  if (c >= 0)
+    corner_bound(aff[c], (float)((g8 & 1) ? i1 : i0), (float)((g8 & 2) ? j1 : j0),
+                 (float)((g8 & 4) ? k1 : k0), zok, u0, u1, v0, v1);
+  for (int o = 4; o >= 1; o >>= 1) {  // min/max over the group's 8 corners
+    u0 = fminf(u0, __shfl_xor_sync(0xffffffffu, u0, o));
+    u1 = fmaxf(u1, __shfl_xor_sync(0xffffffffu, u1, o));
+    v0 = fminf(v0, __shfl_xor_sync(0xffffffffu, v0, o));
+    v1 = fmaxf(v1, __shfl_xor_sync(0xffffffffu, v1, o));
   }
-  for (int w = threadIdx.x; w < kCarveWordsPerBlock; w += blockDim.x) occw[w] = 0;
-  for (int c = threadIdx.x; c < p.ncam; c += blockDim.x) cam_affine(p.cams[c], G, aff[c]);
-  __syncthreads();
-  const int64_t word0 = (b - p.blk_start[g]) * kCarveWordsPerBlock;
-  const int64_t l0 = word0 * 32;
-#pragma unroll 1
-  for (int it = 0; it < kCarveWordsPerBlock / kWarps; ++it) {
-    const int lw = it * kWarps + warp;
-    const int64_t l = l0 + lw * 32 + lane;
-    bool on = false, survivor = false;
-    uint32_t code = 0;
-    if (l < nvox) {
-      int64_t i, j, k;
-      voxel_ijk(l, nx, ny, small, i, j, k);
-      int seen = 0;
-      bool off = false, amb = false;
-      test_cams(p, aff, 0, p.k1, (float)i, (float)j, (float)k, seen, off, amb);
-      if (!off) {
-        if (p.k1 < p.ncam) {
-          survivor = true;
-          code = (uint32_t)(lw * 32 + lane) | ((uint32_t)seen << 12) | ((uint32_t)amb << 19);
-        } else {
-          on = settle(p, G, g, l, seen, amb);
+  const unsigned gmask = 0xffu << (8 * grp);
+  zok = (__ballot_sync(0xffffffffu, zok) & gmask) == gmask;
+  bool query = c >= 0 && zok;
+  // rint(x) lies in [floor(x - 0.5), ceil(x + 0.5)] for x in [u0, u1]
+  const float xl = floorf(u0 - 0.5f), xh = ceilf(u1 + 0.5f);
+  const float yl = floorf(v0 - 0.5f), yh = ceilf(v1 + 0.5f);
+  int x0 = 0, x1 = -1, y0 = 0, y1 = -1;
+  if (query) {
+    const CamAffine &a = aff[c];
+    query = xl >= 0.0f && yl >= 0.0f && xh <= (float)(a.w - 1) && yh <= (float)(a.h - 1);
+    if (query) {  // (false for NaN, or partly outside the image: per voxel)
+      x0 = (int)xl;
+      x1 = (int)xh;
+      y0 = (int)yl;
+      y1 = (int)yh;
+      query = (int64_t)(x1 - x0 + 1) * (y1 - y0 + 1) <= kRectMaxPx;
+    }
+  }
+  bool any = false, all = true;
+  if (query && y1 - y0 >= 16) {  // large rectangle: 8x8 cells covering it
+    const int cx0 = x0 >> 3, cx1 = x1 >> 3, cy0 = y0 >> 3, cy1 = y1 >> 3;
+    const uint32_t *ca = p.cell_any + p.cell_off[c], *cl = p.cell_all + p.cell_off[c];
+    const int stride = p.cell_words[c];
+    const int w0 = cx0 >> 5, w1 = cx1 >> 5;
+    const uint32_t mlo = 0xffffffffu << (cx0 & 31), mhi = 0xffffffffu >> (31 - (cx1 & 31));
+    for (int y = cy0 + g8; y <= cy1; y += 8) {
+      for (int wq = w0; wq <= w1; ++wq) {
+        const uint32_t m = (wq == w0 ? mlo : 0xffffffffu) & (wq == w1 ? mhi : 0xffffffffu);
+        any |= (__ldg(ca + (int64_t)y * stride + wq) & m) != 0;
+        all &= (__ldg(cl + (int64_t)y * stride + wq) & m) == m;
+      }
+    }
+  } else if (query) {
+    const uint32_t *plane = p.sil + p.sil_off[c];
+    const int stride = p.sil_stride[c];
+    const int w0 = x0 >> 5, w1 = x1 >> 5;
+    const uint32_t mlo = 0xffffffffu << (x0 & 31), mhi = 0xffffffffu >> (31 - (x1 & 31));
+    // rows g8, g8 + 8, ...; four rows' words in flight per step
+    for (int y = y0 + g8; y <= y1; y += 32) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int yy = y + 8 * q;
+        if (yy > y1) break;
+        const uint32_t *row = plane + (int64_t)yy * stride;
+        for (int wq = w0; wq <= w1; ++wq) {
+          const uint32_t m = (wq == w0 ? mlo : 0xffffffffu) & (wq == w1 ? mhi : 0xffffffffu);
+          const uint32_t bits = __ldg(row + wq) & m;
+          any |= bits != 0;
+          all &= bits == m;
         }
       }
     }
-    const uint32_t sv = __ballot_sync(0xffffffffu, survivor);
-    if (sv) {
-      int base = 0;
-      if (lane == 0) base = atomicAdd(&qn, __popc(sv));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (survivor) queue[base + __popc(sv & ((1u << lane) - 1u))] = code;
+  }
+  any = (__ballot_sync(0xffffffffu, any) & gmask) != 0;
+  all = (__ballot_sync(0xffffffffu, all) & gmask) == gmask;
+  if (!query) return kTileMixed;
+  return !any ? kTileBg : (all ? kTileFg : kTileMixed);
+}
+
+// 8x8-pixel cell maps of every camera's silhouette bits: any / all
+// foreground over the cell's in-image pixels. One thread per 32 cells.
+__global__ void carve_cells_kernel(const __grid_constant__ CarveParams p) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < p.cell_total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int c = 0;
+    while (c + 1 < p.ncam && e >= p.cell_off[c + 1]) ++c;
+    const int64_t local = e - p.cell_off[c];
+    const int W = p.cams[c].width, H = p.cams[c].height;
+    const int cw = p.cell_words[c];
+    const int cy = (int)(local / cw), wq = (int)(local - (int64_t)cy * cw);
+    const uint32_t *plane = p.sil + p.sil_off[c];
+    const int stride = p.sil_stride[c];
+    uint32_t any = 0, all = 0;
+    // cells 32 wq .. 32 wq + 31 span pixel words 8 wq .. 8 wq + 7 (4 cells each)
+    for (int q = 0; q < 8; ++q) {
+      const int pw = 8 * wq + q;
+      if (pw >= stride) break;
+      // pixels beyond the right edge count as foreground for "all"
+      const int x_end = W - 32 * pw;  // valid bits in this word
+      const uint32_t valid = x_end >= 32 ? 0xffffffffu : (x_end <= 0 ? 0u : (1u << x_end) - 1u);
+      uint32_t o = 0, a = 0xffffffffu;
+      for (int r = 0; r < 8; ++r) {
+        const int y = 8 * cy + r;
+        if (y >= H) break;
+        const uint32_t w = __ldg(plane + (int64_t)y * stride + pw);
+        o |= w;
+        a &= w | ~valid;
+      }
+      for (int bb = 0; bb < 4; ++bb) {
+        const uint32_t bo = (o >> (8 * bb)) & 0xffu, ba = (a >> (8 * bb)) & 0xffu;
+        any |= (uint32_t)(bo != 0) << (4 * q + bb);
+        all |= (uint32_t)(ba == 0xffu) << (4 * q + bb);
+      }
     }
-    const uint32_t bits = __ballot_sync(0xffffffffu, on);
-    if (lane == 0 && bits) atomicOr(&occw[lw], bits);
+    p.cell_any[e] = any;
+    p.cell_all[e] = all;
+  }
+}
+
+// Per-(grid, camera) FP32 coefficients, once per launch.
+__global__ void carve_affine_kernel(const __grid_constant__ CarveParams p, CamAffine *out) {
+  const int n = p.ngrid * p.ncam;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x)
+    cam_affine(p.cams[e % p.ncam], p.grids[e / p.ncam], out[e]);
+}
+
+__global__ void __launch_bounds__(kCarveThreads)
+    carve_kernel(const __grid_constant__ CarveParams p) {
+  __shared__ CamAffine aff[FVV_MAX_CAMS];
+  __shared__ int state[FVV_MAX_CAMS];
+  __shared__ int mixed[FVV_MAX_CAMS];
+  __shared__ int n_mixed, n_fg, culled;
+  const int64_t b = blockIdx.x;
+  int g = 0;  // binary search of the block's grid (uniform across the block)
+  for (int step = FVV_MAX_GRIDS / 2; step >= 1; step >>= 1)
+    if (g + step < p.ngrid && b >= p.blk_start[g + step]) g += step;
+  const fvv_grid &G = p.grids[g];
+  const int64_t nx = G.dims[0], ny = G.dims[1], nz = G.dims[2];
+  const int tl = p.tile_log2, kT = 1 << tl;
+  const uint32_t tx = p.tiles_x[g], ty = p.tiles_y[g];
+  const uint32_t tile = (uint32_t)(b - p.blk_start[g]);  // < 2^32 tiles per grid
+  const uint32_t tq = tile / tx;
+  const int64_t ti = tile - tq * tx, tj = tq % ty, tk = tq / ty;
+  const int i0 = (int)(ti * kT), j0 = (int)(tj * kT), k0 = (int)(tk * kT);
+  const int i1 = (int)min((int64_t)i0 + kT, nx) - 1, j1 = (int)min((int64_t)j0 + kT, ny) - 1,
+            k1 = (int)min((int64_t)k0 + kT, nz) - 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int kWarps = kCarveThreads / 32;
+  if (threadIdx.x == 0) culled = 0;
+  {  // this grid's camera coefficients (carve_affine_kernel) into shared memory
+    const float4 *src = (const float4 *)(p.affine + (int64_t)g * p.ncam);
+    float4 *dst = (float4 *)aff;
+    for (int e = threadIdx.x; e < p.ncam * (int)(sizeof(CamAffine) / 16); e += blockDim.x)
+      dst[e] = __ldg(src + e);
   }
   __syncthreads();
-  const int n = qn;
-#pragma unroll 1
-  for (int q = threadIdx.x; q < n; q += blockDim.x) {
-    const uint32_t code = queue[q];
-    const int li = (int)(code & 0xfffu);
-    int seen = (int)((code >> 12) & 0x7fu);
-    bool amb = (code >> 19) & 1u, off = false;
-    const int64_t l = l0 + li;
-    int64_t i, j, k;
-    voxel_ijk(l, nx, ny, small, i, j, k);
-    test_cams(p, aff, p.k1, p.ncam, (float)i, (float)j, (float)k, seen, off, amb);
-    if (!off && settle(p, G, g, l, seen, amb)) atomicOr(&occw[li >> 5], 1u << (li & 31));
+  // every camera's tile state, four cameras per warp (eight lanes each)
+  for (int t0 = 0; t0 < p.ncam; t0 += 4 * kWarps) {
+    const int t = t0 + 4 * warp + (lane >> 3);
+    const int c = t < p.ncam ? p.order[t] : -1;
+    const int st = tile_camera(p, aff, c, i0, i1, j0, j1, k0, k1, lane);
+    if (c >= 0 && (lane & 7) == 0) {
+      state[t] = st;
+      if (st == kTileBg) culled = 1;
+    }
   }
   __syncthreads();
+  if (culled) {  // every voxel of the tile is OFF (words pre-zeroed)
+    if (threadIdx.x == 0) atomicAdd(p.tile_stats, 1ull);
+    return;
+  }
+  if (threadIdx.x == 0) {
+    int nm = 0, nf = 0;
+    for (int t = 0; t < p.ncam; ++t) {
+      if (state[t] == kTileFg) ++nf;
+      else mixed[nm++] = p.order[t];
+    }
+    n_mixed = nm;
+    n_fg = nf;
+    atomicAdd(p.tile_stats + 1, (unsigned long long)nf);
+    atomicAdd(p.tile_stats + 2, (unsigned long long)nm);
+  }
+  __syncthreads();
+  const int nm = n_mixed;
   int my_on = 0;
-  for (int w = threadIdx.x; w < kCarveWordsPerBlock; w += blockDim.x) {
-    if ((word0 + w) * 32 < nvox) {
-      p.occ[p.word_off[g] + word0 + w] = occw[w];
-      my_on += __popc(occw[w]);
+  const int64_t nvox = nx * ny * nz;
+  for (int v = threadIdx.x; v < (1 << (3 * tl)); v += blockDim.x) {
+    const int i = i0 + (v & (kT - 1)), j = j0 + ((v >> tl) & (kT - 1)), k = k0 + (v >> (2 * tl));
+    if (i > i1 || j > j1 || k > k1) continue;
+    const float fi = (float)i, fj = (float)j, fk = (float)k;
+    int seen = n_fg;
+    bool off = false, amb = false;
+    for (int m = 0; m < nm; ++m) {
+      const int c = mixed[m];
+      int px, py;
+      const int st = classify32(aff[c], fi, fj, fk, px, py);
+      if (st == kOut) continue;
+      if (st == kAmb) {
+        amb = true;
+        continue;
+      }
+      ++seen;
+      if (!sil_bit(p.sil + p.sil_off[c], p.sil_stride[c], px, py)) {
+        off = true;
+        break;
+      }
+    }
+    const int64_t l = (int64_t)i + nx * ((int64_t)j + ny * (int64_t)k);
+    if (!off && settle(p, G, g, l, seen, amb)) {
+      atomicOr(p.occ + p.word_off[g] + (l >> 5), 1u << (l & 31));
+      ++my_on;
     }
   }
-  if (p.count) {
+  (void)nvox;
+  if (p.count) {  // per-warp atomics: no block barrier at the end
     my_on = __reduce_add_sync(0xffffffffu, my_on);
-    if (lane == 0 && my_on) atomicAdd(&block_on, my_on);
-    __syncthreads();
-    if (threadIdx.x == 0 && block_on)
-      atomicAdd((unsigned long long *)&p.count[g], (unsigned long long)block_on);
+    if (lane == 0 && my_on)
+      atomicAdd((unsigned long long *)&p.count[g], (unsigned long long)my_on);
+  }
+}
+
+// Zero the occupancy words of every grid of the batch (tiles only set bits).
+__global__ void carve_zero_kernel(const __grid_constant__ CarveParams p) {
+  for (int g = 0; g < p.ngrid; ++g) {
+    const fvv_grid &G = p.grids[g];
+    const int64_t words = (G.dims[0] * G.dims[1] * G.dims[2] + 31) / 32;
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < words;
+         w += (int64_t)gridDim.x * blockDim.x)
+      p.occ[p.word_off[g] + w] = 0u;
   }
 }
 
@@ -340,8 +527,25 @@ __global__ void __launch_bounds__(kCarveThreads)
 
 using namespace fvv;
 
-extern "C" size_t fvv_carve_workspace_bytes(void) {
-  return sizeof(unsigned long long) * (1 + (size_t)kAmbCap);
+static size_t affine_bytes() {
+  return (sizeof(CamAffine) * FVV_MAX_GRIDS * FVV_MAX_CAMS + 255) & ~(size_t)255;
+}
+
+static int64_t cell_words_total(const fvv_camera *cams, int ncam) {
+  int64_t n = 0;
+  for (int c = 0; c < ncam; ++c)
+    n += (int64_t)((cams[c].height + 7) >> 3) * ((((cams[c].width + 7) >> 3) + 31) >> 5);
+  return n;
+}
+
+static size_t cells_bytes(const fvv_camera *cams, int ncam) {
+  return (2 * sizeof(uint32_t) * (size_t)cell_words_total(cams, ncam) + 255) & ~(size_t)255;
+}
+
+extern "C" size_t fvv_carve_workspace_bytes(const fvv_camera *cams, int ncam) {
+  if (!cams || ncam < 1 || ncam > FVV_MAX_CAMS) return 0;
+  return affine_bytes() + 256 + cells_bytes(cams, ncam) +
+         sizeof(unsigned long long) * (1 + (size_t)kAmbCap);
 }
 
 extern "C" int fvv_carve(const fvv_camera *cams, int ncam, const uint32_t *sil_dev,
@@ -369,9 +573,27 @@ extern "C" int fvv_carve(const fvv_camera *cams, int ncam, const uint32_t *sil_d
   p.sil = sil_dev;
   p.occ = occ_dev;
   p.count = count_dev;
-  const bool deferred = workspace && ws_bytes >= fvv_carve_workspace_bytes();
-  p.amb = deferred ? (unsigned long long *)workspace : nullptr;
-  p.amb_cap = deferred ? kAmbCap : 0;
+  const size_t need = fvv_carve_workspace_bytes(cams, ncam);
+  if (!workspace || ws_bytes < need) {
+    set_error("fvv_carve: workspace of %zu bytes needed", need);
+    return FVV_E_ARG;
+  }
+  char *ws = (char *)workspace;
+  p.affine = (const CamAffine *)ws;
+  p.tile_stats = (unsigned long long *)(ws + affine_bytes());
+  p.cell_any = (uint32_t *)(ws + affine_bytes() + 256);
+  p.cell_all = p.cell_any + cell_words_total(cams, ncam);
+  p.amb = (unsigned long long *)(ws + affine_bytes() + 256 + cells_bytes(cams, ncam));
+  {
+    int64_t off = 0;
+    for (int c = 0; c < ncam; ++c) {
+      p.cell_off[c] = off;
+      p.cell_words[c] = (((cams[c].width + 7) >> 3) + 31) >> 5;
+      off += (int64_t)((cams[c].height + 7) >> 3) * p.cell_words[c];
+    }
+    p.cell_total = off;
+  }
+  p.amb_cap = kAmbCap;
   // phase-1 cameras: up to 4 spread evenly through the rig order (ring rigs:
   // roughly orthogonal views), then the rest in rig order
   p.k1 = ncam < 4 ? ncam : 4;
@@ -391,6 +613,12 @@ extern "C" int fvv_carve(const fvv_camera *cams, int ncam, const uint32_t *sil_d
     p.sil_off[c] = sil_word_off[c];
     p.sil_stride[c] = sil_stride_words(cams[c].width);
   }
+  // large grids (the sparse stage grid) use 16^3 tiles: mostly empty space,
+  // culled whole; ROI grids use 8^3 tiles
+  int64_t biggest = 0;
+  for (int g = 0; g < ngrid; ++g)
+    biggest = std::max(biggest, grids[g].dims[0] * grids[g].dims[1] * grids[g].dims[2]);
+  p.tile_log2 = biggest >= (int64_t)4 << 20 ? 4 : 3;
   p.blk_start[0] = 0;
   for (int g = 0; g < ngrid; ++g) {
     p.grids[g] = grids[g];
@@ -400,8 +628,12 @@ extern "C" int fvv_carve(const fvv_camera *cams, int ncam, const uint32_t *sil_d
       set_error("fvv_carve: grid %d has no voxels", g);
       return FVV_E_ARG;
     }
-    int64_t words = (nvox + 31) / 32;
-    p.blk_start[g + 1] = p.blk_start[g] + (words + kCarveWordsPerBlock - 1) / kCarveWordsPerBlock;
+    const int64_t kT = 1 << p.tile_log2;
+    p.tiles_x[g] = (uint32_t)((grids[g].dims[0] + kT - 1) / kT);
+    p.tiles_y[g] = (uint32_t)((grids[g].dims[1] + kT - 1) / kT);
+    const int64_t tiles = ((grids[g].dims[0] + kT - 1) / kT) * ((grids[g].dims[1] + kT - 1) / kT) *
+                          ((grids[g].dims[2] + kT - 1) / kT);
+    p.blk_start[g + 1] = p.blk_start[g] + tiles;
   }
   for (int g = ngrid; g < FVV_MAX_GRIDS; ++g) p.blk_start[g + 1] = p.blk_start[ngrid];
   int64_t blocks = p.blk_start[ngrid];
@@ -409,12 +641,13 @@ extern "C" int fvv_carve(const fvv_camera *cams, int ncam, const uint32_t *sil_d
     set_error("fvv_carve: %lld blocks", (long long)blocks);
     return FVV_E_LIMIT;
   }
-  if (deferred) cudaMemsetAsync(workspace, 0, sizeof(unsigned long long), st);
+  cudaMemsetAsync(p.tile_stats, 0, 256, st);
+  cudaMemsetAsync(p.amb, 0, sizeof(unsigned long long), st);
+  carve_affine_kernel<<<(ngrid * ncam + 127) / 128, 128, 0, st>>>(p, (CamAffine *)workspace);
+  carve_zero_kernel<<<148 * 2, 256, 0, st>>>(p);
+  carve_cells_kernel<<<(unsigned)((cell_words_total(cams, ncam) + 255) / 256), 256, 0, st>>>(p);
   carve_kernel<<<(unsigned)blocks, kCarveThreads, 0, st>>>(p);
-  note_launches(1);
-  if (deferred) {
-    carve_exact_kernel<<<148 * 4, kCarveThreads, 0, st>>>(p);
-    note_launches(1);
-  }
+  carve_exact_kernel<<<148 * 4, kCarveThreads, 0, st>>>(p);
+  note_launches(5);
   return cuda_check("fvv_carve");
 }

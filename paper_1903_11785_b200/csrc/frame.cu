@@ -21,7 +21,7 @@ int fvv_pack_silhouettes(const fvv_camera *, int, const uint8_t *, const int64_t
                          const int64_t *, void *);
 int fvv_carve(const fvv_camera *, int, const uint32_t *, const int64_t *, const fvv_grid *, int,
               const int64_t *, int, uint32_t *, int64_t *, void *, size_t, void *);
-size_t fvv_carve_workspace_bytes(void);
+size_t fvv_carve_workspace_bytes(const fvv_camera *, int);
 size_t fvv_ccl_workspace_bytes(const fvv_grid *);
 int fvv_ccl26(const uint32_t *, const fvv_grid *, void *, size_t, fvv_component *, int64_t,
               int64_t *, void *);
@@ -280,7 +280,7 @@ fvv_frame *fvv_frame_create(const fvv_camera *cams, int ncam, const fvv_frame_co
       f->cnt_c.ensure(64) || f->ccl_counts.ensure(64) ||
       f->ccl_ws.ensure(fvv_ccl_workspace_bytes(&f->coarse)) ||
       f->comps.ensure(sizeof(fvv_component) * 4096) || f->mesh_totals.ensure(64) ||
-      f->ntri.ensure(64) || f->carve_ws.ensure(fvv_carve_workspace_bytes()) ||
+      f->ntri.ensure(64) || f->carve_ws.ensure(fvv_carve_workspace_bytes(f->cams.data(), f->ncam)) ||
       host_small_ensure(f, 1 << 20)) {
     delete f;
     return nullptr;

@@ -125,7 +125,8 @@ def carve_grids(dsils: DeviceSilhouettes, specs, min_views: int = 1):
         word_off[1:] = np.cumsum(words)[:-1]
     bits = torch.empty(max(int(sum(words)), 1), dtype=torch.int32, device=dev)
     counts = torch.zeros(max(len(specs), 1), dtype=torch.int64, device=dev)
-    ws_bytes = int(_lib.load().fvv_carve_workspace_bytes())
+    ws_bytes = int(_lib.load().fvv_carve_workspace_bytes(_lib.host_ptr(dsils.cams),
+                                                         ctypes.c_int(dsils.ncam)))
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)  # stream-ordered reuse
     for b0 in range(0, len(specs), _lib.FVV_MAX_GRIDS):
         chunk = specs[b0:b0 + _lib.FVV_MAX_GRIDS]

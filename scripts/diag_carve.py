@@ -13,7 +13,7 @@ ex = FrameExecutor(wl.cfg, wl.rig)
 out = ex.run(masks)
 ds = DeviceSilhouettes(wl.rig, masks)
 lib = _lib.load()
-wsb = int(lib.fvv_carve_workspace_bytes())
+wsb = int(lib.fvv_carve_workspace_bytes(_lib.host_ptr(ds.cams), ctypes.c_int(ds.ncam)))
 ws = torch.zeros(wsb, dtype=torch.uint8, device="cuda")
 coarse = grid_table([wl.cfg.coarse_spec()])
 for name, tab in (("coarse", coarse), ("fine", np.ascontiguousarray(out.grids))):
@@ -33,6 +33,13 @@ for name, tab in (("coarse", coarse), ("fine", np.ascontiguousarray(out.grids)))
     a.record()
     for _ in range(20): call()
     b.record(); torch.cuda.synchronize()
-    deferred = int(ws[:8].view(torch.int64).item())
+    aff = (96 * 128 * 64 + 255) & ~255
+    st = ws[aff:aff + 24].view(torch.int64).tolist()
+    cells = 16 * 135 * 8 * 2 * 4
+    deferred = int(ws[wsb - (1 + (1 << 20)) * 8:wsb - (1 << 20) * 8].view(torch.int64).item())
+    T = 16 if max(int(np.prod(g["dims"])) for g in tab) >= 4 << 20 else 8
+    ntiles = sum(((int(g["dims"][0]) + T - 1) // T) * ((int(g["dims"][1]) + T - 1) // T) * ((int(g["dims"][2]) + T - 1) // T) for g in tab)
+    live = ntiles - st[0]
+    print(f"  tiles {ntiles}, culled {st[0]}, per live tile: fg cams {st[1] / max(live, 1):.2f}, mixed {st[2] / max(live, 1):.2f}")
     print(f"{name}: {sum(nvox)} voxels, {int(cnt.sum())} ON, deferred {deferred}, "
           f"{a.elapsed_time(b) / 20 * 1e3:.1f} us/launch pair")
