@@ -236,6 +236,7 @@ def run_b200(args):
     H, W = cams[0].image_height, cams[0].image_width
     top = max(stage_ms, key=stage_ms.get)
     roof = roofline_for(top, stage_ms[top], work, ncam, H, W, hbm_peak, peak_src)
+    roof_stages = stage_rooflines(stage_ms, work, ncam, H, W, hbm_peak, peak_src)
 
     # ---- e2e through the public API from pinned host memory ----
     e2e = None
@@ -315,6 +316,7 @@ def run_b200(args):
             "triangles_per_frame": int(work["tris"] / max(args.steps, 1)),
             "stage_ms": {k: round(v, 4) for k, v in stage_ms.items()},
             "roofline": roof,
+            "roofline_stages": roof_stages,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
@@ -355,6 +357,46 @@ def roofline_for(stage, ms, work, ncam, H, W, hbm_peak, peak_src):
             "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
             "frac": round(achieved / hbm_peak, 5), "traffic": None,
             "algorithmic_bytes": int(nbytes), "ms_per_launch": round(ms, 4)}
+
+
+FP32_LANES_PER_SM = 128  # B200: 128 FP32 lanes per SM
+FLOP_PER_PROJECTION = 26  # 13 FMA-pipe ops per voxel-projection
+
+
+def stage_rooflines(stage_ms, work, ncam, H, W, hbm_peak, peak_src):
+    """BASELINE.md 2's per-stage rooflines: the carves against FP32 issue in
+    voxel-projections/s (algorithmic projections = every voxel x every
+    camera, as hull.py:83-90 computes them; culling and early exits do not
+    reduce the count), CCL against HBM."""
+    import torch
+
+    props = torch.cuda.get_device_properties(0)
+    sm_mhz = 1965.0
+    try:
+        with open(MEASURED_PEAKS) as fh:
+            sm_mhz = float(json.load(fh).get("sm_max_mhz", sm_mhz))
+    except Exception:  # noqa: BLE001
+        pass
+    fp32_tflops = props.multi_processor_count * FP32_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12
+    proj_peak = fp32_tflops * 1e12 / FLOP_PER_PROJECTION  # voxel-projections/s
+    nvox_c, nvox_f = work["last"]
+    out = {}
+    for stage, nvox in (("sparse_carve", nvox_c), ("dense_carve", nvox_f)):
+        ms = stage_ms[stage]
+        rate = nvox * ncam / (ms / 1e3)
+        out[stage] = {"bound": "fp32_issue", "achieved": round(rate / 1e12, 4),
+                      "peak": round(proj_peak / 1e12, 4), "unit": "T voxel-proj/s",
+                      "frac": round(rate / proj_peak, 4), "ms": round(ms, 4),
+                      "peak_basis": f"{props.multi_processor_count} SMs x 128 FP32 x 2 x "
+                                    f"{sm_mhz:.0f} MHz / 26 FLOP"}
+    ms = stage_ms["noise_filter_roi"]
+    ccl_bytes = nvox_c / 8 + 4 * nvox_c
+    gbs = ccl_bytes / (ms / 1e3) / 1e9
+    out["noise_filter_roi"] = {"bound": "hbm", "achieved": round(gbs, 2), "peak": hbm_peak,
+                               "unit": "GB/s", "frac": round(gbs / hbm_peak, 5),
+                               "ms": round(ms, 4), "algorithmic_bytes": int(ccl_bytes),
+                               "peak_source": peak_src}
+    return out
 
 
 # ---------------------------------------------------------------- CPU arm
