@@ -257,12 +257,21 @@ def run_b200(args):
             return (m.vertices.nbytes + m.triangles.nbytes + m.object_ids.nbytes + vis_bytes +
                     img.color.nbytes + img.source.nbytes + img.covered.nbytes)
 
+        trace = os.environ.get("FVV_BENCH_TRACE")
+
         def run_e2e(nsteps):
             fr = [host[i % len(host)][1] for i in range(nsteps)]
             ms_ = [host[i % len(host)][0] for i in range(nsteps)]
             total = 0
+            t_prev = time.perf_counter()
+            gaps = []
             for bundle, img in run_sequence(cfg, rig, fr, ms_, virt):
                 total += d2h_bytes(bundle, img)
+                t_now = time.perf_counter()
+                gaps.append(round((t_now - t_prev) * 1e3, 2))
+                t_prev = t_now
+            if trace:
+                print(f"e2e intervals (ms): {gaps}", file=sys.stderr)
             return total
 
         # warm-up covers every distinct input on every lane (buffer growth,

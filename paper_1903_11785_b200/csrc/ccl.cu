@@ -155,24 +155,26 @@ __device__ __forceinline__ int32_t rank_of(const uint32_t *occ, const int32_t *w
 // -- 2. union over the 13 negative neighbours --------------------------------
 __global__ void ccl_union_kernel(const uint32_t *__restrict__ occ, CclWs w, int64_t nx, int64_t ny,
                                  int64_t nz) {
+  // one thread per (ON voxel, backward neighbour offset): the union work is
+  // a few dependent finds per thread instead of 13 in a row (at C3 only
+  // ~12k voxels are ON, so per-voxel threads left the GPU latency-bound)
   const int64_t n_on = __ldcg(w.counts);
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_on;
-       r += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < 13 * n_on;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / 13;
+    const int o = (int)(e - 13 * r);
     const int64_t l = w.on_list[r];
     const int64_t i = l % nx, j = (l / nx) % ny, k = l / (nx * ny);
-#pragma unroll
-    for (int o = 0; o < 13; ++o) {
-      // offsets with (dk, dj, di) lexicographically negative (hull.py:124-133)
-      const int dk = o < 9 ? -1 : 0;
-      const int rem = o < 9 ? o : o - 9;
-      const int dj = rem / 3 - 1;
-      const int di = rem % 3 - 1;
-      const int64_t ii = i + di, jj = j + dj, kk = k + dk;
-      if (ii < 0 || jj < 0 || kk < 0 || ii >= nx || jj >= ny || kk >= nz) continue;
-      const int64_t m = ii + nx * (jj + ny * kk);
-      if (!occ_bit(occ, m)) continue;
-      uf_unite(w.parent, (int32_t)r, rank_of(occ, w.word_prefix, m));
-    }
+    // offsets with (dk, dj, di) lexicographically negative (hull.py:124-133)
+    const int dk = o < 9 ? -1 : 0;
+    const int rem = o < 9 ? o : o - 9;
+    const int dj = rem / 3 - 1;
+    const int di = rem % 3 - 1;
+    const int64_t ii = i + di, jj = j + dj, kk = k + dk;
+    if (ii < 0 || jj < 0 || kk < 0 || ii >= nx || jj >= ny || kk >= nz) continue;
+    const int64_t m = ii + nx * (jj + ny * kk);
+    if (!occ_bit(occ, m)) continue;
+    uf_unite(w.parent, (int32_t)r, rank_of(occ, w.word_prefix, m));
   }
 }
 

@@ -335,33 +335,38 @@ struct ClassifyArgs {
 };
 
 __global__ void classify_kernel(const __grid_constant__ RasterCams C, ClassifyArgs A) {
+  // one thread per triangle, 32 consecutive triangles (one visibility word)
+  // per warp: the centroid (three divisions) is computed once and projected
+  // into every camera, instead of once per (camera, triangle)
   const int64_t nt = device_count(A.nt_dev, A.nt);
   const bool gemv = nt == 1;
   const int lane = threadIdx.x & 31;
   const int64_t words = (nt + 31) / 32;
-  const int64_t total = words * C.ncam * 32;
-  for (int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; w0 < total;
+  for (int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; w0 < words * 32;
        w0 += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t word = w0 >> 5;
-    const int c = (int)(word / words);
-    const int64_t wi = word - (int64_t)c * words;
-    const int64_t t = wi * 32 + lane;
-    bool vis = false;
+    const int64_t wi = w0 >> 5;
+    const int64_t t = w0 + lane;
+    double mx = 0.0, my = 0.0, mz = 0.0;
     if (t < nt) {
-      const fvv_camera &cam = C.cams[c];
       const double *a = A.V + 3 * (int64_t)A.T[3 * t], *b = A.V + 3 * (int64_t)A.T[3 * t + 1],
                    *cc = A.V + 3 * (int64_t)A.T[3 * t + 2];
-      const double mx = ((a[0] + b[0]) + cc[0]) / 3.0;  // mesh.py:84-85 mean
-      const double my = ((a[1] + b[1]) + cc[1]) / 3.0;
-      const double mz = ((a[2] + b[2]) + cc[2]) / 3.0;
-      double u, v, z;
-      if (project_exact(cam, mx, my, mz, false, gemv, u, v, z)) {
-        const int64_t p = (int64_t)rint(v) * cam.width + (int64_t)rint(u);
-        vis = (z - A.depth[C.depth_off[c] + p]) <= A.t_v;
-      }
+      mx = ((a[0] + b[0]) + cc[0]) / 3.0;  // mesh.py:84-85 mean
+      my = ((a[1] + b[1]) + cc[1]) / 3.0;
+      mz = ((a[2] + b[2]) + cc[2]) / 3.0;
     }
-    const uint32_t bits = __ballot_sync(0xffffffffu, vis);
-    if (lane == 0) A.vis[(int64_t)c * A.vis_stride + wi] = bits;
+    for (int c = 0; c < C.ncam; ++c) {
+      bool vis = false;
+      if (t < nt) {
+        const fvv_camera &cam = C.cams[c];
+        double u, v, z;
+        if (project_exact(cam, mx, my, mz, false, gemv, u, v, z)) {
+          const int64_t p = (int64_t)rint(v) * cam.width + (int64_t)rint(u);
+          vis = (z - __ldg(A.depth + C.depth_off[c] + p)) <= A.t_v;
+        }
+      }
+      const uint32_t bits = __ballot_sync(0xffffffffu, vis);
+      if (lane == 0) A.vis[(int64_t)c * A.vis_stride + wi] = bits;
+    }
   }
 }
 
