@@ -283,6 +283,44 @@ __device__ __forceinline__ void bresenham_px(int ax, int ay, int bx, int by, int
 // lam_i = |last fg pixel - px_on| / |px_off - px_on| clipped to [0,1], 1 if
 // unconstrained, 0 if the start pixel is background; min over cameras
 // (strict <: ties keep the lower id). sel = camera slot or -1 (lam = 0.5).
+// One camera's term of mesh.py:231-272 for one edge: valid (both endpoints
+// in frustum), lam_i, and whether the walk starts on background.
+__device__ __forceinline__ bool edge_lambda_cam(const fvv_camera &cam,
+                                                const uint32_t *__restrict__ plane, int stride,
+                                                const double *pon, const double *poff,
+                                                bool gemv, double &lam_i, bool &incons) {
+  double uo, vo, zo, uf, vf, zf;
+  const bool ino = project_exact(cam, pon[0], pon[1], pon[2], true, gemv, uo, vo, zo);
+  const bool inf = project_exact(cam, poff[0], poff[1], poff[2], true, gemv, uf, vf, zf);
+  incons = false;
+  if (!(ino && inf)) return false;
+  const int ax = (int)rint(uo), ay = (int)rint(vo), bx = (int)rint(uf), by = (int)rint(vf);
+  const int len = max(abs(bx - ax), abs(by - ay)) + 1;
+  int first_bg = -1;
+  for (int t = 0; t < len; ++t) {
+    int x, y;
+    bresenham_px(ax, ay, bx, by, t, x, y);
+    if (!sil_bit(plane, stride, x, y)) {
+      first_bg = t;
+      break;
+    }
+  }
+  const double ddx = uf - uo, ddy = vf - vo;
+  const double denom = sqrt(ddx * ddx + ddy * ddy);
+  lam_i = 1.0;
+  if (first_bg == 0) {
+    incons = true;
+    lam_i = 0.0;
+  } else if (first_bg > 0 && denom > 1e-12) {
+    int lx, ly;
+    bresenham_px(ax, ay, bx, by, first_bg - 1, lx, ly);
+    const double ex = (double)lx - uo, ey = (double)ly - vo;
+    const double qv = sqrt(ex * ex + ey * ey) / denom;
+    lam_i = qv > 1.0 ? 1.0 : qv;
+  }
+  return true;
+}
+
 __device__ __forceinline__ double edge_lambda(const MeshCams &C, const uint32_t *__restrict__ sil,
                                               const double *pon, const double *poff, bool gemv,
                                               int &sel, int &incons) {
@@ -290,36 +328,12 @@ __device__ __forceinline__ double edge_lambda(const MeshCams &C, const uint32_t 
   sel = -1;
   incons = 0;
   for (int c = 0; c < C.ncam; ++c) {
-    const fvv_camera &cam = C.cams[c];
-    double uo, vo, zo, uf, vf, zf;
-    const bool ino = project_exact(cam, pon[0], pon[1], pon[2], true, gemv, uo, vo, zo);
-    const bool inf = project_exact(cam, poff[0], poff[1], poff[2], true, gemv, uf, vf, zf);
-    if (!(ino && inf)) continue;
-    const int ax = (int)rint(uo), ay = (int)rint(vo), bx = (int)rint(uf), by = (int)rint(vf);
-    const int len = max(abs(bx - ax), abs(by - ay)) + 1;
-    const uint32_t *plane = sil + C.sil_off[c];
-    int first_bg = -1;
-    for (int t = 0; t < len; ++t) {
-      int x, y;
-      bresenham_px(ax, ay, bx, by, t, x, y);
-      if (!sil_bit(plane, C.sil_stride[c], x, y)) {
-        first_bg = t;
-        break;
-      }
-    }
-    const double ddx = uf - uo, ddy = vf - vo;
-    const double denom = sqrt(ddx * ddx + ddy * ddy);
-    double lam_i = 1.0;
-    if (first_bg == 0) {
-      ++incons;
-      lam_i = 0.0;
-    } else if (first_bg > 0 && denom > 1e-12) {
-      int lx, ly;
-      bresenham_px(ax, ay, bx, by, first_bg - 1, lx, ly);
-      const double ex = (double)lx - uo, ey = (double)ly - vo;
-      const double qv = sqrt(ex * ex + ey * ey) / denom;
-      lam_i = qv > 1.0 ? 1.0 : qv;
-    }
+    double lam_i;
+    bool inc;
+    if (!edge_lambda_cam(C.cams[c], sil + C.sil_off[c], C.sil_stride[c], pon, poff, gemv, lam_i,
+                         inc))
+      continue;
+    incons += inc;
     if (lam_i < lam) {
       lam = lam_i;
       sel = c;
@@ -407,48 +421,79 @@ __device__ __forceinline__ int cell_case(const MeshBufs &B, const MeshGridInfo &
 }
 
 // ---- B2: surface-cell list, per-slot keep bits (mesh.py:339-373) ------------
+__device__ __forceinline__ void mesh_cell(const MeshGrids &G, const MeshBufs &B, int64_t e,
+                                          int b, int64_t c) {
+  int lo = 0, hi = G.ngrid - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (G.tw_start[mid] <= e) lo = mid; else hi = mid - 1;
+  }
+  const int g = lo;
+  const MeshGridInfo &gi = G.gi[g];
+  const int64_t rw = e - G.tw_start[g];
+  const int64_t q = rw / gi.nzw, w = rw - q * gi.nzw;
+  const int64_t ny = gi.g.dims[1];
+  const int64_t i = q / ny, j = q - i * ny;
+  const int64_t k = w * 32 + b;
+  const int ci = cell_case(B, gi, q, k);
+  const int ntri = c_mc_ntri[ci];
+  const unsigned long long edges = c_mc_edges[ci];
+  int keep = 0;
+  for (int t = 0; t < ntri; ++t) {
+    const int64_t v0 = edge_vertex(G, B, g, i, j, k, (int)((edges >> (12 * t)) & 15));
+    const int64_t v1 = edge_vertex(G, B, g, i, j, k, (int)((edges >> (12 * t + 4)) & 15));
+    const int64_t v2 = edge_vertex(G, B, g, i, j, k, (int)((edges >> (12 * t + 8)) & 15));
+    // reversed winding (v2, v1, v0); area as numpy: 0.5*|cross(B-A, C-A)|
+    const double *A = B.verts + 3 * v2, *Bv = B.verts + 3 * v1, *Cv = B.verts + 3 * v0;
+    const double a0 = Bv[0] - A[0], a1 = Bv[1] - A[1], a2 = Bv[2] - A[2];
+    const double b0 = Cv[0] - A[0], b1 = Cv[1] - A[1], b2 = Cv[2] - A[2];
+    const double c0 = a1 * b2 - a2 * b1;
+    const double c1 = a2 * b0 - a0 * b2;
+    const double c2 = a0 * b1 - a1 * b0;
+    const double area = 0.5 * sqrt((c0 * c0 + c1 * c1) + c2 * c2);
+    if (area > kDegenerateArea) keep |= 1 << t;
+  }
+  B.cell_key[c] = e * 32 + b;
+  B.cell_mask[c] = ci | (keep << 8);
+}
+
+// Surface cells, warp-cooperatively: a warp loads 32 consecutive surface-cell
+// words, scans their popcounts, and hands the cells out one per lane (owner
+// word by a shuffle binary search, then the n-th set bit), so sparse words
+// do not leave lanes idle.
 __global__ void mesh_cells_kernel(const __grid_constant__ MeshGrids G, MeshBufs B) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < G.tw_total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t f = B.sflags[e];
-    if (!f) continue;
-    int lo = 0, hi = G.ngrid - 1;
-    while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (G.tw_start[mid] <= e) lo = mid; else hi = mid - 1;
+  const int lane = threadIdx.x & 31;
+  for (int64_t e0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; e0 < G.tw_total;
+       e0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = e0 + lane;
+    const uint32_t f = e < G.tw_total ? B.sflags[e] : 0u;
+    const int cnt = __popc(f);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
     }
-    const int g = lo;
-    const MeshGridInfo &gi = G.gi[g];
-    const int64_t rw = e - G.tw_start[g];
-    const int64_t q = rw / gi.nzw, w = rw - q * gi.nzw;
-    const int64_t ny = gi.g.dims[1];
-    const int64_t i = q / ny, j = q - i * ny;
-    int64_t c = B.sprefix[e];
-    while (f) {
-      const int b = __ffs(f) - 1;
-      f &= f - 1;
-      const int64_t k = w * 32 + b;
-      const int ci = cell_case(B, gi, q, k);
-      const int ntri = c_mc_ntri[ci];
-      const unsigned long long edges = c_mc_edges[ci];
-      int keep = 0;
-      for (int t = 0; t < ntri; ++t) {
-        const int64_t v0 = edge_vertex(G, B, g, i, j, k, (int)((edges >> (12 * t)) & 15));
-        const int64_t v1 = edge_vertex(G, B, g, i, j, k, (int)((edges >> (12 * t + 4)) & 15));
-        const int64_t v2 = edge_vertex(G, B, g, i, j, k, (int)((edges >> (12 * t + 8)) & 15));
-        // reversed winding (v2, v1, v0); area as numpy: 0.5*|cross(B-A, C-A)|
-        const double *A = B.verts + 3 * v2, *Bv = B.verts + 3 * v1, *Cv = B.verts + 3 * v0;
-        const double a0 = Bv[0] - A[0], a1 = Bv[1] - A[1], a2 = Bv[2] - A[2];
-        const double b0 = Cv[0] - A[0], b1 = Cv[1] - A[1], b2 = Cv[2] - A[2];
-        const double c0 = a1 * b2 - a2 * b1;
-        const double c1 = a2 * b0 - a0 * b2;
-        const double c2 = a0 * b1 - a1 * b0;
-        const double area = 0.5 * sqrt((c0 * c0 + c1 * c1) + c2 * c2);
-        if (area > kDegenerateArea) keep |= 1 << t;
+    const int sum = __shfl_sync(0xffffffffu, incl, 31);
+    if (sum == 0) continue;
+    for (int base = 0; base < sum; base += 32) {
+      const int idx = base + lane;
+      int own = 0;  // number of lanes whose inclusive count is <= idx
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const int v = __shfl_sync(0xffffffffu, incl, own + step - 1);
+        if (v <= idx) own += step;
       }
-      B.cell_key[c] = e * 32 + b;
-      B.cell_mask[c] = ci | (keep << 8);
-      ++c;
+      const int own_incl = __shfl_sync(0xffffffffu, incl, own);
+      const int own_cnt = __shfl_sync(0xffffffffu, cnt, own);
+      uint32_t of = __shfl_sync(0xffffffffu, f, own);
+      if (idx < sum) {
+        const int n = idx - (own_incl - own_cnt);
+        for (int j = 0; j < n; ++j) of &= of - 1;
+        const int bit = __ffs(of) - 1;
+        const int64_t ew = e0 + own;
+        mesh_cell(G, B, ew, bit, B.sprefix[ew] + n);
+      }
     }
   }
 }
@@ -752,7 +797,9 @@ int fvv_mesh_emit(const fvv_camera *cams_by_id, int ncam, const uint32_t *sil_de
   Slot5 *d_total = (Slot5 *)((char *)ws_dev + L.slot5 + sizeof(int64_t) * 5 * ngrid);
   if (num_vertices > 0) {
     mesh_vertex_list_kernel<<<kMeshGrid, 256, 0, st>>>(h_grids, B);
-    mesh_lambda_kernel<<<kMeshGrid, 128, 0, st>>>(h_grids, h_cams, B, sil_dev);
+    // one vertex per thread (latency-bound float64 chains want many warps)
+    const int64_t lam_blocks = std::min<int64_t>(num_vertices / 128 + 1, 148 * 64);
+    mesh_lambda_kernel<<<(unsigned)lam_blocks, 128, 0, st>>>(h_grids, h_cams, B, sil_dev);
     note_launches(2);
   }
   if (num_cells > 0) {
