@@ -803,7 +803,9 @@ int fvv_mesh_emit(const fvv_camera *cams_by_id, int ncam, const uint32_t *sil_de
     note_launches(2);
   }
   if (num_cells > 0) {
-    mesh_cells_kernel<<<kMeshGrid, 256, 0, st>>>(h_grids, B);
+    const int64_t cell_blocks = std::min<int64_t>(h_grids.tw_total / 256 + 1, 148 * 64);
+    mesh_cells_kernel<<<(unsigned)std::max<int64_t>(cell_blocks, kMeshGrid), 256, 0, st>>>(h_grids,
+                                                                                          B);
     note_launches(1);
     TriScan ts{B.cell_mask, B.cprefix};
     ordered_scan(ts, B.totals + 1, 0, cell_sums, d_total, st);

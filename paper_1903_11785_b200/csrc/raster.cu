@@ -12,6 +12,7 @@
 // the depth bits; pass 2 (only when ids are wanted) re-evaluates the
 // identical depth and atomicMin's the id where it equals the stored depth.
 // Integer atomics only; results do not depend on scheduling.
+#include <cstdlib>
 #include <cstring>
 
 #include "fvv_common.cuh"
@@ -603,7 +604,7 @@ int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int
   }
   for (int pass = 0; pass < (tri_id_dev ? 2 : 1); ++pass) {
     A.pass = pass;
-    raster_small_kernel<<<kRasterGrid, kRasterThreads, 0, st>>>(C, A);
+    raster_small_kernel<<<148 * 64, kRasterThreads, 0, st>>>(C, A);  // measured best of 16..128
     raster_big_kernel<<<148 * 4, kBigThreads, 0, st>>>(C, A);
     note_launches(2);
   }
