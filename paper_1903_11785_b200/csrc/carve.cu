@@ -28,7 +28,7 @@ struct CarveParams {
   const uint32_t *sil;
   uint32_t *occ;
   int64_t *count;
-  unsigned long long *amb;  // [0] = queued voxels, then (grid << 40 | voxel) entries
+  unsigned long long *amb;  // [0] = queued voxels, then {key, camera mask} entries
   int64_t amb_cap;
   const struct CamAffine *affine;  // [ngrid][ncam] (carve_affine_kernel)
   unsigned long long *tile_stats;  // culled tiles, sum of fg cameras, sum of mixed cameras
@@ -171,16 +171,19 @@ __device__ __forceinline__ int classify32(const CamAffine &a, float fi, float fj
   return amb ? kAmb : (in ? kIn : kOut);
 }
 
-// The reference's float64 chain for one voxel (hull.py:83-91).
-__device__ __forceinline__ bool carve_exact(const CarveParams &p, const fvv_grid &G, int64_t l) {
+// The reference's float64 chain for one voxel (hull.py:83-91), over the
+// cameras in cam_mask (bit c); seen / the result carry the decided rest.
+__device__ __forceinline__ bool carve_exact(const CarveParams &p, const fvv_grid &G, int64_t l,
+                                            unsigned long long cam_mask, int seen) {
   const int64_t nx = G.dims[0], ny = G.dims[1];
   const int64_t nvox = nx * ny * G.dims[2];
   const int64_t i = l % nx, j = (l / nx) % ny, k = l / (nx * ny);
   double x, y, z;
   voxel_center(G, i, j, k, x, y, z);
   const bool gemv = (nvox % kCarveChunk == 1) && l == nvox - 1;  // 1-row BLAS chunk
-  int seen = 0;
-  for (int c = 0; c < p.ncam; ++c) {
+  while (cam_mask) {
+    const int c = __ffsll((long long)cam_mask) - 1;
+    cam_mask &= cam_mask - 1;
     double u, v, zc;
     if (!project_exact(p.cams[c], x, y, z, true, gemv, u, v, zc)) continue;
     ++seen;
@@ -228,19 +231,21 @@ __device__ __forceinline__ void test_cams(const CarveParams &p, const CamAffine 
   }
 }
 
-// A voxel no FP32 camera rejected: ON/OFF from the counts, or, when a test
-// was undecided, the float64 chain (deferred to carve_exact_kernel).
+// A voxel no FP32 camera rejected: ON/OFF from the counts, or, when some
+// tests were undecided (amb_mask, bit c), the float64 chain for those
+// cameras (deferred to carve_exact_kernel; queue entries are
+// {grid << 40 | seen << 47 | voxel, camera mask}).
 __device__ __forceinline__ bool settle(const CarveParams &p, const fvv_grid &G, int g, int64_t l,
-                                       int seen, bool amb) {
-  if (!amb) return seen >= p.min_views;
-  if (p.amb) {
-    const unsigned long long slot = atomicAdd(p.amb, 1ull);
-    if ((int64_t)slot < p.amb_cap) {
-      p.amb[1 + slot] = ((unsigned long long)g << 40) | (unsigned long long)l;
-      return false;  // its bit is set by carve_exact_kernel
-    }
+                                       int seen, unsigned long long amb_mask) {
+  if (!amb_mask) return seen >= p.min_views;
+  const unsigned long long slot = atomicAdd(p.amb, 1ull);
+  if ((int64_t)slot < p.amb_cap) {
+    p.amb[1 + 2 * slot] = ((unsigned long long)g << 40) | ((unsigned long long)seen << 47) |
+                          (unsigned long long)l;
+    p.amb[2 + 2 * slot] = amb_mask;
+    return false;  // its bit is set by carve_exact_kernel
   }
-  return carve_exact(p, G, l);
+  return carve_exact(p, G, l, amb_mask, seen);
 }
 
 // ---- tile culling ---------------------------------------------------------
@@ -355,9 +360,9 @@ __device__ int tile_camera(const CarveParams &p, const CamAffine *aff, int c, in
 
 // 8x8-pixel cell maps of every camera's silhouette bits: any / all
 // foreground over the cell's in-image pixels. One thread per 32 cells.
-__global__ void carve_cells_kernel(const __grid_constant__ CarveParams p) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < p.cell_total;
-       e += (int64_t)gridDim.x * blockDim.x) {
+__device__ __forceinline__ void carve_cells(const CarveParams &p, int bid, int nblocks) {
+  for (int64_t e = bid * (int64_t)blockDim.x + threadIdx.x; e < p.cell_total;
+       e += (int64_t)nblocks * blockDim.x) {
     int c = 0;
     while (c + 1 < p.ncam && e >= p.cell_off[c + 1]) ++c;
     const int64_t local = e - p.cell_off[c];
@@ -394,9 +399,10 @@ __global__ void carve_cells_kernel(const __grid_constant__ CarveParams p) {
 }
 
 // Per-(grid, camera) FP32 coefficients, once per launch.
-__global__ void carve_affine_kernel(const __grid_constant__ CarveParams p, CamAffine *out) {
+__device__ __forceinline__ void carve_affine(const CarveParams &p, CamAffine *out, int bid,
+                                             int nblocks) {
   const int n = p.ngrid * p.ncam;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x)
+  for (int e = bid * blockDim.x + threadIdx.x; e < n; e += nblocks * blockDim.x)
     cam_affine(p.cams[e % p.ncam], p.grids[e / p.ncam], out[e]);
 }
 
@@ -465,14 +471,15 @@ __global__ void __launch_bounds__(kCarveThreads)
     if (i > i1 || j > j1 || k > k1) continue;
     const float fi = (float)i, fj = (float)j, fk = (float)k;
     int seen = n_fg;
-    bool off = false, amb = false;
+    bool off = false;
+    unsigned long long amb = 0;
     for (int m = 0; m < nm; ++m) {
       const int c = mixed[m];
       int px, py;
       const int st = classify32(aff[c], fi, fj, fk, px, py);
       if (st == kOut) continue;
       if (st == kAmb) {
-        amb = true;
+        amb |= 1ull << c;
         continue;
       }
       ++seen;
@@ -496,27 +503,39 @@ __global__ void __launch_bounds__(kCarveThreads)
 }
 
 // Zero the occupancy words of every grid of the batch (tiles only set bits).
-__global__ void carve_zero_kernel(const __grid_constant__ CarveParams p) {
+__device__ __forceinline__ void carve_zero(const CarveParams &p, int bid, int nblocks) {
   for (int g = 0; g < p.ngrid; ++g) {
     const fvv_grid &G = p.grids[g];
     const int64_t words = (G.dims[0] * G.dims[1] * G.dims[2] + 31) / 32;
-    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < words;
-         w += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t w = bid * (int64_t)blockDim.x + threadIdx.x; w < words;
+         w += (int64_t)nblocks * blockDim.x)
       p.occ[p.word_off[g] + w] = 0u;
   }
 }
 
-// Voxels the FP32 pass left undecided: float64 chain, set their bits.
+// One launch for the per-call preparation: camera coefficients, silhouette
+// cell maps, zeroed occupancy words (block ranges of one grid).
+__global__ void carve_prep_kernel(const __grid_constant__ CarveParams p, CamAffine *aff,
+                                  int nb_aff, int nb_cells) {
+  const int b = blockIdx.x;
+  if (b < nb_aff) carve_affine(p, aff, b, nb_aff);
+  else if (b < nb_aff + nb_cells) carve_cells(p, b - nb_aff, nb_cells);
+  else carve_zero(p, b - nb_aff - nb_cells, gridDim.x - nb_aff - nb_cells);
+}
+
+// Voxels the FP32 pass left undecided: their undecided cameras through the
+// float64 chain, then set their bits.
 __global__ void __launch_bounds__(kCarveThreads)
     carve_exact_kernel(const __grid_constant__ CarveParams p) {
   int64_t n = (int64_t)__ldcg(p.amb);
   if (n > p.amb_cap) n = p.amb_cap;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
        q += (int64_t)gridDim.x * blockDim.x) {
-    const unsigned long long e = p.amb[1 + q];
-    const int g = (int)(e >> 40);
+    const unsigned long long e = p.amb[1 + 2 * q], mask = p.amb[2 + 2 * q];
+    const int g = (int)((e >> 40) & 0x7f);
+    const int seen = (int)((e >> 47) & 0x7f);
     const int64_t l = (int64_t)(e & ((1ull << 40) - 1));
-    if (carve_exact(p, p.grids[g], l)) {
+    if (carve_exact(p, p.grids[g], l, mask, seen)) {
       atomicOr(p.occ + p.word_off[g] + (l >> 5), 1u << (l & 31));
       if (p.count) atomicAdd((unsigned long long *)&p.count[g], 1ull);
     }
@@ -545,7 +564,7 @@ static size_t cells_bytes(const fvv_camera *cams, int ncam) {
 extern "C" size_t fvv_carve_workspace_bytes(const fvv_camera *cams, int ncam) {
   if (!cams || ncam < 1 || ncam > FVV_MAX_CAMS) return 0;
   return affine_bytes() + 256 + cells_bytes(cams, ncam) +
-         sizeof(unsigned long long) * (1 + (size_t)kAmbCap);
+         sizeof(unsigned long long) * (1 + 2 * (size_t)kAmbCap);
 }
 
 extern "C" int fvv_carve(const fvv_camera *cams, int ncam, const uint32_t *sil_dev,
@@ -643,11 +662,12 @@ extern "C" int fvv_carve(const fvv_camera *cams, int ncam, const uint32_t *sil_d
   }
   cudaMemsetAsync(p.tile_stats, 0, 256, st);
   cudaMemsetAsync(p.amb, 0, sizeof(unsigned long long), st);
-  carve_affine_kernel<<<(ngrid * ncam + 127) / 128, 128, 0, st>>>(p, (CamAffine *)workspace);
-  carve_zero_kernel<<<148 * 2, 256, 0, st>>>(p);
-  carve_cells_kernel<<<(unsigned)((cell_words_total(cams, ncam) + 255) / 256), 256, 0, st>>>(p);
+  const int nb_aff = (ngrid * ncam + 255) / 256;
+  const int nb_cells = (int)((cell_words_total(cams, ncam) + 255) / 256);
+  carve_prep_kernel<<<nb_aff + nb_cells + 148 * 2, 256, 0, st>>>(p, (CamAffine *)workspace, nb_aff,
+                                                                nb_cells);
   carve_kernel<<<(unsigned)blocks, kCarveThreads, 0, st>>>(p);
   carve_exact_kernel<<<148 * 4, kCarveThreads, 0, st>>>(p);
-  note_launches(5);
+  note_launches(3);
   return cuda_check("fvv_carve");
 }

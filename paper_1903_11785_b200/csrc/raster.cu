@@ -318,9 +318,16 @@ __global__ void __launch_bounds__(kBigThreads)
 }
 
 __global__ void fill_u64_kernel(unsigned long long *p, int64_t n, unsigned long long v) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = v;
+  // 16-byte stores for the aligned bulk, scalar head/tail
+  const int64_t head = ((uintptr_t)p & 15) ? 1 : 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (tid == 0 && head && n > 0) p[0] = v;
+  const int64_t n2 = (n - head) / 2;
+  ulonglong2 *q = (ulonglong2 *)(p + head);
+  const ulonglong2 vv = make_ulonglong2(v, v);
+  for (int64_t i = tid; i < n2; i += stride) q[i] = vv;
+  if (tid == 0 && head + 2 * n2 < n) p[head + 2 * n2] = v;
 }
 
 // ---- D-2: visibility.py:106-129 ------------------------------------------------
@@ -569,11 +576,18 @@ int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int
   int rc = fill_cams(C, cams, ncam, plane_off);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  // background: depth +inf, id -1 (visibility.py:44-45)
+  // background: depth +inf, id -1 (visibility.py:44-45); one fill when the
+  // planes are contiguous (the executor's layout), else one per camera
+  bool contiguous = true;
+  int64_t total_px = 0;
   for (int c = 0; c < ncam; ++c) {
-    const int64_t n = (int64_t)cams[c].width * cams[c].height;
-    fill_u64_kernel<<<256, 256, 0, st>>>((unsigned long long *)(depth_dev + plane_off[c]), n,
-                                         0x7ff0000000000000ull);
+    contiguous = contiguous && plane_off[c] == plane_off[0] + total_px;
+    total_px += (int64_t)cams[c].width * cams[c].height;
+  }
+  for (int c = 0; c < (contiguous ? 1 : ncam); ++c) {
+    const int64_t n = contiguous ? total_px : (int64_t)cams[c].width * cams[c].height;
+    fill_u64_kernel<<<148 * 8, 256, 0, st>>>((unsigned long long *)(depth_dev + plane_off[c]), n,
+                                             0x7ff0000000000000ull);
     note_launches(1);
     if (tri_id_dev) cudaMemsetAsync(tri_id_dev + plane_off[c], 0xff, 4 * n, st);
   }

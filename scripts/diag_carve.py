@@ -36,7 +36,7 @@ for name, tab in (("coarse", coarse), ("fine", np.ascontiguousarray(out.grids)))
     aff = (96 * 128 * 64 + 255) & ~255
     st = ws[aff:aff + 24].view(torch.int64).tolist()
     cells = 16 * 135 * 8 * 2 * 4
-    deferred = int(ws[wsb - (1 + (1 << 20)) * 8:wsb - (1 << 20) * 8].view(torch.int64).item())
+    deferred = int(ws[wsb - (1 + 2 * (1 << 20)) * 8:wsb - 2 * (1 << 20) * 8].view(torch.int64).item())
     T = 16 if max(int(np.prod(g["dims"])) for g in tab) >= 4 << 20 else 8
     ntiles = sum(((int(g["dims"][0]) + T - 1) // T) * ((int(g["dims"][1]) + T - 1) // T) * ((int(g["dims"][2]) + T - 1) // T) for g in tab)
     live = ntiles - st[0]
