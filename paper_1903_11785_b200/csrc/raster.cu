@@ -201,7 +201,7 @@ __device__ __forceinline__ void smem_to_setup(const TriSmem &m, TriSetup &s) {
 // their bounding-box pixels 32 at a time (each lane finds its pixel's owner
 // by a shuffle binary search over the warp's inclusive pixel-count scan), so
 // uneven bounding boxes and culled triangles do not leave lanes idle.
-__global__ void __launch_bounds__(kRasterThreads)
+__global__ void __launch_bounds__(kRasterThreads, 8)
     raster_small_kernel(const __grid_constant__ RasterCams C, RasterArgs A) {
   __shared__ TriSmem sm[kRasterThreads];
   const int lane = threadIdx.x & 31;
