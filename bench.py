@@ -10,7 +10,10 @@ across ranks (frame f -> rank f mod N, no collective on the data path:
 weak scaling). Rank 0 prints one JSON line.
 
   value : frames/s, inputs resident in HBM, device time (CUDA events,
-          barrier + synchronize on both sides, max over ranks)
+          barrier + synchronize on both sides, max over ranks), the K frames
+          spread over --lanes executor lanes (thread + CUDA stream each);
+          stage_ms / roofline come from a single-stream pass of the same K
+          frames (value_single_stream)
   e2e   : frames/s through the public API (pipeline.run_sequence =
           run_frame + render_view per frame) from pinned host buffers: H2D
           of every frame's silhouettes, the colour pass's zero-copy reads of
@@ -46,6 +49,8 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="C3")
     ap.add_argument("--frames", type=int, default=4, help="distinct input frames per rank")
+    ap.add_argument("--lanes", type=int, default=3,
+                    help="concurrent executor lanes (threads + streams) per GPU")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--stage-json", default=None, help="write per-stage ms here (rank 0)")
@@ -182,15 +187,17 @@ def run_b200(args):
 
     from paper_1903_11785_b200.executor import executor_for
 
-    ex = executor_for(cfg, rig)
+    lanes = max(1, args.lanes)
+    exs = [executor_for(cfg, rig, k) for k in range(lanes)]
+    ex = exs[0]
     stage_names = ("sparse_carve", "noise_filter_roi", "dense_carve", "polygonize",
                    "depth_images", "visibility", "render")
     stage_sum = {k: 0.0 for k in stage_names}
     work = {"proj": 0, "tris": 0, "frames": 0, "nv": 0}
 
-    def device_step(i, timed):
+    def device_step(i, timed, lane_ex=None):
         masks, fb, foff = dev_frames[i % len(dev_frames)]
-        out = ex.run(masks, virt, fb, foff)
+        out = (lane_ex or ex).run(masks, virt, fb, foff)
         if timed:
             st = out.stats_raw
             for k, ms_ in zip(stage_names, st["ms"][:7]):
@@ -203,10 +210,57 @@ def run_b200(args):
             work["frames"] += 1
             work["last"] = (int(st["sparse_tests"]), int(st["dense_tests"]))
 
+    lib = _lib.load()
+    # ---- single-stream pass: per-stage device times (roofline inputs) ----
     for i in range(args.warmup):
         device_step(i, False)
     torch.cuda.synchronize()
-    lib = _lib.load()
+    barrier(world)
+    s_start = torch.cuda.Event(enable_timing=True)
+    s_end = torch.cuda.Event(enable_timing=True)
+    s_start.record()
+    for i in range(args.steps):
+        device_step(i, True)
+    s_end.record()
+    torch.cuda.synchronize()
+    barrier(world)
+    ms_single = max_over_ranks(s_start.elapsed_time(s_end), world)
+    stage_ms = {k: v / args.steps for k, v in stage_sum.items()}
+
+    # ---- timed region: K frames over `lanes` executors (one thread and one
+    # CUDA stream each, frame i on lane i mod lanes), inputs resident in HBM ----
+    import threading
+
+    dev_index = torch.cuda.current_device()
+    streams = [torch.cuda.Stream() for _ in range(lanes)]
+
+    def run_lanes(n, base=0):
+        errors = []
+
+        def lane(k):
+            try:
+                torch.cuda.set_device(dev_index)
+                with torch.cuda.stream(streams[k]):
+                    for i in range(base + k, base + n, lanes):
+                        device_step(i, False, exs[k])
+            except BaseException as exc:  # noqa: BLE001
+                errors.append(exc)
+
+        cur = torch.cuda.current_stream()
+        for st_ in streams:
+            st_.wait_stream(cur)
+        ths = [threading.Thread(target=lane, args=(k,)) for k in range(lanes)]
+        for th in ths:
+            th.start()
+        for th in ths:
+            th.join()
+        for st_ in streams:
+            cur.wait_stream(st_)
+        if errors:
+            raise errors[0]
+
+    run_lanes(max(args.warmup, lanes) * lanes)  # every lane warm
+    torch.cuda.synchronize()
     barrier(world)
     sampler = ClockSampler(local if "CUDA_VISIBLE_DEVICES" not in os.environ else
                            os.environ["CUDA_VISIBLE_DEVICES"].split(",")[local])
@@ -216,8 +270,7 @@ def run_b200(args):
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record()
-    for i in range(args.steps):
-        device_step(i, True)
+    run_lanes(args.steps)
     t_end.record()
     torch.cuda.synchronize()
     launches = lib.fvv_launch_count() - launches0
@@ -225,11 +278,11 @@ def run_b200(args):
     clocks = sampler.stop()
     ms_local = t_start.elapsed_time(t_end)
     ms = max_over_ranks(ms_local, world)
-    stage_ms = {k: v / args.steps for k, v in stage_sum.items()}
 
     total_frames = sum_over_ranks(args.steps, world)
     total_proj = sum_over_ranks(work["proj"], world)
     value = total_frames / (ms / 1e3)
+    value_single = total_frames / (ms_single / 1e3)
 
     # ---- roofline of the dominant kernel ----
     hbm_peak, peak_src, _ = peaks()
@@ -265,7 +318,7 @@ def run_b200(args):
             total = 0
             t_prev = time.perf_counter()
             gaps = []
-            for bundle, img in run_sequence(cfg, rig, fr, ms_, virt):
+            for bundle, img in run_sequence(cfg, rig, fr, ms_, virt, lanes=lanes):
                 total += d2h_bytes(bundle, img)
                 t_now = time.perf_counter()
                 gaps.append(round((t_now - t_prev) * 1e3, 2))
@@ -290,10 +343,11 @@ def run_b200(args):
         e2e = {"value": round(total_frames / (e2e_ms / 1e3), 3), "unit": "frames/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(d2h / args.steps),
                "ms_per_step": round(e2e_ms / args.steps, 3),
-               "api": "pipeline.run_sequence (run_frame + render_view per frame; silhouettes "
-                      "uploaded one frame ahead, pinned colour frames sampled in place "
-                      "(zero-copy: h2d counts the 12 B of bilinear taps per sourced pixel), "
-                      "results read back on a third stream), pinned host inputs"}
+               "api": f"pipeline.run_sequence (run_frame + render_view per frame, {lanes} "
+                      "executor lanes; silhouettes uploaded ahead on a copy stream, pinned "
+                      "colour frames sampled in place (zero-copy: h2d counts the 12 B of "
+                      "bilinear taps per sourced pixel), results read back on a readback "
+                      "stream), pinned host inputs"}
 
     # ---- CPU baseline: the oracle port on this box's host cores, rank 0, N=1 ----
     cpu = None
@@ -320,7 +374,13 @@ def run_b200(args):
                        "frames_cycled": args.frames,
                        "l2": f"inputs cycle over {args.frames} frames x "
                              f"{(ncam * H * W * 4) / 1e6:.0f} MB (> 126 MB L2)",
-                       "parallelism": f"frame-sharded x{world}"},
+                       "parallelism": f"frame-sharded x{world}, {lanes} executor lanes "
+                                      f"per GPU",
+                       "timing": "value: K frames over the lanes (CUDA events, barrier + sync "
+                                 "both sides); stage_ms / roofline: a single-stream pass of "
+                                 "the same K frames"},
+            "value_single_stream": round(value_single, 3),
+            "lanes": lanes,
             "gvoxel_proj_per_s": round(total_proj / (ms / 1e3) / 1e9, 2),
             "triangles_per_frame": int(work["tris"] / max(args.steps, 1)),
             "stage_ms": {k: round(v, 4) for k, v in stage_ms.items()},

@@ -15,16 +15,17 @@ torch.cuda.synchronize()
 host = [(m.cpu().pin_memory(), {c.id: t for c, t in zip(cams, f.cpu().pin_memory())}) for m, f in inputs]
 EV = []
 gc.callbacks.append(lambda ph, info: EV.append((time.perf_counter(), ph, info["generation"])))
-def run(n):
+def run(n, lanes=2):
     fr = [host[i % 4][1] for i in range(n)]; ms = [host[i % 4][0] for i in range(n)]
     EV.clear(); torch.cuda.synchronize(); t0 = time.perf_counter(); ts = []
-    for b, img in run_sequence(wl.cfg, wl.rig, fr, ms, wl.virtual):
+    for b, img in run_sequence(wl.cfg, wl.rig, fr, ms, wl.virtual, lanes=lanes):
         b.merged_mesh.triangles; ts.append(time.perf_counter())
     torch.cuda.synchronize(); t1 = time.perf_counter()
     d = np.diff([t0] + ts) * 1e3
     gcs = [f"{(t - t0) * 1e3:.1f}:{ph[0]}{g}" for t, ph, g in EV]
     return (t1 - t0) / n * 1e3, d, gcs
-run(10)
-for r in range(8):
-    ms, d, gcs = run(10)
-    print(f"rep {r}: {ms:.2f} ms/frame  intervals " + " ".join(f"{x:.1f}" for x in d) + f"  gc {gcs}")
+for lanes in (1, 2, 3, 4):
+    run(12, lanes)
+    for r in range(3):
+        ms, d, gcs = run(30, lanes)
+        print(f"lanes {lanes} rep {r}: {ms:.2f} ms/frame ({1e3 / ms:.0f} fps)  first intervals " + " ".join(f"{x:.1f}" for x in d[:6]))
