@@ -57,6 +57,15 @@ __global__ void raster_vertex_kernel(const __grid_constant__ RasterCams C,
   }
 }
 
+__device__ __forceinline__ double dmin3(double a, double b, double c) {
+  const double m = a < b ? a : b;
+  return m < c ? m : c;
+}
+__device__ __forceinline__ double dmax3(double a, double b, double c) {
+  const double m = a > b ? a : b;
+  return m > c ? m : c;
+}
+
 // visibility.py:48-78 for triangle t from its projected vertices. False = skipped.
 __device__ __forceinline__ bool tri_setup(int width, int height, const double4 *__restrict__ P,
                                           const int32_t *__restrict__ T, int64_t t,
@@ -66,8 +75,9 @@ __device__ __forceinline__ bool tri_setup(int width, int height, const double4 *
   if (!(z[0] > kNearClip && z[1] > kNearClip && z[2] > kNearClip)) return false;
   if (isnan(u[0]) || isnan(u[1]) || isnan(u[2]) || isnan(v[0]) || isnan(v[1]) || isnan(v[2]))
     return false;
-  const double mnx = fmin(fmin(u[0], u[1]), u[2]), mxx = fmax(fmax(u[0], u[1]), u[2]);
-  const double mny = fmin(fmin(v[0], v[1]), v[2]), mxy = fmax(fmax(v[0], v[1]), v[2]);
+  // (no NaN past this point: plain compares instead of fmin/fmax)
+  const double mnx = dmin3(u[0], u[1], u[2]), mxx = dmax3(u[0], u[1], u[2]);
+  const double mny = dmin3(v[0], v[1], v[2]), mxy = dmax3(v[0], v[1], v[2]);
   const double flx = floor(mnx), fly = floor(mny), chx = ceil(mxx), chy = ceil(mxy);
   const double W1 = (double)(width - 1), H1 = (double)(height - 1);
   if (flx > W1 || fly > H1 || chx < 0.0 || chy < 0.0) return false;
@@ -162,16 +172,31 @@ __device__ __forceinline__ unsigned long long candidate_mask(const TriSetup &s) 
   const float m0 = ((fabsf(a0) + fabsf(b0)) * ext + fabsf(c0) + 1.0f) * k;
   const float m1 = ((fabsf(a1) + fabsf(b1)) * ext + fabsf(c1) + 1.0f) * k;
   const float m2 = ((fabsf(a2) + fabsf(b2)) * ext + fabsf(c2) + 1.0f) * k;
+  // per row gy, edge i keeps gx with b_i gx <= r_i(gy) + m_i: an interval
+  // of gx per edge, intersected, widened by 1e-3 px (the reciprocal's error
+  // is ~1e-7 relative over |gx| <= 64), turned into a run of mask bits
+  const float ib0 = __fdividef(1.0f, b0), ib1 = __fdividef(1.0f, b1), ib2 = __fdividef(1.0f, b2);
   unsigned long long mask = 0;
-  int bit = 0;
+  const float top = (float)(bw - 1);
   for (int yy = 0; yy < bh; ++yy) {
     const float gy = (float)yy;
-    const float r0 = fmaf(a0, gy, c0), r1 = fmaf(a1, gy, c1), r2 = fmaf(a2, gy, c2);
-    for (int xx = 0; xx < bw; ++xx, ++bit) {
-      const float gx = (float)xx;
-      const bool keep = fmaf(-b0, gx, r0) >= -m0 && fmaf(-b1, gx, r1) >= -m1 &&
-                        fmaf(-b2, gx, r2) >= -m2;
-      mask |= (unsigned long long)keep << bit;
+    float lo = 0.0f, hi = top;
+    bool empty = false;
+    const float sv0 = fmaf(a0, gy, c0) + m0, sv1 = fmaf(a1, gy, c1) + m1,
+                sv2 = fmaf(a2, gy, c2) + m2;
+    if (b0 > 0.0f) hi = fminf(hi, fmaf(sv0, ib0, 1e-3f));
+    else if (b0 < 0.0f) lo = fmaxf(lo, fmaf(sv0, ib0, -1e-3f));
+    else empty |= sv0 < 0.0f;
+    if (b1 > 0.0f) hi = fminf(hi, fmaf(sv1, ib1, 1e-3f));
+    else if (b1 < 0.0f) lo = fmaxf(lo, fmaf(sv1, ib1, -1e-3f));
+    else empty |= sv1 < 0.0f;
+    if (b2 > 0.0f) hi = fminf(hi, fmaf(sv2, ib2, 1e-3f));
+    else if (b2 < 0.0f) lo = fmaxf(lo, fmaf(sv2, ib2, -1e-3f));
+    else empty |= sv2 < 0.0f;
+    const int x0 = (int)ceilf(lo), x1 = (int)floorf(hi);  // NaN bounds -> empty below
+    if (!empty && x0 <= x1 && lo <= hi) {
+      const unsigned long long run = (x1 - x0 >= 63) ? ~0ull : ((2ull << (x1 - x0)) - 1ull);
+      mask |= run << (yy * bw + x0);
     }
   }
   return mask;
@@ -215,7 +240,8 @@ __global__ void __launch_bounds__(kRasterThreads, 8)
     const int64_t w = w0 + lane;
     int npx = 0;
     if (w < total) {
-      const int c = (int)(w / nt);
+      // camera-major item index; 32-bit division when the item count allows
+      const int c = total < 0xffffffffll ? (int)((uint32_t)w / (uint32_t)nt) : (int)(w / nt);
       const int64_t t = w - (int64_t)c * nt;
       TriSetup s;
       if (tri_setup(C.cams[c].width, C.cams[c].height, A.P + (int64_t)c * A.nv, A.T, t, s)) {
