@@ -173,7 +173,9 @@ __device__ __forceinline__ int classify32(const CamAffine &a, float fi, float fj
 
 // The reference's float64 chain for one voxel (hull.py:83-91), over the
 // cameras in cam_mask (bit c); seen / the result carry the decided rest.
-__device__ __forceinline__ bool carve_exact(const CarveParams &p, const fvv_grid &G, int64_t l,
+// `cams` may be a shared-memory copy (lanes index different cameras).
+__device__ __forceinline__ bool carve_exact(const CarveParams &p, const fvv_camera *cams,
+                                            const fvv_grid &G, int64_t l,
                                             unsigned long long cam_mask, int seen) {
   const int64_t nx = G.dims[0], ny = G.dims[1];
   const int64_t nvox = nx * ny * G.dims[2];
@@ -185,9 +187,10 @@ __device__ __forceinline__ bool carve_exact(const CarveParams &p, const fvv_grid
     const int c = __ffsll((long long)cam_mask) - 1;
     cam_mask &= cam_mask - 1;
     double u, v, zc;
-    if (!project_exact(p.cams[c], x, y, z, true, gemv, u, v, zc)) continue;
+    if (!project_exact(cams[c], x, y, z, true, gemv, u, v, zc)) continue;
     ++seen;
-    if (!sil_bit(p.sil + p.sil_off[c], p.sil_stride[c], (int)rint(u), (int)rint(v)))
+    if (!sil_bit(p.sil + p.sil_off[c], sil_stride_words(cams[c].width), (int)rint(u),
+                 (int)rint(v)))
       return false;
   }
   return seen >= p.min_views;
@@ -245,7 +248,7 @@ __device__ __forceinline__ bool settle(const CarveParams &p, const fvv_grid &G, 
     p.amb[2 + 2 * slot] = amb_mask;
     return false;  // its bit is set by carve_exact_kernel
   }
-  return carve_exact(p, G, l, amb_mask, seen);
+  return carve_exact(p, p.cams, G, l, amb_mask, seen);
 }
 
 // ---- tile culling ---------------------------------------------------------
@@ -527,6 +530,11 @@ __global__ void carve_prep_kernel(const __grid_constant__ CarveParams p, CamAffi
 // float64 chain, then set their bits.
 __global__ void __launch_bounds__(kCarveThreads)
     carve_exact_kernel(const __grid_constant__ CarveParams p) {
+  // lanes test different cameras: a shared-memory copy (divergent indexing of
+  // the parameter block would serialise the constant cache)
+  __shared__ fvv_camera cams[FVV_MAX_CAMS];
+  for (int c = threadIdx.x; c < p.ncam; c += blockDim.x) cams[c] = p.cams[c];
+  __syncthreads();
   int64_t n = (int64_t)__ldcg(p.amb);
   if (n > p.amb_cap) n = p.amb_cap;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
@@ -535,7 +543,7 @@ __global__ void __launch_bounds__(kCarveThreads)
     const int g = (int)((e >> 40) & 0x7f);
     const int seen = (int)((e >> 47) & 0x7f);
     const int64_t l = (int64_t)(e & ((1ull << 40) - 1));
-    if (carve_exact(p, p.grids[g], l, mask, seen)) {
+    if (carve_exact(p, cams, p.grids[g], l, mask, seen)) {
       atomicOr(p.occ + p.word_off[g] + (l >> 5), 1u << (l & 31));
       if (p.count) atomicAdd((unsigned long long *)&p.count[g], 1ull);
     }

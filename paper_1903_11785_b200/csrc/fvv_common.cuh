@@ -71,7 +71,7 @@ __device__ __forceinline__ bool sil_bit(const uint32_t *__restrict__ plane, int 
   return (w >> (x & 31)) & 1u;
 }
 
-inline int sil_stride_words(int width) { return (width + 31) >> 5; }
+__host__ __device__ inline int sil_stride_words(int width) { return (width + 31) >> 5; }
 
 // Element count produced on the device by an earlier launch, else the host
 // value. (A `p ? *p : fallback` select on a __grid_constant__ member makes
