@@ -343,17 +343,46 @@ __global__ void __launch_bounds__(kBigThreads)
   }
 }
 
-__global__ void fill_u64_kernel(unsigned long long *p, int64_t n, unsigned long long v) {
-  // 16-byte stores for the aligned bulk, scalar head/tail
+__device__ __forceinline__ void fill_u64(unsigned long long *p, int64_t n, unsigned long long v,
+                                         int64_t tid, int64_t stride) {
   const int64_t head = ((uintptr_t)p & 15) ? 1 : 0;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (tid == 0 && head && n > 0) p[0] = v;
   const int64_t n2 = (n - head) / 2;
   ulonglong2 *q = (ulonglong2 *)(p + head);
   const ulonglong2 vv = make_ulonglong2(v, v);
   for (int64_t i = tid; i < n2; i += stride) q[i] = vv;
   if (tid == 0 && head + 2 * n2 < n) p[head + 2 * n2] = v;
+}
+
+// D-1 preparation in one launch: the first nb_fill blocks fill the depth
+// planes with +inf (HBM-bound), the others project the vertices (FP64-bound),
+// so the two overlap instead of running back to back.
+__global__ void raster_prep_kernel(const __grid_constant__ RasterCams C,
+                                   const double *__restrict__ V, int64_t nv,
+                                   double4 *__restrict__ proj, unsigned long long *depth,
+                                   int64_t npx, int nb_fill) {
+  if ((int)blockIdx.x < nb_fill) {
+    fill_u64(depth, npx, 0x7ff0000000000000ull, blockIdx.x * (int64_t)blockDim.x + threadIdx.x,
+             (int64_t)nb_fill * blockDim.x);
+    return;
+  }
+  const bool gemv = nv == 1;
+  const int64_t total = nv * C.ncam;
+  const int64_t stride = (int64_t)(gridDim.x - nb_fill) * blockDim.x;
+  for (int64_t w = (blockIdx.x - nb_fill) * (int64_t)blockDim.x + threadIdx.x; w < total;
+       w += stride) {
+    const int c = (int)(w / nv);
+    const int64_t i = w - (int64_t)c * nv;
+    double u, v, z;
+    project_exact(C.cams[c], V[3 * i], V[3 * i + 1], V[3 * i + 2], false, gemv, u, v, z);
+    proj[w] = make_double4(u, v, z, 0.0);
+  }
+}
+
+__global__ void fill_u64_kernel(unsigned long long *p, int64_t n, unsigned long long v) {
+  // 16-byte stores for the aligned bulk, scalar head/tail
+  fill_u64(p, n, v, blockIdx.x * (int64_t)blockDim.x + threadIdx.x,
+           (int64_t)gridDim.x * blockDim.x);
 }
 
 // ---- D-2: visibility.py:106-129 ------------------------------------------------
@@ -610,11 +639,16 @@ int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int
     contiguous = contiguous && plane_off[c] == plane_off[0] + total_px;
     total_px += (int64_t)cams[c].width * cams[c].height;
   }
+  // contiguous planes with a mesh: the fill rides in the vertex-projection
+  // launch (raster_prep_kernel); otherwise fill here
+  const bool fused_fill = contiguous && nt > 0 && nv > 0;
   for (int c = 0; c < (contiguous ? 1 : ncam); ++c) {
     const int64_t n = contiguous ? total_px : (int64_t)cams[c].width * cams[c].height;
-    fill_u64_kernel<<<148 * 8, 256, 0, st>>>((unsigned long long *)(depth_dev + plane_off[c]), n,
-                                             0x7ff0000000000000ull);
-    note_launches(1);
+    if (!fused_fill) {
+      fill_u64_kernel<<<148 * 8, 256, 0, st>>>((unsigned long long *)(depth_dev + plane_off[c]),
+                                               n, 0x7ff0000000000000ull);
+      note_launches(1);
+    }
     if (tri_id_dev) cudaMemsetAsync(tri_id_dev + plane_off[c], 0xff, 4 * n, st);
   }
   if (nt <= 0) return cuda_check("fvv_rasterize");
@@ -639,7 +673,17 @@ int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int
   {
     int64_t blocks = (nv * ncam + 255) / 256;
     if (blocks > kRasterGrid) blocks = kRasterGrid;
-    raster_vertex_kernel<<<(int)(blocks > 0 ? blocks : 1), 256, 0, st>>>(C, verts_dev, nv, proj);
+    if (blocks < 1) blocks = 1;
+    if (fused_fill) {
+      // fill blocks in proportion to the bytes they write (~0.3 us of work per block)
+      int64_t nb_fill = total_px / (256 * 64) + 1;
+      if (nb_fill > 148 * 8) nb_fill = 148 * 8;
+      raster_prep_kernel<<<(int)(blocks + nb_fill), 256, 0, st>>>(
+          C, verts_dev, nv, proj, (unsigned long long *)(depth_dev + plane_off[0]), total_px,
+          (int)nb_fill);
+    } else {
+      raster_vertex_kernel<<<(int)blocks, 256, 0, st>>>(C, verts_dev, nv, proj);
+    }
     note_launches(1);
   }
   for (int pass = 0; pass < (tri_id_dev ? 2 : 1); ++pass) {
