@@ -573,7 +573,7 @@ def _sequence_streams(dev_index, lanes):
 
 
 def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
-                 fallback_color=None, frame_id0: int = 0, lanes: int = 3):
+                 fallback_color=None, frame_id0: int = 0, lanes: int = 4):
     """Reconstruct (and, given ``virtual``, colour) a sequence of frames.
 
     The production form of run_frame + render_view for video, pipelined over
