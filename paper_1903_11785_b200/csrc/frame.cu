@@ -69,6 +69,24 @@ struct DevBuf {
     cap = want;
     return FVV_OK;
   }
+  // grow to >= bytes keeping the first `used` bytes (stream-ordered copy;
+  // the cudaFree of the old block waits for it)
+  int grow_keep(size_t bytes, size_t used, cudaStream_t st) {
+    if (bytes <= cap && p) return FVV_OK;
+    void *old = p;
+    const size_t want = bytes + bytes / 4 + 256;
+    void *np = nullptr;
+    if (cudaMalloc(&np, want) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("frame executor: cudaMalloc(%zu) failed", want);
+      return FVV_E_CUDA;
+    }
+    if (old && used) cudaMemcpyAsync(np, old, used, cudaMemcpyDeviceToDevice, st);
+    if (old) cudaFree(old);
+    p = np;
+    cap = want;
+    return FVV_OK;
+  }
   ~DevBuf() {
     if (p) cudaFree(p);
   }
@@ -421,12 +439,9 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
     if (r0 == 0) {
       FVV_TRY(4, f->verts.ensure(24 * (size_t)(nv > 0 ? nv : 1)));
       FVV_TRY(4, f->tris.ensure(12 * (size_t)(5 * ns > 0 ? 5 * ns : 1)));
-    } else if (24 * (size_t)(v_before + nv) > f->verts.cap ||
-               12 * (size_t)(t_before + 5 * ns) > f->tris.cap) {
-      set_error("frame executor: > %d ROIs with growing outputs is not supported",
-                FVV_MAX_GRIDS);
-      if (out_stage) *out_stage = 4;
-      return FVV_E_LIMIT;
+    } else {  // later ROI batches append: grow keeping the earlier batches
+      FVV_TRY(4, f->verts.grow_keep(24 * (size_t)(v_before + nv), 24 * (size_t)v_before, st));
+      FVV_TRY(4, f->tris.grow_keep(12 * (size_t)(t_before + 5 * ns), 12 * (size_t)t_before, st));
     }
     FVV_TRY(4, fvv_mesh_emit(f->cams_by_id.data(), ncam, f->sil.as<uint32_t>(),
                              f->word_off_by_id.data(), &f->fine[r0], nb,

@@ -119,3 +119,55 @@ def test_executor_matches_staged_composition(gpu):
     for c in wl.rig:
         assert np.array_equal(a.visibility[c.id], b.visibility[c.id])
         assert np.array_equal(a.depths[c.id], b.depths[c.id])
+
+
+def test_executor_more_than_128_rois_vs_oracle(gpu):
+    """A scene whose coarse hull splits into > FVV_MAX_GRIDS (128) components:
+    the executor's batched ROI path (carve, mesh offsets across batches)
+    against the oracle frame."""
+    from paper_1903_11785_b200 import synthetic as S
+    from paper_1903_11785_b200.pipeline import PipelineConfig, run_frame
+
+    rig = S.ring_rig(8, (0, 0, 300), 6000, 5000, 640, 480, 700)
+    objs = [S.Ellipsoid(center=(x, y, 150.0), semi_axes=(60.0, 60.0, 150.0))
+            for x in np.linspace(-2600, 2600, 14) for y in np.linspace(-2600, 2600, 14)]
+    masks, _ = S.render_scene_device(rig, objs)
+    m_np = [m.cpu().numpy().astype(bool) for m in masks]
+    cfg = PipelineConfig(stage_lo=(-3000, -3000, 0), stage_hi=(3000, 3000, 600),
+                         coarse_spacing=50.0, fine_spacing=25.0, t_small=1)
+    bundle = run_frame(cfg, rig, {c.id: None for c in rig}, sils=masks)
+    ref = O.run_frame(list(rig), m_np, cfg.stage_lo, cfg.stage_hi, cfg.coarse_spacing,
+                      cfg.fine_spacing, cfg.min_views, cfg.t_small, cfg.t_large,
+                      cfg.roi_margin, cfg.t_v)
+    assert bundle.stats == ref["stats"]
+    assert bundle.stats["components"] > 128
+    mv, mt, _ = ref["merged"]
+    assert np.array_equal(bundle.merged_mesh.vertices, mv)
+    assert np.array_equal(bundle.merged_mesh.triangles, mt)
+    for c in rig:
+        assert np.array_equal(bundle.visibility[c.id], ref["visibility"][c.id]), c.id
+
+
+@pytest.mark.parametrize("lanes", [1, 3, 4])
+def test_run_sequence_lanes_keep_frame_order(gpu, lanes):
+    """run_sequence hands frames back in input order whatever the lane count
+    and equals run_frame frame by frame (7 distinct C1 frames, pageable and
+    pinned inputs mixed)."""
+    import torch
+
+    from paper_1903_11785_b200 import workloads
+    from paper_1903_11785_b200.pipeline import run_frame, run_sequence
+
+    wl = workloads.get("C1")
+    seq = [_inputs(wl, f) for f in range(7)]
+    frames = [f if i % 2 else {k: torch.from_numpy(v).pin_memory() for k, v in f.items()}
+              for i, (_, _, f) in enumerate(seq)]
+    sils = [m.cpu().pin_memory() if i % 3 else m_np for i, (m, m_np, _) in enumerate(seq)]
+    got = list(run_sequence(wl.cfg, wl.rig, frames, sils, wl.virtual, frame_id0=5, lanes=lanes))
+    assert [b.frame_id for b, _ in got] == list(range(5, 12))
+    for (bundle, img), (masks, _, fr) in zip(got, seq):
+        ref = run_frame(wl.cfg, wl.rig, fr, sils=masks)
+        assert bundle.stats == ref.stats
+        assert np.array_equal(bundle.merged_mesh.triangles, ref.merged_mesh.triangles)
+        assert np.array_equal(bundle.merged_mesh.vertices, ref.merged_mesh.vertices)
+        assert img is not None and img.color.shape == (480, 640, 3)
