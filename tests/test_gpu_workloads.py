@@ -171,3 +171,28 @@ def test_run_sequence_lanes_keep_frame_order(gpu, lanes):
         assert np.array_equal(bundle.merged_mesh.triangles, ref.merged_mesh.triangles)
         assert np.array_equal(bundle.merged_mesh.vertices, ref.merged_mesh.vertices)
         assert img is not None and img.color.shape == (480, 640, 3)
+
+
+def test_executor_more_than_4096_components_vs_oracle(gpu):
+    """Random-noise silhouettes: the coarse hull breaks into > 4096 components
+    (the executor's second component-table read), nearly all filtered."""
+    import torch
+
+    from paper_1903_11785_b200 import workloads
+    from paper_1903_11785_b200.pipeline import run_frame
+
+    wl = workloads.get("C1")
+    rng = np.random.default_rng(7)
+    m_np = [rng.random((c.image_height, c.image_width)) < 0.55 for c in wl.rig]
+    masks = torch.from_numpy(np.stack(m_np).astype(np.uint8)).cuda()
+    cfg = wl.cfg
+    bundle = run_frame(cfg, wl.rig, {c.id: None for c in wl.rig}, sils=masks)
+    ref = O.run_frame(list(wl.rig), m_np, cfg.stage_lo, cfg.stage_hi, cfg.coarse_spacing,
+                      cfg.fine_spacing, cfg.min_views, cfg.t_small, cfg.t_large, cfg.roi_margin,
+                      cfg.t_v)
+    assert bundle.stats == ref["stats"]
+    labels, comps = O.label(ref["coarse"][3], ref["coarse"][2])
+    assert len(comps) > 4096
+    mv, mt, _ = ref["merged"]
+    assert np.array_equal(bundle.merged_mesh.vertices, mv)
+    assert np.array_equal(bundle.merged_mesh.triangles, mt)
