@@ -119,11 +119,30 @@ __device__ __forceinline__ bool tri_depth(const TriSetup &s, int x, int y, doubl
   return d < INFINITY;  // only finite depths can beat the +inf background
 }
 
+// A pass-0 depth candidate kept for the id pass: plane index, triangle,
+// depth bits (the id pass then scans these instead of re-rasterising).
+struct Hit {
+  uint32_t idx, t;
+  unsigned long long bits;
+};
+
 __device__ __forceinline__ void pixel_update(int pass, double d, int64_t t,
-                                             unsigned long long *depth, unsigned *ids) {
+                                             unsigned long long *depth, unsigned *ids,
+                                             Hit *hits = nullptr,
+                                             unsigned long long *nhits = nullptr,
+                                             int64_t hit_cap = 0, int64_t idx = 0) {
   const unsigned long long bits = (unsigned long long)__double_as_longlong(d);
   if (pass == 0) {
     atomicMin(depth, bits);  // result unused -> RED.MIN (no round trip)
+    if (hits) {              // warp-aggregated append
+      const unsigned act = __activemask();
+      const int lane = threadIdx.x & 31, leader = __ffs(act) - 1;
+      unsigned long long base = 0;
+      if (lane == leader) base = atomicAdd(nhits, (unsigned long long)__popc(act));
+      base = __shfl_sync(act, base, leader);
+      const unsigned long long slot = base + __popc(act & ((1u << lane) - 1u));
+      if ((int64_t)slot < hit_cap) hits[slot] = Hit{(uint32_t)idx, (uint32_t)t, bits};
+    }
   } else if (bits == __ldcg(depth)) {
     atomicMin(ids, (unsigned)t);
   }
@@ -141,6 +160,9 @@ struct RasterArgs {
   int64_t *qcount;
   int64_t qcap;
   int pass;
+  Hit *hits;          // id pass by hit list (nullptr: re-rasterise)
+  unsigned long long *nhits;
+  int64_t hit_cap;
 };
 
 // Triangle setup as kept in shared memory for the warp's pixel sweep.
@@ -228,6 +250,7 @@ __device__ __forceinline__ void smem_to_setup(const TriSmem &m, TriSetup &s) {
 // uneven bounding boxes and culled triangles do not leave lanes idle.
 __global__ void __launch_bounds__(kRasterThreads, 8)
     raster_small_kernel(const __grid_constant__ RasterCams C, RasterArgs A) {
+  if (A.pass == 1 && A.hits && (int64_t)__ldcg(A.nhits) <= A.hit_cap) return;  // list did it
   __shared__ TriSmem sm[kRasterThreads];
   const int lane = threadIdx.x & 31;
   TriSmem *wsm = sm + (threadIdx.x & ~31);
@@ -309,7 +332,8 @@ __global__ void __launch_bounds__(kRasterThreads, 8)
           unsigned long long *dp = (unsigned long long *)(A.depth + C.depth_off[m.cam]);
           unsigned *ip = (unsigned *)(A.ids ? A.ids + C.depth_off[m.cam] : nullptr);
           const int64_t pxl = (int64_t)y * W + x;
-          pixel_update(A.pass, d, m.t, dp + pxl, ip ? ip + pxl : nullptr);
+          pixel_update(A.pass, d, m.t, dp + pxl, ip ? ip + pxl : nullptr, A.hits, A.nhits,
+                       A.hit_cap, C.depth_off[m.cam] + pxl);
         }
       }
     }
@@ -319,6 +343,7 @@ __global__ void __launch_bounds__(kRasterThreads, 8)
 
 __global__ void __launch_bounds__(kBigThreads)
     raster_big_kernel(const __grid_constant__ RasterCams C, RasterArgs A) {
+  if (A.pass == 1 && A.hits && (int64_t)__ldcg(A.nhits) <= A.hit_cap) return;  // list did it
   const int64_t nt = device_count(A.nt_dev, A.nt);
   int64_t nq = __ldcg(A.qcount);
   if (nq > A.qcap) nq = A.qcap;
@@ -338,7 +363,8 @@ __global__ void __launch_bounds__(kBigThreads)
       double d;
       if (!tri_depth(s, x, y, d)) continue;
       const int64_t p = (int64_t)y * width + x;
-      pixel_update(A.pass, d, t, dp + p, ip ? ip + p : nullptr);
+      pixel_update(A.pass, d, t, dp + p, ip ? ip + p : nullptr, A.hits, A.nhits, A.hit_cap,
+                   C.depth_off[c] + p);
     }
   }
 }
@@ -376,6 +402,19 @@ __global__ void raster_prep_kernel(const __grid_constant__ RasterCams C,
     double u, v, z;
     project_exact(C.cams[c], V[3 * i], V[3 * i + 1], V[3 * i + 2], false, gemv, u, v, z);
     proj[w] = make_double4(u, v, z, 0.0);
+  }
+}
+
+// The id pass from the hit list: the first (lowest) triangle id among the
+// candidates that reached the final depth (visibility.py:84-91, strict <).
+__global__ void raster_hits_kernel(RasterArgs A) {
+  const int64_t n = (int64_t)__ldcg(A.nhits);
+  if (n > A.hit_cap) return;  // overflowed: the pass-1 raster kernels run instead
+  const unsigned long long *depth = (const unsigned long long *)A.depth;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const Hit h = A.hits[i];
+    if (h.bits == __ldcg(depth + h.idx)) atomicMin((unsigned *)A.ids + h.idx, h.t);
   }
 }
 
@@ -618,9 +657,18 @@ static size_t raster_proj_offset(int64_t num_triangles, int ncam) {
   return (256 + 8 * (size_t)raster_queue_cap(num_triangles, ncam) + 255) & ~(size_t)255;
 }
 
+static int64_t raster_hit_cap(int64_t num_triangles, int ncam) {
+  int64_t cap = 4 * num_triangles * (int64_t)ncam;
+  if (cap > (4ll << 20)) cap = 4ll << 20;
+  return cap > 0 ? cap : 1;
+}
+
+// [counters][big queue][projected vertices][hit list]
 size_t fvv_raster_workspace_bytes(int64_t num_vertices, int64_t num_triangles, int ncam) {
   return raster_proj_offset(num_triangles, ncam) +
-         sizeof(double4) * (size_t)(num_vertices > 0 ? num_vertices : 1) * (size_t)ncam;
+         ((sizeof(double4) * (size_t)(num_vertices > 0 ? num_vertices : 1) * (size_t)ncam + 255) &
+          ~(size_t)255) +
+         sizeof(Hit) * (size_t)raster_hit_cap(num_triangles, ncam);
 }
 
 int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int64_t nv,
@@ -669,7 +717,14 @@ int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int
   A.qcap = raster_queue_cap(nt, ncam);
   double4 *proj = (double4 *)((char *)ws_dev + raster_proj_offset(nt, ncam));
   A.P = proj;
-  cudaMemsetAsync(A.qcount, 0, 8, st);
+  A.nhits = (unsigned long long *)((char *)ws_dev + 8);
+  // the id pass scans the depth pass's candidates when plane indices fit 32 bits
+  const bool use_hits = tri_id_dev && total_px < (1ll << 32);
+  A.hits = use_hits ? (Hit *)((char *)proj + ((sizeof(double4) * (size_t)(nv > 0 ? nv : 1) *
+                                                   (size_t)ncam + 255) & ~(size_t)255))
+                    : nullptr;
+  A.hit_cap = raster_hit_cap(nt, ncam);
+  cudaMemsetAsync(A.qcount, 0, 16, st);  // big-queue and hit counters
   {
     int64_t blocks = (nv * ncam + 255) / 256;
     if (blocks > kRasterGrid) blocks = kRasterGrid;
@@ -688,6 +743,11 @@ int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int
   }
   for (int pass = 0; pass < (tri_id_dev ? 2 : 1); ++pass) {
     A.pass = pass;
+    if (pass == 1 && use_hits) {
+      raster_hits_kernel<<<148 * 8, 256, 0, st>>>(A);
+      note_launches(1);
+    }
+    // (pass 1 with a complete hit list: both kernels return at once)
     raster_small_kernel<<<148 * 64, kRasterThreads, 0, st>>>(C, A);  // measured best of 16..128
     raster_big_kernel<<<148 * 4, kBigThreads, 0, st>>>(C, A);
     note_launches(2);
