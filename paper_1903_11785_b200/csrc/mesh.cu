@@ -532,31 +532,45 @@ struct TriScan {
   }
 };
 
-// ---- B4: per-grid slot bases (one thread; <= 128 grids) --------------------
+// ---- B4: per-grid slot bases (one warp, a lane per grid) ---------------------
 __global__ void mesh_slot_bases_kernel(const __grid_constant__ MeshGrids G, MeshBufs B,
                                        const Slot5 *total) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (blockIdx.x != 0) return;
+  const int lane = threadIdx.x & 31;
   const int64_t S = B.totals[1];
-  int64_t tbase = 0;
-  for (int g = 0; g < G.ngrid; ++g) {
-    int64_t *inf = B.info + 8 * g;
-    const int64_t s0 = inf[kInfoSbase], s1 = s0 + inf[kInfoS];
-    int64_t p0[5], p1[5];
-    for (int t = 0; t < 5; ++t) {
-      p0[t] = s0 < S ? B.cprefix[5 * s0 + t] : total->v[t];
-      p1[t] = s1 < S ? B.cprefix[5 * s1 + t] : total->v[t];
+  int64_t carry = 0;  // triangles of the grids before this chunk of 32
+  for (int g0 = 0; g0 < G.ngrid; g0 += 32) {
+    const int g = g0 + lane;
+    int64_t p0[5], p1[5], cnt = 0;
+    if (g < G.ngrid) {
+      const int64_t *inf = B.info + 8 * g;
+      const int64_t s0 = inf[kInfoSbase], s1 = s0 + inf[kInfoS];
+      for (int t = 0; t < 5; ++t) {
+        p0[t] = s0 < S ? B.cprefix[5 * s0 + t] : total->v[t];
+        p1[t] = s1 < S ? B.cprefix[5 * s1 + t] : total->v[t];
+        cnt += p1[t] - p0[t];
+      }
     }
-    inf[kInfoTbase] = tbase;
-    int64_t run = tbase;
-    for (int t = 0; t < 5; ++t) {
-      // slot_base[g][t] = first triangle index of slot t minus the prefix at the grid start
-      B.slot_base[5 * g + t] = run - p0[t];
-      run += p1[t] - p0[t];
+    int64_t incl = cnt;  // inclusive scan of the grids' triangle counts
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
     }
-    inf[kInfoT] = run - tbase;
-    tbase = run;
+    const int64_t tbase = carry + incl - cnt;
+    if (g < G.ngrid) {
+      int64_t *inf = B.info + 8 * g;
+      inf[kInfoTbase] = tbase;
+      int64_t run = tbase;
+      for (int t = 0; t < 5; ++t) {
+        // slot_base[g][t] = first triangle index of slot t minus the prefix at the grid start
+        B.slot_base[5 * g + t] = run - p0[t];
+        run += p1[t] - p0[t];
+      }
+      inf[kInfoT] = run - tbase;
+    }
+    carry += __shfl_sync(0xffffffffu, incl, 31);
   }
-  B.totals[2] = tbase;
+  if (lane == 0) B.totals[2] = carry;
 }
 
 // ---- B5: triangle emission ----------------------------------------------------
