@@ -630,7 +630,7 @@ static PrepLayout prep_layout(int64_t tw_total, int ngrid) {
   L.vprefix = take(12 * (size_t)tw_total);
   L.sflags = take(4 * (size_t)tw_total);
   L.sprefix = take(4 * (size_t)tw_total);
-  L.sums = take(8 * (size_t)scan_chunks(3 * tw_total + 1));
+  L.sums = take(onepass_bytes<int64_t>(3 * tw_total + 1));  // scan status words
   L.totals = take(8 * 4);
   L.info = take(8 * 8 * (size_t)(ngrid > 0 ? ngrid : 1));
   L.slot5 = take(sizeof(int64_t) * 5 * (size_t)(ngrid > 0 ? ngrid : 1) + sizeof(Slot5));
@@ -731,9 +731,11 @@ int fvv_mesh_prepare(const fvv_grid *grids, int ngrid, const uint32_t *occ_dev,
     mesh_transpose_kernel<<<kMeshGrid, 256, 0, st>>>(h_grids, B);
     note_launches(1);
     EdgeFlags ef{h_grids, B.tw, B.eflags, B.vprefix};
-    ordered_scan(ef, nullptr, 3 * h_grids.tw_total, B.sums, B.totals + 0, st);
+    onepass_scan(ef, nullptr, 3 * h_grids.tw_total, 3 * h_grids.tw_total, (void *)B.sums,
+                 B.totals + 0, st);
     CellFlags cf{h_grids, B.tw, B.sflags, B.sprefix};
-    ordered_scan(cf, nullptr, h_grids.tw_total, B.sums, B.totals + 1, st);
+    onepass_scan(cf, nullptr, h_grids.tw_total, h_grids.tw_total, (void *)B.sums, B.totals + 1,
+                 st);
   }
   mesh_grid_counts_kernel<<<1, 128, 0, st>>>(h_grids, B);
   note_launches(1);
@@ -763,7 +765,7 @@ int fvv_mesh_counts(const fvv_grid *grids, int ngrid, const void *ws_dev, int64_
 size_t fvv_mesh_emit_scratch_bytes(int64_t num_vertices, int64_t num_cells) {
   return al256(8 * (size_t)num_vertices) + al256(8 * (size_t)num_cells) +
          al256(4 * (size_t)num_cells) + al256(20 * (size_t)num_cells) +
-         al256(sizeof(Slot5) * (size_t)scan_chunks(num_cells + 1));
+         al256(onepass_bytes<Slot5>(num_cells + 1));
 }
 
 int fvv_mesh_emit(const fvv_camera *cams_by_id, int ncam, const uint32_t *sil_dev,
@@ -822,7 +824,7 @@ int fvv_mesh_emit(const fvv_camera *cams_by_id, int ncam, const uint32_t *sil_de
                                                                                           B);
     note_launches(1);
     TriScan ts{B.cell_mask, B.cprefix};
-    ordered_scan(ts, B.totals + 1, 0, cell_sums, d_total, st);
+    onepass_scan(ts, B.totals + 1, 0, num_cells, (void *)cell_sums, d_total, st);
   } else {
     cudaMemsetAsync(d_total, 0, sizeof(Slot5), st);
   }
