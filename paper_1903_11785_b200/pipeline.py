@@ -585,9 +585,11 @@ def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
     host->device on a copy stream one frame ahead (pinned colour frames are
     sampled in place by the colour pass), and turns finished frames, streamed
     back on a readback stream, into SceneBundles. Inputs should be pinned
-    host tensors for the copies to be asynchronous. Yields (SceneBundle,
-    RenderedImage or None) per frame, in input order, with the mesh,
-    visibility flags and rendered image on the host."""
+    host tensors for the copies to be asynchronous; pinned colour frames are
+    read in place by the GPU, so a frame's inputs must stay unmodified until
+    that frame has been yielded (up to 2 x lanes frames are in flight).
+    Yields (SceneBundle, RenderedImage or None) per frame, in input order,
+    with the mesh, visibility flags and rendered image on the host."""
     import queue
     import threading
 
@@ -611,6 +613,7 @@ def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
     in_qs = [queue.Queue(maxsize=1) for _ in range(lanes)]
     out_qs = [queue.Queue() for _ in range(lanes)]
     stop = threading.Event()
+    counter_lock = threading.Lock()
     _END = object()
 
     def worker(lane):
@@ -630,7 +633,8 @@ def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
                     if virtual is not None:
                         out = ex.run(d_masks, virtual, fbuf, foff, fallback_color)
                         if isinstance(fbuf, int):  # zero-copy: the bilinear taps crossed PCIe
-                            H2D_BYTES["frames"] += 12 * int(out.stats_raw["sourced_px"])
+                            with counter_lock:
+                                H2D_BYTES["frames"] += 12 * int(out.stats_raw["sourced_px"])
                     else:
                         out = ex.run(d_masks)
                     pinned, slot_free = out.to_host_async(cams, stream=readback)
