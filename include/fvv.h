@@ -108,6 +108,14 @@ int fvv_carve(const fvv_camera *cams, int ncam, const uint32_t *sil_dev,
  * queue of voxels its certified FP32 pass leaves to the float64 chain. */
 size_t fvv_carve_workspace_bytes(const fvv_camera *cams, int ncam);
 
+/* voxels.py:100-162 save_grid: the bit transitions of an occupancy field
+ * (bit l != bit l-1, bit -1 OFF), in ascending order, into pos_dev (capacity
+ * nvox) and their number into *count_dev; run lengths are the differences of
+ * [0, pos..., nvox]. */
+size_t fvv_rle_workspace_bytes(int64_t nvox);
+int fvv_rle_transitions(const uint32_t *occ_dev, int64_t nvox, int64_t *pos_dev,
+                        int64_t *count_dev, void *ws_dev, size_t ws_bytes, void *stream);
+
 /* ---- B-2: hull.py:122-269 ------------------------------------------------ */
 
 /* Device workspace fvv_ccl26 needs for `grid` (compacted ON-voxel ranks,

@@ -442,3 +442,18 @@ def extract_silhouette(frame, mean, std, dm, theta_near=3.0, theta_far=8.0, d_ma
                      ctypes.c_int64(c), ctypes.c_double(theta_near), ctypes.c_double(theta_far),
                      ctypes.c_double(d_max), _p(out))
     return out.astype(bool)
+
+
+def rle_runs(occ):
+    """voxels.py:100-112 _rle_encode: run lengths of a flat bool array, the
+    first run counted as OFF (a leading ON run is preceded by a 0 run)."""
+    bits = np.asarray(occ, dtype=bool).reshape(-1)
+    n = len(bits)
+    if n == 0:
+        return np.zeros(0, dtype=np.uint64)
+    edges = np.flatnonzero(np.diff(bits.view(np.uint8))) + 1
+    bounds = np.concatenate(([0], edges, [n]))
+    runs = np.diff(bounds).astype(np.uint64)
+    if bits[0]:
+        runs = np.concatenate(([np.uint64(0)], runs))
+    return runs

@@ -38,7 +38,8 @@ assert CAM_DTYPE.itemsize == 192 and GRID_DTYPE.itemsize == 56 and COMP_DTYPE.it
 # exported symbols; tests check the .so exports every one of them
 SYMBOLS = (
     "fvv_last_error", "fvv_version", "fvv_launch_count", "fvv_copy_gather", "fvv_host_mapped", "fvv_project",
-    "fvv_pack_silhouettes", "fvv_carve", "fvv_carve_workspace_bytes", "fvv_ccl_workspace_bytes", "fvv_ccl26",
+    "fvv_pack_silhouettes", "fvv_carve", "fvv_carve_workspace_bytes",
+    "fvv_rle_workspace_bytes", "fvv_rle_transitions", "fvv_ccl_workspace_bytes", "fvv_ccl26",
     "fvv_ccl_components", "fvv_ccl_labels", "fvv_filter_labels", "fvv_filter_dense",
     "fvv_mesh_workspace_bytes", "fvv_mesh_prepare", "fvv_mesh_counts",
     "fvv_mesh_emit_scratch_bytes", "fvv_mesh_emit", "fvv_edge_isovalues",
@@ -91,6 +92,8 @@ def load():
         lib.fvv_frame_destroy.argtypes = [ctypes.c_void_p]
         lib.fvv_ccl_workspace_bytes.restype = ctypes.c_size_t
         lib.fvv_carve_workspace_bytes.restype = ctypes.c_size_t
+        lib.fvv_rle_workspace_bytes.restype = ctypes.c_size_t
+        lib.fvv_rle_workspace_bytes.argtypes = [ctypes.c_int64]
         lib.fvv_mesh_workspace_bytes.restype = ctypes.c_size_t
         lib.fvv_mesh_emit_scratch_bytes.restype = ctypes.c_size_t
         lib.fvv_mesh_emit_scratch_bytes.argtypes = [ctypes.c_int64, ctypes.c_int64]

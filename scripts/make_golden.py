@@ -395,8 +395,37 @@ def fixture_silhouette():
     save("silhouette", **arrays)
 
 
+def fixture_grid_dump():
+    """voxels.save_grid files written by the reference: random, all-on,
+    all-off, a 64^3 solid, ragged word tails, and a carved grid."""
+    from freeview.voxels import save_grid
+
+    rng = np.random.default_rng(11)
+    cases = [((4, 5, 6), rng.random(120) < 0.3), ((3, 3, 3), np.ones(27, dtype=bool)),
+             ((3, 3, 3), np.zeros(27, dtype=bool)), ((64, 64, 64), np.ones(64 ** 3, dtype=bool)),
+             ((33, 1, 1), rng.random(33) < 0.5), ((31, 2, 3), rng.random(186) < 0.7),
+             ((1, 1, 1), np.ones(1, dtype=bool))]
+    z = np.load(os.path.join(OUT, "spheres.npz"))
+    sp = z["carve3_spec"]
+    dims = tuple(int(d) for d in sp[4:7])
+    cases.append((dims, np.unpackbits(z["carve3_occ"], bitorder="little")[:int(np.prod(dims))]
+                  .astype(bool)))
+    arrays = {}
+    with tempfile.TemporaryDirectory() as tmp:
+        for i, (dims, occ) in enumerate(cases):
+            spec = GridSpec(origin=(-10.0 + i, 5.0, 0.25 * i), spacing=25.0 + i, dims=dims)
+            path = os.path.join(tmp, f"g{i}.bin")
+            save_grid(VoxelGrid(spec=spec, occ=occ), path)
+            arrays[f"g{i}_dims"] = np.array(dims, dtype=np.int64)
+            arrays[f"g{i}_origin"] = spec.origin
+            arrays[f"g{i}_spacing"] = np.float64(spec.spacing)
+            arrays[f"g{i}_occ"] = pack(occ)
+            arrays[f"g{i}_file"] = np.frombuffer(open(path, "rb").read(), dtype=np.uint8)
+    save("grid_dump", **arrays)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["tiny_cli", "spheres", "distorted", "ccl", "raster", "figures",
-                             "silhouette", "bundle"]
+                             "silhouette", "bundle", "grid_dump"]
     for w in which:
         globals()[f"fixture_{w}"]()
