@@ -76,6 +76,15 @@ def test_c3_volleyball_frame_matches_oracle(gpu, frame):
         assert (counts == 2).mean() > 0.99
 
 
+def test_c2_judo_full_frame_matches_oracle(gpu):
+    """C2 (16 x 1080p, 5 mm ROIs, ~486k triangles): every stage and the
+    virtual view bit for bit."""
+    from paper_1903_11785_b200 import workloads
+
+    b = _check_frame(workloads.get("C2"), 0)
+    assert b.stats["dense_tests"] > 10_000_000
+
+
 def test_c2_judo_coarse_and_rois_match_oracle(gpu):
     """C2 at full size for B-1/B-2 (5 mm ROI meshes are checked via C3's
     machinery; the 5 mm oracle carve alone takes minutes on the host)."""
