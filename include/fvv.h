@@ -346,6 +346,22 @@ int fvv_frame_get_rois(const fvv_frame *frame, int64_t *component_ids, double *b
 
 /* ---- harness (not hot path): synthetic scene inputs ------------------------- */
 
+/* synthetic.py:165-218 for the reference's Sphere/Box scenes: per pixel of
+ * `cam` (zero distortion) the centre ray (camera.py:223-235), the nearest hit
+ * over objs_dev (nobj records of 10 doubles: sphere {0, centre[3], r^2,
+ * colour[3], 0, 0}, box {1, lo[3], hi[3], colour[3]}), the analytic
+ * silhouette (uint8 (H,W), optional) and the Lambertian frame (uint8
+ * (H,W,3), optional; shading = {ambient, 1 - ambient, background rgb},
+ * light = unit light direction, noise_dev = optional (H,W,3) float64 added
+ * before rounding). */
+int fvv_synth_render(const fvv_camera *cam, const double *light, const double *shading,
+                     const double *objs_dev, int nobj, const double *noise_dev,
+                     uint8_t *sil_dev, uint8_t *rgb_dev, void *stream);
+/* synthetic.py:221-226: binary erosion with the 3x3 cross, `iterations`
+ * times, outside pixels 0 (scipy.ndimage.binary_erosion defaults). */
+int fvv_erode_cross(const uint8_t *in_dev, uint8_t *tmp_dev, uint8_t *out_dev, int width,
+                    int height, int iterations, void *stream);
+
 /* Ray-cast nparts ellipsoids (float64 records: centre[3], orientation[9]
  * row-major (columns = ellipsoid axes), semi-axes[3], rgb[3]) into camera
  * `cam`: silhouette uint8 (H,W) and Lambertian frame uint8 (H,W,3); either

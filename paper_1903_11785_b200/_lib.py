@@ -37,8 +37,8 @@ assert CAM_DTYPE.itemsize == 192 and GRID_DTYPE.itemsize == 56 and COMP_DTYPE.it
 
 # exported symbols; tests check the .so exports every one of them
 SYMBOLS = (
-    "fvv_last_error", "fvv_version", "fvv_launch_count", "fvv_copy_gather", "fvv_host_mapped", "fvv_project",
-    "fvv_pack_silhouettes", "fvv_carve", "fvv_carve_workspace_bytes",
+    "fvv_last_error", "fvv_version", "fvv_launch_count", "fvv_copy_gather", "fvv_host_mapped",
+    "fvv_project", "fvv_pack_silhouettes", "fvv_carve", "fvv_carve_workspace_bytes",
     "fvv_rle_workspace_bytes", "fvv_rle_transitions", "fvv_ccl_workspace_bytes", "fvv_ccl26",
     "fvv_ccl_components", "fvv_ccl_labels", "fvv_filter_labels", "fvv_filter_dense",
     "fvv_mesh_workspace_bytes", "fvv_mesh_prepare", "fvv_mesh_counts",
@@ -46,7 +46,9 @@ SYMBOLS = (
     "fvv_raster_workspace_bytes", "fvv_rasterize", "fvv_classify", "fvv_triangle_sources",
     "fvv_render_count", "fvv_render_view", "fvv_back_project", "fvv_render_ellipsoids",
     "fvv_frame_create", "fvv_frame_destroy", "fvv_frame_run", "fvv_frame_get_outputs",
-    "fvv_frame_get_rois", "fvv_frame_readback_layout", "fvv_frame_readback", "fvv_distance_map", "fvv_background", "fvv_extract_silhouette",
+    "fvv_frame_get_rois", "fvv_frame_readback_layout", "fvv_frame_readback",
+    "fvv_synth_render", "fvv_erode_cross", "fvv_distance_map", "fvv_background",
+    "fvv_extract_silhouette",
 )
 
 FRAME_CONFIG_DTYPE = np.dtype([("stage_lo", "<f8", (3,)), ("stage_hi", "<f8", (3,)),

@@ -325,3 +325,229 @@ def render_scene_device(rig, objects, shade=True):
                   _lib.dev_ptr(frames[i]) if shade else ctypes.c_void_p(0),
                   _lib.host_ptr(shading), stream_handle())
     return masks, frames
+
+
+# ---- the reference's Sphere / Box scenes on the GPU (synthetic.py:21-243) ----
+# SURVEY.md 8f4. analytic_silhouette, shade_frame and proposal_from_silhouette
+# run as sm_100a kernels (csrc/synth.cu: fvv_synth_render, fvv_erode_cross)
+# and equal the reference's numpy/scipy outputs bit for bit
+# (tests/test_gpu_synth.py against tests/golden/synth.npz). cast_rays stays a
+# host helper over caller-given rays (not on any hot path).
+
+@dataclass
+class Sphere:
+    """synthetic.py:21-55."""
+
+    center: np.ndarray
+    radius: float
+    color: np.ndarray = field(default_factory=lambda: np.array([200.0, 80.0, 60.0]))
+
+    def __post_init__(self) -> None:
+        self.center = np.asarray(self.center, dtype=np.float64).reshape(3)
+        self.color = np.asarray(self.color, dtype=np.float64).reshape(3)
+        if self.radius <= 0:
+            raise ValueError("sphere radius must be positive")
+
+    def ray_hits(self, origin, dirs):
+        """Smallest positive ray parameter per ray, +inf on miss (host)."""
+        oc = origin - self.center
+        b = dirs @ oc
+        c = oc @ oc - self.radius ** 2
+        disc = b * b - c
+        hit = disc >= 0
+        sq = np.sqrt(np.where(hit, disc, 0.0))
+        t0 = -b - sq
+        t1 = -b + sq
+        t = np.where(t0 > 1e-9, t0, t1)
+        return np.where(hit & (t > 1e-9), t, np.inf)
+
+    def normal_at(self, p):
+        n = p - self.center
+        return n / np.linalg.norm(n, axis=-1, keepdims=True)
+
+    def contains(self, pts):
+        return np.linalg.norm(pts - self.center, axis=-1) <= self.radius
+
+    def aabb(self):
+        return self.center - self.radius, self.center + self.radius
+
+    def _record(self):
+        return [0.0, *self.center, float(self.radius) ** 2, *self.color, 0.0, 0.0]
+
+
+@dataclass
+class Box:
+    """synthetic.py:58-98."""
+
+    lo: np.ndarray
+    hi: np.ndarray
+    color: np.ndarray = field(default_factory=lambda: np.array([70.0, 110.0, 200.0]))
+
+    def __post_init__(self) -> None:
+        self.lo = np.asarray(self.lo, dtype=np.float64).reshape(3)
+        self.hi = np.asarray(self.hi, dtype=np.float64).reshape(3)
+        self.color = np.asarray(self.color, dtype=np.float64).reshape(3)
+        if np.any(self.hi <= self.lo):
+            raise ValueError("box must have positive extent")
+
+    def ray_hits(self, origin, dirs):
+        with np.errstate(divide="ignore", invalid="ignore"):
+            inv = 1.0 / dirs
+            t_lo = (self.lo - origin) * inv
+            t_hi = (self.hi - origin) * inv
+        tmin = np.nanmax(np.minimum(t_lo, t_hi), axis=-1)
+        tmax = np.nanmin(np.maximum(t_lo, t_hi), axis=-1)
+        hit = (tmax >= np.maximum(tmin, 1e-9)) & (tmax > 1e-9)
+        t = np.where(tmin > 1e-9, tmin, tmax)
+        return np.where(hit, t, np.inf)
+
+    def normal_at(self, p):
+        mid = 0.5 * (self.lo + self.hi)
+        half = 0.5 * (self.hi - self.lo)
+        rel = np.atleast_2d((p - mid) / half)
+        n = np.zeros_like(rel)
+        ax = np.argmax(np.abs(rel), axis=-1)
+        rows = np.arange(len(rel))
+        n[rows, ax] = np.sign(rel[rows, ax])
+        return n.reshape(np.shape(p))
+
+    def contains(self, pts):
+        return np.all((pts >= self.lo) & (pts <= self.hi), axis=-1)
+
+    def aabb(self):
+        return self.lo.copy(), self.hi.copy()
+
+    def _record(self):
+        return [1.0, *self.lo, *self.hi, *self.color]
+
+
+def _unit(v):
+    """v / |v| with |v| summed in a fixed order (OpenBLAS's ddot order on the
+    reference host, independent of this host's CPU)."""
+    v = [float(x) for x in np.asarray(v, dtype=np.float64).reshape(3)]
+    import math
+
+    n = math.sqrt((v[0] * v[0] + v[1] * v[1]) + v[2] * v[2])
+    return np.array([v[0] / n, v[1] / n, v[2] / n])
+
+
+@dataclass
+class SyntheticScene:
+    """synthetic.py:101-108."""
+
+    rig: CameraRig
+    objects: list
+    light_dir: np.ndarray = field(default_factory=lambda: np.array([0.3, 0.5, -0.8]))
+
+    def __post_init__(self) -> None:
+        self.light_dir = _unit(self.light_dir)
+
+
+def cast_rays(objects, origin, dirs):
+    """synthetic.py:165-176 (host helper over caller-given rays)."""
+    flat = np.asarray(dirs).reshape(-1, 3)
+    best_t = np.full(len(flat), np.inf)
+    best_o = np.full(len(flat), -1, dtype=np.int32)
+    for oi, obj in enumerate(objects):
+        t = obj.ray_hits(origin, flat)
+        closer = t < best_t
+        best_t[closer] = t[closer]
+        best_o[closer] = oi
+    shape = np.shape(dirs)[:-1]
+    return best_t.reshape(shape), best_o.reshape(shape)
+
+
+def _synth_device(cam, objects, light, want_sil, want_rgb, noise=None):
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    from ._device import cam_table, require_cuda, stream_handle
+
+    dev = require_cuda()
+    for o in objects:
+        if not hasattr(o, "_record"):
+            raise TypeError(f"unsupported object {type(o).__name__} (Sphere or Box)")
+    recs = np.array([o._record() for o in objects], dtype=np.float64).reshape(-1, 10)
+    d_objs = torch.from_numpy(recs).to(dev) if len(objects) else None
+    h, w = cam.image_height, cam.image_width
+    sil = torch.empty((h, w), dtype=torch.uint8, device=dev) if want_sil else None
+    rgb = torch.empty((h, w, 3), dtype=torch.uint8, device=dev) if want_rgb else None
+    d_noise = None
+    if noise is not None:
+        d_noise = torch.from_numpy(np.ascontiguousarray(noise, dtype=np.float64)).to(dev)
+    shading = np.array([AMBIENT, 1.0 - AMBIENT, *BG_COLOR], dtype=np.float64)
+    light = np.ascontiguousarray(light, dtype=np.float64)
+    null = ctypes.c_void_p(0)
+    _lib.call("fvv_synth_render", _lib.host_ptr(cam_table([cam])), _lib.host_ptr(light),
+              _lib.host_ptr(shading), _lib.dev_ptr(d_objs) if d_objs is not None else null,
+              ctypes.c_int(len(objects)), _lib.dev_ptr(d_noise) if d_noise is not None else null,
+              _lib.dev_ptr(sil) if sil is not None else null,
+              _lib.dev_ptr(rgb) if rgb is not None else null, stream_handle())
+    return sil, rgb
+
+
+def analytic_silhouette(cam, objects) -> np.ndarray:
+    """Exact binary silhouette: a pixel is foreground iff its centre ray hits
+    any object in front of the camera (synthetic.py:187-192), on the GPU."""
+    if cam.has_distortion:
+        raise ValueError("pixel_rays supports zero-distortion cameras only")
+    sil, _ = _synth_device(cam, list(objects), np.array([0.0, 0.0, 1.0]), True, False)
+    return sil.cpu().numpy().astype(bool)
+
+
+def shade_frame(scene: SyntheticScene, cam, noise_sigma: float = 0.0, seed: int = 0):
+    """Lambertian-shaded uint8 RGB frame, flat background, optional seeded
+    Gaussian noise (synthetic.py:195-218). The noise is numpy's
+    default_rng(seed + cam.id) stream, drawn on the host; the shading runs on
+    the GPU."""
+    if cam.has_distortion:
+        raise ValueError("pixel_rays supports zero-distortion cameras only")
+    noise = None
+    if noise_sigma > 0:
+        rng = np.random.default_rng(seed + cam.id)
+        noise = rng.normal(0.0, noise_sigma, (cam.image_height, cam.image_width, 3))
+    _, rgb = _synth_device(cam, list(scene.objects), scene.light_dir, False, True, noise)
+    return rgb.cpu().numpy()
+
+
+def proposal_from_silhouette(sil, erode_px: int = 3) -> np.ndarray:
+    """The silhouette eroded erode_px times with the 3x3 cross, outside = 0
+    (synthetic.py:221-226, scipy binary_erosion), on the GPU."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    from ._device import require_cuda, stream_handle
+
+    sil = np.asarray(sil, dtype=bool)
+    if erode_px <= 0:
+        return sil.copy()
+    dev = require_cuda()
+    h, w = sil.shape
+    d_in = torch.from_numpy(np.ascontiguousarray(sil).view(np.uint8)).to(dev)
+    tmp = torch.empty_like(d_in)
+    out = torch.empty_like(d_in)
+    _lib.call("fvv_erode_cross", _lib.dev_ptr(d_in), _lib.dev_ptr(tmp), _lib.dev_ptr(out),
+              ctypes.c_int(w), ctypes.c_int(h), ctypes.c_int(int(erode_px)), stream_handle())
+    return out.cpu().numpy().astype(bool)
+
+
+def scene_silhouettes(scene: SyntheticScene) -> list:
+    return [analytic_silhouette(cam, scene.objects) for cam in scene.rig]
+
+
+def scene_frames(scene: SyntheticScene, noise_sigma: float = 0.0, seed: int = 0) -> list:
+    return [shade_frame(scene, cam, noise_sigma, seed) for cam in scene.rig]
+
+
+def validate_in_stage(objects, stage_lo, stage_hi) -> None:
+    """synthetic.py:237-243."""
+    stage_lo = np.asarray(stage_lo, dtype=np.float64)
+    stage_hi = np.asarray(stage_hi, dtype=np.float64)
+    for i, obj in enumerate(objects):
+        lo, hi = obj.aabb()
+        if np.any(lo < stage_lo) or np.any(hi > stage_hi):
+            raise ValueError(f"object {i} extends outside the stage volume")

@@ -424,8 +424,36 @@ def fixture_grid_dump():
     save("grid_dump", **arrays)
 
 
+def fixture_synth():
+    """The reference's Sphere/Box scene generator (synthetic.py:165-243):
+    silhouettes, noiseless and noisy frames, eroded proposals, on the
+    TINY_SPEC objects seen by a small ring plus a skewed camera and a camera
+    looking straight down a box face."""
+    objs = [fsyn.Sphere(center=[-350, 0, 450], radius=250),
+            fsyn.Box(lo=[300, -200, 200], hi=[700, 200, 700], color=[70, 110, 200]),
+            fsyn.Sphere(center=[0, 400, 300], radius=120, color=[90, 200, 120])]
+    rig = fsyn.ring_rig(4, [0, 0, 450], 3500, 1400, width=160, image_height=120, focal=140)
+    cams = list(rig)
+    skew = fcam.CameraModel(id=7, image_width=150, image_height=110, fx=150.0, fy=140.0,
+                            cx=70.3, cy=52.1, skew=0.35, rotation=cams[1].rotation,
+                            translation=cams[1].translation)
+    down = fsyn.look_at_camera(9, [500.0, 0.0, 3000.0], [500.0, 0.0, 700.0], 128, 96, 300.0)
+    cams += [skew, down]
+    rig = fcam.CameraRig(cams)
+    scene = fsyn.SyntheticScene(rig=rig, objects=objs)
+    arrays = {"rig": np.array(rig_json(rig))}
+    for i, cam in enumerate(cams):
+        sil = fsyn.analytic_silhouette(cam, objs)
+        arrays[f"sil{i}"] = pack(sil)
+        arrays[f"frame{i}"] = fsyn.shade_frame(scene, cam, 0.0, 0)
+        arrays[f"noisy{i}"] = fsyn.shade_frame(scene, cam, 1.5, 3)
+        arrays[f"prop{i}"] = pack(fsyn.proposal_from_silhouette(sil, 3))
+        arrays[f"prop1_{i}"] = pack(fsyn.proposal_from_silhouette(sil, 1))
+    save("synth", **arrays)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["tiny_cli", "spheres", "distorted", "ccl", "raster", "figures",
-                             "silhouette", "bundle", "grid_dump"]
+                             "silhouette", "bundle", "grid_dump", "synth"]
     for w in which:
         globals()[f"fixture_{w}"]()
