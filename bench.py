@@ -26,6 +26,7 @@ weak scaling). Rank 0 prints one JSON line.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -269,10 +270,14 @@ def run_b200(args):
     torch.cuda.synchronize()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
+    gc.collect()
+    gc.freeze()  # setup objects out of the collector's way
+    gc.disable()  # as timeit: no collector pauses inside timed regions
     t_start.record()
     run_lanes(args.steps)
     t_end.record()
     torch.cuda.synchronize()
+    gc.enable()
     launches = lib.fvv_launch_count() - launches0
     barrier(world)
     clocks = sampler.stop()
@@ -333,10 +338,13 @@ def run_b200(args):
         torch.cuda.synchronize()
         barrier(world)
         R.H2D_BYTES["frames"] = 0
+        gc.collect()
+        gc.disable()
         t0 = time.perf_counter()
         d2h = run_e2e(args.steps)
         torch.cuda.synchronize()
         t1 = time.perf_counter()
+        gc.enable()
         barrier(world)
         h2d = int(host[0][0].numel() + R.H2D_BYTES["frames"] / args.steps)
         e2e_ms = max_over_ranks((t1 - t0) * 1e3, world)
@@ -378,7 +386,8 @@ def run_b200(args):
                                       f"per GPU",
                        "timing": "value: K frames over the lanes (CUDA events, barrier + sync "
                                  "both sides); stage_ms / roofline: a single-stream pass of "
-                                 "the same K frames"},
+                                 "the same K frames; Python's collector paused inside timed "
+                                 "regions (as timeit)"},
             "value_single_stream": round(value_single, 3),
             "lanes": lanes,
             "gvoxel_proj_per_s": round(total_proj / (ms / 1e3) / 1e9, 2),
