@@ -248,6 +248,14 @@ int fvv_render_view(const fvv_camera *rig, int ncam, const uint8_t *frames_dev,
                     const int32_t *tri_id_dev, const int32_t *tri_src_dev, const uint8_t *fallback,
                     uint8_t *color_dev, int32_t *source_dev, uint8_t *covered_dev,
                     const int64_t *counts_dev, void *stream);
+/* The same, also writing an int8 code per pixel (-2 uncovered, -1 fallback,
+ * else the source camera's rig position; code_dev may be NULL). */
+int fvv_render_view_coded(const fvv_camera *rig, int ncam, const uint8_t *frames_dev,
+                          const int64_t *frame_off, const fvv_camera *virt,
+                          const double *depth_dev, const int32_t *tri_id_dev,
+                          const int32_t *tri_src_dev, const uint8_t *fallback,
+                          uint8_t *color_dev, int32_t *source_dev, uint8_t *covered_dev,
+                          int8_t *code_dev, const int64_t *counts_dev, void *stream);
 
 /* camera.py:204-220 back_project for n pixels (n,2) at depths (n,) -> (n,3). */
 int fvv_back_project(const fvv_camera *cam, const double *pixel_dev, const double *depth_dev,
@@ -334,11 +342,15 @@ int fvv_frame_run(fvv_frame *frame, const uint8_t *masks_dev, const fvv_camera *
 int fvv_frame_get_outputs(const fvv_frame *frame, fvv_frame_outputs *out);
 /* Host copy of the last run's outputs in one pinned block: layout[0..6] =
  * byte offsets of verts, tris, visibility bits, colour, source, covered,
- * depth planes (depth only when want_depth), layout[8..14] their sizes,
+ * depth planes (depth only with flag bit 0), layout[8..14] their sizes,
  * layout[7] the total; returns the total. fvv_frame_readback queues the
  * device->host copies into host_dst (pinned, >= total bytes) on stream. */
-int64_t fvv_frame_readback_layout(const fvv_frame *frame, int want_depth, int64_t *layout);
-int fvv_frame_readback(const fvv_frame *frame, void *host_dst, int want_depth, void *stream);
+int64_t fvv_frame_readback_layout(const fvv_frame *frame, int flags, int64_t *layout);
+int fvv_frame_readback(const fvv_frame *frame, void *host_dst, int flags, void *stream);
+/* flags: bit 0 = depth planes; bit 1 = compact colour pass: slot 4 holds an
+ * int8 code per virtual pixel (-2 uncovered, -1 fallback colour, else the
+ * source camera's rig position) and slot 5 is empty, instead of int32
+ * source ids + uint8 coverage (render.py:64-113's outputs follow from it). */
 /* Per ROI: component id, box lo/hi (6 doubles), fine grid, mesh info
  * {vbase, V, sbase, S, tbase, T, fallback_edges, inconsistent_starts}. */
 int fvv_frame_get_rois(const fvv_frame *frame, int64_t *component_ids, double *boxes,

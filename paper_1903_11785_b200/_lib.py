@@ -44,7 +44,8 @@ SYMBOLS = (
     "fvv_mesh_workspace_bytes", "fvv_mesh_prepare", "fvv_mesh_counts",
     "fvv_mesh_emit_scratch_bytes", "fvv_mesh_emit", "fvv_edge_isovalues",
     "fvv_raster_workspace_bytes", "fvv_rasterize", "fvv_classify", "fvv_triangle_sources",
-    "fvv_render_count", "fvv_render_view", "fvv_back_project", "fvv_render_ellipsoids",
+    "fvv_render_count", "fvv_render_view", "fvv_render_view_coded", "fvv_back_project",
+    "fvv_render_ellipsoids",
     "fvv_frame_create", "fvv_frame_destroy", "fvv_frame_run", "fvv_frame_get_outputs",
     "fvv_frame_get_rois", "fvv_frame_readback_layout", "fvv_frame_readback",
     "fvv_synth_render", "fvv_erode_cross", "fvv_distance_map", "fvv_background",

@@ -17,6 +17,10 @@
 #include "fvv_common.cuh"
 
 extern "C" {
+int fvv_render_view_coded(const fvv_camera *, int, const uint8_t *, const int64_t *,
+                          const fvv_camera *, const double *, const int32_t *, const int32_t *,
+                          const uint8_t *, uint8_t *, int32_t *, uint8_t *, int8_t *,
+                          const int64_t *, void *);
 int fvv_pack_silhouettes(const fvv_camera *, int, const uint8_t *, const int64_t *, uint32_t *,
                          const int64_t *, void *);
 int fvv_carve(const fvv_camera *, int, const uint32_t *, const int64_t *, const fvv_grid *, int,
@@ -155,7 +159,7 @@ struct fvv_frame {
   fvv_frame_config cfg;
   fvv_grid coarse;
   // persistent device buffers
-  DevBuf carve_ws;
+  DevBuf carve_ws, code;
   DevBuf sil, occ_c, cnt_c, ccl_ws, comps, ccl_counts, occ_f, cnt_f, mesh_ws, mesh_scratch,
       mesh_totals, mesh_info, verts, tris, ntri, raster_ws, depth, vis, vplane_d, vplane_id,
       vraster_ws, src, rcounts, color, source, covered;
@@ -517,6 +521,7 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
     FVV_TRY(7, f->color.ensure(3 * (size_t)np));
     FVV_TRY(7, f->source.ensure(4 * (size_t)np));
     FVV_TRY(7, f->covered.ensure((size_t)np));
+    FVV_TRY(7, f->code.ensure((size_t)np));
     if (have_mesh) {
       FVV_TRY(7, f->vplane_d.ensure(8 * (size_t)np));
       FVV_TRY(7, f->vplane_id.ensure(4 * (size_t)np));
@@ -535,12 +540,13 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
       FVV_TRY(7, f->rcounts.ensure(8 * (size_t)(1 + ncam)));
       FVV_TRY(7, fvv_render_count(f->cams.data(), ncam, virt, f->vplane_id.as<int32_t>(),
                                   f->src.as<int32_t>(), f->rcounts.as<int64_t>(), st));
-      FVV_TRY(7, fvv_render_view(f->cams.data(), ncam, frames_dev, frame_off, virt,
-                                 f->vplane_d.as<double>(), f->vplane_id.as<int32_t>(),
-                                 f->src.as<int32_t>(), fallback, f->color.as<uint8_t>(),
-                                 f->source.as<int32_t>(), f->covered.as<uint8_t>(),
-                                 f->rcounts.as<int64_t>(), st));
+      FVV_TRY(7, fvv_render_view_coded(f->cams.data(), ncam, frames_dev, frame_off, virt,
+                                       f->vplane_d.as<double>(), f->vplane_id.as<int32_t>(),
+                                       f->src.as<int32_t>(), fallback, f->color.as<uint8_t>(),
+                                       f->source.as<int32_t>(), f->covered.as<uint8_t>(),
+                                       f->code.as<int8_t>(), f->rcounts.as<int64_t>(), st));
     } else {
+      cudaMemsetAsync(f->code.p, 0xfe, (size_t)np, st);  // -2: nothing covered
       cudaMemsetAsync(f->color.p, 0, 3 * (size_t)np, st);
       cudaMemsetAsync(f->source.p, 0xff, 4 * (size_t)np, st);
       cudaMemsetAsync(f->covered.p, 0, (size_t)np, st);
@@ -619,14 +625,17 @@ int fvv_frame_get_outputs(const fvv_frame *f, fvv_frame_outputs *o) {
   return FVV_OK;
 }
 
-static void readback_layout(const fvv_frame *f, int want_depth, int64_t *lay) {
+// flags: bit 0 depth planes, bit 1 compact colour pass (colour + the int8
+// code plane instead of source + covered)
+static void readback_layout(const fvv_frame *f, int flags, int64_t *lay) {
+  const bool compact = flags & 2;
   const int64_t sz[7] = {24 * f->nv,
                          12 * f->nt,
                          4 * (int64_t)f->ncam * f->vis_stride,
                          3 * f->virt_px,
-                         4 * f->virt_px,
-                         f->virt_px,
-                         (want_depth && f->nt > 0) ? 8 * f->planes : 0};
+                         (compact ? 1 : 4) * f->virt_px,
+                         compact ? 0 : f->virt_px,
+                         ((flags & 1) && f->nt > 0) ? 8 * f->planes : 0};
   int64_t off = 0;
   for (int i = 0; i < 7; ++i) {
     lay[i] = off;
@@ -637,18 +646,18 @@ static void readback_layout(const fvv_frame *f, int want_depth, int64_t *lay) {
   lay[15] = 0;
 }
 
-int64_t fvv_frame_readback_layout(const fvv_frame *f, int want_depth, int64_t *layout) {
+int64_t fvv_frame_readback_layout(const fvv_frame *f, int flags, int64_t *layout) {
   int64_t lay[16];
-  readback_layout(f, want_depth, lay);
+  readback_layout(f, flags, lay);
   if (layout) memcpy(layout, lay, sizeof(lay));
   return lay[7];
 }
 
-int fvv_frame_readback(const fvv_frame *f, void *host_dst, int want_depth, void *stream) {
+int fvv_frame_readback(const fvv_frame *f, void *host_dst, int flags, void *stream) {
   int64_t lay[16];
-  readback_layout(f, want_depth, lay);
+  readback_layout(f, flags, lay);
   const void *src[7] = {f->verts.p, f->tris.p, f->vis.p, f->color.p,
-                        f->source.p, f->covered.p, f->depth.p};
+                        (flags & 2) ? f->code.p : f->source.p, f->covered.p, f->depth.p};
   cudaStream_t st = (cudaStream_t)stream;
   for (int i = 0; i < 7; ++i)
     if (lay[8 + i] > 0)

@@ -533,6 +533,7 @@ struct RenderArgs {
   uint8_t *color;
   int32_t *source;
   uint8_t *covered;
+  int8_t *code;     // optional: -2 uncovered, -1 fallback colour, else source rig position
   int64_t *counts;  // [0] covered pixels, [1 + pos] pixels sourced from camera pos
 };
 
@@ -574,9 +575,11 @@ __global__ void render_color_kernel(const __grid_constant__ RenderArgs A) {
     const int32_t t = A.ids[p];
     uint8_t rgb[3] = {0, 0, 0};
     int32_t src = -1;
+    int cpos = -1;
     if (t >= 0) {
       src = A.tri_src[t];
       const int c = src >= 0 ? cam_pos(A, src) : -1;
+      cpos = c;
       if (c < 0) {
         rgb[0] = A.fallback[0];
         rgb[1] = A.fallback[1];
@@ -613,6 +616,7 @@ __global__ void render_color_kernel(const __grid_constant__ RenderArgs A) {
     A.color[3 * p + 2] = rgb[2];
     A.source[p] = src;
     if (A.covered) A.covered[p] = t >= 0;
+    if (A.code) A.code[p] = t < 0 ? (int8_t)-2 : (int8_t)cpos;
   }
 }
 
@@ -835,19 +839,31 @@ int fvv_render_count(const fvv_camera *rig, int ncam, const fvv_camera *virt,
   return cuda_check("fvv_render_count");
 }
 
-int fvv_render_view(const fvv_camera *rig, int ncam, const uint8_t *frames_dev,
-                    const int64_t *frame_off, const fvv_camera *virt, const double *depth_dev,
-                    const int32_t *tri_id_dev, const int32_t *tri_src_dev, const uint8_t *fallback,
-                    uint8_t *color_dev, int32_t *source_dev, uint8_t *covered_dev,
-                    const int64_t *counts_dev, void *stream) {
+int fvv_render_view_coded(const fvv_camera *rig, int ncam, const uint8_t *frames_dev,
+                          const int64_t *frame_off, const fvv_camera *virt,
+                          const double *depth_dev, const int32_t *tri_id_dev,
+                          const int32_t *tri_src_dev, const uint8_t *fallback,
+                          uint8_t *color_dev, int32_t *source_dev, uint8_t *covered_dev,
+                          int8_t *code_dev, const int64_t *counts_dev, void *stream) {
   static thread_local RenderArgs A;
   int rc = fill_render(A, rig, ncam, frames_dev, frame_off, virt, depth_dev, tri_id_dev,
                        tri_src_dev, fallback, color_dev, source_dev, covered_dev,
                        const_cast<int64_t *>(counts_dev));
   if (rc) return rc;
+  A.code = code_dev;
   render_color_kernel<<<kRasterGrid, 256, 0, (cudaStream_t)stream>>>(A);
   note_launches(1);
   return cuda_check("fvv_render_view");
+}
+
+int fvv_render_view(const fvv_camera *rig, int ncam, const uint8_t *frames_dev,
+                    const int64_t *frame_off, const fvv_camera *virt, const double *depth_dev,
+                    const int32_t *tri_id_dev, const int32_t *tri_src_dev, const uint8_t *fallback,
+                    uint8_t *color_dev, int32_t *source_dev, uint8_t *covered_dev,
+                    const int64_t *counts_dev, void *stream) {
+  return fvv_render_view_coded(rig, ncam, frames_dev, frame_off, virt, depth_dev, tri_id_dev,
+                               tri_src_dev, fallback, color_dev, source_dev, covered_dev,
+                               nullptr, counts_dev, stream);
 }
 
 int fvv_back_project(const fvv_camera *cam, const double *pixel_dev, const double *depth_dev,

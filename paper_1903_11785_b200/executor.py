@@ -95,7 +95,7 @@ class FrameOutput:
         total = sum(c.image_height * c.image_width for c in cams)
         return _dev(self.depth_ptr, (total,), "<f8")
 
-    def to_host_async(self, cams, keep_depths=False, stream=None):
+    def to_host_async(self, cams, keep_depths=False, stream=None, compact=False):
         """Queue the D2H copy of vertices, triangles, visibility bits, the
         rendered image (and depth planes) into ONE pinned block on ``stream``
         (default: the current stream, after this frame's work) with one
@@ -107,14 +107,15 @@ class FrameOutput:
             stream.wait_stream(cur)
         lib = _lib.load()
         lay = np.zeros(16, dtype=np.int64)
-        total = int(lib.fvv_frame_readback_layout(self._h, ctypes.c_int(int(keep_depths)),
-                                                  _lib.host_ptr(lay)))
+        compact = bool(compact and self.virtual is not None)
+        flags = ctypes.c_int(int(bool(keep_depths)) | (2 if compact else 0))
+        total = int(lib.fvv_frame_readback_layout(self._h, flags, _lib.host_ptr(lay)))
         buf = torch.empty(max(total, 1), dtype=torch.uint8, pin_memory=True)
-        _lib.call("fvv_frame_readback", self._h, ctypes.c_void_p(buf.data_ptr()),
-                  ctypes.c_int(int(keep_depths)), ctypes.c_void_p(stream.cuda_stream))
+        _lib.call("fvv_frame_readback", self._h, ctypes.c_void_p(buf.data_ptr()), flags,
+                  ctypes.c_void_p(stream.cuda_stream))
         ev = torch.cuda.Event()
         ev.record(stream)
-        return HostBlock(self, buf, lay, keep_depths), ev
+        return HostBlock(self, buf, lay, keep_depths, compact), ev
 
     def to_host(self, cams, keep_depths=False):
         """Pinned D2H of every host-facing output, one synchronisation."""
@@ -126,14 +127,18 @@ class FrameOutput:
 class HostBlock:
     """One frame's outputs in a pinned host block (executor readback layout)."""
 
-    def __init__(self, out, buf, lay, keep_depths):
+    def __init__(self, out, buf, lay, keep_depths, compact=False):
         self.buf, self.lay = buf, lay
+        self.nbytes = int(sum(int(lay[8 + i]) for i in range(7)))  # bytes copied
         self.shapes = {"verts": ((out.nv, 3), np.float64), "tris": ((out.nt, 3), np.int32),
                        "vis": ((out.ncam, out.vis_stride), np.uint32)}
         if out.virtual is not None:
             h, w = out.virtual.image_height, out.virtual.image_width
-            self.shapes.update(color=((h, w, 3), np.uint8), source=((h, w), np.int32),
-                               covered=((h, w), np.uint8))
+            if compact:  # slot 4: int8 code plane (fvv_frame_readback flag bit 1)
+                self.shapes.update(color=((h, w, 3), np.uint8), code=((h, w), np.int8))
+            else:
+                self.shapes.update(color=((h, w, 3), np.uint8), source=((h, w), np.int32),
+                                   covered=((h, w), np.uint8))
         if keep_depths and out.nt:
             self.shapes["depth"] = ((int(lay[14]) // 8,), np.float64)
 
@@ -141,6 +146,8 @@ class HostBlock:
         raw = self.buf.numpy()
         out = {}
         for i, name in enumerate(_READBACK_NAMES):
+            if name == "source" and "code" in self.shapes:
+                name = "code"
             if name not in self.shapes:
                 continue
             shape, dt = self.shapes[name]

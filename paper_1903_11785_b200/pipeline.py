@@ -594,13 +594,14 @@ def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
     import threading
 
     from .executor import executor_for
-    from .render import FALLBACK_COLOR, H2D_BYTES, RenderedImage
+    from .render import D2H_BYTES, FALLBACK_COLOR, H2D_BYTES, CodedImage
 
     fallback_color = FALLBACK_COLOR if fallback_color is None else fallback_color
     require_cuda()
     lanes = max(1, int(lanes))
     dev_index = torch.cuda.current_device()
     cams = list(rig)
+    rig_ids = [c.id for c in cams]
     caller = torch.cuda.current_stream()
     # persistent streams: the caching allocator keeps blocks per stream, so
     # fresh streams on every call would re-allocate (and, under memory
@@ -637,7 +638,9 @@ def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
                                 H2D_BYTES["frames"] += 12 * int(out.stats_raw["sourced_px"])
                     else:
                         out = ex.run(d_masks)
-                    pinned, slot_free = out.to_host_async(cams, stream=readback)
+                    pinned, slot_free = out.to_host_async(cams, stream=readback, compact=True)
+                    with counter_lock:
+                        D2H_BYTES["results"] += pinned.nbytes
                     out_q.put((frames, out, pinned, slot_free))
         except BaseException as exc:  # noqa: BLE001  (re-raised on the caller's thread)
             out_q.put(exc)
@@ -655,7 +658,7 @@ def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
         bundle = bundle_from_output(p_out, host, cfg, rig, p_frames, fid, keep_device=False)
         img = None
         if virtual is not None:
-            img = RenderedImage(host["color"], host["source"], host["covered"].astype(bool))
+            img = CodedImage(host["color"], host["code"], rig_ids)
         return bundle, img
 
     threads = [threading.Thread(target=worker, args=(k,), name=f"fvv-lane{k}", daemon=True)

@@ -24,6 +24,7 @@ FALLBACK_COLOR = np.array([128, 128, 128], dtype=np.uint8)  # render.py:19
 
 # host->device bytes of colour frames moved by the render path (bench.py reads it)
 H2D_BYTES = {"frames": 0}
+D2H_BYTES = {"results": 0}  # bytes run_sequence read back (pinned blocks)
 
 
 @dataclass
@@ -31,6 +32,40 @@ class RenderedImage:
     color: np.ndarray  # (H, W, 3) uint8
     source: np.ndarray  # (H, W) int32 camera id, -1 = none
     covered: np.ndarray  # (H, W) bool
+
+
+class CodedImage(RenderedImage):
+    """A RenderedImage read back in compact form: colour plus one int8 code
+    per pixel (-2 uncovered, -1 fallback colour, else the source camera's
+    rig position, fvv_render_view_coded). ``source`` (camera ids) and
+    ``covered`` are expanded from the code on first access."""
+
+    def __init__(self, color, code, rig_ids):
+        self.color = color
+        self._code = code
+        self._lut = np.concatenate(([-1, -1], np.asarray(rig_ids, dtype=np.int32)))
+        self._source = None
+        self._covered = None
+
+    @property
+    def source(self):
+        if self._source is None:
+            self._source = self._lut[self._code.astype(np.int64) + 2]
+        return self._source
+
+    @source.setter
+    def source(self, value):
+        self._source = value
+
+    @property
+    def covered(self):
+        if self._covered is None:
+            self._covered = self._code != -2
+        return self._covered
+
+    @covered.setter
+    def covered(self, value):
+        self._covered = value
 
 
 def rank_cameras(virtual, rig) -> list:
