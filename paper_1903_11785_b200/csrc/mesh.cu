@@ -19,6 +19,7 @@
 // isovalues, vertices and triangles. All float64 work uses the reference's
 // operation order (fvv_common.cuh, -fmad=false).
 #include <cstring>
+#include <mutex>
 
 #include "mc_cases.cuh"
 #include "scan.cuh"
@@ -689,16 +690,18 @@ static MeshBufs bufs_from(void *ws, const PrepLayout &L) {
 
 using namespace fvv;
 
-static bool g_tables_ready = false;
+// marching-cubes tables into constant memory once per process (executor
+// lanes may race here on first use)
+static std::once_flag g_tables_once;
+static int g_tables_rc = FVV_OK;
 
 static int ensure_tables() {
-  if (g_tables_ready) return FVV_OK;
-  if (cudaMemcpyToSymbol(c_mc_edges, FVV_MC_EDGES, sizeof(FVV_MC_EDGES)) != cudaSuccess ||
-      cudaMemcpyToSymbol(c_mc_ntri, FVV_MC_NTRI, sizeof(FVV_MC_NTRI)) != cudaSuccess) {
-    return cuda_check("mesh tables");
-  }
-  g_tables_ready = true;
-  return FVV_OK;
+  std::call_once(g_tables_once, [] {
+    if (cudaMemcpyToSymbol(c_mc_edges, FVV_MC_EDGES, sizeof(FVV_MC_EDGES)) != cudaSuccess ||
+        cudaMemcpyToSymbol(c_mc_ntri, FVV_MC_NTRI, sizeof(FVV_MC_NTRI)) != cudaSuccess)
+      g_tables_rc = cuda_check("mesh tables");
+  });
+  return g_tables_rc;
 }
 
 extern "C" {
