@@ -206,15 +206,17 @@ __device__ __forceinline__ unsigned long long candidate_mask(const TriSetup &s) 
     bool empty = false;
     const float sv0 = fmaf(a0, gy, c0) + m0, sv1 = fmaf(a1, gy, c1) + m1,
                 sv2 = fmaf(a2, gy, c2) + m2;
-    if (b0 > 0.0f) hi = fminf(hi, fmaf(sv0, ib0, 1e-3f));
-    else if (b0 < 0.0f) lo = fmaxf(lo, fmaf(sv0, ib0, -1e-3f));
-    else empty |= sv0 < 0.0f;
-    if (b1 > 0.0f) hi = fminf(hi, fmaf(sv1, ib1, 1e-3f));
-    else if (b1 < 0.0f) lo = fmaxf(lo, fmaf(sv1, ib1, -1e-3f));
-    else empty |= sv1 < 0.0f;
-    if (b2 > 0.0f) hi = fminf(hi, fmaf(sv2, ib2, 1e-3f));
-    else if (b2 < 0.0f) lo = fmaxf(lo, fmaf(sv2, ib2, -1e-3f));
-    else empty |= sv2 < 0.0f;
+    // branchless: b > 0 bounds gx from above, b < 0 from below, b == 0 keeps
+    // the whole row iff sv >= 0
+    const float t0 = sv0 * ib0, t1 = sv1 * ib1, t2 = sv2 * ib2;
+    hi = fminf(hi, b0 > 0.0f ? t0 + 1e-3f : INFINITY);
+    lo = fmaxf(lo, b0 < 0.0f ? t0 - 1e-3f : -INFINITY);
+    hi = fminf(hi, b1 > 0.0f ? t1 + 1e-3f : INFINITY);
+    lo = fmaxf(lo, b1 < 0.0f ? t1 - 1e-3f : -INFINITY);
+    hi = fminf(hi, b2 > 0.0f ? t2 + 1e-3f : INFINITY);
+    lo = fmaxf(lo, b2 < 0.0f ? t2 - 1e-3f : -INFINITY);
+    empty = ((b0 == 0.0f) & (sv0 < 0.0f)) | ((b1 == 0.0f) & (sv1 < 0.0f)) |
+            ((b2 == 0.0f) & (sv2 < 0.0f));
     const int x0 = (int)ceilf(lo), x1 = (int)floorf(hi);  // NaN bounds -> empty below
     if (!empty && x0 <= x1 && lo <= hi) {
       const unsigned long long run = (x1 - x0 >= 63) ? ~0ull : ((2ull << (x1 - x0)) - 1ull);
