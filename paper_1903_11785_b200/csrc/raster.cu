@@ -86,16 +86,14 @@ __device__ __forceinline__ bool tri_setup(int width, int height, const double4 *
   s.hix = chx < W1 ? (int)chx : width - 1;
   s.hiy = chy < H1 ? (int)chy : height - 1;
   if (s.hix < s.lox || s.hiy < s.loy) return false;
-  double x0 = u[0], y0 = v[0], x1 = u[1], y1 = v[1], x2 = u[2], y2 = v[2];
-  double za = z[0], zb = z[1], zc = z[2];
-  double area = (x1 - x0) * (y2 - y0) - (y1 - y0) * (x2 - x0);
-  if (area == 0.0) return false;
-  if (area < 0.0) {  // swap v1 <-> v2 (visibility.py:63-66)
-    double tx = x1, ty = y1;
-    x1 = x2; y1 = y2; x2 = tx; y2 = ty;
-    double tz = zb; zb = zc; zc = tz;
-    area = -area;
-  }
+  const double x0 = u[0], y0 = v[0], za = z[0];
+  const double area0 = (u[1] - x0) * (v[2] - y0) - (v[1] - y0) * (u[2] - x0);
+  if (area0 == 0.0) return false;
+  // swap v1 <-> v2 when the area is negative (visibility.py:63-66), branch-free
+  const bool sw = area0 < 0.0;
+  const double x1 = sw ? u[2] : u[1], y1 = sw ? v[2] : v[1], zb = sw ? z[2] : z[1];
+  const double x2 = sw ? u[1] : u[2], y2 = sw ? v[1] : v[2], zc = sw ? z[1] : z[2];
+  const double area = sw ? -area0 : area0;
   s.x0 = x0; s.y0 = y0; s.x1 = x1; s.y1 = y1; s.x2 = x2; s.y2 = y2;
   s.za = za; s.zb = zb; s.zc = zc; s.area = area;
   s.tl0 = top_left(x1, y1, x2, y2);
