@@ -294,23 +294,30 @@ __global__ void __launch_bounds__(kCarveThreads)
   __shared__ int state[FVV_MAX_CAMS];
   __shared__ int mixed[FVV_MAX_CAMS];
   __shared__ int n_mixed, n_fg, culled;
-  const int64_t b = blockIdx.x;
-  int g = 0;  // binary search of the block's grid (uniform across the block)
-  for (int step = FVV_MAX_GRIDS / 2; step >= 1; step >>= 1)
-    if (g + step < p.ngrid && b >= p.blk_start[g + step]) g += step;
+  __shared__ int blk[4];  // grid, tile origin i0 j0 k0 (thread 0, for the block)
+  const int tl = p.tile_log2, kT = 1 << tl;
+  if (threadIdx.x == 0) {
+    const int64_t b = blockIdx.x;
+    int gg = 0;  // binary search of the block's grid
+    for (int step = FVV_MAX_GRIDS / 2; step >= 1; step >>= 1)
+      if (gg + step < p.ngrid && b >= p.blk_start[gg + step]) gg += step;
+    const uint32_t tx = p.tiles_x[gg], ty = p.tiles_y[gg];
+    const uint32_t tile = (uint32_t)(b - p.blk_start[gg]);  // < 2^32 tiles per grid
+    const uint32_t tq = tile / tx;
+    blk[0] = gg;
+    blk[1] = (int)((tile - tq * tx) * kT);
+    blk[2] = (int)((tq % ty) * kT);
+    blk[3] = (int)((tq / ty) * kT);
+    culled = 0;
+  }
+  __syncthreads();
+  const int g = blk[0], i0 = blk[1], j0 = blk[2], k0 = blk[3];
   const fvv_grid &G = p.grids[g];
   const int64_t nx = G.dims[0], ny = G.dims[1], nz = G.dims[2];
-  const int tl = p.tile_log2, kT = 1 << tl;
-  const uint32_t tx = p.tiles_x[g], ty = p.tiles_y[g];
-  const uint32_t tile = (uint32_t)(b - p.blk_start[g]);  // < 2^32 tiles per grid
-  const uint32_t tq = tile / tx;
-  const int64_t ti = tile - tq * tx, tj = tq % ty, tk = tq / ty;
-  const int i0 = (int)(ti * kT), j0 = (int)(tj * kT), k0 = (int)(tk * kT);
   const int i1 = (int)min((int64_t)i0 + kT, nx) - 1, j1 = (int)min((int64_t)j0 + kT, ny) - 1,
             k1 = (int)min((int64_t)k0 + kT, nz) - 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int kWarps = kCarveThreads / 32;
-  if (threadIdx.x == 0) culled = 0;
   {  // this grid's camera coefficients (carve_affine_kernel) into shared memory
     const float4 *src = (const float4 *)(p.affine + (int64_t)g * p.ncam);
     float4 *dst = (float4 *)aff;
