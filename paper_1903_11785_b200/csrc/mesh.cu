@@ -39,6 +39,7 @@ struct MeshGridInfo {
   int64_t occ_word_off;  // F-order occupancy words of this grid
   int64_t rows, nzw;     // rows = nx*ny (0 when a dim < 2: empty mesh, mesh.py:298-299)
   int64_t tw_off;        // transposed-word offset (S space); V space offset = 3*tw_off
+  uint32_t words32, nzw32, ny32, pad;  // rows*nzw, nzw, ny (3*tw_total < 2^31)
 };
 
 struct MeshGrids {
@@ -82,14 +83,6 @@ __device__ __forceinline__ int grid_of(const MeshGrids &G, int64_t e) {
   return lo;
 }
 
-__device__ __forceinline__ uint32_t kmask(int64_t w, int64_t limit) {
-  // bits b of word w with 32*w + b < limit
-  const int64_t lo = w * 32;
-  if (limit <= lo) return 0u;
-  if (limit >= lo + 32) return 0xffffffffu;
-  return (1u << (limit - lo)) - 1u;
-}
-
 __device__ __forceinline__ uint32_t row_word(const uint32_t *tw, const MeshGridInfo &gi, int64_t q,
                                              int64_t w) {
   return (w < gi.nzw) ? tw[gi.tw_off + q * gi.nzw + w] : 0u;
@@ -107,10 +100,11 @@ __global__ void mesh_transpose_kernel(const __grid_constant__ MeshGrids G, MeshB
        e += (int64_t)gridDim.x * blockDim.x) {
     const int g = grid_of(G, e);
     const MeshGridInfo &gi = G.gi[g];
-    const int64_t local = e - G.tw_start[g];
-    const int64_t q = local / gi.nzw, w = local - q * gi.nzw;
+    const uint32_t local = (uint32_t)(e - G.tw_start[g]);
+    const uint32_t q = local / gi.nzw32, w32 = local - q * gi.nzw32;
+    const uint32_t i32 = q / gi.ny32;
     const int64_t nx = gi.g.dims[0], ny = gi.g.dims[1], nz = gi.g.dims[2];
-    const int64_t i = q / ny, j = q - i * ny;
+    const int64_t w = w32, i = i32, j = q - i32 * gi.ny32;
     uint32_t out = 0;
     const int64_t kend = (w * 32 + 32 < nz) ? w * 32 + 32 : nz;
     for (int64_t k = w * 32; k < kend; ++k) {
@@ -123,41 +117,52 @@ __global__ void mesh_transpose_kernel(const __grid_constant__ MeshGrids G, MeshB
 }
 
 // ---- A2: vertex (edge-flag) scan over (grid, axis, row, word) ---------------
+// bits b of word w (of a row of n bits) with 32*w + b < n
+__device__ __forceinline__ uint32_t kmask32(uint32_t w, int64_t n) {
+  const int64_t r = n - 32 * (int64_t)w;
+  return r <= 0 ? 0u : r >= 32 ? 0xffffffffu : (1u << r) - 1u;
+}
+
+// grid of element e of a space where grid g starts at mult*tw_start[g]
+__device__ __forceinline__ int grid_of_scaled(const MeshGrids &G, int64_t e, int mult) {
+  int lo = 0, hi = G.ngrid - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (mult * G.tw_start[mid] <= e) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// One scan element = one word; decoded with 32-bit arithmetic (fill_grids
+// bounds 3*tw_total below 2^31).
 struct EdgeFlags {
   MeshGrids G;
   const uint32_t *tw;
   uint32_t *eflags;
   int32_t *vprefix;
-  __device__ uint32_t compute(int64_t e) const {
+  typedef uint32_t Item;
+  __device__ uint32_t load(int64_t e) const {
     // V space: grid g occupies [3*tw_start[g], 3*tw_start[g+1]), axis-major
-    const MeshGrids &g_ = G;
-    int lo = 0, hi = g_.ngrid - 1;
-    while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (3 * g_.tw_start[mid] <= e) lo = mid; else hi = mid - 1;
-    }
-    const MeshGridInfo &gi = g_.gi[lo];
-    const int64_t per_axis = gi.rows * gi.nzw;
-    const int64_t local = e - 3 * g_.tw_start[lo];
-    const int axis = (int)(local / per_axis);
-    const int64_t rw = local - axis * per_axis;
-    const int64_t q = rw / gi.nzw, w = rw - q * gi.nzw;
-    const int64_t nx = gi.g.dims[0], ny = gi.g.dims[1], nz = gi.g.dims[2];
-    const int64_t i = q / ny, j = q - i * ny;
-    const uint32_t x = row_word(tw, gi, q, w);
-    uint32_t f;
-    if (axis == 0) {
-      f = (i < nx - 1) ? (x ^ row_word(tw, gi, q + ny, w)) & kmask(w, nz) : 0u;
-    } else if (axis == 1) {
-      f = (j < ny - 1) ? (x ^ row_word(tw, gi, q + 1, w)) & kmask(w, nz) : 0u;
-    } else {
-      f = (x ^ row_next(tw, gi, q, w)) & kmask(w, nz - 1);
-    }
-    return f;
+    const int g = grid_of_scaled(G, e, 3);
+    const MeshGridInfo &gi = G.gi[g];
+    const uint32_t local = (uint32_t)(e - 3 * G.tw_start[g]);
+    const uint32_t per_axis = gi.words32, nzw = gi.nzw32, ny = gi.ny32;
+    const uint32_t axis = local / per_axis;
+    const uint32_t rw = local - axis * per_axis;
+    const uint32_t q = rw / nzw, w = rw - q * nzw;
+    const uint32_t i = q / ny, j = q - i * ny;
+    const uint32_t *row = tw + gi.tw_off + rw;  // word w of row q
+    const uint32_t x = row[0];
+    const int64_t nz = gi.g.dims[2];
+    if (axis == 0)
+      return (i + 1 < (uint32_t)gi.g.dims[0]) ? (x ^ row[ny * nzw]) & kmask32(w, nz) : 0u;
+    if (axis == 1) return (j + 1 < ny) ? (x ^ row[nzw]) & kmask32(w, nz) : 0u;
+    const uint32_t next = (x >> 1) | ((w + 1 < nzw ? row[1] : 0u) << 31);  // bit b holds k+1
+    return (x ^ next) & kmask32(w, nz - 1);
   }
-  __device__ int64_t value(int64_t e) const { return __popc(compute(e)); }
-  __device__ void emit(int64_t e, int64_t prefix, int64_t) const {
-    eflags[e] = compute(e);
+  __device__ int64_t value(uint32_t f) const { return __popc(f); }
+  __device__ void emit(int64_t e, int64_t prefix, uint32_t f) const {
+    eflags[e] = f;
     vprefix[e] = (int32_t)prefix;
   }
 };
@@ -168,32 +173,31 @@ struct CellFlags {
   const uint32_t *tw;
   uint32_t *sflags;
   int32_t *sprefix;
-  __device__ uint32_t compute(int64_t e) const {
-    const MeshGrids &g_ = G;
-    int lo = 0, hi = g_.ngrid - 1;
-    while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (g_.tw_start[mid] <= e) lo = mid; else hi = mid - 1;
-    }
-    const MeshGridInfo &gi = g_.gi[lo];
-    const int64_t rw = e - g_.tw_start[lo];
-    const int64_t q = rw / gi.nzw, w = rw - q * gi.nzw;
-    const int64_t nx = gi.g.dims[0], ny = gi.g.dims[1], nz = gi.g.dims[2];
-    const int64_t i = q / ny, j = q - i * ny;
-    if (i >= nx - 1 || j >= ny - 1) return 0u;
-    const int64_t rows[4] = {q, q + ny, q + ny + 1, q + 1};
+  typedef uint32_t Item;
+  __device__ uint32_t load(int64_t e) const {
+    const int g = grid_of_scaled(G, e, 1);
+    const MeshGridInfo &gi = G.gi[g];
+    const uint32_t rw = (uint32_t)(e - G.tw_start[g]);
+    const uint32_t nzw = gi.nzw32, ny = gi.ny32;
+    const uint32_t q = rw / nzw, w = rw - q * nzw;
+    const uint32_t i = q / ny, j = q - i * ny;
+    if (i + 1 >= (uint32_t)gi.g.dims[0] || j + 1 >= ny) return 0u;
+    const uint32_t *row = tw + gi.tw_off + rw;
+    const uint32_t off[4] = {0u, ny * nzw, (ny + 1) * nzw, nzw};  // rows q, q+ny, q+ny+1, q+1
+    const bool more = w + 1 < nzw;
     uint32_t any = 0u, all = 0xffffffffu;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      const uint32_t a = row_word(tw, gi, rows[r], w), b = row_next(tw, gi, rows[r], w);
+      const uint32_t a = row[off[r]];
+      const uint32_t b = (a >> 1) | ((more ? row[off[r] + 1] : 0u) << 31);
       any |= a | b;
       all &= a & b;
     }
-    return (any & ~all) & kmask(w, nz - 1);
+    return (any & ~all) & kmask32(w, gi.g.dims[2] - 1);
   }
-  __device__ int64_t value(int64_t e) const { return __popc(compute(e)); }
-  __device__ void emit(int64_t e, int64_t prefix, int64_t) const {
-    sflags[e] = compute(e);
+  __device__ int64_t value(uint32_t f) const { return __popc(f); }
+  __device__ void emit(int64_t e, int64_t prefix, uint32_t f) const {
+    sflags[e] = f;
     sprefix[e] = (int32_t)prefix;
   }
 };
@@ -244,15 +248,15 @@ __device__ __forceinline__ int decode_vkey(const MeshGrids &G, int64_t key, int 
     if (3 * G.tw_start[mid] <= e) lo = mid; else hi = mid - 1;
   }
   const MeshGridInfo &gi = G.gi[lo];
-  const int64_t per_axis = gi.rows * gi.nzw;
-  const int64_t local = e - 3 * G.tw_start[lo];
-  axis = (int)(local / per_axis);
-  const int64_t rw = local - axis * per_axis;
-  const int64_t q = rw / gi.nzw, w = rw - q * gi.nzw;
-  const int64_t ny = gi.g.dims[1];
-  i = q / ny;
-  j = q - i * ny;
-  k = w * 32 + (key & 31);
+  const uint32_t local = (uint32_t)(e - 3 * G.tw_start[lo]);  // 32-bit (fill_grids)
+  const uint32_t a = local / gi.words32;
+  const uint32_t rw = local - a * gi.words32;
+  const uint32_t q = rw / gi.nzw32, w = rw - q * gi.nzw32;
+  const uint32_t i32 = q / gi.ny32;
+  axis = (int)a;
+  i = i32;
+  j = q - i32 * gi.ny32;
+  k = (int64_t)w * 32 + (key & 31);
   return lo;
 }
 
@@ -431,11 +435,11 @@ __device__ __forceinline__ void mesh_cell(const MeshGrids &G, const MeshBufs &B,
   }
   const int g = lo;
   const MeshGridInfo &gi = G.gi[g];
-  const int64_t rw = e - G.tw_start[g];
-  const int64_t q = rw / gi.nzw, w = rw - q * gi.nzw;
-  const int64_t ny = gi.g.dims[1];
-  const int64_t i = q / ny, j = q - i * ny;
-  const int64_t k = w * 32 + b;
+  const uint32_t rw = (uint32_t)(e - G.tw_start[g]);
+  const uint32_t q32 = rw / gi.nzw32, w = rw - q32 * gi.nzw32;
+  const uint32_t i32 = q32 / gi.ny32;
+  const int64_t q = q32, i = i32, j = q32 - i32 * gi.ny32;
+  const int64_t k = (int64_t)w * 32 + b;
   const int ci = cell_case(B, gi, q, k);
   const int ntri = c_mc_ntri[ci];
   const unsigned long long edges = c_mc_edges[ci];
@@ -522,13 +526,14 @@ struct Slot5 {
 struct TriScan {
   const int32_t *cell_mask;
   int32_t *cprefix;
-  __device__ Slot5 value(int64_t c) const {
-    const int keep = cell_mask[c] >> 8;
+  typedef int Item;
+  __device__ int load(int64_t c) const { return cell_mask[c] >> 8; }
+  __device__ Slot5 value(int keep) const {
     Slot5 s;
     for (int t = 0; t < 5; ++t) s.v[t] = (keep >> t) & 1;
     return s;
   }
-  __device__ void emit(int64_t c, Slot5 prefix, Slot5) const {
+  __device__ void emit(int64_t c, Slot5 prefix, int) const {
     for (int t = 0; t < 5; ++t) cprefix[5 * c + t] = prefix.v[t];
   }
 };
@@ -592,10 +597,10 @@ __global__ void mesh_emit_kernel(const __grid_constant__ MeshGrids G, MeshBufs B
     }
     const int g = lo;
     const MeshGridInfo &gi = G.gi[g];
-    const int64_t rw = e - G.tw_start[g];
-    const int64_t q = rw / gi.nzw, w = rw - q * gi.nzw;
-    const int64_t ny = gi.g.dims[1];
-    const int64_t i = q / ny, j = q - i * ny, k = w * 32 + (key & 31);
+    const uint32_t rw = (uint32_t)(e - G.tw_start[g]);
+    const uint32_t q32 = rw / gi.nzw32, w = rw - q32 * gi.nzw32;
+    const uint32_t i32 = q32 / gi.ny32;
+    const int64_t q = q32, i = i32, j = q32 - i32 * gi.ny32, k = (int64_t)w * 32 + (key & 31);
     const unsigned long long edges = c_mc_edges[ci];
     for (int t = 0; t < 5; ++t) {
       if (!((keep >> t) & 1)) continue;
@@ -662,8 +667,16 @@ static int fill_grids(const fvv_grid *grids, int ngrid, const int64_t *word_off,
     gi.rows = meshable ? nx * ny : 0;
     gi.nzw = meshable ? (nz + 31) / 32 : 1;
     gi.tw_off = acc;
+    gi.words32 = (uint32_t)(gi.rows * gi.nzw);
+    gi.nzw32 = (uint32_t)gi.nzw;
+    gi.ny32 = (uint32_t)ny;
     h_grids.tw_start[g] = acc;
     acc += gi.rows * gi.nzw;
+    if (3 * acc >= (int64_t)1 << 31) {  // 32-bit word indices (and int32 vertex prefixes)
+      set_error("mesh: %lld occupancy words over the batch (limit %lld)", (long long)acc,
+                (long long)((((int64_t)1 << 31) - 1) / 3));
+      return FVV_E_LIMIT;
+    }
   }
   for (int g = ngrid; g <= FVV_MAX_GRIDS; ++g) h_grids.tw_start[g] = acc;
   h_grids.tw_total = acc;

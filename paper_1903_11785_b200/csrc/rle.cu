@@ -23,9 +23,10 @@ struct RleTransitions {
     if (w == words - 1 && (nvox & 31)) t &= (1u << (nvox & 31)) - 1u;  // positions < nvox
     return t;
   }
-  __device__ int64_t value(int64_t w) const { return __popc(tmask(w)); }
-  __device__ void emit(int64_t w, int64_t prefix, int64_t) const {
-    uint32_t t = tmask(w);
+  typedef uint32_t Item;
+  __device__ uint32_t load(int64_t w) const { return tmask(w); }
+  __device__ int64_t value(uint32_t t) const { return __popc(t); }
+  __device__ void emit(int64_t w, int64_t prefix, uint32_t t) const {
     while (t) {
       const int b = __ffs(t) - 1;
       t &= t - 1;

@@ -111,8 +111,10 @@ inline int64_t scan_chunks(int64_t n_max) { return (n_max + kScanChunk - 1) / kS
 // ---- single pass: decoupled look-back ----------------------------------------
 // Chunks are taken in order from a ticket counter; each publishes its
 // aggregate, then (after looking back over its predecessors) its inclusive
-// prefix. f.value is evaluated once per element; one launch (plus a memset
-// of the status words) replaces the three of ordered_scan.
+// prefix. One launch (plus a memset of the status words) replaces the three
+// of ordered_scan. The functor is split so each element is decoded once:
+// `Item load(int64_t i)`, `T value(const Item &)` and
+// `void emit(int64_t i, T prefix, const Item &)`.
 template <typename T>
 struct ScanStatus {
   T agg, incl;
@@ -169,11 +171,13 @@ __global__ void __launch_bounds__(kScanThreads)
     __syncthreads();
     const int64_t c = tile_s;
     if (c >= nchunks) break;
+    typename F::Item item[kScanItems];
     T v[kScanItems], ex[kScanItems];
 #pragma unroll
     for (int it = 0; it < kScanItems; ++it) {
       const int64_t i = c * kScanChunk + (int64_t)threadIdx.x * kScanItems + it;
-      v[it] = i < n ? f.value(i) : T(0);
+      item[it] = i < n ? f.load(i) : typename F::Item();
+      v[it] = i < n ? f.value(item[it]) : T(0);
     }
     T agg;
     Scan(tmp).ExclusiveSum(v, ex, agg);
@@ -215,7 +219,7 @@ __global__ void __launch_bounds__(kScanThreads)
 #pragma unroll
     for (int it = 0; it < kScanItems; ++it) {
       const int64_t i = c * kScanChunk + (int64_t)threadIdx.x * kScanItems + it;
-      if (i < n) f.emit(i, base + ex[it], v[it]);
+      if (i < n) f.emit(i, base + ex[it], item[it]);
     }
     __syncthreads();
   }
