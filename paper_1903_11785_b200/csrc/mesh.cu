@@ -300,14 +300,28 @@ __device__ __forceinline__ bool edge_lambda_cam(const fvv_camera &cam,
   incons = false;
   if (!(ino && inf)) return false;
   const int ax = (int)rint(uo), ay = (int)rint(vo), bx = (int)rint(uf), by = (int)rint(vf);
-  const int len = max(abs(bx - ax), abs(by - ay)) + 1;
-  int first_bg = -1;
-  for (int t = 0; t < len; ++t) {
-    int x, y;
-    bresenham_px(ax, ay, bx, by, t, x, y);
+  // the pixels of bresenham_px for t = 0..major, walked incrementally: the
+  // minor offset floor((2 t dmin + dmaj) / (2 dmaj)) advances by at most one
+  // per step (dmin <= dmaj), tracked as quotient + remainder
+  const int dx = abs(bx - ax), dy = abs(by - ay);
+  const int sx = bx >= ax ? 1 : -1, sy = by >= ay ? 1 : -1;
+  const bool xmajor = dx >= dy;
+  const int major = xmajor ? dx : dy;
+  const int64_t two_maj = 2 * (int64_t)(major > 1 ? major : 1), two_min = 2 * (int64_t)(xmajor ? dy : dx);
+  int64_t rem = two_maj / 2;
+  int smin = 0, first_bg = -1, lx = ax, ly = ay;
+  for (int t = 0; t <= major; ++t) {
+    const int x = ax + sx * (xmajor ? t : smin), y = ay + sy * (xmajor ? smin : t);
     if (!sil_bit(plane, stride, x, y)) {
       first_bg = t;
       break;
+    }
+    lx = x;  // last foreground pixel so far
+    ly = y;
+    rem += two_min;
+    if (rem >= two_maj) {
+      rem -= two_maj;
+      ++smin;
     }
   }
   const double ddx = uf - uo, ddy = vf - vo;
@@ -317,8 +331,6 @@ __device__ __forceinline__ bool edge_lambda_cam(const fvv_camera &cam,
     incons = true;
     lam_i = 0.0;
   } else if (first_bg > 0 && denom > 1e-12) {
-    int lx, ly;
-    bresenham_px(ax, ay, bx, by, first_bg - 1, lx, ly);
     const double ex = (double)lx - uo, ey = (double)ly - vo;
     const double qv = sqrt(ex * ex + ey * ey) / denom;
     lam_i = qv > 1.0 ? 1.0 : qv;
