@@ -321,6 +321,7 @@ def run_b200(args):
             total = 0
             t_prev = time.perf_counter()
             gaps = []
+            c_prev, m_prev = time.process_time(), time.thread_time()
             d2h0 = R.D2H_BYTES["results"]
             for bundle, img in run_sequence(cfg, rig, fr, ms_, virt, lanes=lanes):
                 consume(bundle, img)
@@ -328,7 +329,15 @@ def run_b200(args):
                 gaps.append(round((t_now - t_prev) * 1e3, 2))
                 t_prev = t_now
             if trace:
+                hs = torch.cuda.host_memory_stats()
                 print(f"e2e intervals (ms): {gaps}", file=sys.stderr)
+                print(f"host CPU ms per frame (all threads): "
+                      f"{(time.process_time() - c_prev) * 1e3 / nsteps:.3f}; caller thread: "
+                      f"{(time.thread_time() - m_prev) * 1e3 / nsteps:.3f}", file=sys.stderr)
+                print("host allocator: " + ", ".join(
+                    f"{k}={hs[k]}" for k in sorted(hs) if k.startswith(("num_host", "allocations.",
+                                                                       "active_requests"))),
+                      file=sys.stderr)
             total = R.D2H_BYTES["results"] - d2h0  # bytes read back (pinned blocks)
             return total
 

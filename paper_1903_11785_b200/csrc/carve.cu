@@ -288,7 +288,7 @@ __device__ __forceinline__ void carve_affine(const CarveParams &p, CamAffine *ou
     cam_affine(p.cams[e % p.ncam], p.grids[e / p.ncam], out[e]);
 }
 
-__global__ void __launch_bounds__(kCarveThreads)
+__global__ void __launch_bounds__(kCarveThreads, 6)
     carve_kernel(const __grid_constant__ CarveParams p) {
   __shared__ CamAffine aff[FVV_MAX_CAMS];
   __shared__ int state[FVV_MAX_CAMS];

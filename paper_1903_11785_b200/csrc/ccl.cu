@@ -53,7 +53,7 @@ static CclWs ccl_layout(void *base, const int64_t *dims) {
   w.counts = (int64_t *)p;
   p += align256(4 * sizeof(int64_t));
   w.sums = (int64_t *)p;
-  p += align256(sizeof(int64_t) * scan_chunks(nvox > w.words ? nvox : w.words));
+  p += align256(onepass_bytes<int64_t>(nvox > w.words ? nvox : w.words));
   w.word_prefix = (int32_t *)p;
   p += align256(sizeof(int32_t) * w.words);
   w.on_list = (int32_t *)p;
@@ -82,10 +82,11 @@ struct WordRank {
     if (w == words - 1 && (nvox & 31)) v &= (1u << (nvox & 31)) - 1u;
     return v;
   }
-  __device__ int64_t value(int64_t w) const { return __popc(word(w)); }
-  __device__ void emit(int64_t w, int64_t prefix, int64_t) const {
+  typedef uint32_t Item;
+  __device__ uint32_t load(int64_t w) const { return word(w); }
+  __device__ int64_t value(uint32_t v) const { return __popc(v); }
+  __device__ void emit(int64_t w, int64_t prefix, uint32_t v) const {
     word_prefix[w] = (int32_t)prefix;
-    uint32_t v = word(w);
     int32_t r = (int32_t)prefix;
     while (v) {
       int b = __ffs(v) - 1;
@@ -158,21 +159,25 @@ __global__ void ccl_union_kernel(const uint32_t *__restrict__ occ, CclWs w, int6
   // one thread per (ON voxel, backward neighbour offset): the union work is
   // a few dependent finds per thread instead of 13 in a row (at C3 only
   // ~12k voxels are ON, so per-voxel threads left the GPU latency-bound)
+  // 32-bit index arithmetic: nvox < 2^31 (fvv_ccl26), so 13 * n_on < 2^35
+  // is the only wider quantity
   const int64_t n_on = __ldcg(w.counts);
+  const uint32_t ux = (uint32_t)nx, uy = (uint32_t)ny;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < 13 * n_on;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / 13;
     const int o = (int)(e - 13 * r);
-    const int64_t l = w.on_list[r];
-    const int64_t i = l % nx, j = (l / nx) % ny, k = l / (nx * ny);
+    const uint32_t l = (uint32_t)w.on_list[r];
+    const uint32_t q = l / ux, k = q / uy;
+    const int i = (int)(l - q * ux), j = (int)(q - k * uy);
     // offsets with (dk, dj, di) lexicographically negative (hull.py:124-133)
     const int dk = o < 9 ? -1 : 0;
     const int rem = o < 9 ? o : o - 9;
     const int dj = rem / 3 - 1;
     const int di = rem % 3 - 1;
-    const int64_t ii = i + di, jj = j + dj, kk = k + dk;
+    const int ii = i + di, jj = j + dj, kk = (int)k + dk;
     if (ii < 0 || jj < 0 || kk < 0 || ii >= nx || jj >= ny || kk >= nz) continue;
-    const int64_t m = ii + nx * (jj + ny * kk);
+    const int64_t m = (int64_t)l + di + nx * (dj + ny * dk);
     if (!occ_bit(occ, m)) continue;
     uf_unite(w.parent, (int32_t)r, rank_of(occ, w.word_prefix, m));
   }
@@ -190,8 +195,10 @@ __global__ void ccl_flatten_kernel(CclWs w) {
 struct RootLabel {
   const int32_t *parent;
   int32_t *rank_label;
-  __device__ int64_t value(int64_t r) const { return parent[r] == (int32_t)r; }
-  __device__ void emit(int64_t r, int64_t prefix, int64_t v) const {
+  typedef int Item;
+  __device__ int load(int64_t r) const { return parent[r] == (int32_t)r; }
+  __device__ int64_t value(int v) const { return v; }
+  __device__ void emit(int64_t r, int64_t prefix, int v) const {
     if (v) rank_label[r] = (int32_t)(prefix + 1);
   }
 };
@@ -223,10 +230,11 @@ __global__ void ccl_stats_kernel(CclWs w, int64_t nx, int64_t ny) {
       const int32_t root = w.parent[r];
       lab = w.rank_label[root];
       if (root != (int32_t)r) w.rank_label[r] = lab;
-      const int64_t l = w.on_list[r];
-      i = (unsigned)(l % nx);
-      j = (unsigned)((l / nx) % ny);
-      k = (unsigned)(l / (nx * ny));
+      const uint32_t l = (uint32_t)w.on_list[r];
+      const uint32_t q = l / (uint32_t)nx;
+      k = q / (uint32_t)ny;
+      i = l - q * (uint32_t)nx;
+      j = q - k * (uint32_t)ny;
     }
     const unsigned grp = __match_any_sync(0xffffffffu, act ? lab : -1);
     const unsigned mn_i = __reduce_min_sync(grp, i), mx_i = __reduce_max_sync(grp, i);
@@ -334,11 +342,11 @@ int fvv_ccl26(const uint32_t *occ_dev, const fvv_grid *grid, void *ws_dev, size_
   CclWs w = ccl_layout(ws_dev, grid->dims);
   cudaMemsetAsync(w.counts, 0, 4 * sizeof(int64_t), st);
   WordRank wr{occ_dev, w.word_prefix, w.on_list, w.parent, w.words, nvox};
-  ordered_scan(wr, nullptr, w.words, w.sums, w.counts + 0, st);
+  onepass_scan(wr, nullptr, w.words, w.words, (void *)w.sums, w.counts + 0, st);
   ccl_union_kernel<<<kCclGrid, 256, 0, st>>>(occ_dev, w, nx, ny, nz);
   ccl_flatten_kernel<<<kCclGrid, 256, 0, st>>>(w);
   RootLabel rl{w.parent, w.rank_label};
-  ordered_scan(rl, w.counts + 0, 0, w.sums, w.counts + 1, st);
+  onepass_scan(rl, w.counts + 0, 0, nvox, (void *)w.sums, w.counts + 1, st);
   ccl_stats_init_kernel<<<kCclGrid, 256, 0, st>>>(w);
   ccl_stats_kernel<<<kCclGrid, 256, 0, st>>>(w, nx, ny);
   if (comps_dev) ccl_export_kernel<<<kCclGrid, 256, 0, st>>>(w, comps_dev, comp_cap);

@@ -11,7 +11,7 @@ for f in range(4):
     host.append((masks.cpu().pin_memory(), {c.id: t for c, t in zip(cams, frames.cpu().pin_memory())}))
 def d2h(bundle, img):
     m = bundle.merged_mesh
-    return m.vertices.nbytes + m.triangles.nbytes + m.object_ids.nbytes + img.color.nbytes + img.source.nbytes
+    return m.vertices.shape[0] + m.triangles.shape[0] + img.color.shape[0]  # as bench.py
 def run(n):
     fr = [host[i % 4][1] for i in range(n)]; ms = [host[i % 4][0] for i in range(n)]
     tot = 0
@@ -21,4 +21,4 @@ def run(n):
 run(12); torch.cuda.synchronize(); gc.collect(); gc.disable()
 t = time.perf_counter(); run(60); torch.cuda.synchronize(); print("e2e ms/frame", (time.perf_counter() - t) / 60 * 1e3)
 pr = cProfile.Profile(); pr.enable(); run(60); torch.cuda.synchronize(); pr.disable()
-pstats.Stats(pr).sort_stats("tottime").print_stats(18)
+pstats.Stats(pr).sort_stats("tottime").print_stats(30)
