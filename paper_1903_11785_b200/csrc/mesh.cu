@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(128)
   }
 }
 
-__global__ void __launch_bounds__(128)
+// ---- B1: isovalues + vertices (mesh.py:231-272, 332-337) --------------------
 __global__ void __launch_bounds__(128)
     mesh_lambda_kernel(const __grid_constant__ MeshGrids G, const __grid_constant__ MeshCams C,
                        MeshBufs B, const uint32_t *__restrict__ sil) {
