@@ -57,6 +57,42 @@ __device__ __forceinline__ bool project_exact(const fvv_camera &c, double x, dou
          (iv <= (double)(c.height - 1));
 }
 
+// rint(u), rint(v) and the in-frustum flag of project_exact(use_dist=false)
+// without the two float64 divisions in the common case: X/sz and Y/sz are
+// replaced by products with a Newton-refined reciprocal (a few ulps off),
+// and the result is kept only when u and v are farther than a generous bound
+// (~1e-12 relative, vs ~1e-15 actual) from a rounding boundary, where it
+// cannot differ from the exact chain's rint. Otherwise (and for NaN) the
+// exact divisions run. Z is the exact camera-space depth either way.
+__device__ __forceinline__ bool project_rint(const fvv_camera &c, double x, double y, double z,
+                                             bool gemv, double &iu, double &iv, double &zc) {
+  double X, Y, Z;
+  world_to_cam(c, x, y, z, gemv, X, Y, Z);
+  zc = Z;
+  const double sz = (Z != 0.0) ? Z : 1.0;
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(sz));
+  r = fma(r, fma(-sz, r, 1.0), r);
+  r = fma(r, fma(-sz, r, 1.0), r);
+  const double xn = X * r, yn = Y * r;
+  const double s = xn + c.skew * yn;
+  double u = c.fx * s + c.cx;
+  double v = c.fy * yn + c.cy;
+  const double eu = 1e-12 * (fabs(c.fx) * (fabs(xn) + fabs(c.skew * yn)) + fabs(u) + fabs(c.cx) + 1.0);
+  const double ev = 1e-12 * (fabs(c.fy * yn) + fabs(v) + fabs(c.cy) + 1.0);
+  iu = rint(u);
+  iv = rint(v);
+  if (!(fabs(u - iu) < 0.5 - eu && fabs(v - iv) < 0.5 - ev)) {  // near a tie (or NaN): exact
+    const double xe = X / sz, ye = Y / sz;
+    u = c.fx * (xe + c.skew * ye) + c.cx;
+    v = c.fy * ye + c.cy;
+    iu = rint(u);
+    iv = rint(v);
+  }
+  return (Z > 0.0) && (iu >= 0.0) && (iu <= (double)(c.width - 1)) && (iv >= 0.0) &&
+         (iv <= (double)(c.height - 1));
+}
+
 // voxels.py:52-56 voxel centre.
 __device__ __forceinline__ void voxel_center(const fvv_grid &g, int64_t i, int64_t j, int64_t k,
                                              double &x, double &y, double &z) {

@@ -460,9 +460,9 @@ __global__ void classify_kernel(const __grid_constant__ RasterCams C, ClassifyAr
       bool vis = false;
       if (t < nt) {
         const fvv_camera &cam = C.cams[c];
-        double u, v, z;
-        if (project_exact(cam, mx, my, mz, false, gemv, u, v, z)) {
-          const int64_t p = (int64_t)rint(v) * cam.width + (int64_t)rint(u);
+        double iu, iv, z;
+        if (project_rint(cam, mx, my, mz, gemv, iu, iv, z)) {
+          const int64_t p = (int64_t)iv * cam.width + (int64_t)iu;
           vis = (z - __ldg(A.depth + C.depth_off[c] + p)) <= A.t_v;
         }
       }

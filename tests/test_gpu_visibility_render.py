@@ -76,6 +76,40 @@ def test_raster_random_meshes_vs_oracle(gpu, seed):
                           O.classify(verts, tris, cam, depth, 40.0))
 
 
+def test_classify_centroids_on_pixel_rounding_ties(gpu):
+    """Centroids projecting exactly onto (and a few ulps either side of) the
+    half-pixel rounding boundaries and the frustum edges: the visibility
+    kernel's reciprocal fast path must fall back to the exact divisions there
+    (np.rint ties to even)."""
+    from paper_1903_11785_b200.camera import CameraModel
+    from paper_1903_11785_b200.mesh import TriangleMesh
+    from paper_1903_11785_b200.visibility import classify_visibility
+
+    W, H = 64, 48
+    cam = CameraModel.from_dict(dict(id=0, image_size=[W, H], fx=1.0, fy=1.0, cx=0.0, cy=0.0,
+                                     skew=0.0, rotation=np.eye(3).tolist(),
+                                     translation=[0.0, 0.0, 0.0]))
+    rng = np.random.default_rng(11)
+    n = 4000
+    Z = rng.integers(500, 3000, n).astype(np.float64)
+    ku = rng.integers(-2, W + 1, n) + 0.5
+    kv = rng.integers(-2, H + 1, n) + 0.5
+    X, Y = ku * Z, kv * Z  # u = X / Z = ku exactly: a rounding tie
+    for arr in (X, Y):  # perturb some by a few ulps either way
+        steps = rng.integers(-3, 4, n)
+        for i in np.nonzero(steps)[0]:
+            for _ in range(abs(int(steps[i]))):
+                arr[i] = np.nextafter(arr[i], np.inf if steps[i] > 0 else -np.inf)
+    verts = np.repeat(np.stack([X, Y, Z], axis=1), 3, axis=0)  # centroid == the point
+    tris = np.arange(3 * n, dtype=np.int32).reshape(n, 3)
+    depth = rng.uniform(400, 3100, (H, W))
+    mesh = TriangleMesh(verts, tris)
+    got = classify_visibility(mesh, cam, depth, 25.0)
+    ref = O.classify(verts, tris, cam, depth, 25.0)
+    assert np.array_equal(got, ref)
+    assert 0 < ref.sum() < n
+
+
 @pytest.mark.parametrize("name", ["tiny_cli", "figures"])
 def test_run_frame_and_render_golden(gpu, name):
     """run_frame (pipeline.py:115-220) + render_view (render.py:64-113) on the
