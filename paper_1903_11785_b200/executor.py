@@ -261,13 +261,14 @@ _EXECUTORS = {}
 def executor_for(cfg, rig, slot: int = 0) -> FrameExecutor:
     """Executors are cached per (config, rig parameters, slot) so repeated
     run_frame / run_sequence calls reuse the device buffers; run_sequence
-    alternates slots 0 and 1 so one frame's D2H overlaps the next frame."""
+    gives each lane two slots, so one frame's D2H overlaps the lane's next
+    frame."""
     from dataclasses import astuple
 
     key = (astuple(cfg), cam_table(list(rig)).tobytes(), int(slot))
     ex = _EXECUTORS.get(key)
     if ex is None:
-        if len(_EXECUTORS) > 8:
+        if len(_EXECUTORS) >= 32:
             _EXECUTORS.clear()
         ex = FrameExecutor(cfg, rig)
         _EXECUTORS[key] = ex

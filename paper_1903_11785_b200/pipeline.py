@@ -610,7 +610,10 @@ def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
     copy.wait_stream(caller)
     for st in computes:
         st.wait_stream(caller)
-    exs = [executor_for(cfg, rig, k) for k in range(lanes)]
+    # two executors per lane, used alternately: a frame's results are read
+    # back from one while the lane's next frame runs in the other
+    exs = [(executor_for(cfg, rig, 2 * k), executor_for(cfg, rig, 2 * k + 1))
+           for k in range(lanes)]
     in_qs = [queue.Queue(maxsize=1) for _ in range(lanes)]
     out_qs = [queue.Queue() for _ in range(lanes)]
     stop = threading.Event()
@@ -618,8 +621,9 @@ def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
     _END = object()
 
     def worker(lane):
-        compute, ex, in_q, out_q = computes[lane], exs[lane], in_qs[lane], out_qs[lane]
-        slot_free = None  # readback event of this lane's previous frame
+        compute, in_q, out_q = computes[lane], in_qs[lane], out_qs[lane]
+        slot_free = [None, None]  # readback event of each executor's last frame
+        n_run = 0
         try:
             torch.cuda.set_device(dev_index)
             with torch.cuda.stream(compute):
@@ -629,8 +633,11 @@ def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
                         break
                     frames, d_masks, (fbuf, foff), ev, _keep = item
                     compute.wait_event(ev)
-                    if slot_free is not None:  # executor buffers still being read back
-                        compute.wait_event(slot_free)
+                    slot = n_run & 1
+                    n_run += 1
+                    ex = exs[lane][slot]
+                    if slot_free[slot] is not None:  # its buffers still being read back
+                        compute.wait_event(slot_free[slot])
                     if virtual is not None:
                         out = ex.run(d_masks, virtual, fbuf, foff, fallback_color)
                         if isinstance(fbuf, int):  # zero-copy: the bilinear taps crossed PCIe
@@ -638,10 +645,11 @@ def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
                                 H2D_BYTES["frames"] += 12 * int(out.stats_raw["sourced_px"])
                     else:
                         out = ex.run(d_masks)
-                    pinned, slot_free = out.to_host_async(cams, stream=readback, compact=True)
+                    pinned, done = out.to_host_async(cams, stream=readback, compact=True)
+                    slot_free[slot] = done
                     with counter_lock:
                         D2H_BYTES["results"] += pinned.nbytes
-                    out_q.put((frames, out, pinned, slot_free))
+                    out_q.put((frames, out, pinned, done))
         except BaseException as exc:  # noqa: BLE001  (re-raised on the caller's thread)
             out_q.put(exc)
             return
