@@ -80,7 +80,8 @@ class TriangleMesh:
     @classmethod
     def _trusted(cls, vertices, triangles, object_ids, dev=None):
         """Wrap kernel outputs without re-validating them (they come from
-        the mesh kernels, whose indices are in range by construction)."""
+        the mesh kernels, whose indices are in range by construction).
+        ``object_ids`` may be a callable producing them on first access."""
         m = cls.__new__(cls)
         m._v, m._t, m._o = vertices, triangles, object_ids
         m._nt = len(triangles)
@@ -110,7 +111,7 @@ class TriangleMesh:
     @vertices.setter
     def vertices(self, value):
         self._load()
-        self._set_host(value, self._t, self._o)
+        self._set_host(value, self._t, self.object_ids)
         self._dev = None
 
     @property
@@ -127,6 +128,8 @@ class TriangleMesh:
     @property
     def object_ids(self) -> np.ndarray:
         self._load()
+        if callable(self._o):  # _trusted with deferred ids
+            self._o = self._o()
         return self._o
 
     @object_ids.setter

@@ -337,8 +337,11 @@ def bundle_from_output(out, host, cfg, rig, frames, frame_id=0, keep_depths=Fals
         meshes.append(TriangleMesh._lazy(nt, load))
     info = out.info
     if len(info) == 0 or np.all((info[:, 1] == 0) | (info[:, 5] > 0)):
-        oids = np.repeat(out.component_ids.astype(np.int32), info[:, 5]) if len(info) else \
-            np.zeros(0, dtype=np.int32)
+        cids, counts = out.component_ids.astype(np.int32), info[:, 5].copy()
+
+        def oids(cids=cids, counts=counts):  # built on first access
+            return np.repeat(cids, counts) if len(counts) else np.zeros(0, dtype=np.int32)
+
         merged = TriangleMesh._trusted(verts if len(tris) else np.zeros((0, 3)), tris, oids)
     else:
         merged = TriangleMesh.concatenate(meshes)
