@@ -41,20 +41,31 @@ __device__ __forceinline__ bool top_left(double ax, double ay, double bx, double
 }
 
 // visibility.py:50: every vertex projected once per camera (zero distortion,
-// gemm order; gemv when the mesh has one vertex) -> (u, v, z, pad) records.
+// gemm order; gemv when the mesh has one vertex) -> (u, v, z, pad) records,
+// plus the float-rounded (u, v) the FP32 filter reads; NaN there when the
+// reference culls every triangle using the vertex (z <= NEAR_CLIP or NaN u/v).
+__device__ __forceinline__ void project_vertex(const RasterCams &C, const double *__restrict__ V,
+                                               int64_t nv, int64_t w, bool gemv,
+                                               double4 *__restrict__ proj,
+                                               float2 *__restrict__ q) {
+  const int c = (int)(w / nv);
+  const int64_t i = w - (int64_t)c * nv;
+  double u, v, z;
+  project_exact(C.cams[c], V[3 * i], V[3 * i + 1], V[3 * i + 2], false, gemv, u, v, z);
+  proj[w] = make_double4(u, v, z, 0.0);
+  q[w] = (z > kNearClip && !isnan(u) && !isnan(v)) ? make_float2((float)u, (float)v)
+                                                   : make_float2(__int_as_float(0x7fffffff),
+                                                                 __int_as_float(0x7fffffff));
+}
+
 __global__ void raster_vertex_kernel(const __grid_constant__ RasterCams C,
                                      const double *__restrict__ V, int64_t nv,
-                                     double4 *__restrict__ proj) {
+                                     double4 *__restrict__ proj, float2 *__restrict__ q) {
   const bool gemv = nv == 1;
   const int64_t total = nv * C.ncam;
   for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
-       w += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(w / nv);
-    const int64_t i = w - (int64_t)c * nv;
-    double u, v, z;
-    project_exact(C.cams[c], V[3 * i], V[3 * i + 1], V[3 * i + 2], false, gemv, u, v, z);
-    proj[w] = make_double4(u, v, z, 0.0);
-  }
+       w += (int64_t)gridDim.x * blockDim.x)
+    project_vertex(C, V, nv, w, gemv, proj, q);
 }
 
 __device__ __forceinline__ double dmin3(double a, double b, double c) {
@@ -117,37 +128,19 @@ __device__ __forceinline__ bool tri_depth(const TriSetup &s, int x, int y, doubl
   return d < INFINITY;  // only finite depths can beat the +inf background
 }
 
-// A pass-0 depth candidate kept for the id pass: plane index, triangle,
-// depth bits (the id pass then scans these instead of re-rasterising).
-struct Hit {
-  uint32_t idx, t;
-  unsigned long long bits;
-};
-
 __device__ __forceinline__ void pixel_update(int pass, double d, int64_t t,
-                                             unsigned long long *depth, unsigned *ids,
-                                             Hit *hits = nullptr,
-                                             unsigned long long *nhits = nullptr,
-                                             int64_t hit_cap = 0, int64_t idx = 0) {
+                                             unsigned long long *depth, unsigned *ids) {
   const unsigned long long bits = (unsigned long long)__double_as_longlong(d);
   if (pass == 0) {
     atomicMin(depth, bits);  // result unused -> RED.MIN (no round trip)
-    if (hits) {              // warp-aggregated append
-      const unsigned act = __activemask();
-      const int lane = threadIdx.x & 31, leader = __ffs(act) - 1;
-      unsigned long long base = 0;
-      if (lane == leader) base = atomicAdd(nhits, (unsigned long long)__popc(act));
-      base = __shfl_sync(act, base, leader);
-      const unsigned long long slot = base + __popc(act & ((1u << lane) - 1u));
-      if ((int64_t)slot < hit_cap) hits[slot] = Hit{(uint32_t)idx, (uint32_t)t, bits};
-    }
   } else if (bits == __ldcg(depth)) {
     atomicMin(ids, (unsigned)t);
   }
 }
 
 struct RasterArgs {
-  const double4 *P;  // [ncam][nv] projected vertices
+  const double4 *P;  // [ncam][nv] projected vertices (u, v, z, 0)
+  const float2 *Q;   // [ncam][nv] (u, v) rounded to float; NaN: the vertex culls its triangles
   const int32_t *T;
   int64_t nt;
   const int64_t *nt_dev;
@@ -157,10 +150,16 @@ struct RasterArgs {
   int64_t *queue;     // big (camera, triangle) entries
   int64_t *qcount;
   int64_t qcap;
+  // work lists of the FP32 filter: one pair list and one item list per
+  // filter warp (appends need no atomics); wl_items bounds the items one
+  // filter warp sees, so the item lists cannot overflow; a full pair list
+  // sets *overflow and the sweep kernel then redoes every item
+  int64_t nwl, wl_items, wl_pairs;
+  uint32_t *slow;     // items the FP32 filter leaves to the warp-sweep kernel
+  uint2 *pairs;       // (item, y << 16 | x): candidate pixels from the FP32 filter
+  int *wcount;        // [nwl][2]: pairs, items
+  int *overflow;
   int pass;
-  Hit *hits;          // id pass by hit list (nullptr: re-rasterise)
-  unsigned long long *nhits;
-  int64_t hit_cap;
 };
 
 // Triangle setup as kept in shared memory for the warp's pixel sweep.
@@ -243,29 +242,263 @@ __device__ __forceinline__ void smem_to_setup(const TriSmem &m, TriSetup &s) {
   s.tl0 = m.tl & 1; s.tl1 = (m.tl >> 1) & 1; s.tl2 = (m.tl >> 2) & 1;
 }
 
-// Warp-cooperative small-triangle raster: the 32 lanes set up 32 (camera,
-// triangle) items, publish them in shared memory, then sweep the union of
-// their bounding-box pixels 32 at a time (each lane finds its pixel's owner
-// by a shuffle binary search over the warp's inclusive pixel-count scan), so
-// uneven bounding boxes and culled triangles do not leave lanes idle.
+// ---- FP32 filter: which (camera, triangle) items can cover which pixels ----
+//
+// At C3 the projected triangles are ~1 px: 10.4 M (camera, triangle) items
+// per frame cover 2.5 M pixels, and three quarters of the items cover none.
+// raster_filter_kernel decides each item from the float-rounded vertices
+// (Q, rounded from the exact float64 projections) with certified margins and
+// emits (item, pixel) pairs for the pixels that may be inside; the float64
+// test of the reference then runs only on those (raster_pair_kernel).
+// Items it cannot decide go to the warp-sweep kernel, unchanged semantics.
+//
+// Certification (vertices u_j exact float64, U_j = float(u_j)):
+//  * |U_j - u_j| <= 2^-24 max|U|, and the local coordinates X_j = U_j - ox
+//    (ox = floor of the float min, |X_j| <= 65) add <= 2^-24 * 65; dd =
+//    2^-22 (max|U| + 128) bounds the sum twice over.
+//  * a pixel centre farther than mt = 2 dd + 2^-12 outside the float extent
+//    [min U, max U] lies >= 2^-12 outside the exact extent [min u, max u].
+//    With exact |area| >= A = 2^-6 and an extent <= 64 px, its barycentric
+//    coordinates give some edge function w <= -2^-12 A / 128 = -2^-25 in
+//    exact arithmetic, while the float64 evaluation of w in the reference
+//    (visibility.py:67-78, |terms| <= 65 * 64) errs by < 2^-36: the reference
+//    rejects the pixel. Pixels outside the tight integer range are skipped.
+//  * inside the range, a pixel is dropped when some float edge function is
+//    below -m, m twice the bound of the float error plus the effect of the
+//    vertex perturbation dd: its exact w is < -m/2 < 0 and the float64
+//    rounding (< 2^-36) cannot lift it to >= 0.
+//  * the orientation (the reference's v1 <-> v2 swap) is taken from the float
+//    area only when |area32| exceeds its error bound by A (then the exact and
+//    the float64 area have the same sign and |area| >= A); otherwise, or with
+//    a tight range of more than kMaxTight pixels or an extent above 60 px, the
+//    item goes to the warp-sweep kernel.
+// Every emitted pixel is re-tested in float64 exactly as the reference does,
+// so the filter decides how much work runs, never a result.
+constexpr int kMaxTight = 16;
+
+__device__ __forceinline__ float2 ldq(const float2 *__restrict__ q) { return __ldg(q); }
+
+__global__ void __launch_bounds__(256)
+    raster_filter_kernel(const __grid_constant__ RasterCams C, RasterArgs A) {
+  const int64_t nt = device_count(A.nt_dev, A.nt);
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  uint2 *pl = A.pairs + wid * A.wl_pairs;
+  uint32_t *sl = A.slow + wid * A.wl_items;
+  int np = 0, ns = 0;  // this warp's list lengths
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // a thread takes one triangle through every camera: its vertex indices are
+  // read once and the next camera's vertices are fetched while this one runs
+  for (int64_t t0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; t0 < nt;
+       t0 += stride) {
+    const int64_t t = t0 + lane;
+    const bool valid = t < nt;
+    const float2 *q0 = A.Q, *q1 = A.Q, *q2 = A.Q;  // this triangle's vertices, camera c
+    float2 n0 = make_float2(0.f, 0.f), n1 = n0, n2 = n0;
+    if (valid) {
+      q0 += __ldg(A.T + 3 * t);
+      q1 += __ldg(A.T + 3 * t + 1);
+      q2 += __ldg(A.T + 3 * t + 2);
+      n0 = ldq(q0);
+      n1 = ldq(q1);
+      n2 = ldq(q2);
+    }
+    for (int c = 0; c < C.ncam; ++c) {
+    const float2 p0 = n0, p1 = n1, p2 = n2;
+    q0 += A.nv;
+    q1 += A.nv;
+    q2 += A.nv;
+    if (valid && c + 1 < C.ncam) {
+      n0 = ldq(q0);
+      n1 = ldq(q1);
+      n2 = ldq(q2);
+    }
+    const int W = C.cams[c].width, H = C.cams[c].height;
+    const uint32_t w = (uint32_t)(c * nt + t);  // camera-major item index
+    int state = 0;          // 0 nothing, 1 pixels in `bits`, 2 slow path
+    unsigned bits = 0;      // candidate pixels of the tight range, row-major
+    int gx0 = 0, gy0 = 0, rw = 1;
+    if (valid) {
+      const bool culled = isnan(p0.x) | isnan(p1.x) | isnan(p2.x);  // near clip / NaN vertex
+      const float mnx = fminf(fminf(p0.x, p1.x), p2.x), mxx = fmaxf(fmaxf(p0.x, p1.x), p2.x);
+      const float mny = fminf(fminf(p0.y, p1.y), p2.y), mxy = fmaxf(fmaxf(p0.y, p1.y), p2.y);
+      const float mx = fmaxf(fmaxf(fabsf(mnx), fabsf(mxx)), fmaxf(fabsf(mny), fabsf(mxy)));
+      const float ext = fmaxf(mxx - mnx, mxy - mny);
+      if (culled) {
+        state = 0;
+      } else if (!(mx <= 1048576.0f) || !(ext <= 60.0f)) {
+        state = 2;  // inf / huge coordinates, or a large triangle
+      } else {
+        const float dd = 0x1p-22f * (mx + 128.0f);
+        const float ox = floorf(mnx), oy = floorf(mny);
+        const float X0 = p0.x - ox, Y0 = p0.y - oy, X1 = p1.x - ox, Y1 = p1.y - oy,
+                    X2 = p2.x - ox, Y2 = p2.y - oy;
+        const float area = (X1 - X0) * (Y2 - Y0) - (Y1 - Y0) * (X2 - X0);
+        // |X1-X0| + |Y2-Y0| + |Y1-Y0| + |X2-X0| <= 4 ext, |q1| + |q2| <= 2 ext^2
+        const float aerr = 2.0f * (8.0f * dd * ext + 4.0f * dd * dd + 0x1p-20f * ext * ext);
+        const float mt = 2.0f * dd + 0x1p-12f;
+        // pixel range: the tight integer range of the extent when |area| >= A
+        // is certain, else the whole (widened) bounding box
+        const bool tight = fabsf(area) > aerr + 0x1p-6f;
+        const float lx = mnx - mt, hx = mxx + mt, ly = mny - mt, hy = mxy + mt;
+        const int tx0 = max((int)(tight ? ceilf(lx) : floorf(lx)), 0);
+        const int tx1 = min((int)(tight ? floorf(hx) : ceilf(hx)), W - 1);
+        const int ty0 = max((int)(tight ? ceilf(ly) : floorf(ly)), 0);
+        const int ty1 = min((int)(tight ? floorf(hy) : ceilf(hy)), H - 1);
+        rw = tx1 - tx0 + 1;
+        const int rh = ty1 - ty0 + 1;
+        if (rw > 0 && rh > 0) {
+          if (rw > 2 || rh > 2 || !(fabsf(area) > aerr)) {
+            state = 2;  // (4 % of the C3 items) the warp-sweep kernel takes it
+          } else {
+            // edge functions in the reference's vertex order (tri_depth); the
+            // v1 <-> v2 swap of visibility.py:63-66 negates all three, so with
+            // the sign s of the (certain) orientation a pixel is kept iff
+            // min(s w) >= -m. One margin for the three edges (|a| + |b| <=
+            // 2 ext, |g - X| <= ext + 2, a few more roundings for the 2 x 2
+            // block stepped from its corner). Branch-free over the block; bit
+            // yy * rw + xx for the pixels inside the range.
+            const float s = area > 0.0f ? 1.0f : -1.0f;
+            const float a0 = s * (X2 - X1), b0 = s * (Y2 - Y1), a1 = s * (X0 - X2),
+                        b1 = s * (Y0 - Y2), a2 = s * (X1 - X0), b2 = s * (Y1 - Y0);
+            const float m = -2.0f * (dd * (6.0f * ext + 9.0f) +
+                                     0x1p-20f * (2.0f * ext * (ext + 2.0f) + 1.0f));
+            gx0 = tx0;
+            gy0 = ty0;
+            const float gx = (float)tx0 - ox, gy = (float)ty0 - oy;
+            const float r0 = a0 * (gy - Y1) - b0 * (gx - X1);
+            const float r1 = a1 * (gy - Y2) - b1 * (gx - X2);
+            const float r2 = a2 * (gy - Y0) - b2 * (gx - X0);
+#pragma unroll
+            for (int yy = 0; yy < 2; ++yy) {
+#pragma unroll
+              for (int xx = 0; xx < 2; ++xx) {
+                const float w0 = (yy ? r0 + a0 : r0) - (xx ? b0 : 0.0f);
+                const float w1 = (yy ? r1 + a1 : r1) - (xx ? b1 : 0.0f);
+                const float w2 = (yy ? r2 + a2 : r2) - (xx ? b2 : 0.0f);
+                if (fminf(fminf(w0, w1), w2) >= m && xx < rw && yy < rh)
+                  bits |= 1u << (yy * rw + xx);
+              }
+            }
+            state = bits ? 1 : 0;
+          }
+        }
+      }
+    }
+    // appends to this warp's own lists (no atomics): pixel pairs, then the
+    // items left to the sweep kernel
+    const int npx = __popc(bits);
+    int incl = npx;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int sum = __shfl_sync(0xffffffffu, incl, 31);
+    if (sum) {
+      if (np + sum > A.wl_pairs) {
+        if (lane == 0) atomicOr(A.overflow, 1);  // the sweep kernel redoes every item
+      } else {
+        if (bits) {
+        uint2 *slot = pl + np + (incl - npx);
+        const int sh = rw == 2;  // k / rw for rw in {1, 2}
+        unsigned b = bits;
+        while (b) {
+          const int k = __ffs(b) - 1;
+          b &= b - 1;
+          const int qy = k >> sh;
+          *slot++ = make_uint2(w, ((uint32_t)(gy0 + qy) << 16) | (uint32_t)(gx0 + k - qy * rw));
+        }
+        }
+        np += sum;  // = entries written
+      }
+    }
+    const unsigned slow = __ballot_sync(0xffffffffu, state == 2);
+    if (state == 2) sl[ns + __popc(slow & ((1u << lane) - 1u))] = w;
+    ns += __popc(slow);
+    }
+  }
+  if (lane == 0) {
+    A.wcount[2 * wid] = np;
+    A.wcount[2 * wid + 1] = ns;
+  }
+}
+
+// The float64 test of one emitted (item, pixel) pair, exactly as the
+// reference evaluates that pixel for that triangle (visibility.py:48-91):
+// the same setup, the pixel must lie in the clamped bounding box, then the
+// inside test with top-left ties and the perspective-correct depth. One
+// warp per filter-warp list.
+__global__ void __launch_bounds__(256)
+    raster_pair_kernel(const __grid_constant__ RasterCams C, RasterArgs A) {
+  const int64_t nt = device_count(A.nt_dev, A.nt);
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t wl = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); wl < A.nwl;
+       wl += nwarps) {
+    const int n = __ldcg(A.wcount + 2 * wl);
+    const uint2 *pl = A.pairs + wl * A.wl_pairs;
+    for (int i = lane; i < n; i += 32) {
+      const uint2 e = pl[i];
+      const int c = (int)(e.x / (uint32_t)nt);
+      const int64_t t = (int64_t)e.x - (int64_t)c * nt;
+      const int x = (int)(e.y & 0xffffu), y = (int)(e.y >> 16);
+      const int width = C.cams[c].width;
+      TriSetup s;
+      if (!tri_setup(width, C.cams[c].height, A.P + (int64_t)c * A.nv, A.T, t, s)) continue;
+      if (x < s.lox || x > s.hix || y < s.loy || y > s.hiy) continue;
+      double d;
+      if (!tri_depth(s, x, y, d)) continue;
+      const int64_t p = C.depth_off[c] + (int64_t)y * width + x;
+      pixel_update(A.pass, d, t, (unsigned long long *)A.depth + p,
+                   A.ids ? (unsigned *)A.ids + p : nullptr);
+    }
+  }
+}
+
+// Warp-cooperative small-triangle raster for the items the FP32 filter could
+// not decide (raster_filter_kernel: near-degenerate or large triangles,
+// coordinates beyond 2^20 px): the 32 lanes set up 32 (camera, triangle)
+// items, publish them in shared memory, then sweep the union of their
+// bounding-box pixels 32 at a time (each lane finds its pixel's owner by a
+// shuffle binary search over the warp's inclusive pixel-count scan), so uneven
+// bounding boxes and culled triangles do not leave lanes idle.
 __global__ void __launch_bounds__(kRasterThreads, 8)
     raster_small_kernel(const __grid_constant__ RasterCams C, RasterArgs A) {
-  if (A.pass == 1 && A.hits && (int64_t)__ldcg(A.nhits) <= A.hit_cap) return;  // list did it
   __shared__ TriSmem sm[kRasterThreads];
   const int lane = threadIdx.x & 31;
   TriSmem *wsm = sm + (threadIdx.x & ~31);
   const int64_t nt = device_count(A.nt_dev, A.nt);
-  const int64_t total = nt * C.ncam;
   const bool overflow = A.pass == 1 && __ldcg(A.qcount) > A.qcap;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; w0 < total;
-       w0 += stride) {
-    const int64_t w = w0 + lane;
+  // work: the filter warps' item lists, or (pair list overflow) every item
+  const bool all = __ldcg(A.overflow) != 0;
+  const int64_t total_all = nt * C.ncam;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  int64_t cur = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);  // list or chunk
+  int off = 0;
+  for (;;) {
+    bool valid;
+    uint32_t w;
+    if (all) {
+      if (cur * 32 >= total_all) break;
+      valid = cur * 32 + lane < total_all;
+      w = (uint32_t)(cur * 32 + lane);
+      cur += nw;
+    } else {
+      int n = 0;
+      while (cur < A.nwl && off >= (n = __ldcg(A.wcount + 2 * cur + 1))) {
+        cur += nw;
+        off = 0;
+      }
+      if (cur >= A.nwl) break;
+      valid = off + lane < n;
+      w = valid ? __ldcg(A.slow + cur * A.wl_items + off + lane) : 0u;
+      off += 32;
+    }
     int npx = 0;
-    if (w < total) {
-      // camera-major item index; 32-bit division when the item count allows
-      const int c = total < 0xffffffffll ? (int)((uint32_t)w / (uint32_t)nt) : (int)(w / nt);
-      const int64_t t = w - (int64_t)c * nt;
+    if (valid) {
+      const int c = (int)(w / (uint32_t)nt);  // camera-major item index
+      const int64_t t = (int64_t)w - (int64_t)c * nt;
       TriSetup s;
       if (tri_setup(C.cams[c].width, C.cams[c].height, A.P + (int64_t)c * A.nv, A.T, t, s)) {
         const int64_t n = (int64_t)(s.hix - s.lox + 1) * (s.hiy - s.loy + 1);
@@ -332,8 +565,7 @@ __global__ void __launch_bounds__(kRasterThreads, 8)
           unsigned long long *dp = (unsigned long long *)(A.depth + C.depth_off[m.cam]);
           unsigned *ip = (unsigned *)(A.ids ? A.ids + C.depth_off[m.cam] : nullptr);
           const int64_t pxl = (int64_t)y * W + x;
-          pixel_update(A.pass, d, m.t, dp + pxl, ip ? ip + pxl : nullptr, A.hits, A.nhits,
-                       A.hit_cap, C.depth_off[m.cam] + pxl);
+          pixel_update(A.pass, d, m.t, dp + pxl, ip ? ip + pxl : nullptr);
         }
       }
     }
@@ -343,7 +575,6 @@ __global__ void __launch_bounds__(kRasterThreads, 8)
 
 __global__ void __launch_bounds__(kBigThreads)
     raster_big_kernel(const __grid_constant__ RasterCams C, RasterArgs A) {
-  if (A.pass == 1 && A.hits && (int64_t)__ldcg(A.nhits) <= A.hit_cap) return;  // list did it
   const int64_t nt = device_count(A.nt_dev, A.nt);
   int64_t nq = __ldcg(A.qcount);
   if (nq > A.qcap) nq = A.qcap;
@@ -363,8 +594,7 @@ __global__ void __launch_bounds__(kBigThreads)
       double d;
       if (!tri_depth(s, x, y, d)) continue;
       const int64_t p = (int64_t)y * width + x;
-      pixel_update(A.pass, d, t, dp + p, ip ? ip + p : nullptr, A.hits, A.nhits, A.hit_cap,
-                   C.depth_off[c] + p);
+      pixel_update(A.pass, d, t, dp + p, ip ? ip + p : nullptr);
     }
   }
 }
@@ -385,8 +615,8 @@ __device__ __forceinline__ void fill_u64(unsigned long long *p, int64_t n, unsig
 // so the two overlap instead of running back to back.
 __global__ void raster_prep_kernel(const __grid_constant__ RasterCams C,
                                    const double *__restrict__ V, int64_t nv,
-                                   double4 *__restrict__ proj, unsigned long long *depth,
-                                   int64_t npx, int nb_fill) {
+                                   double4 *__restrict__ proj, float2 *__restrict__ q,
+                                   unsigned long long *depth, int64_t npx, int nb_fill) {
   if ((int)blockIdx.x < nb_fill) {
     fill_u64(depth, npx, 0x7ff0000000000000ull, blockIdx.x * (int64_t)blockDim.x + threadIdx.x,
              (int64_t)nb_fill * blockDim.x);
@@ -396,26 +626,8 @@ __global__ void raster_prep_kernel(const __grid_constant__ RasterCams C,
   const int64_t total = nv * C.ncam;
   const int64_t stride = (int64_t)(gridDim.x - nb_fill) * blockDim.x;
   for (int64_t w = (blockIdx.x - nb_fill) * (int64_t)blockDim.x + threadIdx.x; w < total;
-       w += stride) {
-    const int c = (int)(w / nv);
-    const int64_t i = w - (int64_t)c * nv;
-    double u, v, z;
-    project_exact(C.cams[c], V[3 * i], V[3 * i + 1], V[3 * i + 2], false, gemv, u, v, z);
-    proj[w] = make_double4(u, v, z, 0.0);
-  }
-}
-
-// The id pass from the hit list: the first (lowest) triangle id among the
-// candidates that reached the final depth (visibility.py:84-91, strict <).
-__global__ void raster_hits_kernel(RasterArgs A) {
-  const int64_t n = (int64_t)__ldcg(A.nhits);
-  if (n > A.hit_cap) return;  // overflowed: the pass-1 raster kernels run instead
-  const unsigned long long *depth = (const unsigned long long *)A.depth;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const Hit h = A.hits[i];
-    if (h.bits == __ldcg(depth + h.idx)) atomicMin((unsigned *)A.ids + h.idx, h.t);
-  }
+       w += stride)
+    project_vertex(C, V, nv, w, gemv, proj, q);
 }
 
 __global__ void fill_u64_kernel(unsigned long long *p, int64_t n, unsigned long long v) {
@@ -657,22 +869,47 @@ static int64_t raster_queue_cap(int64_t num_triangles, int ncam) {
   return cap > 0 ? cap : 1;
 }
 
-static size_t raster_proj_offset(int64_t num_triangles, int ncam) {
-  return (256 + 8 * (size_t)raster_queue_cap(num_triangles, ncam) + 255) & ~(size_t)255;
+static size_t align256(size_t n) { return (n + 255) & ~(size_t)255; }
+
+// The FP32 filter's launch shape and its per-warp list sizes.
+struct FilterShape {
+  int64_t bx, nwl, wl_items, wl_pairs;
+};
+
+static FilterShape filter_shape(int64_t num_triangles, int ncam) {
+  const int64_t nt = num_triangles > 0 ? num_triangles : 1;
+  FilterShape f;
+  f.bx = (nt + 255) / 256;
+  if (f.bx > 148 * 8) f.bx = 148 * 8;
+  f.nwl = f.bx * 8;  // 256-thread blocks
+  // a filter warp visits ceil(nt / stride) chunks of 32 triangles x ncam cameras
+  f.wl_items = (int64_t)ncam * 32 * ((nt + 256 * f.bx - 1) / (256 * f.bx));
+  f.wl_pairs = 2 * f.wl_items;
+  return f;
 }
 
-static int64_t raster_hit_cap(int64_t num_triangles, int ncam) {
-  int64_t cap = 4 * num_triangles * (int64_t)ncam;
-  if (cap > (4ll << 20)) cap = 4ll << 20;
-  return cap > 0 ? cap : 1;
+struct RasterLayout {
+  size_t counts, queue, proj, q, slow, pairs, total;
+};
+
+// [counters][per-warp list counts][big queue][projected vertices f64]
+// [projected vertices f32][sweep items][candidate pixel pairs]
+static RasterLayout raster_layout(int64_t num_vertices, int64_t num_triangles, int ncam) {
+  const size_t nvc = (size_t)(num_vertices > 0 ? num_vertices : 1) * (size_t)ncam;
+  const FilterShape f = filter_shape(num_triangles, ncam);
+  RasterLayout L;
+  L.counts = 256;
+  L.queue = align256(L.counts + 2 * 4 * (size_t)f.nwl);
+  L.proj = align256(L.queue + 8 * (size_t)raster_queue_cap(num_triangles, ncam));
+  L.q = align256(L.proj + sizeof(double4) * nvc);
+  L.slow = align256(L.q + sizeof(float2) * nvc);
+  L.pairs = align256(L.slow + 4 * (size_t)(f.nwl * f.wl_items));
+  L.total = L.pairs + sizeof(uint2) * (size_t)(f.nwl * f.wl_pairs);
+  return L;
 }
 
-// [counters][big queue][projected vertices][hit list]
 size_t fvv_raster_workspace_bytes(int64_t num_vertices, int64_t num_triangles, int ncam) {
-  return raster_proj_offset(num_triangles, ncam) +
-         ((sizeof(double4) * (size_t)(num_vertices > 0 ? num_vertices : 1) * (size_t)ncam + 255) &
-          ~(size_t)255) +
-         sizeof(Hit) * (size_t)raster_hit_cap(num_triangles, ncam);
+  return raster_layout(num_vertices, num_triangles, ncam).total;
 }
 
 int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int64_t nv,
@@ -682,6 +919,17 @@ int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int
   static thread_local RasterCams C;
   int rc = fill_cams(C, cams, ncam, plane_off);
   if (rc) return rc;
+  for (int c = 0; c < ncam; ++c) {
+    if (cams[c].width > 65535 || cams[c].height > 65535) {  // packed pixel pairs
+      set_error("fvv_rasterize: camera %d image %dx%d exceeds 65535", cams[c].id, cams[c].width,
+                cams[c].height);
+      return FVV_E_LIMIT;
+    }
+  }
+  if (nt > 0 && nt * (int64_t)ncam >= 0xffffffffll) {  // 32-bit item indices
+    set_error("fvv_rasterize: %lld triangles x %d cameras exceeds 2^32 - 1", (long long)nt, ncam);
+    return FVV_E_LIMIT;
+  }
   cudaStream_t st = (cudaStream_t)stream;
   // background: depth +inf, id -1 (visibility.py:44-45); one fill when the
   // planes are contiguous (the executor's layout), else one per camera
@@ -704,11 +952,12 @@ int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int
     if (tri_id_dev) cudaMemsetAsync(tri_id_dev + plane_off[c], 0xff, 4 * n, st);
   }
   if (nt <= 0) return cuda_check("fvv_rasterize");
-  if (ws_bytes < fvv_raster_workspace_bytes(nv, nt, ncam)) {
-    set_error("fvv_rasterize: workspace %zu < %zu bytes", ws_bytes,
-              fvv_raster_workspace_bytes(nv, nt, ncam));
+  const RasterLayout L = raster_layout(nv, nt, ncam);
+  if (ws_bytes < L.total) {
+    set_error("fvv_rasterize: workspace %zu < %zu bytes", ws_bytes, L.total);
     return FVV_E_ARG;
   }
+  char *ws = (char *)ws_dev;
   RasterArgs A;
   A.T = tris_dev;
   A.nt = nt;
@@ -716,20 +965,23 @@ int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int
   A.nv = nv;
   A.depth = depth_dev;
   A.ids = tri_id_dev;
-  A.qcount = (int64_t *)ws_dev;
-  A.queue = (int64_t *)((char *)ws_dev + 256);
+  A.qcount = (int64_t *)ws;
+  const FilterShape fs = filter_shape(nt, ncam);
+  A.overflow = (int *)(ws + 8);
+  A.wcount = (int *)(ws + L.counts);
+  A.nwl = fs.nwl;
+  A.wl_items = fs.wl_items;
+  A.wl_pairs = fs.wl_pairs;
+  A.queue = (int64_t *)(ws + L.queue);
   A.qcap = raster_queue_cap(nt, ncam);
-  double4 *proj = (double4 *)((char *)ws_dev + raster_proj_offset(nt, ncam));
-  A.P = proj;
-  A.nhits = (unsigned long long *)((char *)ws_dev + 8);
-  // the id pass scans the depth pass's candidates when plane indices fit 32 bits
-  const bool use_hits = tri_id_dev && total_px < (1ll << 32);
-  A.hits = use_hits ? (Hit *)((char *)proj + ((sizeof(double4) * (size_t)(nv > 0 ? nv : 1) *
-                                                   (size_t)ncam + 255) & ~(size_t)255))
-                    : nullptr;
-  A.hit_cap = raster_hit_cap(nt, ncam);
-  cudaMemsetAsync(A.qcount, 0, 16, st);  // big-queue and hit counters
+  A.P = (const double4 *)(ws + L.proj);
+  A.Q = (const float2 *)(ws + L.q);
+  A.slow = (uint32_t *)(ws + L.slow);
+  A.pairs = (uint2 *)(ws + L.pairs);
+  cudaMemsetAsync(ws, 0, 16, st);  // big-queue counter, overflow flag
   {
+    double4 *proj = (double4 *)(ws + L.proj);
+    float2 *q = (float2 *)(ws + L.q);
     int64_t blocks = (nv * ncam + 255) / 256;
     if (blocks > kRasterGrid) blocks = kRasterGrid;
     if (blocks < 1) blocks = 1;
@@ -738,23 +990,25 @@ int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int
       int64_t nb_fill = total_px / (256 * 64) + 1;
       if (nb_fill > 148 * 8) nb_fill = 148 * 8;
       raster_prep_kernel<<<(int)(blocks + nb_fill), 256, 0, st>>>(
-          C, verts_dev, nv, proj, (unsigned long long *)(depth_dev + plane_off[0]), total_px,
+          C, verts_dev, nv, proj, q, (unsigned long long *)(depth_dev + plane_off[0]), total_px,
           (int)nb_fill);
     } else {
-      raster_vertex_kernel<<<(int)blocks, 256, 0, st>>>(C, verts_dev, nv, proj);
+      raster_vertex_kernel<<<(int)blocks, 256, 0, st>>>(C, verts_dev, nv, proj, q);
     }
     note_launches(1);
   }
+  {
+    raster_filter_kernel<<<(unsigned)fs.bx, 256, 0, st>>>(C, A);
+    note_launches(1);
+  }
+  // pass 0: depth (RED.MIN of the depth bits); pass 1 (ids wanted): the
+  // lowest triangle id reaching the final depth, over the same work lists
   for (int pass = 0; pass < (tri_id_dev ? 2 : 1); ++pass) {
     A.pass = pass;
-    if (pass == 1 && use_hits) {
-      raster_hits_kernel<<<148 * 8, 256, 0, st>>>(A);
-      note_launches(1);
-    }
-    // (pass 1 with a complete hit list: both kernels return at once)
-    raster_small_kernel<<<148 * 64, kRasterThreads, 0, st>>>(C, A);  // measured best of 16..128
+    raster_pair_kernel<<<148 * 16, 256, 0, st>>>(C, A);
+    raster_small_kernel<<<148 * 16, kRasterThreads, 0, st>>>(C, A);
     raster_big_kernel<<<148 * 4, kBigThreads, 0, st>>>(C, A);
-    note_launches(2);
+    note_launches(3);
   }
   return cuda_check("fvv_rasterize");
 }

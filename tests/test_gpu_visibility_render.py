@@ -249,3 +249,42 @@ def test_run_sequence_matches_golden_frames(gpu):
                                   G.unpack(z["vis"][i], bundle.merged_mesh.num_triangles))
         assert np.array_equal(img.color, z["render_color"])
         assert np.array_equal(img.source, z["render_source"])
+
+
+@pytest.mark.parametrize("width", [96, 4000])
+def test_raster_fp32_filter_adversarial(gpu, width):
+    """The FP32 candidate filter (raster_filter_kernel) against the exact
+    float64 raster on tiny triangles built to sit on its decision boundaries:
+    vertices on a 1/4-pixel lattice (edges through pixel centres: w == 0 and
+    the top-left rule), slivers of near-zero area, vertices perturbed by a few
+    ulps, triangles just outside the float extent, far from the image origin
+    (4000 px wide: larger float rounding) and beyond the image border."""
+    from paper_1903_11785_b200.camera import CameraModel
+    from paper_1903_11785_b200.mesh import TriangleMesh
+    from paper_1903_11785_b200.visibility import rasterize
+
+    h = 48
+    # R = I, t = 0, fx = fy = 1024, Z = 1024: u = X + cx exactly
+    cam = CameraModel(0, width, h, 1024.0, 1024.0, 0.0, 0.0)
+    rng = np.random.default_rng(width)
+    n = 6000
+    c = np.stack([rng.uniform(-2, width + 1, n), rng.uniform(-2, h + 1, n)], 1)
+    uv = np.repeat(c[:, None, :], 3, axis=1)
+    kind = rng.integers(0, 4, n)
+    lat = np.round((uv + rng.uniform(-1.5, 1.5, (n, 3, 2))) * 4) / 4  # 1/4 px lattice
+    uv = np.where(kind[:, None, None] == 0, lat, uv + rng.uniform(-1.2, 1.2, (n, 3, 2)))
+    sl = kind == 1  # slivers: third vertex a hair off the first edge
+    t = rng.uniform(0, 1, sl.sum())[:, None]
+    uv[sl, 2] = uv[sl, 0] + t * (uv[sl, 1] - uv[sl, 0]) + rng.normal(0, 1e-4, (sl.sum(), 2))
+    ulp = kind == 2  # lattice vertices nudged by a few ulps
+    uv[ulp] = lat[ulp] + rng.integers(-3, 4, (ulp.sum(), 3, 2)) * np.spacing(lat[ulp] + 0.0)
+    z = 1024.0 + np.round(rng.uniform(0, 64, (n, 3)))
+    z[(kind == 0) | (kind == 2)] = 1024.0  # u = X exactly on the lattice
+    verts = np.concatenate([uv * (z[..., None] / 1024.0), z[..., None]], axis=2).reshape(-1, 3)
+    tris = np.arange(3 * n, dtype=np.int32).reshape(n, 3)
+    mesh = TriangleMesh(verts, tris)
+    res = rasterize(mesh, cam)
+    depth, tid = O.rasterize(verts, tris, cam)
+    assert np.isfinite(depth).sum() > 1000
+    assert np.array_equal(res.depth, depth)
+    assert np.array_equal(res.tri_id, tid)
