@@ -250,32 +250,32 @@ __device__ __forceinline__ void smem_to_setup(const TriSmem &m, TriSetup &s) {
 // (Q, rounded from the exact float64 projections) with certified margins and
 // emits (item, pixel) pairs for the pixels that may be inside; the float64
 // test of the reference then runs only on those (raster_pair_kernel).
-// Items it cannot decide go to the warp-sweep kernel, unchanged semantics.
+// Items it cannot decide go to the warp-sweep kernel (raster_small_kernel),
+// which rasterises them exactly as before.
 //
 // Certification (vertices u_j exact float64, U_j = float(u_j)):
 //  * |U_j - u_j| <= 2^-24 max|U|, and the local coordinates X_j = U_j - ox
 //    (ox = floor of the float min, |X_j| <= 65) add <= 2^-24 * 65; dd =
 //    2^-22 (max|U| + 128) bounds the sum twice over.
-//  * a pixel centre farther than mt = 2 dd + 2^-12 outside the float extent
-//    [min U, max U] lies >= 2^-12 outside the exact extent [min u, max u].
-//    With exact |area| >= A = 2^-6 and an extent <= 64 px, its barycentric
-//    coordinates give some edge function w <= -2^-12 A / 128 = -2^-25 in
-//    exact arithmetic, while the float64 evaluation of w in the reference
-//    (visibility.py:67-78, |terms| <= 65 * 64) errs by < 2^-36: the reference
-//    rejects the pixel. Pixels outside the tight integer range are skipped.
-//  * inside the range, a pixel is dropped when some float edge function is
-//    below -m, m twice the bound of the float error plus the effect of the
-//    vertex perturbation dd: its exact w is < -m/2 < 0 and the float64
-//    rounding (< 2^-36) cannot lift it to >= 0.
-//  * the orientation (the reference's v1 <-> v2 swap) is taken from the float
-//    area only when |area32| exceeds its error bound by A (then the exact and
-//    the float64 area have the same sign and |area| >= A); otherwise, or with
-//    a tight range of more than kMaxTight pixels or an extent above 60 px, the
-//    item goes to the warp-sweep kernel.
+//  * the float area's error is bounded by aerr; |area32| > aerr fixes the
+//    orientation (the reference's v1 <-> v2 swap, visibility.py:63-66, which
+//    negates the three edge functions). Uncertain orientation -> sweep kernel.
+//  * candidate pixels: the tight integer range of the float extent widened by
+//    mt = 2 dd + 2^-12 when |area32| > aerr + A (A = 2^-6), else the whole
+//    widened bounding box. A pixel centre outside the tight range lies >=
+//    2^-12 outside the exact extent; with exact |area| >= A and an extent
+//    <= 64 px its barycentric coordinates give some edge function
+//    w <= -2^-12 A / 128 = -2^-25 in exact arithmetic, while the float64
+//    evaluation of w in the reference (|terms| <= 65 * 64) errs by < 2^-36:
+//    the reference rejects the pixel.
+//  * a candidate is dropped when some float edge function (oriented) is below
+//    -m, m twice the bound of the float rounding plus the effect of the vertex
+//    perturbation dd: its exact w is < -m/2 < 0 and the float64 rounding
+//    (< 2^-36) cannot lift it to >= 0.
+//  * ranges larger than 2 x 2 pixels (4 % of the C3 items), extents above
+//    60 px and coordinates beyond 2^20 px go to the sweep kernel.
 // Every emitted pixel is re-tested in float64 exactly as the reference does,
 // so the filter decides how much work runs, never a result.
-constexpr int kMaxTight = 16;
-
 __device__ __forceinline__ float2 ldq(const float2 *__restrict__ q) { return __ldg(q); }
 
 __global__ void __launch_bounds__(256)
