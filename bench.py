@@ -289,12 +289,16 @@ def run_b200(args):
     value = total_frames / (ms / 1e3)
     value_single = total_frames / (ms_single / 1e3)
 
-    # ---- roofline of the dominant kernel ----
+    # ---- roofline of the dominant kernel: the
+    # carve kernel (B-1 + B-3) has the largest GPU time per frame in the ncu
+    # launch list (profiles/); north_star asks for it against the FFMA roofline
     hbm_peak, peak_src, _ = peaks()
     H, W = cams[0].image_height, cams[0].image_width
-    top = max(stage_ms, key=stage_ms.get)
-    roof = roofline_for(top, stage_ms[top], work, ncam, H, W, hbm_peak, peak_src)
     roof_stages = stage_rooflines(stage_ms, work, ncam, H, W, hbm_peak, peak_src)
+    roof = carve_roofline(stage_ms, work, ncam)
+    for st_name in ("depth_images", "polygonize", "visibility", "render"):
+        roof_stages[st_name] = roofline_for(st_name, stage_ms[st_name], work, ncam, H, W,
+                                            hbm_peak, peak_src)
 
     # ---- e2e through the public API from pinned host memory ----
     e2e = None
@@ -452,6 +456,51 @@ def roofline_for(stage, ms, work, ncam, H, W, hbm_peak, peak_src):
             "frac": round(achieved / hbm_peak, 5), "traffic": traffic,
             "traffic_source": "profiles/traffic.json (ncu --set full, per frame)",
             "algorithmic_bytes": int(nbytes), "ms_per_launch": round(ms, 4)}
+
+
+def fp32_peak_tflops():
+    """148 SMs x 128 FP32 lanes x 2 FLOP x the max SM clock (MEASURED_PEAKS.json
+    has no FP32 figure; the clock is the driver-measured sm_max_mhz)."""
+    import torch
+
+    props = torch.cuda.get_device_properties(0)
+    sm_mhz = 1965.0
+    try:
+        with open(MEASURED_PEAKS) as fh:
+            sm_mhz = float(json.load(fh).get("sm_max_mhz", sm_mhz))
+    except Exception:  # noqa: BLE001
+        pass
+    basis = (f"derived: {props.multi_processor_count} SMs x 128 FP32 lanes x 2 FLOP x "
+             f"{sm_mhz:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json; it holds no FP32 figure)")
+    return props.multi_processor_count * FP32_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12, basis
+
+
+def carve_roofline(stage_ms, work, ncam):
+    """The carve kernel (B-1 stage grid + B-3 ROI grids, one launch each per
+    frame) against the FP32 FFMA roofline: algorithmic FLOP = every voxel x
+    every camera x 26 FLOP (BASELINE.md 2 / SURVEY.md 8d: 13 FMA-pipe ops per
+    voxel-projection), as hull.py:83-90 evaluates them; tile culling and the
+    early exit execute fewer, so the fraction is of the algorithmic work."""
+    nvox_c, nvox_f = work["last"]
+    proj = (nvox_c + nvox_f) * ncam
+    ms = stage_ms["sparse_carve"] + stage_ms["dense_carve"]
+    peak, basis = fp32_peak_tflops()
+    achieved = FLOP_PER_PROJECTION * proj / (ms / 1e3) / 1e12
+    traffic = None  # DRAM bytes per launch (profiles/traffic.json, ncu --set full)
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            traffic = json.load(fh).get("carve_kernel", {}).get("bytes_per_launch")
+    except Exception:  # noqa: BLE001
+        pass
+    return {"bound": "fp32", "kernel": "carve_kernel (B-1 stage grid + B-3 ROI grids)",
+            "stage": "sparse_carve + dense_carve", "achieved": round(achieved, 3),
+            "peak": round(peak, 2), "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+            "traffic": traffic,
+            "traffic_source": "profiles/traffic.json (ncu --set full, DRAM bytes per launch)",
+            "peak_source": basis, "launches_per_frame": 2,
+            "algorithmic_flop_per_launch": int(FLOP_PER_PROJECTION * proj / 2),
+            "voxel_projections_per_frame": int(proj), "ms_per_launch": round(ms / 2, 4),
+            "note": "tensor cores unused: no stage is a dense contraction (north_star)"}
 
 
 FP32_LANES_PER_SM = 128  # B200: 128 FP32 lanes per SM (BASELINE.md 2)
