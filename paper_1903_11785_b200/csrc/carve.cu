@@ -23,6 +23,7 @@ namespace fvv {
 constexpr int kCarveThreads = 256;
 constexpr int kCarveWordsPerBlock = 128;  // 4096 voxels per block
 constexpr int64_t kAmbCap = 1 << 20;     // deferred-voxel queue entries
+constexpr int64_t kTileCap = 1 << 19;    // split mode: surviving-tile records
 
 struct CarveParams {
   int ncam, ngrid, min_views, pad;
@@ -34,6 +35,10 @@ struct CarveParams {
   const struct CamAffine *affine;  // [ngrid][ncam] (carve_affine_kernel)
   unsigned long long *tile_stats;  // culled tiles, sum of fg cameras, sum of mixed cameras
   int tile_log2;                   // tile edge 1 << tile_log2 voxels
+  struct TileWork *tiles;          // split mode: surviving tiles (carve_voxels_kernel)
+  unsigned long long *ntiles;      //   and their count
+  int64_t tile_cap;
+  int parts;                       //   blocks per surviving tile
   uint32_t tiles_x[FVV_MAX_GRIDS], tiles_y[FVV_MAX_GRIDS];
   // 8x8-pixel cell maps per camera (carve_cells_kernel): bit = some / every
   // pixel of the cell is foreground; rows of cell_words[c] words
@@ -288,6 +293,57 @@ __device__ __forceinline__ void carve_affine(const CarveParams &p, CamAffine *ou
     cam_affine(p.cams[e % p.ncam], p.grids[e / p.ncam], out[e]);
 }
 
+struct __align__(16) TileWork {
+  int g, i0, j0, k0, n_fg, nm;
+  uint8_t mixed[FVV_MAX_CAMS];  // cameras whose silhouette boundary crosses the tile, test order
+  int pad[2];
+};
+
+// The voxels v0 .. v1 of a tile (v = di + kT (dj + kT dk)): the mixed
+// cameras per voxel in FP32 (float64 deferral via settle), ON bits set.
+// Returns this thread's ON count.
+__device__ __forceinline__ int carve_voxels(const CarveParams &p, const CamAffine *aff,
+                                            const fvv_grid &G, int g, int i0, int j0, int k0,
+                                            int i1, int j1, int k1, const int *mixed, int nm,
+                                            int n_fg, int v0, int v1) {
+  const int tl = p.tile_log2, kT = 1 << tl;
+  const int64_t nx = G.dims[0], ny = G.dims[1];
+  int my_on = 0;
+  for (int v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
+    const int i = i0 + (v & (kT - 1)), j = j0 + ((v >> tl) & (kT - 1)), k = k0 + (v >> (2 * tl));
+    if (i > i1 || j > j1 || k > k1) continue;
+    const float fi = (float)i, fj = (float)j, fk = (float)k;
+    int seen = n_fg;
+    bool off = false;
+    unsigned long long amb = 0;
+    for (int m = 0; m < nm; ++m) {
+      const int c = mixed[m];
+      int px, py;
+      const int st = classify32(aff[c], fi, fj, fk, px, py);
+      if (st == kOut) continue;
+      if (st == kAmb) {
+        amb |= 1ull << c;
+        continue;
+      }
+      ++seen;
+      if (!sil_bit(p.sil + p.sil_off[c], p.sil_stride[c], px, py)) {
+        off = true;
+        break;
+      }
+    }
+    const int64_t l = (int64_t)i + nx * ((int64_t)j + ny * (int64_t)k);
+    if (!off && settle(p, G, g, l, seen, amb)) {
+      atomicOr(p.occ + p.word_off[g] + (l >> 5), 1u << (l & 31));
+      ++my_on;
+    }
+  }
+  return my_on;
+}
+
+// One block per tile: classify the tile for every camera, then (fused mode)
+// carve its voxels, or (kSplit, the 16^3 stage-grid tiles) append the
+// surviving tile to p.tiles for carve_voxels_kernel.
+template <bool kSplit>
 __global__ void __launch_bounds__(kCarveThreads, 6)
     carve_kernel(const __grid_constant__ CarveParams p) {
   __shared__ CamAffine aff[FVV_MAX_CAMS];
@@ -352,42 +408,66 @@ __global__ void __launch_bounds__(kCarveThreads, 6)
     atomicAdd(p.tile_stats + 2, (unsigned long long)nm);
   }
   __syncthreads();
-  const int nm = n_mixed;
-  int my_on = 0;
-  const int64_t nvox = nx * ny * nz;
-  for (int v = threadIdx.x; v < (1 << (3 * tl)); v += blockDim.x) {
-    const int i = i0 + (v & (kT - 1)), j = j0 + ((v >> tl) & (kT - 1)), k = k0 + (v >> (2 * tl));
-    if (i > i1 || j > j1 || k > k1) continue;
-    const float fi = (float)i, fj = (float)j, fk = (float)k;
-    int seen = n_fg;
-    bool off = false;
-    unsigned long long amb = 0;
-    for (int m = 0; m < nm; ++m) {
-      const int c = mixed[m];
-      int px, py;
-      const int st = classify32(aff[c], fi, fj, fk, px, py);
-      if (st == kOut) continue;
-      if (st == kAmb) {
-        amb |= 1ull << c;
-        continue;
-      }
-      ++seen;
-      if (!sil_bit(p.sil + p.sil_off[c], p.sil_stride[c], px, py)) {
-        off = true;
-        break;
+  if (kSplit) {  // hand the tile to carve_voxels_kernel
+    if (threadIdx.x == 0) {
+      const unsigned long long slot = atomicAdd(p.ntiles, 1ull);
+      if ((int64_t)slot < p.tile_cap) {
+        TileWork &tw = p.tiles[slot];
+        tw.g = g;
+        tw.i0 = i0;
+        tw.j0 = j0;
+        tw.k0 = k0;
+        tw.n_fg = n_fg;
+        tw.nm = n_mixed;
+        for (int m = 0; m < n_mixed; ++m) tw.mixed[m] = (uint8_t)mixed[m];
       }
     }
-    const int64_t l = (int64_t)i + nx * ((int64_t)j + ny * (int64_t)k);
-    if (!off && settle(p, G, g, l, seen, amb)) {
-      atomicOr(p.occ + p.word_off[g] + (l >> 5), 1u << (l & 31));
-      ++my_on;
-    }
+    return;
   }
-  (void)nvox;
+  const int my_on = carve_voxels(p, aff, G, g, i0, j0, k0, i1, j1, k1, mixed, n_mixed, n_fg, 0,
+                                 1 << (3 * tl));
   if (p.count) {  // per-warp atomics: no block barrier at the end
-    my_on = __reduce_add_sync(0xffffffffu, my_on);
-    if (lane == 0 && my_on)
-      atomicAdd((unsigned long long *)&p.count[g], (unsigned long long)my_on);
+    const int s = __reduce_add_sync(0xffffffffu, my_on);
+    if (lane == 0 && s) atomicAdd((unsigned long long *)&p.count[g], (unsigned long long)s);
+  }
+}
+
+// Split mode, part 2: the voxels of the surviving tiles, p.parts (4) blocks
+// per 16^3 tile (1024 voxels each, four per thread): the latency-bound voxel
+// chains of a tile run on four SMs instead of one (B-1 120 -> 15 + 52 us per
+// C3 frame). Launched for every tile; blocks past the surviving count exit.
+__global__ void __launch_bounds__(kCarveThreads, 6)
+    carve_voxels_kernel(const __grid_constant__ CarveParams p) {
+  __shared__ CamAffine aff[FVV_MAX_CAMS];
+  __shared__ int mixed[FVV_MAX_CAMS];
+  int64_t n = (int64_t)__ldcg(p.ntiles);
+  if (n > p.tile_cap) n = p.tile_cap;
+  const int64_t w = blockIdx.x;
+  if (w >= n * p.parts) return;
+  const TileWork &tw = p.tiles[w / p.parts];
+  const int part = (int)(w % p.parts);
+  const int g = __ldcg(&tw.g), nm = __ldcg(&tw.nm), n_fg = __ldcg(&tw.n_fg);
+  const int i0 = __ldcg(&tw.i0), j0 = __ldcg(&tw.j0), k0 = __ldcg(&tw.k0);
+  {
+    const float4 *src = (const float4 *)(p.affine + (int64_t)g * p.ncam);
+    float4 *dst = (float4 *)aff;
+    for (int e = threadIdx.x; e < p.ncam * (int)(sizeof(CamAffine) / 16); e += blockDim.x)
+      dst[e] = __ldg(src + e);
+  }
+  for (int m = threadIdx.x; m < nm; m += blockDim.x) mixed[m] = __ldcg(&tw.mixed[m]);
+  __syncthreads();
+  const int tl = p.tile_log2, kT = 1 << tl;
+  const int per = (1 << (3 * tl)) / p.parts;
+  const fvv_grid &G = p.grids[g];
+  const int i1 = (int)min((int64_t)i0 + kT, G.dims[0]) - 1,
+            j1 = (int)min((int64_t)j0 + kT, G.dims[1]) - 1,
+            k1 = (int)min((int64_t)k0 + kT, G.dims[2]) - 1;
+  const int my_on = carve_voxels(p, aff, G, g, i0, j0, k0, i1, j1, k1, mixed, nm, n_fg,
+                                 part * per, (part + 1) * per);
+  if (p.count) {
+    const int s = __reduce_add_sync(0xffffffffu, my_on);
+    if ((threadIdx.x & 31) == 0 && s)
+      atomicAdd((unsigned long long *)&p.count[g], (unsigned long long)s);
   }
 }
 
@@ -458,7 +538,8 @@ static size_t cells_bytes(const fvv_camera *cams, int ncam) {
 extern "C" size_t fvv_carve_workspace_bytes(const fvv_camera *cams, int ncam) {
   if (!cams || ncam < 1 || ncam > FVV_MAX_CAMS) return 0;
   return affine_bytes() + 256 + cells_bytes(cams, ncam) +
-         sizeof(unsigned long long) * (1 + 2 * (size_t)kAmbCap);
+         sizeof(unsigned long long) * (1 + 2 * (size_t)kAmbCap) + 512 +
+         sizeof(TileWork) * (size_t)kTileCap;
 }
 
 extern "C" int fvv_carve(const fvv_camera *cams, int ncam, const uint32_t *sil_dev,
@@ -497,6 +578,9 @@ extern "C" int fvv_carve(const fvv_camera *cams, int ncam, const uint32_t *sil_d
   p.cell_any = (uint32_t *)(ws + affine_bytes() + 256);
   p.cell_all = p.cell_any + cell_words_total(cams, ncam);
   p.amb = (unsigned long long *)(ws + affine_bytes() + 256 + cells_bytes(cams, ncam));
+  p.ntiles = (unsigned long long *)(((uintptr_t)(p.amb + 1 + 2 * kAmbCap) + 255) & ~(uintptr_t)255);
+  p.tiles = (TileWork *)((char *)p.ntiles + 256);
+  p.tile_cap = kTileCap;
   {
     int64_t off = 0;
     for (int c = 0; c < ncam; ++c) {
@@ -560,8 +644,20 @@ extern "C" int fvv_carve(const fvv_camera *cams, int ncam, const uint32_t *sil_d
   const int nb_cells = (int)((cell_words_total(cams, ncam) + 255) / 256);
   carve_prep_kernel<<<nb_aff + nb_cells + 148 * 2, 256, 0, st>>>(p, (CamAffine *)workspace, nb_aff,
                                                                 nb_cells);
-  carve_kernel<<<(unsigned)blocks, kCarveThreads, 0, st>>>(p);
+  // large (stage) grids: classify the 16^3 tiles, then carve the surviving
+  // tiles' voxels with kParts blocks each; ROI grids: one kernel per 8^3 tile
+  // (measured for the ROI grids: split 8^3 tiles 89 + 105 us, split 16^3 tiles
+  // 18 + 155 us, fused 8^3 tiles 160 us per C3 frame)
+  p.parts = 4;
+  const bool split = p.tile_log2 == 4 && blocks <= kTileCap;
+  if (split) {
+    cudaMemsetAsync(p.ntiles, 0, sizeof(unsigned long long), st);
+    carve_kernel<true><<<(unsigned)blocks, kCarveThreads, 0, st>>>(p);
+    carve_voxels_kernel<<<(unsigned)(blocks * p.parts), kCarveThreads, 0, st>>>(p);
+  } else {
+    carve_kernel<false><<<(unsigned)blocks, kCarveThreads, 0, st>>>(p);
+  }
   carve_exact_kernel<<<148 * 4, kCarveThreads, 0, st>>>(p);
-  note_launches(3);
+  note_launches(split ? 4 : 3);
   return cuda_check("fvv_carve");
 }
