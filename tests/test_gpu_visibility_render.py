@@ -288,3 +288,27 @@ def test_raster_fp32_filter_adversarial(gpu, width):
     assert np.isfinite(depth).sum() > 1000
     assert np.array_equal(res.depth, depth)
     assert np.array_equal(res.tri_id, tid)
+
+
+def test_raster_pair_list_overflow_falls_back(gpu):
+    """Every item of a warp list emitting three candidate pixels (more than
+    the list's two per item) overflows the FP32 filter's pair lists: the
+    sweep kernel then rasterises every item, with identical results."""
+    from paper_1903_11785_b200.camera import CameraModel
+    from paper_1903_11785_b200.mesh import TriangleMesh
+    from paper_1903_11785_b200.visibility import rasterize
+
+    cam = CameraModel(0, 160, 120, 1024.0, 1024.0, 0.0, 0.0)
+    rng = np.random.default_rng(7)
+    n = 4000
+    base = np.stack([rng.integers(1, 150, n), rng.integers(1, 110, n)], 1) - 0.45
+    uv = np.stack([base, base + [1.9, 0.0], base + [0.0, 1.9]], 1)  # 3 of 4 centres inside
+    z = np.round(rng.uniform(1024.0, 1100.0, (n, 1)))  # ties between overlapping triangles
+    z = np.repeat(z, 3, axis=1)
+    verts = np.concatenate([uv * (z[..., None] / 1024.0), z[..., None]], axis=2).reshape(-1, 3)
+    tris = np.arange(3 * n, dtype=np.int32).reshape(n, 3)
+    res = rasterize(TriangleMesh(verts, tris), cam)
+    depth, tid = O.rasterize(verts, tris, cam)
+    assert np.isfinite(depth).sum() > 5000
+    assert np.array_equal(res.depth, depth)
+    assert np.array_equal(res.tri_id, tid)
