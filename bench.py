@@ -45,8 +45,8 @@ METRIC = "FVV frames/sec (carve+CCL+mesh+color) at 1/2/4/8 B200; Gvoxel-projecti
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=300,
-                    help="timed frames (default: the C3 sequence length, 300 frames)")
+    ap.add_argument("--steps", type=int, default=60,
+                    help="timed frames (the reference arm: one full CPU frame per step)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="C3")
