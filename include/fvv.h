@@ -196,8 +196,10 @@ int fvv_edge_isovalues(const fvv_camera *cams_by_id, int ncam, const uint32_t *s
 
 /* ---- D-1 / D-2: visibility.py:34-140 --------------------------------------- */
 
-/* Scratch for fvv_rasterize: projected vertices of every camera and the
- * queue of large-bbox triangles. */
+/* Scratch for fvv_rasterize: projected vertices of every camera (float64
+ * records + float-rounded (u, v) for the FP32 filter), the FP32 filter's
+ * per-warp (item, pixel) pair lists and sweep-item lists, and the queue of
+ * large-bbox triangles (~40 B per camera-vertex + 20 B per camera-triangle). */
 size_t fvv_raster_workspace_bytes(int64_t num_vertices, int64_t num_triangles, int ncam);
 
 /* visibility.py:34-98 rasterize for ncam cameras at once (zero-distortion
@@ -206,7 +208,8 @@ size_t fvv_raster_workspace_bytes(int64_t num_vertices, int64_t num_triangles, i
  * plane_off[c]; when tri_id_dev is non-NULL its int32 winning-triangle
  * plane (-1 background; lowest id on exact depth ties) is tri_id_dev +
  * plane_off[c]. The triangle count is *nt_dev when nt_dev is non-NULL
- * (nt is then an upper bound), else nt. */
+ * (nt is then an upper bound), else nt. Limits: nt * ncam < 2^32 - 1 and
+ * image sides <= 65535 (FVV_E_LIMIT otherwise). */
 int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int64_t nv,
                   const int32_t *tris_dev, int64_t nt, const int64_t *nt_dev, double *depth_dev,
                   const int64_t *plane_off, int32_t *tri_id_dev, void *ws_dev, size_t ws_bytes,
