@@ -24,6 +24,8 @@ constexpr int kCarveThreads = 256;
 constexpr int kCarveWordsPerBlock = 128;  // 4096 voxels per block
 constexpr int64_t kAmbCap = 1 << 20;     // deferred-voxel queue entries
 constexpr int64_t kTileCap = 1 << 19;    // split mode: surviving-tile records
+constexpr int64_t kVoxelGrid = 100000;   // split mode: one block per octant up to this
+constexpr int64_t kVoxelCap = 148 * 64;  //   else this many blocks loop over the octants
 
 struct CarveParams {
   int ncam, ngrid, min_views, pad;
@@ -436,6 +438,7 @@ __global__ void __launch_bounds__(kCarveThreads, 6)
 // whole tile only (a camera all-foreground over the tile is so over the
 // octant), which culls like 8^3 tiles do, then its 512 voxels are carved.
 // Launched for every tile; blocks past the surviving count exit.
+template <bool kLoop>
 __global__ void __launch_bounds__(kCarveThreads, 6)
     carve_voxels_kernel(const __grid_constant__ CarveParams p) {
   __shared__ CamAffine aff[FVV_MAX_CAMS];
@@ -443,15 +446,20 @@ __global__ void __launch_bounds__(kCarveThreads, 6)
   __shared__ int n_mixed, n_fg, culled;
   int64_t n = (int64_t)__ldcg(p.ntiles);
   if (n > p.tile_cap) n = p.tile_cap;
-  const int64_t w = blockIdx.x;
-  if (w >= n * 8) return;
+  // kLoop: a capped grid takes the octants in turn (many tiles, most culled:
+  // one block per octant would spend its time launching empty blocks)
+  for (int64_t w = blockIdx.x; w < n * 8; w += gridDim.x) {
+  if (kLoop) __syncthreads();  // the previous octant is done with the shared arrays
   const TileWork &tw = p.tiles[w >> 3];
   const int oct = (int)(w & 7);
   const int g = __ldcg(&tw.g), tnm = __ldcg(&tw.nm);
   const int i0 = __ldcg(&tw.i0) + 8 * (oct & 1), j0 = __ldcg(&tw.j0) + 8 * ((oct >> 1) & 1),
             k0 = __ldcg(&tw.k0) + 8 * (oct >> 2);
   const fvv_grid &G = p.grids[g];
-  if (i0 >= G.dims[0] || j0 >= G.dims[1] || k0 >= G.dims[2]) return;  // octant off the grid
+  if (i0 >= G.dims[0] || j0 >= G.dims[1] || k0 >= G.dims[2]) {  // octant off the grid
+    if (kLoop) continue;
+    return;
+  }
   const int i1 = (int)min((int64_t)i0 + 8, G.dims[0]) - 1,
             j1 = (int)min((int64_t)j0 + 8, G.dims[1]) - 1,
             k1 = (int)min((int64_t)k0 + 8, G.dims[2]) - 1;
@@ -477,7 +485,10 @@ __global__ void __launch_bounds__(kCarveThreads, 6)
     }
   }
   __syncthreads();
-  if (culled) return;
+  if (culled) {
+    if (kLoop) continue;
+    return;
+  }
   if (threadIdx.x == 0) {
     int nm = 0, nf = __ldcg(&tw.n_fg);
     for (int m = 0; m < tnm; ++m) {
@@ -493,6 +504,8 @@ __global__ void __launch_bounds__(kCarveThreads, 6)
   if (p.count) {
     const int s = __reduce_add_sync(0xffffffffu, my_on);
     if (lane == 0 && s) atomicAdd((unsigned long long *)&p.count[g], (unsigned long long)s);
+  }
+  if (!kLoop) return;
   }
 }
 
@@ -679,7 +692,12 @@ extern "C" int fvv_carve(const fvv_camera *cams, int ncam, const uint32_t *sil_d
   if (split) {
     cudaMemsetAsync(p.ntiles, 0, sizeof(unsigned long long), st);
     carve_kernel<true><<<(unsigned)blocks, kCarveThreads, 0, st>>>(p);
-    carve_voxels_kernel<<<(unsigned)(blocks * 8), kCarveThreads, 0, st>>>(p);
+    // one block per octant of every tile (C3 ROI batch: ~70k octants); more
+    // octants (C5 512^3: 131k, mostly of culled tiles): a capped grid loops
+    if (blocks * 8 <= kVoxelGrid)
+      carve_voxels_kernel<false><<<(unsigned)(blocks * 8), kCarveThreads, 0, st>>>(p);
+    else
+      carve_voxels_kernel<true><<<(unsigned)kVoxelCap, kCarveThreads, 0, st>>>(p);
   } else {
     carve_kernel<false><<<(unsigned)blocks, kCarveThreads, 0, st>>>(p);
   }
