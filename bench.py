@@ -497,7 +497,7 @@ def carve_roofline(stage_ms, work, ncam):
             "stage": "sparse_carve + dense_carve", "achieved": round(achieved, 3),
             "peak": round(peak, 2), "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
             "traffic": traffic,
-            "traffic_source": "profiles/traffic.json (ncu --set full, DRAM bytes per launch)",
+            "traffic_source": "profiles/traffic.json (ncu --set full, DRAM bytes per carve stage: prep + classification + octants + float64 queue)",
             "peak_source": basis, "launches_per_frame": 2,
             "algorithmic_flop_per_launch": int(FLOP_PER_PROJECTION * proj / 2),
             "voxel_projections_per_frame": int(proj), "ms_per_launch": round(ms / 2, 4),
