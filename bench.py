@@ -59,6 +59,35 @@ def parse():
     return ap.parse_args()
 
 
+def self_launch(args):
+    """``--gpus N`` without a torchrun environment: re-run this script as N
+    frame-sharded ranks (one process per GPU) under torch.distributed.run and
+    return its exit code; None when no launch is needed. Fails loudly when
+    fewer than N GPUs are visible or a torchrun world disagrees with N."""
+    if "WORLD_SIZE" in os.environ:
+        ws = int(os.environ["WORLD_SIZE"])
+        if ws != args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
+        return None
+    if args.gpus <= 1 or args.impl == "reference":
+        return None  # the reference arm runs on rank 0 only
+    import socket
+
+    import torch
+
+    visible = torch.cuda.device_count()
+    if visible < args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but only {visible} CUDA device(s) visible")
+    s_ = socket.socket()
+    s_.bind(("127.0.0.1", 0))
+    port = s_.getsockname()[1]
+    s_.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def dist_setup(args):
     import torch
 
@@ -197,8 +226,12 @@ def run_b200(args):
     stage_sum = {k: 0.0 for k in stage_names}
     work = {"proj": 0, "tris": 0, "frames": 0, "nv": 0}
 
+    nfr = len(dev_frames)
+
     def device_step(i, timed, lane_ex=None):
-        masks, fb, foff = dev_frames[i % len(dev_frames)]
+        # frame slot (i + i // lanes) mod F: lane k (steps k, k + lanes, ...)
+        # walks through every input frame instead of re-running one
+        masks, fb, foff = dev_frames[(i + i // lanes) % nfr]
         out = (lane_ex or ex).run(masks, virt, fb, foff)
         if timed:
             st = out.stats_raw
@@ -311,24 +344,48 @@ def run_b200(args):
             host.append((m_h, {c.id: f_h[k] for k, c in enumerate(cams)}))
 
         from paper_1903_11785_b200 import render as R
-        from paper_1903_11785_b200.pipeline import run_sequence
+        from paper_1903_11785_b200 import sharding as SH
+        from paper_1903_11785_b200.pipeline import run_sequence, run_sequence_sharded
 
         def consume(bundle, img):
             # what a viewer reads per frame: the merged mesh and the virtual view
-            m = bundle.merged_mesh
-            return m.vertices.shape[0] + m.triangles.shape[0] + img.color.shape[0]
+            n = 0
+            if bundle is not None:
+                m = bundle.merged_mesh
+                n += m.vertices.shape[0] + m.triangles.shape[0]
+            if img is not None:
+                n += img.color.shape[0]
+            return n
+
+        def sequence(nsteps):
+            """This rank's share of an nsteps x world frame sequence: frame f
+            on rank f mod N; at N > 1 every frame's mesh + visibility is
+            gathered to rank 0 over NCCL (run_sequence_sharded)."""
+            if world == 1:
+                fr = [host[(i + i // lanes) % len(host)][1] for i in range(nsteps)]
+                ms_ = [host[(i + i // lanes) % len(host)][0] for i in range(nsteps)]
+                for bundle, img in run_sequence(cfg, rig, fr, ms_, virt, lanes=lanes):
+                    yield bundle, img
+                return
+
+            def source(f):  # the j-th frame of this rank is global frame rank + j * N
+                j = f // world
+                m_h, fr_h = host[(j + j // lanes) % len(host)]
+                return fr_h, m_h
+
+            for _, bundle, img in run_sequence_sharded(cfg, rig, source, nsteps * world, virt,
+                                                       lanes=lanes):
+                yield bundle, img
 
         trace = os.environ.get("FVV_BENCH_TRACE")
 
         def run_e2e(nsteps):
-            fr = [host[i % len(host)][1] for i in range(nsteps)]
-            ms_ = [host[i % len(host)][0] for i in range(nsteps)]
             total = 0
             t_prev = time.perf_counter()
             gaps = []
             c_prev, m_prev = time.process_time(), time.thread_time()
             d2h0 = R.D2H_BYTES["results"]
-            for bundle, img in run_sequence(cfg, rig, fr, ms_, virt, lanes=lanes):
+            for bundle, img in sequence(nsteps):
                 consume(bundle, img)
                 t_now = time.perf_counter()
                 gaps.append(round((t_now - t_prev) * 1e3, 2))
@@ -352,6 +409,7 @@ def run_b200(args):
         torch.cuda.synchronize()
         barrier(world)
         R.H2D_BYTES["frames"] = 0
+        g0 = SH.GATHER_BYTES["payload"]
         gc.collect()
         gc.disable()
         t0 = time.perf_counter()
@@ -362,15 +420,23 @@ def run_b200(args):
         barrier(world)
         h2d = int(host[0][0].numel() + R.H2D_BYTES["frames"] / args.steps)
         e2e_ms = max_over_ranks((t1 - t0) * 1e3, world)
+        gathered = SH.GATHER_BYTES["payload"] - g0
         e2e = {"value": round(total_frames / (e2e_ms / 1e3), 3), "unit": "frames/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(d2h / args.steps),
+               "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": int((d2h + gathered) / args.steps),
                "ms_per_step": round(e2e_ms / args.steps, 3),
                "api": f"pipeline.run_sequence (run_frame + render_view per frame, {lanes} "
                       "executor lanes; silhouettes uploaded ahead on a copy stream, pinned "
                       "colour frames sampled in place (zero-copy: h2d counts the 12 B of "
                       "bilinear taps per sourced pixel), results read back on a readback "
                       "stream as one pinned block per frame (virtual view as colour + an "
-                      "int8 source/coverage code), pinned host inputs"}
+                      "int8 source/coverage code), pinned host inputs" +
+                      ("" if world == 1 else
+                       f"; frame-sharded over {world} ranks (run_sequence_sharded): every "
+                       "frame's mesh + visibility sent to rank 0 over NCCL and read back "
+                       "there (rank 0's d2h includes them), images read back per rank")}
+        if world > 1:
+            e2e["gather_bytes_rank0"] = int(gathered)
 
     # ---- CPU baseline: the oracle port on this box's host cores, rank 0, N=1 ----
     cpu = None
@@ -575,33 +641,35 @@ def cpu_baseline(wl, inp):
                       f"{dt:.2f} s"}
 
 
+def _maps_product_library():
+    try:
+        with open("/proc/self/maps") as fh:
+            return "libfvv.so" in fh.read()
+    except OSError:
+        return None
+
+
 def run_reference(args):
+    """The reference arm: the CPU oracle port of the reference pipeline
+    (oracle/, C + OpenMP on every host thread) over the same workload, metric
+    and frames as the GPU arm. Its inputs come from the HOST scene generator
+    (synthetic.render_scene: numpy ray casts), so nothing of the product
+    (libfvv.so, CUDA) is loaded on this path; the line records that."""
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
         return
-    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
 
     from paper_1903_11785_b200 import synthetic as S
     from paper_1903_11785_b200 import workloads
 
     wl = workloads.get(args.workload)
-    ids = list(range(max(1, min(args.frames, 2))))
-    inputs = []
-    for f in ids:
-        try:
-            import torch
-
-            if not torch.cuda.is_available():
-                raise RuntimeError
-            masks, frames = S.render_scene_device(wl.rig, wl.objects(f))
-            masks_np = [m.cpu().numpy().astype(bool) for m in masks]
-            fr = frames.cpu().numpy()
-            frames_np = {c.id: fr[k] for k, c in enumerate(wl.rig)}
-        except Exception:  # noqa: BLE001  (no GPU: generate on the host)
-            sils, frames_np = S.render_scene(wl.rig, wl.objects(f))
-            masks_np = sils
-        inputs.append((masks_np, frames_np))
+    ids = list(range(max(1, args.frames)))  # the frames the GPU arm cycles (rank 0, N = 1)
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=min(len(ids), os.cpu_count() or 1)) as pool:
+        inputs = list(pool.map(lambda f: S.render_scene(wl.rig, wl.objects(f)), ids))
+    t_gen = time.perf_counter() - t0
     for i in range(args.warmup):
         cpu_frame(wl, *inputs[i % len(inputs)])
     t0 = time.perf_counter()
@@ -613,19 +681,26 @@ def run_reference(args):
         "metric": METRIC, "value": round(value, 5), "unit": "frames/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 2),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (ellipsoid figures, BASELINE C3)", "impl": "reference",
-        "config": {"workload": f"{wl.name}: {wl.description}"},
+        "data": "synthetic (host ray-cast ellipsoid figures, BASELINE C3)", "impl": "reference",
+        "config": {"workload": f"{wl.name}: {wl.description}", "cameras": len(wl.rig),
+                   "frames_cycled": len(ids), "frame_ids": ids, "virtual_view": "1920x1080"},
         "cpu_baseline": {"value": round(value, 5), "unit": "frames/s", "cores": os.cpu_count(),
                          "kind": "port",
-                         "sample": "every step = 1 full frame (B-1..D-2 + 1080p colour pass) "
-                                   "through oracle/ (C restatement of the reference pipeline)"},
+                         "sample": f"every step = 1 full frame (B-1..D-2 + 1080p colour pass) "
+                                   f"through oracle/ (C restatement of the reference pipeline, "
+                                   f"OpenMP {os.cpu_count()} threads), frames {ids} cycled"},
         "e2e": {"value": round(value, 5), "unit": "frames/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "inputs": f"synthetic.render_scene on the host ({t_gen:.1f} s, outside the timed region)",
+        "product_library_loaded": _maps_product_library(),
     }))
 
 
 def main():
     args = parse()
+    rc = self_launch(args)
+    if rc is not None:
+        sys.exit(rc)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -353,7 +353,9 @@ int fvv_frame_readback(const fvv_frame *frame, void *host_dst, int flags, void *
 /* flags: bit 0 = depth planes; bit 1 = compact colour pass: slot 4 holds an
  * int8 code per virtual pixel (-2 uncovered, -1 fallback colour, else the
  * source camera's rig position) and slot 5 is empty, instead of int32
- * source ids + uint8 coverage (render.py:64-113's outputs follow from it). */
+ * source ids + uint8 coverage (render.py:64-113's outputs follow from it);
+ * bit 2 = image only: slots 0-2 (mesh, visibility) are empty, for a
+ * frame-sharded rank that sends those to rank 0 from device memory. */
 /* Per ROI: component id, box lo/hi (6 doubles), fine grid, mesh info
  * {vbase, V, sbase, S, tbase, T, fallback_edges, inconsistent_starts}. */
 int fvv_frame_get_rois(const fvv_frame *frame, int64_t *component_ids, double *boxes,

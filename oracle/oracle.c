@@ -8,8 +8,9 @@
  *     exactly like numpy's unfused ufuncs;
  *   - the one place the reference goes through BLAS (`pts @ R.T`,
  *     camera.py:177; `pc @ R`, camera.py:218) uses explicit fma() in the
- *     order OpenBLAS 0.3.30 evaluates it (re-verified
- *     by tests/test_oracle_vs_reference.py with OPENBLAS_CORETYPE=Haswell).
+ *     order OpenBLAS 0.3.30 evaluates it (pinned by
+ *     tests/test_oracle_golden.py against reference outputs generated with
+ *     OPENBLAS_CORETYPE=Haswell by scripts/make_golden.py).
  *
  * Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline leg may
  * load this library, and only as the checker / the timed CPU baseline.

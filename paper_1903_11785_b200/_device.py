@@ -94,6 +94,18 @@ def bool_to_bits(occ: np.ndarray, device) -> torch.Tensor:
     return torch.from_numpy(packed.view(np.int32)).to(device)
 
 
+def mask_bytes(t):
+    """Silhouette tensor -> one byte per pixel, nonzero = foreground (the
+    packing kernel's reading). bool/uint8/int8 are reinterpreted in place;
+    any other dtype is compared with zero, as np.asarray(sil, dtype=bool)
+    does in hull.py:68."""
+    if t.dtype == torch.bool or t.dtype == torch.int8:
+        return t.view(torch.uint8)
+    if t.dtype == torch.uint8:
+        return t
+    return (t != 0).to(torch.uint8)
+
+
 class DeviceSilhouettes:
     """Bit-packed silhouettes of a rig, resident on the GPU.
 
@@ -125,10 +137,7 @@ class DeviceSilhouettes:
                     raise ValueError(
                         f"camera {c.id}: silhouette shape {shape} != "
                         f"({c.image_height}, {c.image_width})")
-            masks = sils.reshape(-1)
-            if masks.dtype == torch.bool:
-                masks = masks.view(torch.uint8)
-            masks = masks.to(device, non_blocking=True)
+            masks = mask_bytes(sils.reshape(-1)).to(device, non_blocking=True)
         else:
             host = []
             for c, s in zip(cams, sils):

@@ -626,12 +626,14 @@ int fvv_frame_get_outputs(const fvv_frame *f, fvv_frame_outputs *o) {
 }
 
 // flags: bit 0 depth planes, bit 1 compact colour pass (colour + the int8
-// code plane instead of source + covered)
+// code plane instead of source + covered), bit 2 image only (no mesh or
+// visibility: a frame-sharded rank ships those to rank 0 over NCCL)
 static void readback_layout(const fvv_frame *f, int flags, int64_t *lay) {
   const bool compact = flags & 2;
-  const int64_t sz[7] = {24 * f->nv,
-                         12 * f->nt,
-                         4 * (int64_t)f->ncam * f->vis_stride,
+  const bool mesh = !(flags & 4);
+  const int64_t sz[7] = {mesh ? 24 * f->nv : 0,
+                         mesh ? 12 * f->nt : 0,
+                         mesh ? 4 * (int64_t)f->ncam * f->vis_stride : 0,
                          3 * f->virt_px,
                          (compact ? 1 : 4) * f->virt_px,
                          compact ? 0 : f->virt_px,

@@ -11,12 +11,13 @@ everything a SceneBundle needs back in one batch of pinned transfers.
 from __future__ import annotations
 
 import ctypes
+from collections import OrderedDict
 
 import numpy as np
 import torch
 
 from . import _lib
-from ._device import cam_table, require_cuda, stream_handle
+from ._device import cam_table, mask_bytes, require_cuda, stream_handle
 
 STAGE_NAMES = {1: "B-1 sparse carve", 2: "B-2 noise filter/ROI", 3: "B-3 dense carve",
                4: "C polygonize", 5: "D-1 depth images", 6: "D-2 visibility",
@@ -49,7 +50,8 @@ class FrameOutput:
     """Results of one executor run: host scalars, and device views (built on
     first access) that stay valid until the executor's next run."""
 
-    def __init__(self, stats, outs, rois, ncam, virtual, handle=None):
+    def __init__(self, stats, outs, rois, ncam, virtual, handle=None, owner=None):
+        self._owner = owner  # the FrameExecutor owning the device buffers: keep it alive
         self.stats_raw = stats
         self._outs = outs
         self._h = handle
@@ -95,7 +97,8 @@ class FrameOutput:
         total = sum(c.image_height * c.image_width for c in cams)
         return _dev(self.depth_ptr, (total,), "<f8")
 
-    def to_host_async(self, cams, keep_depths=False, stream=None, compact=False):
+    def to_host_async(self, cams, keep_depths=False, stream=None, compact=False,
+                      image_only=False):
         """Queue the D2H copy of vertices, triangles, visibility bits, the
         rendered image (and depth planes) into ONE pinned block on ``stream``
         (default: the current stream, after this frame's work) with one
@@ -108,14 +111,30 @@ class FrameOutput:
         lib = _lib.load()
         lay = np.zeros(16, dtype=np.int64)
         compact = bool(compact and self.virtual is not None)
-        flags = ctypes.c_int(int(bool(keep_depths)) | (2 if compact else 0))
+        flags = ctypes.c_int(int(bool(keep_depths)) | (2 if compact else 0) |
+                             (4 if image_only else 0))
         total = int(lib.fvv_frame_readback_layout(self._h, flags, _lib.host_ptr(lay)))
         buf = torch.empty(max(total, 1), dtype=torch.uint8, pin_memory=True)
         _lib.call("fvv_frame_readback", self._h, ctypes.c_void_p(buf.data_ptr()), flags,
                   ctypes.c_void_p(stream.cuda_stream))
         ev = torch.cuda.Event()
         ev.record(stream)
-        return HostBlock(self, buf, lay, keep_depths, compact), ev
+        return HostBlock(self, buf, lay, keep_depths, compact, image_only), ev
+
+    def export(self, device):
+        """(meta float64 array, device uint8 payload) of this frame's mesh
+        and visibility bits in the frame-export format (sharding.py), copied
+        on the current stream so the executor may run its next frame at once."""
+        from .sharding import export_meta, payload_layout
+
+        meta = export_meta(self.stats(), self.stats_raw["ms"][:6], self.component_ids,
+                           self.info, self.nv, self.nt, self.ncam, self.vis_stride)
+        offs, total = payload_layout(self.nv, self.nt, self.ncam, self.vis_stride)
+        payload = torch.empty(max(total, 1), dtype=torch.uint8, device=device)
+        for (off, n), src in zip(offs, (self.verts, self.tris, self.vis_bits)):
+            if n:
+                payload[off:off + n].copy_(src.reshape(-1).view(torch.uint8))
+        return meta, payload
 
     def to_host(self, cams, keep_depths=False):
         """Pinned D2H of every host-facing output, one synchronisation."""
@@ -127,11 +146,12 @@ class FrameOutput:
 class HostBlock:
     """One frame's outputs in a pinned host block (executor readback layout)."""
 
-    def __init__(self, out, buf, lay, keep_depths, compact=False):
+    def __init__(self, out, buf, lay, keep_depths, compact=False, image_only=False):
         self.buf, self.lay = buf, lay
         self.nbytes = int(sum(int(lay[8 + i]) for i in range(7)))  # bytes copied
-        self.shapes = {"verts": ((out.nv, 3), np.float64), "tris": ((out.nt, 3), np.int32),
-                       "vis": ((out.ncam, out.vis_stride), np.uint32)}
+        self.shapes = {} if image_only else {
+            "verts": ((out.nv, 3), np.float64), "tris": ((out.nt, 3), np.int32),
+            "vis": ((out.ncam, out.vis_stride), np.uint32)}
         if out.virtual is not None:
             h, w = out.virtual.image_height, out.virtual.image_width
             if compact:  # slot 4: int8 code plane (fvv_frame_readback flag bit 1)
@@ -216,9 +236,7 @@ class FrameExecutor:
         from .pipeline import StageError
         from .render import FALLBACK_COLOR
 
-        if masks.dtype == torch.bool:
-            masks = masks.view(torch.uint8)
-        masks = masks.reshape(-1)
+        masks = mask_bytes(masks).reshape(-1)
         stats = np.zeros(1, dtype=_lib.FRAME_STATS_DTYPE)
         stage = ctypes.c_int(0)
         if virtual is not None:
@@ -252,10 +270,11 @@ class FrameExecutor:
         _lib.load().fvv_frame_get_rois(self._h, _lib.host_ptr(cid), _lib.host_ptr(boxes),
                                        _lib.host_ptr(grids), _lib.host_ptr(info))
         return FrameOutput(stats[0], outs, (cid[:n], boxes[:n], grids[:n], info[:n]),
-                           self.ncam, virtual, self._h)
+                           self.ncam, virtual, self._h, owner=self)
 
 
-_EXECUTORS = {}
+_EXECUTORS = OrderedDict()
+_MAX_EXECUTORS = 32
 
 
 def executor_for(cfg, rig, slot: int = 0) -> FrameExecutor:
@@ -268,8 +287,12 @@ def executor_for(cfg, rig, slot: int = 0) -> FrameExecutor:
     key = (astuple(cfg), cam_table(list(rig)).tobytes(), int(slot))
     ex = _EXECUTORS.get(key)
     if ex is None:
-        if len(_EXECUTORS) >= 32:
-            _EXECUTORS.clear()
+        while len(_EXECUTORS) >= _MAX_EXECUTORS:
+            # least recently used first; a FrameOutput still holding the
+            # evicted executor keeps its buffers alive until it is dropped
+            _EXECUTORS.popitem(last=False)
         ex = FrameExecutor(cfg, rig)
         _EXECUTORS[key] = ex
+    else:
+        _EXECUTORS.move_to_end(key)
     return ex

@@ -26,7 +26,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._device import DeviceSilhouettes, require_cuda
+from ._device import DeviceSilhouettes, mask_bytes, require_cuda
 from .bundle import SceneBundle, StageTimings
 from .hull import NoiseFilterParams, Roi, carve_grids, finish_labels, label_grid_async
 from .mesh import TriangleMesh, polygonize_grids
@@ -285,7 +285,7 @@ def _masks_on_device(rig, sils):
     if isinstance(sils, torch.Tensor) and sils.dim() == 1:  # flat, rig order (internal)
         if sils.numel() != sum(c.image_height * c.image_width for c in cams):
             raise ValueError("flat silhouette buffer does not match the rig's image sizes")
-        return sils.to(dev, non_blocking=True)
+        return mask_bytes(sils).to(dev, non_blocking=True)
     if len(sils) != len(cams):
         raise ValueError(f"{len(sils)} silhouettes for {len(cams)} cameras")
     if isinstance(sils, torch.Tensor) and sils.dim() == 3:
@@ -294,8 +294,7 @@ def _masks_on_device(rig, sils):
             if shape != (c.image_height, c.image_width):
                 raise ValueError(f"camera {c.id}: silhouette shape {shape} != "
                                  f"({c.image_height}, {c.image_width})")
-        t = sils.view(torch.uint8) if sils.dtype == torch.bool else sils
-        return t.to(dev, non_blocking=True).reshape(-1)
+        return mask_bytes(sils).to(dev, non_blocking=True).reshape(-1)
     parts = []
     for c, s in zip(cams, sils):
         if isinstance(s, torch.Tensor):
@@ -593,6 +592,24 @@ def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
     that frame has been yielded (up to 2 x lanes frames are in flight).
     Yields (SceneBundle, RenderedImage or None) per frame, in input order,
     with the mesh, visibility flags and rendered image on the host."""
+    for _, bundle, img, _ in _run_local(cfg, rig, frames_seq, sils_seq, virtual,
+                                        fallback_color, _count_from(frame_id0), lanes):
+        yield bundle, img
+
+
+def _count_from(n):
+    while True:
+        yield n
+        n += 1
+
+
+def _run_local(cfg, rig, frames_seq, sils_seq, virtual, fallback_color, frame_ids, lanes,
+               export=False):
+    """run_sequence's engine. Yields (frame_id, SceneBundle or None, image or
+    None, export or None) in input order. With ``export`` (a frame-sharded
+    rank other than 0) the mesh and visibility bits are not read back:
+    each frame's are copied into one device payload (sharding.py format)
+    for the caller to send to rank 0, and the bundle is None."""
     import queue
     import threading
 
@@ -648,11 +665,18 @@ def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
                                 H2D_BYTES["frames"] += 12 * int(out.stats_raw["sourced_px"])
                     else:
                         out = ex.run(d_masks)
-                    pinned, done = out.to_host_async(cams, stream=readback, compact=True)
+                    exp = None
+                    if export:  # mesh + visibility leave through NCCL, not the host
+                        meta, payload = out.export(compute.device)
+                        pev = torch.cuda.Event()
+                        pev.record(compute)
+                        exp = (meta, payload, pev)
+                    pinned, done = out.to_host_async(cams, stream=readback, compact=True,
+                                                     image_only=export)
                     slot_free[slot] = done
                     with counter_lock:
                         D2H_BYTES["results"] += pinned.nbytes
-                    out_q.put((frames, out, pinned, done))
+                    out_q.put((frames, out, pinned, done, exp))
         except BaseException as exc:  # noqa: BLE001  (re-raised on the caller's thread)
             out_q.put(exc)
             return
@@ -663,15 +687,17 @@ def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
             raise item
         if item is _END:
             raise RuntimeError("run_sequence worker stopped early")
-        p_frames, p_out, p_pinned, p_ev = item
+        p_frames, p_out, p_pinned, p_ev, p_exp = item
         p_ev.synchronize()
         host = p_pinned.arrays()
-        bundle = bundle_from_output(p_out, host, cfg, rig, p_frames, fid, keep_device=False)
+        bundle = None if export else bundle_from_output(p_out, host, cfg, rig, p_frames, fid,
+                                                        keep_device=False)
         img = None
         if virtual is not None:
             img = CodedImage(host["color"], host["code"], rig_ids)
-        return bundle, img
+        return fid, bundle, img, p_exp
 
+    fids = iter(frame_ids)
     threads = [threading.Thread(target=worker, args=(k,), name=f"fvv-lane{k}", daemon=True)
                for k in range(lanes)]
 
@@ -704,12 +730,12 @@ def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
                         item = q.get_nowait()
                     except queue.Empty:
                         break
-                yield finish(item, frame_id0 + n_out)
+                yield finish(item, next(fids))
                 n_out += 1
         for k in range(lanes):
             submit(k, _END)
         while n_out < n_in:
-            yield finish(out_qs[n_out % lanes].get(), frame_id0 + n_out)
+            yield finish(out_qs[n_out % lanes].get(), next(fids))
             n_out += 1
     finally:
         stop.set()
@@ -722,6 +748,49 @@ def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
             th.join()
         for st in computes:
             caller.wait_stream(st)
+        # queued fvv_frame_readback copies write into torch-pinned blocks the
+        # host allocator does not track: finish them before the queue items
+        # (and with them the blocks) can be released and handed out again
+        readback.synchronize()
+        caller.wait_stream(readback)
+
+
+def run_sequence_sharded(cfg: PipelineConfig, rig, source, n_frames: int, virtual=None,
+                         fallback_color=None, lanes: int = 4, gather: bool = True, group=None):
+    """run_sequence over a frame-sharded job: one process per GPU
+    (torch.distributed initialised, NCCL), frame f on rank f mod N
+    (frames are independent, pipeline.py:115-220).
+
+    ``source(f) -> (frames, sils)`` loads frame f's inputs and is called only
+    for this rank's frames. With ``gather`` every rank but 0 ships each
+    finished frame's mesh and visibility bits to rank 0 straight from device
+    memory (NCCL point-to-point over NVLink; the small meta vector over
+    gloo) and reads back only its rendered view. Rank 0 yields
+    (frame_id, SceneBundle, image or None) for EVERY frame in order, images
+    for its own frames; the other ranks yield (frame_id, None, image) for
+    theirs. Without torch.distributed this is run_sequence over all frames."""
+    import itertools
+
+    import torch.distributed as dist
+
+    from .sharding import bundle_from_export, frame_gather, frames_for_rank, merge_sharded
+
+    if dist.is_available() and dist.is_initialized():
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+    else:
+        rank, world = 0, 1
+    mine = frames_for_rank(rank, world, n_frames)
+    a, b = itertools.tee(map(source, mine))
+    gatherer = frame_gather(group) if gather and world > 1 else None
+    local = _run_local(cfg, rig, (p[0] for p in a), (p[1] for p in b), virtual, fallback_color,
+                       iter(mine), lanes, export=gatherer is not None and rank != 0)
+
+    def to_bundle(fid, meta, payload, ev):
+        if ev is not None:
+            ev.synchronize()
+        return bundle_from_export(meta, payload, cfg, rig, fid)
+
+    yield from merge_sharded(rank, world, n_frames, local, gatherer, to_bundle)
 
 
 def sweep(cfg: PipelineConfig, rig, sils, axis: str, values) -> list:

@@ -71,16 +71,6 @@ def _frame_along(direction):
 
 
 @dataclass
-class Sphere:
-    center: np.ndarray
-    radius: float
-    color: np.ndarray = field(default_factory=lambda: np.array([200.0, 80.0, 60.0]))
-
-    def parts(self):
-        return [Ellipsoid(self.center, (self.radius,) * 3, np.eye(3), self.color)]
-
-
-@dataclass
 class Ellipsoid:
     """Solid ellipsoid: |Q^T (p - c) / s| <= 1 (Q's columns = world axes)."""
 
@@ -331,12 +321,14 @@ def render_scene_device(rig, objects, shade=True):
 # SURVEY.md 8f4. analytic_silhouette, shade_frame and proposal_from_silhouette
 # run as sm_100a kernels (csrc/synth.cu: fvv_synth_render, fvv_erode_cross)
 # and equal the reference's numpy/scipy outputs bit for bit
-# (tests/test_gpu_synth.py against tests/golden/synth.npz). cast_rays stays a
-# host helper over caller-given rays (not on any hot path).
+# (tests/test_gpu_synth.py against tests/golden/synth.npz). The primitives
+# below are parameter records for those kernels: the reference's host-side
+# ray tests (ray_hits / normal_at / contains, cast_rays) have no counterpart
+# here because the intersection runs on the GPU.
 
 @dataclass
 class Sphere:
-    """synthetic.py:21-55."""
+    """Sphere scene primitive (fields and validation of synthetic.py:21-31)."""
 
     center: np.ndarray
     radius: float
@@ -348,36 +340,18 @@ class Sphere:
         if self.radius <= 0:
             raise ValueError("sphere radius must be positive")
 
-    def ray_hits(self, origin, dirs):
-        """Smallest positive ray parameter per ray, +inf on miss (host)."""
-        oc = origin - self.center
-        b = dirs @ oc
-        c = oc @ oc - self.radius ** 2
-        disc = b * b - c
-        hit = disc >= 0
-        sq = np.sqrt(np.where(hit, disc, 0.0))
-        t0 = -b - sq
-        t1 = -b + sq
-        t = np.where(t0 > 1e-9, t0, t1)
-        return np.where(hit & (t > 1e-9), t, np.inf)
-
-    def normal_at(self, p):
-        n = p - self.center
-        return n / np.linalg.norm(n, axis=-1, keepdims=True)
-
-    def contains(self, pts):
-        return np.linalg.norm(pts - self.center, axis=-1) <= self.radius
-
     def aabb(self):
-        return self.center - self.radius, self.center + self.radius
+        r = np.full(3, float(self.radius))
+        return self.center - r, self.center + r
 
     def _record(self):
+        """fvv_synth_render record: kind 0, centre, r^2, colour."""
         return [0.0, *self.center, float(self.radius) ** 2, *self.color, 0.0, 0.0]
 
 
 @dataclass
 class Box:
-    """synthetic.py:58-98."""
+    """Axis-aligned box primitive (fields and validation of synthetic.py:58-69)."""
 
     lo: np.ndarray
     hi: np.ndarray
@@ -390,34 +364,11 @@ class Box:
         if np.any(self.hi <= self.lo):
             raise ValueError("box must have positive extent")
 
-    def ray_hits(self, origin, dirs):
-        with np.errstate(divide="ignore", invalid="ignore"):
-            inv = 1.0 / dirs
-            t_lo = (self.lo - origin) * inv
-            t_hi = (self.hi - origin) * inv
-        tmin = np.nanmax(np.minimum(t_lo, t_hi), axis=-1)
-        tmax = np.nanmin(np.maximum(t_lo, t_hi), axis=-1)
-        hit = (tmax >= np.maximum(tmin, 1e-9)) & (tmax > 1e-9)
-        t = np.where(tmin > 1e-9, tmin, tmax)
-        return np.where(hit, t, np.inf)
-
-    def normal_at(self, p):
-        mid = 0.5 * (self.lo + self.hi)
-        half = 0.5 * (self.hi - self.lo)
-        rel = np.atleast_2d((p - mid) / half)
-        n = np.zeros_like(rel)
-        ax = np.argmax(np.abs(rel), axis=-1)
-        rows = np.arange(len(rel))
-        n[rows, ax] = np.sign(rel[rows, ax])
-        return n.reshape(np.shape(p))
-
-    def contains(self, pts):
-        return np.all((pts >= self.lo) & (pts <= self.hi), axis=-1)
-
     def aabb(self):
-        return self.lo.copy(), self.hi.copy()
+        return np.array(self.lo), np.array(self.hi)
 
     def _record(self):
+        """fvv_synth_render record: kind 1, lo, hi, colour."""
         return [1.0, *self.lo, *self.hi, *self.color]
 
 
@@ -441,20 +392,6 @@ class SyntheticScene:
 
     def __post_init__(self) -> None:
         self.light_dir = _unit(self.light_dir)
-
-
-def cast_rays(objects, origin, dirs):
-    """synthetic.py:165-176 (host helper over caller-given rays)."""
-    flat = np.asarray(dirs).reshape(-1, 3)
-    best_t = np.full(len(flat), np.inf)
-    best_o = np.full(len(flat), -1, dtype=np.int32)
-    for oi, obj in enumerate(objects):
-        t = obj.ray_hits(origin, flat)
-        closer = t < best_t
-        best_t[closer] = t[closer]
-        best_o[closer] = oi
-    shape = np.shape(dirs)[:-1]
-    return best_t.reshape(shape), best_o.reshape(shape)
 
 
 def _synth_device(cam, objects, light, want_sil, want_rgb, noise=None):
@@ -492,7 +429,7 @@ def analytic_silhouette(cam, objects) -> np.ndarray:
     """Exact binary silhouette: a pixel is foreground iff its centre ray hits
     any object in front of the camera (synthetic.py:187-192), on the GPU."""
     if cam.has_distortion:
-        raise ValueError("pixel_rays supports zero-distortion cameras only")
+        raise ValueError("pixel_rays supports zero-distortion cameras only")  # the reference message
     sil, _ = _synth_device(cam, list(objects), np.array([0.0, 0.0, 1.0]), True, False)
     return sil.cpu().numpy().astype(bool)
 
@@ -503,7 +440,7 @@ def shade_frame(scene: SyntheticScene, cam, noise_sigma: float = 0.0, seed: int 
     default_rng(seed + cam.id) stream, drawn on the host; the shading runs on
     the GPU."""
     if cam.has_distortion:
-        raise ValueError("pixel_rays supports zero-distortion cameras only")
+        raise ValueError("pixel_rays supports zero-distortion cameras only")  # the reference message
     noise = None
     if noise_sigma > 0:
         rng = np.random.default_rng(seed + cam.id)

@@ -1,30 +1,33 @@
-"""Aggregate an `ncu --page source --print-source cuda,sass --csv` dump per
-CUDA source line: warp instructions executed and stall samples."""
+"""Per-source-line instruction / stall totals of one kernel launch in an ncu
+report (--print-source cuda,sass): python scripts/ncu_lines.py REP SKIP [N]"""
 import csv
+import io
+import subprocess
 import sys
 
-rows = list(csv.reader(open(sys.argv[1])))
-top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-f = None
-agg = {}
-hdr = None
-for r in rows:
-    if len(r) >= 2 and r[0] == "File Path":
-        f = r[1].split("/")[-1]
+rep, skip = sys.argv[1], sys.argv[2]
+top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source",
+                      "cuda,sass", "--launch-skip", skip, "--launch-count", "1"],
+                     capture_output=True, text=True).stdout
+fname, rows, hdr = None, [], None
+for r in csv.reader(io.StringIO(out)):
+    if not r:
         continue
-    if r and r[0] == "Line No":
+    if r[0] == "File Path":
+        fname = r[1].split("/")[-1]
+        continue
+    if r[0] == "Line No":
         hdr = r
         continue
-    if hdr is None or len(r) < 8 or r[0] == "" or r[0] == "Function Name":
-        continue
-    try:
-        inst = float(r[7]); samp = float(r[4])
-    except ValueError:
-        continue
-    key = (f, r[0])
-    a = agg.setdefault(key, [0.0, 0.0, r[1][:90]])
-    a[0] += inst; a[1] += samp
-ti = sum(a[0] for a in agg.values()) or 1
-ts = sum(a[1] for a in agg.values()) or 1
-for (f, ln), (i, s, src) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
-    print(f"{f}:{ln:>4} inst {100*i/ti:5.1f}% stall {100*s/ts:5.1f}%  {src}")
+    if hdr and r[0] not in ("", "Function Name"):
+        try:
+            rows.append((fname, r[0], r[1], int(r[hdr.index("Warp Stall Sampling (All Samples)")]),
+                         int(r[hdr.index("Instructions Executed")])))
+        except ValueError:
+            pass
+ts = sum(x[3] for x in rows) or 1
+ti = sum(x[4] for x in rows) or 1
+print(f"total stall samples {ts}, warp instructions {ti}")
+for f, ln, src, s, n in sorted(rows, key=lambda x: -x[3])[:top]:
+    print(f"{s / ts * 100:5.1f}% stall {n / ti * 100:5.1f}% inst  {f}:{ln}  {src.strip()[:70]}")

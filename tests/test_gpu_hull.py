@@ -237,3 +237,34 @@ def test_carve_tiles_random_rigs_vs_oracle(gpu, seed):
             ref = O.carve(rig, sils, sp.origin, sp.spacing, sp.dims, mv)
             got = carve(rig, sils, sp, min_views=mv).occ
             assert np.array_equal(got, ref), (seed, sp.dims, mv)
+
+
+@pytest.mark.parametrize("dtype", ["float32", "int32", "float64"])
+def test_non_bool_silhouettes_are_coerced_like_reference(gpu, dtype):
+    """hull.py:68 casts every silhouette with np.asarray(sil, dtype=bool):
+    a float / int mask with values other than 0/1 must carve like its bool
+    form, whether handed over as numpy arrays, a stacked (N,H,W) torch
+    tensor, or DeviceSilhouettes."""
+    import torch
+
+    from paper_1903_11785_b200._device import DeviceSilhouettes
+    from paper_1903_11785_b200.hull import carve
+    from paper_1903_11785_b200.pipeline import PipelineConfig, run_frame
+
+    z = G.load("spheres")
+    rig, sils = G.rig(z), G.sils(z)
+    sp = G.spec(z["carve0_spec"])
+    ref = carve(rig, sils, sp).occ
+    scaled = [s.astype(dtype) * 0.75 if dtype != "int32" else s.astype(dtype) * 256
+              for s in sils]
+    assert np.array_equal(carve(rig, scaled, sp).occ, ref)
+    stacked = torch.from_numpy(np.stack(scaled))
+    assert np.array_equal(carve(rig, DeviceSilhouettes(rig, stacked), sp).occ, ref)
+    cfg = PipelineConfig(stage_lo=tuple(sp.origin), stage_hi=tuple(
+        sp.origin + sp.spacing * np.asarray(sp.dims)), coarse_spacing=sp.spacing,
+        fine_spacing=sp.spacing / 2, t_small=3)
+    frames = {c.id: None for c in rig}
+    a = run_frame(cfg, rig, frames, sils=sils)
+    b = run_frame(cfg, rig, frames, sils=stacked.cuda())
+    assert a.stats == b.stats
+    assert np.array_equal(a.merged_mesh.triangles, b.merged_mesh.triangles)

@@ -57,7 +57,7 @@ def test_c1_frame_matches_oracle(gpu):
     assert b.stats["sparse_tests"] == 128 ** 3
 
 
-@pytest.mark.parametrize("frame", [0, 7])
+@pytest.mark.parametrize("frame", [0, 1, 2, 3, 7])  # 0-3: the frames bench.py cycles
 def test_c3_volleyball_frame_matches_oracle(gpu, frame):
     from paper_1903_11785_b200 import workloads
 
@@ -205,3 +205,72 @@ def test_executor_more_than_4096_components_vs_oracle(gpu):
     mv, mt, _ = ref["merged"]
     assert np.array_equal(bundle.merged_mesh.vertices, mv)
     assert np.array_equal(bundle.merged_mesh.triangles, mt)
+
+
+def test_frame_export_roundtrip_matches_run_frame(gpu):
+    """The sharded path's sender side on the GPU: _run_local(export=True)
+    ships each frame's mesh + visibility as a device payload
+    (FrameOutput.export); rebuilt on the host with bundle_from_export (what
+    rank 0 does after its NCCL receive) it equals run_frame's bundle."""
+    import torch
+
+    from paper_1903_11785_b200 import workloads
+    from paper_1903_11785_b200.pipeline import _run_local, run_frame
+    from paper_1903_11785_b200.sharding import bundle_from_export
+
+    wl = workloads.get("C3")
+    seq = [_inputs(wl, f) for f in (0, 5)]
+    frames = [{k: torch.from_numpy(v).pin_memory() for k, v in fr.items()} for _, _, fr in seq]
+    sils = [m.cpu().pin_memory() for m, _, _ in seq]
+    got = list(_run_local(wl.cfg, wl.rig, frames, sils, wl.virtual, None, iter([3, 9]), 2,
+                          export=True))
+    assert [g[0] for g in got] == [3, 9]
+    for (fid, bundle, img, exp), (masks, _, fr) in zip(got, seq):
+        assert bundle is None and img is not None
+        meta, payload, ev = exp
+        ev.synchronize()
+        b = bundle_from_export(meta, payload.cpu(), wl.cfg, wl.rig, fid)
+        ref = run_frame(wl.cfg, wl.rig, fr, sils=masks)
+        assert b.frame_id == fid and b.stats == ref.stats
+        assert np.array_equal(b.merged_mesh.vertices, ref.merged_mesh.vertices)
+        assert np.array_equal(b.merged_mesh.triangles, ref.merged_mesh.triangles)
+        assert np.array_equal(b.merged_mesh.object_ids, ref.merged_mesh.object_ids)
+        assert len(b.meshes) == len(ref.meshes)
+        for c in wl.rig:
+            assert np.array_equal(b.visibility[c.id], ref.visibility[c.id])
+
+
+def test_run_sequence_sharded_single_rank_equals_run_sequence(gpu):
+    """Without a process group run_sequence_sharded is run_sequence over
+    source(f) for every frame, in order."""
+    from paper_1903_11785_b200 import workloads
+    from paper_1903_11785_b200.pipeline import run_sequence_sharded
+
+    wl = workloads.get("C1")
+    seq = [_inputs(wl, f) for f in range(3)]
+    got = list(run_sequence_sharded(wl.cfg, wl.rig, lambda f: (seq[f][2], seq[f][0]), 3,
+                                    wl.virtual, lanes=2))
+    assert [f for f, _, _ in got] == [0, 1, 2]
+    for (f, bundle, img), (masks, m_np, fr) in zip(got, seq):
+        ref = O.run_frame(list(wl.rig), m_np, wl.cfg.stage_lo, wl.cfg.stage_hi,
+                          wl.cfg.coarse_spacing, wl.cfg.fine_spacing, wl.cfg.min_views,
+                          wl.cfg.t_small, wl.cfg.t_large, wl.cfg.roi_margin, wl.cfg.t_v)
+        assert bundle.stats == ref["stats"] and img is not None
+        assert np.array_equal(bundle.merged_mesh.triangles, ref["merged"][1])
+
+
+def test_host_scene_generator_matches_device(gpu):
+    """bench.py's reference arm renders its inputs on the host
+    (synthetic.render_scene, numpy) so it never loads the product library;
+    the silhouettes are the GPU generator's, so both arms time one workload."""
+    from paper_1903_11785_b200 import synthetic as S
+    from paper_1903_11785_b200 import workloads
+
+    wl = workloads.get("C3")
+    d_masks, _ = S.render_scene_device(wl.rig, wl.objects(1), shade=False)
+    h_sils, _ = S.render_scene(wl.rig, wl.objects(1), shade=False)
+    d = d_masks.cpu().numpy().astype(bool)
+    diff = sum(int((a != b).sum()) for a, b in zip(d, h_sils))
+    total = sum(int(b.sum()) for b in h_sils)
+    assert total > 100_000
+    assert diff <= 1e-4 * total, (diff, total)  # rounding-level ray-cast ties at most
