@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfvv.so")
+LIB_PATH = os.environ.get("FVV_LIB") or os.path.join(_HERE, "libfvv.so")  # FVV_LIB: experiment builds
 
 FVV_MAX_CAMS = 64
 FVV_MAX_GRIDS = 128
