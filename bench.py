@@ -408,7 +408,7 @@ def run_b200(args):
         run_e2e(max(args.warmup, 2 * len(host) + 2))
         torch.cuda.synchronize()
         barrier(world)
-        R.H2D_BYTES["frames"] = 0
+        R.H2D_BYTES["frames"] = R.H2D_BYTES["masks"] = 0
         g0 = SH.GATHER_BYTES["payload"]
         gc.collect()
         gc.disable()
@@ -418,16 +418,17 @@ def run_b200(args):
         t1 = time.perf_counter()
         gc.enable()
         barrier(world)
-        h2d = int(host[0][0].numel() + R.H2D_BYTES["frames"] / args.steps)
+        h2d = int((R.H2D_BYTES["masks"] + R.H2D_BYTES["frames"]) / args.steps)
         e2e_ms = max_over_ranks((t1 - t0) * 1e3, world)
         gathered = SH.GATHER_BYTES["payload"] - g0
         e2e = {"value": round(total_frames / (e2e_ms / 1e3), 3), "unit": "frames/s",
                "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": int((d2h + gathered) / args.steps),
                "ms_per_step": round(e2e_ms / args.steps, 3),
-               "api": f"pipeline.run_sequence (run_frame + render_view per frame, {lanes} "
-                      "executor lanes; silhouettes uploaded ahead on a copy stream, pinned "
-                      "colour frames sampled in place (zero-copy: h2d counts the 12 B of "
+               "api": f"pipeline.run_sequence (run_frame + render_view per frame) on the "
+                      f"native sequence runner (csrc/seq.cu: {lanes} C++ lanes, each with its "
+                      "own streams and two frame executors); silhouettes uploaded per frame by "
+                      "its lane, pinned colour frames sampled in place (zero-copy: h2d counts the 12 B of "
                       "bilinear taps per sourced pixel), results read back on a readback "
                       "stream as one pinned block per frame (virtual view as colour + an "
                       "int8 source/coverage code), pinned host inputs" +

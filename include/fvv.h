@@ -361,6 +361,57 @@ int fvv_frame_readback(const fvv_frame *frame, void *host_dst, int flags, void *
 int fvv_frame_get_rois(const fvv_frame *frame, int64_t *component_ids, double *boxes,
                    fvv_grid *grids, int64_t *info);
 
+/* ---- native sequence runner: pipeline.run_sequence's engine ------------------ */
+/* `lanes` host threads, each with its own CUDA streams and two frame
+ * executors, run frames n = lane (mod lanes) of a video sequence: the
+ * silhouette upload, fvv_frame_run and one fvv_frame_readback into a pooled
+ * pinned block per frame (pipeline.py:115-220 + render.py:64-113 per frame,
+ * pipelined over threads as PAPER.md:561 describes). Results come back in
+ * submission order and own their outputs until fvv_seq_result_free. */
+typedef struct fvv_seq fvv_seq;
+typedef struct fvv_seq_result fvv_seq_result;
+
+typedef struct fvv_seq_config {
+    int32_t lanes;
+    int32_t readback_flags;   /* fvv_frame_readback flags (bit 1: compact colour) */
+    int32_t has_virtual;      /* run the colour pass for virt */
+    int32_t export_payload;   /* mesh + visibility into a device payload, not read back */
+    fvv_camera virt;
+    int32_t rank_pos[FVV_MAX_CAMS];  /* render.py:29-32 ranking (rig positions) */
+    uint8_t fallback[4];             /* render.py:19 FALLBACK_COLOR */
+} fvv_seq_config;
+
+typedef struct fvv_seq_result_info {
+    int64_t id;
+    int32_t status, stage;    /* fvv_frame_run status; stage as its out_stage */
+    const char *err;
+    fvv_frame_stats stats;
+    int64_t nv, nt, vis_stride, n_rois;
+    const int64_t *component_ids;  /* n_rois */
+    const double *boxes;           /* n_rois x 6 */
+    const fvv_grid *grids;         /* n_rois */
+    const int64_t *roi_info;       /* n_rois x 8, as fvv_frame_get_rois */
+    int64_t layout[16];            /* fvv_frame_readback_layout of the pinned block */
+    const void *host;              /* the pinned block */
+    void *payload_dev;             /* export: verts | tris | visibility bits (256-aligned) */
+    int64_t payload_bytes;
+} fvv_seq_result_info;
+
+fvv_seq *fvv_seq_create(const fvv_camera *cams, int ncam, const fvv_frame_config *cfg,
+                        const fvv_seq_config *seq_cfg);
+void fvv_seq_destroy(fvv_seq *seq);
+/* Queue frame `id`: nmask silhouette buffers (one rig-order buffer or one per
+ * camera; host pageable/pinned or device) with their byte sizes, and per
+ * camera colour frames (H, W, 3) uint8 or NULL. Inputs must stay alive until
+ * the frame's result is returned. Blocks while the lane holds 2 queued frames. */
+int fvv_seq_submit(fvv_seq *seq, int64_t id, const void *const *mask_src,
+                   const int64_t *mask_bytes, int nmask, const void *const *frame_src);
+/* Next result in submission order (its copies complete): 1 = *out set, 0 =
+ * none pending (or, with wait = 0, none ready yet). */
+int fvv_seq_next(fvv_seq *seq, int wait, fvv_seq_result **out);
+int fvv_seq_result_get(const fvv_seq_result *res, fvv_seq_result_info *info);
+void fvv_seq_result_free(fvv_seq_result *res);
+
 /* ---- harness (not hot path): synthetic scene inputs ------------------------- */
 
 /* synthetic.py:165-218 for the reference's Sphere/Box scenes: per pixel of

@@ -50,6 +50,8 @@ SYMBOLS = (
     "fvv_frame_get_rois", "fvv_frame_readback_layout", "fvv_frame_readback",
     "fvv_synth_render", "fvv_erode_cross", "fvv_distance_map", "fvv_background",
     "fvv_extract_silhouette",
+    "fvv_seq_create", "fvv_seq_destroy", "fvv_seq_submit", "fvv_seq_next", "fvv_seq_result_get",
+    "fvv_seq_result_free",
 )
 
 FRAME_CONFIG_DTYPE = np.dtype([("stage_lo", "<f8", (3,)), ("stage_hi", "<f8", (3,)),
@@ -69,6 +71,31 @@ class FrameOutputs(ctypes.Structure):
                 ("depth", ctypes.c_void_p), ("color", ctypes.c_void_p),
                 ("source", ctypes.c_void_p), ("covered", ctypes.c_void_p),
                 ("n_rois", ctypes.c_int64), ("ntri_dev", ctypes.c_void_p)]
+
+
+class FrameStats(ctypes.Structure):  # include/fvv.h fvv_frame_stats (128 bytes)
+    _fields_ = [(k, ctypes.c_int64) for k in FRAME_STATS_DTYPE.names[:10]] + [
+        ("ms", ctypes.c_float * 8), ("covered_px", ctypes.c_int64), ("sourced_px", ctypes.c_int64)]
+
+
+class SeqConfig(ctypes.Structure):  # include/fvv.h fvv_seq_config
+    _fields_ = [("lanes", ctypes.c_int32), ("readback_flags", ctypes.c_int32),
+                ("has_virtual", ctypes.c_int32), ("export_payload", ctypes.c_int32),
+                ("virt", ctypes.c_uint8 * 192), ("rank_pos", ctypes.c_int32 * FVV_MAX_CAMS),
+                ("fallback", ctypes.c_uint8 * 4)]
+
+
+class SeqResultInfo(ctypes.Structure):  # include/fvv.h fvv_seq_result_info
+    _fields_ = [("id", ctypes.c_int64), ("status", ctypes.c_int32), ("stage", ctypes.c_int32),
+                ("err", ctypes.c_char_p), ("stats", FrameStats), ("nv", ctypes.c_int64),
+                ("nt", ctypes.c_int64), ("vis_stride", ctypes.c_int64), ("n_rois", ctypes.c_int64),
+                ("component_ids", ctypes.c_void_p), ("boxes", ctypes.c_void_p),
+                ("grids", ctypes.c_void_p), ("roi_info", ctypes.c_void_p),
+                ("layout", ctypes.c_int64 * 16), ("host", ctypes.c_void_p),
+                ("payload_dev", ctypes.c_void_p), ("payload_bytes", ctypes.c_int64)]
+
+
+assert ctypes.sizeof(FrameStats) == FRAME_STATS_DTYPE.itemsize == 128
 
 
 class FvvError(RuntimeError):
@@ -93,6 +120,14 @@ def load():
         lib.fvv_frame_create.restype = ctypes.c_void_p
         lib.fvv_frame_readback_layout.restype = ctypes.c_int64
         lib.fvv_frame_destroy.argtypes = [ctypes.c_void_p]
+        lib.fvv_seq_create.restype = ctypes.c_void_p
+        lib.fvv_seq_destroy.argtypes = [ctypes.c_void_p]
+        lib.fvv_seq_result_free.argtypes = [ctypes.c_void_p]
+        lib.fvv_seq_result_get.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+        lib.fvv_seq_next.argtypes = [ctypes.c_void_p, ctypes.c_int,
+                                     ctypes.POINTER(ctypes.c_void_p)]
+        lib.fvv_seq_submit.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
         lib.fvv_ccl_workspace_bytes.restype = ctypes.c_size_t
         lib.fvv_carve_workspace_bytes.restype = ctypes.c_size_t
         lib.fvv_rle_workspace_bytes.restype = ctypes.c_size_t

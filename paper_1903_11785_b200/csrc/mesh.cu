@@ -377,7 +377,10 @@ __global__ void __launch_bounds__(128)
 }
 
 // ---- B1: isovalues + vertices (mesh.py:231-272, 332-337) --------------------
-__global__ void __launch_bounds__(128)
+#ifndef FVV_LAMBDA_MINB1
+#define FVV_LAMBDA_MINB1 1
+#endif
+__global__ void __launch_bounds__(128, FVV_LAMBDA_MINB1)
     mesh_lambda_kernel(const __grid_constant__ MeshGrids G, const __grid_constant__ MeshCams C,
                        MeshBufs B, const uint32_t *__restrict__ sil) {
   const int64_t nv = __ldcg(B.totals);
@@ -923,7 +926,11 @@ int fvv_mesh_emit(const fvv_camera *cams_by_id, int ncam, const uint32_t *sil_de
   Slot5 *d_total = (Slot5 *)((char *)ws_dev + L.slot5 + sizeof(int64_t) * 5 * ngrid);
   if (num_vertices > 0) {
     mesh_vertex_list_kernel<<<kMeshGrid, 256, 0, st>>>(h_grids, B);
+#ifndef FVV_LAMBDA_GROUPS
+    if (false) {  // measured slower (profiles/r2_mesh_lambda.md): the per-vertex loop wins
+#else
     if (exact) {  // (vertex, camera) items, a lane group per vertex
+#endif
       const int gs = ncam <= 4 ? 4 : ncam <= 8 ? 8 : ncam <= 16 ? 16 : 32;
       const int64_t lam_blocks = std::min<int64_t>(num_vertices * gs / 256 + 1, 148 * 32);
       switch (gs) {

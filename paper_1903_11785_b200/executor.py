@@ -176,6 +176,24 @@ class HostBlock:
         return out
 
 
+def frame_config(cfg, budget) -> np.ndarray:
+    """PipelineConfig -> include/fvv.h fvv_frame_config record."""
+    conf = np.zeros(1, dtype=_lib.FRAME_CONFIG_DTYPE)
+    conf["stage_lo"] = np.asarray(cfg.stage_lo, dtype=np.float64)
+    conf["stage_hi"] = np.asarray(cfg.stage_hi, dtype=np.float64)
+    conf["coarse_spacing"] = cfg.coarse_spacing
+    conf["fine_spacing"] = cfg.fine_spacing
+    conf["roi_margin"] = cfg.roi_margin
+    conf["t_v"] = cfg.t_v
+    conf["t_large"] = float(cfg.t_large)
+    conf["fixed_isovalue"] = cfg.fixed_isovalue
+    conf["t_small"] = int(cfg.t_small)
+    conf["budget"] = int(budget)
+    conf["min_views"] = int(cfg.min_views)
+    conf["exact"] = int(cfg.iso_mode == "exact")
+    return conf
+
+
 class FrameExecutor:
     """fvv_frame handle for one rig + PipelineConfig."""
 
@@ -186,19 +204,7 @@ class FrameExecutor:
         self.cams = list(rig)
         self.ncam = len(self.cams)
         self._tab = cam_table(self.cams)
-        conf = np.zeros(1, dtype=_lib.FRAME_CONFIG_DTYPE)
-        conf["stage_lo"] = np.asarray(cfg.stage_lo, dtype=np.float64)
-        conf["stage_hi"] = np.asarray(cfg.stage_hi, dtype=np.float64)
-        conf["coarse_spacing"] = cfg.coarse_spacing
-        conf["fine_spacing"] = cfg.fine_spacing
-        conf["roi_margin"] = cfg.roi_margin
-        conf["t_v"] = cfg.t_v
-        conf["t_large"] = float(cfg.t_large)
-        conf["fixed_isovalue"] = cfg.fixed_isovalue
-        conf["t_small"] = int(cfg.t_small)
-        conf["budget"] = int(DEFAULT_VOXEL_BUDGET if budget is None else budget)
-        conf["min_views"] = int(cfg.min_views)
-        conf["exact"] = int(cfg.iso_mode == "exact")
+        conf = frame_config(cfg, DEFAULT_VOXEL_BUDGET if budget is None else budget)
         self._conf = conf
         h = _lib.load().fvv_frame_create(_lib.host_ptr(self._tab), ctypes.c_int(self.ncam),
                                          _lib.host_ptr(conf))
@@ -296,3 +302,269 @@ def executor_for(cfg, rig, slot: int = 0) -> FrameExecutor:
     else:
         _EXECUTORS.move_to_end(key)
     return ex
+
+
+# ---------------------------------------------------------------- native sequences
+class _SeqOwner:
+    """Frees a native sequence result (its pinned block and device payload)
+    when the last array or tensor viewing it is gone."""
+
+    __slots__ = ("h",)
+
+    def __init__(self, h):
+        self.h = h
+
+    def __del__(self):
+        if self.h:
+            try:
+                _lib.load().fvv_seq_result_free(ctypes.c_void_p(self.h))
+            except Exception:  # noqa: BLE001  (interpreter shutdown)
+                pass
+            self.h = None
+
+
+_STATS_KEYS = ("sparse_tests", "sparse_occupied", "components", "dense_tests", "dense_occupied",
+               "fallback_edges", "inconsistent_edge_starts", "triangles", "vertices", "n_rois",
+               "covered_px", "sourced_px")
+
+
+class SeqOutput:
+    """One native-sequence frame: the FrameOutput fields the bundle builders
+    read (stats, per-ROI tables, sizes), host arrays in the result's pinned
+    block (views that keep it alive), and the device export payload."""
+
+    def __init__(self, info, ncam, virtual, owner, frames):
+        st = info.stats
+        self.stats_raw = {k: int(getattr(st, k)) for k in _STATS_KEYS}
+        self.stats_raw["ms"] = np.array(list(st.ms), dtype=np.float32)
+        self.frame_id = int(info.id)
+        self.ncam, self.virtual, self.frames = ncam, virtual, frames
+        self.nv, self.nt = int(info.nv), int(st.triangles)
+        self.vis_stride = int(info.vis_stride)
+        n = int(info.n_rois)
+
+        def arr(ptr, dtype, shape):
+            if n == 0 or not ptr:
+                return np.zeros(shape, dtype=dtype)
+            nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+            raw = (ctypes.c_uint8 * nbytes).from_address(ptr)
+            return np.frombuffer(bytes(raw), dtype=dtype).reshape(shape)  # small: copied
+
+        self.component_ids = arr(info.component_ids, np.int64, (n,))
+        self.boxes = arr(info.boxes, np.float64, (n, 6))
+        self.grids = arr(info.grids, _lib.GRID_DTYPE, (n,))
+        self.info = arr(info.roi_info, np.int64, (n, 8))
+        lay = np.array(list(info.layout), dtype=np.int64)
+        self.layout = lay
+        self.nbytes = int(lay[8:15].sum())
+        self.host = {}
+        total = int(lay[7])
+        if info.host and total:
+            carr = (ctypes.c_uint8 * total).from_address(info.host)
+            carr._owner = owner  # numpy views -> memoryview -> carr -> owner
+            raw = np.ctypeslib.as_array(carr)
+            shapes = {"verts": ((self.nv, 3), np.float64), "tris": ((self.nt, 3), np.int32),
+                      "vis": ((ncam, self.vis_stride), np.uint32)}
+            if virtual is not None:
+                h, w = virtual.image_height, virtual.image_width
+                shapes.update(color=((h, w, 3), np.uint8), code=((h, w), np.int8))
+            for i, name in enumerate(("verts", "tris", "vis", "color", "code")):
+                off, nb = int(lay[i]), int(lay[8 + i])
+                if name in shapes and (nb or name in ("verts", "tris", "vis")) and \
+                        nb == int(np.prod(shapes[name][0])) * np.dtype(shapes[name][1]).itemsize:
+                    shape, dt = shapes[name]
+                    self.host[name] = raw[off:off + nb].view(dt).reshape(shape)
+        self.payload = None
+        if info.payload_dev:
+            view = _CudaView(info.payload_dev, (max(int(info.payload_bytes), 1),), "|u1")
+            view._owner = owner
+            self.payload = torch.as_tensor(view, device="cuda")
+        self._owner = owner
+
+    def stats(self) -> dict:
+        s = self.stats_raw
+        return {k: int(s[k]) for k in _STATS_KEYS[:8]}
+
+
+class NativeSequence:
+    """fvv_seq (csrc/seq.cu): lanes of native threads, each with its own
+    CUDA streams and two frame executors, run a video sequence frame by
+    frame; submit() queues a frame, next() returns finished frames in
+    submission order. The caller's interpreter lock is never held per frame
+    on the lanes."""
+
+    def __init__(self, cfg, rig, lanes=4, virtual=None, fallback=None, export=False):
+        from .render import FALLBACK_COLOR, rank_cameras
+        from .voxels import DEFAULT_VOXEL_BUDGET
+
+        require_cuda()
+        self.cams = list(rig)
+        self.ncam = len(self.cams)
+        self.virtual = virtual
+        self.lanes = int(lanes)
+        self._tab = cam_table(self.cams)
+        conf = frame_config(cfg, DEFAULT_VOXEL_BUDGET)
+        sc = _lib.SeqConfig()
+        sc.lanes = self.lanes
+        sc.readback_flags = 2 if virtual is not None else 0
+        sc.has_virtual = int(virtual is not None)
+        sc.export_payload = int(bool(export))
+        if virtual is not None:
+            ctypes.memmove(sc.virt, cam_table([virtual]).tobytes(), 192)
+            pos = {c.id: i for i, c in enumerate(self.cams)}
+            for r, cid in enumerate(rank_cameras(virtual, self.cams)):
+                sc.rank_pos[r] = pos[cid]
+        fb = np.asarray(FALLBACK_COLOR if fallback is None else fallback, dtype=np.uint8)
+        for k in range(3):
+            sc.fallback[k] = int(fb.reshape(3)[k])
+        self._sc = sc
+        self._mask_px = [c.image_height * c.image_width for c in self.cams]
+        lib = _lib.load()
+        h = lib.fvv_seq_create(_lib.host_ptr(self._tab), ctypes.c_int(self.ncam),
+                               _lib.host_ptr(conf), ctypes.byref(sc))
+        if not h:
+            raise ValueError(lib.fvv_last_error().decode(errors="replace"))
+        self._h = ctypes.c_void_p(h)
+        self._pending = {}
+        self.h2d_masks = 0  # silhouette bytes uploaded
+        self.h2d_frames = 0  # colour bytes over PCIe (zero-copy taps or uploads)
+
+    def close(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib = _lib.load()
+            while True:  # results never collected: free them
+                res = ctypes.c_void_p()
+                if lib.fvv_seq_next(h, 1, ctypes.byref(res)) != 1:
+                    break
+                lib.fvv_seq_result_free(res)
+            lib.fvv_seq_destroy(h)
+            self._h = None
+            self._pending.clear()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    @staticmethod
+    def _piece(a, keep):
+        if isinstance(a, torch.Tensor):
+            a = mask_bytes(a) if a.dtype != torch.uint8 else a
+            a = a.contiguous()
+            keep.append(a)
+            return a.data_ptr(), a.numel() * a.element_size(), a.is_cuda
+        arr = np.asarray(a)
+        if arr.dtype == np.bool_:
+            arr = arr.view(np.uint8)
+        elif arr.dtype != np.uint8:
+            arr = (arr != 0).view(np.uint8)
+        arr = np.ascontiguousarray(arr)
+        keep.append(arr)
+        return arr.ctypes.data, arr.size, False
+
+    def submit(self, frame_id, sils, frames=None):
+        """Queue one frame: ``sils`` in rig order (list of (H, W) arrays or
+        tensors, a stacked (N, H, W) or flat tensor, or a dict by camera
+        id); ``frames`` a dict camera id -> (H, W, 3) uint8 for the colour
+        pass. Inputs must stay unmodified until the frame is returned."""
+        keep = []
+        if isinstance(sils, torch.Tensor) and sils.dim() in (1, 3):
+            pieces = [self._piece(sils.reshape(-1), keep)]
+        else:
+            sl = [sils[c.id] for c in self.cams] if isinstance(sils, dict) else list(sils)
+            if len(sl) != self.ncam:
+                raise ValueError(f"{len(sl)} silhouettes for {self.ncam} cameras")
+            pieces = []
+            for c, sv in zip(self.cams, sl):
+                shp = tuple(sv.shape)
+                if shp != (c.image_height, c.image_width):
+                    raise ValueError(f"camera {c.id}: silhouette shape {shp} != "
+                                     f"({c.image_height}, {c.image_width})")
+                pieces.append(self._piece(sv, keep))
+        if sum(n for _, n, _ in pieces) != sum(self._mask_px):
+            raise ValueError("silhouettes do not match the rig's image sizes")
+        ptrs = np.array([p for p, _, _ in pieces], dtype=np.uint64)
+        sizes = np.array([n for _, n, _ in pieces], dtype=np.int64)
+        fptr = None
+        zero_copy = False
+        if self.virtual is not None and frames is not None:
+            fp = []
+            for c in self.cams:
+                f = frames[c.id]
+                p, n, acc = self._piece(f, keep)
+                if n != 3 * c.image_height * c.image_width:
+                    raise ValueError(f"camera {c.id}: colour frame has {n} bytes")
+                fp.append(p)
+            fptr = np.array(fp, dtype=np.uint64)
+            zero_copy = all(isinstance(frames[c.id], torch.Tensor) and
+                            (frames[c.id].is_cuda or frames[c.id].is_pinned()) for c in self.cams)
+        in_place = len(pieces) == 1 and isinstance(keep[0], torch.Tensor) and keep[0].is_cuda
+        keep += [ptrs, sizes]
+        self._pending[int(frame_id)] = (keep, frames, zero_copy, not in_place)
+        rc = _lib.load().fvv_seq_submit(
+            self._h, ctypes.c_int64(int(frame_id)), ctypes.c_void_p(ptrs.ctypes.data),
+            ctypes.c_void_p(sizes.ctypes.data), ctypes.c_int(len(pieces)),
+            ctypes.c_void_p(fptr.ctypes.data) if fptr is not None else None)
+        if rc != 0:
+            self._pending.pop(int(frame_id), None)
+            raise ValueError(_lib.load().fvv_last_error().decode(errors="replace"))
+
+    def next(self, wait=True):
+        """The next finished frame (SeqOutput) in submission order, or None."""
+        from .pipeline import StageError
+
+        lib = _lib.load()
+        res = ctypes.c_void_p()
+        if lib.fvv_seq_next(self._h, int(bool(wait)), ctypes.byref(res)) != 1:
+            return None
+        owner = _SeqOwner(res.value)
+        info = _lib.SeqResultInfo()
+        lib.fvv_seq_result_get(res, ctypes.byref(info))
+        keep, frames, zero_copy, uploaded_masks = self._pending.pop(int(info.id), (None,) * 4)
+        if info.status != 0:
+            msg = (info.err or b"").decode(errors="replace")
+            cause = ValueError(msg) if info.status in (_lib.FVV_E_ARG, _lib.FVV_E_LIMIT) else \
+                _lib.FvvError(msg)
+            raise StageError(STAGE_NAMES.get(int(info.stage), "B-1 sparse carve"), cause)
+        out = SeqOutput(info, self.ncam, self.virtual, owner, frames)
+        if uploaded_masks:
+            self.h2d_masks += sum(self._mask_px)
+        if self.virtual is not None and frames is not None:
+            self.h2d_frames += (12 * out.stats_raw["sourced_px"] if zero_copy else
+                                3 * sum(self._mask_px))
+        return out
+
+
+_SEQUENCES = OrderedDict()
+
+
+def sequence_for(cfg, rig, lanes, virtual, fallback, export=False) -> NativeSequence:
+    """Native sequences are cached per (config, rig, lanes, view, fallback,
+    export) and reused by later run_sequence calls."""
+    from dataclasses import astuple
+
+    key = (astuple(cfg), cam_table(list(rig)).tobytes(), int(lanes),
+           None if virtual is None else cam_table([virtual]).tobytes(),
+           None if fallback is None else tuple(int(v) for v in np.asarray(fallback).reshape(-1)),
+           bool(export))
+    seq = _SEQUENCES.get(key)
+    if seq is None:
+        while len(_SEQUENCES) >= 4:
+            _SEQUENCES.popitem(last=False)[1].close()
+        seq = NativeSequence(cfg, rig, lanes, virtual, fallback, export)
+        _SEQUENCES[key] = seq
+    else:
+        _SEQUENCES.move_to_end(key)
+    return seq
+
+
+def _close_sequences():
+    while _SEQUENCES:
+        _SEQUENCES.popitem()[1].close()
+
+
+import atexit  # noqa: E402
+
+atexit.register(_close_sequences)

@@ -18,14 +18,12 @@ flags, depth images) are materialised when the bundle is read.
 
 from __future__ import annotations
 
-import ctypes
 import json
 from dataclasses import asdict, dataclass, replace
 
 import numpy as np
 import torch
 
-from . import _lib
 from ._device import DeviceSilhouettes, mask_bytes, require_cuda
 from .bundle import SceneBundle, StageTimings
 from .hull import NoiseFilterParams, Roi, carve_grids, finish_labels, label_grid_async
@@ -427,104 +425,6 @@ def bundle_from(r: FrameResult, cfg, rig, frames, frame_id=0, keep_depths=False)
     return bundle
 
 
-def _host_piece(a, keep):
-    """(pointer, bytes) of one host input, converted to contiguous uint8 if
-    needed (the converted array is kept alive in ``keep``)."""
-    if isinstance(a, torch.Tensor):
-        if a.dtype == torch.bool:
-            a = a.view(torch.uint8)
-        if a.dtype != torch.uint8:
-            a = a.to(torch.uint8)
-        a = a.contiguous()
-        keep.append(a)
-        return a.data_ptr(), a.numel()
-    arr = np.asarray(a)
-    if arr.dtype == bool:
-        arr = arr.view(np.uint8)
-    arr = np.ascontiguousarray(arr, dtype=np.uint8)
-    keep.append(arr)
-    return arr.ctypes.data, arr.size
-
-
-def _gather_to_device(pieces, dst, stream, keep):
-    ptrs = np.array([p for p, _ in pieces], dtype=np.uint64)
-    sizes = np.array([n for _, n in pieces], dtype=np.int64)
-    _lib.call("fvv_copy_gather", _lib.host_ptr(ptrs), _lib.host_ptr(sizes),
-              _lib.i64(len(pieces)), _lib.dev_ptr(dst), ctypes.c_void_p(stream.cuda_stream))
-    keep.append(ptrs)
-
-
-def _zero_copy_frames(cams, frames, keep):
-    """(base address, byte offsets) when every camera's colour frame is a
-    contiguous uint8 (H, W, 3) tensor in mapped pinned host memory, else None."""
-    ptrs = []
-    lib = _lib.load()
-    for c in cams:
-        f = frames[c.id]
-        if not (isinstance(f, torch.Tensor) and f.device.type == "cpu" and
-                f.dtype == torch.uint8 and f.is_contiguous() and
-                tuple(f.shape) == (c.image_height, c.image_width, 3)):
-            return None
-        p = f.data_ptr()
-        if not lib.fvv_host_mapped(ctypes.c_void_p(p)):
-            return None
-        ptrs.append(p)
-        keep.append(f)
-    base = min(ptrs)
-    return base, np.array([p - base for p in ptrs], dtype=np.int64)
-
-
-def _prefetch(rig, frames, sils, want_frames, copy_stream, compute_stream):
-    """Queue the H2D copies of one frame's inputs on ``copy_stream``:
-    silhouette masks and (when rendering) every camera's colour frame, each
-    into one device buffer with one fvv_copy_gather call."""
-    dev = require_cuda()
-    cams = list(rig)
-    fbuf = foff = None
-    keep = []
-    if isinstance(sils, torch.Tensor):
-        m_pieces = [_host_piece(sils, keep)]
-    else:
-        sl = [sils[c.id] for c in cams] if isinstance(sils, dict) else list(sils)
-        m_pieces = [_host_piece(s, keep) for s in sl]
-    npx = sum(c.image_height * c.image_width for c in cams)
-    if sum(n for _, n in m_pieces) != npx:
-        raise ValueError("silhouettes do not match the rig's image sizes")
-    with torch.cuda.stream(copy_stream):
-        d_masks = torch.empty(npx, dtype=torch.uint8, device=dev)
-    if isinstance(sils, torch.Tensor) and sils.is_cuda:
-        with torch.cuda.stream(copy_stream):
-            d_masks.copy_(keep[0].reshape(-1), non_blocking=True)
-    else:
-        _gather_to_device(m_pieces, d_masks, copy_stream, keep)
-    d_masks.record_stream(compute_stream)
-    if want_frames and frames is not None:
-        from .render import H2D_BYTES
-
-        zc = _zero_copy_frames(cams, frames, keep)
-        if zc is not None:  # sampled in place by the colour pass
-            ev = torch.cuda.Event()
-            ev.record(copy_stream)
-            return d_masks, zc, ev, keep
-        sizes = [c.image_height * c.image_width * 3 for c in cams]
-        foff = np.zeros(len(cams), dtype=np.int64)
-        foff[1:] = np.cumsum(sizes)[:-1]
-        with torch.cuda.stream(copy_stream):
-            fbuf = torch.empty(int(sum(sizes)), dtype=torch.uint8, device=dev)
-        f_pieces = [_host_piece(frames[c.id], keep) for c in cams]
-        for (_, n), sz, c in zip(f_pieces, sizes, cams):
-            if n != sz:
-                raise ValueError(f"camera {c.id}: colour frame has {n} bytes, expected {sz}")
-        _gather_to_device(f_pieces, fbuf, copy_stream, keep)
-        H2D_BYTES["frames"] += int(sum(sizes))
-        fbuf.record_stream(compute_stream)
-    ev = torch.cuda.Event()
-    ev.record(copy_stream)
-    # pinned sources must outlive the copies: the caller holds ``keep`` until
-    # the frame has run
-    return d_masks, (fbuf, foff), ev, keep
-
-
 def _readback(r, image):
     """Copy every host-facing result of a frame back with two syncs: the
     small counters first (they size the rest), then the mesh, visibility
@@ -560,33 +460,20 @@ def _readback(r, image):
     return [x.numpy() for x in himg] if himg is not None else None
 
 
-_SEQ_STREAMS = {}
-
-
-def _sequence_streams(dev_index, lanes):
-    """(copy, readback, [compute per lane]) streams reused across calls."""
-    key = (dev_index, lanes)
-    hit = _SEQ_STREAMS.get(key)
-    if hit is None:
-        hit = (torch.cuda.Stream(), torch.cuda.Stream(),
-               [torch.cuda.Stream() for _ in range(lanes)])
-        _SEQ_STREAMS[key] = hit
-    return hit
-
-
 def run_sequence(cfg: PipelineConfig, rig, frames_seq, sils_seq, virtual=None,
                  fallback_color=None, frame_id0: int = 0, lanes: int = 4):
     """Reconstruct (and, given ``virtual``, colour) a sequence of frames.
 
     The production form of run_frame + render_view for video, pipelined over
-    CPU threads like the paper's system. Frame f goes to lane
-    f mod ``lanes``; each lane is a worker thread driving its own native
-    executor on its own CUDA stream (the ctypes calls release the GIL), so
-    one lane's host synchronisations and small kernels overlap the other
-    lane's work. The caller's thread stages each frame's silhouettes
-    host->device on a copy stream one frame ahead (pinned colour frames are
-    sampled in place by the colour pass), and turns finished frames, streamed
-    back on a readback stream, into SceneBundles. Inputs should be pinned
+    CPU threads like the paper's system: the native sequence
+    runner (csrc/seq.cu) sends frame f to lane f mod ``lanes``, a C++ thread
+    with its own CUDA streams and two frame executors, which uploads the
+    silhouettes, runs the frame and reads its results back into a pooled
+    pinned block, so one lane's host synchronisations and small kernels
+    overlap the other lanes' work and no Python runs per frame on the lanes
+    (pinned colour frames are sampled in place by the colour pass). The
+    caller's thread only queues inputs and turns finished frames into
+    SceneBundles. Inputs should be pinned
     host tensors for the copies to be asynchronous; pinned colour frames are
     read in place by the GPU, so a frame's inputs must stay unmodified until
     that frame has been yielded (up to 2 x lanes frames are in flight).
@@ -605,154 +492,66 @@ def _count_from(n):
 
 def _run_local(cfg, rig, frames_seq, sils_seq, virtual, fallback_color, frame_ids, lanes,
                export=False):
-    """run_sequence's engine. Yields (frame_id, SceneBundle or None, image or
-    None, export or None) in input order. With ``export`` (a frame-sharded
-    rank other than 0) the mesh and visibility bits are not read back:
-    each frame's are copied into one device payload (sharding.py format)
-    for the caller to send to rank 0, and the bundle is None."""
-    import queue
-    import threading
+    """run_sequence's engine over the native sequence runner (executor.
+    NativeSequence, csrc/seq.cu). Yields (frame_id, SceneBundle or None,
+    image or None, export or None) in input order. With ``export`` (a
+    frame-sharded rank other than 0) the mesh and visibility bits are not
+    read back: the lanes copy each frame's into a device payload
+    (sharding.py format) for the caller to send to rank 0, and the bundle is
+    None."""
+    from .executor import sequence_for
+    from .render import D2H_BYTES, H2D_BYTES, CodedImage
 
-    from .executor import executor_for
-    from .render import D2H_BYTES, FALLBACK_COLOR, H2D_BYTES, CodedImage
-
-    fallback_color = FALLBACK_COLOR if fallback_color is None else fallback_color
     require_cuda()
     lanes = max(1, int(lanes))
-    dev_index = torch.cuda.current_device()
     cams = list(rig)
     rig_ids = [c.id for c in cams]
+    seq = sequence_for(cfg, rig, lanes, virtual, fallback_color, export)
     caller = torch.cuda.current_stream()
-    # persistent streams: the caching allocator keeps blocks per stream, so
-    # fresh streams on every call would re-allocate (and, under memory
-    # pressure, synchronise) at the start of each sequence
-    copy, readback, computes = _sequence_streams(dev_index, lanes)
-    copy.wait_stream(caller)
-    for st in computes:
-        st.wait_stream(caller)
-    # two executors per lane, used alternately: a frame's results are read
-    # back from one while the lane's next frame runs in the other
-    exs = [(executor_for(cfg, rig, 2 * k), executor_for(cfg, rig, 2 * k + 1))
-           for k in range(lanes)]
-    in_qs = [queue.Queue(maxsize=1) for _ in range(lanes)]
-    out_qs = [queue.Queue() for _ in range(lanes)]
-    stop = threading.Event()
-    counter_lock = threading.Lock()
-    _END = object()
-
-    def worker(lane):
-        compute, in_q, out_q = computes[lane], in_qs[lane], out_qs[lane]
-        slot_free = [None, None]  # readback event of each executor's last frame
-        n_run = 0
-        try:
-            torch.cuda.set_device(dev_index)
-            with torch.cuda.stream(compute):
-                while True:
-                    item = in_q.get()
-                    if item is _END or stop.is_set():
-                        break
-                    frames, d_masks, (fbuf, foff), ev, _keep = item
-                    compute.wait_event(ev)
-                    slot = n_run & 1
-                    n_run += 1
-                    ex = exs[lane][slot]
-                    if slot_free[slot] is not None:  # its buffers still being read back
-                        compute.wait_event(slot_free[slot])
-                    if virtual is not None:
-                        out = ex.run(d_masks, virtual, fbuf, foff, fallback_color)
-                        if isinstance(fbuf, int):  # zero-copy: the bilinear taps crossed PCIe
-                            with counter_lock:
-                                H2D_BYTES["frames"] += 12 * int(out.stats_raw["sourced_px"])
-                    else:
-                        out = ex.run(d_masks)
-                    exp = None
-                    if export:  # mesh + visibility leave through NCCL, not the host
-                        meta, payload = out.export(compute.device)
-                        pev = torch.cuda.Event()
-                        pev.record(compute)
-                        exp = (meta, payload, pev)
-                    pinned, done = out.to_host_async(cams, stream=readback, compact=True,
-                                                     image_only=export)
-                    slot_free[slot] = done
-                    with counter_lock:
-                        D2H_BYTES["results"] += pinned.nbytes
-                    out_q.put((frames, out, pinned, done, exp))
-        except BaseException as exc:  # noqa: BLE001  (re-raised on the caller's thread)
-            out_q.put(exc)
-            return
-        out_q.put(_END)
-
-    def finish(item, fid):
-        if isinstance(item, BaseException):
-            raise item
-        if item is _END:
-            raise RuntimeError("run_sequence worker stopped early")
-        p_frames, p_out, p_pinned, p_ev, p_exp = item
-        p_ev.synchronize()
-        host = p_pinned.arrays()
-        bundle = None if export else bundle_from_output(p_out, host, cfg, rig, p_frames, fid,
-                                                        keep_device=False)
-        img = None
-        if virtual is not None:
-            img = CodedImage(host["color"], host["code"], rig_ids)
-        return fid, bundle, img, p_exp
-
+    caller.synchronize()  # inputs the caller produced on its stream are complete
     fids = iter(frame_ids)
-    threads = [threading.Thread(target=worker, args=(k,), name=f"fvv-lane{k}", daemon=True)
-               for k in range(lanes)]
+    h2d0 = (seq.h2d_masks, seq.h2d_frames)
 
-    def submit(lane, item):
-        while True:
-            try:
-                in_qs[lane].put(item, timeout=0.05)
-                return
-            except queue.Full:
-                if not threads[lane].is_alive():  # the lane failed: surface its exception
-                    while True:
-                        finish(out_qs[lane].get(), 0)
+    def finish(out):
+        D2H_BYTES["results"] += out.nbytes
+        host = out.host
+        bundle = None if export else bundle_from_output(out, host, cfg, rig, out.frames,
+                                                        out.frame_id, keep_device=False)
+        img = CodedImage(host["color"], host["code"], rig_ids) if virtual is not None else None
+        exp = None
+        if export:
+            from .sharding import export_meta
 
-    for th in threads:
-        th.start()
+            meta = export_meta(out.stats(), out.stats_raw["ms"][:6], out.component_ids,
+                               out.info, out.nv, out.nt, out.ncam, out.vis_stride)
+            exp = (meta, out.payload, None)
+        return out.frame_id, bundle, img, exp
+
     n_in = n_out = 0
     try:
         for frames, sils in zip(frames_seq, sils_seq):
-            lane = n_in % lanes
-            d_masks, fb, ev, keep = _prefetch(cams, frames, sils, virtual is not None, copy,
-                                              computes[lane])
-            submit(lane, (frames, d_masks, fb, ev, keep))
+            seq.submit(next(fids), sils, frames if virtual is not None else None)
             n_in += 1
             while n_out < n_in:  # hand back, in order, every frame already done
-                q = out_qs[n_out % lanes]
-                if n_in - n_out > 2 * lanes:  # bound the pinned readbacks in flight
-                    item = q.get()
-                else:
-                    try:
-                        item = q.get_nowait()
-                    except queue.Empty:
-                        break
-                yield finish(item, next(fids))
+                out = seq.next(wait=n_in - n_out > 2 * lanes)  # bound the frames in flight
+                if out is None:
+                    break
                 n_out += 1
-        for k in range(lanes):
-            submit(k, _END)
+                yield finish(out)
         while n_out < n_in:
-            yield finish(out_qs[n_out % lanes].get(), next(fids))
+            out = seq.next(wait=True)
             n_out += 1
+            yield finish(out)
     finally:
-        stop.set()
-        for k in range(lanes):
+        while n_out < n_in:  # closed early or failed: drain (results free themselves)
             try:
-                in_qs[k].put_nowait(_END)
-            except queue.Full:
+                if seq.next(wait=True) is None:
+                    break
+            except Exception:  # noqa: BLE001
                 pass
-        for th in threads:
-            th.join()
-        for st in computes:
-            caller.wait_stream(st)
-        # queued fvv_frame_readback copies write into torch-pinned blocks the
-        # host allocator does not track: finish them before the queue items
-        # (and with them the blocks) can be released and handed out again
-        readback.synchronize()
-        caller.wait_stream(readback)
+            n_out += 1
+        H2D_BYTES["masks"] += seq.h2d_masks - h2d0[0]
+        H2D_BYTES["frames"] += seq.h2d_frames - h2d0[1]
 
 
 def run_sequence_sharded(cfg: PipelineConfig, rig, source, n_frames: int, virtual=None,

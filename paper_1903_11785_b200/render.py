@@ -23,7 +23,7 @@ from .visibility import classify_bits, raster_planes  # noqa: F401  (re-exported
 FALLBACK_COLOR = np.array([128, 128, 128], dtype=np.uint8)  # render.py:19
 
 # host->device bytes of colour frames moved by the render path (bench.py reads it)
-H2D_BYTES = {"frames": 0}
+H2D_BYTES = {"frames": 0, "masks": 0}  # bytes run_sequence moved host->device
 D2H_BYTES = {"results": 0}  # bytes run_sequence read back (pinned blocks)
 
 

@@ -180,6 +180,7 @@ class FrameGather:
         # collective over all ranks: every rank constructs its FrameGather
         self.meta_group = dist.new_group(backend="gloo") if self.nccl else group
         self._streams = None
+        self._inflight = []
         self._device = None
         if self.nccl:
             import torch
@@ -209,7 +210,14 @@ class FrameGather:
                 if ready_event is not None:
                     st.wait_event(ready_event)
                 dist.send(payload, dst, group=self.data_group)
-            payload.record_stream(st)
+                done = torch.cuda.Event()
+                done.record(st)
+            # the payload may be a view of a native sequence result's device
+            # block (not torch-allocated: record_stream cannot guard it):
+            # hold it until its send has completed
+            self._inflight.append((done, payload))
+            while self._inflight and self._inflight[0][0].query():
+                self._inflight.pop(0)
         else:
             dist.send(payload.cpu(), dst, group=self.data_group)
 

@@ -240,7 +240,8 @@ def test_frame_export_roundtrip_matches_run_frame(gpu):
     for (fid, bundle, img, exp), (masks, _, fr) in zip(got, seq):
         assert bundle is None and img is not None
         meta, payload, ev = exp
-        ev.synchronize()
+        if ev is not None:
+            ev.synchronize()
         b = bundle_from_export(meta, payload.cpu(), wl.cfg, wl.rig, fid)
         ref = run_frame(wl.cfg, wl.rig, fr, sils=masks)
         assert b.frame_id == fid and b.stats == ref.stats
