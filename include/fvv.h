@@ -411,6 +411,10 @@ int fvv_seq_submit(fvv_seq *seq, int64_t id, const void *const *mask_src,
 int fvv_seq_next(fvv_seq *seq, int wait, fvv_seq_result **out);
 int fvv_seq_result_get(const fvv_seq_result *res, fvv_seq_result_info *info);
 void fvv_seq_result_free(fvv_seq_result *res);
+/* sizeof of the ABI records (fvv_camera, fvv_grid, fvv_component,
+ * fvv_frame_config, fvv_frame_stats, fvv_frame_outputs, fvv_seq_config,
+ * fvv_seq_result_info) into out[0..n): bindings check their layouts. */
+int fvv_abi_sizes(int64_t *out, int n);
 
 /* ---- harness (not hot path): synthetic scene inputs ------------------------- */
 

@@ -51,7 +51,7 @@ SYMBOLS = (
     "fvv_synth_render", "fvv_erode_cross", "fvv_distance_map", "fvv_background",
     "fvv_extract_silhouette",
     "fvv_seq_create", "fvv_seq_destroy", "fvv_seq_submit", "fvv_seq_next", "fvv_seq_result_get",
-    "fvv_seq_result_free",
+    "fvv_seq_result_free", "fvv_abi_sizes",
 )
 
 FRAME_CONFIG_DTYPE = np.dtype([("stage_lo", "<f8", (3,)), ("stage_hi", "<f8", (3,)),
@@ -82,7 +82,7 @@ class SeqConfig(ctypes.Structure):  # include/fvv.h fvv_seq_config
     _fields_ = [("lanes", ctypes.c_int32), ("readback_flags", ctypes.c_int32),
                 ("has_virtual", ctypes.c_int32), ("export_payload", ctypes.c_int32),
                 ("virt", ctypes.c_uint8 * 192), ("rank_pos", ctypes.c_int32 * FVV_MAX_CAMS),
-                ("fallback", ctypes.c_uint8 * 4)]
+                ("fallback", ctypes.c_uint8 * 4), ("_pad", ctypes.c_uint8 * 4)]  # C: 8-aligned
 
 
 class SeqResultInfo(ctypes.Structure):  # include/fvv.h fvv_seq_result_info

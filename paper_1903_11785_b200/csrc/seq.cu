@@ -566,3 +566,12 @@ void fvv_seq_destroy(fvv_seq *s) {
 }
 
 }  // extern "C"
+
+extern "C" int fvv_abi_sizes(int64_t *out, int n) {
+  const int64_t s[8] = {(int64_t)sizeof(fvv_camera),        (int64_t)sizeof(fvv_grid),
+                        (int64_t)sizeof(fvv_component),     (int64_t)sizeof(fvv_frame_config),
+                        (int64_t)sizeof(fvv_frame_stats),   (int64_t)sizeof(fvv_frame_outputs),
+                        (int64_t)sizeof(fvv_seq_config),    (int64_t)sizeof(fvv_seq_result_info)};
+  for (int i = 0; i < n && i < 8; ++i) out[i] = s[i];
+  return 8;
+}

@@ -36,6 +36,13 @@ def test_record_layouts_match_header():
     assert _lib.CAM_DTYPE.itemsize == 192 and oracle.CAM_DTYPE == _lib.CAM_DTYPE
     assert _lib.GRID_DTYPE.itemsize == 56
     assert _lib.COMP_DTYPE.itemsize == 64
+    # every record the binding builds has the size the compiled library uses
+    sizes = np.zeros(8, dtype=np.int64)
+    assert _lib.load().fvv_abi_sizes(_lib.host_ptr(sizes), 8) == 8
+    assert list(sizes) == [_lib.CAM_DTYPE.itemsize, _lib.GRID_DTYPE.itemsize,
+                           _lib.COMP_DTYPE.itemsize, _lib.FRAME_CONFIG_DTYPE.itemsize,
+                           _lib.FRAME_STATS_DTYPE.itemsize, ctypes.sizeof(_lib.FrameOutputs),
+                           ctypes.sizeof(_lib.SeqConfig), ctypes.sizeof(_lib.SeqResultInfo)]
 
 
 def test_hot_path_refuses_to_run_without_cuda():
