@@ -59,7 +59,6 @@ class FrameOutput:
         self.virtual = virtual
         self.nv, self.nt = int(outs.nv), int(stats["triangles"])
         self.vis_stride = int(outs.vis_stride)
-        self.depth_ptr = outs.depth
         self.component_ids, self.boxes, self.grids, self.info = rois
 
     @property
@@ -92,10 +91,6 @@ class FrameOutput:
         return {k: int(s[k]) for k in ("sparse_tests", "sparse_occupied", "components",
                                        "dense_tests", "dense_occupied", "fallback_edges",
                                        "inconsistent_edge_starts", "triangles")}
-
-    def depth_planes(self, cams):
-        total = sum(c.image_height * c.image_width for c in cams)
-        return _dev(self.depth_ptr, (total,), "<f8")
 
     def to_host_async(self, cams, keep_depths=False, stream=None, compact=False,
                       image_only=False):

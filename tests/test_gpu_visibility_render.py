@@ -2,6 +2,7 @@
 triangle ids, visibility flags, rendered colours and source maps equal the
 reference's golden outputs and the CPU oracle bit for bit."""
 
+import ctypes
 import json
 
 import numpy as np
@@ -233,10 +234,11 @@ def test_run_sequence_matches_golden_frames(gpu):
     masks = torch.from_numpy(np.stack(sils).astype(np.uint8)).pin_memory()
     virtual = G.camera(z, "virtual")
     np_frames = {c.id: z["frames"][i] for i, c in enumerate(rig)}  # pageable: uploaded
-    from paper_1903_11785_b200.pipeline import _zero_copy_frames
+    from paper_1903_11785_b200 import _lib
 
-    assert _zero_copy_frames(rig, frames, []) is not None  # pinned: sampled in place
-    assert _zero_copy_frames(rig, np_frames, []) is None
+    lib = _lib.load()  # pinned frames are sampled in place, pageable ones uploaded
+    assert all(lib.fvv_host_mapped(ctypes.c_void_p(f.data_ptr())) for f in frames.values())
+    assert not any(lib.fvv_host_mapped(ctypes.c_void_p(f.ctypes.data)) for f in np_frames.values())
     out = list(run_sequence(cfg, rig, [frames, np_frames, frames], [masks, masks, sils],
                             virtual))
     assert len(out) == 3
