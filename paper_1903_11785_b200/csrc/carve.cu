@@ -1,10 +1,15 @@
 // B-1 sparse carve / B-3 dense carve (hull.py:78-119, hull.py:287-302).
 //
-// One thread per voxel, 32 consecutive voxels (consecutive i, so their
-// projections land in neighbouring silhouette words) per warp; a warp ballot
-// packs the 32 ON flags into one occupancy word. Every grid of the batch
-// (the coarse stage grid, or all ROI grids) is carved by one launch: blocks
-// are assigned to grids by a prefix table in the parameter block.
+// Work is tiled: 16^3 / 8^3 voxel tiles are first classified per camera
+// from certified bounds at their corners (all-background culls the tile,
+// all-foreground passes the camera for every voxel), then the surviving
+// tiles' voxels are tested against the remaining "mixed" cameras, one thread
+// per voxel. A warp covers 32 voxels of one tile: rows of kT consecutive i
+// (kT = tile edge) in 32 / kT consecutive j; a warp ballot packs the ON flags
+// and one lane per row ORs the row's bits into the occupancy words (one or
+// two 32-bit atomics per row instead of one per ON voxel). Every grid of the
+// batch (the coarse stage grid, or all ROI grids) is carved by one launch:
+// blocks are assigned to grids by a prefix table in the parameter block.
 //
 // Exactness: each (voxel, camera) test is decided either by a certified
 // FP32 evaluation (below) or by the reference's float64 chain
@@ -21,6 +26,9 @@
 namespace fvv {
 
 constexpr int kCarveThreads = 256;
+#ifndef FVV_CARVE_MINB
+#define FVV_CARVE_MINB 6  // resident 256-thread blocks per SM the tile kernels are built for
+#endif
 constexpr int kCarveWordsPerBlock = 128;  // 4096 voxels per block
 constexpr int64_t kAmbCap = 1 << 20;     // deferred-voxel queue entries
 constexpr int64_t kTileCap = 1 << 19;    // split mode: surviving-tile records
@@ -310,14 +318,16 @@ __device__ __forceinline__ int carve_voxels(const CarveParams &p, const CamAffin
   const int kT = 1 << tl;
   const int64_t nx = G.dims[0], ny = G.dims[1];
   int my_on = 0;
+  const int lane = threadIdx.x & 31;
+  // (v1 - v0 and blockDim.x are multiples of 32: whole warps take the loop)
   for (int v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
     const int i = i0 + (v & (kT - 1)), j = j0 + ((v >> tl) & (kT - 1)), k = k0 + (v >> (2 * tl));
-    if (i > i1 || j > j1 || k > k1) continue;
+    const bool inside = i <= i1 && j <= j1 && k <= k1;
     const float fi = (float)i, fj = (float)j, fk = (float)k;
     int seen = n_fg;
-    bool off = false;
+    bool off = !inside;
     unsigned long long amb = 0;
-    for (int m = 0; m < nm; ++m) {
+    for (int m = 0; m < (inside ? nm : 0); ++m) {
       const int c = mixed[m];
       int px, py;
       const int st = classify32(aff[c], fi, fj, fk, px, py);
@@ -333,9 +343,20 @@ __device__ __forceinline__ int carve_voxels(const CarveParams &p, const CamAffin
       }
     }
     const int64_t l = (int64_t)i + nx * ((int64_t)j + ny * (int64_t)k);
-    if (!off && settle(p, G, g, l, seen, amb)) {
-      atomicOr(p.occ + p.word_off[g] + (l >> 5), 1u << (l & 31));
-      ++my_on;
+    const bool on = !off && settle(p, G, g, l, seen, amb);
+    my_on += on;
+    // warp-ballot packing: lane r * kT holds row r's ON bits (consecutive i,
+    // so consecutive linear indices l .. l + kT - 1)
+    const unsigned ballot = __ballot_sync(0xffffffffu, on);
+    if ((lane & (kT - 1)) == 0) {
+      const unsigned rowmask = kT >= 32 ? 0xffffffffu : ((1u << kT) - 1u);
+      const unsigned row = (ballot >> lane) & rowmask;
+      if (row) {
+        uint32_t *w = p.occ + p.word_off[g] + (l >> 5);
+        const int sh = (int)(l & 31);
+        atomicOr(w, row << sh);
+        if (sh + kT > 32 && (row >> (32 - sh))) atomicOr(w + 1, row >> (32 - sh));
+      }
     }
   }
   return my_on;
@@ -345,7 +366,7 @@ __device__ __forceinline__ int carve_voxels(const CarveParams &p, const CamAffin
 // carve its voxels, or (kSplit, the 16^3 stage-grid tiles) append the
 // surviving tile to p.tiles for carve_voxels_kernel.
 template <bool kSplit>
-__global__ void __launch_bounds__(kCarveThreads, 6)
+__global__ void __launch_bounds__(kCarveThreads, FVV_CARVE_MINB)
     carve_kernel(const __grid_constant__ CarveParams p) {
   __shared__ CamAffine aff[FVV_MAX_CAMS];
   __shared__ int state[FVV_MAX_CAMS];
@@ -439,7 +460,7 @@ __global__ void __launch_bounds__(kCarveThreads, 6)
 // octant), which culls like 8^3 tiles do, then its 512 voxels are carved.
 // Launched for every tile; blocks past the surviving count exit.
 template <bool kLoop>
-__global__ void __launch_bounds__(kCarveThreads, 6)
+__global__ void __launch_bounds__(kCarveThreads, FVV_CARVE_MINB)
     carve_voxels_kernel(const __grid_constant__ CarveParams p) {
   __shared__ CamAffine aff[FVV_MAX_CAMS];
   __shared__ int tmixed[FVV_MAX_CAMS], state[FVV_MAX_CAMS], mixed[FVV_MAX_CAMS];
