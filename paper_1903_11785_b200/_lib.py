@@ -43,7 +43,7 @@ SYMBOLS = (
     "fvv_ccl_components", "fvv_ccl_labels", "fvv_filter_labels", "fvv_filter_dense",
     "fvv_mesh_workspace_bytes", "fvv_mesh_prepare", "fvv_mesh_counts",
     "fvv_mesh_emit_scratch_bytes", "fvv_mesh_emit", "fvv_edge_isovalues",
-    "fvv_raster_workspace_bytes", "fvv_rasterize", "fvv_classify", "fvv_triangle_sources",
+    "fvv_raster_workspace_bytes", "fvv_rasterize", "fvv_rasterize_tracked", "fvv_classify", "fvv_triangle_sources",
     "fvv_render_count", "fvv_render_view", "fvv_render_view_coded", "fvv_back_project",
     "fvv_render_ellipsoids",
     "fvv_frame_create", "fvv_frame_destroy", "fvv_frame_run", "fvv_frame_get_outputs",

@@ -41,6 +41,9 @@ int fvv_mesh_emit(const fvv_camera *, int, const uint32_t *, const int64_t *, co
 size_t fvv_raster_workspace_bytes(int64_t, int64_t, int);
 int fvv_rasterize(const fvv_camera *, int, const double *, int64_t, const int32_t *, int64_t,
                   const int64_t *, double *, const int64_t *, int32_t *, void *, size_t, void *);
+int fvv_rasterize_tracked(const fvv_camera *, int, const double *, int64_t, const int32_t *,
+                          int64_t, const int64_t *, double *, const int64_t *, int32_t *, void *,
+                          size_t, uint8_t *, int, void *);
 int fvv_classify(const fvv_camera *, int, const double *, const int32_t *, int64_t,
                  const int64_t *, const double *, const int64_t *, double, uint32_t *, int64_t,
                  void *);
@@ -163,6 +166,12 @@ struct fvv_frame {
   DevBuf sil, occ_c, cnt_c, ccl_ws, comps, ccl_counts, occ_f, cnt_f, mesh_ws, mesh_scratch,
       mesh_totals, mesh_info, verts, tris, ntri, raster_ws, depth, vis, vplane_d, vplane_id,
       vraster_ws, src, rcounts, color, source, covered;
+  // 32-pixel dirty-tile maps of the depth planes and of the virtual view's
+  // depth/id planes: only tiles written by the previous frame are reset
+  DevBuf dirty, vdirty;
+  // the planes (and map allocations) the maps describe
+  const void *dirty_for[2] = {nullptr, nullptr}, *vdirty_for[3] = {nullptr, nullptr, nullptr};
+  int64_t vdirty_px = 0;
   // pinned host staging
   int64_t virt_px = 0;         // pixels of the last colour pass (0: none)
   void *host_small = nullptr;  // mapped pinned block (kHs* layout)
@@ -498,11 +507,17 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
   const bool have_mesh = f->nv > 0 && nt_ub > 0;
   if (have_mesh) {
     FVV_TRY(5, f->depth.ensure(8 * (size_t)f->planes));
+    FVV_TRY(5, f->dirty.ensure((size_t)(f->planes + 31) / 32));
     const size_t rwb = fvv_raster_workspace_bytes(f->nv, nt_ub, ncam);
     FVV_TRY(5, f->raster_ws.ensure(rwb));
-    FVV_TRY(5, fvv_rasterize(f->cams.data(), ncam, f->verts.as<double>(), f->nv,
-                             f->tris.as<int32_t>(), nt_ub, ntri_dev, f->depth.as<double>(),
-                             f->plane_off.data(), nullptr, f->raster_ws.p, f->raster_ws.cap, st));
+    const bool fresh = f->dirty_for[0] != f->depth.p || f->dirty_for[1] != f->dirty.p;
+    FVV_TRY(5, fvv_rasterize_tracked(f->cams.data(), ncam, f->verts.as<double>(), f->nv,
+                                     f->tris.as<int32_t>(), nt_ub, ntri_dev,
+                                     f->depth.as<double>(), f->plane_off.data(), nullptr,
+                                     f->raster_ws.p, f->raster_ws.cap, f->dirty.as<uint8_t>(),
+                                     fresh, st));
+    f->dirty_for[0] = f->depth.p;  // new planes or map: filled once above
+    f->dirty_for[1] = f->dirty.p;
   }
   cudaEventRecord(f->ev[5], st);
   FVV_TRY(6, f->vis.ensure(4 * (size_t)ncam * f->vis_stride));
@@ -528,10 +543,19 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
       const size_t vwb = fvv_raster_workspace_bytes(f->nv, nt_ub, 1);
       FVV_TRY(7, f->vraster_ws.ensure(vwb));
       const int64_t off0 = 0;
-      FVV_TRY(7, fvv_rasterize(virt, 1, f->verts.as<double>(), f->nv, f->tris.as<int32_t>(),
-                               nt_ub, ntri_dev, f->vplane_d.as<double>(), &off0,
-                               f->vplane_id.as<int32_t>(), f->vraster_ws.p, f->vraster_ws.cap,
-                               st));
+      FVV_TRY(7, f->vdirty.ensure((size_t)(np + 31) / 32));
+      // the map is valid for one plane pair at one image size
+      const bool vfresh = f->vdirty_for[0] != f->vplane_d.p || f->vdirty_for[1] != f->vplane_id.p ||
+                          f->vdirty_for[2] != f->vdirty.p || f->vdirty_px != np;
+      FVV_TRY(7, fvv_rasterize_tracked(virt, 1, f->verts.as<double>(), f->nv,
+                                       f->tris.as<int32_t>(), nt_ub, ntri_dev,
+                                       f->vplane_d.as<double>(), &off0, f->vplane_id.as<int32_t>(),
+                                       f->vraster_ws.p, f->vraster_ws.cap,
+                                       f->vdirty.as<uint8_t>(), vfresh, st));
+      f->vdirty_for[0] = f->vplane_d.p;
+      f->vdirty_for[1] = f->vplane_id.p;
+      f->vdirty_for[2] = f->vdirty.p;
+      f->vdirty_px = np;
       std::vector<int32_t> rank_id(ncam);
       for (int r = 0; r < ncam; ++r) rank_id[r] = f->cams[rank_pos[r]].id;
       FVV_TRY(7, f->src.ensure(4 * (size_t)(nt_ub > 0 ? nt_ub : 1)));

@@ -377,10 +377,7 @@ __global__ void __launch_bounds__(128)
 }
 
 // ---- B1: isovalues + vertices (mesh.py:231-272, 332-337) --------------------
-#ifndef FVV_LAMBDA_MINB1
-#define FVV_LAMBDA_MINB1 1
-#endif
-__global__ void __launch_bounds__(128, FVV_LAMBDA_MINB1)
+__global__ void __launch_bounds__(128)
     mesh_lambda_kernel(const __grid_constant__ MeshGrids G, const __grid_constant__ MeshCams C,
                        MeshBufs B, const uint32_t *__restrict__ sil) {
   const int64_t nv = __ldcg(B.totals);
@@ -410,88 +407,6 @@ __global__ void __launch_bounds__(128, FVV_LAMBDA_MINB1)
       lam = G.fixed_iso;
     }
     for (int d = 0; d < 3; ++d) B.verts[3 * v + d] = pon[d] + lam * (poff[d] - pon[d]);
-  }
-}
-
-// B1 as (vertex, camera) work items: a group of GS lanes (GS = the camera
-// count rounded up to a power of two, at most 32) owns one vertex, lane c
-// evaluates cameras c, c + GS, ... (two float64 projections + the
-// Bresenham walk each), and the group reduces (lam_i, camera position)
-// lexicographically (the reference's strict < over ascending ids: the
-// smallest lam, the lowest id among equal ones) plus the inconsistent-start
-// count with xor shuffles. Five million balanced items instead of 326k
-// threads each looping over 16 cameras (C3): the float64 pipe stays fed.
-// Camera records are staged in shared memory (lane-indexed loads from the
-// parameter space would serialise).
-template <int GS>
-#ifndef FVV_LAMBDA_MINB
-#define FVV_LAMBDA_MINB 2
-#endif
-__global__ void __launch_bounds__(256, FVV_LAMBDA_MINB)
-    mesh_lambda_group_kernel(const __grid_constant__ MeshGrids G,
-                             const __grid_constant__ MeshCams C, MeshBufs B,
-                             const uint32_t *__restrict__ sil) {
-  __shared__ fvv_camera s_cam[FVV_MAX_CAMS];
-  __shared__ int64_t s_off[FVV_MAX_CAMS];
-  __shared__ int32_t s_stride[FVV_MAX_CAMS];
-  const int ncam = C.ncam;
-  for (int t = threadIdx.x; t < ncam * (int)(sizeof(fvv_camera) / 8); t += blockDim.x)
-    reinterpret_cast<double *>(s_cam)[t] = reinterpret_cast<const double *>(C.cams)[t];
-  for (int t = threadIdx.x; t < ncam; t += blockDim.x) {
-    s_off[t] = C.sil_off[t];
-    s_stride[t] = C.sil_stride[t];
-  }
-  __syncthreads();
-  const int sub = threadIdx.x & (GS - 1);
-  const int64_t nv = __ldcg(B.totals);
-  const int64_t groups = (int64_t)gridDim.x * (blockDim.x / GS);
-  // every lane of a group runs the same trip count (whole groups share v)
-  for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / GS; v < nv; v += groups) {
-    int axis;
-    int64_t i, j, k;
-    const int g = decode_vkey(G, B.vert_key[v], axis, i, j, k);
-    const MeshGridInfo &gi = G.gi[g];
-    const int64_t q = i * gi.g.dims[1] + j;
-    const bool on = (row_word(B.tw, gi, q, k >> 5) >> (k & 31)) & 1u;
-    double p0[3], p1[3];
-    voxel_center(gi.g, i, j, k, p0[0], p0[1], p0[2]);
-    for (int d = 0; d < 3; ++d) p1[d] = p0[d] + gi.g.spacing * (double)(d == axis);
-    const double *pon = on ? p0 : p1, *poff = on ? p1 : p0;
-    const bool gemv = B.info[8 * g + kInfoV] == 1;  // one-edge batch: numpy gemv order
-    double lam = INFINITY;
-    int sel = ncam;  // camera position of lam (ncam: none qualified)
-    int incons = 0;
-    for (int c = sub; c < ncam; c += GS) {
-      double lam_i;
-      bool inc;
-      if (!edge_lambda_cam(s_cam[c], sil + s_off[c], s_stride[c], pon, poff, gemv, lam_i, inc))
-        continue;
-      incons += inc;
-      if (lam_i < lam) {  // c ascends within a lane: strict < keeps the lower id
-        lam = lam_i;
-        sel = c;
-      }
-    }
-#pragma unroll
-    for (int o = GS / 2; o >= 1; o >>= 1) {
-      const double l2 = __shfl_xor_sync(0xffffffffu, lam, o);
-      const int s2 = __shfl_xor_sync(0xffffffffu, sel, o);
-      incons += __shfl_xor_sync(0xffffffffu, incons, o);
-      if (l2 < lam || (l2 == lam && s2 < sel)) {
-        lam = l2;
-        sel = s2;
-      }
-    }
-    if (sub == 0) {
-      if (sel == ncam) {
-        lam = 0.5;
-        atomicAdd((unsigned long long *)(B.info + 8 * g + kInfoFallback), 1ull);
-      }
-      if (incons)
-        atomicAdd((unsigned long long *)(B.info + 8 * g + kInfoIncons),
-                  (unsigned long long)incons);
-      for (int d = 0; d < 3; ++d) B.verts[3 * v + d] = pon[d] + lam * (poff[d] - pon[d]);
-    }
   }
 }
 
@@ -926,23 +841,11 @@ int fvv_mesh_emit(const fvv_camera *cams_by_id, int ncam, const uint32_t *sil_de
   Slot5 *d_total = (Slot5 *)((char *)ws_dev + L.slot5 + sizeof(int64_t) * 5 * ngrid);
   if (num_vertices > 0) {
     mesh_vertex_list_kernel<<<kMeshGrid, 256, 0, st>>>(h_grids, B);
-#ifndef FVV_LAMBDA_GROUPS
-    if (false) {  // measured slower (profiles/r2_mesh_lambda.md): the per-vertex loop wins
-#else
-    if (exact) {  // (vertex, camera) items, a lane group per vertex
-#endif
-      const int gs = ncam <= 4 ? 4 : ncam <= 8 ? 8 : ncam <= 16 ? 16 : 32;
-      const int64_t lam_blocks = std::min<int64_t>(num_vertices * gs / 256 + 1, 148 * 32);
-      switch (gs) {
-        case 4: mesh_lambda_group_kernel<4><<<(unsigned)lam_blocks, 256, 0, st>>>(h_grids, h_cams, B, sil_dev); break;
-        case 8: mesh_lambda_group_kernel<8><<<(unsigned)lam_blocks, 256, 0, st>>>(h_grids, h_cams, B, sil_dev); break;
-        case 16: mesh_lambda_group_kernel<16><<<(unsigned)lam_blocks, 256, 0, st>>>(h_grids, h_cams, B, sil_dev); break;
-        default: mesh_lambda_group_kernel<32><<<(unsigned)lam_blocks, 256, 0, st>>>(h_grids, h_cams, B, sil_dev); break;
-      }
-    } else {  // fixed isovalue: one vertex per thread
-      const int64_t lam_blocks = std::min<int64_t>(num_vertices / 128 + 1, 148 * 64);
-      mesh_lambda_kernel<<<(unsigned)lam_blocks, 128, 0, st>>>(h_grids, h_cams, B, sil_dev);
-    }
+    // one vertex per thread, cameras in a loop; measured against (vertex,
+    // camera) lane groups and a certified-FP32 endpoint projection with the
+    // float64 terms deferred to full warps, both slower
+    const int64_t lam_blocks = std::min<int64_t>(num_vertices / 128 + 1, 148 * 64);
+    mesh_lambda_kernel<<<(unsigned)lam_blocks, 128, 0, st>>>(h_grids, h_cams, B, sil_dev);
     note_launches(2);
   }
   if (num_cells > 0) {

@@ -128,11 +128,14 @@ __device__ __forceinline__ bool tri_depth(const TriSetup &s, int x, int y, doubl
   return d < INFINITY;  // only finite depths can beat the +inf background
 }
 
+// p: the pixel's element index in the depth buffer (its dirty tile is p / 32)
 __device__ __forceinline__ void pixel_update(int pass, double d, int64_t t,
-                                             unsigned long long *depth, unsigned *ids) {
+                                             unsigned long long *depth, unsigned *ids,
+                                             uint8_t *dirty, int64_t p) {
   const unsigned long long bits = (unsigned long long)__double_as_longlong(d);
   if (pass == 0) {
     atomicMin(depth, bits);  // result unused -> RED.MIN (no round trip)
+    if (dirty) dirty[p >> 5] = 1;
   } else if (bits == __ldcg(depth)) {
     atomicMin(ids, (unsigned)t);
   }
@@ -155,6 +158,7 @@ struct RasterArgs {
   // filter warp sees, so the item lists cannot overflow; a full pair list
   // sets *overflow and the sweep kernel then redoes every item
   int64_t nwl, wl_items, wl_pairs;
+  uint8_t *dirty;     // optional: per 32-pixel tile of the planes, set when a depth is written
   uint32_t *slow;     // items the FP32 filter leaves to the warp-sweep kernel
   uint2 *pairs;       // (item, y << 16 | x): candidate pixels from the FP32 filter
   int *wcount;        // [nwl][2]: pairs, items
@@ -451,7 +455,7 @@ __global__ void __launch_bounds__(256)
       if (!tri_depth(s, x, y, d)) continue;
       const int64_t p = C.depth_off[c] + (int64_t)y * width + x;
       pixel_update(A.pass, d, t, (unsigned long long *)A.depth + p,
-                   A.ids ? (unsigned *)A.ids + p : nullptr);
+                   A.ids ? (unsigned *)A.ids + p : nullptr, A.dirty, p);
     }
   }
 }
@@ -565,7 +569,8 @@ __global__ void __launch_bounds__(kRasterThreads, 8)
           unsigned long long *dp = (unsigned long long *)(A.depth + C.depth_off[m.cam]);
           unsigned *ip = (unsigned *)(A.ids ? A.ids + C.depth_off[m.cam] : nullptr);
           const int64_t pxl = (int64_t)y * W + x;
-          pixel_update(A.pass, d, m.t, dp + pxl, ip ? ip + pxl : nullptr);
+          pixel_update(A.pass, d, m.t, dp + pxl, ip ? ip + pxl : nullptr, A.dirty,
+                       C.depth_off[m.cam] + pxl);
         }
       }
     }
@@ -594,7 +599,7 @@ __global__ void __launch_bounds__(kBigThreads)
       double d;
       if (!tri_depth(s, x, y, d)) continue;
       const int64_t p = (int64_t)y * width + x;
-      pixel_update(A.pass, d, t, dp + p, ip ? ip + p : nullptr);
+      pixel_update(A.pass, d, t, dp + p, ip ? ip + p : nullptr, A.dirty, C.depth_off[c] + p);
     }
   }
 }
@@ -610,16 +615,54 @@ __device__ __forceinline__ void fill_u64(unsigned long long *p, int64_t n, unsig
   if (tid == 0 && head + 2 * n2 < n) p[head + 2 * n2] = v;
 }
 
-// D-1 preparation in one launch: the first nb_fill blocks fill the depth
-// planes with +inf (HBM-bound), the others project the vertices (FP64-bound),
-// so the two overlap instead of running back to back.
+// Background reset of tracked planes: every 32-pixel tile whose flag the
+// previous raster into these planes set goes back to +inf depth (and -1 ids),
+// and its flag is cleared. The other tiles still hold the background, so
+// only the pixels written last time are rewritten.
+__device__ __forceinline__ void reset_dirty(unsigned long long *depth, int32_t *ids,
+                                            uint8_t *dirty, int64_t npx, int64_t tid,
+                                            int64_t stride) {
+  const int64_t ntile = (npx + 31) >> 5;
+  for (int64_t f = tid; f < ntile; f += stride) {
+    if (!dirty[f]) continue;
+    const int64_t p0 = f << 5, n = npx - p0 < 32 ? npx - p0 : 32;
+    if (n == 32 && ((uintptr_t)(depth + p0) & 15) == 0) {
+      ulonglong2 *q = (ulonglong2 *)(depth + p0);
+      const ulonglong2 inf2 = make_ulonglong2(0x7ff0000000000000ull, 0x7ff0000000000000ull);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) q[i] = inf2;
+    } else {
+      for (int64_t i = 0; i < n; ++i) depth[p0 + i] = 0x7ff0000000000000ull;
+    }
+    if (ids) {
+      if (n == 32 && ((uintptr_t)(ids + p0) & 15) == 0) {
+        int4 *q = (int4 *)(ids + p0);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) q[i] = make_int4(-1, -1, -1, -1);
+      } else {
+        for (int64_t i = 0; i < n; ++i) ids[p0 + i] = -1;
+      }
+    }
+    dirty[f] = 0;
+  }
+}
+
+// D-1 preparation in one launch: the first nb_fill blocks bring the depth
+// planes back to the +inf background (a full fill, or with a dirty map only
+// the tiles the last raster wrote; HBM-bound), the others project the
+// vertices (FP64-bound), so the two overlap instead of running back to back.
 __global__ void raster_prep_kernel(const __grid_constant__ RasterCams C,
                                    const double *__restrict__ V, int64_t nv,
                                    double4 *__restrict__ proj, float2 *__restrict__ q,
-                                   unsigned long long *depth, int64_t npx, int nb_fill) {
+                                   unsigned long long *depth, int32_t *ids, uint8_t *dirty,
+                                   int64_t npx, int nb_fill) {
   if ((int)blockIdx.x < nb_fill) {
-    fill_u64(depth, npx, 0x7ff0000000000000ull, blockIdx.x * (int64_t)blockDim.x + threadIdx.x,
-             (int64_t)nb_fill * blockDim.x);
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)nb_fill * blockDim.x;
+    if (dirty)
+      reset_dirty(depth, ids, dirty, npx, tid, stride);
+    else
+      fill_u64(depth, npx, 0x7ff0000000000000ull, tid, stride);
     return;
   }
   const bool gemv = nv == 1;
@@ -912,10 +955,15 @@ size_t fvv_raster_workspace_bytes(int64_t num_vertices, int64_t num_triangles, i
   return raster_layout(num_vertices, num_triangles, ncam).total;
 }
 
-int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int64_t nv,
-                  const int32_t *tris_dev, int64_t nt, const int64_t *nt_dev, double *depth_dev,
-                  const int64_t *plane_off, int32_t *tri_id_dev, void *ws_dev, size_t ws_bytes,
-                  void *stream) {
+// dirty == nullptr: the planes are filled with the background here.
+// dirty != nullptr (contiguous planes only): the planes already hold the
+// background except the 32-pixel tiles flagged in dirty[], which are reset;
+// full_reset fills everything and clears the flags instead (first use).
+static int rasterize_impl(const fvv_camera *cams, int ncam, const double *verts_dev, int64_t nv,
+                          const int32_t *tris_dev, int64_t nt, const int64_t *nt_dev,
+                          double *depth_dev, const int64_t *plane_off, int32_t *tri_id_dev,
+                          void *ws_dev, size_t ws_bytes, uint8_t *dirty, bool full_reset,
+                          cudaStream_t st) {
   static thread_local RasterCams C;
   int rc = fill_cams(C, cams, ncam, plane_off);
   if (rc) return rc;
@@ -930,7 +978,6 @@ int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int
     set_error("fvv_rasterize: %lld triangles x %d cameras exceeds 2^32 - 1", (long long)nt, ncam);
     return FVV_E_LIMIT;
   }
-  cudaStream_t st = (cudaStream_t)stream;
   // background: depth +inf, id -1 (visibility.py:44-45); one fill when the
   // planes are contiguous (the executor's layout), else one per camera
   bool contiguous = true;
@@ -939,9 +986,15 @@ int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int
     contiguous = contiguous && plane_off[c] == plane_off[0] + total_px;
     total_px += (int64_t)cams[c].width * cams[c].height;
   }
-  // contiguous planes with a mesh: the fill rides in the vertex-projection
-  // launch (raster_prep_kernel); otherwise fill here
-  const bool fused_fill = contiguous && nt > 0 && nv > 0;
+  if (dirty && !contiguous) {
+    set_error("fvv_rasterize_tracked: planes must be contiguous");
+    return FVV_E_ARG;
+  }
+  if (dirty && full_reset) cudaMemsetAsync(dirty, 0, (size_t)((total_px + 31) >> 5), st);
+  const bool tracked = dirty && !full_reset;
+  // contiguous planes: the fill (or tracked reset) rides in the
+  // vertex-projection launch (raster_prep_kernel); otherwise fill here
+  const bool fused_fill = contiguous;
   for (int c = 0; c < (contiguous ? 1 : ncam); ++c) {
     const int64_t n = contiguous ? total_px : (int64_t)cams[c].width * cams[c].height;
     if (!fused_fill) {
@@ -949,22 +1002,45 @@ int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int
                                                n, 0x7ff0000000000000ull);
       note_launches(1);
     }
-    if (tri_id_dev) cudaMemsetAsync(tri_id_dev + plane_off[c], 0xff, 4 * n, st);
+    if (tri_id_dev && !tracked) cudaMemsetAsync(tri_id_dev + plane_off[c], 0xff, 4 * n, st);
   }
-  if (nt <= 0) return cuda_check("fvv_rasterize");
+  const bool work = nt > 0 && nv > 0;
   const RasterLayout L = raster_layout(nv, nt, ncam);
-  if (ws_bytes < L.total) {
+  if (work && ws_bytes < L.total) {
     set_error("fvv_rasterize: workspace %zu < %zu bytes", ws_bytes, L.total);
     return FVV_E_ARG;
   }
   char *ws = (char *)ws_dev;
+  if (fused_fill) {
+    double4 *proj = work ? (double4 *)(ws + L.proj) : nullptr;
+    float2 *q = work ? (float2 *)(ws + L.q) : nullptr;
+    int64_t blocks = work ? (nv * ncam + 255) / 256 : 0;
+    if (blocks > kRasterGrid) blocks = kRasterGrid;
+    // fill blocks in proportion to the bytes they write (~0.3 us of work per
+    // block); a tracked reset reads one flag per 32 pixels
+    int64_t nb_fill = tracked ? total_px / (256 * 32 * 8) + 1 : total_px / (256 * 64) + 1;
+    if (nb_fill > 148 * 8) nb_fill = 148 * 8;
+    raster_prep_kernel<<<(int)(blocks + nb_fill), 256, 0, st>>>(
+        C, verts_dev, work ? nv : 0, proj, q, (unsigned long long *)(depth_dev + plane_off[0]),
+        tracked ? tri_id_dev + plane_off[0] : nullptr, tracked ? dirty : nullptr, total_px,
+        (int)nb_fill);
+    note_launches(1);
+  } else if (work) {
+    int64_t blocks = (nv * ncam + 255) / 256;
+    if (blocks > kRasterGrid) blocks = kRasterGrid;
+    raster_vertex_kernel<<<(int)blocks, 256, 0, st>>>(C, verts_dev, nv, (double4 *)(ws + L.proj),
+                                                     (float2 *)(ws + L.q));
+    note_launches(1);
+  }
+  if (!work) return cuda_check("fvv_rasterize");
   RasterArgs A;
   A.T = tris_dev;
   A.nt = nt;
   A.nt_dev = nt_dev;
   A.nv = nv;
-  A.depth = depth_dev;
-  A.ids = tri_id_dev;
+  A.depth = depth_dev + (dirty ? plane_off[0] : 0);
+  A.ids = tri_id_dev ? tri_id_dev + (dirty ? plane_off[0] : 0) : nullptr;
+  A.dirty = dirty;
   A.qcount = (int64_t *)ws;
   const FilterShape fs = filter_shape(nt, ncam);
   A.overflow = (int *)(ws + 8);
@@ -978,29 +1054,11 @@ int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int
   A.Q = (const float2 *)(ws + L.q);
   A.slow = (uint32_t *)(ws + L.slow);
   A.pairs = (uint2 *)(ws + L.pairs);
+  if (dirty)  // planes addressed relative to plane 0 (the dirty map's origin)
+    for (int c = 0; c < ncam; ++c) C.depth_off[c] = plane_off[c] - plane_off[0];
   cudaMemsetAsync(ws, 0, 16, st);  // big-queue counter, overflow flag
-  {
-    double4 *proj = (double4 *)(ws + L.proj);
-    float2 *q = (float2 *)(ws + L.q);
-    int64_t blocks = (nv * ncam + 255) / 256;
-    if (blocks > kRasterGrid) blocks = kRasterGrid;
-    if (blocks < 1) blocks = 1;
-    if (fused_fill) {
-      // fill blocks in proportion to the bytes they write (~0.3 us of work per block)
-      int64_t nb_fill = total_px / (256 * 64) + 1;
-      if (nb_fill > 148 * 8) nb_fill = 148 * 8;
-      raster_prep_kernel<<<(int)(blocks + nb_fill), 256, 0, st>>>(
-          C, verts_dev, nv, proj, q, (unsigned long long *)(depth_dev + plane_off[0]), total_px,
-          (int)nb_fill);
-    } else {
-      raster_vertex_kernel<<<(int)blocks, 256, 0, st>>>(C, verts_dev, nv, proj, q);
-    }
-    note_launches(1);
-  }
-  {
-    raster_filter_kernel<<<(unsigned)fs.bx, 256, 0, st>>>(C, A);
-    note_launches(1);
-  }
+  raster_filter_kernel<<<(unsigned)fs.bx, 256, 0, st>>>(C, A);
+  note_launches(1);
   // pass 0: depth (RED.MIN of the depth bits); pass 1 (ids wanted): the
   // lowest triangle id reaching the final depth, over the same work lists
   for (int pass = 0; pass < (tri_id_dev ? 2 : 1); ++pass) {
@@ -1011,6 +1069,28 @@ int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int
     note_launches(3);
   }
   return cuda_check("fvv_rasterize");
+}
+
+int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int64_t nv,
+                  const int32_t *tris_dev, int64_t nt, const int64_t *nt_dev, double *depth_dev,
+                  const int64_t *plane_off, int32_t *tri_id_dev, void *ws_dev, size_t ws_bytes,
+                  void *stream) {
+  return rasterize_impl(cams, ncam, verts_dev, nv, tris_dev, nt, nt_dev, depth_dev, plane_off,
+                        tri_id_dev, ws_dev, ws_bytes, nullptr, false, (cudaStream_t)stream);
+}
+
+int fvv_rasterize_tracked(const fvv_camera *cams, int ncam, const double *verts_dev, int64_t nv,
+                          const int32_t *tris_dev, int64_t nt, const int64_t *nt_dev,
+                          double *depth_dev, const int64_t *plane_off, int32_t *tri_id_dev,
+                          void *ws_dev, size_t ws_bytes, uint8_t *dirty_dev, int full_reset,
+                          void *stream) {
+  if (!dirty_dev) {
+    set_error("fvv_rasterize_tracked: dirty map required");
+    return FVV_E_ARG;
+  }
+  return rasterize_impl(cams, ncam, verts_dev, nv, tris_dev, nt, nt_dev, depth_dev, plane_off,
+                        tri_id_dev, ws_dev, ws_bytes, dirty_dev, full_reset != 0,
+                        (cudaStream_t)stream);
 }
 
 int fvv_classify(const fvv_camera *cams, int ncam, const double *verts_dev,
