@@ -118,4 +118,37 @@ __device__ __forceinline__ int64_t device_count(const int64_t *p, int64_t fallba
   return v;
 }
 
+// Grid table of one batched carve launch, in device memory (written by the
+// host wrapper's store launch, or on the device by the frame planner):
+// block b of the tile kernels carves tile b - blk_start[g] of the grid g
+// with blk_start[g] <= b < blk_start[g + 1].
+struct __align__(16) CarveGrids {
+  int ngrid, tile_log2;
+  int64_t total_tiles;  // blk_start[ngrid]
+  fvv_grid grids[FVV_MAX_GRIDS];
+  int64_t word_off[FVV_MAX_GRIDS];
+  int64_t blk_start[FVV_MAX_GRIDS + 1];
+  uint32_t tiles_x[FVV_MAX_GRIDS], tiles_y[FVV_MAX_GRIDS];
+};
+
+// Tiles of a grid at tile edge 1 << tl; false when the grid has no voxels.
+__host__ __device__ inline bool carve_grid_tiles(const fvv_grid &g, int tl, uint32_t &tx,
+                                                 uint32_t &ty, int64_t &tiles) {
+  const int64_t kT = (int64_t)1 << tl;
+  if (g.dims[0] <= 0 || g.dims[1] <= 0 || g.dims[2] <= 0) return false;
+  tx = (uint32_t)((g.dims[0] + kT - 1) / kT);
+  ty = (uint32_t)((g.dims[1] + kT - 1) / kT);
+  tiles = (int64_t)tx * ty * ((g.dims[2] + kT - 1) / kT);
+  return true;
+}
+
+// B-1 / B-3 carve of the grids in *gt (device) - the body of fvv_carve.
+// ngrid_max bounds gt->ngrid and blocks_cap the tile count (device-planned
+// batches: capacities; blocks past gt->total_tiles exit).
+int carve_batch(const fvv_camera *cams, int ncam, const uint32_t *sil_dev,
+                const int64_t *sil_word_off, const CarveGrids *gt_dev, int ngrid_max,
+                int tile_log2, int64_t blocks_cap, int min_views, uint32_t *occ_dev,
+                int64_t *count_dev, void *workspace, size_t ws_bytes, cudaStream_t st);
+size_t carve_grids_offset(const fvv_camera *cams, int ncam);  // table slot in the workspace
+
 }  // namespace fvv
