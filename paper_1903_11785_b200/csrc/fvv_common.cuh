@@ -151,4 +151,54 @@ int carve_batch(const fvv_camera *cams, int ncam, const uint32_t *sil_dev,
                 int64_t *count_dev, void *workspace, size_t ws_bytes, cudaStream_t st);
 size_t carve_grids_offset(const fvv_camera *cams, int ncam);  // table slot in the workspace
 
+// Grid table of one batched polygonize (mesh.cu), in device memory: grid g's
+// occupancy transposed into k-rows occupies words [tw_start[g], tw_start[g+1]).
+struct MeshGridInfo {
+  fvv_grid g;
+  int64_t occ_word_off;  // F-order occupancy words of this grid
+  int64_t rows, nzw;     // rows = nx*ny (0 when a dim < 2: empty mesh, mesh.py:298-299)
+  int64_t tw_off;        // transposed-word offset (S space); V space offset = 3*tw_off
+  uint32_t words32, nzw32, ny32, pad;  // rows*nzw, nzw, ny (3*tw_total < 2^31)
+};
+
+struct __align__(16) MeshGrids {
+  int ngrid, pad;
+  int64_t tw_total, tw3;  // k-row words of the batch, and 3x (the edge scan's length)
+  int64_t tw_start[FVV_MAX_GRIDS + 1];  // prefix of rows*nzw
+  MeshGridInfo gi[FVV_MAX_GRIDS];
+};
+
+// grid info at k-row word offset acc; returns the grid's k-row words
+__host__ __device__ inline int64_t mesh_grid_info(const fvv_grid &g, int64_t word_off,
+                                                  int64_t acc, MeshGridInfo &gi) {
+  gi.g = g;
+  gi.occ_word_off = word_off;
+  const int64_t nx = g.dims[0], ny = g.dims[1], nz = g.dims[2];
+  const bool meshable = nx >= 2 && ny >= 2 && nz >= 2;  // mesh.py:298-299
+  gi.rows = meshable ? nx * ny : 0;
+  gi.nzw = meshable ? (nz + 31) / 32 : 1;
+  gi.tw_off = acc;
+  gi.words32 = (uint32_t)(gi.rows * gi.nzw);
+  gi.nzw32 = (uint32_t)gi.nzw;
+  gi.ny32 = (uint32_t)ny;
+  gi.pad = 0;
+  return gi.rows * gi.nzw;
+}
+
+// C polygonize of the grids in *G_dev (device) - the bodies of
+// fvv_mesh_prepare / fvv_mesh_emit. tw_cap / ngrid_max bound the batch's
+// k-row words and grids (the workspace layout); cap_v / cap_s the vertex and
+// surface-cell counts phase B has room for (a batch beyond them skips phase B).
+size_t mesh_ws_bytes(int64_t tw_cap, int ngrid_max);
+int64_t *mesh_ws_totals(void *ws, int64_t tw_cap, int ngrid_max);  // V, S, T
+int64_t *mesh_ws_info(void *ws, int64_t tw_cap, int ngrid_max);    // [ngrid][8]
+int mesh_prepare_batch(const MeshGrids *G_dev, int64_t tw_cap, int ngrid_max,
+                       const uint32_t *occ_dev, void *ws_dev, size_t ws_bytes, cudaStream_t st);
+size_t mesh_emit_scratch(int64_t cap_v, int64_t cap_s);
+int mesh_emit_batch(const fvv_camera *cams_by_id, int ncam, const uint32_t *sil_dev,
+                    const int64_t *sil_word_off, const MeshGrids *G_dev, int64_t tw_cap,
+                    int ngrid_max, int exact, double fixed_iso, void *ws_dev, size_t ws_bytes,
+                    int64_t cap_v, int64_t cap_s, void *scratch_dev, size_t scratch_bytes,
+                    double *verts_dev, int32_t *tris_dev, cudaStream_t st);
+
 }  // namespace fvv

@@ -34,22 +34,6 @@ __constant__ unsigned char c_edge_base[12][4] = {
     {0, 0, 0, 0}, {1, 0, 0, 1}, {0, 1, 0, 0}, {0, 0, 0, 1}, {0, 0, 1, 0}, {1, 0, 1, 1},
     {0, 1, 1, 0}, {0, 0, 1, 1}, {0, 0, 0, 2}, {1, 0, 0, 2}, {1, 1, 0, 2}, {0, 1, 0, 2}};
 
-struct MeshGridInfo {
-  fvv_grid g;
-  int64_t occ_word_off;  // F-order occupancy words of this grid
-  int64_t rows, nzw;     // rows = nx*ny (0 when a dim < 2: empty mesh, mesh.py:298-299)
-  int64_t tw_off;        // transposed-word offset (S space); V space offset = 3*tw_off
-  uint32_t words32, nzw32, ny32, pad;  // rows*nzw, nzw, ny (3*tw_total < 2^31)
-};
-
-struct MeshGrids {
-  int ngrid, exact;
-  double fixed_iso;
-  int64_t tw_total;
-  int64_t tw_start[FVV_MAX_GRIDS + 1];  // prefix of rows*nzw
-  MeshGridInfo gi[FVV_MAX_GRIDS];
-};
-
 struct MeshBufs {
   const uint32_t *occ;
   uint32_t *tw;        // transposed words [tw_total]
@@ -69,7 +53,13 @@ struct MeshBufs {
   int64_t *cell_sums;
   double *verts;       // [V][3]
   int32_t *tris;       // [T][3] global vertex indices
+  int64_t cap_v, cap_s;  // phase-B capacities (emit kernels skip a batch that exceeds them)
 };
+
+// phase B runs only when the counts fit the buffers it was given
+__device__ __forceinline__ bool emit_fits(const MeshBufs &B) {
+  return __ldcg(B.totals) <= B.cap_v && __ldcg(B.totals + 1) <= B.cap_s;
+}
 
 enum { kInfoVbase, kInfoV, kInfoSbase, kInfoS, kInfoTbase, kInfoT, kInfoFallback, kInfoIncons };
 
@@ -95,7 +85,8 @@ __device__ __forceinline__ uint32_t row_next(const uint32_t *tw, const MeshGridI
 }
 
 // ---- A1: transpose F-order occupancy into k-rows --------------------------
-__global__ void mesh_transpose_kernel(const __grid_constant__ MeshGrids G, MeshBufs B) {
+__global__ void mesh_transpose_kernel(const MeshGrids *__restrict__ Gp, MeshBufs B) {
+  const MeshGrids &G = *Gp;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < G.tw_total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int g = grid_of(G, e);
@@ -136,12 +127,13 @@ __device__ __forceinline__ int grid_of_scaled(const MeshGrids &G, int64_t e, int
 // One scan element = one word; decoded with 32-bit arithmetic (fill_grids
 // bounds 3*tw_total below 2^31).
 struct EdgeFlags {
-  MeshGrids G;
+  const MeshGrids *Gp;
   const uint32_t *tw;
   uint32_t *eflags;
   int32_t *vprefix;
   typedef uint32_t Item;
   __device__ uint32_t load(int64_t e) const {
+    const MeshGrids &G = *Gp;
     // V space: grid g occupies [3*tw_start[g], 3*tw_start[g+1]), axis-major
     const int g = grid_of_scaled(G, e, 3);
     const MeshGridInfo &gi = G.gi[g];
@@ -169,12 +161,13 @@ struct EdgeFlags {
 
 // ---- A3: surface-cell scan over (grid, row, word) ---------------------------
 struct CellFlags {
-  MeshGrids G;
+  const MeshGrids *Gp;
   const uint32_t *tw;
   uint32_t *sflags;
   int32_t *sprefix;
   typedef uint32_t Item;
   __device__ uint32_t load(int64_t e) const {
+    const MeshGrids &G = *Gp;
     const int g = grid_of_scaled(G, e, 1);
     const MeshGridInfo &gi = G.gi[g];
     const uint32_t rw = (uint32_t)(e - G.tw_start[g]);
@@ -203,7 +196,8 @@ struct CellFlags {
 };
 
 // per-grid vertex / surface-cell bases and counts (prefix at grid starts)
-__global__ void mesh_grid_counts_kernel(const __grid_constant__ MeshGrids G, MeshBufs B) {
+__global__ void mesh_grid_counts_kernel(const MeshGrids *__restrict__ Gp, MeshBufs B) {
+  const MeshGrids &G = *Gp;
   for (int g = threadIdx.x; g < G.ngrid; g += blockDim.x) {
     const int64_t s0 = G.tw_start[g], s1 = G.tw_start[g + 1];
     const int64_t vb = (3 * s0 < 3 * G.tw_total) ? B.vprefix[3 * s0] : B.totals[0];
@@ -223,7 +217,9 @@ __global__ void mesh_grid_counts_kernel(const __grid_constant__ MeshGrids G, Mes
 }
 
 // ---- B0: vertex list ----------------------------------------------------------
-__global__ void mesh_vertex_list_kernel(const __grid_constant__ MeshGrids G, MeshBufs B) {
+__global__ void mesh_vertex_list_kernel(const MeshGrids *__restrict__ Gp, MeshBufs B) {
+  const MeshGrids &G = *Gp;
+  if (!emit_fits(B)) return;
   const int64_t n = 3 * G.tw_total;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -378,8 +374,11 @@ __global__ void __launch_bounds__(128)
 
 // ---- B1: isovalues + vertices (mesh.py:231-272, 332-337) --------------------
 __global__ void __launch_bounds__(128)
-    mesh_lambda_kernel(const __grid_constant__ MeshGrids G, const __grid_constant__ MeshCams C,
-                       MeshBufs B, const uint32_t *__restrict__ sil) {
+    mesh_lambda_kernel(const MeshGrids *__restrict__ Gp, const __grid_constant__ MeshCams C,
+                       MeshBufs B, const uint32_t *__restrict__ sil, int exact,
+                       double fixed_iso) {
+  const MeshGrids &G = *Gp;
+  if (!emit_fits(B)) return;
   const int64_t nv = __ldcg(B.totals);
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv;
        v += (int64_t)gridDim.x * blockDim.x) {
@@ -394,7 +393,7 @@ __global__ void __launch_bounds__(128)
     for (int d = 0; d < 3; ++d) p1[d] = p0[d] + gi.g.spacing * (double)(d == axis);
     const double *pon = on ? p0 : p1, *poff = on ? p1 : p0;
     double lam;
-    if (G.exact) {
+    if (exact) {
       const bool gemv = B.info[8 * g + kInfoV] == 1;  // one-edge batch: numpy gemv order
       int sel, incons;
       lam = edge_lambda(C, sil, pon, poff, gemv, sel, incons);
@@ -404,7 +403,7 @@ __global__ void __launch_bounds__(128)
         atomicAdd((unsigned long long *)(B.info + 8 * g + kInfoIncons),
                   (unsigned long long)incons);
     } else {
-      lam = G.fixed_iso;
+      lam = fixed_iso;
     }
     for (int d = 0; d < 3; ++d) B.verts[3 * v + d] = pon[d] + lam * (poff[d] - pon[d]);
   }
@@ -478,7 +477,10 @@ __device__ __forceinline__ void mesh_cell(const MeshGrids &G, const MeshBufs &B,
 // words, scans their popcounts, and hands the cells out one per lane (owner
 // word by a shuffle binary search, then the n-th set bit), so sparse words
 // do not leave lanes idle.
-__global__ void mesh_cells_kernel(const __grid_constant__ MeshGrids G, MeshBufs B) {
+__global__ void mesh_cells_kernel(const MeshGrids *__restrict__ Gp, MeshBufs B) {
+  const MeshGrids &G = *Gp;
+  if (!emit_fits(B)) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) B.totals[3] = __ldcg(B.totals + 1);  // tri-scan length
   const int lane = threadIdx.x & 31;
   for (int64_t e0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; e0 < G.tw_total;
        e0 += (int64_t)gridDim.x * blockDim.x) {
@@ -551,8 +553,10 @@ struct TriScan {
 };
 
 // ---- B4: per-grid slot bases (one warp, a lane per grid) ---------------------
-__global__ void mesh_slot_bases_kernel(const __grid_constant__ MeshGrids G, MeshBufs B,
+__global__ void mesh_slot_bases_kernel(const MeshGrids *__restrict__ Gp, MeshBufs B,
                                        const Slot5 *total) {
+  const MeshGrids &G = *Gp;
+  if (!emit_fits(B)) return;
   if (blockIdx.x != 0) return;
   const int lane = threadIdx.x & 31;
   const int64_t S = B.totals[1];
@@ -592,7 +596,9 @@ __global__ void mesh_slot_bases_kernel(const __grid_constant__ MeshGrids G, Mesh
 }
 
 // ---- B5: triangle emission ----------------------------------------------------
-__global__ void mesh_emit_kernel(const __grid_constant__ MeshGrids G, MeshBufs B) {
+__global__ void mesh_emit_kernel(const MeshGrids *__restrict__ Gp, MeshBufs B) {
+  const MeshGrids &G = *Gp;
+  if (!emit_fits(B)) return;
   const int64_t S = __ldcg(B.totals + 1);
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < S;
        c += (int64_t)gridDim.x * blockDim.x) {
@@ -632,9 +638,10 @@ constexpr int kMeshGrid = 148 * 8;
 static size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
 
 struct PrepLayout {
-  size_t tw, eflags, vprefix, sflags, sprefix, sums, totals, info, slot5, cell_sums, total;
+  size_t tw, eflags, vprefix, sflags, sprefix, sums, totals, info, slot5, grids, total;
 };
 
+// workspace of a batch of up to ngrid grids and tw_total k-row words
 static PrepLayout prep_layout(int64_t tw_total, int ngrid) {
   PrepLayout L;
   size_t off = 0;
@@ -649,50 +656,12 @@ static PrepLayout prep_layout(int64_t tw_total, int ngrid) {
   L.sflags = take(4 * (size_t)tw_total);
   L.sprefix = take(4 * (size_t)tw_total);
   L.sums = take(onepass_bytes<int64_t>(3 * tw_total + 1));  // scan status words
-  L.totals = take(8 * 4);
+  L.totals = take(8 * 4);  // V, S, T, S for the triangle scan (0: phase B skipped)
   L.info = take(8 * 8 * (size_t)(ngrid > 0 ? ngrid : 1));
   L.slot5 = take(sizeof(int64_t) * 5 * (size_t)(ngrid > 0 ? ngrid : 1) + sizeof(Slot5));
-  L.cell_sums = 0;
+  L.grids = take(sizeof(MeshGrids));  // the host wrappers' grid table
   L.total = off;
   return L;
-}
-
-static thread_local MeshGrids h_grids;
-
-static int fill_grids(const fvv_grid *grids, int ngrid, const int64_t *word_off, int exact,
-                      double fixed_iso) {
-  if (ngrid < 1 || ngrid > FVV_MAX_GRIDS) {
-    set_error("mesh: %d grids (1..%d)", ngrid, FVV_MAX_GRIDS);
-    return FVV_E_LIMIT;
-  }
-  memset(&h_grids, 0, sizeof(h_grids));
-  h_grids.ngrid = ngrid;
-  h_grids.exact = exact;
-  h_grids.fixed_iso = fixed_iso;
-  int64_t acc = 0;
-  for (int g = 0; g < ngrid; ++g) {
-    MeshGridInfo &gi = h_grids.gi[g];
-    gi.g = grids[g];
-    gi.occ_word_off = word_off[g];
-    const int64_t nx = grids[g].dims[0], ny = grids[g].dims[1], nz = grids[g].dims[2];
-    const bool meshable = nx >= 2 && ny >= 2 && nz >= 2;  // mesh.py:298-299
-    gi.rows = meshable ? nx * ny : 0;
-    gi.nzw = meshable ? (nz + 31) / 32 : 1;
-    gi.tw_off = acc;
-    gi.words32 = (uint32_t)(gi.rows * gi.nzw);
-    gi.nzw32 = (uint32_t)gi.nzw;
-    gi.ny32 = (uint32_t)ny;
-    h_grids.tw_start[g] = acc;
-    acc += gi.rows * gi.nzw;
-    if (3 * acc >= (int64_t)1 << 31) {  // 32-bit word indices (and int32 vertex prefixes)
-      set_error("mesh: %lld occupancy words over the batch (limit %lld)", (long long)acc,
-                (long long)((((int64_t)1 << 31) - 1) / 3));
-      return FVV_E_LIMIT;
-    }
-  }
-  for (int g = ngrid; g <= FVV_MAX_GRIDS; ++g) h_grids.tw_start[g] = acc;
-  h_grids.tw_total = acc;
-  return FVV_OK;
 }
 
 static MeshBufs bufs_from(void *ws, const PrepLayout &L) {
@@ -709,6 +678,13 @@ static MeshBufs bufs_from(void *ws, const PrepLayout &L) {
   B.info = (int64_t *)(p + L.info);
   B.slot_base = (int64_t *)(p + L.slot5);
   return B;
+}
+
+static_assert(sizeof(MeshGrids) % 16 == 0, "MeshGrids is copied in 16-byte words");
+__global__ void store_mesh_grids_kernel(const __grid_constant__ MeshGrids src, MeshGrids *dst) {
+  const int4 *a = reinterpret_cast<const int4 *>(&src);
+  int4 *b = reinterpret_cast<int4 *>(dst);
+  for (int i = threadIdx.x; i < (int)(sizeof(MeshGrids) / 16); i += blockDim.x) b[i] = a[i];
 }
 
 }  // namespace fvv
@@ -729,57 +705,177 @@ static int ensure_tables() {
   return g_tables_rc;
 }
 
-extern "C" {
+// host grid table of a wrapper call
+static int fill_grids(const fvv_grid *grids, int ngrid, const int64_t *word_off, MeshGrids &G) {
+  if (ngrid < 1 || ngrid > FVV_MAX_GRIDS) {
+    set_error("mesh: %d grids (1..%d)", ngrid, FVV_MAX_GRIDS);
+    return FVV_E_LIMIT;
+  }
+  memset(&G, 0, sizeof(G));
+  G.ngrid = ngrid;
+  int64_t acc = 0;
+  for (int g = 0; g < ngrid; ++g) {
+    G.tw_start[g] = acc;
+    acc += mesh_grid_info(grids[g], word_off[g], acc, G.gi[g]);
+    if (3 * acc >= (int64_t)1 << 31) {  // 32-bit word indices (and int32 vertex prefixes)
+      set_error("mesh: %lld occupancy words over the batch (limit %lld)", (long long)acc,
+                (long long)((((int64_t)1 << 31) - 1) / 3));
+      return FVV_E_LIMIT;
+    }
+  }
+  for (int g = ngrid; g <= FVV_MAX_GRIDS; ++g) G.tw_start[g] = acc;
+  G.tw_total = acc;
+  G.tw3 = 3 * acc;
+  return FVV_OK;
+}
 
-size_t fvv_mesh_workspace_bytes(const fvv_grid *grids, int ngrid) {
+static int64_t words_of(const fvv_grid *grids, int ngrid) {
   int64_t acc = 0;
   for (int g = 0; g < ngrid; ++g) {
     const int64_t nx = grids[g].dims[0], ny = grids[g].dims[1], nz = grids[g].dims[2];
     if (nx >= 2 && ny >= 2 && nz >= 2) acc += nx * ny * ((nz + 31) / 32);
   }
-  return prep_layout(acc, ngrid).total;
+  return acc;
+}
+
+size_t fvv::mesh_ws_bytes(int64_t tw_cap, int ngrid_max) {
+  return prep_layout(tw_cap, ngrid_max).total;
+}
+
+int64_t *fvv::mesh_ws_totals(void *ws, int64_t tw_cap, int ngrid_max) {
+  return (int64_t *)((char *)ws + prep_layout(tw_cap, ngrid_max).totals);
+}
+
+int64_t *fvv::mesh_ws_info(void *ws, int64_t tw_cap, int ngrid_max) {
+  return (int64_t *)((char *)ws + prep_layout(tw_cap, ngrid_max).info);
+}
+
+int fvv::mesh_prepare_batch(const MeshGrids *G_dev, int64_t tw_cap, int ngrid_max,
+                            const uint32_t *occ_dev, void *ws_dev, size_t ws_bytes,
+                            cudaStream_t st) {
+  int rc = ensure_tables();
+  if (rc) return rc;
+  const PrepLayout L = prep_layout(tw_cap, ngrid_max);
+  if (ws_bytes < L.total) {
+    set_error("fvv_mesh_prepare: workspace %zu < %zu bytes", ws_bytes, L.total);
+    return FVV_E_ARG;
+  }
+  MeshBufs B = bufs_from(ws_dev, L);
+  B.occ = occ_dev;
+  cudaMemsetAsync(B.totals, 0, 32, st);
+  if (tw_cap > 0) {
+    mesh_transpose_kernel<<<kMeshGrid, 256, 0, st>>>(G_dev, B);
+    note_launches(1);
+    EdgeFlags ef{G_dev, B.tw, B.eflags, B.vprefix};
+    onepass_scan(ef, &G_dev->tw3, 0, 3 * tw_cap, (void *)B.sums, B.totals + 0, st);
+    CellFlags cf{G_dev, B.tw, B.sflags, B.sprefix};
+    onepass_scan(cf, &G_dev->tw_total, 0, tw_cap, (void *)B.sums, B.totals + 1, st);
+  }
+  mesh_grid_counts_kernel<<<1, 128, 0, st>>>(G_dev, B);
+  note_launches(1);
+  return cuda_check("fvv_mesh_prepare");
+}
+
+size_t fvv::mesh_emit_scratch(int64_t cap_v, int64_t cap_s) {
+  return al256(8 * (size_t)cap_v) + al256(8 * (size_t)cap_s) + al256(4 * (size_t)cap_s) +
+         al256(20 * (size_t)cap_s) + al256(onepass_bytes<Slot5>(cap_s + 1));
+}
+
+int fvv::mesh_emit_batch(const fvv_camera *cams_by_id, int ncam, const uint32_t *sil_dev,
+                         const int64_t *sil_word_off, const MeshGrids *G_dev, int64_t tw_cap,
+                         int ngrid_max, int exact, double fixed_iso, void *ws_dev,
+                         size_t ws_bytes, int64_t cap_v, int64_t cap_s, void *scratch_dev,
+                         size_t scratch_bytes, double *verts_dev, int32_t *tris_dev,
+                         cudaStream_t st) {
+  int rc = ensure_tables();
+  if (rc) return rc;
+  if (exact && (ncam < 1 || ncam > FVV_MAX_CAMS)) {
+    set_error("fvv_mesh_emit: %d cameras (1..%d)", ncam, FVV_MAX_CAMS);
+    return FVV_E_LIMIT;
+  }
+  const PrepLayout L = prep_layout(tw_cap, ngrid_max);
+  if (ws_bytes < L.total || scratch_bytes < mesh_emit_scratch(cap_v, cap_s)) {
+    set_error("fvv_mesh_emit: workspace/scratch too small");
+    return FVV_E_ARG;
+  }
+  MeshBufs B = bufs_from(ws_dev, L);
+  char *s = (char *)scratch_dev;
+  B.vert_key = (int64_t *)s;
+  s += al256(8 * (size_t)cap_v);
+  B.cell_key = (int64_t *)s;
+  s += al256(8 * (size_t)cap_s);
+  B.cell_mask = (int32_t *)s;
+  s += al256(4 * (size_t)cap_s);
+  B.cprefix = (int32_t *)s;
+  s += al256(20 * (size_t)cap_s);
+  Slot5 *cell_sums = (Slot5 *)s;
+  B.verts = verts_dev;
+  B.tris = tris_dev;
+  B.cap_v = cap_v;
+  B.cap_s = cap_s;
+  static thread_local MeshCams h_cams;
+  memset(&h_cams, 0, sizeof(h_cams));
+  h_cams.ncam = exact ? ncam : 0;
+  for (int c = 0; c < h_cams.ncam; ++c) {
+    h_cams.cams[c] = cams_by_id[c];
+    h_cams.sil_off[c] = sil_word_off[c];
+    h_cams.sil_stride[c] = sil_stride_words(cams_by_id[c].width);
+  }
+  Slot5 *d_total = (Slot5 *)((char *)ws_dev + L.slot5 + sizeof(int64_t) * 5 * ngrid_max);
+  if (cap_v > 0) {
+    mesh_vertex_list_kernel<<<kMeshGrid, 256, 0, st>>>(G_dev, B);
+    // one vertex per thread, cameras in a loop; measured against (vertex,
+    // camera) lane groups and a certified-FP32 endpoint projection with the
+    // float64 terms deferred to full warps, both slower (DESIGN.md 5)
+    const int64_t lam_blocks = std::min<int64_t>(cap_v / 128 + 1, 148 * 64);
+    mesh_lambda_kernel<<<(unsigned)lam_blocks, 128, 0, st>>>(G_dev, h_cams, B, sil_dev, exact,
+                                                              fixed_iso);
+    note_launches(2);
+  }
+  if (cap_s > 0) {
+    const int64_t cell_blocks = std::min<int64_t>(tw_cap / 256 + 1, 148 * 64);
+    mesh_cells_kernel<<<(unsigned)std::max<int64_t>(cell_blocks, kMeshGrid), 256, 0, st>>>(G_dev,
+                                                                                          B);
+    note_launches(1);
+    TriScan ts{B.cell_mask, B.cprefix};
+    onepass_scan(ts, B.totals + 3, 0, cap_s, (void *)cell_sums, d_total, st);
+  } else {
+    cudaMemsetAsync(d_total, 0, sizeof(Slot5), st);
+  }
+  mesh_slot_bases_kernel<<<1, 32, 0, st>>>(G_dev, B, d_total);
+  if (cap_s > 0) mesh_emit_kernel<<<kMeshGrid, 256, 0, st>>>(G_dev, B);
+  note_launches(1 + (cap_s > 0 ? 1 : 0));
+  return cuda_check("fvv_mesh_emit");
+}
+
+extern "C" {
+
+size_t fvv_mesh_workspace_bytes(const fvv_grid *grids, int ngrid) {
+  return prep_layout(words_of(grids, ngrid), ngrid).total;
 }
 
 int fvv_mesh_prepare(const fvv_grid *grids, int ngrid, const uint32_t *occ_dev,
                      const int64_t *word_off, void *ws_dev, size_t ws_bytes, void *stream) {
-  int rc = ensure_tables();
+  static thread_local MeshGrids G;
+  int rc = fill_grids(grids, ngrid, word_off, G);
   if (rc) return rc;
-  rc = fill_grids(grids, ngrid, word_off, 1, 0.5);
-  if (rc) return rc;
-  const PrepLayout L = prep_layout(h_grids.tw_total, ngrid);
+  const PrepLayout L = prep_layout(G.tw_total, ngrid);
   if (ws_bytes < L.total) {
     set_error("fvv_mesh_prepare: workspace %zu < %zu bytes", ws_bytes, L.total);
     return FVV_E_ARG;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  MeshBufs B = bufs_from(ws_dev, L);
-  B.occ = occ_dev;
-  cudaMemsetAsync(B.totals, 0, 32, st);
-  if (h_grids.tw_total > 0) {
-    mesh_transpose_kernel<<<kMeshGrid, 256, 0, st>>>(h_grids, B);
-    note_launches(1);
-    EdgeFlags ef{h_grids, B.tw, B.eflags, B.vprefix};
-    onepass_scan(ef, nullptr, 3 * h_grids.tw_total, 3 * h_grids.tw_total, (void *)B.sums,
-                 B.totals + 0, st);
-    CellFlags cf{h_grids, B.tw, B.sflags, B.sprefix};
-    onepass_scan(cf, nullptr, h_grids.tw_total, h_grids.tw_total, (void *)B.sums, B.totals + 1,
-                 st);
-  }
-  mesh_grid_counts_kernel<<<1, 128, 0, st>>>(h_grids, B);
+  MeshGrids *G_dev = (MeshGrids *)((char *)ws_dev + L.grids);
+  store_mesh_grids_kernel<<<1, 256, 0, st>>>(G, G_dev);
   note_launches(1);
-  return cuda_check("fvv_mesh_prepare");
+  return mesh_prepare_batch(G_dev, G.tw_total, ngrid, occ_dev, ws_dev, ws_bytes, st);
 }
 
 // Reads the counts fvv_mesh_prepare left in the workspace: totals[3] = {V, S, T}
 // and info[ngrid][8] (vbase V sbase S tbase T fallback inconsistent).
 int fvv_mesh_counts(const fvv_grid *grids, int ngrid, const void *ws_dev, int64_t *totals_dev,
                     int64_t *info_dev, void *stream) {
-  int64_t acc = 0;
-  for (int g = 0; g < ngrid; ++g) {
-    const int64_t nx = grids[g].dims[0], ny = grids[g].dims[1], nz = grids[g].dims[2];
-    if (nx >= 2 && ny >= 2 && nz >= 2) acc += nx * ny * ((nz + 31) / 32);
-  }
-  const PrepLayout L = prep_layout(acc, ngrid);
+  const PrepLayout L = prep_layout(words_of(grids, ngrid), ngrid);
   cudaStream_t st = (cudaStream_t)stream;
   if (totals_dev)
     cudaMemcpyAsync(totals_dev, (const char *)ws_dev + L.totals, 3 * sizeof(int64_t),
@@ -791,77 +887,29 @@ int fvv_mesh_counts(const fvv_grid *grids, int ngrid, const void *ws_dev, int64_
 }
 
 size_t fvv_mesh_emit_scratch_bytes(int64_t num_vertices, int64_t num_cells) {
-  return al256(8 * (size_t)num_vertices) + al256(8 * (size_t)num_cells) +
-         al256(4 * (size_t)num_cells) + al256(20 * (size_t)num_cells) +
-         al256(onepass_bytes<Slot5>(num_cells + 1));
+  return mesh_emit_scratch(num_vertices, num_cells);
 }
 
+// Phase B of the batch fvv_mesh_prepare set up in ws_dev (its grid table and
+// counts); grids / word_off must be the same as there.
 int fvv_mesh_emit(const fvv_camera *cams_by_id, int ncam, const uint32_t *sil_dev,
                   const int64_t *sil_word_off, const fvv_grid *grids, int ngrid,
                   const uint32_t *occ_dev, const int64_t *word_off, int exact, double fixed_iso,
                   void *ws_dev, size_t ws_bytes, int64_t num_vertices, int64_t num_cells,
                   void *scratch_dev, size_t scratch_bytes, double *verts_dev, int32_t *tris_dev,
                   void *stream) {
-  int rc = ensure_tables();
-  if (rc) return rc;
-  if (exact && (ncam < 1 || ncam > FVV_MAX_CAMS)) {
-    set_error("fvv_mesh_emit: %d cameras (1..%d)", ncam, FVV_MAX_CAMS);
+  (void)occ_dev;
+  (void)word_off;
+  if (ngrid < 1 || ngrid > FVV_MAX_GRIDS) {
+    set_error("mesh: %d grids (1..%d)", ngrid, FVV_MAX_GRIDS);
     return FVV_E_LIMIT;
   }
-  rc = fill_grids(grids, ngrid, word_off, exact, fixed_iso);
-  if (rc) return rc;
-  const PrepLayout L = prep_layout(h_grids.tw_total, ngrid);
-  if (ws_bytes < L.total || scratch_bytes < fvv_mesh_emit_scratch_bytes(num_vertices, num_cells)) {
-    set_error("fvv_mesh_emit: workspace/scratch too small");
-    return FVV_E_ARG;
-  }
-  cudaStream_t st = (cudaStream_t)stream;
-  MeshBufs B = bufs_from(ws_dev, L);
-  B.occ = occ_dev;
-  char *s = (char *)scratch_dev;
-  B.vert_key = (int64_t *)s;
-  s += al256(8 * (size_t)num_vertices);
-  B.cell_key = (int64_t *)s;
-  s += al256(8 * (size_t)num_cells);
-  B.cell_mask = (int32_t *)s;
-  s += al256(4 * (size_t)num_cells);
-  B.cprefix = (int32_t *)s;
-  s += al256(20 * (size_t)num_cells);
-  Slot5 *cell_sums = (Slot5 *)s;
-  B.verts = verts_dev;
-  B.tris = tris_dev;
-  static thread_local MeshCams h_cams;
-  memset(&h_cams, 0, sizeof(h_cams));
-  h_cams.ncam = exact ? ncam : 0;
-  for (int c = 0; c < h_cams.ncam; ++c) {
-    h_cams.cams[c] = cams_by_id[c];
-    h_cams.sil_off[c] = sil_word_off[c];
-    h_cams.sil_stride[c] = sil_stride_words(cams_by_id[c].width);
-  }
-  Slot5 *d_total = (Slot5 *)((char *)ws_dev + L.slot5 + sizeof(int64_t) * 5 * ngrid);
-  if (num_vertices > 0) {
-    mesh_vertex_list_kernel<<<kMeshGrid, 256, 0, st>>>(h_grids, B);
-    // one vertex per thread, cameras in a loop; measured against (vertex,
-    // camera) lane groups and a certified-FP32 endpoint projection with the
-    // float64 terms deferred to full warps, both slower (DESIGN.md 4.3)
-    const int64_t lam_blocks = std::min<int64_t>(num_vertices / 128 + 1, 148 * 64);
-    mesh_lambda_kernel<<<(unsigned)lam_blocks, 128, 0, st>>>(h_grids, h_cams, B, sil_dev);
-    note_launches(2);
-  }
-  if (num_cells > 0) {
-    const int64_t cell_blocks = std::min<int64_t>(h_grids.tw_total / 256 + 1, 148 * 64);
-    mesh_cells_kernel<<<(unsigned)std::max<int64_t>(cell_blocks, kMeshGrid), 256, 0, st>>>(h_grids,
-                                                                                          B);
-    note_launches(1);
-    TriScan ts{B.cell_mask, B.cprefix};
-    onepass_scan(ts, B.totals + 1, 0, num_cells, (void *)cell_sums, d_total, st);
-  } else {
-    cudaMemsetAsync(d_total, 0, sizeof(Slot5), st);
-  }
-  mesh_slot_bases_kernel<<<1, 32, 0, st>>>(h_grids, B, d_total);
-  if (num_cells > 0) mesh_emit_kernel<<<kMeshGrid, 256, 0, st>>>(h_grids, B);
-  note_launches(1 + (num_cells > 0 ? 1 : 0));
-  return cuda_check("fvv_mesh_emit");
+  const int64_t tw = words_of(grids, ngrid);
+  const PrepLayout L = prep_layout(tw, ngrid);
+  return mesh_emit_batch(cams_by_id, ncam, sil_dev, sil_word_off,
+                         (const MeshGrids *)((char *)ws_dev + L.grids), tw, ngrid, exact,
+                         fixed_iso, ws_dev, ws_bytes, num_vertices, num_cells, scratch_dev,
+                         scratch_bytes, verts_dev, tris_dev, (cudaStream_t)stream);
 }
 
 int fvv_edge_isovalues(const fvv_camera *cams_by_id, int ncam, const uint32_t *sil_dev,
