@@ -246,17 +246,20 @@ def run_b200(args):
             work["last"] = (int(st["sparse_tests"]), int(st["dense_tests"]))
 
     lib = _lib.load()
-    # ---- single-stream pass: per-stage device times (roofline inputs) ----
-    for i in range(args.warmup):
-        device_step(i, False)
-    torch.cuda.synchronize()
-    barrier(world)
-    s_start = torch.cuda.Event(enable_timing=True)
-    s_end = torch.cuda.Event(enable_timing=True)
-    s_start.record()
-    for i in range(args.steps):
-        device_step(i, True)
-    s_end.record()
+    # ---- single-stream pass: per-stage device times (roofline inputs); one
+    # CUDA stream (not the legacy default stream, so frames replay as graphs) ----
+    single = torch.cuda.Stream()
+    with torch.cuda.stream(single):
+        for i in range(args.warmup):
+            device_step(i, False)
+        torch.cuda.synchronize()
+        barrier(world)
+        s_start = torch.cuda.Event(enable_timing=True)
+        s_end = torch.cuda.Event(enable_timing=True)
+        s_start.record()
+        for i in range(args.steps):
+            device_step(i, True)
+        s_end.record()
     torch.cuda.synchronize()
     barrier(world)
     ms_single = max_over_ranks(s_start.elapsed_time(s_end), world)
@@ -405,7 +408,8 @@ def run_b200(args):
 
         # warm-up covers every distinct input on every lane (buffer growth,
         # pinned readback pool) so the timed steps are steady state
-        run_e2e(max(args.warmup, 2 * len(host) + 2))
+        # (>= 3 frames per executor: host-planned, device-planned, graph capture)
+        run_e2e(max(args.warmup, 2 * len(host) + 2, 6 * lanes + 2))
         torch.cuda.synchronize()
         barrier(world)
         R.H2D_BYTES["frames"] = R.H2D_BYTES["masks"] = 0

@@ -219,11 +219,14 @@ int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int
  * depth (and tri_id) planes contiguous from plane_off[0], already holding the
  * background except the 32-pixel tiles flagged in dirty_dev (one byte per
  * tile of plane 0's element index / 32, ceil(total_px / 32) bytes), which
- * are reset first; the call flags the tiles it writes. full_reset != 0 fills
+ * are reset first; the call flags the tiles it writes. The vertex count is
+ * *nv_dev when nv_dev is non-NULL (nv: the capacity, the records' stride),
+ * like nt / nt_dev. full_reset != 0 fills
  * the planes and clears the map instead (first use, or new buffers). Same
  * results as fvv_rasterize; only the background writes differ. */
 int fvv_rasterize_tracked(const fvv_camera *cams, int ncam, const double *verts_dev, int64_t nv,
-                          const int32_t *tris_dev, int64_t nt, const int64_t *nt_dev,
+                          const int64_t *nv_dev, const int32_t *tris_dev, int64_t nt,
+                          const int64_t *nt_dev,
                           double *depth_dev, const int64_t *plane_off, int32_t *tri_id_dev,
                           void *ws_dev, size_t ws_bytes, uint8_t *dirty_dev, int full_reset,
                           void *stream);

@@ -47,6 +47,7 @@ __global__ void project_kernel(fvv_camera cam, const double *__restrict__ pts, i
 struct PackParams {
   int ncam;
   const uint8_t *masks;
+  const FrameInputs *in;  // when set: masks from in->masks
   uint32_t *sil;
   int64_t mask_off[FVV_MAX_CAMS];
   int64_t sil_off[FVV_MAX_CAMS];
@@ -57,14 +58,21 @@ struct PackParams {
 
 // Rows whose width is a multiple of 32 (1080p, 4K): each thread turns 32
 // mask bytes (two 16-byte loads) into one word, so a warp streams 1 KB.
+__device__ __forceinline__ const uint8_t *pack_masks(const PackParams &p) {
+  const uint8_t *m = p.masks;
+  if (p.in != nullptr) m = p.in->masks;
+  return m;
+}
+
 __global__ void pack_wide_kernel(const __grid_constant__ PackParams p) {
   const int64_t total = p.word_start[p.ncam];
+  const uint8_t *masks = pack_masks(p);
   for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
        w += (int64_t)gridDim.x * blockDim.x) {
     int c = 0;
     while (w >= p.word_start[c + 1]) ++c;
     const int64_t local = w - p.word_start[c];
-    const uint4 *src = reinterpret_cast<const uint4 *>(p.masks + p.mask_off[c] + local * 32);
+    const uint4 *src = reinterpret_cast<const uint4 *>(masks + p.mask_off[c] + local * 32);
     const uint4 a = __ldcs(src), b = __ldcs(src + 1);
     const uint32_t q[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
     uint32_t bits = 0;
@@ -86,6 +94,7 @@ __global__ void pack_kernel(const __grid_constant__ PackParams p) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * blockDim.x / 32;
   const int64_t total = p.word_start[p.ncam];
+  const uint8_t *masks = pack_masks(p);
   for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; w < total; w += warps) {
     int c = 0;
     while (w >= p.word_start[c + 1]) ++c;
@@ -94,10 +103,48 @@ __global__ void pack_kernel(const __grid_constant__ PackParams p) {
     int64_t row = local / stride;
     int x = (int)(local - row * stride) * 32 + lane;
     bool fg = false;
-    if (x < p.width[c]) fg = p.masks[p.mask_off[c] + row * p.width[c] + x] != 0;
+    if (x < p.width[c]) fg = masks[p.mask_off[c] + row * p.width[c] + x] != 0;
     uint32_t bits = __ballot_sync(0xffffffffu, fg);
     if (lane == 0) p.sil[p.sil_off[c] + local] = bits;
   }
+}
+
+int pack_silhouettes_bound(const fvv_camera *cams, int ncam, const uint8_t *masks_dev,
+                           const FrameInputs *in, const int64_t *mask_off, uint32_t *sil_dev,
+                           const int64_t *sil_word_off, cudaStream_t st) {
+  if (ncam < 1 || ncam > FVV_MAX_CAMS) {
+    set_error("fvv_pack_silhouettes: %d cameras (limit %d)", ncam, FVV_MAX_CAMS);
+    return ncam < 1 ? FVV_E_ARG : FVV_E_LIMIT;
+  }
+  PackParams p;
+  memset(&p, 0, sizeof(p));
+  p.ncam = ncam;
+  p.masks = masks_dev;
+  p.in = in;
+  p.sil = sil_dev;
+  p.word_start[0] = 0;
+  for (int c = 0; c < ncam; ++c) {
+    p.mask_off[c] = mask_off[c];
+    p.sil_off[c] = sil_word_off[c];
+    p.width[c] = cams[c].width;
+    p.height[c] = cams[c].height;
+    p.word_start[c + 1] = p.word_start[c] + (int64_t)sil_stride_words(cams[c].width) * cams[c].height;
+  }
+  bool wide = ((uintptr_t)masks_dev & 15) == 0;
+  for (int c = 0; c < ncam; ++c)
+    wide = wide && (cams[c].width % 32 == 0) && (mask_off[c] % 16 == 0);
+  int64_t words = p.word_start[ncam];
+  if (wide) {
+    int64_t blocks = (words + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    pack_wide_kernel<<<(int)blocks, 256, 0, st>>>(p);
+  } else {
+    int64_t blocks = (words * 32 + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    pack_kernel<<<(int)blocks, 256, 0, st>>>(p);
+  }
+  note_launches(1);
+  return cuda_check("fvv_pack_silhouettes");
 }
 
 }  // namespace fvv
@@ -162,38 +209,8 @@ int fvv_project(const fvv_camera *cam, const double *pts_dev, int64_t n, int use
 int fvv_pack_silhouettes(const fvv_camera *cams, int ncam, const uint8_t *masks_dev,
                          const int64_t *mask_off, uint32_t *sil_dev, const int64_t *sil_word_off,
                          void *stream) {
-  if (ncam < 1 || ncam > FVV_MAX_CAMS) {
-    set_error("fvv_pack_silhouettes: %d cameras (limit %d)", ncam, FVV_MAX_CAMS);
-    return ncam < 1 ? FVV_E_ARG : FVV_E_LIMIT;
-  }
-  PackParams p;
-  memset(&p, 0, sizeof(p));
-  p.ncam = ncam;
-  p.masks = masks_dev;
-  p.sil = sil_dev;
-  p.word_start[0] = 0;
-  for (int c = 0; c < ncam; ++c) {
-    p.mask_off[c] = mask_off[c];
-    p.sil_off[c] = sil_word_off[c];
-    p.width[c] = cams[c].width;
-    p.height[c] = cams[c].height;
-    p.word_start[c + 1] = p.word_start[c] + (int64_t)sil_stride_words(cams[c].width) * cams[c].height;
-  }
-  bool wide = ((uintptr_t)masks_dev & 15) == 0;
-  for (int c = 0; c < ncam; ++c)
-    wide = wide && (cams[c].width % 32 == 0) && (mask_off[c] % 16 == 0);
-  int64_t words = p.word_start[ncam];
-  if (wide) {
-    int64_t blocks = (words + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
-    pack_wide_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(p);
-  } else {
-    int64_t blocks = (words * 32 + 255) / 256;
-    if (blocks > 148 * 32) blocks = 148 * 32;
-    pack_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(p);
-  }
-  note_launches(1);
-  return cuda_check("fvv_pack_silhouettes");
+  return pack_silhouettes_bound(cams, ncam, masks_dev, nullptr, mask_off, sil_dev, sil_word_off,
+                                (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -10,6 +10,8 @@
 // tiny pinned read: the component table (to size the ROI grids), the mesh
 // vertex/cell counts (to size the mesh outputs) and the final counters.
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <initializer_list>
 #include <vector>
@@ -41,9 +43,9 @@ int fvv_mesh_emit(const fvv_camera *, int, const uint32_t *, const int64_t *, co
 size_t fvv_raster_workspace_bytes(int64_t, int64_t, int);
 int fvv_rasterize(const fvv_camera *, int, const double *, int64_t, const int32_t *, int64_t,
                   const int64_t *, double *, const int64_t *, int32_t *, void *, size_t, void *);
-int fvv_rasterize_tracked(const fvv_camera *, int, const double *, int64_t, const int32_t *,
-                          int64_t, const int64_t *, double *, const int64_t *, int32_t *, void *,
-                          size_t, uint8_t *, int, void *);
+int fvv_rasterize_tracked(const fvv_camera *, int, const double *, int64_t, const int64_t *,
+                          const int32_t *, int64_t, const int64_t *, double *, const int64_t *,
+                          int32_t *, void *, size_t, uint8_t *, int, void *);
 int fvv_classify(const fvv_camera *, int, const double *, const int32_t *, int64_t,
                  const int64_t *, const double *, const int64_t *, double, uint32_t *, int64_t,
                  void *);
@@ -124,8 +126,9 @@ struct ReadPiece {
   int64_t words;         // words to copy when count == nullptr
   int64_t elem_words, max_elems;
 };
+constexpr int kReadPieces = 10;
 struct ReadBatch {
-  ReadPiece p[4];
+  ReadPiece p[kReadPieces];
 };
 
 __global__ void readback_kernel(ReadBatch B) {
@@ -141,6 +144,181 @@ __global__ void readback_kernel(ReadBatch B) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < w;
        i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = __ldcg(src + i);
+}
+
+__global__ void bind_inputs_kernel(const __grid_constant__ FrameInputs v, FrameInputs *dst) {
+  const int4 *a = reinterpret_cast<const int4 *>(&v);
+  int4 *b = reinterpret_cast<int4 *>(dst);
+  for (int i = threadIdx.x; i < (int)(sizeof(FrameInputs) / 16); i += blockDim.x) b[i] = a[i];
+}
+
+// ---- device-side frame planning -------------------------------------------
+// What the host does between B-2 and B-3 (the noise band filter, extract_rois
+// and GridSpec.from_aabb, hull.py:46-47, 257-284, voxels.py:62-71), done on
+// the device in the same IEEE double arithmetic, plus the B-3 carve and C
+// polygonize grid tables, so a frame runs without a host round trip. Batches
+// the planner does not take (more than FVV_MAX_GRIDS ROIs or 4096
+// components, an ROI error, a capacity overflow) come back with a status and
+// the host-planned path redoes the frame.
+enum : int32_t { kPlanManyRois = 1, kPlanError = 2, kPlanCapacity = 4 };
+
+struct __align__(16) FramePlan {
+  int64_t status, nroi;  // (nroi: all ROIs of the band filter, may exceed FVV_MAX_GRIDS)
+  int64_t dense_tests, fine_words;
+  int64_t roi_component[FVV_MAX_GRIDS];
+  double roi_box[FVV_MAX_GRIDS][6];
+  CarveGrids carve;  // B-3 (16^3 tiles)
+  MeshGrids mesh;    // C
+};
+
+struct PlanArgs {
+  fvv_grid coarse;
+  double roi_margin, fine_spacing, t_large;
+  int64_t t_small, budget;
+  int64_t comp_cap;  // component records in comps[]
+  int64_t cap_words, cap_tiles, cap_tw;
+};
+
+constexpr int kPlanThreads = 1024;
+
+__global__ void __launch_bounds__(kPlanThreads)
+    frame_plan_kernel(const __grid_constant__ PlanArgs a, const fvv_component *__restrict__ comps,
+                      const int64_t *__restrict__ ccl_counts, FramePlan *plan) {
+  __shared__ int s_warp[kPlanThreads / 32];
+  __shared__ int s_nroi, s_status;
+  __shared__ int64_t s_words[FVV_MAX_GRIDS], s_tiles[FVV_MAX_GRIDS], s_tw[FVV_MAX_GRIDS];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t ncomp = __ldcg(ccl_counts + 1);
+  if (tid == 0) {
+    s_nroi = 0;
+    s_status = ncomp > a.comp_cap ? kPlanManyRois : 0;
+  }
+  __syncthreads();
+  const fvv_grid &G = a.coarse;
+  double extent[3];
+  for (int j = 0; j < 3; ++j) extent[j] = G.origin[j] + G.spacing * (double)G.dims[j];
+  const int64_t n = ncomp < a.comp_cap ? ncomp : a.comp_cap;
+  // band filter + ROI boxes in component order (an ordered block scan per chunk)
+  for (int64_t c0 = 0; c0 < n; c0 += kPlanThreads) {
+    const int64_t c = c0 + tid;
+    bool keep = false;
+    if (c < n) {
+      const double cnt = (double)comps[c].voxel_count;
+      keep = (double)a.t_small <= cnt && cnt <= a.t_large;  // hull.py:46-47
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) s_warp[warp] = __popc(b);
+    __syncthreads();
+    int before = 0;
+    for (int w = 0; w < warp; ++w) before += s_warp[w];
+    const int base = s_nroi;
+    const int r = base + before + __popc(b & ((1u << lane) - 1u));
+    if (keep && r < FVV_MAX_GRIDS) {
+      const fvv_component &cp = comps[c];
+      double lo[3], hi[3];
+      bool ok = true;
+      for (int j = 0; j < 3; ++j) {  // hull.py:279-282
+        lo[j] = G.origin[j] + G.spacing * (double)cp.bbox_min[j] - a.roi_margin;
+        hi[j] = G.origin[j] + G.spacing * ((double)cp.bbox_max[j] + 1.0) + a.roi_margin;
+        lo[j] = lo[j] >= G.origin[j] ? lo[j] : G.origin[j];  // np.maximum(lo, stage_lo)
+        hi[j] = hi[j] <= extent[j] ? hi[j] : extent[j];      // np.minimum(hi, stage_hi)
+        ok = ok && lo[j] < hi[j];
+      }
+      // voxels.py:62-71 GridSpec.from_aabb (+ the budget check, voxels.py:34-37)
+      fvv_grid fg;
+      int64_t nv = 1;
+      for (int j = 0; j < 3; ++j) {
+        int64_t d = (int64_t)ceil((hi[j] - lo[j]) / a.fine_spacing - 1e-9);
+        d = d < 1 ? 1 : d;
+        fg.origin[j] = lo[j];
+        fg.dims[j] = d;
+        nv *= d;
+      }
+      fg.spacing = a.fine_spacing;
+      if (!ok || nv > a.budget) atomicOr(&s_status, kPlanError);
+      plan->roi_component[r] = cp.id;
+      for (int j = 0; j < 3; ++j) {
+        plan->roi_box[r][j] = lo[j];
+        plan->roi_box[r][3 + j] = hi[j];
+      }
+      plan->carve.grids[r] = fg;
+      s_words[r] = (nv + 31) / 32;
+      uint32_t tx, ty;
+      int64_t tiles;
+      carve_grid_tiles(fg, 4, tx, ty, tiles);
+      plan->carve.tiles_x[r] = tx;
+      plan->carve.tiles_y[r] = ty;
+      s_tiles[r] = tiles;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int tot = 0;
+      for (int w = 0; w < kPlanThreads / 32; ++w) tot += s_warp[w];
+      s_nroi += tot;
+    }
+    __syncthreads();
+  }
+  const int nroi_all = s_nroi;
+  if (nroi_all > FVV_MAX_GRIDS && tid == 0) atomicOr(&s_status, kPlanManyRois);
+  __syncthreads();
+  const int nroi = nroi_all < FVV_MAX_GRIDS ? nroi_all : FVV_MAX_GRIDS;
+  // per-grid prefixes (one warp, 32 grids per step): occupancy words, tiles, k-row words
+  if (warp == 0) {
+    int64_t cw = 0, ct = 0, ck = 0, dense = 0;
+    for (int g0 = 0; g0 < FVV_MAX_GRIDS; g0 += 32) {
+      const int g = g0 + lane;
+      const bool live = g < nroi;
+      int64_t w = live ? s_words[g] : 0, t = live ? s_tiles[g] : 0, k = 0, vox = 0;
+      MeshGridInfo gi;
+      if (live) {
+        const fvv_grid &fg = plan->carve.grids[g];
+        vox = fg.dims[0] * fg.dims[1] * fg.dims[2];
+        k = mesh_grid_info(fg, 0, 0, gi);  // offsets filled in below
+      }
+      int64_t iw = w, it = t, ik = k, iv = vox;  // inclusive scans
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t xw = __shfl_up_sync(0xffffffffu, iw, o), xt = __shfl_up_sync(0xffffffffu, it, o),
+                      xk = __shfl_up_sync(0xffffffffu, ik, o), xv = __shfl_up_sync(0xffffffffu, iv, o);
+        if (lane >= o) {
+          iw += xw;
+          it += xt;
+          ik += xk;
+          iv += xv;
+        }
+      }
+      const int64_t ow = cw + iw - w, ot = ct + it - t, ok = ck + ik - k;
+      if (live) {
+        plan->carve.word_off[g] = ow;
+        plan->carve.blk_start[g] = ot;
+        mesh_grid_info(plan->carve.grids[g], ow, ok, gi);
+        plan->mesh.gi[g] = gi;
+        plan->mesh.tw_start[g] = ok;
+      }
+      cw += __shfl_sync(0xffffffffu, iw, 31);
+      ct += __shfl_sync(0xffffffffu, it, 31);
+      ck += __shfl_sync(0xffffffffu, ik, 31);
+      dense += __shfl_sync(0xffffffffu, iv, 31);
+    }
+    if (lane == 0) {
+      int st = s_status;
+      if (cw > a.cap_words || ct > a.cap_tiles || ck > a.cap_tw) st |= kPlanCapacity;
+      if (3 * ck >= ((int64_t)1 << 31)) st |= kPlanError;
+      const bool run = st == 0;  // otherwise the device stages find nothing to do
+      const int ng = run ? nroi : 0;
+      plan->status = st;
+      plan->nroi = nroi_all;
+      plan->dense_tests = dense;
+      plan->fine_words = cw;
+      plan->carve.ngrid = ng;
+      plan->carve.tile_log2 = 4;
+      plan->carve.total_tiles = run ? ct : 0;
+      for (int g = ng; g <= FVV_MAX_GRIDS; ++g) plan->carve.blk_start[g] = run ? ct : 0;
+      plan->mesh.ngrid = ng;
+      plan->mesh.tw_total = run ? ck : 0;
+      plan->mesh.tw3 = run ? 3 * ck : 0;
+      for (int g = ng; g <= FVV_MAX_GRIDS; ++g) plan->mesh.tw_start[g] = run ? ck : 0;
+    }
+  }
 }
 
 }  // namespace fvv
@@ -186,7 +364,30 @@ struct fvv_frame {
   int64_t nv = 0, nt = 0, vis_stride = 0;
   fvv_frame_stats stats;
   cudaEvent_t ev[9];
+  // device-planned frames: capacities from the sizes seen so far
+  int64_t seen_words = 0, seen_tiles = 0, seen_tw = 0, seen_v = 0, seen_s = 0;
+  bool seen_plannable = false, caps_grown = false;
+  struct Caps {
+    int64_t words = 0, tiles = 0, tw = 0, v = 0, s = 0;
+    bool ready = false;
+  } caps;
+  DevBuf plan, inputs;  // FramePlan, FrameInputs (device-planned frames)
+  // one CUDA graph of the device-planned frame per input binding
+  cudaGraphExec_t graph = nullptr;
+  std::vector<char> graph_key, pending_key;
+  long long graph_launches = 0;
 };
+
+// Stage boundary event; inside a graph capture an external event-record node,
+// so the replayed frame still reports its stage times.
+static void stage_mark(fvv_frame *f, int e, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(f->ev[e], st, cudaEventRecordExternal);
+  else
+    cudaEventRecord(f->ev[e], st);
+}
 
 static int grid_from_aabb(const double lo[3], const double hi[3], double spacing, int64_t budget,
                           fvv_grid &g) {
@@ -243,6 +444,7 @@ static void readback(fvv_frame *f, cudaStream_t st, std::initializer_list<HostPi
   int n = 0;
   int64_t most = 0;
   for (const HostPiece &h : pieces) {
+    if (n == kReadPieces) break;
     ReadPiece &r = b.p[n++];
     r.src = (const int64_t *)h.src;
     r.dst = (int64_t *)((char *)f->host_small_dev + h.dst_off);
@@ -321,12 +523,125 @@ fvv_frame *fvv_frame_create(const fvv_camera *cams, int ncam, const fvv_frame_co
 
 void fvv_frame_destroy(fvv_frame *f) {
   if (!f) return;
+  if (f->graph) cudaGraphExecDestroy(f->graph);
   for (int e = 0; e < 9; ++e) cudaEventDestroy(f->ev[e]);
   if (f->host_small) cudaFreeHost(f->host_small);
   delete f;
 }
 
-int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt,
+// B-1 sparse carve + B-2 CCL (events 0, 1), common to both paths.
+static int enqueue_b12(fvv_frame *f, const uint8_t *masks_dev, const FrameInputs *in,
+                       cudaStream_t st, int *out_stage) {
+  const fvv_frame_config &cfg = f->cfg;
+  const int ncam = f->ncam;
+  fvv_frame_stats &S = f->stats;
+  stage_mark(f, 0, st);
+  // ---- B-1 sparse carve (pipeline.py:154-157) ----
+  const fvv_grid &G = f->coarse;
+  const int64_t nvox_c = G.dims[0] * G.dims[1] * G.dims[2];
+  S.sparse_tests = nvox_c;
+  FVV_TRY(1, pack_silhouettes_bound(f->cams.data(), ncam, masks_dev, in, f->mask_off.data(),
+                                    f->sil.as<uint32_t>(), f->word_off.data(), st));
+  const int64_t zero = 0;
+  FVV_TRY(1, fvv_carve(f->cams.data(), ncam, f->sil.as<uint32_t>(), f->word_off.data(), &G, 1,
+                       &zero, cfg.min_views, f->occ_c.as<uint32_t>(), f->cnt_c.as<int64_t>(),
+                       f->carve_ws.p, f->carve_ws.cap, st));
+  stage_mark(f, 1, st);
+
+  // ---- B-2 CCL, noise filter, ROIs (pipeline.py:159-166) ----
+  FVV_TRY(2, fvv_ccl26(f->occ_c.as<uint32_t>(), &G, f->ccl_ws.p, f->ccl_ws.cap,
+                       f->comps.as<fvv_component>(), 4096, f->ccl_counts.as<int64_t>(), st));
+  return FVV_OK;
+}
+
+// D-1 depth images, D-2 visibility, E colour pass (events 5..7). nv: vertex
+// count or capacity (the raster records' stride), *nv_dev the count when
+// non-null; nt_ub: triangle-count upper bound, *ntri_dev the count.
+static int enqueue_tail(fvv_frame *f, const fvv_camera *virt, const int32_t *rank_pos,
+                        const uint8_t *frames_dev, const int64_t *frame_off,
+                        const uint8_t *fallback, cudaStream_t st, int *out_stage, int64_t nv,
+                        const int64_t *nv_dev, int64_t nt_ub, const int64_t *ntri_dev,
+                        bool have_mesh, const FrameInputs *in) {
+  const fvv_frame_config &cfg = f->cfg;
+  const int ncam = f->ncam;
+  // ---- D-1 depth images, D-2 visibility (pipeline.py:198-207) ----
+  if (have_mesh) {
+    FVV_TRY(5, f->depth.ensure(8 * (size_t)f->planes));
+    FVV_TRY(5, f->dirty.ensure((size_t)(f->planes + 31) / 32));
+    const size_t rwb = fvv_raster_workspace_bytes(nv, nt_ub, ncam);
+    FVV_TRY(5, f->raster_ws.ensure(rwb));
+    const bool fresh = f->dirty_for[0] != f->depth.p || f->dirty_for[1] != f->dirty.p;
+    FVV_TRY(5, fvv_rasterize_tracked(f->cams.data(), ncam, f->verts.as<double>(), nv,
+                                     nv_dev, f->tris.as<int32_t>(), nt_ub, ntri_dev,
+                                     f->depth.as<double>(), f->plane_off.data(), nullptr,
+                                     f->raster_ws.p, f->raster_ws.cap, f->dirty.as<uint8_t>(),
+                                     fresh, st));
+    f->dirty_for[0] = f->depth.p;  // new planes or map: filled once above
+    f->dirty_for[1] = f->dirty.p;
+  }
+  stage_mark(f, 5, st);
+  FVV_TRY(6, f->vis.ensure(4 * (size_t)ncam * f->vis_stride));
+  cudaMemsetAsync(f->vis.p, 0, 4 * (size_t)ncam * f->vis_stride, st);
+  if (have_mesh)
+    FVV_TRY(6, fvv_classify(f->cams.data(), ncam, f->verts.as<double>(), f->tris.as<int32_t>(),
+                            nt_ub, ntri_dev, f->depth.as<double>(), f->plane_off.data(),
+                            cfg.t_v, f->vis.as<uint32_t>(), f->vis_stride, st));
+  stage_mark(f, 6, st);
+
+  // ---- E: one virtual view (render.py:64-113) ----
+  f->virt_px = 0;
+  if (virt) {
+    const int64_t np = (int64_t)virt->width * virt->height;
+    f->virt_px = np;
+    FVV_TRY(7, f->color.ensure(3 * (size_t)np));
+    FVV_TRY(7, f->source.ensure(4 * (size_t)np));
+    FVV_TRY(7, f->covered.ensure((size_t)np));
+    FVV_TRY(7, f->code.ensure((size_t)np));
+    if (have_mesh) {
+      FVV_TRY(7, f->vplane_d.ensure(8 * (size_t)np));
+      FVV_TRY(7, f->vplane_id.ensure(4 * (size_t)np));
+      const size_t vwb = fvv_raster_workspace_bytes(nv, nt_ub, 1);
+      FVV_TRY(7, f->vraster_ws.ensure(vwb));
+      const int64_t off0 = 0;
+      FVV_TRY(7, f->vdirty.ensure((size_t)(np + 31) / 32));
+      // the map is valid for one plane pair at one image size
+      const bool vfresh = f->vdirty_for[0] != f->vplane_d.p || f->vdirty_for[1] != f->vplane_id.p ||
+                          f->vdirty_for[2] != f->vdirty.p || f->vdirty_px != np;
+      FVV_TRY(7, fvv_rasterize_tracked(virt, 1, f->verts.as<double>(), nv, nv_dev,
+                                       f->tris.as<int32_t>(), nt_ub, ntri_dev,
+                                       f->vplane_d.as<double>(), &off0, f->vplane_id.as<int32_t>(),
+                                       f->vraster_ws.p, f->vraster_ws.cap,
+                                       f->vdirty.as<uint8_t>(), vfresh, st));
+      f->vdirty_for[0] = f->vplane_d.p;
+      f->vdirty_for[1] = f->vplane_id.p;
+      f->vdirty_for[2] = f->vdirty.p;
+      f->vdirty_px = np;
+      std::vector<int32_t> rank_id(ncam);
+      for (int r = 0; r < ncam; ++r) rank_id[r] = f->cams[rank_pos[r]].id;
+      FVV_TRY(7, f->src.ensure(4 * (size_t)(nt_ub > 0 ? nt_ub : 1)));
+      FVV_TRY(7, fvv_triangle_sources(rank_pos, rank_id.data(), ncam, f->vis.as<uint32_t>(),
+                                      f->vis_stride, nt_ub, ntri_dev, f->src.as<int32_t>(), st));
+      FVV_TRY(7, f->rcounts.ensure(8 * (size_t)(1 + ncam)));
+      FVV_TRY(7, fvv_render_count(f->cams.data(), ncam, virt, f->vplane_id.as<int32_t>(),
+                                  f->src.as<int32_t>(), f->rcounts.as<int64_t>(), st));
+      FVV_TRY(7, render_view_coded_bound(f->cams.data(), ncam, frames_dev, frame_off, in, virt,
+                                         f->vplane_d.as<double>(), f->vplane_id.as<int32_t>(),
+                                         f->src.as<int32_t>(), fallback, f->color.as<uint8_t>(),
+                                         f->source.as<int32_t>(), f->covered.as<uint8_t>(),
+                                         f->code.as<int8_t>(), f->rcounts.as<int64_t>(), st));
+    } else {
+      cudaMemsetAsync(f->code.p, 0xfe, (size_t)np, st);  // -2: nothing covered
+      cudaMemsetAsync(f->color.p, 0, 3 * (size_t)np, st);
+      cudaMemsetAsync(f->source.p, 0xff, 4 * (size_t)np, st);
+      cudaMemsetAsync(f->covered.p, 0, (size_t)np, st);
+    }
+  }
+  stage_mark(f, 7, st);
+
+  return FVV_OK;
+}
+
+static int run_host_planned(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt,
                   const int32_t *rank_pos, const uint8_t *frames_dev, const int64_t *frame_off,
                   const uint8_t *fallback, void *stream, fvv_frame_stats *out_stats,
                   int *out_stage) {
@@ -336,23 +651,8 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
   if (out_stage) *out_stage = 0;
   memset(&f->stats, 0, sizeof(f->stats));
   fvv_frame_stats &S = f->stats;
-  cudaEventRecord(f->ev[0], st);
-
-  // ---- B-1 sparse carve (pipeline.py:154-157) ----
+  FVV_TRY(1, enqueue_b12(f, masks_dev, nullptr, st, out_stage));
   const fvv_grid &G = f->coarse;
-  const int64_t nvox_c = G.dims[0] * G.dims[1] * G.dims[2];
-  S.sparse_tests = nvox_c;
-  FVV_TRY(1, fvv_pack_silhouettes(f->cams.data(), ncam, masks_dev, f->mask_off.data(),
-                                  f->sil.as<uint32_t>(), f->word_off.data(), st));
-  const int64_t zero = 0;
-  FVV_TRY(1, fvv_carve(f->cams.data(), ncam, f->sil.as<uint32_t>(), f->word_off.data(), &G, 1,
-                       &zero, cfg.min_views, f->occ_c.as<uint32_t>(), f->cnt_c.as<int64_t>(),
-                       f->carve_ws.p, f->carve_ws.cap, st));
-  cudaEventRecord(f->ev[1], st);
-
-  // ---- B-2 CCL, noise filter, ROIs (pipeline.py:159-166) ----
-  FVV_TRY(2, fvv_ccl26(f->occ_c.as<uint32_t>(), &G, f->ccl_ws.p, f->ccl_ws.cap,
-                       f->comps.as<fvv_component>(), 4096, f->ccl_counts.as<int64_t>(), st));
   int64_t *hs = (int64_t *)f->host_small;
   readback(f, st, {{f->ccl_counts.p, 0, 16, nullptr, 0, 0},
                    {f->cnt_c.p, 16, 8, nullptr, 0, 0},
@@ -401,7 +701,7 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
     for (int j = 0; j < 3; ++j) f->roi_box.push_back(hi[j]);
   }
   S.components = (int64_t)f->roi_component.size();
-  cudaEventRecord(f->ev[2], st);
+  stage_mark(f, 2, st);
 
   // ---- B-3 dense carve (pipeline.py:168-173) ----
   const int nroi = (int)f->roi_component.size();
@@ -416,6 +716,18 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
     f->fine_word_off[r] = fw;
     fw += (n + 31) / 32;
   }
+  f->seen_words = fw;
+  f->seen_tiles = f->seen_tw = 0;
+  for (int r = 0; r < nroi; ++r) {
+    uint32_t tx, ty;
+    int64_t tiles;
+    carve_grid_tiles(f->fine[r], 4, tx, ty, tiles);
+    MeshGridInfo gi;
+    f->seen_tiles += tiles;
+    f->seen_tw += mesh_grid_info(f->fine[r], 0, 0, gi);
+  }
+  f->seen_plannable = nroi <= FVV_MAX_GRIDS && ncomp <= 4096;
+  f->seen_v = f->seen_s = 0;
   FVV_TRY(3, f->occ_f.ensure(4 * (size_t)(fw > 0 ? fw : 1)));
   FVV_TRY(3, f->cnt_f.ensure(8 * (size_t)(nroi > 0 ? nroi : 1)));
   for (int r0 = 0; r0 < nroi; r0 += FVV_MAX_GRIDS) {
@@ -425,7 +737,7 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
                          f->occ_f.as<uint32_t>(), f->cnt_f.as<int64_t>() + r0, f->carve_ws.p,
                          f->carve_ws.cap, st));
   }
-  cudaEventRecord(f->ev[3], st);
+  stage_mark(f, 3, st);
 
   // ---- C polygonize every ROI (pipeline.py:175-190) ----
   f->info.assign(8 * (size_t)nroi, 0);
@@ -446,6 +758,8 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
       return cuda_check("fvv_frame_run C");
     }
     const int64_t nv = hs[0], ns = hs[1];
+    f->seen_v = nv;  // (single-batch frames: the device planner's capacities)
+    f->seen_s = ns;
     const size_t sb = fvv_mesh_emit_scratch_bytes(nv, ns);
     FVV_TRY(4, f->mesh_scratch.ensure(sb));
     // vertices / triangles of all batches share one array; keep prior batches
@@ -492,7 +806,7 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
       f->nt = t_before + 5 * ns;  // upper bound until the final read
     }
   }
-  cudaEventRecord(f->ev[4], st);
+  stage_mark(f, 4, st);
 
   // device-side total triangle count for D-1 / D-2 / E (no host round trip)
   int64_t *ntri_dev = f->ntri.as<int64_t>();
@@ -503,80 +817,9 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
   const int64_t nt_ub = f->nt;
   f->vis_stride = (nt_ub + 31) / 32 > 0 ? (nt_ub + 31) / 32 : 1;
 
-  // ---- D-1 depth images, D-2 visibility (pipeline.py:198-207) ----
   const bool have_mesh = f->nv > 0 && nt_ub > 0;
-  if (have_mesh) {
-    FVV_TRY(5, f->depth.ensure(8 * (size_t)f->planes));
-    FVV_TRY(5, f->dirty.ensure((size_t)(f->planes + 31) / 32));
-    const size_t rwb = fvv_raster_workspace_bytes(f->nv, nt_ub, ncam);
-    FVV_TRY(5, f->raster_ws.ensure(rwb));
-    const bool fresh = f->dirty_for[0] != f->depth.p || f->dirty_for[1] != f->dirty.p;
-    FVV_TRY(5, fvv_rasterize_tracked(f->cams.data(), ncam, f->verts.as<double>(), f->nv,
-                                     f->tris.as<int32_t>(), nt_ub, ntri_dev,
-                                     f->depth.as<double>(), f->plane_off.data(), nullptr,
-                                     f->raster_ws.p, f->raster_ws.cap, f->dirty.as<uint8_t>(),
-                                     fresh, st));
-    f->dirty_for[0] = f->depth.p;  // new planes or map: filled once above
-    f->dirty_for[1] = f->dirty.p;
-  }
-  cudaEventRecord(f->ev[5], st);
-  FVV_TRY(6, f->vis.ensure(4 * (size_t)ncam * f->vis_stride));
-  cudaMemsetAsync(f->vis.p, 0, 4 * (size_t)ncam * f->vis_stride, st);
-  if (have_mesh)
-    FVV_TRY(6, fvv_classify(f->cams.data(), ncam, f->verts.as<double>(), f->tris.as<int32_t>(),
-                            nt_ub, ntri_dev, f->depth.as<double>(), f->plane_off.data(),
-                            cfg.t_v, f->vis.as<uint32_t>(), f->vis_stride, st));
-  cudaEventRecord(f->ev[6], st);
-
-  // ---- E: one virtual view (render.py:64-113) ----
-  f->virt_px = 0;
-  if (virt) {
-    const int64_t np = (int64_t)virt->width * virt->height;
-    f->virt_px = np;
-    FVV_TRY(7, f->color.ensure(3 * (size_t)np));
-    FVV_TRY(7, f->source.ensure(4 * (size_t)np));
-    FVV_TRY(7, f->covered.ensure((size_t)np));
-    FVV_TRY(7, f->code.ensure((size_t)np));
-    if (have_mesh) {
-      FVV_TRY(7, f->vplane_d.ensure(8 * (size_t)np));
-      FVV_TRY(7, f->vplane_id.ensure(4 * (size_t)np));
-      const size_t vwb = fvv_raster_workspace_bytes(f->nv, nt_ub, 1);
-      FVV_TRY(7, f->vraster_ws.ensure(vwb));
-      const int64_t off0 = 0;
-      FVV_TRY(7, f->vdirty.ensure((size_t)(np + 31) / 32));
-      // the map is valid for one plane pair at one image size
-      const bool vfresh = f->vdirty_for[0] != f->vplane_d.p || f->vdirty_for[1] != f->vplane_id.p ||
-                          f->vdirty_for[2] != f->vdirty.p || f->vdirty_px != np;
-      FVV_TRY(7, fvv_rasterize_tracked(virt, 1, f->verts.as<double>(), f->nv,
-                                       f->tris.as<int32_t>(), nt_ub, ntri_dev,
-                                       f->vplane_d.as<double>(), &off0, f->vplane_id.as<int32_t>(),
-                                       f->vraster_ws.p, f->vraster_ws.cap,
-                                       f->vdirty.as<uint8_t>(), vfresh, st));
-      f->vdirty_for[0] = f->vplane_d.p;
-      f->vdirty_for[1] = f->vplane_id.p;
-      f->vdirty_for[2] = f->vdirty.p;
-      f->vdirty_px = np;
-      std::vector<int32_t> rank_id(ncam);
-      for (int r = 0; r < ncam; ++r) rank_id[r] = f->cams[rank_pos[r]].id;
-      FVV_TRY(7, f->src.ensure(4 * (size_t)(nt_ub > 0 ? nt_ub : 1)));
-      FVV_TRY(7, fvv_triangle_sources(rank_pos, rank_id.data(), ncam, f->vis.as<uint32_t>(),
-                                      f->vis_stride, nt_ub, ntri_dev, f->src.as<int32_t>(), st));
-      FVV_TRY(7, f->rcounts.ensure(8 * (size_t)(1 + ncam)));
-      FVV_TRY(7, fvv_render_count(f->cams.data(), ncam, virt, f->vplane_id.as<int32_t>(),
-                                  f->src.as<int32_t>(), f->rcounts.as<int64_t>(), st));
-      FVV_TRY(7, fvv_render_view_coded(f->cams.data(), ncam, frames_dev, frame_off, virt,
-                                       f->vplane_d.as<double>(), f->vplane_id.as<int32_t>(),
-                                       f->src.as<int32_t>(), fallback, f->color.as<uint8_t>(),
-                                       f->source.as<int32_t>(), f->covered.as<uint8_t>(),
-                                       f->code.as<int8_t>(), f->rcounts.as<int64_t>(), st));
-    } else {
-      cudaMemsetAsync(f->code.p, 0xfe, (size_t)np, st);  // -2: nothing covered
-      cudaMemsetAsync(f->color.p, 0, 3 * (size_t)np, st);
-      cudaMemsetAsync(f->source.p, 0xff, 4 * (size_t)np, st);
-      cudaMemsetAsync(f->covered.p, 0, (size_t)np, st);
-    }
-  }
-  cudaEventRecord(f->ev[7], st);
+  FVV_TRY(5, enqueue_tail(f, virt, rank_pos, frames_dev, frame_off, fallback, st, out_stage, f->nv,
+                          nullptr, nt_ub, ntri_dev, have_mesh, nullptr));
 
   // ---- final counters (one read) ----
   int64_t *h = hs;
@@ -597,7 +840,7 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
                      rc_piece});
   else
     readback(f, st, {{ntri_dev, 0, 8, nullptr, 0, 0}, rc_piece});
-  cudaEventRecord(f->ev[8], st);
+  stage_mark(f, 8, st);
   if (cudaStreamSynchronize(st) != cudaSuccess) {
     if (out_stage) *out_stage = 8;
     return cuda_check("fvv_frame_run");
@@ -631,6 +874,332 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
   if (out_stats) *out_stats = S;
   return cuda_check("fvv_frame_run");
 }
+
+// ---- device-planned frames -------------------------------------------------
+// B-1 .. E enqueued without a host round trip: the planner kernel replaces the
+// host's ROI step, B-3 / C run over its tables with capacities taken from the
+// sizes seen so far (x1.25), and one final read brings back every count. A
+// frame the planner does not take, or one that outgrows a capacity, is redone
+// by the host-planned path (which also sets the capacities).
+constexpr size_t kDs = 800 * 1024;  // mapped-block region of the device-planned read
+constexpr size_t kDsRCounts = 128, kDsComp = 1024, kDsBox = 2048, kDsGrid = 8192,
+                 kDsCntF = 16384, kDsInfo = 17408;
+
+static int enqueue_device_planned(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt,
+                                  const int32_t *rank_pos, const uint8_t *frames_dev,
+                                  const int64_t *frame_off, const uint8_t *fallback,
+                                  cudaStream_t st, int *out_stage) {
+  const fvv_frame_config &cfg = f->cfg;
+  const int ncam = f->ncam;
+  const fvv_frame::Caps &K = f->caps;
+  FVV_TRY(1, enqueue_b12(f, masks_dev, f->inputs.as<FrameInputs>(), st, out_stage));
+  // ---- B-2 noise filter + ROIs on the device (pipeline.py:159-166) ----
+  FVV_TRY(2, f->plan.ensure(sizeof(FramePlan)));
+  FramePlan *P = f->plan.as<FramePlan>();
+  PlanArgs pa;
+  pa.coarse = f->coarse;
+  pa.roi_margin = cfg.roi_margin;
+  pa.fine_spacing = cfg.fine_spacing;
+  pa.t_large = cfg.t_large;
+  pa.t_small = cfg.t_small;
+  pa.budget = cfg.budget;
+  pa.comp_cap = 4096;
+  pa.cap_words = K.words;
+  pa.cap_tiles = K.tiles;
+  pa.cap_tw = K.tw;
+  frame_plan_kernel<<<1, kPlanThreads, 0, st>>>(pa, f->comps.as<fvv_component>(),
+                                                f->ccl_counts.as<int64_t>(), P);
+  note_launches(1);
+  stage_mark(f, 2, st);
+  // ---- B-3 dense carve over the planned grids ----
+  FVV_TRY(3, f->occ_f.ensure(4 * (size_t)K.words));
+  FVV_TRY(3, f->cnt_f.ensure(8 * (size_t)FVV_MAX_GRIDS));
+  FVV_TRY(3, carve_batch(f->cams.data(), ncam, f->sil.as<uint32_t>(), f->word_off.data(),
+                         &P->carve, FVV_MAX_GRIDS, 4, K.tiles, cfg.min_views,
+                         f->occ_f.as<uint32_t>(), f->cnt_f.as<int64_t>(), f->carve_ws.p,
+                         f->carve_ws.cap, st));
+  stage_mark(f, 3, st);
+  // ---- C polygonize ----
+  FVV_TRY(4, f->mesh_ws.ensure(mesh_ws_bytes(K.tw, FVV_MAX_GRIDS)));
+  FVV_TRY(4, mesh_prepare_batch(&P->mesh, K.tw, FVV_MAX_GRIDS, f->occ_f.as<uint32_t>(),
+                                f->mesh_ws.p, f->mesh_ws.cap, st));
+  FVV_TRY(4, f->mesh_scratch.ensure(mesh_emit_scratch(K.v, K.s)));
+  FVV_TRY(4, f->verts.ensure(24 * (size_t)K.v));
+  FVV_TRY(4, f->tris.ensure(12 * (size_t)(5 * K.s)));
+  FVV_TRY(4, mesh_emit_batch(f->cams_by_id.data(), ncam, f->sil.as<uint32_t>(),
+                             f->word_off_by_id.data(), &P->mesh, K.tw, FVV_MAX_GRIDS, cfg.exact,
+                             cfg.fixed_isovalue, f->mesh_ws.p, f->mesh_ws.cap, K.v, K.s,
+                             f->mesh_scratch.p, f->mesh_scratch.cap, f->verts.as<double>(),
+                             f->tris.as<int32_t>(), st));
+  stage_mark(f, 4, st);
+  int64_t *totals = mesh_ws_totals(f->mesh_ws.p, K.tw, FVV_MAX_GRIDS);  // V, S, T
+  const int64_t nt_ub = 5 * K.s;
+  f->vis_stride = (nt_ub + 31) / 32 > 0 ? (nt_ub + 31) / 32 : 1;
+  FVV_TRY(5, enqueue_tail(f, virt, rank_pos, frames_dev, frame_off, fallback, st, out_stage, K.v,
+                          totals, nt_ub, totals + 2, true, f->inputs.as<FrameInputs>()));
+  // ---- every count in one read ----
+  const int64_t *nroi = &P->nroi;
+  readback(f, st, {{f->ccl_counts.p, kDs, 16, nullptr, 0, 0},
+                   {f->cnt_c.p, kDs + 16, 8, nullptr, 0, 0},
+                   {P, kDs + 32, 32, nullptr, 0, 0},  // status, nroi, dense_tests, fine_words
+                   {totals, kDs + 64, 24, nullptr, 0, 0},
+                   {virt ? f->rcounts.p : totals, kDs + kDsRCounts,
+                    virt ? 8 * (int64_t)(1 + ncam) : 0, nullptr, 0, 0},
+                   {P->roi_component, kDs + kDsComp, 0, nroi, 8, FVV_MAX_GRIDS},
+                   {P->roi_box, kDs + kDsBox, 0, nroi, 48, FVV_MAX_GRIDS},
+                   {P->carve.grids, kDs + kDsGrid, 0, nroi, (int64_t)sizeof(fvv_grid),
+                    FVV_MAX_GRIDS},
+                   {f->cnt_f.p, kDs + kDsCntF, 0, nroi, 8, FVV_MAX_GRIDS},
+                   {mesh_ws_info(f->mesh_ws.p, K.tw, FVV_MAX_GRIDS), kDs + kDsInfo, 0, nroi, 64,
+                    FVV_MAX_GRIDS}});
+  stage_mark(f, 8, st);
+  return FVV_OK;
+}
+
+// After the frame's synchronisation: host state and stats from the final
+// read. False when the host-planned path must redo the frame.
+static bool finish_device_planned(fvv_frame *f, bool colour) {
+  const char *hb = (const char *)f->host_small + kDs;
+  const int64_t *h = (const int64_t *)hb;
+  const int64_t status = h[4], nroi = h[5], V = h[8], Sn = h[9], T = h[10];
+  if (status != 0 || V > f->caps.v || Sn > f->caps.s) {
+    static const bool dbg = getenv("FVV_PLAN_DEBUG") != nullptr;
+    if (dbg)
+      fprintf(stderr, "fvv: device-planned frame redone on the host: status %lld nroi %lld "
+              "V %lld/%lld S %lld/%lld words %lld/%lld\n", (long long)status, (long long)nroi,
+              (long long)V, (long long)f->caps.v, (long long)Sn, (long long)f->caps.s,
+              (long long)h[7], (long long)f->caps.words);
+    return false;
+  }
+  fvv_frame_stats &S = f->stats;
+  S.sparse_occupied = h[2];
+  S.components = nroi;
+  S.dense_tests = h[6];
+  S.n_rois = nroi;
+  S.vertices = V;
+  S.triangles = T;
+  f->nv = V;
+  f->nt = T;
+  const int64_t *comp = (const int64_t *)(hb + kDsComp);
+  const double *box = (const double *)(hb + kDsBox);
+  const fvv_grid *grid = (const fvv_grid *)(hb + kDsGrid);
+  const int64_t *cnt = (const int64_t *)(hb + kDsCntF);
+  const int64_t *info = (const int64_t *)(hb + kDsInfo);
+  f->roi_component.assign(comp, comp + nroi);
+  f->roi_box.assign(box, box + 6 * nroi);
+  f->fine.assign(grid, grid + nroi);
+  f->info.assign(info, info + 8 * nroi);
+  f->fine_word_off.clear();
+  for (int64_t r = 0; r < nroi; ++r) {
+    S.dense_occupied += cnt[r];
+    S.fallback_edges += info[8 * r + 6];
+    S.inconsistent_edge_starts += info[8 * r + 7];
+  }
+  if (!f->cfg.exact) S.fallback_edges = S.inconsistent_edge_starts = 0;
+  if (colour) {
+    const int64_t *rcn = (const int64_t *)(hb + kDsRCounts);
+    S.covered_px = rcn[0];
+    for (int c = 0; c < f->ncam; ++c) S.sourced_px += rcn[1 + c];
+  }
+  for (int e = 0; e < 8; ++e)
+    if (cudaEventElapsedTime(&S.ms[e], f->ev[e], f->ev[e + 1]) != cudaSuccess) S.ms[e] = 0.0f;
+  cudaGetLastError();
+  return true;
+}
+
+static int64_t with_headroom(int64_t need) { return need + need / 4 + 1024; }
+
+// capacities for the next device-planned frames (grown only: buffers and a
+// captured graph stay valid while they hold)
+static void update_caps(fvv_frame *f, int64_t words, int64_t tiles, int64_t tw, int64_t v,
+                        int64_t sn) {
+  fvv_frame::Caps &K = f->caps;
+  bool grew = false;
+  auto fit = [&grew](int64_t need, int64_t &cap) {
+    if (need > cap - cap / 16 || cap == 0) {  // within 6 % of the capacity: grow now
+      cap = with_headroom(need > cap ? need : cap);
+      grew = true;
+    }
+  };
+  fit(words, K.words);
+  fit(tiles, K.tiles);
+  fit(tw, K.tw);
+  fit(v, K.v);
+  fit(sn, K.s);
+  if (K.tiles > (int64_t)1 << 19) K.tiles = (int64_t)1 << 19;  // carve's split-mode tile cap
+  K.ready = true;
+  if (grew) f->caps_grown = true;  // buffers re-sized before the next device-planned frame
+  if (grew && f->graph) {  // the graph's launches were sized for the old capacities
+    cudaGraphExecDestroy(f->graph);
+    f->graph = nullptr;
+    f->graph_key.clear();
+  }
+}
+
+// The device-planned frame's buffers at the current capacities, allocated
+// before the frame is enqueued (never while a captured graph could use them;
+// the previous frame's outputs are dropped, as any new frame drops them).
+static void reserve_buffers(fvv_frame *f) {
+  const fvv_frame::Caps &K = f->caps;
+  {
+    const int64_t nt_ub = 5 * K.s;
+    f->occ_f.ensure(4 * (size_t)K.words);
+    f->cnt_f.ensure(8 * (size_t)FVV_MAX_GRIDS);
+    f->mesh_ws.ensure(mesh_ws_bytes(K.tw, FVV_MAX_GRIDS));
+    f->mesh_scratch.ensure(mesh_emit_scratch(K.v, K.s));
+    f->verts.ensure(24 * (size_t)K.v);
+    f->tris.ensure(12 * (size_t)nt_ub);
+    f->raster_ws.ensure(fvv_raster_workspace_bytes(K.v, nt_ub, f->ncam));
+    f->vraster_ws.ensure(fvv_raster_workspace_bytes(K.v, nt_ub, 1));
+    f->vis.ensure(4 * (size_t)f->ncam * ((nt_ub + 31) / 32 > 0 ? (nt_ub + 31) / 32 : 1));
+    f->src.ensure(4 * (size_t)(nt_ub > 0 ? nt_ub : 1));
+    f->plan.ensure(sizeof(FramePlan));
+    f->inputs.ensure(sizeof(FrameInputs));
+  }
+  f->caps_grown = false;
+}
+
+// What a captured frame graph bakes in: the virtual camera, ranks, fallback
+// colour, stream, capacities and the masks' alignment class (the masks and
+// frame pointers are bound per frame through FrameInputs).
+static std::vector<char> graph_key(const fvv_frame *f, const uint8_t *masks_dev,
+                                   const fvv_camera *virt, const int32_t *rank_pos,
+                                   const uint8_t *frames_dev, const int64_t *frame_off,
+                                   const uint8_t *fallback, cudaStream_t st) {
+  std::vector<char> k;
+  auto put = [&k](const void *p, size_t n) {
+    const char *c = (const char *)p;
+    k.insert(k.end(), c, c + n);
+  };
+  const char wide = ((uintptr_t)masks_dev & 15) == 0;  // the pack kernel's variant
+  put(&wide, 1);
+  put(&st, sizeof(st));
+  put(&f->caps, sizeof(f->caps));
+  const char has_virt = virt != nullptr;
+  put(&has_virt, 1);
+  if (virt) {
+    put(virt, sizeof(*virt));
+    put(rank_pos, sizeof(int32_t) * f->ncam);
+    put(fallback, 3);
+  }
+  return k;
+}
+
+static bool graphs_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("FVV_FRAME_GRAPH");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+static bool device_planning_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("FVV_DEVICE_PLAN");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// One device-planned frame: a plain enqueue, a graph capture (the second
+// frame with the same bindings) or a graph replay. True when it completed.
+static int run_device_planned(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt,
+                              const int32_t *rank_pos, const uint8_t *frames_dev,
+                              const int64_t *frame_off, const uint8_t *fallback, cudaStream_t st,
+                              int *out_stage, bool &done) {
+  done = false;
+  memset(&f->stats, 0, sizeof(f->stats));
+  if (out_stage) *out_stage = 0;
+  if (f->caps_grown) reserve_buffers(f);
+  const bool graphs = graphs_enabled() && st != nullptr && st != cudaStreamLegacy &&
+                      st != cudaStreamPerThread;
+  std::vector<char> key;
+  if (graphs) key = graph_key(f, masks_dev, virt, rank_pos, frames_dev, frame_off, fallback, st);
+  {  // this frame's input pointers, read by the pack and colour kernels
+    if (f->inputs.ensure(sizeof(FrameInputs))) return FVV_E_CUDA;
+    static thread_local FrameInputs in;
+    memset(&in, 0, sizeof(in));
+    in.masks = masks_dev;
+    in.frames = frames_dev;
+    if (virt && frame_off)
+      for (int c = 0; c < f->ncam; ++c) in.frame_off[c] = frame_off[c];
+    bind_inputs_kernel<<<1, 32, 0, st>>>(in, f->inputs.as<FrameInputs>());
+    note_launches(1);
+  }
+  if (graphs && f->graph && key == f->graph_key) {
+    f->stats.sparse_tests = f->coarse.dims[0] * f->coarse.dims[1] * f->coarse.dims[2];
+    f->virt_px = virt ? (int64_t)virt->width * virt->height : 0;
+    const int64_t nt_ub = 5 * f->caps.s;
+    f->vis_stride = (nt_ub + 31) / 32 > 0 ? (nt_ub + 31) / 32 : 1;
+    if (cudaGraphLaunch(f->graph, st) != cudaSuccess) return cuda_check("fvv_frame_run graph");
+    note_launches(f->graph_launches);
+  } else if (graphs && key == f->pending_key) {
+    // second frame with these bindings (buffers and dirty maps settled by the
+    // first): capture the frame once, then replay it
+    if (f->graph) cudaGraphExecDestroy(f->graph);
+    f->graph = nullptr;
+    f->graph_key.clear();
+    const long long n0 = fvv_launch_count();
+    if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+      return cuda_check("fvv_frame_run capture");
+    const int rc = enqueue_device_planned(f, masks_dev, virt, rank_pos, frames_dev, frame_off,
+                                          fallback, st, out_stage);
+    cudaGraph_t g = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(st, &g);
+    if (rc != FVV_OK) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (ec != cudaSuccess || cudaGraphInstantiate(&f->graph, g, 0) != cudaSuccess) {
+      if (g) cudaGraphDestroy(g);
+      f->graph = nullptr;
+      return cuda_check("fvv_frame_run graph capture");
+    }
+    cudaGraphDestroy(g);
+    f->graph_key = key;
+    f->graph_launches = fvv_launch_count() - n0;
+    if (cudaGraphLaunch(f->graph, st) != cudaSuccess) return cuda_check("fvv_frame_run graph");
+  } else {
+    FVV_TRY(0, enqueue_device_planned(f, masks_dev, virt, rank_pos, frames_dev, frame_off,
+                                      fallback, st, out_stage));
+    if (graphs) f->pending_key = key;
+  }
+  if (cudaStreamSynchronize(st) != cudaSuccess) {
+    if (out_stage) *out_stage = 8;
+    return cuda_check("fvv_frame_run");
+  }
+  done = finish_device_planned(f, virt != nullptr);
+  if (done) {
+    const int64_t *h = (const int64_t *)((const char *)f->host_small + kDs);
+    // (tiles / k-row words of this frame are not read back: their
+    // capacities grow through a host-planned frame when the planner reports one)
+    update_caps(f, h[7], 0, 0, h[8], h[9]);
+  }
+  return cuda_check("fvv_frame_run");
+}
+
+int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt,
+                  const int32_t *rank_pos, const uint8_t *frames_dev, const int64_t *frame_off,
+                  const uint8_t *fallback, void *stream, fvv_frame_stats *out_stats,
+                  int *out_stage) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (f->caps.ready && device_planning_enabled()) {
+    bool done = false;
+    const int rc = run_device_planned(f, masks_dev, virt, rank_pos, frames_dev, frame_off,
+                                      fallback, st, out_stage, done);
+    if (rc != FVV_OK) return rc;
+    if (done) {
+      if (out_stats) *out_stats = f->stats;
+      return FVV_OK;
+    }
+  }
+  const int rc = run_host_planned(f, masks_dev, virt, rank_pos, frames_dev, frame_off, fallback,
+                                  stream, out_stats, out_stage);
+  if (rc == FVV_OK && f->seen_plannable)
+    update_caps(f, f->seen_words, f->seen_tiles, f->seen_tw, f->seen_v, f->seen_s);
+  return rc;
+}
+
 
 int fvv_frame_get_outputs(const fvv_frame *f, fvv_frame_outputs *o) {
   memset(o, 0, sizeof(*o));

@@ -118,6 +118,30 @@ __device__ __forceinline__ int64_t device_count(const int64_t *p, int64_t fallba
   return v;
 }
 
+// Per-frame input pointers of a device-planned (graph-captured) frame, read
+// by the kernels from device memory so one captured frame serves new inputs:
+// the masks (pack) and the colour frames (render), camera c's frame at
+// frames + frame_off[c].
+struct __align__(16) FrameInputs {
+  const uint8_t *masks;
+  const uint8_t *frames;
+  int64_t frame_off[FVV_MAX_CAMS];
+};
+
+// fvv_pack_silhouettes / fvv_render_view_coded with the masks / frames
+// pointers taken from *in (device) when in is non-null (masks_dev, frames_dev
+// and frame_off then only describe the alignment and the camera set).
+int pack_silhouettes_bound(const fvv_camera *cams, int ncam, const uint8_t *masks_dev,
+                           const FrameInputs *in, const int64_t *mask_off, uint32_t *sil_dev,
+                           const int64_t *sil_word_off, cudaStream_t st);
+int render_view_coded_bound(const fvv_camera *rig, int ncam, const uint8_t *frames_dev,
+                            const int64_t *frame_off, const FrameInputs *in,
+                            const fvv_camera *virt, const double *depth_dev,
+                            const int32_t *tri_id_dev, const int32_t *tri_src_dev,
+                            const uint8_t *fallback, uint8_t *color_dev, int32_t *source_dev,
+                            uint8_t *covered_dev, int8_t *code_dev, const int64_t *counts_dev,
+                            cudaStream_t st);
+
 // Grid table of one batched carve launch, in device memory (written by the
 // host wrapper's store launch, or on the device by the frame planner):
 // block b of the tile kernels carves tile b - blk_start[g] of the grid g

@@ -58,14 +58,23 @@ __device__ __forceinline__ void project_vertex(const RasterCams &C, const double
                                                                  __int_as_float(0x7fffffff));
 }
 
+// (camera, vertex) records for vertices i < nvd of a [ncam][nv] layout
+__device__ __forceinline__ void project_vertices(const RasterCams &C, const double *__restrict__ V,
+                                                 int64_t nv, int64_t nvd, int64_t tid,
+                                                 int64_t stride, double4 *__restrict__ proj,
+                                                 float2 *__restrict__ q) {
+  const bool gemv = nvd == 1;
+  const int64_t total = nv * C.ncam;
+  for (int64_t w = tid; w < total; w += stride)
+    if (w - (w / nv) * nv < nvd) project_vertex(C, V, nv, w, gemv, proj, q);
+}
+
 __global__ void raster_vertex_kernel(const __grid_constant__ RasterCams C,
                                      const double *__restrict__ V, int64_t nv,
-                                     double4 *__restrict__ proj, float2 *__restrict__ q) {
-  const bool gemv = nv == 1;
-  const int64_t total = nv * C.ncam;
-  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
-       w += (int64_t)gridDim.x * blockDim.x)
-    project_vertex(C, V, nv, w, gemv, proj, q);
+                                     const int64_t *nv_dev, double4 *__restrict__ proj,
+                                     float2 *__restrict__ q) {
+  project_vertices(C, V, nv, device_count(nv_dev, nv), blockIdx.x * (int64_t)blockDim.x + threadIdx.x,
+                   (int64_t)gridDim.x * blockDim.x, proj, q);
 }
 
 __device__ __forceinline__ double dmin3(double a, double b, double c) {
@@ -653,9 +662,9 @@ __device__ __forceinline__ void reset_dirty(unsigned long long *depth, int32_t *
 // vertices (FP64-bound), so the two overlap instead of running back to back.
 __global__ void raster_prep_kernel(const __grid_constant__ RasterCams C,
                                    const double *__restrict__ V, int64_t nv,
-                                   double4 *__restrict__ proj, float2 *__restrict__ q,
-                                   unsigned long long *depth, int32_t *ids, uint8_t *dirty,
-                                   int64_t npx, int nb_fill) {
+                                   const int64_t *nv_dev, double4 *__restrict__ proj,
+                                   float2 *__restrict__ q, unsigned long long *depth, int32_t *ids,
+                                   uint8_t *dirty, int64_t npx, int nb_fill) {
   if ((int)blockIdx.x < nb_fill) {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)nb_fill * blockDim.x;
@@ -665,12 +674,10 @@ __global__ void raster_prep_kernel(const __grid_constant__ RasterCams C,
       fill_u64(depth, npx, 0x7ff0000000000000ull, tid, stride);
     return;
   }
-  const bool gemv = nv == 1;
-  const int64_t total = nv * C.ncam;
-  const int64_t stride = (int64_t)(gridDim.x - nb_fill) * blockDim.x;
-  for (int64_t w = (blockIdx.x - nb_fill) * (int64_t)blockDim.x + threadIdx.x; w < total;
-       w += stride)
-    project_vertex(C, V, nv, w, gemv, proj, q);
+  if (nv > 0)
+    project_vertices(C, V, nv, device_count(nv_dev, nv),
+                     (blockIdx.x - nb_fill) * (int64_t)blockDim.x + threadIdx.x,
+                     (int64_t)(gridDim.x - nb_fill) * blockDim.x, proj, q);
 }
 
 __global__ void fill_u64_kernel(unsigned long long *p, int64_t n, unsigned long long v) {
@@ -790,6 +797,7 @@ struct RenderArgs {
   uint8_t *covered;
   int8_t *code;     // optional: -2 uncovered, -1 fallback colour, else source rig position
   int64_t *counts;  // [0] covered pixels, [1 + pos] pixels sourced from camera pos
+  const FrameInputs *in;  // when set: frames / frame_off from here (device)
 };
 
 __device__ __forceinline__ int cam_pos(const RenderArgs &A, int32_t id) {
@@ -851,7 +859,7 @@ __global__ void render_color_kernel(const __grid_constant__ RenderArgs A) {
         const int x0 = (int)floor(u), y0 = (int)floor(v);
         const int x1 = min(x0 + 1, w - 1), y1 = min(y0 + 1, h - 1);
         const double fx = u - (double)x0, fy = v - (double)y0;
-        const uint8_t *img = A.frames + A.frame_off[c];
+        const uint8_t *img = A.in ? A.in->frames + A.in->frame_off[c] : A.frames + A.frame_off[c];
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) {
           const double a = img[((int64_t)y0 * w + x0) * 3 + ch];
@@ -960,7 +968,8 @@ size_t fvv_raster_workspace_bytes(int64_t num_vertices, int64_t num_triangles, i
 // background except the 32-pixel tiles flagged in dirty[], which are reset;
 // full_reset fills everything and clears the flags instead (first use).
 static int rasterize_impl(const fvv_camera *cams, int ncam, const double *verts_dev, int64_t nv,
-                          const int32_t *tris_dev, int64_t nt, const int64_t *nt_dev,
+                          const int64_t *nv_dev, const int32_t *tris_dev, int64_t nt,
+                          const int64_t *nt_dev,
                           double *depth_dev, const int64_t *plane_off, int32_t *tri_id_dev,
                           void *ws_dev, size_t ws_bytes, uint8_t *dirty, bool full_reset,
                           cudaStream_t st) {
@@ -1021,15 +1030,16 @@ static int rasterize_impl(const fvv_camera *cams, int ncam, const double *verts_
     int64_t nb_fill = tracked ? total_px / (256 * 32 * 8) + 1 : total_px / (256 * 64) + 1;
     if (nb_fill > 148 * 8) nb_fill = 148 * 8;
     raster_prep_kernel<<<(int)(blocks + nb_fill), 256, 0, st>>>(
-        C, verts_dev, work ? nv : 0, proj, q, (unsigned long long *)(depth_dev + plane_off[0]),
+        C, verts_dev, work ? nv : 0, nv_dev, proj, q,
+        (unsigned long long *)(depth_dev + plane_off[0]),
         tracked ? tri_id_dev + plane_off[0] : nullptr, tracked ? dirty : nullptr, total_px,
         (int)nb_fill);
     note_launches(1);
   } else if (work) {
     int64_t blocks = (nv * ncam + 255) / 256;
     if (blocks > kRasterGrid) blocks = kRasterGrid;
-    raster_vertex_kernel<<<(int)blocks, 256, 0, st>>>(C, verts_dev, nv, (double4 *)(ws + L.proj),
-                                                     (float2 *)(ws + L.q));
+    raster_vertex_kernel<<<(int)blocks, 256, 0, st>>>(C, verts_dev, nv, nv_dev,
+                                                     (double4 *)(ws + L.proj), (float2 *)(ws + L.q));
     note_launches(1);
   }
   if (!work) return cuda_check("fvv_rasterize");
@@ -1075,12 +1085,14 @@ int fvv_rasterize(const fvv_camera *cams, int ncam, const double *verts_dev, int
                   const int32_t *tris_dev, int64_t nt, const int64_t *nt_dev, double *depth_dev,
                   const int64_t *plane_off, int32_t *tri_id_dev, void *ws_dev, size_t ws_bytes,
                   void *stream) {
-  return rasterize_impl(cams, ncam, verts_dev, nv, tris_dev, nt, nt_dev, depth_dev, plane_off,
-                        tri_id_dev, ws_dev, ws_bytes, nullptr, false, (cudaStream_t)stream);
+  return rasterize_impl(cams, ncam, verts_dev, nv, nullptr, tris_dev, nt, nt_dev, depth_dev,
+                        plane_off, tri_id_dev, ws_dev, ws_bytes, nullptr, false,
+                        (cudaStream_t)stream);
 }
 
 int fvv_rasterize_tracked(const fvv_camera *cams, int ncam, const double *verts_dev, int64_t nv,
-                          const int32_t *tris_dev, int64_t nt, const int64_t *nt_dev,
+                          const int64_t *nv_dev, const int32_t *tris_dev, int64_t nt,
+                          const int64_t *nt_dev,
                           double *depth_dev, const int64_t *plane_off, int32_t *tri_id_dev,
                           void *ws_dev, size_t ws_bytes, uint8_t *dirty_dev, int full_reset,
                           void *stream) {
@@ -1088,8 +1100,8 @@ int fvv_rasterize_tracked(const fvv_camera *cams, int ncam, const double *verts_
     set_error("fvv_rasterize_tracked: dirty map required");
     return FVV_E_ARG;
   }
-  return rasterize_impl(cams, ncam, verts_dev, nv, tris_dev, nt, nt_dev, depth_dev, plane_off,
-                        tri_id_dev, ws_dev, ws_bytes, dirty_dev, full_reset != 0,
+  return rasterize_impl(cams, ncam, verts_dev, nv, nv_dev, tris_dev, nt, nt_dev, depth_dev,
+                        plane_off, tri_id_dev, ws_dev, ws_bytes, dirty_dev, full_reset != 0,
                         (cudaStream_t)stream);
 }
 
@@ -1159,6 +1171,29 @@ static int fill_render(RenderArgs &A, const fvv_camera *rig, int ncam, const uin
   return FVV_OK;
 }
 
+}  // extern "C"
+
+int fvv::render_view_coded_bound(const fvv_camera *rig, int ncam, const uint8_t *frames_dev,
+                                 const int64_t *frame_off, const FrameInputs *in,
+                                 const fvv_camera *virt, const double *depth_dev,
+                                 const int32_t *tri_id_dev, const int32_t *tri_src_dev,
+                                 const uint8_t *fallback, uint8_t *color_dev,
+                                 int32_t *source_dev, uint8_t *covered_dev, int8_t *code_dev,
+                                 const int64_t *counts_dev, cudaStream_t st) {
+  static thread_local RenderArgs A;
+  int rc = fill_render(A, rig, ncam, frames_dev, frame_off, virt, depth_dev, tri_id_dev,
+                       tri_src_dev, fallback, color_dev, source_dev, covered_dev,
+                       const_cast<int64_t *>(counts_dev));
+  if (rc) return rc;
+  A.code = code_dev;
+  A.in = in;
+  render_color_kernel<<<kRasterGrid, 256, 0, st>>>(A);
+  note_launches(1);
+  return cuda_check("fvv_render_view");
+}
+
+extern "C" {
+
 int fvv_render_count(const fvv_camera *rig, int ncam, const fvv_camera *virt,
                      const int32_t *tri_id_dev, const int32_t *tri_src_dev, int64_t *counts_dev,
                      void *stream) {
@@ -1179,15 +1214,9 @@ int fvv_render_view_coded(const fvv_camera *rig, int ncam, const uint8_t *frames
                           const int32_t *tri_src_dev, const uint8_t *fallback,
                           uint8_t *color_dev, int32_t *source_dev, uint8_t *covered_dev,
                           int8_t *code_dev, const int64_t *counts_dev, void *stream) {
-  static thread_local RenderArgs A;
-  int rc = fill_render(A, rig, ncam, frames_dev, frame_off, virt, depth_dev, tri_id_dev,
-                       tri_src_dev, fallback, color_dev, source_dev, covered_dev,
-                       const_cast<int64_t *>(counts_dev));
-  if (rc) return rc;
-  A.code = code_dev;
-  render_color_kernel<<<kRasterGrid, 256, 0, (cudaStream_t)stream>>>(A);
-  note_launches(1);
-  return cuda_check("fvv_render_view");
+  return render_view_coded_bound(rig, ncam, frames_dev, frame_off, nullptr, virt, depth_dev,
+                                 tri_id_dev, tri_src_dev, fallback, color_dev, source_dev,
+                                 covered_dev, code_dev, counts_dev, (cudaStream_t)stream);
 }
 
 int fvv_render_view(const fvv_camera *rig, int ncam, const uint8_t *frames_dev,

@@ -290,10 +290,11 @@ def test_host_scene_generator_matches_device(gpu):
 
 
 def test_reused_executor_equals_fresh_executor(gpu):
-    """Depth planes of a re-used executor are reset per 32-pixel tile from the
-    previous frame's dirty map (fvv_rasterize_tracked), not refilled: after
+    """A re-used executor runs device-planned frames (planner kernel, no host
+    round trip; the third frame as a captured CUDA graph) and resets its
+    depth planes per 32-pixel tile from the previous frame's dirty map: after
     frames 4 -> 0 -> 7 on one executor, frame 7's depth planes, visibility,
-    mesh and virtual view equal those of a fresh executor (full fill)."""
+    mesh and virtual view equal those of a fresh (host-planned) executor."""
     import torch
 
     from paper_1903_11785_b200 import workloads
@@ -319,7 +320,42 @@ def test_reused_executor_equals_fresh_executor(gpu):
     s_b, b = run(FrameExecutor(wl.cfg, wl.rig), 7)
     assert s_a == s_b
     assert a.keys() == b.keys() and "depth" in a
+    words = (s_a["triangles"] + 31) // 32  # (the row stride is a capacity, not part of the result)
+    a["vis"], b["vis"] = a["vis"][:, :words], b["vis"][:, :words]
     for k in a:
         assert np.array_equal(a[k], b[k]), k
     d = a["depth"]
     assert np.isinf(d).any() and np.isfinite(d).any()
+
+
+def test_device_planner_falls_back_to_host_planning(gpu):
+    """An executor that device-plans its frames (after a host-planned first
+    frame) meets a frame with more ROIs than one planned batch holds
+    (FVV_MAX_GRIDS) and then one whose ROIs outgrow its capacities: both are
+    redone by the host-planned path and match the oracle; a small frame
+    after them is device-planned again and matches too."""
+    from paper_1903_11785_b200 import synthetic as S
+    from paper_1903_11785_b200.pipeline import PipelineConfig, run_frame
+
+    rig = S.ring_rig(8, (0, 0, 300), 6000, 5000, 640, 480, 700)
+    cfg = PipelineConfig(stage_lo=(-3000, -3000, 0), stage_hi=(3000, 3000, 600),
+                         coarse_spacing=50.0, fine_spacing=25.0, t_small=1)
+    few = [S.Ellipsoid(center=(x, 0.0, 150.0), semi_axes=(60.0, 60.0, 150.0))
+           for x in (-1500.0, 0.0, 1500.0)]
+    many = [S.Ellipsoid(center=(x, y, 150.0), semi_axes=(60.0, 60.0, 150.0))
+            for x in np.linspace(-2600, 2600, 14) for y in np.linspace(-2600, 2600, 14)]
+    big = [S.Ellipsoid(center=(x, 0.0, 250.0), semi_axes=(400.0, 400.0, 250.0))
+           for x in (-1500.0, 0.0, 1500.0)]
+    for objs in (few, few, few, many, big, few):
+        masks, _ = S.render_scene_device(rig, objs)
+        m_np = [m.cpu().numpy().astype(bool) for m in masks]
+        bundle = run_frame(cfg, rig, {c.id: None for c in rig}, sils=masks)
+        ref = O.run_frame(list(rig), m_np, cfg.stage_lo, cfg.stage_hi, cfg.coarse_spacing,
+                          cfg.fine_spacing, cfg.min_views, cfg.t_small, cfg.t_large,
+                          cfg.roi_margin, cfg.t_v)
+        assert bundle.stats == ref["stats"]
+        mv, mt, _ = ref["merged"]
+        assert np.array_equal(bundle.merged_mesh.vertices, mv)
+        assert np.array_equal(bundle.merged_mesh.triangles, mt)
+        for c in rig:
+            assert np.array_equal(bundle.visibility[c.id], ref["visibility"][c.id]), c.id
