@@ -582,10 +582,20 @@ static int enqueue_tail(fvv_frame *f, const fvv_camera *virt, const int32_t *ran
   stage_mark(f, 5, st);
   FVV_TRY(6, f->vis.ensure(4 * (size_t)ncam * f->vis_stride));
   cudaMemsetAsync(f->vis.p, 0, 4 * (size_t)ncam * f->vis_stride, st);
+  // (with a colour pass, the triangle sources of render.py:35-43 come out of
+  // the same launch)
+  std::vector<int32_t> rank_id(ncam);
+  const bool sources = virt && have_mesh;
+  if (sources) {
+    for (int r = 0; r < ncam; ++r) rank_id[r] = f->cams[rank_pos[r]].id;
+    FVV_TRY(6, f->src.ensure(4 * (size_t)(nt_ub > 0 ? nt_ub : 1)));
+  }
   if (have_mesh)
-    FVV_TRY(6, fvv_classify(f->cams.data(), ncam, f->verts.as<double>(), f->tris.as<int32_t>(),
-                            nt_ub, ntri_dev, f->depth.as<double>(), f->plane_off.data(),
-                            cfg.t_v, f->vis.as<uint32_t>(), f->vis_stride, st));
+    FVV_TRY(6, classify_sources(f->cams.data(), ncam, f->verts.as<double>(),
+                                f->tris.as<int32_t>(), nt_ub, ntri_dev, f->depth.as<double>(),
+                                f->plane_off.data(), cfg.t_v, f->vis.as<uint32_t>(),
+                                f->vis_stride, ncam, rank_pos, rank_id.data(),
+                                sources ? f->src.as<int32_t>() : nullptr, st));
   stage_mark(f, 6, st);
 
   // ---- E: one virtual view (render.py:64-113) ----
@@ -616,11 +626,6 @@ static int enqueue_tail(fvv_frame *f, const fvv_camera *virt, const int32_t *ran
       f->vdirty_for[1] = f->vplane_id.p;
       f->vdirty_for[2] = f->vdirty.p;
       f->vdirty_px = np;
-      std::vector<int32_t> rank_id(ncam);
-      for (int r = 0; r < ncam; ++r) rank_id[r] = f->cams[rank_pos[r]].id;
-      FVV_TRY(7, f->src.ensure(4 * (size_t)(nt_ub > 0 ? nt_ub : 1)));
-      FVV_TRY(7, fvv_triangle_sources(rank_pos, rank_id.data(), ncam, f->vis.as<uint32_t>(),
-                                      f->vis_stride, nt_ub, ntri_dev, f->src.as<int32_t>(), st));
       FVV_TRY(7, f->rcounts.ensure(8 * (size_t)(1 + ncam)));
       FVV_TRY(7, fvv_render_count(f->cams.data(), ncam, virt, f->vplane_id.as<int32_t>(),
                                   f->src.as<int32_t>(), f->rcounts.as<int64_t>(), st));

@@ -93,6 +93,49 @@ __device__ __forceinline__ bool project_rint(const fvv_camera &c, double x, doub
          (iv <= (double)(c.height - 1));
 }
 
+// project_rint with the perspective division in FP32: the float64 chain's
+// X, Y, Z (exact Z: the depth test needs it), then u, v from their float
+// roundings with one reciprocal, kept when u and v lie farther than a
+// rigorous bound (2^-19 relative: >= 2x the ~10 FP32 roundings involved, and
+// the float64 chain's own error) from a rounding boundary; the float64
+// divisions otherwise (near a tie, |u| >= 2^22, tiny Z).
+__device__ __forceinline__ float recip32(float z) {
+  const float r = __fdividef(1.0f, z);
+  return fmaf(r, fmaf(-z, r, 1.0f), r);
+}
+
+__device__ __forceinline__ bool project_rint32(const fvv_camera &c, double x, double y, double z,
+                                               bool gemv, double &iu, double &iv, double &zc) {
+  double X, Y, Z;
+  world_to_cam(c, x, y, z, gemv, X, Y, Z);
+  zc = Z;
+  if (!(Z > 0.0)) return false;  // (the float64 chain's frustum test needs Z > 0 too)
+  const float Zf = (float)Z, Xf = (float)X, Yf = (float)Y;
+  bool ok = Zf > 1e-30f;
+  const float r = recip32(ok ? Zf : 1.0f);
+  const float xn = Xf * r, yn = Yf * r;
+  const float fx = (float)c.fx, fy = (float)c.fy, cx = (float)c.cx, cy = (float)c.cy,
+              sk = (float)c.skew;
+  const float syn = sk * yn;
+  const float su = fx * (xn + syn), sv = fy * yn;
+  const float u = su + cx, v = sv + cy;
+  const float eu = 0x1p-19f * (fabsf(fx) * (fabsf(xn) + fabsf(syn)) + fabsf(cx) + fabsf(u) + 1.0f);
+  const float ev = 0x1p-19f * (fabsf(sv) + fabsf(cy) + fabsf(v) + 1.0f);
+  const float ru = rintf(u), rv = rintf(v);
+  ok = ok && fabsf(u) < 4194304.0f && fabsf(v) < 4194304.0f && fabsf(u - ru) < 0.5f - eu &&
+       fabsf(v - rv) < 0.5f - ev;
+  if (ok) {
+    iu = ru;
+    iv = rv;
+  } else {  // the float64 chain (project_exact, no distortion)
+    const double xe = X / Z, ye = Y / Z;
+    iu = rint(c.fx * (xe + c.skew * ye) + c.cx);
+    iv = rint(c.fy * ye + c.cy);
+  }
+  return (iu >= 0.0) && (iu <= (double)(c.width - 1)) && (iv >= 0.0) &&
+         (iv <= (double)(c.height - 1));
+}
+
 // voxels.py:52-56 voxel centre.
 __device__ __forceinline__ void voxel_center(const fvv_grid &g, int64_t i, int64_t j, int64_t k,
                                              double &x, double &y, double &z) {
@@ -141,6 +184,16 @@ int render_view_coded_bound(const fvv_camera *rig, int ncam, const uint8_t *fram
                             const uint8_t *fallback, uint8_t *color_dev, int32_t *source_dev,
                             uint8_t *covered_dev, int8_t *code_dev, const int64_t *counts_dev,
                             cudaStream_t st);
+
+// fvv_classify, plus (src_dev non-null) fvv_triangle_sources fused into it:
+// src_dev[t] = rank_id[r] of the first r with triangle t visible in rig
+// camera rank_pos[r], -1 if none.
+int classify_sources(const fvv_camera *cams, int ncam, const double *verts_dev,
+                     const int32_t *tris_dev, int64_t nt, const int64_t *nt_dev,
+                     const double *depth_dev, const int64_t *plane_off, double t_v,
+                     uint32_t *vis_dev, int64_t vis_stride_words, int nrank,
+                     const int32_t *rank_pos, const int32_t *rank_id, int32_t *src_dev,
+                     cudaStream_t st);
 
 // Grid table of one batched carve launch, in device memory (written by the
 // host wrapper's store launch, or on the device by the frame planner):

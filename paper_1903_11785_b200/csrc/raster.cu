@@ -696,12 +696,19 @@ struct ClassifyArgs {
   double t_v;
   uint32_t *vis;       // [ncam][stride] bits
   int64_t vis_stride;  // words per camera
+  // optional (render.py:35-43 triangle_sources, fused): the first ranked
+  // camera seeing each triangle, by rig position rank_pos[r] / id rank_id[r]
+  int32_t *src;
+  int nrank;
+  int32_t rank_pos[FVV_MAX_CAMS], rank_id[FVV_MAX_CAMS];
 };
 
-__global__ void classify_kernel(const __grid_constant__ RasterCams C, ClassifyArgs A) {
+__global__ void classify_kernel(const __grid_constant__ RasterCams C,
+                                const __grid_constant__ ClassifyArgs A) {
   // one thread per triangle, 32 consecutive triangles (one visibility word)
   // per warp: the centroid (three divisions) is computed once and projected
-  // into every camera, instead of once per (camera, triangle)
+  // into every camera, instead of once per (camera, triangle); the pixel
+  // rounding is certified in FP32 (project_rint32)
   const int64_t nt = device_count(A.nt_dev, A.nt);
   const bool gemv = nt == 1;
   const int lane = threadIdx.x & 31;
@@ -718,18 +725,29 @@ __global__ void classify_kernel(const __grid_constant__ RasterCams C, ClassifyAr
       my = ((a[1] + b[1]) + cc[1]) / 3.0;
       mz = ((a[2] + b[2]) + cc[2]) / 3.0;
     }
+    unsigned long long seen = 0;  // rig positions that see triangle t
     for (int c = 0; c < C.ncam; ++c) {
       bool vis = false;
       if (t < nt) {
         const fvv_camera &cam = C.cams[c];
         double iu, iv, z;
-        if (project_rint(cam, mx, my, mz, gemv, iu, iv, z)) {
+        if (project_rint32(cam, mx, my, mz, gemv, iu, iv, z)) {
           const int64_t p = (int64_t)iv * cam.width + (int64_t)iu;
           vis = (z - __ldg(A.depth + C.depth_off[c] + p)) <= A.t_v;
         }
       }
+      seen |= (unsigned long long)vis << c;
       const uint32_t bits = __ballot_sync(0xffffffffu, vis);
       if (lane == 0) A.vis[(int64_t)c * A.vis_stride + wi] = bits;
+    }
+    if (A.src != nullptr && t < nt) {
+      int32_t s = -1;
+      for (int r = 0; r < A.nrank; ++r)
+        if ((seen >> A.rank_pos[r]) & 1ull) {
+          s = A.rank_id[r];
+          break;
+        }
+      A.src[t] = s;
     }
   }
 }
@@ -1109,13 +1127,9 @@ int fvv_classify(const fvv_camera *cams, int ncam, const double *verts_dev,
                  const int32_t *tris_dev, int64_t nt, const int64_t *nt_dev,
                  const double *depth_dev, const int64_t *plane_off, double t_v,
                  uint32_t *vis_dev, int64_t vis_stride_words, void *stream) {
-  static thread_local RasterCams C;
-  int rc = fill_cams(C, cams, ncam, plane_off);
-  if (rc) return rc;
-  ClassifyArgs A{verts_dev, tris_dev, nt, nt_dev, depth_dev, t_v, vis_dev, vis_stride_words};
-  classify_kernel<<<kRasterGrid, 256, 0, (cudaStream_t)stream>>>(C, A);
-  note_launches(1);
-  return cuda_check("fvv_classify");
+  return classify_sources(cams, ncam, verts_dev, tris_dev, nt, nt_dev, depth_dev, plane_off, t_v,
+                          vis_dev, vis_stride_words, 0, nullptr, nullptr, nullptr,
+                          (cudaStream_t)stream);
 }
 
 int fvv_triangle_sources(const int32_t *rank_pos, const int32_t *rank_id, int nrank,
@@ -1172,6 +1186,40 @@ static int fill_render(RenderArgs &A, const fvv_camera *rig, int ncam, const uin
 }
 
 }  // extern "C"
+
+int fvv::classify_sources(const fvv_camera *cams, int ncam, const double *verts_dev,
+                          const int32_t *tris_dev, int64_t nt, const int64_t *nt_dev,
+                          const double *depth_dev, const int64_t *plane_off, double t_v,
+                          uint32_t *vis_dev, int64_t vis_stride_words, int nrank,
+                          const int32_t *rank_pos, const int32_t *rank_id, int32_t *src_dev,
+                          cudaStream_t st) {
+  static thread_local RasterCams C;
+  int rc = fill_cams(C, cams, ncam, plane_off);
+  if (rc) return rc;
+  if (nrank < 0 || nrank > FVV_MAX_CAMS) {
+    set_error("fvv_classify: %d ranked cameras", nrank);
+    return FVV_E_LIMIT;
+  }
+  static thread_local ClassifyArgs A;
+  memset(&A, 0, sizeof(A));
+  A.V = verts_dev;
+  A.T = tris_dev;
+  A.nt = nt;
+  A.nt_dev = nt_dev;
+  A.depth = depth_dev;
+  A.t_v = t_v;
+  A.vis = vis_dev;
+  A.vis_stride = vis_stride_words;
+  A.src = src_dev;
+  A.nrank = src_dev ? nrank : 0;
+  for (int r = 0; r < A.nrank; ++r) {
+    A.rank_pos[r] = rank_pos[r];
+    A.rank_id[r] = rank_id[r];
+  }
+  classify_kernel<<<kRasterGrid, 256, 0, st>>>(C, A);
+  note_launches(1);
+  return cuda_check("fvv_classify");
+}
 
 int fvv::render_view_coded_bound(const fvv_camera *rig, int ncam, const uint8_t *frames_dev,
                                  const int64_t *frame_off, const FrameInputs *in,
