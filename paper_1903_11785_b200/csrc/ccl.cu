@@ -7,10 +7,12 @@
 // linear index), so a union-find forest over ranks keeps the reference's
 // canonical numbering:
 //   1. rank scan      : word_prefix[w], on_list[r] = l, parent[r] = r
-//   2. union          : each ON voxel unites with its 13 lexicographically
-//                       negative 26-neighbours (hull.py:124-133); roots are
-//                       linked by atomicMin, so every root ends as its
-//                       component's minimum rank = minimum linear index
+//   2. union          : runs of ON voxels along i are linked to their first
+//                       voxel; each run unites with the runs among its 13
+//                       lexicographically negative 26-neighbours
+//                       (hull.py:124-133); roots are linked by atomicMin, so
+//                       every root ends as its component's minimum rank =
+//                       minimum linear index
 //   3. flatten        : parent[r] = find(r)
 //   4. root scan      : label(root) = 1 + #roots before it — ascending
 //                       minimum linear index, as hull.py:195-197 numbers them
@@ -153,33 +155,94 @@ __device__ __forceinline__ int32_t rank_of(const uint32_t *occ, const int32_t *w
   return word_prefix[l >> 5] + __popc(w & ((1u << (l & 31)) - 1u));
 }
 
-// -- 2. union over the 13 negative neighbours --------------------------------
+// -- 2. union over runs ---------------------------------------------------------
+// ON voxels come in runs along i (consecutive linear indices, so consecutive
+// ranks). A run needs no union inside: every voxel points at the run's first
+// rank. The 13 lexicographically negative 26-neighbours (hull.py:124-133) of
+// a run's voxels are its own row's i - 1 (inside the run) and, in the four
+// rows (dj, dk) = (-1, 0), (-1, -1), (0, -1), (1, -1), the voxels with
+// i in [i0 - 1, i1 + 1]; the run is united with every run meeting that range,
+// once per run instead of once per (voxel, offset).
+
+// first voxel of the run holding ON position p (row positions [row0, p])
+__device__ __forceinline__ int64_t run_first(const uint32_t *occ, int64_t row0, int64_t p) {
+  int64_t q = p;
+  while (q > row0) {
+    const int64_t b = q - 1, wbase = b & ~31ll;
+    const int sh = (int)(b & 31);
+    uint32_t off = ~__ldg(occ + (b >> 5)) & (sh == 31 ? 0xffffffffu : ((2u << sh) - 1u));
+    if (row0 > wbase) off &= 0xffffffffu << (row0 - wbase);
+    if (off) return wbase + (31 - __clz(off)) + 1;  // one past the nearest OFF bit
+    if (wbase <= row0) return row0;
+    q = wbase;
+  }
+  return row0;
+}
+
+// last voxel of the run holding ON position p (row positions [p, row1))
+__device__ __forceinline__ int64_t run_last(const uint32_t *occ, int64_t row1, int64_t p) {
+  int64_t b = p + 1;
+  while (b < row1) {
+    const int64_t wbase = b & ~31ll;
+    const uint32_t off = ~__ldg(occ + (b >> 5)) & (0xffffffffu << (b & 31));
+    if (off) {
+      const int64_t z = wbase + __ffs(off) - 1;
+      return (z < row1 ? z : row1) - 1;
+    }
+    b = wbase + 32;
+  }
+  return row1 - 1;
+}
+
+// first ON position in [p, pe], or -1
+__device__ __forceinline__ int64_t next_on(const uint32_t *occ, int64_t p, int64_t pe) {
+  while (p <= pe) {
+    const int64_t wbase = p & ~31ll;
+    const uint32_t on = __ldg(occ + (p >> 5)) & (0xffffffffu << (p & 31));
+    if (on) {
+      const int64_t z = wbase + __ffs(on) - 1;
+      return z <= pe ? z : -1;
+    }
+    p = wbase + 32;
+  }
+  return -1;
+}
+
 __global__ void ccl_union_kernel(const uint32_t *__restrict__ occ, CclWs w, int64_t nx, int64_t ny,
                                  int64_t nz) {
-  // one thread per (ON voxel, backward neighbour offset): the union work is
-  // a few dependent finds per thread instead of 13 in a row (at C3 only
-  // ~12k voxels are ON, so per-voxel threads left the GPU latency-bound)
-  // 32-bit index arithmetic: nvox < 2^31 (fvv_ccl26), so 13 * n_on < 2^35
-  // is the only wider quantity
+  // four threads per ON voxel: the run's first voxel unites with the runs of
+  // one neighbour row each; the others link to their run's first voxel.
+  // 32-bit index arithmetic (nvox < 2^31, fvv_ccl26)
   const int64_t n_on = __ldcg(w.counts);
   const uint32_t ux = (uint32_t)nx, uy = (uint32_t)ny;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < 13 * n_on;
+  const int djs[4] = {-1, -1, 0, 1}, dks[4] = {0, -1, -1, -1};
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < 4 * n_on;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e / 13;
-    const int o = (int)(e - 13 * r);
+    const int64_t r = e >> 2;
+    const int n = (int)(e & 3);
     const uint32_t l = (uint32_t)w.on_list[r];
     const uint32_t q = l / ux, k = q / uy;
-    const int i = (int)(l - q * ux), j = (int)(q - k * uy);
-    // offsets with (dk, dj, di) lexicographically negative (hull.py:124-133)
-    const int dk = o < 9 ? -1 : 0;
-    const int rem = o < 9 ? o : o - 9;
-    const int dj = rem / 3 - 1;
-    const int di = rem % 3 - 1;
-    const int ii = i + di, jj = j + dj, kk = (int)k + dk;
-    if (ii < 0 || jj < 0 || kk < 0 || ii >= nx || jj >= ny || kk >= nz) continue;
-    const int64_t m = (int64_t)l + di + nx * (dj + ny * dk);
-    if (!occ_bit(occ, m)) continue;
-    uf_unite(w.parent, (int32_t)r, rank_of(occ, w.word_prefix, m));
+    const uint32_t i = l - q * ux, j = q - k * uy;
+    const int64_t row0 = (int64_t)l - i;
+    const int64_t first = run_first(occ, row0, l);
+    if (first != (int64_t)l) {  // inside a run: link to its first voxel (consecutive ranks)
+      if (n == 0) w.parent[r] = (int32_t)(r - ((int64_t)l - first));
+      continue;
+    }
+    const int64_t jj = (int64_t)j + djs[n], kk = (int64_t)k + dks[n];
+    if (jj < 0 || jj >= ny || kk < 0) continue;
+    const int64_t last = run_last(occ, row0 + nx, l);
+    const int64_t a = i > 0 ? i - 1 : 0, i1 = last - row0, b = i1 + 1 < nx ? i1 + 1 : nx - 1;
+    const int64_t nrow = nx * (jj + ny * kk);
+    int64_t p = nrow + a;
+    const int64_t pe = nrow + b;
+    while (p <= pe) {
+      const int64_t s = next_on(occ, p, pe);
+      if (s < 0) break;
+      const int64_t sf = run_first(occ, nrow, s);
+      uf_unite(w.parent, (int32_t)r, rank_of(occ, w.word_prefix, sf));
+      p = run_last(occ, nrow + nx, s) + 2;  // (the bit after a run is OFF)
+    }
   }
 }
 
