@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kPlanThreads)
   const int nroi = nroi_all < FVV_MAX_GRIDS ? nroi_all : FVV_MAX_GRIDS;
   // per-grid prefixes (one warp, 32 grids per step): occupancy words, tiles, k-row words
   if (warp == 0) {
-    int64_t cw = 0, ct = 0, ck = 0, dense = 0;
+    int64_t cw = 0, ct = 0, ck = 0, dense = 0, cr = 0;
     for (int g0 = 0; g0 < FVV_MAX_GRIDS; g0 += 32) {
       const int g = g0 + lane;
       const bool live = g < nroi;
@@ -275,22 +275,26 @@ __global__ void __launch_bounds__(kPlanThreads)
         vox = fg.dims[0] * fg.dims[1] * fg.dims[2];
         k = mesh_grid_info(fg, 0, 0, gi);  // offsets filled in below
       }
-      int64_t iw = w, it = t, ik = k, iv = vox;  // inclusive scans
+      const int64_t tr = live ? mesh_grid_tr_items(gi) : 0;
+      int64_t iw = w, it = t, ik = k, iv = vox, ir = tr;  // inclusive scans
       for (int o = 1; o < 32; o <<= 1) {
         const int64_t xw = __shfl_up_sync(0xffffffffu, iw, o), xt = __shfl_up_sync(0xffffffffu, it, o),
-                      xk = __shfl_up_sync(0xffffffffu, ik, o), xv = __shfl_up_sync(0xffffffffu, iv, o);
+                      xk = __shfl_up_sync(0xffffffffu, ik, o), xv = __shfl_up_sync(0xffffffffu, iv, o),
+                      xr = __shfl_up_sync(0xffffffffu, ir, o);
         if (lane >= o) {
           iw += xw;
           it += xt;
           ik += xk;
           iv += xv;
+          ir += xr;
         }
       }
-      const int64_t ow = cw + iw - w, ot = ct + it - t, ok = ck + ik - k;
+      const int64_t ow = cw + iw - w, ot = ct + it - t, ok = ck + ik - k, orr = cr + ir - tr;
       if (live) {
         plan->carve.word_off[g] = ow;
         plan->carve.blk_start[g] = ot;
         mesh_grid_info(plan->carve.grids[g], ow, ok, gi);
+        gi.tr_off = orr;
         plan->mesh.gi[g] = gi;
         plan->mesh.tw_start[g] = ok;
       }
@@ -298,6 +302,7 @@ __global__ void __launch_bounds__(kPlanThreads)
       ct += __shfl_sync(0xffffffffu, it, 31);
       ck += __shfl_sync(0xffffffffu, ik, 31);
       dense += __shfl_sync(0xffffffffu, iv, 31);
+      cr += __shfl_sync(0xffffffffu, ir, 31);
     }
     if (lane == 0) {
       int st = s_status;
@@ -316,6 +321,7 @@ __global__ void __launch_bounds__(kPlanThreads)
       plan->mesh.ngrid = ng;
       plan->mesh.tw_total = run ? ck : 0;
       plan->mesh.tw3 = run ? 3 * ck : 0;
+      plan->mesh.tr_total = run ? cr : 0;
       for (int g = ng; g <= FVV_MAX_GRIDS; ++g) plan->mesh.tw_start[g] = run ? ck : 0;
     }
   }

@@ -235,12 +235,14 @@ struct MeshGridInfo {
   int64_t occ_word_off;  // F-order occupancy words of this grid
   int64_t rows, nzw;     // rows = nx*ny (0 when a dim < 2: empty mesh, mesh.py:298-299)
   int64_t tw_off;        // transposed-word offset (S space); V space offset = 3*tw_off
-  uint32_t words32, nzw32, ny32, pad;  // rows*nzw, nzw, ny (3*tw_total < 2^31)
+  int64_t tr_off;        // first transpose work item (32 i x one k-row word)
+  uint32_t words32, nzw32, ny32, nxw32;  // rows*nzw, nzw, ny, ceil(nx/32) (3*tw_total < 2^31)
 };
 
 struct __align__(16) MeshGrids {
   int ngrid, pad;
   int64_t tw_total, tw3;  // k-row words of the batch, and 3x (the edge scan's length)
+  int64_t tr_total;       // transpose work items of the batch
   int64_t tw_start[FVV_MAX_GRIDS + 1];  // prefix of rows*nzw
   MeshGridInfo gi[FVV_MAX_GRIDS];
 };
@@ -258,8 +260,14 @@ __host__ __device__ inline int64_t mesh_grid_info(const fvv_grid &g, int64_t wor
   gi.words32 = (uint32_t)(gi.rows * gi.nzw);
   gi.nzw32 = (uint32_t)gi.nzw;
   gi.ny32 = (uint32_t)ny;
-  gi.pad = 0;
+  gi.nxw32 = meshable ? (uint32_t)((nx + 31) / 32) : 0;
+  gi.tr_off = 0;
   return gi.rows * gi.nzw;
+}
+
+// transpose work items of a grid (one per 32 i of a k-row word)
+__host__ __device__ inline int64_t mesh_grid_tr_items(const MeshGridInfo &gi) {
+  return (int64_t)gi.nxw32 * gi.ny32 * gi.nzw32;
 }
 
 // C polygonize of the grids in *G_dev (device) - the bodies of

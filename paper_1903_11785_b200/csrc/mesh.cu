@@ -85,25 +85,45 @@ __device__ __forceinline__ uint32_t row_next(const uint32_t *tw, const MeshGridI
 }
 
 // ---- A1: transpose F-order occupancy into k-rows --------------------------
+// A warp takes 32 consecutive i of one (grid, j, k-row word w): lane L loads
+// the 32 occupancy bits of row (j, k = 32 w + L) starting at i0 (a funnel
+// shift of two words), and 32 ballots turn the 32 x 32 bit block around:
+// ballot b collects bit b (= i0 + b) over the lanes (= k), i.e. the k-row
+// word of column i0 + b. Two loads per 32 output words instead of 32 per word.
 __global__ void mesh_transpose_kernel(const MeshGrids *__restrict__ Gp, MeshBufs B) {
   const MeshGrids &G = *Gp;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < G.tw_total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int g = grid_of(G, e);
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t total = G.tr_total;
+  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < total;
+       t += nwarps) {
+    int g = 0;  // last grid with tr_off <= t
+    for (int step = FVV_MAX_GRIDS / 2; step >= 1; step >>= 1)
+      if (g + step < G.ngrid && G.gi[g + step].tr_off <= t) g += step;
     const MeshGridInfo &gi = G.gi[g];
-    const uint32_t local = (uint32_t)(e - G.tw_start[g]);
-    const uint32_t q = local / gi.nzw32, w32 = local - q * gi.nzw32;
-    const uint32_t i32 = q / gi.ny32;
+    const uint32_t local = (uint32_t)(t - gi.tr_off);
+    const uint32_t rest = local / gi.nzw32, w = local - rest * gi.nzw32;
+    const uint32_t ic = rest / gi.ny32, j = rest - ic * gi.ny32;
     const int64_t nx = gi.g.dims[0], ny = gi.g.dims[1], nz = gi.g.dims[2];
-    const int64_t w = w32, i = i32, j = q - i32 * gi.ny32;
-    uint32_t out = 0;
-    const int64_t kend = (w * 32 + 32 < nz) ? w * 32 + 32 : nz;
-    for (int64_t k = w * 32; k < kend; ++k) {
-      const int64_t l = i + nx * (j + ny * k);
-      const uint32_t word = __ldg(B.occ + gi.occ_word_off + (l >> 5));
-      out |= ((word >> (l & 31)) & 1u) << (k - w * 32);
+    const int64_t i0 = 32 * (int64_t)ic, k = 32 * (int64_t)w + lane;
+    const int64_t nvalid = nx - i0 < 32 ? nx - i0 : 32;
+    uint32_t bits = 0;
+    if (k < nz) {
+      const int64_t l0 = i0 + nx * (j + ny * k);
+      const uint32_t *p = B.occ + gi.occ_word_off + (l0 >> 5);
+      const int sh = (int)(l0 & 31);
+      const uint32_t lo = __ldg(p), hi = (sh + nvalid > 32) ? __ldg(p + 1) : 0u;
+      bits = __funnelshift_r(lo, hi, sh);
+      if (nvalid < 32) bits &= (1u << nvalid) - 1u;
     }
-    B.tw[e] = out;
+    uint32_t mine = 0;
+#pragma unroll
+    for (int b = 0; b < 32; ++b) {
+      const uint32_t col = __ballot_sync(0xffffffffu, (bits >> b) & 1u);
+      if (lane == b) mine = col;
+    }
+    if (lane < nvalid)
+      B.tw[gi.tw_off + ((i0 + lane) * ny + j) * (int64_t)gi.nzw32 + w] = mine;
   }
 }
 
@@ -713,10 +733,12 @@ static int fill_grids(const fvv_grid *grids, int ngrid, const int64_t *word_off,
   }
   memset(&G, 0, sizeof(G));
   G.ngrid = ngrid;
-  int64_t acc = 0;
+  int64_t acc = 0, tr = 0;
   for (int g = 0; g < ngrid; ++g) {
     G.tw_start[g] = acc;
     acc += mesh_grid_info(grids[g], word_off[g], acc, G.gi[g]);
+    G.gi[g].tr_off = tr;
+    tr += mesh_grid_tr_items(G.gi[g]);
     if (3 * acc >= (int64_t)1 << 31) {  // 32-bit word indices (and int32 vertex prefixes)
       set_error("mesh: %lld occupancy words over the batch (limit %lld)", (long long)acc,
                 (long long)((((int64_t)1 << 31) - 1) / 3));
@@ -726,6 +748,7 @@ static int fill_grids(const fvv_grid *grids, int ngrid, const int64_t *word_off,
   for (int g = ngrid; g <= FVV_MAX_GRIDS; ++g) G.tw_start[g] = acc;
   G.tw_total = acc;
   G.tw3 = 3 * acc;
+  G.tr_total = tr;
   return FVV_OK;
 }
 
