@@ -336,6 +336,7 @@ def run_b200(args):
     for st_name in ("depth_images", "polygonize", "visibility", "render"):
         roof_stages[st_name] = roofline_for(st_name, stage_ms[st_name], work, ncam, H, W,
                                             hbm_peak, peak_src)
+    attach_executed(roof_stages, stage_ms)
 
     # ---- e2e through the public API from pinned host memory ----
     e2e = None
@@ -558,17 +559,18 @@ def carve_roofline(stage_ms, work, ncam):
     ms = stage_ms["sparse_carve"] + stage_ms["dense_carve"]
     peak, basis = fp32_peak_tflops()
     achieved = FLOP_PER_PROJECTION * proj / (ms / 1e3) / 1e12
-    traffic = None  # DRAM bytes per launch (profiles/traffic.json, ncu --set full)
+    traffic = None  # DRAM bytes per launch (B-1 + B-3 stages of profiles/exec_counters.json)
     try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            traffic = json.load(fh).get("carve_kernel", {}).get("bytes_per_launch")
+        with open(EXEC_COUNTERS) as fh:
+            st_ = json.load(fh)["stages"]
+        traffic = int((st_["B-1"]["dram_mb"] + st_["B-3"]["dram_mb"]) * 1e6 / 2)
     except Exception:  # noqa: BLE001
         pass
     return {"bound": "fp32", "kernel": "carve_kernel (B-1 stage grid + B-3 ROI grids)",
             "stage": "sparse_carve + dense_carve", "achieved": round(achieved, 3),
             "peak": round(peak, 2), "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
             "traffic": traffic,
-            "traffic_source": "profiles/traffic.json (ncu --set full, DRAM bytes per carve stage: prep + classification + octants + float64 queue)",
+            "traffic_source": "profiles/exec_counters.json (ncu --set full: dram bytes of the B-1 and B-3 stages, prep + classification + octants + float64 queue, per launch)",
             "peak_source": basis, "launches_per_frame": 2,
             "algorithmic_flop_per_launch": int(FLOP_PER_PROJECTION * proj / 2),
             "voxel_projections_per_frame": int(proj), "ms_per_launch": round(ms / 2, 4),
@@ -613,6 +615,54 @@ def stage_rooflines(stage_ms, work, ncam, H, W, hbm_peak, peak_src):
                                "ms": round(ms, 4), "algorithmic_bytes": int(ccl_bytes),
                                "peak_source": peak_src}
     return out
+
+
+EXEC_COUNTERS = os.path.join(ROOT, "profiles", "exec_counters.json")
+STAGE_OF = {"sparse_carve": "B-1", "noise_filter_roi": "B-2", "dense_carve": "B-3",
+            "polygonize": "C", "depth_images": "D-1", "visibility": "D-2", "render": "E"}
+
+
+def attach_executed(roof_stages, stage_ms):
+    """Executed-work counters per stage from the committed ncu capture of one
+    C3 frame (profiles/exec_counters.json, scripts/exec_counters.py): FP32 /
+    FP64 pipe and issue utilisation, executed FLOP rates, DRAM bytes per
+    frame (the stage's measured traffic) and L2 / L1-gather throughput. C is
+    bounded by the FP64 pipe (the float64 isovalue chain) and B-2 by launch /
+    dependency latency (a few thousand ON voxels), so those two rooflines are
+    stated against them."""
+    try:
+        with open(EXEC_COUNTERS) as fh:
+            ex = json.load(fh)
+    except Exception:  # noqa: BLE001
+        return
+    peaks_ = ex.get("peaks", {})
+    for stage, key in STAGE_OF.items():
+        c = ex.get("stages", {}).get(key)
+        if not c or stage not in roof_stages:
+            continue
+        keep = ("us", "launches", "fp32_tflops", "fp64_tflops", "fma_pipe_pct", "fp64_pipe_pct",
+                "issue_pct", "dram_mb", "dram_gbps", "l2_gbps", "l1_gather_gbps")
+        r = roof_stages[stage]
+        r["executed"] = {k: c[k] for k in keep if k in c}
+        r["executed"]["source"] = "profiles/exec_counters.json (ncu --set full, cold caches, serialised)"
+        r["traffic"] = int(c["dram_mb"] * 1e6) if "dram_mb" in c else r.get("traffic")
+        r["traffic_source"] = "profiles/exec_counters.json (dram__bytes read+write, per frame)"
+    if "polygonize" in roof_stages and "C" in ex.get("stages", {}):
+        c = ex["stages"]["C"]
+        pk = peaks_.get("fp64_tflops", 37.22)
+        roof_stages["polygonize"].update({
+            "bound": "fp64", "unit": "TFLOP/s", "achieved": c.get("fp64_tflops"), "peak": pk,
+            "frac": round(c.get("fp64_tflops", 0.0) / pk, 4),
+            "peak_source": "148 SMs x 64 DFMA lanes x 2 x 1965 MHz",
+            "note": "executed FP64 FLOP rate of the C kernels (ncu); the float64 isovalue "
+                    "chain of mesh.py:231-272 dominates"})
+    if "noise_filter_roi" in roof_stages:
+        r = roof_stages["noise_filter_roi"]
+        r.update({"bound": "latency", "ms": round(stage_ms["noise_filter_roi"], 4),
+                  "note": "launch / dependency-latency bound: a few thousand ON voxels "
+                          "through a rank scan, a run-based union-find, a root scan, "
+                          "stats and the ROI planner; its HBM fraction (algorithmic "
+                          "bytes / time) is kept in 'frac'"})
 
 
 # ---------------------------------------------------------------- CPU arm

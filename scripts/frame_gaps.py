@@ -1,5 +1,6 @@
 """GPU busy time vs. wall time of single-stream C3 frames (torch.profiler /
-CUPTI kernel records): how much of a frame is host-side bubble.
+CUPTI kernel records): how much of a frame is host-side bubble, and each
+kernel's warm device time inside the replayed frame graph.
 
     python scripts/frame_gaps.py [--workload C3] [--frames 5]
 """
@@ -24,13 +25,15 @@ masks, frames = S.render_scene_device(wl.rig, wl.objects(1))
 fb = frames.reshape(-1)
 foff = np.arange(len(wl.rig), dtype=np.int64) * (frames.shape[1] * frames.shape[2] * 3)
 ex = executor_for(wl.cfg, wl.rig)
-for _ in range(3):
-    ex.run(masks, wl.virtual, fb, foff)
-torch.cuda.synchronize()
-with profile(activities=[ProfilerActivity.CUDA]) as prof:
-    for _ in range(args.frames):
+side = torch.cuda.Stream()  # (not the legacy default stream: frames replay as CUDA graphs)
+with torch.cuda.stream(side):
+    for _ in range(3):
         ex.run(masks, wl.virtual, fb, foff)
     torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(args.frames):
+            ex.run(masks, wl.virtual, fb, foff)
+        torch.cuda.synchronize()
 ev = [e for e in prof.events() if e.device_type.name == "CUDA"]
 ks = sorted((e.time_range.start, e.time_range.end, e.name) for e in ev)
 t0, t1 = ks[0][0], max(k[1] for k in ks)
@@ -47,6 +50,13 @@ gaps = sorted(((ks[i + 1][0] - ks[i][1]), ks[i][2][:40], ks[i + 1][2][:40])
               for i in range(len(ks) - 1))[::-1]
 print(f"{len(ks) / args.frames:.0f} GPU records/frame; wall {(t1 - t0) / args.frames:.1f} us/frame, "
       f"busy {busy / args.frames:.1f} us/frame ({busy / (t1 - t0):.1%})")
+per = {}
+for s_, e_, n_ in ks:
+    k = n_.split("(")[0].replace("void ", "")[:48]
+    per.setdefault(k, []).append(e_ - s_)
+print("per-kernel device time (us/frame, warm, in-graph):")
+for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
+    print(f"  {sum(v) / args.frames:8.1f}  x{len(v) / args.frames:4.1f}  {k}")
 print("largest gaps (us):")
 for g, a, b in gaps[:12]:
     print(f"  {g:7.1f}  {a} -> {b}")

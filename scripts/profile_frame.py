@@ -25,13 +25,15 @@ masks, frames = S.render_scene_device(wl.rig, wl.objects(1))
 fb = frames.reshape(-1)
 foff = np.arange(len(wl.rig), dtype=np.int64) * (frames.shape[1] * frames.shape[2] * 3)
 ex = executor_for(wl.cfg, wl.rig)
-for _ in range(args.warm):
-    ex.run(masks, wl.virtual, fb, foff)
-torch.cuda.synchronize()
-torch.cuda.profiler.start()
-for _ in range(args.frames):
-    out = ex.run(masks, wl.virtual, fb, foff)
-torch.cuda.synchronize()
-torch.cuda.profiler.stop()
+side = torch.cuda.Stream()  # frames replay as captured graphs after the warm-up
+with torch.cuda.stream(side):
+    for _ in range(args.warm):
+        ex.run(masks, wl.virtual, fb, foff)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
+    for _ in range(args.frames):
+        out = ex.run(masks, wl.virtual, fb, foff)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
 print({k: int(out.stats_raw[k]) for k in ("sparse_tests", "dense_tests", "triangles", "vertices")},
       [round(float(x), 4) for x in out.stats_raw["ms"]])
