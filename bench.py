@@ -518,16 +518,11 @@ def roofline_for(stage, ms, work, ncam, H, W, hbm_peak, peak_src):
     }
     kernel, nbytes = per_stage.get(stage, (stage, 0.0))
     achieved = nbytes / (ms / 1e3) / 1e9
-    traffic = None  # measured DRAM bytes of the stage's kernels (profiles/traffic.json, ncu)
-    try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            traffic = json.load(fh).get(stage, {}).get("bytes")
-    except Exception:  # noqa: BLE001
-        pass
+    traffic = None  # measured DRAM bytes: attach_executed (profiles/exec_counters.json)
     return {"bound": "hbm", "kernel": kernel, "stage": stage, "achieved": round(achieved, 2),
             "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
             "frac": round(achieved / hbm_peak, 5), "traffic": traffic,
-            "traffic_source": "profiles/traffic.json (ncu --set full, per frame)",
+            "traffic_source": None,
             "algorithmic_bytes": int(nbytes), "ms_per_launch": round(ms, 4)}
 
 
