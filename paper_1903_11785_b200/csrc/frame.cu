@@ -1033,7 +1033,13 @@ static void update_caps(fvv_frame *f, int64_t words, int64_t tiles, int64_t tw, 
     }
   };
   fit(words, K.words);
-  fit(tiles, K.tiles);
+  // tiles: one B-3 classification block per tile and eight octant blocks per
+  // tile are launched for the capacity, so it carries less headroom
+  if (tiles > K.tiles - K.tiles / 32 || K.tiles == 0) {
+    const int64_t base = tiles > K.tiles ? tiles : K.tiles;
+    K.tiles = base + base / 16 + 32;
+    grew = true;
+  }
   fit(tw, K.tw);
   fit(v, K.v);
   fit(sn, K.s);
