@@ -46,8 +46,8 @@ struct MeshBufs {
   int64_t *info;       // [ngrid][8]: vbase V sbase S tbase T fallback inconsistent
   // phase B
   int64_t *vert_key;   // [V] V-element*32 + bit
-  int64_t *cell_key;   // [S] S-element*32 + bit
-  int32_t *cell_mask;  // [S] case | keep<<8
+  int32_t *cell_tri;   // [S][5][3] vertex indices of the cell's triangles, emitted order
+  int32_t *cell_mask;  // [S] case | keep<<8 | grid<<16
   int32_t *cprefix;    // [S][5]
   int64_t *slot_base;  // [ngrid][5]
   int64_t *cell_sums;
@@ -457,6 +457,8 @@ __device__ __forceinline__ int cell_case(const MeshBufs &B, const MeshGridInfo &
 }
 
 // ---- B2: surface-cell list, per-slot keep bits (mesh.py:339-373) ------------
+// The case's distinct edges are looked up once each; the triangles' vertex
+// indices (reversed winding, mesh.py:365) are kept for the emit pass.
 __device__ __forceinline__ void mesh_cell(const MeshGrids &G, const MeshBufs &B, int64_t e,
                                           int b, int64_t c) {
   int lo = 0, hi = G.ngrid - 1;
@@ -474,13 +476,22 @@ __device__ __forceinline__ void mesh_cell(const MeshGrids &G, const MeshBufs &B,
   const int ci = cell_case(B, gi, q, k);
   const int ntri = c_mc_ntri[ci];
   const unsigned long long edges = c_mc_edges[ci];
+  uint32_t used = 0;
+  for (int n = 0; n < 3 * ntri; ++n) used |= 1u << ((edges >> (4 * n)) & 15);
+  int32_t ev[12];
+  for (uint32_t m = used; m; m &= m - 1) {
+    const int ed = __ffs(m) - 1;
+    ev[ed] = (int32_t)edge_vertex(G, B, g, i, j, k, ed);
+  }
   int keep = 0;
+  int32_t *out = B.cell_tri + 15 * c;
   for (int t = 0; t < ntri; ++t) {
-    const int64_t v0 = edge_vertex(G, B, g, i, j, k, (int)((edges >> (12 * t)) & 15));
-    const int64_t v1 = edge_vertex(G, B, g, i, j, k, (int)((edges >> (12 * t + 4)) & 15));
-    const int64_t v2 = edge_vertex(G, B, g, i, j, k, (int)((edges >> (12 * t + 8)) & 15));
+    const int32_t v0 = ev[(edges >> (12 * t)) & 15];
+    const int32_t v1 = ev[(edges >> (12 * t + 4)) & 15];
+    const int32_t v2 = ev[(edges >> (12 * t + 8)) & 15];
     // reversed winding (v2, v1, v0); area as numpy: 0.5*|cross(B-A, C-A)|
-    const double *A = B.verts + 3 * v2, *Bv = B.verts + 3 * v1, *Cv = B.verts + 3 * v0;
+    const double *A = B.verts + 3 * (int64_t)v2, *Bv = B.verts + 3 * (int64_t)v1,
+                 *Cv = B.verts + 3 * (int64_t)v0;
     const double a0 = Bv[0] - A[0], a1 = Bv[1] - A[1], a2 = Bv[2] - A[2];
     const double b0 = Cv[0] - A[0], b1 = Cv[1] - A[1], b2 = Cv[2] - A[2];
     const double c0 = a1 * b2 - a2 * b1;
@@ -488,9 +499,11 @@ __device__ __forceinline__ void mesh_cell(const MeshGrids &G, const MeshBufs &B,
     const double c2 = a0 * b1 - a1 * b0;
     const double area = 0.5 * sqrt((c0 * c0 + c1 * c1) + c2 * c2);
     if (area > kDegenerateArea) keep |= 1 << t;
+    out[3 * t] = v2;
+    out[3 * t + 1] = v1;
+    out[3 * t + 2] = v0;
   }
-  B.cell_key[c] = e * 32 + b;
-  B.cell_mask[c] = ci | (keep << 8);
+  B.cell_mask[c] = ci | (keep << 8) | (g << 16);
 }
 
 // Surface cells, warp-cooperatively: a warp loads 32 consecutive surface-cell
@@ -561,7 +574,7 @@ struct TriScan {
   const int32_t *cell_mask;
   int32_t *cprefix;
   typedef int Item;
-  __device__ int load(int64_t c) const { return cell_mask[c] >> 8; }
+  __device__ int load(int64_t c) const { return (cell_mask[c] >> 8) & 31; }
   __device__ Slot5 value(int keep) const {
     Slot5 s;
     for (int t = 0; t < 5; ++t) s.v[t] = (keep >> t) & 1;
@@ -617,38 +630,21 @@ __global__ void mesh_slot_bases_kernel(const MeshGrids *__restrict__ Gp, MeshBuf
 
 // ---- B5: triangle emission ----------------------------------------------------
 __global__ void mesh_emit_kernel(const MeshGrids *__restrict__ Gp, MeshBufs B) {
-  const MeshGrids &G = *Gp;
   if (!emit_fits(B)) return;
   const int64_t S = __ldcg(B.totals + 1);
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < S;
        c += (int64_t)gridDim.x * blockDim.x) {
     const int m = B.cell_mask[c];
-    const int keep = m >> 8;
+    const int keep = (m >> 8) & 31;
     if (!keep) continue;
-    const int ci = m & 255;
-    const int64_t key = B.cell_key[c];
-    const int64_t e = key >> 5;
-    int lo = 0, hi = G.ngrid - 1;
-    while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (G.tw_start[mid] <= e) lo = mid; else hi = mid - 1;
-    }
-    const int g = lo;
-    const MeshGridInfo &gi = G.gi[g];
-    const uint32_t rw = (uint32_t)(e - G.tw_start[g]);
-    const uint32_t q32 = rw / gi.nzw32, w = rw - q32 * gi.nzw32;
-    const uint32_t i32 = q32 / gi.ny32;
-    const int64_t q = q32, i = i32, j = q32 - i32 * gi.ny32, k = (int64_t)w * 32 + (key & 31);
-    const unsigned long long edges = c_mc_edges[ci];
+    const int g = m >> 16;
+    const int32_t *tv = B.cell_tri + 15 * c;
     for (int t = 0; t < 5; ++t) {
       if (!((keep >> t) & 1)) continue;
       const int64_t idx = B.slot_base[5 * g + t] + B.cprefix[5 * c + t];
-      const int64_t v0 = edge_vertex(G, B, g, i, j, k, (int)((edges >> (12 * t)) & 15));
-      const int64_t v1 = edge_vertex(G, B, g, i, j, k, (int)((edges >> (12 * t + 4)) & 15));
-      const int64_t v2 = edge_vertex(G, B, g, i, j, k, (int)((edges >> (12 * t + 8)) & 15));
-      B.tris[3 * idx] = (int32_t)v2;
-      B.tris[3 * idx + 1] = (int32_t)v1;
-      B.tris[3 * idx + 2] = (int32_t)v0;
+      B.tris[3 * idx] = tv[3 * t];
+      B.tris[3 * idx + 1] = tv[3 * t + 1];
+      B.tris[3 * idx + 2] = tv[3 * t + 2];
     }
   }
 }
@@ -800,7 +796,7 @@ int fvv::mesh_prepare_batch(const MeshGrids *G_dev, int64_t tw_cap, int ngrid_ma
 }
 
 size_t fvv::mesh_emit_scratch(int64_t cap_v, int64_t cap_s) {
-  return al256(8 * (size_t)cap_v) + al256(8 * (size_t)cap_s) + al256(4 * (size_t)cap_s) +
+  return al256(8 * (size_t)cap_v) + al256(60 * (size_t)cap_s) + al256(4 * (size_t)cap_s) +
          al256(20 * (size_t)cap_s) + al256(onepass_bytes<Slot5>(cap_s + 1));
 }
 
@@ -825,8 +821,8 @@ int fvv::mesh_emit_batch(const fvv_camera *cams_by_id, int ncam, const uint32_t 
   char *s = (char *)scratch_dev;
   B.vert_key = (int64_t *)s;
   s += al256(8 * (size_t)cap_v);
-  B.cell_key = (int64_t *)s;
-  s += al256(8 * (size_t)cap_s);
+  B.cell_tri = (int32_t *)s;
+  s += al256(60 * (size_t)cap_s);
   B.cell_mask = (int32_t *)s;
   s += al256(4 * (size_t)cap_s);
   B.cprefix = (int32_t *)s;
