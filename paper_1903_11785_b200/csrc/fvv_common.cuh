@@ -22,11 +22,15 @@ void note_launches(long long n);
 
 // camera.py:177 `pts @ R.T + t`: OpenBLAS gemm (>= 2 rows) accumulates
 // fma(z,R2, fma(y,R1, x*R0)); the 1-row gemv kernel fma(z,R2, fma(x,R0, y*R1)).
+// (the two orders differ only in which product is fused: the first factor
+// pair of each row is selected, so one product and one fma are evaluated)
 __device__ __forceinline__ void world_to_cam(const fvv_camera &c, double x, double y, double z,
                                              bool gemv, double &X, double &Y, double &Z) {
-  double a0 = gemv ? fma(x, c.R[0], y * c.R[1]) : fma(y, c.R[1], x * c.R[0]);
-  double a1 = gemv ? fma(x, c.R[3], y * c.R[4]) : fma(y, c.R[4], x * c.R[3]);
-  double a2 = gemv ? fma(x, c.R[6], y * c.R[7]) : fma(y, c.R[7], x * c.R[6]);
+  const double m = gemv ? y : x, f = gemv ? x : y;  // m * R[m-col] first, then fma(f, ...)
+  const int cm = gemv ? 1 : 0, cf = gemv ? 0 : 1;
+  const double a0 = fma(f, c.R[cf], m * c.R[cm]);
+  const double a1 = fma(f, c.R[3 + cf], m * c.R[3 + cm]);
+  const double a2 = fma(f, c.R[6 + cf], m * c.R[6 + cm]);
   X = fma(z, c.R[2], a0) + c.t[0];
   Y = fma(z, c.R[5], a1) + c.t[1];
   Z = fma(z, c.R[8], a2) + c.t[2];
