@@ -127,4 +127,36 @@ __device__ __forceinline__ int classify32(const CamAffine &a, float fi, float fj
   return amb ? kAmb : (in ? kIn : kOut);
 }
 
+// classify32 for a voxel of a box over which the camera's Z is certainly
+// positive (every box corner has Z32 >= ez; Z is affine) and whose rounding
+// bounds are at most eu, ev (box_bounds below): the same decisions without
+// the per-voxel sign checks and error terms.
+__device__ __forceinline__ int classify32_box(const CamAffine &a, float eu, float ev, float fi,
+                                              float fj, float fk, int &px, int &py) {
+  const float Z = fmaf(fk, a.z[3], fmaf(fj, a.z[2], fmaf(fi, a.z[1], a.z[0])));
+  const float U = fmaf(fk, a.u[3], fmaf(fj, a.u[2], fmaf(fi, a.u[1], a.u[0])));
+  const float V = fmaf(fk, a.v[3], fmaf(fj, a.v[2], fmaf(fi, a.v[1], a.v[0])));
+  const float rz = recip(Z);
+  const float u = U * rz, v = V * rz;
+  const float ru = rintf(u), rv = rintf(v);
+  px = (int)ru;
+  py = (int)rv;
+  const bool in = (unsigned)px < (unsigned)a.w && (unsigned)py < (unsigned)a.h;
+  const bool amb = (fabsf(u - ru) >= 0.5f - eu && fabsf(u) <= a.ulim) ||
+                   (fabsf(v - rv) >= 0.5f - ev && fabsf(v) <= a.ulim);
+  return amb ? kAmb : (in ? kIn : kOut);
+}
+
+// Rounding bounds valid for every voxel of a box from the box's corner
+// values: classify32's E = (|u| + 1) k(rz) + bu rz + 2^-20 grows with |u| and
+// with rz = 1/Z, and over the box |u| and rz peak at corners (u is
+// linear-fractional, Z affine and positive), so the bound at (max |u|,
+// max rz) covers every voxel; inflated for the rounding of this evaluation.
+__device__ __forceinline__ void box_bounds(const CamAffine &a, float umax, float vmax, float rzmax,
+                                           float &eu, float &ev) {
+  const float k = fmaf(a.A, rzmax, 3.75f * kEps);
+  eu = (fmaf(umax + 1.0f, k, fmaf(a.bu, rzmax, 9.5367432e-7f))) * 1.001f + 1e-7f;
+  ev = (fmaf(vmax + 1.0f, k, fmaf(a.bv, rzmax, 9.5367432e-7f))) * 1.001f + 1e-7f;
+}
+
 }  // namespace fvv

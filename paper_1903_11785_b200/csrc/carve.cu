@@ -159,12 +159,13 @@ enum : int { kTileBg = 0, kTileFg = 1, kTileMixed = 2 };
 
 __device__ __forceinline__ void corner_bound(const CamAffine &a, float fi, float fj, float fk,
                                              bool &zok, float &u0, float &u1, float &v0,
-                                             float &v1) {
+                                             float &v1, float &rz_out) {
   const float Z = fmaf(fk, a.z[3], fmaf(fj, a.z[2], fmaf(fi, a.z[1], a.z[0])));
   const float U = fmaf(fk, a.u[3], fmaf(fj, a.u[2], fmaf(fi, a.u[1], a.u[0])));
   const float V = fmaf(fk, a.v[3], fmaf(fj, a.v[2], fmaf(fi, a.v[1], a.v[0])));
   zok = Z >= a.ez;  // Z > 0 for certain
   const float rz = recip(zok ? Z : 1.0f);
+  rz_out = rz;
   const float u = U * rz, v = V * rz;
   const float k = fmaf(a.A, rz, 3.75f * kEps);
   // + 1e-3 covers the rounding of these few float operations
@@ -179,22 +180,31 @@ __device__ __forceinline__ void corner_bound(const CamAffine &a, float fi, float
 // Eight lanes (one group of a warp; g8 = lane & 7) classify camera c for
 // the tile [i0, i1] x [j0, j1] x [k0, k1]; every lane of the warp calls this
 // (c < 0: idle group) and gets its own group's result.
+// Also returns (box, eu, ev) the per-voxel rounding bounds of classify32_box
+// over the tile, box = false when they do not hold (some corner's Z not
+// certainly positive): the voxels then take classify32.
 __device__ int tile_camera(const CarveParams &p, const CamAffine *aff, int c, int i0, int i1,
-                           int j0, int j1, int k0, int k1, int lane) {
+                           int j0, int j1, int k0, int k1, int lane, bool &box, float &beu,
+                           float &bev) {
   const int g8 = lane & 7, grp = lane >> 3;
-  float u0 = INFINITY, u1 = -INFINITY, v0 = INFINITY, v1 = -INFINITY;
+  float u0 = INFINITY, u1 = -INFINITY, v0 = INFINITY, v1 = -INFINITY, rz = 0.0f;
   bool zok = false;
   if (c >= 0)
     corner_bound(aff[c], (float)((g8 & 1) ? i1 : i0), (float)((g8 & 2) ? j1 : j0),
-                 (float)((g8 & 4) ? k1 : k0), zok, u0, u1, v0, v1);
+                 (float)((g8 & 4) ? k1 : k0), zok, u0, u1, v0, v1, rz);
   for (int o = 4; o >= 1; o >>= 1) {  // min/max over the group's 8 corners
     u0 = fminf(u0, __shfl_xor_sync(0xffffffffu, u0, o));
     u1 = fmaxf(u1, __shfl_xor_sync(0xffffffffu, u1, o));
     v0 = fminf(v0, __shfl_xor_sync(0xffffffffu, v0, o));
     v1 = fmaxf(v1, __shfl_xor_sync(0xffffffffu, v1, o));
+    rz = fmaxf(rz, __shfl_xor_sync(0xffffffffu, rz, o));
   }
   const unsigned gmask = 0xffu << (8 * grp);
   zok = (__ballot_sync(0xffffffffu, zok) & gmask) == gmask;
+  box = zok && c >= 0;
+  beu = bev = 0.0f;
+  if (box)  // (u0..u1 / v0..v1 include each corner's own bound: |u| <= max(|u0|, |u1|))
+    box_bounds(aff[c], fmaxf(fabsf(u0), fabsf(u1)), fmaxf(fabsf(v0), fabsf(v1)), rz, beu, bev);
   bool query = c >= 0 && zok;
   // rint(x) lies in [floor(x - 0.5), ceil(x + 0.5)] for x in [u0, u1]
   const float xl = floorf(u0 - 0.5f), xh = ceilf(u1 + 0.5f);
@@ -311,7 +321,8 @@ struct __align__(16) TileWork {
 // Returns this thread's ON count.
 __device__ __forceinline__ int carve_voxels(const CarveParams &p, const CamAffine *aff,
                                             const fvv_grid &G, int g, int i0, int j0, int k0,
-                                            int i1, int j1, int k1, const int *mixed, int nm,
+                                            int i1, int j1, int k1, const int *mixed,
+                                            const float2 *mbound, int nm,
                                             int n_fg, int v0, int v1, int tl,
                                             int64_t word_off) {
   const int kT = 1 << tl;
@@ -329,8 +340,10 @@ __device__ __forceinline__ int carve_voxels(const CarveParams &p, const CamAffin
     unsigned long long amb = 0;
     for (int m = 0; m < (inside ? nm : 0); ++m) {
       const int c = mixed[m];
+      const float2 eb = mbound[m];  // (negative: no box bounds for this camera)
       int px, py;
-      const int st = classify32(aff[c], fi, fj, fk, px, py);
+      const int st = eb.x >= 0.0f ? classify32_box(aff[c], eb.x, eb.y, fi, fj, fk, px, py)
+                                  : classify32(aff[c], fi, fj, fk, px, py);
       if (st == kOut) continue;
       if (st == kAmb) {
         amb |= 1ull << c;
@@ -371,6 +384,7 @@ __global__ void __launch_bounds__(kCarveThreads, FVV_CARVE_MINB)
   __shared__ CamAffine aff[FVV_MAX_CAMS];
   __shared__ int state[FVV_MAX_CAMS];
   __shared__ int mixed[FVV_MAX_CAMS];
+  __shared__ float2 sbound[FVV_MAX_CAMS], mbound[FVV_MAX_CAMS];
   __shared__ int n_mixed, n_fg, culled;
   __shared__ int blk[4];  // grid, tile origin i0 j0 k0 (thread 0, for the block)
   __shared__ fvv_grid s_grid;  // its grid and occupancy word offset
@@ -419,9 +433,12 @@ __global__ void __launch_bounds__(kCarveThreads, FVV_CARVE_MINB)
   for (int t0 = 0; t0 < p.ncam; t0 += 4 * kWarps) {
     const int t = t0 + 4 * warp + (lane >> 3);
     const int c = t < p.ncam ? p.order[t] : -1;
-    const int st = tile_camera(p, aff, c, i0, i1, j0, j1, k0, k1, lane);
+    bool box;
+    float beu, bev;
+    const int st = tile_camera(p, aff, c, i0, i1, j0, j1, k0, k1, lane, box, beu, bev);
     if (c >= 0 && (lane & 7) == 0) {
       state[t] = st;
+      sbound[t] = box ? make_float2(beu, bev) : make_float2(-1.0f, -1.0f);
       if (st == kTileBg) culled = 1;
     }
   }
@@ -433,8 +450,12 @@ __global__ void __launch_bounds__(kCarveThreads, FVV_CARVE_MINB)
   if (threadIdx.x == 0) {
     int nm = 0, nf = 0;
     for (int t = 0; t < p.ncam; ++t) {
-      if (state[t] == kTileFg) ++nf;
-      else mixed[nm++] = p.order[t];
+      if (state[t] == kTileFg) {
+        ++nf;
+      } else {
+        mbound[nm] = sbound[t];
+        mixed[nm++] = p.order[t];
+      }
     }
     n_mixed = nm;
     n_fg = nf;
@@ -458,8 +479,8 @@ __global__ void __launch_bounds__(kCarveThreads, FVV_CARVE_MINB)
     }
     return;
   }
-  const int my_on = carve_voxels(p, aff, G, g, i0, j0, k0, i1, j1, k1, mixed, n_mixed, n_fg, 0,
-                                 1 << (3 * tl), tl, s_woff);
+  const int my_on = carve_voxels(p, aff, G, g, i0, j0, k0, i1, j1, k1, mixed, mbound, n_mixed,
+                                 n_fg, 0, 1 << (3 * tl), tl, s_woff);
   if (p.count) {  // per-warp atomics: no block barrier at the end
     const int s = __reduce_add_sync(0xffffffffu, my_on);
     if (lane == 0 && s) atomicAdd((unsigned long long *)&p.count[g], (unsigned long long)s);
@@ -476,6 +497,7 @@ __global__ void __launch_bounds__(kCarveThreads, FVV_CARVE_MINB)
     carve_voxels_kernel(const __grid_constant__ CarveParams p) {
   __shared__ CamAffine aff[FVV_MAX_CAMS];
   __shared__ int tmixed[FVV_MAX_CAMS], state[FVV_MAX_CAMS], mixed[FVV_MAX_CAMS];
+  __shared__ float2 sbound[FVV_MAX_CAMS], mbound[FVV_MAX_CAMS];
   __shared__ int n_mixed, n_fg, culled;
   __shared__ fvv_grid s_grid;
   __shared__ int64_t s_woff;
@@ -518,9 +540,12 @@ __global__ void __launch_bounds__(kCarveThreads, FVV_CARVE_MINB)
     if (m0 + 4 * warp >= tnm) break;  // (warp-uniform)
     const int m = m0 + 4 * warp + (lane >> 3);
     const int c = m < tnm ? tmixed[m] : -1;
-    const int st = tile_camera(p, aff, c, i0, i1, j0, j1, k0, k1, lane);
+    bool box;
+    float beu, bev;
+    const int st = tile_camera(p, aff, c, i0, i1, j0, j1, k0, k1, lane, box, beu, bev);
     if (c >= 0 && (lane & 7) == 0) {
       state[m] = st;
+      sbound[m] = box ? make_float2(beu, bev) : make_float2(-1.0f, -1.0f);
       if (st == kTileBg) culled = 1;
     }
   }
@@ -532,15 +557,19 @@ __global__ void __launch_bounds__(kCarveThreads, FVV_CARVE_MINB)
   if (threadIdx.x == 0) {
     int nm = 0, nf = __ldcg(&tw.n_fg);
     for (int m = 0; m < tnm; ++m) {
-      if (state[m] == kTileFg) ++nf;
-      else mixed[nm++] = tmixed[m];
+      if (state[m] == kTileFg) {
+        ++nf;
+      } else {
+        mbound[nm] = sbound[m];
+        mixed[nm++] = tmixed[m];
+      }
     }
     n_mixed = nm;
     n_fg = nf;
   }
   __syncthreads();
-  const int my_on = carve_voxels(p, aff, G, g, i0, j0, k0, i1, j1, k1, mixed, n_mixed, n_fg, 0,
-                                 512, 3, s_woff);
+  const int my_on = carve_voxels(p, aff, G, g, i0, j0, k0, i1, j1, k1, mixed, mbound, n_mixed,
+                                 n_fg, 0, 512, 3, s_woff);
   if (p.count) {
     const int s = __reduce_add_sync(0xffffffffu, my_on);
     if (lane == 0 && s) atomicAdd((unsigned long long *)&p.count[g], (unsigned long long)s);
