@@ -594,8 +594,17 @@ __device__ __forceinline__ void carve_zero(const CarveParams &p, int bid, int nb
 // One launch for the per-call preparation: camera coefficients, silhouette
 // cell maps, zeroed occupancy words (block ranges of one grid).
 __global__ void carve_prep_kernel(const __grid_constant__ CarveParams p, CamAffine *aff,
-                                  int nb_aff, int nb_cells) {
+                                  int nb_aff, int nb_cells, int ncount) {
   const int b = blockIdx.x;
+  if (b == 0) {  // the launch's counters (the carve kernels run after this one)
+    if (threadIdx.x < 32) p.tile_stats[threadIdx.x] = 0ull;
+    if (threadIdx.x == 0) {
+      p.amb[0] = 0ull;
+      p.ntiles[0] = p.ntiles[1] = 0ull;
+    }
+    if (p.count)
+      for (int g = threadIdx.x; g < ncount; g += blockDim.x) p.count[g] = 0;
+  }
   if (b < nb_aff) carve_affine(p, aff, b, nb_aff);
   else if (b < nb_aff + nb_cells) carve_cells(p, b - nb_aff, nb_cells);
   else carve_zero(p, b - nb_aff - nb_cells, gridDim.x - nb_aff - nb_cells);
@@ -671,8 +680,10 @@ int fvv::carve_batch(const fvv_camera *cams, int ncam, const uint32_t *sil_dev,
                      const int64_t *sil_word_off, const CarveGrids *gt_dev, int ngrid_max,
                      int tile_log2, int64_t blocks, int min_views, uint32_t *occ_dev,
                      int64_t *count_dev, void *workspace, size_t ws_bytes, cudaStream_t st) {
-  if (count_dev && ngrid_max) cudaMemsetAsync(count_dev, 0, sizeof(int64_t) * ngrid_max, st);
-  if (ngrid_max == 0 || blocks == 0) return cuda_check("fvv_carve");
+  if (ngrid_max == 0 || blocks == 0) {
+    if (count_dev && ngrid_max) cudaMemsetAsync(count_dev, 0, sizeof(int64_t) * ngrid_max, st);
+    return cuda_check("fvv_carve");
+  }
   static thread_local CarveParams p;  // ~13 KB: keep it off the host stack
   memset(&p, 0, sizeof(p));
   p.ncam = ncam;
@@ -729,17 +740,14 @@ int fvv::carve_batch(const fvv_camera *cams, int ncam, const uint32_t *sil_dev,
     set_error("fvv_carve: %lld blocks", (long long)blocks);
     return FVV_E_LIMIT;
   }
-  cudaMemsetAsync(p.tile_stats, 0, 256, st);
-  cudaMemsetAsync(p.amb, 0, sizeof(unsigned long long), st);
   const int nb_aff = (ngrid_max * ncam + 255) / 256;
   const int nb_cells = (int)((cell_words_total(cams, ncam) + 255) / 256);
   carve_prep_kernel<<<nb_aff + nb_cells + 148 * 2, 256, 0, st>>>(p, (CamAffine *)workspace, nb_aff,
-                                                                nb_cells);
+                                                                nb_cells, ngrid_max);
   // large (stage) grids: classify the 16^3 tiles, then carve the surviving
   // tiles' voxels with kParts blocks each; ROI grids: one kernel per 8^3 tile
   const bool split = p.tile_log2 == 4 && blocks <= kTileCap;
   if (split) {
-    cudaMemsetAsync(p.ntiles, 0, sizeof(unsigned long long), st);
     carve_kernel<true><<<(unsigned)blocks, kCarveThreads, 0, st>>>(p);
     // one block per octant of every tile (C3 ROI batch: ~70k octants); more
     // octants (C5 512^3: 131k, mostly of culled tiles): a capped grid loops
