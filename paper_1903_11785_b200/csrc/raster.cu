@@ -168,12 +168,41 @@ struct RasterArgs {
   // sets *overflow and the sweep kernel then redoes every item
   int64_t nwl, wl_items, wl_pairs;
   uint8_t *dirty;     // optional: per 32-pixel tile of the planes, set when a depth is written
+  // ids wanted: pass 0 also records every depth write (pixel, triangle, depth
+  // bits); one pass over that list then finds each pixel's lowest id at the
+  // final depth (pass 1 re-runs the raster only if the list overflowed)
+  uint4 *hits;
+  unsigned long long *hit_count;
+  int64_t hit_cap;
   uint32_t *slow;     // items the FP32 filter leaves to the warp-sweep kernel
   uint2 *pairs;       // (item, y << 16 | x): candidate pixels from the FP32 filter
   int *wcount;        // [nwl][2]: pairs, items
   int *overflow;
   int pass;
 };
+
+// Warp-aggregated append of this lane's depth write (hit) to the hit list;
+// called by every lane of the warp.
+__device__ __forceinline__ void record_hit(const RasterArgs &A, bool hit, int64_t p, int64_t t,
+                                           double d) {
+  const unsigned m = __ballot_sync(0xffffffffu, hit);
+  if (!m) return;
+  const int lane = threadIdx.x & 31, lead = __ffs(m) - 1;
+  unsigned long long base = 0;
+  if (lane == lead) base = atomicAdd(A.hit_count, (unsigned long long)__popc(m));
+  base = __shfl_sync(0xffffffffu, base, lead);
+  if (hit) {
+    const unsigned long long slot = base + __popc(m & ((1u << lane) - 1u));
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(d);
+    if ((int64_t)slot < A.hit_cap)
+      A.hits[slot] = make_uint4((uint32_t)p, (uint32_t)t, (uint32_t)bits, (uint32_t)(bits >> 32));
+  }
+}
+
+// pass 1 kernels: nothing to do when the hit list holds every depth write
+__device__ __forceinline__ bool pass1_covered(const RasterArgs &A) {
+  return A.pass == 1 && A.hits != nullptr && (int64_t)__ldcg(A.hit_count) <= A.hit_cap;
+}
 
 // Triangle setup as kept in shared memory for the warp's pixel sweep.
 struct TriSmem {
@@ -442,8 +471,10 @@ __global__ void __launch_bounds__(256)
 // the same setup, the pixel must lie in the clamped bounding box, then the
 // inside test with top-left ties and the perspective-correct depth. One
 // warp per filter-warp list.
+template <bool kRec>
 __global__ void __launch_bounds__(256)
     raster_pair_kernel(const __grid_constant__ RasterCams C, RasterArgs A) {
+  if (pass1_covered(A)) return;
   const int64_t nt = device_count(A.nt_dev, A.nt);
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -451,20 +482,47 @@ __global__ void __launch_bounds__(256)
        wl += nwarps) {
     const int n = __ldcg(A.wcount + 2 * wl);
     const uint2 *pl = A.pairs + wl * A.wl_pairs;
-    for (int i = lane; i < n; i += 32) {
-      const uint2 e = pl[i];
-      const int c = (int)(e.x / (uint32_t)nt);
-      const int64_t t = (int64_t)e.x - (int64_t)c * nt;
-      const int x = (int)(e.y & 0xffffu), y = (int)(e.y >> 16);
-      const int width = C.cams[c].width;
-      TriSetup s;
-      if (!tri_setup(width, C.cams[c].height, A.P + (int64_t)c * A.nv, A.T, t, s)) continue;
-      if (x < s.lox || x > s.hix || y < s.loy || y > s.hiy) continue;
-      double d;
-      if (!tri_depth(s, x, y, d)) continue;
-      const int64_t p = C.depth_off[c] + (int64_t)y * width + x;
-      pixel_update(A.pass, d, t, (unsigned long long *)A.depth + p,
-                   A.ids ? (unsigned *)A.ids + p : nullptr, A.dirty, p);
+    if (!kRec) {
+      for (int i = lane; i < n; i += 32) {
+        const uint2 e = pl[i];
+        const int c = (int)(e.x / (uint32_t)nt);
+        const int64_t t = (int64_t)e.x - (int64_t)c * nt;
+        const int x = (int)(e.y & 0xffffu), y = (int)(e.y >> 16);
+        const int width = C.cams[c].width;
+        TriSetup s;
+        if (!tri_setup(width, C.cams[c].height, A.P + (int64_t)c * A.nv, A.T, t, s)) continue;
+        if (x < s.lox || x > s.hix || y < s.loy || y > s.hiy) continue;
+        double d;
+        if (!tri_depth(s, x, y, d)) continue;
+        const int64_t p = C.depth_off[c] + (int64_t)y * width + x;
+        pixel_update(A.pass, d, t, (unsigned long long *)A.depth + p,
+                     A.ids ? (unsigned *)A.ids + p : nullptr, A.dirty, p);
+      }
+      continue;
+    }
+    // kRec (pass 0 of an id raster): warp-uniform trip count, since the
+    // depth writes are appended to the hit list warp-aggregated
+    for (int i0 = 0; i0 < n; i0 += 32) {
+      const int i = i0 + lane;
+      bool hit = false;
+      double d = 0.0;
+      int64_t p = 0, t = 0;
+      if (i < n) {
+        const uint2 e = pl[i];
+        const int c = (int)(e.x / (uint32_t)nt);
+        t = (int64_t)e.x - (int64_t)c * nt;
+        const int x = (int)(e.y & 0xffffu), y = (int)(e.y >> 16);
+        const int width = C.cams[c].width;
+        TriSetup s;
+        if (tri_setup(width, C.cams[c].height, A.P + (int64_t)c * A.nv, A.T, t, s) &&
+            !(x < s.lox || x > s.hix || y < s.loy || y > s.hiy) && tri_depth(s, x, y, d)) {
+          p = C.depth_off[c] + (int64_t)y * width + x;
+          pixel_update(A.pass, d, t, (unsigned long long *)A.depth + p,
+                       A.ids ? (unsigned *)A.ids + p : nullptr, A.dirty, p);
+          hit = true;
+        }
+      }
+      record_hit(A, hit, p, t, d);
     }
   }
 }
@@ -479,6 +537,8 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(kRasterThreads, 8)
     raster_small_kernel(const __grid_constant__ RasterCams C, RasterArgs A) {
   __shared__ TriSmem sm[kRasterThreads];
+  if (pass1_covered(A)) return;
+  const bool rec = A.hits != nullptr && A.pass == 0;
   const int lane = threadIdx.x & 31;
   TriSmem *wsm = sm + (threadIdx.x & ~31);
   const int64_t nt = device_count(A.nt_dev, A.nt);
@@ -557,6 +617,9 @@ __global__ void __launch_bounds__(kRasterThreads, 8)
       }
       const int own_incl = __shfl_sync(0xffffffffu, incl, own);
       const int own_cnt = __shfl_sync(0xffffffffu, npx, own);
+      bool hit = false;
+      double hd = 0.0;
+      int64_t hp = 0, ht = 0;
       if (idx < sum) {
         const TriSmem &m = wsm[own];
         int k = idx - (own_incl - own_cnt);
@@ -572,16 +635,19 @@ __global__ void __launch_bounds__(kRasterThreads, 8)
         const int y = m.loy + qy, x = m.lox + (k - qy * m.bw);
         TriSetup s;
         smem_to_setup(m, s);
-        double d;
-        if (tri_depth(s, x, y, d)) {
+        if (tri_depth(s, x, y, hd)) {
           const int W = C.cams[m.cam].width;
           unsigned long long *dp = (unsigned long long *)(A.depth + C.depth_off[m.cam]);
           unsigned *ip = (unsigned *)(A.ids ? A.ids + C.depth_off[m.cam] : nullptr);
           const int64_t pxl = (int64_t)y * W + x;
-          pixel_update(A.pass, d, m.t, dp + pxl, ip ? ip + pxl : nullptr, A.dirty,
+          pixel_update(A.pass, hd, m.t, dp + pxl, ip ? ip + pxl : nullptr, A.dirty,
                        C.depth_off[m.cam] + pxl);
+          hit = true;
+          hp = C.depth_off[m.cam] + pxl;
+          ht = m.t;
         }
       }
+      if (rec) record_hit(A, hit, hp, ht, hd);
     }
     __syncwarp();
   }
@@ -589,6 +655,8 @@ __global__ void __launch_bounds__(kRasterThreads, 8)
 
 __global__ void __launch_bounds__(kBigThreads)
     raster_big_kernel(const __grid_constant__ RasterCams C, RasterArgs A) {
+  if (pass1_covered(A)) return;
+  const bool rec = A.hits != nullptr && A.pass == 0;
   const int64_t nt = device_count(A.nt_dev, A.nt);
   int64_t nq = __ldcg(A.qcount);
   if (nq > A.qcap) nq = A.qcap;
@@ -603,13 +671,37 @@ __global__ void __launch_bounds__(kBigThreads)
     const int64_t npx = (int64_t)bw * (s.hiy - s.loy + 1);
     unsigned long long *dp = (unsigned long long *)(A.depth + C.depth_off[c]);
     unsigned *ip = (unsigned *)(A.ids ? A.ids + C.depth_off[c] : nullptr);
-    for (int64_t k = threadIdx.x; k < npx; k += blockDim.x) {
-      const int y = s.loy + (int)(k / bw), x = s.lox + (int)(k % bw);
-      double d;
-      if (!tri_depth(s, x, y, d)) continue;
-      const int64_t p = (int64_t)y * width + x;
-      pixel_update(A.pass, d, t, dp + p, ip ? ip + p : nullptr, A.dirty, C.depth_off[c] + p);
+    for (int64_t k0 = 0; k0 < npx; k0 += blockDim.x) {  // (block-uniform trip count)
+      const int64_t k = k0 + threadIdx.x;
+      bool hit = false;
+      double d = 0.0;
+      int64_t hp = 0;
+      if (k < npx) {
+        const int y = s.loy + (int)(k / bw), x = s.lox + (int)(k % bw);
+        if (tri_depth(s, x, y, d)) {
+          const int64_t p = (int64_t)y * width + x;
+          pixel_update(A.pass, d, t, dp + p, ip ? ip + p : nullptr, A.dirty, C.depth_off[c] + p);
+          hit = true;
+          hp = C.depth_off[c] + p;
+        }
+      }
+      if (rec) record_hit(A, hit, hp, t, d);
     }
+  }
+}
+
+// The id pass over the hit list: the lowest triangle id among the writes
+// that reached the pixel's final depth (visibility.py:80-91 keeps the first
+// triangle, in id order, with the minimum depth).
+__global__ void raster_hits_kernel(RasterArgs A) {
+  const unsigned long long n = __ldcg(A.hit_count);
+  if ((int64_t)n > A.hit_cap) return;  // overflow: the pass-1 raster does it
+  const unsigned long long *depth = (const unsigned long long *)A.depth;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint4 h = A.hits[i];
+    const unsigned long long bits = (unsigned long long)h.z | ((unsigned long long)h.w << 32);
+    if (bits == __ldcg(depth + h.x)) atomicMin((unsigned *)A.ids + h.x, h.y);
   }
 }
 
@@ -958,8 +1050,17 @@ static FilterShape filter_shape(int64_t num_triangles, int ncam) {
 }
 
 struct RasterLayout {
-  size_t counts, queue, proj, q, slow, pairs, total;
+  size_t counts, queue, proj, q, slow, pairs, hits, total;
+  int64_t hit_cap;
 };
+
+// hit-list entries of a one-camera raster (the virtual view's id pass)
+static int64_t raster_hit_cap(int64_t num_triangles, int ncam) {
+  if (ncam != 1) return 0;
+  int64_t cap = 2 * num_triangles;
+  cap = cap < (1 << 16) ? (1 << 16) : cap;
+  return cap > ((int64_t)8 << 20) ? ((int64_t)8 << 20) : cap;
+}
 
 // [counters][per-warp list counts][big queue][projected vertices f64]
 // [projected vertices f32][sweep items][candidate pixel pairs]
@@ -973,7 +1074,9 @@ static RasterLayout raster_layout(int64_t num_vertices, int64_t num_triangles, i
   L.q = align256(L.proj + sizeof(double4) * nvc);
   L.slow = align256(L.q + sizeof(float2) * nvc);
   L.pairs = align256(L.slow + 4 * (size_t)(f.nwl * f.wl_items));
-  L.total = L.pairs + sizeof(uint2) * (size_t)(f.nwl * f.wl_pairs);
+  L.hits = align256(L.pairs + sizeof(uint2) * (size_t)(f.nwl * f.wl_pairs));
+  L.hit_cap = raster_hit_cap(num_triangles, ncam);
+  L.total = L.hits + sizeof(uint4) * (size_t)L.hit_cap;
   return L;
 }
 
@@ -1084,14 +1187,27 @@ static int rasterize_impl(const fvv_camera *cams, int ncam, const double *verts_
   A.pairs = (uint2 *)(ws + L.pairs);
   if (dirty)  // planes addressed relative to plane 0 (the dirty map's origin)
     for (int c = 0; c < ncam; ++c) C.depth_off[c] = plane_off[c] - plane_off[0];
-  cudaMemsetAsync(ws, 0, 16, st);  // big-queue counter, overflow flag
+  const bool hits = tri_id_dev && L.hit_cap > 0;
+  A.hits = hits ? (uint4 *)(ws + L.hits) : nullptr;
+  A.hit_count = (unsigned long long *)(ws + 16);
+  A.hit_cap = L.hit_cap;
+  cudaMemsetAsync(ws, 0, 32, st);  // big-queue counter, overflow flag, hit count
   raster_filter_kernel<<<(unsigned)fs.bx, 256, 0, st>>>(C, A);
   note_launches(1);
-  // pass 0: depth (RED.MIN of the depth bits); pass 1 (ids wanted): the
-  // lowest triangle id reaching the final depth, over the same work lists
+  // pass 0: depth (RED.MIN of the depth bits); ids wanted: the lowest
+  // triangle id reaching the final depth, from the hit list pass 0 recorded
+  // (one camera), else (or when the list overflowed) a pass 1 over the same
+  // work lists
   for (int pass = 0; pass < (tri_id_dev ? 2 : 1); ++pass) {
     A.pass = pass;
-    raster_pair_kernel<<<148 * 16, 256, 0, st>>>(C, A);
+    if (pass == 1 && hits) {
+      raster_hits_kernel<<<148 * 8, 256, 0, st>>>(A);
+      note_launches(1);
+    }
+    if (hits && pass == 0)
+      raster_pair_kernel<true><<<148 * 16, 256, 0, st>>>(C, A);
+    else
+      raster_pair_kernel<false><<<148 * 16, 256, 0, st>>>(C, A);
     raster_small_kernel<<<148 * 16, kRasterThreads, 0, st>>>(C, A);
     raster_big_kernel<<<148 * 4, kBigThreads, 0, st>>>(C, A);
     note_launches(3);

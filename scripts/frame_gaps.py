@@ -56,7 +56,9 @@ for s_, e_, n_ in ks:
     per.setdefault(k, []).append(e_ - s_)
 print("per-kernel device time (us/frame, warm, in-graph):")
 for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
-    print(f"  {sum(v) / args.frames:8.1f}  x{len(v) / args.frames:4.1f}  {k}")
+    n = max(1, round(len(v) / args.frames))
+    each = [round(sum(v[i::n]) / args.frames, 1) for i in range(n)] if n > 1 else ""
+    print(f"  {sum(v) / args.frames:8.1f}  x{len(v) / args.frames:4.1f}  {k} {each}")
 print("largest gaps (us):")
 for g, a, b in gaps[:12]:
     print(f"  {g:7.1f}  {a} -> {b}")
