@@ -30,7 +30,10 @@ constexpr int kCarveThreads = 256;
 #define FVV_CARVE_MINB 6  // resident 256-thread blocks per SM the tile kernels are built for
 #endif
 constexpr int kCarveWordsPerBlock = 128;  // 4096 voxels per block
-constexpr int64_t kAmbCap = 1 << 20;     // deferred-voxel queue entries
+#ifndef FVV_AMB_CAP
+#define FVV_AMB_CAP (1 << 22)  // 64 MB: large grids x many cameras (C5 1024^3) fill 1M
+#endif
+constexpr int64_t kAmbCap = FVV_AMB_CAP;  // deferred-voxel queue entries
 constexpr int64_t kTileCap = 1 << 19;    // split mode: surviving-tile records
 constexpr int64_t kVoxelGrid = 100000;   // split mode: one block per octant up to this
 constexpr int64_t kVoxelCap = 148 * 64;  //   else this many blocks loop over the octants
