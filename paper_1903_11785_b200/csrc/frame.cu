@@ -378,6 +378,8 @@ struct fvv_frame {
     bool ready = false;
   } caps;
   DevBuf plan, inputs;  // FramePlan, FrameInputs (device-planned frames)
+  cudaStream_t side = nullptr;  // device-planned frames: the virtual view's raster
+  cudaEvent_t fork = nullptr, join = nullptr;
   // one CUDA graph of the device-planned frame per input binding
   cudaGraphExec_t graph = nullptr;
   std::vector<char> graph_key, pending_key;
@@ -514,6 +516,9 @@ fvv_frame *fvv_frame_create(const fvv_camera *cams, int ncam, const fvv_frame_co
     return nullptr;
   }
   for (int e = 0; e < 9; ++e) cudaEventCreate(&f->ev[e]);
+  cudaStreamCreateWithFlags(&f->side, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&f->fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&f->join, cudaEventDisableTiming);
   if (f->sil.ensure(4 * (size_t)f->sil_words) || f->occ_c.ensure(4 * (size_t)((
           f->coarse.dims[0] * f->coarse.dims[1] * f->coarse.dims[2] + 31) / 32)) ||
       f->cnt_c.ensure(64) || f->ccl_counts.ensure(64) ||
@@ -530,6 +535,9 @@ fvv_frame *fvv_frame_create(const fvv_camera *cams, int ncam, const fvv_frame_co
 void fvv_frame_destroy(fvv_frame *f) {
   if (!f) return;
   if (f->graph) cudaGraphExecDestroy(f->graph);
+  if (f->side) cudaStreamDestroy(f->side);
+  if (f->fork) cudaEventDestroy(f->fork);
+  if (f->join) cudaEventDestroy(f->join);
   for (int e = 0; e < 9; ++e) cudaEventDestroy(f->ev[e]);
   if (f->host_small) cudaFreeHost(f->host_small);
   delete f;
@@ -567,9 +575,50 @@ static int enqueue_tail(fvv_frame *f, const fvv_camera *virt, const int32_t *ran
                         const uint8_t *frames_dev, const int64_t *frame_off,
                         const uint8_t *fallback, cudaStream_t st, int *out_stage, int64_t nv,
                         const int64_t *nv_dev, int64_t nt_ub, const int64_t *ntri_dev,
-                        bool have_mesh, const FrameInputs *in) {
+                        bool have_mesh, const FrameInputs *in, cudaStream_t side) {
   const fvv_frame_config &cfg = f->cfg;
   const int ncam = f->ncam;
+  // ---- E raster of the virtual view (render.py:64-113): it needs only the
+  // mesh, so with a side stream it runs beside D-1 / D-2 (a fork in the
+  // captured frame graph), joined before the colour pass ----
+  f->virt_px = 0;
+  const bool vraster = virt && have_mesh;
+  int64_t np = 0;
+  if (virt) {
+    np = (int64_t)virt->width * virt->height;
+    f->virt_px = np;
+    FVV_TRY(7, f->color.ensure(3 * (size_t)np));
+    FVV_TRY(7, f->source.ensure(4 * (size_t)np));
+    FVV_TRY(7, f->covered.ensure((size_t)np));
+    FVV_TRY(7, f->code.ensure((size_t)np));
+  }
+  if (vraster) {
+    cudaStream_t vs = side ? side : st;
+    if (side) {
+      cudaEventRecord(f->fork, st);
+      cudaStreamWaitEvent(side, f->fork, 0);
+    }
+    FVV_TRY(7, f->vplane_d.ensure(8 * (size_t)np));
+    FVV_TRY(7, f->vplane_id.ensure(4 * (size_t)np));
+    const size_t vwb = fvv_raster_workspace_bytes(nv, nt_ub, 1);
+    FVV_TRY(7, f->vraster_ws.ensure(vwb));
+    const int64_t off0 = 0;
+    FVV_TRY(7, f->vdirty.ensure((size_t)(np + 31) / 32));
+    // the map is valid for one plane pair at one image size
+    const bool vfresh = f->vdirty_for[0] != f->vplane_d.p || f->vdirty_for[1] != f->vplane_id.p ||
+                        f->vdirty_for[2] != f->vdirty.p || f->vdirty_px != np;
+    FVV_TRY(7, fvv_rasterize_tracked(virt, 1, f->verts.as<double>(), nv, nv_dev,
+                                     f->tris.as<int32_t>(), nt_ub, ntri_dev,
+                                     f->vplane_d.as<double>(), &off0, f->vplane_id.as<int32_t>(),
+                                     f->vraster_ws.p, f->vraster_ws.cap, f->vdirty.as<uint8_t>(),
+                                     vfresh, vs));
+    f->vdirty_for[0] = f->vplane_d.p;
+    f->vdirty_for[1] = f->vplane_id.p;
+    f->vdirty_for[2] = f->vdirty.p;
+    f->vdirty_px = np;
+    if (side) cudaEventRecord(f->join, side);
+  }
+
   // ---- D-1 depth images, D-2 visibility (pipeline.py:198-207) ----
   if (have_mesh) {
     FVV_TRY(5, f->depth.ensure(8 * (size_t)f->planes));
@@ -604,34 +653,10 @@ static int enqueue_tail(fvv_frame *f, const fvv_camera *virt, const int32_t *ran
                                 sources ? f->src.as<int32_t>() : nullptr, st));
   stage_mark(f, 6, st);
 
-  // ---- E: one virtual view (render.py:64-113) ----
-  f->virt_px = 0;
+  // ---- E colour pass ----
   if (virt) {
-    const int64_t np = (int64_t)virt->width * virt->height;
-    f->virt_px = np;
-    FVV_TRY(7, f->color.ensure(3 * (size_t)np));
-    FVV_TRY(7, f->source.ensure(4 * (size_t)np));
-    FVV_TRY(7, f->covered.ensure((size_t)np));
-    FVV_TRY(7, f->code.ensure((size_t)np));
-    if (have_mesh) {
-      FVV_TRY(7, f->vplane_d.ensure(8 * (size_t)np));
-      FVV_TRY(7, f->vplane_id.ensure(4 * (size_t)np));
-      const size_t vwb = fvv_raster_workspace_bytes(nv, nt_ub, 1);
-      FVV_TRY(7, f->vraster_ws.ensure(vwb));
-      const int64_t off0 = 0;
-      FVV_TRY(7, f->vdirty.ensure((size_t)(np + 31) / 32));
-      // the map is valid for one plane pair at one image size
-      const bool vfresh = f->vdirty_for[0] != f->vplane_d.p || f->vdirty_for[1] != f->vplane_id.p ||
-                          f->vdirty_for[2] != f->vdirty.p || f->vdirty_px != np;
-      FVV_TRY(7, fvv_rasterize_tracked(virt, 1, f->verts.as<double>(), nv, nv_dev,
-                                       f->tris.as<int32_t>(), nt_ub, ntri_dev,
-                                       f->vplane_d.as<double>(), &off0, f->vplane_id.as<int32_t>(),
-                                       f->vraster_ws.p, f->vraster_ws.cap,
-                                       f->vdirty.as<uint8_t>(), vfresh, st));
-      f->vdirty_for[0] = f->vplane_d.p;
-      f->vdirty_for[1] = f->vplane_id.p;
-      f->vdirty_for[2] = f->vdirty.p;
-      f->vdirty_px = np;
+    if (vraster) {
+      if (side) cudaStreamWaitEvent(st, f->join, 0);
       FVV_TRY(7, f->rcounts.ensure(8 * (size_t)(1 + ncam)));
       FVV_TRY(7, fvv_render_count(f->cams.data(), ncam, virt, f->vplane_id.as<int32_t>(),
                                   f->src.as<int32_t>(), f->rcounts.as<int64_t>(), st));
@@ -830,7 +855,7 @@ static int run_host_planned(fvv_frame *f, const uint8_t *masks_dev, const fvv_ca
 
   const bool have_mesh = f->nv > 0 && nt_ub > 0;
   FVV_TRY(5, enqueue_tail(f, virt, rank_pos, frames_dev, frame_off, fallback, st, out_stage, f->nv,
-                          nullptr, nt_ub, ntri_dev, have_mesh, nullptr));
+                          nullptr, nt_ub, ntri_dev, have_mesh, nullptr, nullptr));
 
   // ---- final counters (one read) ----
   int64_t *h = hs;
@@ -947,7 +972,8 @@ static int enqueue_device_planned(fvv_frame *f, const uint8_t *masks_dev, const 
   const int64_t nt_ub = 5 * K.s;
   f->vis_stride = (nt_ub + 31) / 32 > 0 ? (nt_ub + 31) / 32 : 1;
   FVV_TRY(5, enqueue_tail(f, virt, rank_pos, frames_dev, frame_off, fallback, st, out_stage, K.v,
-                          totals, nt_ub, totals + 2, true, f->inputs.as<FrameInputs>()));
+                          totals, nt_ub, totals + 2, true, f->inputs.as<FrameInputs>(),
+                          f->side));
   // ---- every count in one read ----
   const int64_t *nroi = &P->nroi;
   readback(f, st, {{f->ccl_counts.p, kDs, 16, nullptr, 0, 0},
