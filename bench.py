@@ -409,8 +409,10 @@ def run_b200(args):
 
         # warm-up covers every distinct input on every lane (buffer growth,
         # pinned readback pool) so the timed steps are steady state
-        # (>= 3 frames per executor: host-planned, device-planned, graph capture)
-        run_e2e(max(args.warmup, 2 * len(host) + 2, 6 * lanes + 2))
+        # (>= 6 frames per executor, two executors per lane: host-planned,
+        # device-planned, graph capture, and capacity growth over the cycled
+        # frames all happen before the timed region)
+        run_e2e(max(args.warmup, 2 * len(host) + 2, 12 * lanes + 2))
         torch.cuda.synchronize()
         barrier(world)
         R.H2D_BYTES["frames"] = R.H2D_BYTES["masks"] = 0

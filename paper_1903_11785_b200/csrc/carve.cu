@@ -682,7 +682,8 @@ __global__ void store_carve_grids_kernel(const __grid_constant__ CarveGrids src,
 int fvv::carve_batch(const fvv_camera *cams, int ncam, const uint32_t *sil_dev,
                      const int64_t *sil_word_off, const CarveGrids *gt_dev, int ngrid_max,
                      int tile_log2, int64_t blocks, int min_views, uint32_t *occ_dev,
-                     int64_t *count_dev, void *workspace, size_t ws_bytes, cudaStream_t st) {
+                     int64_t *count_dev, void *workspace, size_t ws_bytes, cudaStream_t st,
+                     bool reuse_cells) {
   if (ngrid_max == 0 || blocks == 0) {
     if (count_dev && ngrid_max) cudaMemsetAsync(count_dev, 0, sizeof(int64_t) * ngrid_max, st);
     return cuda_check("fvv_carve");
@@ -744,7 +745,9 @@ int fvv::carve_batch(const fvv_camera *cams, int ncam, const uint32_t *sil_dev,
     return FVV_E_LIMIT;
   }
   const int nb_aff = (ngrid_max * ncam + 255) / 256;
-  const int nb_cells = (int)((cell_words_total(cams, ncam) + 255) / 256);
+  // (the cell maps depend on the silhouettes only: a batch over the same
+  // planes as the previous carve into this workspace reuses them)
+  const int nb_cells = reuse_cells ? 0 : (int)((cell_words_total(cams, ncam) + 255) / 256);
   carve_prep_kernel<<<nb_aff + nb_cells + 148 * 2, 256, 0, st>>>(p, (CamAffine *)workspace, nb_aff,
                                                                 nb_cells, ngrid_max);
   // large (stage) grids: classify the 16^3 tiles, then carve the surviving
@@ -816,5 +819,5 @@ extern "C" int fvv_carve(const fvv_camera *cams, int ncam, const uint32_t *sil_d
     note_launches(1);
   }
   return carve_batch(cams, ncam, sil_dev, sil_word_off, dst, ngrid, T.tile_log2, T.total_tiles,
-                     min_views, occ_dev, count_dev, workspace, ws_bytes, st);
+                     min_views, occ_dev, count_dev, workspace, ws_bytes, st, false);
 }

@@ -953,12 +953,12 @@ static int enqueue_device_planned(fvv_frame *f, const uint8_t *masks_dev, const 
   FVV_TRY(3, carve_batch(f->cams.data(), ncam, f->sil.as<uint32_t>(), f->word_off.data(),
                          &P->carve, FVV_MAX_GRIDS, 4, K.tiles, cfg.min_views,
                          f->occ_f.as<uint32_t>(), f->cnt_f.as<int64_t>(), f->carve_ws.p,
-                         f->carve_ws.cap, st));
+                         f->carve_ws.cap, st, true));  // (B-1 built the cell maps)
   stage_mark(f, 3, st);
   // ---- C polygonize ----
   FVV_TRY(4, f->mesh_ws.ensure(mesh_ws_bytes(K.tw, FVV_MAX_GRIDS)));
   FVV_TRY(4, mesh_prepare_batch(&P->mesh, K.tw, FVV_MAX_GRIDS, f->occ_f.as<uint32_t>(),
-                                f->mesh_ws.p, f->mesh_ws.cap, st));
+                                f->mesh_ws.p, f->mesh_ws.cap, st, f->side, f->fork, f->join));
   FVV_TRY(4, f->mesh_scratch.ensure(mesh_emit_scratch(K.v, K.s)));
   FVV_TRY(4, f->verts.ensure(24 * (size_t)K.v));
   FVV_TRY(4, f->tris.ensure(12 * (size_t)(5 * K.s)));

@@ -229,7 +229,8 @@ __host__ __device__ inline bool carve_grid_tiles(const fvv_grid &g, int tl, uint
 int carve_batch(const fvv_camera *cams, int ncam, const uint32_t *sil_dev,
                 const int64_t *sil_word_off, const CarveGrids *gt_dev, int ngrid_max,
                 int tile_log2, int64_t blocks_cap, int min_views, uint32_t *occ_dev,
-                int64_t *count_dev, void *workspace, size_t ws_bytes, cudaStream_t st);
+                int64_t *count_dev, void *workspace, size_t ws_bytes, cudaStream_t st,
+                bool reuse_cells = false);  // cell maps left by the previous carve of these planes
 size_t carve_grids_offset(const fvv_camera *cams, int ncam);  // table slot in the workspace
 
 // Grid table of one batched polygonize (mesh.cu), in device memory: grid g's
@@ -282,7 +283,9 @@ size_t mesh_ws_bytes(int64_t tw_cap, int ngrid_max);
 int64_t *mesh_ws_totals(void *ws, int64_t tw_cap, int ngrid_max);  // V, S, T
 int64_t *mesh_ws_info(void *ws, int64_t tw_cap, int ngrid_max);    // [ngrid][8]
 int mesh_prepare_batch(const MeshGrids *G_dev, int64_t tw_cap, int ngrid_max,
-                       const uint32_t *occ_dev, void *ws_dev, size_t ws_bytes, cudaStream_t st);
+                       const uint32_t *occ_dev, void *ws_dev, size_t ws_bytes, cudaStream_t st,
+                       cudaStream_t side = nullptr, cudaEvent_t fork = nullptr,
+                       cudaEvent_t join = nullptr);
 size_t mesh_emit_scratch(int64_t cap_v, int64_t cap_s);
 int mesh_emit_batch(const fvv_camera *cams_by_id, int ncam, const uint32_t *sil_dev,
                     const int64_t *sil_word_off, const MeshGrids *G_dev, int64_t tw_cap,

@@ -42,6 +42,7 @@ struct MeshBufs {
   uint32_t *sflags;    // [tw_total]
   int32_t *sprefix;    // [tw_total]
   int64_t *sums;       // scan chunk sums
+  int64_t *sums2;      // the cell scan's when it runs beside the vertex scan
   int64_t *totals;     // [0] V, [1] S, [2] T
   int64_t *info;       // [ngrid][8]: vbase V sbase S tbase T fallback inconsistent
   // phase B
@@ -654,7 +655,7 @@ constexpr int kMeshGrid = 148 * 8;
 static size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
 
 struct PrepLayout {
-  size_t tw, eflags, vprefix, sflags, sprefix, sums, totals, info, slot5, grids, total;
+  size_t tw, eflags, vprefix, sflags, sprefix, sums, sums2, totals, info, slot5, grids, total;
 };
 
 // workspace of a batch of up to ngrid grids and tw_total k-row words
@@ -672,6 +673,7 @@ static PrepLayout prep_layout(int64_t tw_total, int ngrid) {
   L.sflags = take(4 * (size_t)tw_total);
   L.sprefix = take(4 * (size_t)tw_total);
   L.sums = take(onepass_bytes<int64_t>(3 * tw_total + 1));  // scan status words
+  L.sums2 = take(onepass_bytes<int64_t>(tw_total + 1));      // (the concurrent cell scan's)
   L.totals = take(8 * 4);  // V, S, T, S for the triangle scan (0: phase B skipped)
   L.info = take(8 * 8 * (size_t)(ngrid > 0 ? ngrid : 1));
   L.slot5 = take(sizeof(int64_t) * 5 * (size_t)(ngrid > 0 ? ngrid : 1) + sizeof(Slot5));
@@ -690,6 +692,7 @@ static MeshBufs bufs_from(void *ws, const PrepLayout &L) {
   B.sflags = (uint32_t *)(p + L.sflags);
   B.sprefix = (int32_t *)(p + L.sprefix);
   B.sums = (int64_t *)(p + L.sums);
+  B.sums2 = (int64_t *)(p + L.sums2);
   B.totals = (int64_t *)(p + L.totals);
   B.info = (int64_t *)(p + L.info);
   B.slot_base = (int64_t *)(p + L.slot5);
@@ -771,7 +774,8 @@ int64_t *fvv::mesh_ws_info(void *ws, int64_t tw_cap, int ngrid_max) {
 
 int fvv::mesh_prepare_batch(const MeshGrids *G_dev, int64_t tw_cap, int ngrid_max,
                             const uint32_t *occ_dev, void *ws_dev, size_t ws_bytes,
-                            cudaStream_t st) {
+                            cudaStream_t st, cudaStream_t side, cudaEvent_t fork,
+                            cudaEvent_t join) {
   int rc = ensure_tables();
   if (rc) return rc;
   const PrepLayout L = prep_layout(tw_cap, ngrid_max);
@@ -785,10 +789,19 @@ int fvv::mesh_prepare_batch(const MeshGrids *G_dev, int64_t tw_cap, int ngrid_ma
   if (tw_cap > 0) {
     mesh_transpose_kernel<<<kMeshGrid, 256, 0, st>>>(G_dev, B);
     note_launches(1);
+    // the vertex and surface-cell scans read the same k-rows only: with a
+    // side stream they run side by side (own scan status words each)
+    if (side) {
+      cudaEventRecord(fork, st);
+      cudaStreamWaitEvent(side, fork, 0);
+    }
+    CellFlags cf{G_dev, B.tw, B.sflags, B.sprefix};
+    onepass_scan(cf, &G_dev->tw_total, 0, tw_cap, (void *)(side ? B.sums2 : B.sums),
+                 B.totals + 1, side ? side : st);
+    if (side) cudaEventRecord(join, side);
     EdgeFlags ef{G_dev, B.tw, B.eflags, B.vprefix};
     onepass_scan(ef, &G_dev->tw3, 0, 3 * tw_cap, (void *)B.sums, B.totals + 0, st);
-    CellFlags cf{G_dev, B.tw, B.sflags, B.sprefix};
-    onepass_scan(cf, &G_dev->tw_total, 0, tw_cap, (void *)B.sums, B.totals + 1, st);
+    if (side) cudaStreamWaitEvent(st, join, 0);
   }
   mesh_grid_counts_kernel<<<1, 128, 0, st>>>(G_dev, B);
   note_launches(1);
@@ -887,7 +900,8 @@ int fvv_mesh_prepare(const fvv_grid *grids, int ngrid, const uint32_t *occ_dev,
   MeshGrids *G_dev = (MeshGrids *)((char *)ws_dev + L.grids);
   store_mesh_grids_kernel<<<1, 256, 0, st>>>(G, G_dev);
   note_launches(1);
-  return mesh_prepare_batch(G_dev, G.tw_total, ngrid, occ_dev, ws_dev, ws_bytes, st);
+  return mesh_prepare_batch(G_dev, G.tw_total, ngrid, occ_dev, ws_dev, ws_bytes, st, nullptr,
+                            nullptr, nullptr);
 }
 
 // Reads the counts fvv_mesh_prepare left in the workspace: totals[3] = {V, S, T}
