@@ -51,8 +51,9 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="C3")
     ap.add_argument("--frames", type=int, default=4, help="distinct input frames per rank")
-    ap.add_argument("--lanes", type=int, default=8,
-                    help="concurrent executor lanes (threads + streams) per GPU")
+    ap.add_argument("--lanes", type=int, default=None,
+                    help="concurrent executor lanes (threads + streams) per GPU; default 8, "
+                         "3 for C4 (its 32 x 4K depth planes take 2.1 GB per executor)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--stage-json", default=None, help="write per-stage ms here (rank 0)")
@@ -750,6 +751,8 @@ def run_reference(args):
 
 def main():
     args = parse()
+    if args.lanes is None:
+        args.lanes = 3 if args.workload == "C4" else 8
     rc = self_launch(args)
     if rc is not None:
         sys.exit(rc)

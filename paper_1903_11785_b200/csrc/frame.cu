@@ -69,7 +69,9 @@ struct DevBuf {
     if (p) cudaFree(p);
     p = nullptr;
     cap = 0;
-    size_t want = bytes + bytes / 4 + 256;
+    // exact (rounded to 256 B): device-planned buffers come sized from
+    // capacities that already carry headroom, the others are fixed per rig
+    size_t want = (bytes + 255) & ~(size_t)255;
     if (cudaMalloc(&p, want) != cudaSuccess) {
       cudaGetLastError();
       set_error("frame executor: cudaMalloc(%zu) failed", want);
