@@ -13,11 +13,13 @@
 //                       (hull.py:124-133); roots are linked by atomicMin, so
 //                       every root ends as its component's minimum rank =
 //                       minimum linear index
-//   3. flatten        : parent[r] = find(r)
-//   4. root scan      : label(root) = 1 + #roots before it — ascending
+//   3. root scan      : label(root) = 1 + #roots before it — ascending
 //                       minimum linear index, as hull.py:195-197 numbers them
-//   5. stats          : per-label count and inclusive bbox with
-//                       warp-aggregated integer atomics (hull.py:201-214)
+//                       (and the component's stats record initialised)
+//   4. stats          : each voxel's root by find, per-label count and
+//                       inclusive bbox with warp-aggregated integer atomics
+//                       (hull.py:201-214); the last block out writes the
+//                       component table
 // Integer-only and order independent; results are bit-identical to the
 // reference for every launch configuration (its block_dims independence,
 // tests/test_hull.py:159-168, holds trivially).
@@ -246,40 +248,50 @@ __global__ void ccl_union_kernel(const uint32_t *__restrict__ occ, CclWs w, int6
   }
 }
 
-// -- 3. flatten ----------------------------------------------------------------
-__global__ void ccl_flatten_kernel(CclWs w) {
-  const int64_t n_on = __ldcg(w.counts);
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_on;
-       r += (int64_t)gridDim.x * blockDim.x)
-    w.parent[r] = uf_find(w.parent, (int32_t)r);
-}
-
 // -- 4. label roots in rank order --------------------------------------------
+// (a root's emit also initialises its component's stats record)
 struct RootLabel {
   const int32_t *parent;
   int32_t *rank_label;
+  int32_t *stats;
   typedef int Item;
   __device__ int load(int64_t r) const { return parent[r] == (int32_t)r; }
   __device__ int64_t value(int v) const { return v; }
   __device__ void emit(int64_t r, int64_t prefix, int v) const {
-    if (v) rank_label[r] = (int32_t)(prefix + 1);
-  }
-};
-
-__global__ void ccl_stats_init_kernel(CclWs w) {
-  const int64_t ncomp = __ldcg(w.counts + 1);
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ncomp;
-       c += (int64_t)gridDim.x * blockDim.x) {
-    int32_t *s = w.stats + 8 * c;
+    if (!v) return;
+    rank_label[r] = (int32_t)(prefix + 1);
+    int32_t *s = stats + 8 * prefix;
     s[0] = 0;
     s[1] = s[2] = s[3] = 0x7fffffff;
     s[4] = s[5] = s[6] = -1;
     s[7] = 0;
   }
-}
+};
 
 // -- 5. per-rank label + component count/bbox ----------------------------------
-__global__ void ccl_stats_kernel(CclWs w, int64_t nx, int64_t ny) {
+__device__ __forceinline__ void export_components(const CclWs &w, fvv_component *out, int64_t cap,
+                                                  int64_t tid, int64_t stride) {
+  const int64_t ncomp = __ldcg(w.counts + 1);
+  const int64_t n = ncomp < cap ? ncomp : cap;
+  for (int64_t c = tid; c < n; c += stride) {
+    const int32_t *s = w.stats + 8 * c;
+    fvv_component rec;
+    rec.id = c + 1;
+    rec.voxel_count = __ldcg(s);
+    for (int d = 0; d < 3; ++d) {
+      rec.bbox_min[d] = __ldcg(s + 1 + d);
+      rec.bbox_max[d] = __ldcg(s + 4 + d);
+    }
+    out[c] = rec;
+  }
+}
+
+// Labels and component stats of every ON voxel; the root comes from the
+// union-find forest directly (no separate flatten pass). With `out`, the
+// last block to finish writes the component table (counts[2] counts the
+// finished blocks).
+__global__ void ccl_stats_kernel(CclWs w, int64_t nx, int64_t ny, fvv_component *out,
+                                 int64_t cap) {
   const int64_t n_on = __ldcg(w.counts);
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -290,8 +302,8 @@ __global__ void ccl_stats_kernel(CclWs w, int64_t nx, int64_t ny) {
     int32_t lab = 0;
     unsigned i = 0, j = 0, k = 0;
     if (act) {
-      const int32_t root = w.parent[r];
-      lab = w.rank_label[root];
+      const int32_t root = uf_find(w.parent, (int32_t)r);
+      lab = __ldcg(w.rank_label + root);
       if (root != (int32_t)r) w.rank_label[r] = lab;
       const uint32_t l = (uint32_t)w.on_list[r];
       const uint32_t q = l / (uint32_t)nx;
@@ -314,23 +326,22 @@ __global__ void ccl_stats_kernel(CclWs w, int64_t nx, int64_t ny) {
       atomicMax(s + 6, (int32_t)mx_k);
     }
   }
+  if (out == nullptr) return;
+  __shared__ bool last;
+  __threadfence();  // this block's stats atomics before its completion count
+  __syncthreads();
+  if (threadIdx.x == 0)
+    last = atomicAdd((unsigned long long *)(w.counts + 2), 1ull) == gridDim.x - 1;
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    export_components(w, out, cap, threadIdx.x, blockDim.x);
+  }
 }
 
 __global__ void ccl_export_kernel(CclWs w, fvv_component *out, int64_t cap) {
-  const int64_t ncomp = __ldcg(w.counts + 1);
-  const int64_t n = ncomp < cap ? ncomp : cap;
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n;
-       c += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t *s = w.stats + 8 * c;
-    fvv_component rec;
-    rec.id = c + 1;
-    rec.voxel_count = s[0];
-    for (int d = 0; d < 3; ++d) {
-      rec.bbox_min[d] = s[1 + d];
-      rec.bbox_max[d] = s[4 + d];
-    }
-    out[c] = rec;
-  }
+  export_components(w, out, cap, blockIdx.x * (int64_t)blockDim.x + threadIdx.x,
+                    (int64_t)gridDim.x * blockDim.x);
 }
 
 __global__ void ccl_expand_kernel(CclWs w, int32_t *labels) {
@@ -407,13 +418,10 @@ int fvv_ccl26(const uint32_t *occ_dev, const fvv_grid *grid, void *ws_dev, size_
   WordRank wr{occ_dev, w.word_prefix, w.on_list, w.parent, w.words, nvox};
   onepass_scan(wr, nullptr, w.words, w.words, (void *)w.sums, w.counts + 0, st);
   ccl_union_kernel<<<kCclGrid, 256, 0, st>>>(occ_dev, w, nx, ny, nz);
-  ccl_flatten_kernel<<<kCclGrid, 256, 0, st>>>(w);
-  RootLabel rl{w.parent, w.rank_label};
+  RootLabel rl{w.parent, w.rank_label, w.stats};
   onepass_scan(rl, w.counts + 0, 0, nvox, (void *)w.sums, w.counts + 1, st);
-  ccl_stats_init_kernel<<<kCclGrid, 256, 0, st>>>(w);
-  ccl_stats_kernel<<<kCclGrid, 256, 0, st>>>(w, nx, ny);
-  if (comps_dev) ccl_export_kernel<<<kCclGrid, 256, 0, st>>>(w, comps_dev, comp_cap);
-  note_launches(4 + (comps_dev ? 1 : 0));
+  ccl_stats_kernel<<<kCclGrid, 256, 0, st>>>(w, nx, ny, comps_dev, comp_cap);
+  note_launches(2);
   if (counts_dev) cudaMemcpyAsync(counts_dev, w.counts, 2 * sizeof(int64_t),
                                   cudaMemcpyDeviceToDevice, st);
   return cuda_check("fvv_ccl26");
