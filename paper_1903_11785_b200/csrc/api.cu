@@ -2,6 +2,7 @@
 // fvv_project (camera.py:164-201) and fvv_pack_silhouettes (hull.py:63-75).
 #include <atomic>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 
 #include "fvv_common.cuh"
@@ -12,6 +13,14 @@ static thread_local char g_err[512] = "";
 static std::atomic<long long> g_launches{0};
 
 void note_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("FVV_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 void set_error(const char *fmt, ...) {
   va_list ap;
@@ -32,6 +41,7 @@ int cuda_check(const char *what) {
 __global__ void project_kernel(fvv_camera cam, const double *__restrict__ pts, int64_t n,
                                bool use_dist, bool gemv, double *__restrict__ pix,
                                double *__restrict__ zo, uint8_t *__restrict__ ino) {
+  pdl_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     double u, v, z;
@@ -65,6 +75,7 @@ __device__ __forceinline__ const uint8_t *pack_masks(const PackParams &p) {
 }
 
 __global__ void pack_wide_kernel(const __grid_constant__ PackParams p) {
+  pdl_wait();
   const int64_t total = p.word_start[p.ncam];
   const uint8_t *masks = pack_masks(p);
   for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
@@ -91,6 +102,7 @@ __global__ void pack_wide_kernel(const __grid_constant__ PackParams p) {
 
 // One warp builds one 32-pixel word from 32 coalesced mask bytes (ballot).
 __global__ void pack_kernel(const __grid_constant__ PackParams p) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * blockDim.x / 32;
   const int64_t total = p.word_start[p.ncam];
@@ -137,11 +149,11 @@ int pack_silhouettes_bound(const fvv_camera *cams, int ncam, const uint8_t *mask
   if (wide) {
     int64_t blocks = (words + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    pack_wide_kernel<<<(int)blocks, 256, 0, st>>>(p);
+    launch_k(pack_wide_kernel, (int)blocks, 256, 0, st, p);
   } else {
     int64_t blocks = (words * 32 + 255) / 256;
     if (blocks > 148 * 32) blocks = 148 * 32;
-    pack_kernel<<<(int)blocks, 256, 0, st>>>(p);
+    launch_k(pack_kernel, (int)blocks, 256, 0, st, p);
   }
   note_launches(1);
   return cuda_check("fvv_pack_silhouettes");
@@ -199,7 +211,7 @@ int fvv_project(const fvv_camera *cam, const double *pts_dev, int64_t n, int use
   if (n == 0) return FVV_OK;
   int blocks = (int)((n + 255) / 256);
   if (blocks > 148 * 64) blocks = 148 * 64;
-  project_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(*cam, pts_dev, n, use_distortion != 0,
+  launch_k(project_kernel, blocks, 256, 0, (cudaStream_t)stream, *cam, pts_dev, n, use_distortion != 0,
                                                            single_point != 0, pixel_dev, z_dev,
                                                            in_dev);
   note_launches(1);

@@ -384,6 +384,7 @@ __device__ __forceinline__ int carve_voxels(const CarveParams &p, const CamAffin
 template <bool kSplit>
 __global__ void __launch_bounds__(kCarveThreads, FVV_CARVE_MINB)
     carve_kernel(const __grid_constant__ CarveParams p) {
+  pdl_wait();
   __shared__ CamAffine aff[FVV_MAX_CAMS];
   __shared__ int state[FVV_MAX_CAMS];
   __shared__ int mixed[FVV_MAX_CAMS];
@@ -498,6 +499,7 @@ __global__ void __launch_bounds__(kCarveThreads, FVV_CARVE_MINB)
 template <bool kLoop>
 __global__ void __launch_bounds__(kCarveThreads, FVV_CARVE_MINB)
     carve_voxels_kernel(const __grid_constant__ CarveParams p) {
+  pdl_wait();
   __shared__ CamAffine aff[FVV_MAX_CAMS];
   __shared__ int tmixed[FVV_MAX_CAMS], state[FVV_MAX_CAMS], mixed[FVV_MAX_CAMS];
   __shared__ float2 sbound[FVV_MAX_CAMS], mbound[FVV_MAX_CAMS];
@@ -598,6 +600,7 @@ __device__ __forceinline__ void carve_zero(const CarveParams &p, int bid, int nb
 // cell maps, zeroed occupancy words (block ranges of one grid).
 __global__ void carve_prep_kernel(const __grid_constant__ CarveParams p, CamAffine *aff,
                                   int nb_aff, int nb_cells, int ncount) {
+  pdl_wait();
   const int b = blockIdx.x;
   if (b == 0) {  // the launch's counters (the carve kernels run after this one)
     if (threadIdx.x < 32) p.tile_stats[threadIdx.x] = 0ull;
@@ -617,6 +620,7 @@ __global__ void carve_prep_kernel(const __grid_constant__ CarveParams p, CamAffi
 // float64 chain, then set their bits.
 __global__ void __launch_bounds__(kCarveThreads)
     carve_exact_kernel(const __grid_constant__ CarveParams p) {
+  pdl_wait();
   // lanes test different cameras: a shared-memory copy (divergent indexing of
   // the parameter block would serialise the constant cache)
   __shared__ fvv_camera cams[FVV_MAX_CAMS];
@@ -673,6 +677,7 @@ extern "C" size_t fvv_carve_workspace_bytes(const fvv_camera *cams, int ncam) {
 namespace fvv {
 static_assert(sizeof(CarveGrids) % 16 == 0, "CarveGrids is copied in 16-byte words");
 __global__ void store_carve_grids_kernel(const __grid_constant__ CarveGrids src, CarveGrids *dst) {
+  pdl_wait();
   const int4 *a = reinterpret_cast<const int4 *>(&src);
   int4 *b = reinterpret_cast<int4 *>(dst);
   for (int i = threadIdx.x; i < (int)(sizeof(CarveGrids) / 16); i += blockDim.x) b[i] = a[i];
@@ -748,23 +753,23 @@ int fvv::carve_batch(const fvv_camera *cams, int ncam, const uint32_t *sil_dev,
   // (the cell maps depend on the silhouettes only: a batch over the same
   // planes as the previous carve into this workspace reuses them)
   const int nb_cells = reuse_cells ? 0 : (int)((cell_words_total(cams, ncam) + 255) / 256);
-  carve_prep_kernel<<<nb_aff + nb_cells + 148 * 2, 256, 0, st>>>(p, (CamAffine *)workspace, nb_aff,
+  launch_k(carve_prep_kernel, nb_aff + nb_cells + 148 * 2, 256, 0, st, p, (CamAffine *)workspace, nb_aff,
                                                                 nb_cells, ngrid_max);
   // large (stage) grids: classify the 16^3 tiles, then carve the surviving
   // tiles' voxels with kParts blocks each; ROI grids: one kernel per 8^3 tile
   const bool split = p.tile_log2 == 4 && blocks <= kTileCap;
   if (split) {
-    carve_kernel<true><<<(unsigned)blocks, kCarveThreads, 0, st>>>(p);
+    launch_k(carve_kernel<true>, (unsigned)blocks, kCarveThreads, 0, st, p);
     // one block per octant of every tile (C3 ROI batch: ~70k octants); more
     // octants (C5 512^3: 131k, mostly of culled tiles): a capped grid loops
     if (blocks * 8 <= kVoxelGrid)
-      carve_voxels_kernel<false><<<(unsigned)(blocks * 8), kCarveThreads, 0, st>>>(p);
+      launch_k(carve_voxels_kernel<false>, (unsigned)(blocks * 8), kCarveThreads, 0, st, p);
     else
-      carve_voxels_kernel<true><<<(unsigned)kVoxelCap, kCarveThreads, 0, st>>>(p);
+      launch_k(carve_voxels_kernel<true>, (unsigned)kVoxelCap, kCarveThreads, 0, st, p);
   } else {
-    carve_kernel<false><<<(unsigned)blocks, kCarveThreads, 0, st>>>(p);
+    launch_k(carve_kernel<false>, (unsigned)blocks, kCarveThreads, 0, st, p);
   }
-  carve_exact_kernel<<<148 * 4, kCarveThreads, 0, st>>>(p);
+  launch_k(carve_exact_kernel, 148 * 4, kCarveThreads, 0, st, p);
   note_launches(split ? 4 : 3);
   return cuda_check("fvv_carve");
 }
@@ -815,7 +820,7 @@ extern "C" int fvv_carve(const fvv_camera *cams, int ncam, const uint32_t *sil_d
   CarveGrids *dst = nullptr;
   if (ngrid > 0) {
     dst = (CarveGrids *)((char *)workspace + carve_grids_offset(cams, ncam));
-    store_carve_grids_kernel<<<1, 256, 0, st>>>(T, dst);
+    launch_k(store_carve_grids_kernel, 1, 256, 0, st, T, dst);
     note_launches(1);
   }
   return carve_batch(cams, ncam, sil_dev, sil_word_off, dst, ngrid, T.tile_log2, T.total_tiles,

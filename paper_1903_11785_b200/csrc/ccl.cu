@@ -212,6 +212,7 @@ __device__ __forceinline__ int64_t next_on(const uint32_t *occ, int64_t p, int64
 
 __global__ void ccl_union_kernel(const uint32_t *__restrict__ occ, CclWs w, int64_t nx, int64_t ny,
                                  int64_t nz) {
+  pdl_wait();
   // four threads per ON voxel: the run's first voxel unites with the runs of
   // one neighbour row each; the others link to their run's first voxel.
   // 32-bit index arithmetic (nvox < 2^31, fvv_ccl26)
@@ -292,6 +293,7 @@ __device__ __forceinline__ void export_components(const CclWs &w, fvv_component 
 // finished blocks).
 __global__ void ccl_stats_kernel(CclWs w, int64_t nx, int64_t ny, fvv_component *out,
                                  int64_t cap) {
+  pdl_wait();
   const int64_t n_on = __ldcg(w.counts);
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -340,11 +342,13 @@ __global__ void ccl_stats_kernel(CclWs w, int64_t nx, int64_t ny, fvv_component 
 }
 
 __global__ void ccl_export_kernel(CclWs w, fvv_component *out, int64_t cap) {
+  pdl_wait();
   export_components(w, out, cap, blockIdx.x * (int64_t)blockDim.x + threadIdx.x,
                     (int64_t)gridDim.x * blockDim.x);
 }
 
 __global__ void ccl_expand_kernel(CclWs w, int32_t *labels) {
+  pdl_wait();
   const int64_t n_on = __ldcg(w.counts);
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_on;
        r += (int64_t)gridDim.x * blockDim.x)
@@ -354,6 +358,7 @@ __global__ void ccl_expand_kernel(CclWs w, int32_t *labels) {
 // hull.py:257-269: keep[label] selects survivors; ids are not renumbered.
 __global__ void ccl_filter_kernel(CclWs w, const uint8_t *__restrict__ keep, int32_t *labels,
                                   uint32_t *occ_out, int64_t *kept) {
+  pdl_wait();
   const int64_t n_on = __ldcg(w.counts);
   int64_t mine = 0;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_on;
@@ -372,6 +377,7 @@ __global__ void ccl_filter_kernel(CclWs w, const uint8_t *__restrict__ keep, int
 __global__ void dense_filter_kernel(const int32_t *__restrict__ in, int64_t nvox, int64_t nkeep,
                                     const uint8_t *__restrict__ keep, int32_t *out,
                                     uint32_t *occ_out, int64_t *kept) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   int64_t mine = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -417,10 +423,10 @@ int fvv_ccl26(const uint32_t *occ_dev, const fvv_grid *grid, void *ws_dev, size_
   cudaMemsetAsync(w.counts, 0, 4 * sizeof(int64_t), st);
   WordRank wr{occ_dev, w.word_prefix, w.on_list, w.parent, w.words, nvox};
   onepass_scan(wr, nullptr, w.words, w.words, (void *)w.sums, w.counts + 0, st);
-  ccl_union_kernel<<<kCclGrid, 256, 0, st>>>(occ_dev, w, nx, ny, nz);
+  launch_k(ccl_union_kernel, kCclGrid, 256, 0, st, occ_dev, w, nx, ny, nz);
   RootLabel rl{w.parent, w.rank_label, w.stats};
   onepass_scan(rl, w.counts + 0, 0, nvox, (void *)w.sums, w.counts + 1, st);
-  ccl_stats_kernel<<<kCclGrid, 256, 0, st>>>(w, nx, ny, comps_dev, comp_cap);
+  launch_k(ccl_stats_kernel, kCclGrid, 256, 0, st, w, nx, ny, comps_dev, comp_cap);
   note_launches(2);
   if (counts_dev) cudaMemcpyAsync(counts_dev, w.counts, 2 * sizeof(int64_t),
                                   cudaMemcpyDeviceToDevice, st);
@@ -431,7 +437,7 @@ int fvv_ccl_components(const fvv_grid *grid, const void *ws_dev, fvv_component *
                        int64_t comp_cap, void *stream) {
   const int64_t nvox = grid->dims[0] * grid->dims[1] * grid->dims[2];
   CclWs w = ccl_layout((void *)ws_dev, grid->dims);
-  ccl_export_kernel<<<kCclGrid, 256, 0, (cudaStream_t)stream>>>(w, comps_dev, comp_cap);
+  launch_k(ccl_export_kernel, kCclGrid, 256, 0, (cudaStream_t)stream, w, comps_dev, comp_cap);
   note_launches(1);
   return cuda_check("fvv_ccl_components");
 }
@@ -441,7 +447,7 @@ int fvv_ccl_labels(const fvv_grid *grid, const void *ws_dev, int32_t *labels_dev
   CclWs w = ccl_layout((void *)ws_dev, grid->dims);
   cudaStream_t st = (cudaStream_t)stream;
   cudaMemsetAsync(labels_dev, 0, sizeof(int32_t) * nvox, st);
-  ccl_expand_kernel<<<kCclGrid, 256, 0, st>>>(w, labels_dev);
+  launch_k(ccl_expand_kernel, kCclGrid, 256, 0, st, w, labels_dev);
   note_launches(1);
   return cuda_check("fvv_ccl_labels");
 }
@@ -454,7 +460,7 @@ int fvv_filter_labels(const fvv_grid *grid, const void *ws_dev, const uint8_t *k
   if (labels_dev) cudaMemsetAsync(labels_dev, 0, sizeof(int32_t) * nvox, st);
   if (occ_dev) cudaMemsetAsync(occ_dev, 0, sizeof(uint32_t) * ((nvox + 31) / 32), st);
   if (kept_dev) cudaMemsetAsync(kept_dev, 0, sizeof(int64_t), st);
-  ccl_filter_kernel<<<kCclGrid, 256, 0, st>>>(w, keep_dev, labels_dev, occ_dev, kept_dev);
+  launch_k(ccl_filter_kernel, kCclGrid, 256, 0, st, w, keep_dev, labels_dev, occ_dev, kept_dev);
   note_launches(1);
   return cuda_check("fvv_filter_labels");
 }
@@ -464,7 +470,7 @@ int fvv_filter_dense(const int32_t *labels_in_dev, int64_t nvox, const uint8_t *
                      void *stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (kept_dev) cudaMemsetAsync(kept_dev, 0, sizeof(int64_t), st);
-  dense_filter_kernel<<<kCclGrid, 256, 0, st>>>(labels_in_dev, nvox, nkeep, keep_dev, labels_dev,
+  launch_k(dense_filter_kernel, kCclGrid, 256, 0, st, labels_in_dev, nvox, nkeep, keep_dev, labels_dev,
                                                 occ_dev, kept_dev);
   note_launches(1);
   return cuda_check("fvv_filter_dense");

@@ -108,10 +108,12 @@ struct DevBuf {
 };
 
 __global__ void add_count_kernel(int64_t *dst, const int64_t *src, int64_t add) {
+  pdl_wait();
   if (threadIdx.x == 0 && blockIdx.x == 0) *dst = *src + add;
 }
 
 __global__ void offset_tris_kernel(int32_t *tris, int64_t n3, int32_t add) {
+  pdl_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n3;
        i += (int64_t)gridDim.x * blockDim.x)
     tris[i] += add;
@@ -134,6 +136,7 @@ struct ReadBatch {
 };
 
 __global__ void readback_kernel(ReadBatch B) {
+  pdl_wait();
   const int y = blockIdx.y;
   const int64_t *src = B.p[y].src;
   int64_t *dst = B.p[y].dst;
@@ -149,6 +152,7 @@ __global__ void readback_kernel(ReadBatch B) {
 }
 
 __global__ void bind_inputs_kernel(const __grid_constant__ FrameInputs v, FrameInputs *dst) {
+  pdl_wait();
   const int4 *a = reinterpret_cast<const int4 *>(&v);
   int4 *b = reinterpret_cast<int4 *>(dst);
   for (int i = threadIdx.x; i < (int)(sizeof(FrameInputs) / 16); i += blockDim.x) b[i] = a[i];
@@ -186,6 +190,7 @@ constexpr int kPlanThreads = 1024;
 __global__ void __launch_bounds__(kPlanThreads)
     frame_plan_kernel(const __grid_constant__ PlanArgs a, const fvv_component *__restrict__ comps,
                       const int64_t *__restrict__ ccl_counts, FramePlan *plan) {
+  pdl_wait();
   __shared__ int s_warp[kPlanThreads / 32];
   __shared__ int s_nroi, s_status;
   __shared__ int64_t s_words[FVV_MAX_GRIDS], s_tiles[FVV_MAX_GRIDS], s_tw[FVV_MAX_GRIDS];
@@ -467,7 +472,7 @@ static void readback(fvv_frame *f, cudaStream_t st, std::initializer_list<HostPi
   }
   int64_t bx = (most + 255) / 256;
   bx = bx < 1 ? 1 : (bx > 32 ? 32 : bx);
-  readback_kernel<<<dim3((unsigned)bx, (unsigned)n), 256, 0, st>>>(b);
+  launch_k(readback_kernel, dim3((unsigned)bx, (unsigned)n), 256, 0, st, b);
   note_launches(1);
 }
 
@@ -823,7 +828,7 @@ static int run_host_planned(fvv_frame *f, const uint8_t *masks_dev, const fvv_ca
       memcpy(f->info.data() + 8 * (size_t)r0, (char *)f->host_small + kHsInfo, 64 * (size_t)nb);
       const int64_t tb = hs[2];
       if (v_before)
-        offset_tris_kernel<<<148 * 4, 256, 0, st>>>(f->tris.as<int32_t>() + 3 * t_before, 3 * tb,
+        launch_k(offset_tris_kernel, 148 * 4, 256, 0, st, f->tris.as<int32_t>() + 3 * t_before, 3 * tb,
                                                     (int32_t)v_before);
       for (int r = r0; r < r0 + nb; ++r) {
         f->info[8 * r + 0] += v_before;
@@ -837,7 +842,7 @@ static int run_host_planned(fvv_frame *f, const uint8_t *masks_dev, const fvv_ca
       if (v_before) {
         readback(f, st, {{f->mesh_totals.p, 0, 24, nullptr, 0, 0}});
         cudaStreamSynchronize(st);
-        offset_tris_kernel<<<148 * 4, 256, 0, st>>>(f->tris.as<int32_t>() + 3 * t_before,
+        launch_k(offset_tris_kernel, 148 * 4, 256, 0, st, f->tris.as<int32_t>() + 3 * t_before,
                                                     3 * hs[2], (int32_t)v_before);
       }
       f->nv = v_before + nv;
@@ -849,7 +854,7 @@ static int run_host_planned(fvv_frame *f, const uint8_t *masks_dev, const fvv_ca
   // device-side total triangle count for D-1 / D-2 / E (no host round trip)
   int64_t *ntri_dev = f->ntri.as<int64_t>();
   if (nroi > 0)
-    add_count_kernel<<<1, 32, 0, st>>>(ntri_dev, f->mesh_totals.as<int64_t>() + 2, t_before);
+    launch_k(add_count_kernel, 1, 32, 0, st, ntri_dev, f->mesh_totals.as<int64_t>() + 2, t_before);
   else
     cudaMemsetAsync(ntri_dev, 0, 8, st);
   const int64_t nt_ub = f->nt;
@@ -945,7 +950,7 @@ static int enqueue_device_planned(fvv_frame *f, const uint8_t *masks_dev, const 
   pa.cap_words = K.words;
   pa.cap_tiles = K.tiles;
   pa.cap_tw = K.tw;
-  frame_plan_kernel<<<1, kPlanThreads, 0, st>>>(pa, f->comps.as<fvv_component>(),
+  launch_k(frame_plan_kernel, 1, kPlanThreads, 0, st, pa, f->comps.as<fvv_component>(),
                                                 f->ccl_counts.as<int64_t>(), P);
   note_launches(1);
   stage_mark(f, 2, st);
@@ -1168,7 +1173,7 @@ static int run_device_planned(fvv_frame *f, const uint8_t *masks_dev, const fvv_
     in.frames = frames_dev;
     if (virt && frame_off)
       for (int c = 0; c < f->ncam; ++c) in.frame_off[c] = frame_off[c];
-    bind_inputs_kernel<<<1, 32, 0, st>>>(in, f->inputs.as<FrameInputs>());
+    launch_k(bind_inputs_kernel, 1, 32, 0, st, in, f->inputs.as<FrameInputs>());
     note_launches(1);
   }
   if (graphs && f->graph && key == f->graph_key) {

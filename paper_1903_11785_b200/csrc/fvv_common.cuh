@@ -20,6 +20,31 @@ int cuda_check(const char *what);
 // kernels launched by this library (bench.py reports the timed-region delta)
 void note_launches(long long n);
 
+// Programmatic dependent launch: every kernel is launched with the
+// programmatic-serialisation attribute and waits for its predecessor's
+// completion (griddepcontrol.wait, a no-op without one) before it touches
+// memory, so a launch's setup and block scheduling overlap the previous
+// kernel's tail - inside a captured frame graph too. FVV_PDL=0 turns it off.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                     Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<Args &&>(args)...);
+}
+
 // camera.py:177 `pts @ R.T + t`: OpenBLAS gemm (>= 2 rows) accumulates
 // fma(z,R2, fma(y,R1, x*R0)); the 1-row gemv kernel fma(z,R2, fma(x,R0, y*R1)).
 // (the two orders differ only in which product is fused: the first factor

@@ -92,6 +92,7 @@ __device__ __forceinline__ uint32_t row_next(const uint32_t *tw, const MeshGridI
 // ballot b collects bit b (= i0 + b) over the lanes (= k), i.e. the k-row
 // word of column i0 + b. Two loads per 32 output words instead of 32 per word.
 __global__ void mesh_transpose_kernel(const MeshGrids *__restrict__ Gp, MeshBufs B) {
+  pdl_wait();
   const MeshGrids &G = *Gp;
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -218,6 +219,7 @@ struct CellFlags {
 
 // per-grid vertex / surface-cell bases and counts (prefix at grid starts)
 __global__ void mesh_grid_counts_kernel(const MeshGrids *__restrict__ Gp, MeshBufs B) {
+  pdl_wait();
   const MeshGrids &G = *Gp;
   for (int g = threadIdx.x; g < G.ngrid; g += blockDim.x) {
     const int64_t s0 = G.tw_start[g], s1 = G.tw_start[g + 1];
@@ -239,6 +241,7 @@ __global__ void mesh_grid_counts_kernel(const MeshGrids *__restrict__ Gp, MeshBu
 
 // ---- B0: vertex list ----------------------------------------------------------
 __global__ void mesh_vertex_list_kernel(const MeshGrids *__restrict__ Gp, MeshBufs B) {
+  pdl_wait();
   const MeshGrids &G = *Gp;
   if (!emit_fits(B)) return;
   const int64_t n = 3 * G.tw_total;
@@ -381,6 +384,7 @@ __global__ void __launch_bounds__(128)
     edge_isovalues_kernel(const __grid_constant__ MeshCams C, const uint32_t *__restrict__ sil,
                           const double *__restrict__ pon, const double *__restrict__ poff, int64_t n,
                           double *lam_out, int32_t *cam_out, int64_t *stats) {
+  pdl_wait();
   const bool gemv = (n == 1);
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -398,6 +402,7 @@ __global__ void __launch_bounds__(128)
     mesh_lambda_kernel(const MeshGrids *__restrict__ Gp, const __grid_constant__ MeshCams C,
                        MeshBufs B, const uint32_t *__restrict__ sil, int exact,
                        double fixed_iso) {
+  pdl_wait();
   const MeshGrids &G = *Gp;
   if (!emit_fits(B)) return;
   const int64_t nv = __ldcg(B.totals);
@@ -512,6 +517,7 @@ __device__ __forceinline__ void mesh_cell(const MeshGrids &G, const MeshBufs &B,
 // word by a shuffle binary search, then the n-th set bit), so sparse words
 // do not leave lanes idle.
 __global__ void mesh_cells_kernel(const MeshGrids *__restrict__ Gp, MeshBufs B) {
+  pdl_wait();
   const MeshGrids &G = *Gp;
   if (!emit_fits(B)) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) B.totals[3] = __ldcg(B.totals + 1);  // tri-scan length
@@ -589,6 +595,7 @@ struct TriScan {
 // ---- B4: per-grid slot bases (one warp, a lane per grid) ---------------------
 __global__ void mesh_slot_bases_kernel(const MeshGrids *__restrict__ Gp, MeshBufs B,
                                        const Slot5 *total) {
+  pdl_wait();
   const MeshGrids &G = *Gp;
   if (!emit_fits(B)) return;
   if (blockIdx.x != 0) return;
@@ -631,6 +638,7 @@ __global__ void mesh_slot_bases_kernel(const MeshGrids *__restrict__ Gp, MeshBuf
 
 // ---- B5: triangle emission ----------------------------------------------------
 __global__ void mesh_emit_kernel(const MeshGrids *__restrict__ Gp, MeshBufs B) {
+  pdl_wait();
   if (!emit_fits(B)) return;
   const int64_t S = __ldcg(B.totals + 1);
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < S;
@@ -701,6 +709,7 @@ static MeshBufs bufs_from(void *ws, const PrepLayout &L) {
 
 static_assert(sizeof(MeshGrids) % 16 == 0, "MeshGrids is copied in 16-byte words");
 __global__ void store_mesh_grids_kernel(const __grid_constant__ MeshGrids src, MeshGrids *dst) {
+  pdl_wait();
   const int4 *a = reinterpret_cast<const int4 *>(&src);
   int4 *b = reinterpret_cast<int4 *>(dst);
   for (int i = threadIdx.x; i < (int)(sizeof(MeshGrids) / 16); i += blockDim.x) b[i] = a[i];
@@ -787,7 +796,7 @@ int fvv::mesh_prepare_batch(const MeshGrids *G_dev, int64_t tw_cap, int ngrid_ma
   B.occ = occ_dev;
   cudaMemsetAsync(B.totals, 0, 32, st);
   if (tw_cap > 0) {
-    mesh_transpose_kernel<<<kMeshGrid, 256, 0, st>>>(G_dev, B);
+    launch_k(mesh_transpose_kernel, kMeshGrid, 256, 0, st, G_dev, B);
     note_launches(1);
     // the vertex and surface-cell scans read the same k-rows only: with a
     // side stream they run side by side (own scan status words each)
@@ -803,7 +812,7 @@ int fvv::mesh_prepare_batch(const MeshGrids *G_dev, int64_t tw_cap, int ngrid_ma
     onepass_scan(ef, &G_dev->tw3, 0, 3 * tw_cap, (void *)B.sums, B.totals + 0, st);
     if (side) cudaStreamWaitEvent(st, join, 0);
   }
-  mesh_grid_counts_kernel<<<1, 128, 0, st>>>(G_dev, B);
+  launch_k(mesh_grid_counts_kernel, 1, 128, 0, st, G_dev, B);
   note_launches(1);
   return cuda_check("fvv_mesh_prepare");
 }
@@ -855,18 +864,18 @@ int fvv::mesh_emit_batch(const fvv_camera *cams_by_id, int ncam, const uint32_t 
   }
   Slot5 *d_total = (Slot5 *)((char *)ws_dev + L.slot5 + sizeof(int64_t) * 5 * ngrid_max);
   if (cap_v > 0) {
-    mesh_vertex_list_kernel<<<kMeshGrid, 256, 0, st>>>(G_dev, B);
+    launch_k(mesh_vertex_list_kernel, kMeshGrid, 256, 0, st, G_dev, B);
     // one vertex per thread, cameras in a loop; measured against (vertex,
     // camera) lane groups and a certified-FP32 endpoint projection with the
     // float64 terms deferred to full warps, both slower
     const int64_t lam_blocks = std::min<int64_t>(cap_v / 128 + 1, 148 * 64);
-    mesh_lambda_kernel<<<(unsigned)lam_blocks, 128, 0, st>>>(G_dev, h_cams, B, sil_dev, exact,
+    launch_k(mesh_lambda_kernel, (unsigned)lam_blocks, 128, 0, st, G_dev, h_cams, B, sil_dev, exact,
                                                               fixed_iso);
     note_launches(2);
   }
   if (cap_s > 0) {
     const int64_t cell_blocks = std::min<int64_t>(tw_cap / 256 + 1, 148 * 64);
-    mesh_cells_kernel<<<(unsigned)std::max<int64_t>(cell_blocks, kMeshGrid), 256, 0, st>>>(G_dev,
+    launch_k(mesh_cells_kernel, (unsigned)std::max<int64_t>(cell_blocks, kMeshGrid), 256, 0, st, G_dev,
                                                                                           B);
     note_launches(1);
     TriScan ts{B.cell_mask, B.cprefix};
@@ -874,8 +883,8 @@ int fvv::mesh_emit_batch(const fvv_camera *cams_by_id, int ncam, const uint32_t 
   } else {
     cudaMemsetAsync(d_total, 0, sizeof(Slot5), st);
   }
-  mesh_slot_bases_kernel<<<1, 32, 0, st>>>(G_dev, B, d_total);
-  if (cap_s > 0) mesh_emit_kernel<<<kMeshGrid, 256, 0, st>>>(G_dev, B);
+  launch_k(mesh_slot_bases_kernel, 1, 32, 0, st, G_dev, B, d_total);
+  if (cap_s > 0) launch_k(mesh_emit_kernel, kMeshGrid, 256, 0, st, G_dev, B);
   note_launches(1 + (cap_s > 0 ? 1 : 0));
   return cuda_check("fvv_mesh_emit");
 }
@@ -898,7 +907,7 @@ int fvv_mesh_prepare(const fvv_grid *grids, int ngrid, const uint32_t *occ_dev,
   }
   cudaStream_t st = (cudaStream_t)stream;
   MeshGrids *G_dev = (MeshGrids *)((char *)ws_dev + L.grids);
-  store_mesh_grids_kernel<<<1, 256, 0, st>>>(G, G_dev);
+  launch_k(store_mesh_grids_kernel, 1, 256, 0, st, G, G_dev);
   note_launches(1);
   return mesh_prepare_batch(G_dev, G.tw_total, ngrid, occ_dev, ws_dev, ws_bytes, st, nullptr,
                             nullptr, nullptr);
@@ -966,7 +975,7 @@ int fvv_edge_isovalues(const fvv_camera *cams_by_id, int ncam, const uint32_t *s
   }
   int64_t blocks = (n + 127) / 128;
   if (blocks > kMeshGrid) blocks = kMeshGrid;
-  edge_isovalues_kernel<<<(int)blocks, 128, 0, st>>>(h_cams, sil_dev, p_on_dev, p_off_dev, n,
+  launch_k(edge_isovalues_kernel, (int)blocks, 128, 0, st, h_cams, sil_dev, p_on_dev, p_off_dev, n,
                                                       lam_dev, cam_dev, stats_dev);
   note_launches(1);
   return cuda_check("fvv_edge_isovalues");

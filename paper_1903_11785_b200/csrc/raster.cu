@@ -73,6 +73,7 @@ __global__ void raster_vertex_kernel(const __grid_constant__ RasterCams C,
                                      const double *__restrict__ V, int64_t nv,
                                      const int64_t *nv_dev, double4 *__restrict__ proj,
                                      float2 *__restrict__ q) {
+  pdl_wait();
   project_vertices(C, V, nv, device_count(nv_dev, nv), blockIdx.x * (int64_t)blockDim.x + threadIdx.x,
                    (int64_t)gridDim.x * blockDim.x, proj, q);
 }
@@ -322,6 +323,7 @@ __device__ __forceinline__ float2 ldq(const float2 *__restrict__ q) { return __l
 
 __global__ void __launch_bounds__(256)
     raster_filter_kernel(const __grid_constant__ RasterCams C, RasterArgs A) {
+  pdl_wait();
   const int64_t nt = device_count(A.nt_dev, A.nt);
   const int lane = threadIdx.x & 31;
   const int64_t wid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -474,6 +476,7 @@ __global__ void __launch_bounds__(256)
 template <bool kRec>
 __global__ void __launch_bounds__(256)
     raster_pair_kernel(const __grid_constant__ RasterCams C, RasterArgs A) {
+  pdl_wait();
   if (pass1_covered(A)) return;
   const int64_t nt = device_count(A.nt_dev, A.nt);
   const int lane = threadIdx.x & 31;
@@ -536,6 +539,7 @@ __global__ void __launch_bounds__(256)
 // bounding boxes and culled triangles do not leave lanes idle.
 __global__ void __launch_bounds__(kRasterThreads, 8)
     raster_small_kernel(const __grid_constant__ RasterCams C, RasterArgs A) {
+  pdl_wait();
   __shared__ TriSmem sm[kRasterThreads];
   if (pass1_covered(A)) return;
   const bool rec = A.hits != nullptr && A.pass == 0;
@@ -655,6 +659,7 @@ __global__ void __launch_bounds__(kRasterThreads, 8)
 
 __global__ void __launch_bounds__(kBigThreads)
     raster_big_kernel(const __grid_constant__ RasterCams C, RasterArgs A) {
+  pdl_wait();
   if (pass1_covered(A)) return;
   const bool rec = A.hits != nullptr && A.pass == 0;
   const int64_t nt = device_count(A.nt_dev, A.nt);
@@ -694,6 +699,7 @@ __global__ void __launch_bounds__(kBigThreads)
 // that reached the pixel's final depth (visibility.py:80-91 keeps the first
 // triangle, in id order, with the minimum depth).
 __global__ void raster_hits_kernel(RasterArgs A) {
+  pdl_wait();
   const unsigned long long n = __ldcg(A.hit_count);
   if ((int64_t)n > A.hit_cap) return;  // overflow: the pass-1 raster does it
   const unsigned long long *depth = (const unsigned long long *)A.depth;
@@ -757,6 +763,7 @@ __global__ void raster_prep_kernel(const __grid_constant__ RasterCams C,
                                    const int64_t *nv_dev, double4 *__restrict__ proj,
                                    float2 *__restrict__ q, unsigned long long *depth, int32_t *ids,
                                    uint8_t *dirty, int64_t npx, int nb_fill) {
+  pdl_wait();
   if ((int)blockIdx.x < nb_fill) {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)nb_fill * blockDim.x;
@@ -773,6 +780,7 @@ __global__ void raster_prep_kernel(const __grid_constant__ RasterCams C,
 }
 
 __global__ void fill_u64_kernel(unsigned long long *p, int64_t n, unsigned long long v) {
+  pdl_wait();
   // 16-byte stores for the aligned bulk, scalar head/tail
   fill_u64(p, n, v, blockIdx.x * (int64_t)blockDim.x + threadIdx.x,
            (int64_t)gridDim.x * blockDim.x);
@@ -797,6 +805,7 @@ struct ClassifyArgs {
 
 __global__ void classify_kernel(const __grid_constant__ RasterCams C,
                                 const __grid_constant__ ClassifyArgs A) {
+  pdl_wait();
   // one thread per triangle, 32 consecutive triangles (one visibility word)
   // per warp: the centroid (three divisions) is computed once and projected
   // into every camera, instead of once per (camera, triangle); the pixel
@@ -857,6 +866,7 @@ struct SourceArgs {
 };
 
 __global__ void sources_kernel(const __grid_constant__ SourceArgs A) {
+  pdl_wait();
   const int64_t nt = device_count(A.nt_dev, A.nt);
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nt;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -919,6 +929,7 @@ __device__ __forceinline__ int cam_pos(const RenderArgs &A, int32_t id) {
 // covered pixels and pixels per source camera (numpy's one-row gemv rule
 // applies when a count is 1); warp-aggregated atomics.
 __global__ void render_count_kernel(const __grid_constant__ RenderArgs A) {
+  pdl_wait();
   const int64_t np = (int64_t)A.virt.width * A.virt.height;
   const int lane = threadIdx.x & 31;
   for (int64_t p0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; p0 < np;
@@ -940,6 +951,7 @@ __global__ void render_count_kernel(const __grid_constant__ RenderArgs A) {
 
 // render.py:46-61 sample_bilinear, render.py:104-113 rint/clip.
 __global__ void render_color_kernel(const __grid_constant__ RenderArgs A) {
+  pdl_wait();
   const int W = A.virt.width;
   const int64_t np = (int64_t)W * A.virt.height;
   const bool bp_gemv = A.counts[0] == 1;
@@ -995,6 +1007,7 @@ __global__ void render_color_kernel(const __grid_constant__ RenderArgs A) {
 
 __global__ void back_project_kernel(fvv_camera cam, const double *__restrict__ px,
                                     const double *__restrict__ d, int64_t n, double *out) {
+  pdl_wait();
   const bool gemv = n == 1;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -1128,7 +1141,7 @@ static int rasterize_impl(const fvv_camera *cams, int ncam, const double *verts_
   for (int c = 0; c < (contiguous ? 1 : ncam); ++c) {
     const int64_t n = contiguous ? total_px : (int64_t)cams[c].width * cams[c].height;
     if (!fused_fill) {
-      fill_u64_kernel<<<148 * 8, 256, 0, st>>>((unsigned long long *)(depth_dev + plane_off[c]),
+      launch_k(fill_u64_kernel, 148 * 8, 256, 0, st, (unsigned long long *)(depth_dev + plane_off[c]),
                                                n, 0x7ff0000000000000ull);
       note_launches(1);
     }
@@ -1150,8 +1163,7 @@ static int rasterize_impl(const fvv_camera *cams, int ncam, const double *verts_
     // block); a tracked reset reads one flag per 32 pixels
     int64_t nb_fill = tracked ? total_px / (256 * 32 * 8) + 1 : total_px / (256 * 64) + 1;
     if (nb_fill > 148 * 8) nb_fill = 148 * 8;
-    raster_prep_kernel<<<(int)(blocks + nb_fill), 256, 0, st>>>(
-        C, verts_dev, work ? nv : 0, nv_dev, proj, q,
+    launch_k(raster_prep_kernel, (int)(blocks + nb_fill), 256, 0, st, C, verts_dev, work ? nv : 0, nv_dev, proj, q,
         (unsigned long long *)(depth_dev + plane_off[0]),
         tracked ? tri_id_dev + plane_off[0] : nullptr, tracked ? dirty : nullptr, total_px,
         (int)nb_fill);
@@ -1159,7 +1171,7 @@ static int rasterize_impl(const fvv_camera *cams, int ncam, const double *verts_
   } else if (work) {
     int64_t blocks = (nv * ncam + 255) / 256;
     if (blocks > kRasterGrid) blocks = kRasterGrid;
-    raster_vertex_kernel<<<(int)blocks, 256, 0, st>>>(C, verts_dev, nv, nv_dev,
+    launch_k(raster_vertex_kernel, (int)blocks, 256, 0, st, C, verts_dev, nv, nv_dev,
                                                      (double4 *)(ws + L.proj), (float2 *)(ws + L.q));
     note_launches(1);
   }
@@ -1192,7 +1204,7 @@ static int rasterize_impl(const fvv_camera *cams, int ncam, const double *verts_
   A.hit_count = (unsigned long long *)(ws + 16);
   A.hit_cap = L.hit_cap;
   cudaMemsetAsync(ws, 0, 32, st);  // big-queue counter, overflow flag, hit count
-  raster_filter_kernel<<<(unsigned)fs.bx, 256, 0, st>>>(C, A);
+  launch_k(raster_filter_kernel, (unsigned)fs.bx, 256, 0, st, C, A);
   note_launches(1);
   // pass 0: depth (RED.MIN of the depth bits); ids wanted: the lowest
   // triangle id reaching the final depth, from the hit list pass 0 recorded
@@ -1201,15 +1213,15 @@ static int rasterize_impl(const fvv_camera *cams, int ncam, const double *verts_
   for (int pass = 0; pass < (tri_id_dev ? 2 : 1); ++pass) {
     A.pass = pass;
     if (pass == 1 && hits) {
-      raster_hits_kernel<<<148 * 8, 256, 0, st>>>(A);
+      launch_k(raster_hits_kernel, 148 * 8, 256, 0, st, A);
       note_launches(1);
     }
     if (hits && pass == 0)
-      raster_pair_kernel<true><<<148 * 16, 256, 0, st>>>(C, A);
+      launch_k(raster_pair_kernel<true>, 148 * 16, 256, 0, st, C, A);
     else
-      raster_pair_kernel<false><<<148 * 16, 256, 0, st>>>(C, A);
-    raster_small_kernel<<<148 * 16, kRasterThreads, 0, st>>>(C, A);
-    raster_big_kernel<<<148 * 4, kBigThreads, 0, st>>>(C, A);
+      launch_k(raster_pair_kernel<false>, 148 * 16, 256, 0, st, C, A);
+    launch_k(raster_small_kernel, 148 * 16, kRasterThreads, 0, st, C, A);
+    launch_k(raster_big_kernel, 148 * 4, kBigThreads, 0, st, C, A);
     note_launches(3);
   }
   return cuda_check("fvv_rasterize");
@@ -1267,7 +1279,7 @@ int fvv_triangle_sources(const int32_t *rank_pos, const int32_t *rank_id, int nr
   A.nt = nt;
   A.nt_dev = nt_dev;
   A.src = src_dev;
-  sources_kernel<<<kRasterGrid, 256, 0, (cudaStream_t)stream>>>(A);
+  launch_k(sources_kernel, kRasterGrid, 256, 0, (cudaStream_t)stream, A);
   note_launches(1);
   return cuda_check("fvv_triangle_sources");
 }
@@ -1332,7 +1344,7 @@ int fvv::classify_sources(const fvv_camera *cams, int ncam, const double *verts_
     A.rank_pos[r] = rank_pos[r];
     A.rank_id[r] = rank_id[r];
   }
-  classify_kernel<<<kRasterGrid, 256, 0, st>>>(C, A);
+  launch_k(classify_kernel, kRasterGrid, 256, 0, st, C, A);
   note_launches(1);
   return cuda_check("fvv_classify");
 }
@@ -1351,7 +1363,7 @@ int fvv::render_view_coded_bound(const fvv_camera *rig, int ncam, const uint8_t 
   if (rc) return rc;
   A.code = code_dev;
   A.in = in;
-  render_color_kernel<<<kRasterGrid, 256, 0, st>>>(A);
+  launch_k(render_color_kernel, kRasterGrid, 256, 0, st, A);
   note_launches(1);
   return cuda_check("fvv_render_view");
 }
@@ -1367,7 +1379,7 @@ int fvv_render_count(const fvv_camera *rig, int ncam, const fvv_camera *virt,
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   cudaMemsetAsync(counts_dev, 0, sizeof(int64_t) * (1 + ncam), st);
-  render_count_kernel<<<kRasterGrid, 256, 0, st>>>(A);
+  launch_k(render_count_kernel, kRasterGrid, 256, 0, st, A);
   note_launches(1);
   return cuda_check("fvv_render_count");
 }
@@ -1398,7 +1410,7 @@ int fvv_back_project(const fvv_camera *cam, const double *pixel_dev, const doubl
   if (n <= 0) return FVV_OK;
   int64_t blocks = (n + 255) / 256;
   if (blocks > kRasterGrid) blocks = kRasterGrid;
-  back_project_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(*cam, pixel_dev, depth_dev,
+  launch_k(back_project_kernel, (int)blocks, 256, 0, (cudaStream_t)stream, *cam, pixel_dev, depth_dev,
                                                                       n, out_dev);
   note_launches(1);
   return cuda_check("fvv_back_project");

@@ -73,6 +73,7 @@ template <class F, typename T>
 __global__ void __launch_bounds__(kScanThreads)
     onepass_scan_kernel(const __grid_constant__ F f, const int64_t *n_dev, int64_t n_host,
                         ScanStatus<T> *status, unsigned long long *ticket, T *total) {
+  pdl_wait();
   using Scan = cub::BlockScan<T, kScanThreads>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ long long tile_s;
@@ -155,8 +156,7 @@ inline void onepass_scan(const F &f, const int64_t *n_dev, int64_t n_host, int64
                          void *ws, T *total, cudaStream_t st) {
   const size_t sbytes = onepass_status_bytes<T>(n_max);
   cudaMemsetAsync(ws, 0, sbytes + 64, st);
-  onepass_scan_kernel<F, T><<<kScanGrid, kScanThreads, 0, st>>>(
-      f, n_dev, n_host, (ScanStatus<T> *)ws, (unsigned long long *)((char *)ws + sbytes),
+  launch_k(onepass_scan_kernel<F, T>, kScanGrid, kScanThreads, 0, st, f, n_dev, n_host, (ScanStatus<T> *)ws, (unsigned long long *)((char *)ws + sbytes),
       total);
   note_launches(1);
 }

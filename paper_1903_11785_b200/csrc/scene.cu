@@ -12,6 +12,7 @@ constexpr int kPartDoubles = 18;  // centre[3] orient[9] (row-major) semi[3] rgb
 __global__ void render_parts_kernel(fvv_camera cam, const double *__restrict__ parts, int nparts,
                                     uint8_t *sil, uint8_t *rgb, double ambient, double lx,
                                     double ly, double lz, double bg_r, double bg_g, double bg_b) {
+  pdl_wait();
   extern __shared__ double sp[];
   for (int i = threadIdx.x; i < nparts * kPartDoubles; i += blockDim.x) sp[i] = parts[i];
   __syncthreads();
@@ -104,8 +105,7 @@ extern "C" int fvv_render_ellipsoids(const fvv_camera *cam, const double *parts_
     cudaFuncSetAttribute(render_parts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
   // shading = {ambient, light x, y, z, background r, g, b}
-  render_parts_kernel<<<148 * 4, 256, smem, (cudaStream_t)stream>>>(
-      *cam, parts_dev, nparts, sil_dev, rgb_dev, shading[0], shading[1], shading[2], shading[3],
+  launch_k(render_parts_kernel, 148 * 4, 256, smem, (cudaStream_t)stream, *cam, parts_dev, nparts, sil_dev, rgb_dev, shading[0], shading[1], shading[2], shading[3],
       shading[4], shading[5], shading[6]);
   note_launches(1);
   return cuda_check("fvv_render_ellipsoids");

@@ -19,6 +19,7 @@ constexpr int32_t kNoFeature = INT32_MAX;
 
 __global__ void edt_columns_kernel(const uint8_t *__restrict__ prop, int H, int W,
                                    int32_t *__restrict__ g) {
+  pdl_wait();
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < W; x += gridDim.x * blockDim.x) {
     int last = -1;
     for (int y = 0; y < H; ++y) {
@@ -48,6 +49,7 @@ __device__ __forceinline__ void breakpoint(int p, int64_t fp, int q, int64_t fq,
 // of shared memory.
 __global__ void edt_rows_kernel(const int32_t *__restrict__ g, int H, int W, int rows_per_block,
                                 int32_t *__restrict__ sq) {
+  pdl_wait();
   extern __shared__ uint16_t roots[];
   const int lane = threadIdx.x;
   const int y = blockIdx.x * rows_per_block + lane;
@@ -84,6 +86,7 @@ __global__ void edt_rows_kernel(const int32_t *__restrict__ g, int H, int W, int
 }
 
 __global__ void sq_to_dm_kernel(const int32_t *__restrict__ sq, int64_t n, double *__restrict__ dm) {
+  pdl_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     dm[i] = sq[i] == kNoFeature ? INFINITY : sqrt((double)sq[i]);
@@ -92,6 +95,7 @@ __global__ void sq_to_dm_kernel(const int32_t *__restrict__ sq, int64_t n, doubl
 // silhouette.py:72-87: numpy reduces axis 0 of the (K, ...) stack in order.
 __global__ void background_kernel(const uint8_t *__restrict__ frames, int64_t K, int64_t n,
                                   double *__restrict__ mean, double *__restrict__ sd) {
+  pdl_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     double s = (double)frames[i];
@@ -114,6 +118,7 @@ __global__ void extract_kernel(const uint8_t *__restrict__ frame, const double *
                                const int32_t *__restrict__ sq, const double *__restrict__ dm,
                                double theta_near, double theta_far, double d_max,
                                uint8_t *__restrict__ out) {
+  pdl_wait();
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npx;
        p += (int64_t)gridDim.x * blockDim.x) {
     double dev = -INFINITY;
@@ -149,7 +154,7 @@ int fvv_distance_map(const uint8_t *prop_dev, int64_t H, int64_t W, int32_t *sqd
     return FVV_E_ARG;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  edt_columns_kernel<<<blocks_for(W, 128, 148 * 8), 128, 0, st>>>(prop_dev, (int)H, (int)W,
+  launch_k(edt_columns_kernel, blocks_for(W, 128, 148 * 8), 128, 0, st, prop_dev, (int)H, (int)W,
                                                                   ws_dev);
   int rows = (int)((160 * 1024) / (2 * W));
   if (rows > 32) rows = 32;
@@ -158,11 +163,11 @@ int fvv_distance_map(const uint8_t *prop_dev, int64_t H, int64_t W, int32_t *sqd
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(edt_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-  edt_rows_kernel<<<(int)((H + rows - 1) / rows), 32, smem, st>>>(ws_dev, (int)H, (int)W, rows,
+  launch_k(edt_rows_kernel, (int)((H + rows - 1) / rows), 32, smem, st, ws_dev, (int)H, (int)W, rows,
                                                                   sqdist_dev);
   note_launches(2);
   if (dm_dev) {
-    sq_to_dm_kernel<<<blocks_for(H * W, 256, 148 * 8), 256, 0, st>>>(sqdist_dev, H * W, dm_dev);
+    launch_k(sq_to_dm_kernel, blocks_for(H * W, 256, 148 * 8), 256, 0, st, sqdist_dev, H * W, dm_dev);
     note_launches(1);
   }
   return cuda_check("fvv_distance_map");
@@ -174,8 +179,7 @@ int fvv_background(const uint8_t *frames_dev, int64_t K, int64_t n, double *mean
     set_error("need at least 2 background frames");
     return FVV_E_ARG;
   }
-  background_kernel<<<blocks_for(n, 256, 148 * 8), 256, 0, (cudaStream_t)stream>>>(
-      frames_dev, K, n, mean_dev, std_dev);
+  launch_k(background_kernel, blocks_for(n, 256, 148 * 8), 256, 0, (cudaStream_t)stream, frames_dev, K, n, mean_dev, std_dev);
   note_launches(1);
   return cuda_check("fvv_background");
 }
@@ -184,8 +188,7 @@ int fvv_extract_silhouette(const uint8_t *frame_dev, const double *mean_dev,
                            const double *std_dev, int64_t npx, int C, const int32_t *sqdist_dev,
                            const double *dm_dev, double theta_near, double theta_far,
                            double d_max, uint8_t *mask_dev, void *stream) {
-  extract_kernel<<<blocks_for(npx, 256, 148 * 8), 256, 0, (cudaStream_t)stream>>>(
-      frame_dev, mean_dev, std_dev, npx, C, sqdist_dev, dm_dev, theta_near, theta_far, d_max,
+  launch_k(extract_kernel, blocks_for(npx, 256, 148 * 8), 256, 0, (cudaStream_t)stream, frame_dev, mean_dev, std_dev, npx, C, sqdist_dev, dm_dev, theta_near, theta_far, d_max,
       mask_dev);
   note_launches(1);
   return cuda_check("fvv_extract_silhouette");

@@ -80,6 +80,7 @@ __device__ __forceinline__ double box_hit(const double *r, const double o[3], co
 }
 
 __global__ void synth_kernel(const __grid_constant__ SynthArgs A) {
+  pdl_wait();
   const int W = A.cam.width, H = A.cam.height;
   const int64_t np_ = (int64_t)W * H;
   const fvv_camera &c = A.cam;
@@ -154,6 +155,7 @@ __global__ void synth_kernel(const __grid_constant__ SynthArgs A) {
 // One erosion iteration with the 3x3 cross, outside pixels = 0.
 __global__ void erode_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, int W,
                              int H) {
+  pdl_wait();
   const int64_t np_ = (int64_t)W * H;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < np_;
        p += (int64_t)gridDim.x * blockDim.x) {
@@ -196,7 +198,7 @@ int fvv_synth_render(const fvv_camera *cam, const double *light,
   const int64_t np_ = (int64_t)cam->width * cam->height;
   int64_t blocks = (np_ + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  synth_kernel<<<(int)(blocks > 0 ? blocks : 1), 256, 0, (cudaStream_t)stream>>>(A);
+  launch_k(synth_kernel, (int)(blocks > 0 ? blocks : 1), 256, 0, (cudaStream_t)stream, A);
   note_launches(1);
   return cuda_check("fvv_synth_render");
 }
@@ -219,7 +221,7 @@ int fvv_erode_cross(const uint8_t *in_dev, uint8_t *tmp_dev, uint8_t *out_dev, i
   for (int i = 0; i < iterations; ++i) {
     // ping-pong so the last iteration lands in out_dev
     uint8_t *dst = ((iterations - 1 - i) % 2 == 0) ? out_dev : tmp_dev;
-    erode_kernel<<<(int)blocks, 256, 0, st>>>(src, dst, width, height);
+    launch_k(erode_kernel, (int)blocks, 256, 0, st, src, dst, width, height);
     src = dst;
   }
   note_launches(iterations);
