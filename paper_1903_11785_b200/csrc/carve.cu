@@ -46,7 +46,8 @@ struct CarveParams {
   unsigned long long *amb;  // [0] = queued voxels, then {key, camera mask} entries
   int64_t amb_cap;
   const struct CamAffine *affine;  // [ngrid][ncam] (carve_affine_kernel)
-  unsigned long long *tile_stats;  // culled tiles, sum of fg cameras, sum of mixed cameras
+  unsigned long long *tile_stats;  // culled tiles, sum of fg cameras, sum of mixed cameras;
+                                   // culled octants, carved octants, their mixed cameras
   int tile_log2;                   // tile edge 1 << tile_log2 voxels
   struct TileWork *tiles;          // split mode: surviving tiles (carve_voxels_kernel)
   unsigned long long *ntiles;      //   and their count
@@ -566,11 +567,13 @@ __global__ void __launch_bounds__(kCarveThreads, FVV_CARVE_MINB)
   }
   __syncthreads();
   if (culled) {
+    if (threadIdx.x == 0) atomicAdd(p.tile_stats + 3, 1ull);  // culled octants
     if (kLoop) continue;
     return;
   }
   if (threadIdx.x == 0) {
     int nm = 0, nf = __ldcg(&tw.n_fg);
+    atomicAdd(p.tile_stats + 4, 1ull);  // carved octants
     for (int m = 0; m < tnm; ++m) {
       if (state[m] == kTileFg) {
         ++nf;
@@ -581,6 +584,7 @@ __global__ void __launch_bounds__(kCarveThreads, FVV_CARVE_MINB)
     }
     n_mixed = nm;
     n_fg = nf;
+    atomicAdd(p.tile_stats + 5, (unsigned long long)nm);  // their mixed cameras
   }
   __syncthreads();
   const int my_on = carve_voxels(p, aff, G, g, i0, j0, k0, i1, j1, k1, mixed, mbound, n_mixed,

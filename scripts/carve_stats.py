@@ -50,8 +50,9 @@ for name, specs in (("B-1 stage grid", [coarse]), ("B-3 ROI grids", fine)):
               _lib.dev_ptr(bits), _lib.dev_ptr(counts), _lib.dev_ptr(ws), ctypes.c_size_t(ws_bytes),
               stream_handle())
     torch.cuda.synchronize()
-    st = ws[aff:aff + 24].view(torch.int64).cpu().numpy()
+    st = ws[aff:aff + 48].view(torch.int64).cpu().numpy()
     amb = int(ws[amb_off:amb_off + 8].view(torch.int64).cpu().numpy()[0])
     nvox = sum(s.num_voxels for s in specs)
     print(f"{name}: {nvox} voxels, culled tiles {st[0]}, fg (tile,cam) {st[1]}, "
-          f"mixed (tile,cam) {st[2]}, float64-queued voxels {amb}, ON {int(counts.sum())}")
+          f"mixed (tile,cam) {st[2]}; octants culled {st[3]}, carved {st[4]} with {st[5]} "
+          f"mixed cameras; float64-queued voxels {amb}, ON {int(counts.sum())}")
