@@ -928,6 +928,16 @@ constexpr size_t kDs = 800 * 1024;  // mapped-block region of the device-planned
 constexpr size_t kDsRCounts = 128, kDsComp = 1024, kDsBox = 2048, kDsGrid = 8192,
                  kDsCntF = 16384, kDsInfo = 17408;
 
+// FVV_FORK=0: the device-planned frame as one chain (no side-stream
+// branches; ncu launch lists then follow the stage order)
+static cudaStream_t side_stream(const fvv_frame *f) {
+  static const bool on = [] {
+    const char *e = getenv("FVV_FORK");
+    return !(e && e[0] == '0');
+  }();
+  return on ? f->side : nullptr;
+}
+
 static int enqueue_device_planned(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt,
                                   const int32_t *rank_pos, const uint8_t *frames_dev,
                                   const int64_t *frame_off, const uint8_t *fallback,
@@ -965,7 +975,8 @@ static int enqueue_device_planned(fvv_frame *f, const uint8_t *masks_dev, const 
   // ---- C polygonize ----
   FVV_TRY(4, f->mesh_ws.ensure(mesh_ws_bytes(K.tw, FVV_MAX_GRIDS)));
   FVV_TRY(4, mesh_prepare_batch(&P->mesh, K.tw, FVV_MAX_GRIDS, f->occ_f.as<uint32_t>(),
-                                f->mesh_ws.p, f->mesh_ws.cap, st, f->side, f->fork, f->join));
+                                f->mesh_ws.p, f->mesh_ws.cap, st, side_stream(f), f->fork,
+                                f->join));
   FVV_TRY(4, f->mesh_scratch.ensure(mesh_emit_scratch(K.v, K.s)));
   FVV_TRY(4, f->verts.ensure(24 * (size_t)K.v));
   FVV_TRY(4, f->tris.ensure(12 * (size_t)(5 * K.s)));
@@ -980,7 +991,7 @@ static int enqueue_device_planned(fvv_frame *f, const uint8_t *masks_dev, const 
   f->vis_stride = (nt_ub + 31) / 32 > 0 ? (nt_ub + 31) / 32 : 1;
   FVV_TRY(5, enqueue_tail(f, virt, rank_pos, frames_dev, frame_off, fallback, st, out_stage, K.v,
                           totals, nt_ub, totals + 2, true, f->inputs.as<FrameInputs>(),
-                          f->side));
+                          side_stream(f)));
   // ---- every count in one read ----
   const int64_t *nroi = &P->nroi;
   readback(f, st, {{f->ccl_counts.p, kDs, 16, nullptr, 0, 0},

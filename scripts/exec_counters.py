@@ -10,7 +10,9 @@ rates they reach, FMA / FP64 pipe utilisation, issue-slot utilisation, DRAM
 bytes, L2 sectors and L1 global-load sectors (the gathers) with their
 throughputs. Stages follow the executor's launch order (csrc/frame.cu):
 B-1 sparse carve, B-2 CCL/ROI, B-3 dense carve, C polygonize, D-1 depth
-images (16 cameras), D-2 visibility, E virtual view (raster + colour).
+images (16 cameras), D-2 visibility, E virtual view (raster + colour). Run
+the captured program with FVV_FORK=0 (scripts/gpu/ncu_frame.sh does) so the
+launches come in that order.
 """
 import csv
 import io
@@ -46,10 +48,15 @@ def stage_of(names):
         elif n.startswith("mesh_transpose"):
             stage = "C"
         elif n.startswith("raster_prep") or n.startswith("raster_vertex"):
+            # the executor enqueues the virtual view's raster (E) right after
+            # C (a side-stream branch; FVV_FORK=0 keeps it in the chain), then
+            # D-1's; the colour pass follows D-2
             rasters += 1
-            stage = "D-1" if rasters == 1 else "E"
+            stage = "E" if rasters == 1 else "D-1"
         elif n.startswith("classify"):
             stage = "D-2"
+        elif n.startswith("render_count") or n.startswith("render_color"):
+            stage = "E"
         out.append(stage)
     return out
 
