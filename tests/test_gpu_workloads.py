@@ -330,9 +330,10 @@ def test_reused_executor_equals_fresh_executor(gpu):
 
 def test_device_planner_falls_back_to_host_planning(gpu):
     """An executor that device-plans its frames (after a host-planned first
-    frame) meets a frame with more ROIs than one planned batch holds
-    (FVV_MAX_GRIDS) and then one whose ROIs outgrow its capacities: both are
-    redone by the host-planned path and match the oracle; a small frame
+    frame) meets an empty frame (no ROI: device-planned, nothing to mesh),
+    a frame with more ROIs than one planned batch holds (FVV_MAX_GRIDS) and
+    one whose ROIs outgrow its capacities: the last two are redone by the
+    host-planned path; every frame matches the oracle, and a small frame
     after them is device-planned again and matches too."""
     from paper_1903_11785_b200 import synthetic as S
     from paper_1903_11785_b200.pipeline import PipelineConfig, run_frame
@@ -346,7 +347,7 @@ def test_device_planner_falls_back_to_host_planning(gpu):
             for x in np.linspace(-2600, 2600, 14) for y in np.linspace(-2600, 2600, 14)]
     big = [S.Ellipsoid(center=(x, 0.0, 250.0), semi_axes=(400.0, 400.0, 250.0))
            for x in (-1500.0, 0.0, 1500.0)]
-    for objs in (few, few, few, many, big, few):
+    for objs in (few, few, few, [], many, big, few):  # ([]: no ROI at all, device-planned)
         masks, _ = S.render_scene_device(rig, objs)
         m_np = [m.cpu().numpy().astype(bool) for m in masks]
         bundle = run_frame(cfg, rig, {c.id: None for c in rig}, sils=masks)
