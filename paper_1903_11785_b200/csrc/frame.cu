@@ -974,17 +974,17 @@ static int enqueue_device_planned(fvv_frame *f, const uint8_t *masks_dev, const 
   stage_mark(f, 3, st);
   // ---- C polygonize ----
   FVV_TRY(4, f->mesh_ws.ensure(mesh_ws_bytes(K.tw, FVV_MAX_GRIDS)));
+  FVV_TRY(4, f->mesh_scratch.ensure(mesh_emit_scratch(K.v, K.s)));
   FVV_TRY(4, mesh_prepare_batch(&P->mesh, K.tw, FVV_MAX_GRIDS, f->occ_f.as<uint32_t>(),
                                 f->mesh_ws.p, f->mesh_ws.cap, st, side_stream(f), f->fork,
-                                f->join));
-  FVV_TRY(4, f->mesh_scratch.ensure(mesh_emit_scratch(K.v, K.s)));
+                                f->join, f->mesh_scratch.p, K.v, K.s));
   FVV_TRY(4, f->verts.ensure(24 * (size_t)K.v));
   FVV_TRY(4, f->tris.ensure(12 * (size_t)(5 * K.s)));
   FVV_TRY(4, mesh_emit_batch(f->cams_by_id.data(), ncam, f->sil.as<uint32_t>(),
                              f->word_off_by_id.data(), &P->mesh, K.tw, FVV_MAX_GRIDS, cfg.exact,
                              cfg.fixed_isovalue, f->mesh_ws.p, f->mesh_ws.cap, K.v, K.s,
                              f->mesh_scratch.p, f->mesh_scratch.cap, f->verts.as<double>(),
-                             f->tris.as<int32_t>(), st));
+                             f->tris.as<int32_t>(), st, true));
   stage_mark(f, 4, st);
   int64_t *totals = mesh_ws_totals(f->mesh_ws.p, K.tw, FVV_MAX_GRIDS);  // V, S, T
   const int64_t nt_ub = 5 * K.s;

@@ -310,12 +310,14 @@ int64_t *mesh_ws_info(void *ws, int64_t tw_cap, int ngrid_max);    // [ngrid][8]
 int mesh_prepare_batch(const MeshGrids *G_dev, int64_t tw_cap, int ngrid_max,
                        const uint32_t *occ_dev, void *ws_dev, size_t ws_bytes, cudaStream_t st,
                        cudaStream_t side = nullptr, cudaEvent_t fork = nullptr,
-                       cudaEvent_t join = nullptr);
+                       cudaEvent_t join = nullptr, void *scratch_dev = nullptr,
+                       int64_t cap_v = 0, int64_t cap_s = 0);  // scratch: also list keys
 size_t mesh_emit_scratch(int64_t cap_v, int64_t cap_s);
 int mesh_emit_batch(const fvv_camera *cams_by_id, int ncam, const uint32_t *sil_dev,
                     const int64_t *sil_word_off, const MeshGrids *G_dev, int64_t tw_cap,
                     int ngrid_max, int exact, double fixed_iso, void *ws_dev, size_t ws_bytes,
                     int64_t cap_v, int64_t cap_s, void *scratch_dev, size_t scratch_bytes,
-                    double *verts_dev, int32_t *tris_dev, cudaStream_t st);
+                    double *verts_dev, int32_t *tris_dev, cudaStream_t st,
+                    bool fused = false);  // fused: prepare wrote the vertex / cell lists
 
 }  // namespace fvv

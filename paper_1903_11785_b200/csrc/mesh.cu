@@ -48,6 +48,7 @@ struct MeshBufs {
   // phase B
   int64_t *vert_key;   // [V] V-element*32 + bit
   int32_t *cell_tri;   // [S][5][3] vertex indices of the cell's triangles, emitted order
+  int64_t *cell_key;   // [S] S-element*32 + bit (the fused path's cell list)
   int32_t *cell_mask;  // [S] case | keep<<8 | grid<<16
   int32_t *cprefix;    // [S][5]
   int64_t *slot_base;  // [ngrid][5]
@@ -175,9 +176,16 @@ struct EdgeFlags {
     return (x ^ next) & kmask32(w, nz - 1);
   }
   __device__ int64_t value(uint32_t f) const { return __popc(f); }
+  int64_t *vert_key;  // optional: the vertex list (V-element * 32 + bit), at most cap_v
+  int64_t cap_v;
   __device__ void emit(int64_t e, int64_t prefix, uint32_t f) const {
     eflags[e] = f;
     vprefix[e] = (int32_t)prefix;
+    if (vert_key)
+      for (int64_t v = prefix; f && v < cap_v; ++v) {
+        vert_key[v] = e * 32 + (__ffs(f) - 1);
+        f &= f - 1;
+      }
   }
 };
 
@@ -211,9 +219,16 @@ struct CellFlags {
     return (any & ~all) & kmask32(w, gi.g.dims[2] - 1);
   }
   __device__ int64_t value(uint32_t f) const { return __popc(f); }
+  int64_t *cell_key;  // optional: the surface-cell list (S-element * 32 + bit), at most cap_s
+  int64_t cap_s;
   __device__ void emit(int64_t e, int64_t prefix, uint32_t f) const {
     sflags[e] = f;
     sprefix[e] = (int32_t)prefix;
+    if (cell_key)
+      for (int64_t c = prefix; f && c < cap_s; ++c) {
+        cell_key[c] = e * 32 + (__ffs(f) - 1);
+        f &= f - 1;
+      }
   }
 };
 
@@ -405,6 +420,7 @@ __global__ void __launch_bounds__(128)
   pdl_wait();
   const MeshGrids &G = *Gp;
   if (!emit_fits(B)) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) B.totals[3] = __ldcg(B.totals + 1);  // tri-scan length
   const int64_t nv = __ldcg(B.totals);
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv;
        v += (int64_t)gridDim.x * blockDim.x) {
@@ -592,6 +608,28 @@ struct TriScan {
   }
 };
 
+// The fused path: the triangle scan's load evaluates the surface cell itself
+// (case, per-slot keep bits, triangle vertex indices) from the cell list the
+// cell scan emitted - one pass over the cells instead of two.
+struct TriCells {
+  const MeshGrids *Gp;
+  MeshBufs B;
+  typedef int Item;
+  __device__ int load(int64_t c) const {
+    const int64_t key = B.cell_key[c];
+    mesh_cell(*Gp, B, key >> 5, (int)(key & 31), c);
+    return (B.cell_mask[c] >> 8) & 31;
+  }
+  __device__ Slot5 value(int keep) const {
+    Slot5 s;
+    for (int t = 0; t < 5; ++t) s.v[t] = (keep >> t) & 1;
+    return s;
+  }
+  __device__ void emit(int64_t c, Slot5 prefix, int) const {
+    for (int t = 0; t < 5; ++t) B.cprefix[5 * c + t] = prefix.v[t];
+  }
+};
+
 // ---- B4: per-grid slot bases (one warp, a lane per grid) ---------------------
 __global__ void mesh_slot_bases_kernel(const MeshGrids *__restrict__ Gp, MeshBufs B,
                                        const Slot5 *total) {
@@ -707,6 +745,34 @@ static MeshBufs bufs_from(void *ws, const PrepLayout &L) {
   return B;
 }
 
+// phase-B scratch: vertex list, cell list, per-cell triangles / case+keep /
+// slot prefixes, the triangle scan's status words
+struct ScratchLayout {
+  int64_t *vert_key, *cell_key;
+  int32_t *cell_tri, *cell_mask, *cprefix;
+  Slot5 *cell_sums;
+  size_t total;
+};
+
+static ScratchLayout scratch_layout(void *scratch, int64_t cap_v, int64_t cap_s) {
+  ScratchLayout S;
+  char *base = (char *)scratch, *s = base;
+  S.vert_key = (int64_t *)s;
+  s += al256(8 * (size_t)cap_v);
+  S.cell_key = (int64_t *)s;
+  s += al256(8 * (size_t)cap_s);
+  S.cell_tri = (int32_t *)s;
+  s += al256(60 * (size_t)cap_s);
+  S.cell_mask = (int32_t *)s;
+  s += al256(4 * (size_t)cap_s);
+  S.cprefix = (int32_t *)s;
+  s += al256(20 * (size_t)cap_s);
+  S.cell_sums = (Slot5 *)s;
+  s += al256(onepass_bytes<Slot5>(cap_s + 1));
+  S.total = (size_t)(s - base);
+  return S;
+}
+
 static_assert(sizeof(MeshGrids) % 16 == 0, "MeshGrids is copied in 16-byte words");
 __global__ void store_mesh_grids_kernel(const __grid_constant__ MeshGrids src, MeshGrids *dst) {
   pdl_wait();
@@ -784,7 +850,7 @@ int64_t *fvv::mesh_ws_info(void *ws, int64_t tw_cap, int ngrid_max) {
 int fvv::mesh_prepare_batch(const MeshGrids *G_dev, int64_t tw_cap, int ngrid_max,
                             const uint32_t *occ_dev, void *ws_dev, size_t ws_bytes,
                             cudaStream_t st, cudaStream_t side, cudaEvent_t fork,
-                            cudaEvent_t join) {
+                            cudaEvent_t join, void *scratch_dev, int64_t cap_v, int64_t cap_s) {
   int rc = ensure_tables();
   if (rc) return rc;
   const PrepLayout L = prep_layout(tw_cap, ngrid_max);
@@ -804,11 +870,13 @@ int fvv::mesh_prepare_batch(const MeshGrids *G_dev, int64_t tw_cap, int ngrid_ma
       cudaEventRecord(fork, st);
       cudaStreamWaitEvent(side, fork, 0);
     }
-    CellFlags cf{G_dev, B.tw, B.sflags, B.sprefix};
+    // with a phase-B scratch, the scans also write the vertex and cell lists
+    const ScratchLayout SL = scratch_layout(scratch_dev, cap_v, cap_s);
+    CellFlags cf{G_dev, B.tw, B.sflags, B.sprefix, scratch_dev ? SL.cell_key : nullptr, cap_s};
     onepass_scan(cf, &G_dev->tw_total, 0, tw_cap, (void *)(side ? B.sums2 : B.sums),
                  B.totals + 1, side ? side : st);
     if (side) cudaEventRecord(join, side);
-    EdgeFlags ef{G_dev, B.tw, B.eflags, B.vprefix};
+    EdgeFlags ef{G_dev, B.tw, B.eflags, B.vprefix, scratch_dev ? SL.vert_key : nullptr, cap_v};
     onepass_scan(ef, &G_dev->tw3, 0, 3 * tw_cap, (void *)B.sums, B.totals + 0, st);
     if (side) cudaStreamWaitEvent(st, join, 0);
   }
@@ -818,8 +886,7 @@ int fvv::mesh_prepare_batch(const MeshGrids *G_dev, int64_t tw_cap, int ngrid_ma
 }
 
 size_t fvv::mesh_emit_scratch(int64_t cap_v, int64_t cap_s) {
-  return al256(8 * (size_t)cap_v) + al256(60 * (size_t)cap_s) + al256(4 * (size_t)cap_s) +
-         al256(20 * (size_t)cap_s) + al256(onepass_bytes<Slot5>(cap_s + 1));
+  return scratch_layout(nullptr, cap_v, cap_s).total;
 }
 
 int fvv::mesh_emit_batch(const fvv_camera *cams_by_id, int ncam, const uint32_t *sil_dev,
@@ -827,7 +894,7 @@ int fvv::mesh_emit_batch(const fvv_camera *cams_by_id, int ncam, const uint32_t 
                          int ngrid_max, int exact, double fixed_iso, void *ws_dev,
                          size_t ws_bytes, int64_t cap_v, int64_t cap_s, void *scratch_dev,
                          size_t scratch_bytes, double *verts_dev, int32_t *tris_dev,
-                         cudaStream_t st) {
+                         cudaStream_t st, bool fused) {
   int rc = ensure_tables();
   if (rc) return rc;
   if (exact && (ncam < 1 || ncam > FVV_MAX_CAMS)) {
@@ -840,16 +907,13 @@ int fvv::mesh_emit_batch(const fvv_camera *cams_by_id, int ncam, const uint32_t 
     return FVV_E_ARG;
   }
   MeshBufs B = bufs_from(ws_dev, L);
-  char *s = (char *)scratch_dev;
-  B.vert_key = (int64_t *)s;
-  s += al256(8 * (size_t)cap_v);
-  B.cell_tri = (int32_t *)s;
-  s += al256(60 * (size_t)cap_s);
-  B.cell_mask = (int32_t *)s;
-  s += al256(4 * (size_t)cap_s);
-  B.cprefix = (int32_t *)s;
-  s += al256(20 * (size_t)cap_s);
-  Slot5 *cell_sums = (Slot5 *)s;
+  const ScratchLayout SL = scratch_layout(scratch_dev, cap_v, cap_s);
+  B.vert_key = SL.vert_key;
+  B.cell_key = SL.cell_key;
+  B.cell_tri = SL.cell_tri;
+  B.cell_mask = SL.cell_mask;
+  B.cprefix = SL.cprefix;
+  Slot5 *cell_sums = SL.cell_sums;
   B.verts = verts_dev;
   B.tris = tris_dev;
   B.cap_v = cap_v;
@@ -864,16 +928,19 @@ int fvv::mesh_emit_batch(const fvv_camera *cams_by_id, int ncam, const uint32_t 
   }
   Slot5 *d_total = (Slot5 *)((char *)ws_dev + L.slot5 + sizeof(int64_t) * 5 * ngrid_max);
   if (cap_v > 0) {
-    launch_k(mesh_vertex_list_kernel, kMeshGrid, 256, 0, st, G_dev, B);
+    if (!fused) launch_k(mesh_vertex_list_kernel, kMeshGrid, 256, 0, st, G_dev, B);
     // one vertex per thread, cameras in a loop; measured against (vertex,
     // camera) lane groups and a certified-FP32 endpoint projection with the
     // float64 terms deferred to full warps, both slower
     const int64_t lam_blocks = std::min<int64_t>(cap_v / 128 + 1, 148 * 64);
     launch_k(mesh_lambda_kernel, (unsigned)lam_blocks, 128, 0, st, G_dev, h_cams, B, sil_dev, exact,
                                                               fixed_iso);
-    note_launches(2);
+    note_launches(fused ? 1 : 2);
   }
-  if (cap_s > 0) {
+  if (cap_s > 0 && fused) {  // the cells evaluated inside the triangle scan
+    TriCells tc{G_dev, B};
+    onepass_scan(tc, B.totals + 3, 0, cap_s, (void *)cell_sums, d_total, st);
+  } else if (cap_s > 0) {
     const int64_t cell_blocks = std::min<int64_t>(tw_cap / 256 + 1, 148 * 64);
     launch_k(mesh_cells_kernel, (unsigned)std::max<int64_t>(cell_blocks, kMeshGrid), 256, 0, st, G_dev,
                                                                                           B);
@@ -910,7 +977,7 @@ int fvv_mesh_prepare(const fvv_grid *grids, int ngrid, const uint32_t *occ_dev,
   launch_k(store_mesh_grids_kernel, 1, 256, 0, st, G, G_dev);
   note_launches(1);
   return mesh_prepare_batch(G_dev, G.tw_total, ngrid, occ_dev, ws_dev, ws_bytes, st, nullptr,
-                            nullptr, nullptr);
+                            nullptr, nullptr, nullptr, 0, 0);
 }
 
 // Reads the counts fvv_mesh_prepare left in the workspace: totals[3] = {V, S, T}
@@ -951,7 +1018,7 @@ int fvv_mesh_emit(const fvv_camera *cams_by_id, int ncam, const uint32_t *sil_de
   return mesh_emit_batch(cams_by_id, ncam, sil_dev, sil_word_off,
                          (const MeshGrids *)((char *)ws_dev + L.grids), tw, ngrid, exact,
                          fixed_iso, ws_dev, ws_bytes, num_vertices, num_cells, scratch_dev,
-                         scratch_bytes, verts_dev, tris_dev, (cudaStream_t)stream);
+                         scratch_bytes, verts_dev, tris_dev, (cudaStream_t)stream, false);
 }
 
 int fvv_edge_isovalues(const fvv_camera *cams_by_id, int ncam, const uint32_t *sil_dev,
