@@ -125,9 +125,14 @@ __device__ __forceinline__ bool project_rint(const fvv_camera &c, double x, doub
 // project_rint with the perspective division in FP32: the float64 chain's
 // X, Y, Z (exact Z: the depth test needs it), then u, v from their float
 // roundings with one reciprocal, kept when u and v lie farther than a
-// rigorous bound (2^-19 relative: >= 2x the ~10 FP32 roundings involved, and
-// the float64 chain's own error) from a rounding boundary; the float64
-// divisions otherwise (near a tie, |u| >= 2^22, tiny Z).
+// rigorous bound from a rounding boundary; the float64 divisions otherwise
+// (near a tie, |u| >= 2^22, tiny Z). Bound: with unit roundoff eps = 2^-24,
+// X/Y/Z to float (eps each), the refined reciprocal (2 eps), the products
+// give xn, yn within 5 eps; skew * yn 7 eps; their sum 8 eps of
+// (|xn| + |syn|); fx (float) times it 10 eps of |fx| (|xn| + |syn|); + cx
+// (eps |cx|) and the final rounding (eps |u|): |u32 - u| <= 10 eps M with
+// M = |fx| (|xn| + |syn|) + |cx| + |u|. 2^-20 M is 1.6x that (the float64
+// chain's own ~1e-16 relative error and second-order terms are far below).
 __device__ __forceinline__ float recip32(float z) {
   const float r = __fdividef(1.0f, z);
   return fmaf(r, fmaf(-z, r, 1.0f), r);
@@ -148,8 +153,8 @@ __device__ __forceinline__ bool project_rint32(const fvv_camera &c, double x, do
   const float syn = sk * yn;
   const float su = fx * (xn + syn), sv = fy * yn;
   const float u = su + cx, v = sv + cy;
-  const float eu = 0x1p-19f * (fabsf(fx) * (fabsf(xn) + fabsf(syn)) + fabsf(cx) + fabsf(u) + 1.0f);
-  const float ev = 0x1p-19f * (fabsf(sv) + fabsf(cy) + fabsf(v) + 1.0f);
+  const float eu = 0x1p-20f * (fabsf(fx) * (fabsf(xn) + fabsf(syn)) + fabsf(cx) + fabsf(u) + 1.0f);
+  const float ev = 0x1p-20f * (fabsf(sv) + fabsf(cy) + fabsf(v) + 1.0f);
   const float ru = rintf(u), rv = rintf(v);
   ok = ok && fabsf(u) < 4194304.0f && fabsf(v) < 4194304.0f && fabsf(u - ru) < 0.5f - eu &&
        fabsf(v - rv) < 0.5f - ev;
