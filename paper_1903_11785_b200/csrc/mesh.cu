@@ -615,6 +615,7 @@ struct TriCells {
   const MeshGrids *Gp;
   MeshBufs B;
   typedef int Item;
+  static constexpr int kItems = 1;  // a cell's evaluation is a long chain (measured: 57 -> 51 us)
   __device__ int load(int64_t c) const {
     const int64_t key = B.cell_key[c];
     mesh_cell(*Gp, B, key >> 5, (int)(key & 31), c);

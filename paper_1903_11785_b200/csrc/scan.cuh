@@ -20,7 +20,21 @@ __device__ __forceinline__ int64_t scan_len(const int64_t *n_dev, int64_t n_host
   return device_count(n_dev, n_host);
 }
 
-inline int64_t scan_chunks(int64_t n_max) { return (n_max + kScanChunk - 1) / kScanChunk + 1; }
+inline int64_t scan_chunks(int64_t n_max, int items = kScanItems) {
+  const int64_t chunk = (int64_t)kScanThreads * items;
+  return (n_max + chunk - 1) / chunk + 1;
+}
+
+// Elements per thread of a functor's scan: F::kItems when it declares one
+// (heavy loads: fewer per thread, more chunks in flight), else kScanItems.
+template <class F, class = void>
+struct scan_items {
+  static constexpr int value = kScanItems;
+};
+template <class F>
+struct scan_items<F, decltype((void)F::kItems)> {
+  static constexpr int value = F::kItems;
+};
 
 // ---- single pass: decoupled look-back ----------------------------------------
 // Chunks are taken in order from a ticket counter; each publishes its
@@ -79,17 +93,19 @@ __global__ void __launch_bounds__(kScanThreads)
   __shared__ long long tile_s;
   __shared__ T prefix_s;
   const int64_t n = scan_len(n_dev, n_host);
-  const int64_t nchunks = (n + kScanChunk - 1) / kScanChunk;
+  constexpr int kItems = scan_items<F>::value;
+  constexpr int64_t kChunk = (int64_t)kScanThreads * kItems;
+  const int64_t nchunks = (n + kChunk - 1) / kChunk;
   while (true) {
     if (threadIdx.x == 0) tile_s = (long long)atomicAdd(ticket, 1ull);
     __syncthreads();
     const int64_t c = tile_s;
     if (c >= nchunks) break;
-    typename F::Item item[kScanItems];
-    T v[kScanItems], ex[kScanItems];
+    typename F::Item item[kItems];
+    T v[kItems], ex[kItems];
 #pragma unroll
-    for (int it = 0; it < kScanItems; ++it) {
-      const int64_t i = c * kScanChunk + (int64_t)threadIdx.x * kScanItems + it;
+    for (int it = 0; it < kItems; ++it) {
+      const int64_t i = c * kChunk + (int64_t)threadIdx.x * kItems + it;
       item[it] = i < n ? f.load(i) : typename F::Item();
       v[it] = i < n ? f.value(item[it]) : T(0);
     }
@@ -131,8 +147,8 @@ __global__ void __launch_bounds__(kScanThreads)
     __syncthreads();
     const T base = prefix_s;
 #pragma unroll
-    for (int it = 0; it < kScanItems; ++it) {
-      const int64_t i = c * kScanChunk + (int64_t)threadIdx.x * kScanItems + it;
+    for (int it = 0; it < kItems; ++it) {
+      const int64_t i = c * kChunk + (int64_t)threadIdx.x * kItems + it;
       if (i < n) f.emit(i, base + ex[it], item[it]);
     }
     __syncthreads();
@@ -143,7 +159,7 @@ __global__ void __launch_bounds__(kScanThreads)
 // Workspace of onepass_scan for n_max elements: status words + ticket.
 template <typename T>
 inline size_t onepass_status_bytes(int64_t n_max) {  // 8-byte aligned ticket after it
-  return (sizeof(ScanStatus<T>) * (size_t)scan_chunks(n_max) + 15) & ~(size_t)15;
+  return (sizeof(ScanStatus<T>) * (size_t)scan_chunks(n_max, 1) + 15) & ~(size_t)15;
 }
 
 template <typename T>
