@@ -54,7 +54,7 @@ static CclWs ccl_layout(void *base, const int64_t *dims) {
   w.nvox = nvox;
   w.words = (nvox + 31) / 32;
   w.comp_cap = max_components(dims);
-  w.counts = (int64_t *)p;
+  w.counts = (int64_t *)p;  // (first: the frame executor reads n_on / ncomp here in place)
   p += align256(4 * sizeof(int64_t));
   w.sums = (int64_t *)p;
   p += align256(onepass_bytes<int64_t>(nvox > w.words ? nvox : w.words));

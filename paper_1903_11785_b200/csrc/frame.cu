@@ -354,7 +354,7 @@ struct fvv_frame {
   fvv_grid coarse;
   // persistent device buffers
   DevBuf carve_ws, code;
-  DevBuf sil, occ_c, cnt_c, ccl_ws, comps, ccl_counts, occ_f, cnt_f, mesh_ws, mesh_scratch,
+  DevBuf sil, occ_c, cnt_c, ccl_ws, comps, occ_f, cnt_f, mesh_ws, mesh_scratch,
       mesh_totals, mesh_info, verts, tris, ntri, raster_ws, depth, vis, vplane_d, vplane_id,
       vraster_ws, src, rcounts, color, source, covered;
   // 32-pixel dirty-tile maps of the depth planes and of the virtual view's
@@ -392,6 +392,10 @@ struct fvv_frame {
   std::vector<char> graph_key, pending_key;
   long long graph_launches = 0;
 };
+
+// B-2's ON-voxel and component counts: the first words of the CCL workspace
+// (fvv_ccl26's layout), read in place
+static int64_t *ccl_counts(fvv_frame *f) { return f->ccl_ws.as<int64_t>(); }
 
 // Stage boundary event; inside a graph capture an external event-record node,
 // so the replayed frame still reports its stage times.
@@ -528,7 +532,7 @@ fvv_frame *fvv_frame_create(const fvv_camera *cams, int ncam, const fvv_frame_co
   cudaEventCreateWithFlags(&f->join, cudaEventDisableTiming);
   if (f->sil.ensure(4 * (size_t)f->sil_words) || f->occ_c.ensure(4 * (size_t)((
           f->coarse.dims[0] * f->coarse.dims[1] * f->coarse.dims[2] + 31) / 32)) ||
-      f->cnt_c.ensure(64) || f->ccl_counts.ensure(64) ||
+      f->cnt_c.ensure(64) ||
       f->ccl_ws.ensure(fvv_ccl_workspace_bytes(&f->coarse)) ||
       f->comps.ensure(sizeof(fvv_component) * 4096) || f->mesh_totals.ensure(64) ||
       f->ntri.ensure(64) || f->carve_ws.ensure(fvv_carve_workspace_bytes(f->cams.data(), f->ncam)) ||
@@ -571,7 +575,7 @@ static int enqueue_b12(fvv_frame *f, const uint8_t *masks_dev, const FrameInputs
 
   // ---- B-2 CCL, noise filter, ROIs (pipeline.py:159-166) ----
   FVV_TRY(2, fvv_ccl26(f->occ_c.as<uint32_t>(), &G, f->ccl_ws.p, f->ccl_ws.cap,
-                       f->comps.as<fvv_component>(), 4096, f->ccl_counts.as<int64_t>(), st));
+                       f->comps.as<fvv_component>(), 4096, nullptr, st));
   return FVV_OK;
 }
 
@@ -697,9 +701,9 @@ static int run_host_planned(fvv_frame *f, const uint8_t *masks_dev, const fvv_ca
   FVV_TRY(1, enqueue_b12(f, masks_dev, nullptr, st, out_stage));
   const fvv_grid &G = f->coarse;
   int64_t *hs = (int64_t *)f->host_small;
-  readback(f, st, {{f->ccl_counts.p, 0, 16, nullptr, 0, 0},
+  readback(f, st, {{ccl_counts(f), 0, 16, nullptr, 0, 0},
                    {f->cnt_c.p, 16, 8, nullptr, 0, 0},
-                   {f->comps.p, kHsComps, 0, f->ccl_counts.as<int64_t>() + 1,
+                   {f->comps.p, kHsComps, 0, ccl_counts(f) + 1,
                     (int64_t)sizeof(fvv_component), 4096}});
   if (cudaStreamSynchronize(st) != cudaSuccess) {
     if (out_stage) *out_stage = 2;
@@ -961,7 +965,7 @@ static int enqueue_device_planned(fvv_frame *f, const uint8_t *masks_dev, const 
   pa.cap_tiles = K.tiles;
   pa.cap_tw = K.tw;
   launch_k(frame_plan_kernel, 1, kPlanThreads, 0, st, pa, f->comps.as<fvv_component>(),
-                                                f->ccl_counts.as<int64_t>(), P);
+                                                ccl_counts(f), P);
   note_launches(1);
   stage_mark(f, 2, st);
   // ---- B-3 dense carve over the planned grids ----
@@ -994,7 +998,7 @@ static int enqueue_device_planned(fvv_frame *f, const uint8_t *masks_dev, const 
                           side_stream(f)));
   // ---- every count in one read ----
   const int64_t *nroi = &P->nroi;
-  readback(f, st, {{f->ccl_counts.p, kDs, 16, nullptr, 0, 0},
+  readback(f, st, {{ccl_counts(f), kDs, 16, nullptr, 0, 0},
                    {f->cnt_c.p, kDs + 16, 8, nullptr, 0, 0},
                    {P, kDs + 32, 32, nullptr, 0, 0},  // status, nroi, dense_tests, fine_words
                    {totals, kDs + 64, 24, nullptr, 0, 0},
