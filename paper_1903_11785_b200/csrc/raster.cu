@@ -151,6 +151,11 @@ __device__ __forceinline__ void pixel_update(int pass, double d, int64_t t,
   }
 }
 
+// (item, pixel) pair entries carry the camera in the top bits of the
+// triangle index (no division to split a camera-major item index)
+constexpr int kPairCamShift = 26;
+constexpr uint32_t kPairTriMask = (1u << kPairCamShift) - 1u;
+
 struct RasterArgs {
   const double4 *P;  // [ncam][nv] projected vertices (u, v, z, 0)
   const float2 *Q;   // [ncam][nv] (u, v) rounded to float; NaN: the vertex culls its triangles
@@ -359,6 +364,7 @@ __global__ void __launch_bounds__(256)
     }
     const int W = C.cams[c].width, H = C.cams[c].height;
     const uint32_t w = (uint32_t)(c * nt + t);  // camera-major item index
+    const uint32_t pw = ((uint32_t)c << kPairCamShift) | (uint32_t)t;  // pair entries: (camera, t)
     int state = 0;          // 0 nothing, 1 pixels in `bits`, 2 slow path
     unsigned bits = 0;      // candidate pixels of the tight range, row-major
     int gx0 = 0, gy0 = 0, rw = 1;
@@ -451,7 +457,7 @@ __global__ void __launch_bounds__(256)
           const int k = __ffs(b) - 1;
           b &= b - 1;
           const int qy = k >> sh;
-          *slot++ = make_uint2(w, ((uint32_t)(gy0 + qy) << 16) | (uint32_t)(gx0 + k - qy * rw));
+          *slot++ = make_uint2(pw, ((uint32_t)(gy0 + qy) << 16) | (uint32_t)(gx0 + k - qy * rw));
         }
         }
         np += sum;  // = entries written
@@ -488,8 +494,8 @@ __global__ void __launch_bounds__(256)
     if (!kRec) {
       for (int i = lane; i < n; i += 32) {
         const uint2 e = pl[i];
-        const int c = (int)(e.x / (uint32_t)nt);
-        const int64_t t = (int64_t)e.x - (int64_t)c * nt;
+        const int c = (int)(e.x >> kPairCamShift);
+        const int64_t t = (int64_t)(e.x & kPairTriMask);
         const int x = (int)(e.y & 0xffffu), y = (int)(e.y >> 16);
         const int width = C.cams[c].width;
         TriSetup s;
@@ -512,8 +518,8 @@ __global__ void __launch_bounds__(256)
       int64_t p = 0, t = 0;
       if (i < n) {
         const uint2 e = pl[i];
-        const int c = (int)(e.x / (uint32_t)nt);
-        t = (int64_t)e.x - (int64_t)c * nt;
+        const int c = (int)(e.x >> kPairCamShift);
+        t = (int64_t)(e.x & kPairTriMask);
         const int x = (int)(e.y & 0xffffu), y = (int)(e.y >> 16);
         const int width = C.cams[c].width;
         TriSetup s;
@@ -1117,8 +1123,10 @@ static int rasterize_impl(const fvv_camera *cams, int ncam, const double *verts_
       return FVV_E_LIMIT;
     }
   }
-  if (nt > 0 && nt * (int64_t)ncam >= 0xffffffffll) {  // 32-bit item indices
-    set_error("fvv_rasterize: %lld triangles x %d cameras exceeds 2^32 - 1", (long long)nt, ncam);
+  if (nt > 0 && (nt * (int64_t)ncam >= 0xffffffffll || nt > (int64_t)kPairTriMask)) {
+    // 32-bit item indices; pair entries hold 26-bit triangle indices
+    set_error("fvv_rasterize: %lld triangles x %d cameras exceeds 2^32 - 1 (or 2^26 triangles)",
+              (long long)nt, ncam);
     return FVV_E_LIMIT;
   }
   // background: depth +inf, id -1 (visibility.py:44-45); one fill when the
