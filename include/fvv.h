@@ -326,6 +326,11 @@ typedef struct fvv_frame_stats {
     int64_t covered_px, sourced_px;
 } fvv_frame_stats;
 
+/* How the last fvv_frame_run ran: 0 host-planned (first frame, or a frame
+ * the device planner handed back), 1 device-planned enqueue, 2 device-planned
+ * graph capture + launch, 3 graph replay. */
+int fvv_frame_last_mode(const fvv_frame *f);
+
 /* Device outputs of the last fvv_frame_run (valid until the next run):
  * merged-order triangles indexing verts (per-ROI slices via fvv_frame_rois),
  * visibility bits (ncam x vis_stride words), depth planes (rig order,

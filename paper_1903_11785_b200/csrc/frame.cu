@@ -391,6 +391,7 @@ struct fvv_frame {
   cudaGraphExec_t graph = nullptr;
   std::vector<char> graph_key, pending_key;
   long long graph_launches = 0;
+  int last_mode = 0;  // fvv_frame_last_mode
 };
 
 // B-2's ON-voxel and component counts: the first words of the CCL workspace
@@ -1081,13 +1082,7 @@ static void update_caps(fvv_frame *f, int64_t words, int64_t tiles, int64_t tw, 
     }
   };
   fit(words, K.words);
-  // tiles: one B-3 classification block per tile and eight octant blocks per
-  // tile are launched for the capacity, so it carries less headroom
-  if (tiles > K.tiles - K.tiles / 32 || K.tiles == 0) {
-    const int64_t base = tiles > K.tiles ? tiles : K.tiles;
-    K.tiles = base + base / 16 + 32;
-    grew = true;
-  }
+  fit(tiles, K.tiles);  // (launch size of B-3's tile classification only)
   fit(tw, K.tw);
   fit(v, K.v);
   fit(sn, K.s);
@@ -1191,7 +1186,9 @@ static int run_device_planned(fvv_frame *f, const uint8_t *masks_dev, const fvv_
     launch_k(bind_inputs_kernel, 1, 32, 0, st, in, f->inputs.as<FrameInputs>());
     note_launches(1);
   }
+  f->last_mode = 1;  // device-planned, enqueued
   if (graphs && f->graph && key == f->graph_key) {
+    f->last_mode = 3;  // graph replay
     f->stats.sparse_tests = f->coarse.dims[0] * f->coarse.dims[1] * f->coarse.dims[2];
     f->virt_px = virt ? (int64_t)virt->width * virt->height : 0;
     const int64_t nt_ub = 5 * f->caps.s;
@@ -1199,6 +1196,7 @@ static int run_device_planned(fvv_frame *f, const uint8_t *masks_dev, const fvv_
     if (cudaGraphLaunch(f->graph, st) != cudaSuccess) return cuda_check("fvv_frame_run graph");
     note_launches(f->graph_launches);
   } else if (graphs && key == f->pending_key) {
+    f->last_mode = 2;  // graph capture + launch
     // second frame with these bindings (buffers and dirty maps settled by the
     // first): capture the frame once, then replay it
     if (f->graph) cudaGraphExecDestroy(f->graph);
@@ -1258,6 +1256,7 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
       return FVV_OK;
     }
   }
+  f->last_mode = 0;  // host-planned
   const int rc = run_host_planned(f, masks_dev, virt, rank_pos, frames_dev, frame_off, fallback,
                                   stream, out_stats, out_stage);
   if (rc == FVV_OK && f->seen_plannable)
@@ -1265,6 +1264,8 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
   return rc;
 }
 
+
+int fvv_frame_last_mode(const fvv_frame *f) { return f ? f->last_mode : -1; }
 
 int fvv_frame_get_outputs(const fvv_frame *f, fvv_frame_outputs *o) {
   memset(o, 0, sizeof(*o));

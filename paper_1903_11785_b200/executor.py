@@ -229,6 +229,12 @@ class FrameExecutor:
             self._ranks[key] = hit
         return hit[1]
 
+    @property
+    def last_mode(self) -> int:
+        """How the last run went: 0 host-planned, 1 device-planned, 2 captured
+        as a CUDA graph, 3 graph replay (fvv_frame_last_mode)."""
+        return int(_lib.load().fvv_frame_last_mode(self._h))
+
     def run(self, masks, virtual=None, frames_buf=None, frame_off=None, fallback=None):
         """masks: uint8 (N,H,W) (or flat) CUDA tensor in rig order; for the
         colour pass, frames_buf (uint8 CUDA tensor, or the int base address of

@@ -289,18 +289,22 @@ def test_host_scene_generator_matches_device(gpu):
     assert diff <= 1e-4 * total, (diff, total)  # rounding-level ray-cast ties at most
 
 
-def test_reused_executor_equals_fresh_executor(gpu):
-    """A re-used executor runs device-planned frames (planner kernel, no host
-    round trip; the third frame as a captured CUDA graph) and resets its
-    depth planes per 32-pixel tile from the previous frame's dirty map: after
-    frames 4 -> 0 -> 7 on one executor, frame 7's depth planes, visibility,
-    mesh and virtual view equal those of a fresh (host-planned) executor."""
+@pytest.mark.parametrize("workload", ["C3", "C4"])
+def test_reused_executor_equals_fresh_executor(gpu, workload):
+    """A re-used executor on its own stream runs device-planned frames
+    (planner kernel, no host round trip), captures one as a CUDA graph and
+    replays it, and resets its depth planes per 32-pixel tile from the
+    previous frame's dirty map: after frames 4 -> 0 -> 7 -> 2 on one
+    executor, frames 7 and 2 replayed from the graph - depth planes (C3),
+    visibility, mesh and virtual view - equal those of a fresh
+    (host-planned) executor. C4: 32 x 4K cameras, 2.5 M triangles."""
     import torch
 
     from paper_1903_11785_b200 import workloads
     from paper_1903_11785_b200.executor import FrameExecutor
 
-    wl = workloads.get("C3")
+    wl = workloads.get(workload)
+    keep = workload == "C3"  # (C4's 32 4K depth planes are 2.1 GB)
 
     def run(ex, frame):
         from paper_1903_11785_b200 import synthetic as S
@@ -309,23 +313,33 @@ def test_reused_executor_equals_fresh_executor(gpu):
         fb = frames.reshape(-1)
         foff = np.arange(len(wl.rig), dtype=np.int64) * (frames.shape[1] * frames.shape[2] * 3)
         out = ex.run(masks, wl.virtual, fb, foff)
-        host = out.to_host(wl.rig, keep_depths=True)
+        host = out.to_host(wl.rig, keep_depths=keep)
         torch.cuda.synchronize()
         return out.stats(), {k: np.array(v) for k, v in host.items()}
 
-    reused = FrameExecutor(wl.cfg, wl.rig)
-    for f in (4, 0):
-        run(reused, f)
-    s_a, a = run(reused, 7)
-    s_b, b = run(FrameExecutor(wl.cfg, wl.rig), 7)
-    assert s_a == s_b
-    assert a.keys() == b.keys() and "depth" in a
-    words = (s_a["triangles"] + 31) // 32  # (the row stride is a capacity, not part of the result)
-    a["vis"], b["vis"] = a["vis"][:, :words], b["vis"][:, :words]
-    for k in a:
-        assert np.array_equal(a[k], b[k]), k
-    d = a["depth"]
-    assert np.isinf(d).any() and np.isfinite(d).any()
+    side = torch.cuda.Stream()  # (graphs need a stream other than the legacy default)
+    with torch.cuda.stream(side):
+        reused = FrameExecutor(wl.cfg, wl.rig)
+        modes = []
+        for f in (4, 0, 7, 2):  # (a larger frame may be re-planned on the host once)
+            run(reused, f)
+            modes.append(reused.last_mode)
+        assert modes[0] == 0 and 2 in modes  # host-planned first, a graph captured
+        got = {}
+        for f in (7, 2):
+            got[f] = run(reused, f)
+            assert reused.last_mode == 3, (f, modes)  # graph replays
+        for f in (7, 2):
+            s_a, a = got[f]
+            s_b, b = run(FrameExecutor(wl.cfg, wl.rig), f)
+            assert s_a == s_b, f
+            assert a.keys() == b.keys() and ("depth" in a) == keep
+            words = (s_a["triangles"] + 31) // 32  # (the row stride is a capacity)
+            a["vis"], b["vis"] = a["vis"][:, :words], b["vis"][:, :words]
+            for k in a:
+                assert np.array_equal(a[k], b[k]), (f, k)
+            if keep:
+                assert np.isinf(a["depth"]).any() and np.isfinite(a["depth"]).any()
 
 
 def test_device_planner_falls_back_to_host_planning(gpu):
