@@ -12,7 +12,10 @@
 namespace fvv {
 
 constexpr int kScanThreads = 256;
-constexpr int kScanItems = 4;
+#ifndef FVV_SCAN_ITEMS
+#define FVV_SCAN_ITEMS 4
+#endif
+constexpr int kScanItems = FVV_SCAN_ITEMS;
 constexpr int kScanChunk = kScanThreads * kScanItems;  // 1024 elements per chunk
 constexpr int kScanGrid = 148 * 4;
 
@@ -42,11 +45,59 @@ struct scan_items<F, decltype((void)F::kItems)> {
 // prefix. The functor is split so each element is decoded once:
 // `Item load(int64_t i)`, `T value(const Item &)` and
 // `void emit(int64_t i, T prefix, const Item &)`.
+//
+// The grid's first wave takes ~600 chunks at once, so a late chunk's
+// predecessors are still looking back themselves and it sums aggregates a
+// long way. So a status is read in one L2 round trip, no fence between flag
+// and value: 8-byte values share one 16-byte word with their flag; values of
+// up to 24 bytes (the mesh's 5-slot counts) are split over two 16-byte
+// halves that each carry the flag, and a reader takes a status only when
+// both halves show the same nonzero flag (each half is written by one vector
+// store, and a flag value is published once per status). Each lane reads
+// FVV_SCAN_LB statuses of 8-byte values per round (EdgeFlags 42 -> 31 us at
+// C3; 4 or 8 per lane were slower).
+#ifndef FVV_SCAN_LB
+#define FVV_SCAN_LB 2
+#endif
+#ifndef FVV_SCAN_LB2
+#define FVV_SCAN_LB2 1
+#endif
+
+// 1: (value, flag) in 16 bytes; 2: two 16-byte halves (flag + 12 value bytes each)
 template <typename T>
+struct status_kind {
+  static constexpr int value =
+      sizeof(T) == 8 ? 1 : ((sizeof(T) % 4 == 0 && sizeof(T) <= 24) ? 2 : 0);
+};
+
+template <typename T, int kKind = status_kind<T>::value>
 struct ScanStatus {
   T agg, incl;
   int flag;  // 0 none, 1 aggregate, 2 inclusive prefix
 };
+template <typename T>
+struct __align__(16) ScanStatus<T, 1> {
+  unsigned long long value;  // the aggregate (flag 1) or the inclusive prefix (flag 2)
+  unsigned long long flag;
+};
+template <typename T>
+struct __align__(16) ScanStatus<T, 2> {
+  unsigned half[2][4];  // [h][0] flag, [h][1..3] value words 3h .. 3h+2
+};
+
+template <typename T>
+__device__ __forceinline__ T from_bits(unsigned long long b) {
+  static_assert(sizeof(T) == 8, "packed scan values are 8 bytes");
+  T v;
+  memcpy(&v, &b, 8);
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ unsigned long long to_bits(const T &v) {
+  unsigned long long b;
+  memcpy(&b, &v, 8);
+  return b;
+}
 
 // L2 read of a status value written by another SM (never a stale L1 line)
 template <typename T>
@@ -71,9 +122,9 @@ __device__ __forceinline__ T shfl_xor_value(const T &v, int o) {
 }
 
 template <typename T>
-__device__ __forceinline__ void scan_publish(ScanStatus<T> *st, const T &agg, const T &incl,
+__device__ __forceinline__ void scan_publish(ScanStatus<T, 0> *st, const T &agg, const T &incl,
                                              int flag) {
-  volatile ScanStatus<T> *v = st;
+  volatile ScanStatus<T, 0> *v = st;
   if (flag == 1) {
     st->agg = agg;
   } else {
@@ -81,6 +132,82 @@ __device__ __forceinline__ void scan_publish(ScanStatus<T> *st, const T &agg, co
   }
   __threadfence();
   v->flag = flag;
+}
+template <typename T>
+__device__ __forceinline__ void scan_publish(ScanStatus<T, 1> *st, const T &agg, const T &incl,
+                                             int flag) {
+  const unsigned long long v = to_bits(flag == 1 ? agg : incl), f = (unsigned long long)flag;
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(st), "l"(v), "l"(f) : "memory");
+}
+template <typename T>
+__device__ __forceinline__ void scan_publish(ScanStatus<T, 2> *st, const T &agg, const T &incl,
+                                             int flag) {
+  unsigned w[6] = {0u, 0u, 0u, 0u, 0u, 0u};
+  memcpy(w, flag == 1 ? &agg : &incl, sizeof(T));
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+    asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(&st->half[h][0]),
+                 "r"((unsigned)flag), "r"(w[3 * h]), "r"(w[3 * h + 1]), "r"(w[3 * h + 2])
+                 : "memory");
+}
+
+// K statuses once published: flags (1 or 2) and the matching values (q < 0:
+// before tile 0, an inclusive prefix of zero). Unpacked: all flags first,
+// one fence, then the values.
+template <typename T, int K>
+__device__ __forceinline__ void scan_wait(const ScanStatus<T, 0> *status, const int64_t *q,
+                                          int *fl, T *val) {
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    fl[r] = 2;
+    if (q[r] >= 0) {
+      volatile const ScanStatus<T, 0> *sq = status + q[r];
+      while ((fl[r] = sq->flag) == 0) {
+      }
+    }
+  }
+  __threadfence();
+#pragma unroll
+  for (int r = 0; r < K; ++r)
+    val[r] = q[r] < 0 ? T(0)
+                      : (fl[r] == 2 ? ldcg_value(&status[q[r]].incl) : ldcg_value(&status[q[r]].agg));
+}
+template <typename T, int K>
+__device__ __forceinline__ void scan_wait(const ScanStatus<T, 1> *status, const int64_t *q,
+                                          int *fl, T *val) {
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    unsigned long long v = 0, f = 2;
+    if (q[r] >= 0) {
+      do {
+        asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];"
+                     : "=l"(v), "=l"(f) : "l"(status + q[r]) : "memory");
+      } while (f == 0);
+    }
+    fl[r] = (int)f;
+    val[r] = from_bits<T>(v);
+  }
+}
+template <typename T, int K>
+__device__ __forceinline__ void scan_wait(const ScanStatus<T, 2> *status, const int64_t *q,
+                                          int *fl, T *val) {
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    unsigned a[4] = {2u, 0u, 0u, 0u}, b[4] = {2u, 0u, 0u, 0u};
+    if (q[r] >= 0) {
+      do {
+        asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3])
+                     : "l"(&status[q[r]].half[0][0]) : "memory");
+        asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(b[0]), "=r"(b[1]), "=r"(b[2]), "=r"(b[3])
+                     : "l"(&status[q[r]].half[1][0]) : "memory");
+      } while (a[0] == 0u || a[0] != b[0]);
+    }
+    fl[r] = (int)a[0];
+    const unsigned w[6] = {a[1], a[2], a[3], b[1], b[2], b[3]};
+    memcpy(&val[r], w, sizeof(T));
+  }
 }
 
 template <class F, typename T>
@@ -111,27 +238,34 @@ __global__ void __launch_bounds__(kScanThreads)
     }
     T agg;
     Scan(tmp).ExclusiveSum(v, ex, agg);
-    if (threadIdx.x < 32) {  // warp 0: publish, then look back 32 tiles at a time
+    constexpr int kLookBack = status_kind<T>::value == 1 ? FVV_SCAN_LB
+                              : (status_kind<T>::value == 2 ? FVV_SCAN_LB2 : 1);
+    if (threadIdx.x < 32) {  // warp 0: publish, then look back 32 x kLookBack tiles at a time
       const int lane = threadIdx.x;
       T prefix = T(0);
       if (c == 0) {
         if (lane == 0) scan_publish(status + c, agg, agg, 2);
       } else {
         if (lane == 0) scan_publish(status + c, agg, agg, 1);
-        for (int64_t q0 = c - 1;; q0 -= 32) {
-          const int64_t q = q0 - lane;
-          int fl = 2;  // before tile 0: an inclusive prefix of zero
-          T val = T(0);
-          if (q >= 0) {
-            volatile ScanStatus<T> *sq = status + q;
-            while ((fl = sq->flag) == 0) {
-            }
-            __threadfence();
-            val = fl == 2 ? ldcg_value(&status[q].incl) : ldcg_value(&status[q].agg);
+        for (int64_t q0 = c - 1;; q0 -= 32 * kLookBack) {
+          // lane's tiles q0 - kLookBack lane - r (r = 0 .. kLookBack-1: farther back);
+          // its part stops at its nearest inclusive tile
+          T val[kLookBack];
+          int fl[kLookBack];
+          int64_t q[kLookBack];
+#pragma unroll
+          for (int r = 0; r < kLookBack; ++r) q[r] = q0 - (int64_t)kLookBack * lane - r;
+          scan_wait<T, kLookBack>(status, q, fl, val);
+          T part = T(0);
+          bool has = false;
+#pragma unroll
+          for (int r = 0; r < kLookBack; ++r) {
+            if (!has) part = part + val[r];
+            has = has || fl[r] == 2;
           }
-          const unsigned inc = __ballot_sync(0xffffffffu, fl == 2);
-          const int first = inc ? __ffs(inc) - 1 : 32;  // nearest inclusive tile
-          T part = lane <= first ? val : T(0);
+          const unsigned inc = __ballot_sync(0xffffffffu, has);
+          const int first = inc ? __ffs(inc) - 1 : 32;  // lane holding the nearest inclusive tile
+          if (lane > first) part = T(0);
 #pragma unroll
           for (int o = 16; o >= 1; o >>= 1) part = part + shfl_xor_value(part, o);
           prefix = prefix + part;
