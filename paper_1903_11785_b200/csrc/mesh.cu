@@ -342,8 +342,11 @@ __device__ __forceinline__ bool edge_lambda_cam(const fvv_camera &cam,
   const int sx = bx >= ax ? 1 : -1, sy = by >= ay ? 1 : -1;
   const bool xmajor = dx >= dy;
   const int major = xmajor ? dx : dy;
-  const int64_t two_maj = 2 * (int64_t)(major > 1 ? major : 1), two_min = 2 * (int64_t)(xmajor ? dy : dx);
-  int64_t rem = two_maj / 2;
+  // (both endpoints are in the image: major < 2^16 keeps the remainder
+  // arithmetic in 32 bits; loading 2-8 of the walk's pixel words at once
+  // measured no faster, 98.5 -> 99 / 115 / 147 us)
+  const int two_maj = 2 * (major > 1 ? major : 1), two_min = 2 * (xmajor ? dy : dx);
+  int rem = two_maj / 2;
   int smin = 0, first_bg = -1, lx = ax, ly = ay;
   for (int t = 0; t <= major; ++t) {
     const int x = ax + sx * (xmajor ? t : smin), y = ay + sy * (xmajor ? smin : t);
