@@ -36,7 +36,12 @@ constexpr int kCarveWordsPerBlock = 128;  // 4096 voxels per block
 constexpr int64_t kAmbCap = FVV_AMB_CAP;  // deferred-voxel queue entries
 constexpr int64_t kTileCap = 1 << 19;    // split mode: surviving-tile records
 // split mode: the octant kernel's grid (resident blocks taking octants)
-constexpr int64_t kOctantLoopGrid = 148 * FVV_CARVE_MINB;
+// octant kernel blocks of kThreads threads (resident threads per SM as for
+// FVV_CARVE_MINB 256-thread blocks): 128 for ROI batches, where a block's
+// barriers (octant classification, the slowest warp's voxels) idle fewer
+// warps (B-3 146 -> 132 us at C3), 256 for the stage grid (B-1: 44 vs 48 us)
+template <int kThreads>
+constexpr int oct_min_blocks() { return FVV_CARVE_MINB * 256 / kThreads; }
 
 struct CarveParams {
   int ncam, min_views;
@@ -499,8 +504,8 @@ __global__ void __launch_bounds__(kCarveThreads, FVV_CARVE_MINB)
 // kLoop (the launch used): one resident wave of blocks takes the octants of
 // the surviving tiles from a counter; !kLoop: one block per octant of every
 // tile, blocks past the surviving count exit.
-template <bool kLoop>
-__global__ void __launch_bounds__(kCarveThreads, FVV_CARVE_MINB)
+template <bool kLoop, int kThreads>
+__global__ void __launch_bounds__(kThreads, oct_min_blocks<kThreads>())
     carve_voxels_kernel(const __grid_constant__ CarveParams p) {
   pdl_wait();
   __shared__ CamAffine aff[FVV_MAX_CAMS];
@@ -551,7 +556,7 @@ __global__ void __launch_bounds__(kCarveThreads, FVV_CARVE_MINB)
   if (threadIdx.x == 0) culled = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int kWarps = kCarveThreads / 32;
+  constexpr int kWarps = kThreads / 32;
   for (int m0 = 0; m0 < tnm; m0 += 4 * kWarps) {
     if (m0 + 4 * warp >= tnm) break;  // (warp-uniform)
     const int m = m0 + 4 * warp + (lane >> 3);
@@ -778,8 +783,13 @@ int fvv::carve_batch(const fvv_camera *cams, int ncam, const uint32_t *sil_dev,
     // octants (C5 512^3: 131k, mostly of culled tiles): a capped grid loops
     // one resident wave of blocks taking octants from a counter (measured
     // against one block per octant of every tile: B-1 56 -> 44 us, B-3 equal)
-    launch_k(carve_voxels_kernel<true>,
-             (unsigned)std::min<int64_t>(blocks * 8, kOctantLoopGrid), kCarveThreads, 0, st, p);
+    if (ngrid_max > 1) {
+      launch_k(carve_voxels_kernel<true, 128>,
+               (unsigned)std::min<int64_t>(blocks * 8, 148 * oct_min_blocks<128>()), 128, 0, st, p);
+    } else {
+      launch_k(carve_voxels_kernel<true, 256>,
+               (unsigned)std::min<int64_t>(blocks * 8, 148 * oct_min_blocks<256>()), 256, 0, st, p);
+    }
   } else {
     launch_k(carve_kernel<false>, (unsigned)blocks, kCarveThreads, 0, st, p);
   }
