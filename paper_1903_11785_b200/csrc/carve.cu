@@ -643,10 +643,18 @@ __global__ void __launch_bounds__(kCarveThreads)
   // lanes test different cameras: a shared-memory copy (divergent indexing of
   // the parameter block would serialise the constant cache)
   __shared__ fvv_camera cams[FVV_MAX_CAMS];
-  for (int c = threadIdx.x; c < p.ncam; c += blockDim.x) cams[c] = p.cams[c];
-  __syncthreads();
   int64_t n = (int64_t)__ldcg(p.amb);
   if (n > p.amb_cap) n = p.amb_cap;
+  if (blockIdx.x * (int64_t)blockDim.x >= n) return;  // (block-uniform: no entries here)
+  {  // copied word by word by the whole block (one thread per camera would
+     // serialise ~50 divergent parameter loads per lane)
+    static_assert(sizeof(fvv_camera) % 4 == 0, "cameras are copied in 32-bit words");
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(p.cams);
+    uint32_t *dst = reinterpret_cast<uint32_t *>(cams);
+    for (int e = threadIdx.x; e < p.ncam * (int)(sizeof(fvv_camera) / 4); e += blockDim.x)
+      dst[e] = src[e];
+  }
+  __syncthreads();
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
        q += (int64_t)gridDim.x * blockDim.x) {
     const unsigned long long e = p.amb[1 + 2 * q], mask = p.amb[2 + 2 * q];
