@@ -14,6 +14,34 @@ static std::atomic<long long> g_launches{0};
 
 void note_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+// cudaMemsetAsync as a kernel launched with programmatic serialisation:
+// inside a frame graph a memset node would break the chain of early-launched
+// kernels (each following launch then starts cold). 16-byte stores for the
+// aligned body, bytes for the head and tail.
+__global__ void fill_bytes_kernel(uint8_t *p, size_t n, uint32_t v4) {
+  pdl_wait();
+  size_t head = (16 - ((uintptr_t)p & 15)) & 15;
+  if (head > n) head = n;
+  const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  if (tid < head) p[tid] = (uint8_t)v4;
+  const size_t body = (n - head) / 16;
+  uint4 *q = reinterpret_cast<uint4 *>(p + head);
+  const uint4 vv = make_uint4(v4, v4, v4, v4);
+  for (size_t i = tid; i < body; i += stride) q[i] = vv;
+  const size_t tail = head + body * 16;
+  if (tid < n - tail) p[tail + tid] = (uint8_t)v4;
+}
+
+void fill_async(void *p, int value, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return;
+  const uint32_t v4 = (uint32_t)(uint8_t)value * 0x01010101u;
+  size_t blocks = (bytes / 16 + 255) / 256 + 1;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  launch_k(fill_bytes_kernel, (unsigned)blocks, 256, 0, st, (uint8_t *)p, bytes, v4);
+  note_launches(1);
+}
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char *e = getenv("FVV_PDL");

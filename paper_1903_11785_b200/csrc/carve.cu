@@ -71,31 +71,6 @@ struct CarveParams {
   const CarveGrids *gt;  // the batch's grids (device memory)
 };
 
-// The reference's float64 chain for one voxel (hull.py:83-91), over the
-// cameras in cam_mask (bit c); seen / the result carry the decided rest.
-// `cams` may be a shared-memory copy (lanes index different cameras).
-__device__ __forceinline__ bool carve_exact(const CarveParams &p, const fvv_camera *cams,
-                                            const fvv_grid &G, int64_t l,
-                                            unsigned long long cam_mask, int seen) {
-  const int64_t nx = G.dims[0], ny = G.dims[1];
-  const int64_t nvox = nx * ny * G.dims[2];
-  const int64_t i = l % nx, j = (l / nx) % ny, k = l / (nx * ny);
-  double x, y, z;
-  voxel_center(G, i, j, k, x, y, z);
-  const bool gemv = (nvox % kCarveChunk == 1) && l == nvox - 1;  // 1-row BLAS chunk
-  while (cam_mask) {
-    const int c = __ffsll((long long)cam_mask) - 1;
-    cam_mask &= cam_mask - 1;
-    double u, v, zc;
-    if (!project_exact(cams[c], x, y, z, true, gemv, u, v, zc)) continue;
-    ++seen;
-    if (!sil_bit(p.sil + p.sil_off[c], sil_stride_words(cams[c].width), (int)rint(u),
-                 (int)rint(v)))
-      return false;
-  }
-  return seen >= p.min_views;
-}
-
 // (i, j, k) of linear voxel index l (F order), 32-bit when the grid allows.
 __device__ __forceinline__ void voxel_ijk(int64_t l, int64_t nx, int64_t ny, bool small,
                                           int64_t &i, int64_t &j, int64_t &k) {
@@ -110,6 +85,32 @@ __device__ __forceinline__ void voxel_ijk(int64_t l, int64_t nx, int64_t ny, boo
     j = (l / nx) % ny;
     k = l / (nx * ny);
   }
+}
+
+// The reference's float64 chain for one voxel (hull.py:83-91), over the
+// cameras in cam_mask (bit c); seen / the result carry the decided rest.
+// `cams` may be a shared-memory copy (lanes index different cameras).
+__device__ __forceinline__ bool carve_exact(const CarveParams &p, const fvv_camera *cams,
+                                            const fvv_grid &G, int64_t l,
+                                            unsigned long long cam_mask, int seen) {
+  const int64_t nx = G.dims[0], ny = G.dims[1];
+  const int64_t nvox = nx * ny * G.dims[2];
+  int64_t i, j, k;
+  voxel_ijk(l, nx, ny, nvox <= 0xffffffffll, i, j, k);
+  double x, y, z;
+  voxel_center(G, i, j, k, x, y, z);
+  const bool gemv = (nvox % kCarveChunk == 1) && l == nvox - 1;  // 1-row BLAS chunk
+  while (cam_mask) {
+    const int c = __ffsll((long long)cam_mask) - 1;
+    cam_mask &= cam_mask - 1;
+    double u, v, zc;
+    if (!project_exact(cams[c], x, y, z, true, gemv, u, v, zc)) continue;
+    ++seen;
+    if (!sil_bit(p.sil + p.sil_off[c], sil_stride_words(cams[c].width), (int)rint(u),
+                 (int)rint(v)))
+      return false;
+  }
+  return seen >= p.min_views;
 }
 
 // Cameras order[t0 .. t1) against one voxel in FP32: sets off on a
@@ -717,7 +718,7 @@ int fvv::carve_batch(const fvv_camera *cams, int ncam, const uint32_t *sil_dev,
                      int64_t *count_dev, void *workspace, size_t ws_bytes, cudaStream_t st,
                      bool reuse_cells) {
   if (ngrid_max == 0 || blocks == 0) {
-    if (count_dev && ngrid_max) cudaMemsetAsync(count_dev, 0, sizeof(int64_t) * ngrid_max, st);
+    if (count_dev && ngrid_max) fill_async(count_dev, 0, sizeof(int64_t) * ngrid_max, st);
     return cuda_check("fvv_carve");
   }
   static thread_local CarveParams p;  // ~13 KB: keep it off the host stack

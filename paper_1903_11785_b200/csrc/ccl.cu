@@ -420,7 +420,7 @@ int fvv_ccl26(const uint32_t *occ_dev, const fvv_grid *grid, void *ws_dev, size_
   }
   cudaStream_t st = (cudaStream_t)stream;
   CclWs w = ccl_layout(ws_dev, grid->dims);
-  cudaMemsetAsync(w.counts, 0, 4 * sizeof(int64_t), st);
+  fill_async(w.counts, 0, 4 * sizeof(int64_t), st);
   WordRank wr{occ_dev, w.word_prefix, w.on_list, w.parent, w.words, nvox};
   onepass_scan(wr, nullptr, w.words, w.words, (void *)w.sums, w.counts + 0, st);
   launch_k(ccl_union_kernel, kCclGrid, 256, 0, st, occ_dev, w, nx, ny, nz);
@@ -446,7 +446,7 @@ int fvv_ccl_labels(const fvv_grid *grid, const void *ws_dev, int32_t *labels_dev
   const int64_t nvox = grid->dims[0] * grid->dims[1] * grid->dims[2];
   CclWs w = ccl_layout((void *)ws_dev, grid->dims);
   cudaStream_t st = (cudaStream_t)stream;
-  cudaMemsetAsync(labels_dev, 0, sizeof(int32_t) * nvox, st);
+  fill_async(labels_dev, 0, sizeof(int32_t) * nvox, st);
   launch_k(ccl_expand_kernel, kCclGrid, 256, 0, st, w, labels_dev);
   note_launches(1);
   return cuda_check("fvv_ccl_labels");
@@ -457,9 +457,9 @@ int fvv_filter_labels(const fvv_grid *grid, const void *ws_dev, const uint8_t *k
   const int64_t nvox = grid->dims[0] * grid->dims[1] * grid->dims[2];
   CclWs w = ccl_layout((void *)ws_dev, grid->dims);
   cudaStream_t st = (cudaStream_t)stream;
-  if (labels_dev) cudaMemsetAsync(labels_dev, 0, sizeof(int32_t) * nvox, st);
-  if (occ_dev) cudaMemsetAsync(occ_dev, 0, sizeof(uint32_t) * ((nvox + 31) / 32), st);
-  if (kept_dev) cudaMemsetAsync(kept_dev, 0, sizeof(int64_t), st);
+  if (labels_dev) fill_async(labels_dev, 0, sizeof(int32_t) * nvox, st);
+  if (occ_dev) fill_async(occ_dev, 0, sizeof(uint32_t) * ((nvox + 31) / 32), st);
+  if (kept_dev) fill_async(kept_dev, 0, sizeof(int64_t), st);
   launch_k(ccl_filter_kernel, kCclGrid, 256, 0, st, w, keep_dev, labels_dev, occ_dev, kept_dev);
   note_launches(1);
   return cuda_check("fvv_filter_labels");
@@ -469,7 +469,7 @@ int fvv_filter_dense(const int32_t *labels_in_dev, int64_t nvox, const uint8_t *
                      int64_t nkeep, int32_t *labels_dev, uint32_t *occ_dev, int64_t *kept_dev,
                      void *stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  if (kept_dev) cudaMemsetAsync(kept_dev, 0, sizeof(int64_t), st);
+  if (kept_dev) fill_async(kept_dev, 0, sizeof(int64_t), st);
   launch_k(dense_filter_kernel, kCclGrid, 256, 0, st, labels_in_dev, nvox, nkeep, keep_dev, labels_dev,
                                                 occ_dev, kept_dev);
   note_launches(1);

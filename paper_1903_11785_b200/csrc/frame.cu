@@ -648,7 +648,7 @@ static int enqueue_tail(fvv_frame *f, const fvv_camera *virt, const int32_t *ran
   }
   stage_mark(f, 5, st);
   FVV_TRY(6, f->vis.ensure(4 * (size_t)ncam * f->vis_stride));
-  cudaMemsetAsync(f->vis.p, 0, 4 * (size_t)ncam * f->vis_stride, st);
+  fill_async(f->vis.p, 0, 4 * (size_t)ncam * f->vis_stride, st);
   // (with a colour pass, the triangle sources of render.py:35-43 come out of
   // the same launch)
   std::vector<int32_t> rank_id(ncam);
@@ -678,10 +678,10 @@ static int enqueue_tail(fvv_frame *f, const fvv_camera *virt, const int32_t *ran
                                          f->source.as<int32_t>(), f->covered.as<uint8_t>(),
                                          f->code.as<int8_t>(), f->rcounts.as<int64_t>(), st));
     } else {
-      cudaMemsetAsync(f->code.p, 0xfe, (size_t)np, st);  // -2: nothing covered
-      cudaMemsetAsync(f->color.p, 0, 3 * (size_t)np, st);
-      cudaMemsetAsync(f->source.p, 0xff, 4 * (size_t)np, st);
-      cudaMemsetAsync(f->covered.p, 0, (size_t)np, st);
+      fill_async(f->code.p, 0xfe, (size_t)np, st);  // -2: nothing covered
+      fill_async(f->color.p, 0, 3 * (size_t)np, st);
+      fill_async(f->source.p, 0xff, 4 * (size_t)np, st);
+      fill_async(f->covered.p, 0, (size_t)np, st);
     }
   }
   stage_mark(f, 7, st);
@@ -861,7 +861,7 @@ static int run_host_planned(fvv_frame *f, const uint8_t *masks_dev, const fvv_ca
   if (nroi > 0)
     launch_k(add_count_kernel, 1, 32, 0, st, ntri_dev, f->mesh_totals.as<int64_t>() + 2, t_before);
   else
-    cudaMemsetAsync(ntri_dev, 0, 8, st);
+    fill_async(ntri_dev, 0, 8, st);
   const int64_t nt_ub = f->nt;
   f->vis_stride = (nt_ub + 31) / 32 > 0 ? (nt_ub + 31) / 32 : 1;
 

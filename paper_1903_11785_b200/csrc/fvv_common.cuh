@@ -29,6 +29,9 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 
 bool pdl_enabled();
 
+// cudaMemsetAsync(p, value, bytes, st) as a programmatic-dependent kernel (api.cu)
+void fill_async(void *p, int value, size_t bytes, cudaStream_t st);
+
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                      Args &&...args) {

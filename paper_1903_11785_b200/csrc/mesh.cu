@@ -864,7 +864,7 @@ int fvv::mesh_prepare_batch(const MeshGrids *G_dev, int64_t tw_cap, int ngrid_ma
   }
   MeshBufs B = bufs_from(ws_dev, L);
   B.occ = occ_dev;
-  cudaMemsetAsync(B.totals, 0, 32, st);
+  fill_async(B.totals, 0, 32, st);
   if (tw_cap > 0) {
     launch_k(mesh_transpose_kernel, kMeshGrid, 256, 0, st, G_dev, B);
     note_launches(1);
@@ -952,7 +952,7 @@ int fvv::mesh_emit_batch(const fvv_camera *cams_by_id, int ncam, const uint32_t 
     TriScan ts{B.cell_mask, B.cprefix};
     onepass_scan(ts, B.totals + 3, 0, cap_s, (void *)cell_sums, d_total, st);
   } else {
-    cudaMemsetAsync(d_total, 0, sizeof(Slot5), st);
+    fill_async(d_total, 0, sizeof(Slot5), st);
   }
   launch_k(mesh_slot_bases_kernel, 1, 32, 0, st, G_dev, B, d_total);
   if (cap_s > 0) launch_k(mesh_emit_kernel, kMeshGrid, 256, 0, st, G_dev, B);
@@ -1034,7 +1034,7 @@ int fvv_edge_isovalues(const fvv_camera *cams_by_id, int ncam, const uint32_t *s
     return FVV_E_LIMIT;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  cudaMemsetAsync(stats_dev, 0, 2 * sizeof(int64_t), st);
+  fill_async(stats_dev, 0, 2 * sizeof(int64_t), st);
   if (n <= 0) return cuda_check("fvv_edge_isovalues");
   static thread_local MeshCams h_cams;
   memset(&h_cams, 0, sizeof(h_cams));

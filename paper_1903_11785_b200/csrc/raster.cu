@@ -1141,7 +1141,7 @@ static int rasterize_impl(const fvv_camera *cams, int ncam, const double *verts_
     set_error("fvv_rasterize_tracked: planes must be contiguous");
     return FVV_E_ARG;
   }
-  if (dirty && full_reset) cudaMemsetAsync(dirty, 0, (size_t)((total_px + 31) >> 5), st);
+  if (dirty && full_reset) fill_async(dirty, 0, (size_t)((total_px + 31) >> 5), st);
   const bool tracked = dirty && !full_reset;
   // contiguous planes: the fill (or tracked reset) rides in the
   // vertex-projection launch (raster_prep_kernel); otherwise fill here
@@ -1153,7 +1153,7 @@ static int rasterize_impl(const fvv_camera *cams, int ncam, const double *verts_
                                                n, 0x7ff0000000000000ull);
       note_launches(1);
     }
-    if (tri_id_dev && !tracked) cudaMemsetAsync(tri_id_dev + plane_off[c], 0xff, 4 * n, st);
+    if (tri_id_dev && !tracked) fill_async(tri_id_dev + plane_off[c], 0xff, 4 * n, st);
   }
   const bool work = nt > 0 && nv > 0;
   const RasterLayout L = raster_layout(nv, nt, ncam);
@@ -1211,7 +1211,7 @@ static int rasterize_impl(const fvv_camera *cams, int ncam, const double *verts_
   A.hits = hits ? (uint4 *)(ws + L.hits) : nullptr;
   A.hit_count = (unsigned long long *)(ws + 16);
   A.hit_cap = L.hit_cap;
-  cudaMemsetAsync(ws, 0, 32, st);  // big-queue counter, overflow flag, hit count
+  fill_async(ws, 0, 32, st);  // big-queue counter, overflow flag, hit count
   launch_k(raster_filter_kernel, (unsigned)fs.bx, 256, 0, st, C, A);
   note_launches(1);
   // pass 0: depth (RED.MIN of the depth bits); ids wanted: the lowest
@@ -1386,7 +1386,7 @@ int fvv_render_count(const fvv_camera *rig, int ncam, const fvv_camera *virt,
                        nullptr, nullptr, nullptr, nullptr, counts_dev);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  cudaMemsetAsync(counts_dev, 0, sizeof(int64_t) * (1 + ncam), st);
+  fill_async(counts_dev, 0, sizeof(int64_t) * (1 + ncam), st);
   launch_k(render_count_kernel, kRasterGrid, 256, 0, st, A);
   note_launches(1);
   return cuda_check("fvv_render_count");

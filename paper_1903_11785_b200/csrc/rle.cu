@@ -59,7 +59,7 @@ int fvv_rle_transitions(const uint32_t *occ_dev, int64_t nvox, int64_t *pos_dev,
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t words = (nvox + 31) / 32;
   if (words == 0) {
-    cudaMemsetAsync(count_dev, 0, sizeof(int64_t), st);
+    fill_async(count_dev, 0, sizeof(int64_t), st);
     return cuda_check("fvv_rle_transitions");
   }
   RleTransitions f{occ_dev, words, nvox, pos_dev};

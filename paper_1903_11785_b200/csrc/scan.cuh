@@ -305,7 +305,7 @@ template <class F, typename T>
 inline void onepass_scan(const F &f, const int64_t *n_dev, int64_t n_host, int64_t n_max,
                          void *ws, T *total, cudaStream_t st) {
   const size_t sbytes = onepass_status_bytes<T>(n_max);
-  cudaMemsetAsync(ws, 0, sbytes + 64, st);
+  fill_async(ws, 0, sbytes + 64, st);
   launch_k(onepass_scan_kernel<F, T>, kScanGrid, kScanThreads, 0, st, f, n_dev, n_host, (ScanStatus<T> *)ws, (unsigned long long *)((char *)ws + sbytes),
       total);
   note_launches(1);
