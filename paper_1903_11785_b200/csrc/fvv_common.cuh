@@ -141,8 +141,20 @@ __device__ __forceinline__ float recip32(float z) {
   return fmaf(r, fmaf(-z, r, 1.0f), r);
 }
 
-__device__ __forceinline__ bool project_rint32(const fvv_camera &c, double x, double y, double z,
-                                               bool gemv, double &iu, double &iv, double &zc) {
+// The FP32 constants of project_rint32 for one camera (once per block).
+struct CamF32 {
+  float fx, fy, cx, cy, sk;
+  int width, height;
+};
+__device__ __forceinline__ CamF32 cam_f32(const fvv_camera &c) {
+  return CamF32{(float)c.fx, (float)c.fy, (float)c.cx, (float)c.cy, (float)c.skew, c.width,
+                c.height};
+}
+
+// Returns in_frustum; (ix, iy) = the rounded pixel when in frustum.
+__device__ __forceinline__ bool project_rint32(const fvv_camera &c, const CamF32 &f, double x,
+                                               double y, double z, bool gemv, int &ix, int &iy,
+                                               double &zc) {
   double X, Y, Z;
   world_to_cam(c, x, y, z, gemv, X, Y, Z);
   zc = Z;
@@ -151,26 +163,28 @@ __device__ __forceinline__ bool project_rint32(const fvv_camera &c, double x, do
   bool ok = Zf > 1e-30f;
   const float r = recip32(ok ? Zf : 1.0f);
   const float xn = Xf * r, yn = Yf * r;
-  const float fx = (float)c.fx, fy = (float)c.fy, cx = (float)c.cx, cy = (float)c.cy,
-              sk = (float)c.skew;
-  const float syn = sk * yn;
-  const float su = fx * (xn + syn), sv = fy * yn;
-  const float u = su + cx, v = sv + cy;
-  const float eu = 0x1p-20f * (fabsf(fx) * (fabsf(xn) + fabsf(syn)) + fabsf(cx) + fabsf(u) + 1.0f);
-  const float ev = 0x1p-20f * (fabsf(sv) + fabsf(cy) + fabsf(v) + 1.0f);
+  const float syn = f.sk * yn;
+  const float su = f.fx * (xn + syn), sv = f.fy * yn;
+  const float u = su + f.cx, v = sv + f.cy;
+  const float eu = 0x1p-20f * (fabsf(f.fx) * (fabsf(xn) + fabsf(syn)) + fabsf(f.cx) + fabsf(u) + 1.0f);
+  const float ev = 0x1p-20f * (fabsf(sv) + fabsf(f.cy) + fabsf(v) + 1.0f);
   const float ru = rintf(u), rv = rintf(v);
   ok = ok && fabsf(u) < 4194304.0f && fabsf(v) < 4194304.0f && fabsf(u - ru) < 0.5f - eu &&
        fabsf(v - rv) < 0.5f - ev;
-  if (ok) {
-    iu = ru;
-    iv = rv;
-  } else {  // the float64 chain (project_exact, no distortion)
-    const double xe = X / Z, ye = Y / Z;
-    iu = rint(c.fx * (xe + c.skew * ye) + c.cx);
-    iv = rint(c.fy * ye + c.cy);
+  if (ok) {  // |ru|, |rv| < 2^22
+    ix = (int)ru;
+    iy = (int)rv;
+    return ix >= 0 && ix < f.width && iy >= 0 && iy < f.height;
   }
-  return (iu >= 0.0) && (iu <= (double)(c.width - 1)) && (iv >= 0.0) &&
-         (iv <= (double)(c.height - 1));
+  // the float64 chain (project_exact, no distortion)
+  const double xe = X / Z, ye = Y / Z;
+  const double iu = rint(c.fx * (xe + c.skew * ye) + c.cx), iv = rint(c.fy * ye + c.cy);
+  if (!((iu >= 0.0) && (iu <= (double)(c.width - 1)) && (iv >= 0.0) &&
+        (iv <= (double)(c.height - 1))))
+    return false;
+  ix = (int)iu;
+  iy = (int)iv;
+  return true;
 }
 
 // voxels.py:52-56 voxel centre.

@@ -816,6 +816,9 @@ __global__ void classify_kernel(const __grid_constant__ RasterCams C,
   // per warp: the centroid (three divisions) is computed once and projected
   // into every camera, instead of once per (camera, triangle); the pixel
   // rounding is certified in FP32 (project_rint32)
+  __shared__ CamF32 cf[FVV_MAX_CAMS];
+  for (int c = threadIdx.x; c < C.ncam; c += blockDim.x) cf[c] = cam_f32(C.cams[c]);
+  __syncthreads();
   const int64_t nt = device_count(A.nt_dev, A.nt);
   const bool gemv = nt == 1;
   const int lane = threadIdx.x & 31;
@@ -836,10 +839,11 @@ __global__ void classify_kernel(const __grid_constant__ RasterCams C,
     for (int c = 0; c < C.ncam; ++c) {
       bool vis = false;
       if (t < nt) {
-        const fvv_camera &cam = C.cams[c];
-        double iu, iv, z;
-        if (project_rint32(cam, mx, my, mz, gemv, iu, iv, z)) {
-          const int64_t p = (int64_t)iv * cam.width + (int64_t)iu;
+        const CamF32 &f = cf[c];
+        int ix, iy;
+        double z;
+        if (project_rint32(C.cams[c], f, mx, my, mz, gemv, ix, iy, z)) {
+          const int64_t p = (int64_t)iy * f.width + ix;
           vis = (z - __ldg(A.depth + C.depth_off[c] + p)) <= A.t_v;
         }
       }
