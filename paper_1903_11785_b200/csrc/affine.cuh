@@ -34,7 +34,8 @@ struct __align__(16) CamAffine {
   float su, sv, sz, ez;    // magnitude sums at the far corner; |Z32 - Z| bound
   float zsafe, ulim, bu, bv;  // E_u = (|u|+1)(A rz + C) + bu rz + 2^-20
   float A;                 // 8 eps sz
-  int w, h, pad0;
+  int w, h;
+  int sil_off;             // word offset of the camera's silhouette plane (carve_affine)
 };
 
 constexpr float kEps = 5.9604645e-8f;  // 2^-24

@@ -316,8 +316,10 @@ __device__ __forceinline__ void carve_cells(const CarveParams &p, int bid, int n
 __device__ __forceinline__ void carve_affine(const CarveParams &p, CamAffine *out, int bid,
                                              int nblocks) {
   const int n = p.gt->ngrid * p.ncam;
-  for (int e = bid * blockDim.x + threadIdx.x; e < n; e += nblocks * blockDim.x)
+  for (int e = bid * blockDim.x + threadIdx.x; e < n; e += nblocks * blockDim.x) {
     cam_affine(p.cams[e % p.ncam], p.gt->grids[e / p.ncam], out[e]);
+    out[e].sil_off = (int)p.sil_off[e % p.ncam];  // (< 2^31 words: checked in carve_batch)
+  }
 }
 
 struct __align__(16) TileWork {
@@ -360,7 +362,8 @@ __device__ __forceinline__ int carve_voxels(const CarveParams &p, const CamAffin
         continue;
       }
       ++seen;
-      if (!sil_bit(p.sil + p.sil_off[c], p.sil_stride[c], px, py)) {
+      const CamAffine &a = aff[c];
+      if (!sil_bit(p.sil + a.sil_off, (a.w + 31) >> 5, px, py)) {
         off = true;
         break;
       }
@@ -770,6 +773,11 @@ int fvv::carve_batch(const fvv_camera *cams, int ncam, const uint32_t *sil_dev,
   for (int c = 0; c < ncam; ++c) {
     p.cams[c] = cams[c];
     p.sil_off[c] = sil_word_off[c];
+    if (sil_word_off[c] < 0 || sil_word_off[c] > 0x7fffffffll) {
+      set_error("fvv_carve: silhouette plane %d at word %lld (the carve addresses < 2^31 words)",
+                c, (long long)sil_word_off[c]);
+      return FVV_E_LIMIT;
+    }
     p.sil_stride[c] = sil_stride_words(cams[c].width);
   }
   p.tile_log2 = tile_log2;
