@@ -113,28 +113,6 @@ __device__ __forceinline__ bool carve_exact(const CarveParams &p, const fvv_came
   return seen >= p.min_views;
 }
 
-// Cameras order[t0 .. t1) against one voxel in FP32: sets off on a
-// background view, counts in-frustum views, flags undecided tests.
-__device__ __forceinline__ void test_cams(const CarveParams &p, const CamAffine *aff, int t0,
-                                          int t1, float fi, float fj, float fk, int &seen,
-                                          bool &off, bool &amb) {
-  for (int t = t0; t < t1; ++t) {
-    const int c = p.order[t];
-    int px, py;
-    const int st = classify32(aff[c], fi, fj, fk, px, py);
-    if (st == kOut) continue;
-    if (st == kAmb) {
-      amb = true;
-      continue;
-    }
-    ++seen;
-    if (!sil_bit(p.sil + p.sil_off[c], p.sil_stride[c], px, py)) {
-      off = true;  // hull.py:91: one background view removes the voxel
-      return;
-    }
-  }
-}
-
 // A voxel no FP32 camera rejected: ON/OFF from the counts, or, when some
 // tests were undecided (amb_mask, bit c), the float64 chain for those
 // cameras (deferred to carve_exact_kernel; queue entries are
