@@ -95,9 +95,12 @@ __device__ __forceinline__ void cam_affine(const fvv_camera &c, const fvv_grid &
 
 enum : int { kOut = 0, kIn = 1, kAmb = 2 };
 
-// 1/z to ~1 ulp: MUFU.RCP (<= 2 ulp) refined by one Newton step.
+// 1/z to ~1 ulp: MUFU.RCP (<= 2 ulp) refined by one Newton step. Callers
+// pass z >= ez >= 1e-6 (or 1): a normal float, so the flush-to-zero
+// approximation is the plain one without __fdividef's range handling.
 __device__ __forceinline__ float recip(float z) {
-  const float r = __fdividef(1.0f, z);
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(z));
   return fmaf(r, fmaf(-z, r, 1.0f), r);
 }
 
