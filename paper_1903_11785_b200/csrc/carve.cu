@@ -340,8 +340,10 @@ __device__ __forceinline__ int carve_voxels(const CarveParams &p, const CamAffin
         continue;
       }
       ++seen;
-      const CamAffine &a = aff[c];
-      if (!sil_bit(p.sil + a.sil_off, (a.w + 31) >> 5, px, py)) {
+      const CamAffine &a = aff[c];  // (32-bit word index: planes < 2^31 words)
+      const uint32_t wi = (uint32_t)a.sil_off + (uint32_t)py * (uint32_t)((a.w + 31) >> 5) +
+                          ((uint32_t)px >> 5);
+      if (!((__ldg(p.sil + wi) >> (px & 31)) & 1u)) {
         off = true;
         break;
       }
