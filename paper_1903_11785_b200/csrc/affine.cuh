@@ -36,6 +36,8 @@ struct __align__(16) CamAffine {
   float A;                 // 8 eps sz
   int w, h;
   int sil_off;             // word offset of the camera's silhouette plane (carve_affine)
+  int sil_stride;          // its words per row
+  int pad[3];
 };
 
 constexpr float kEps = 5.9604645e-8f;  // 2^-24

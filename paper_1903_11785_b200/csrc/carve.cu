@@ -297,6 +297,7 @@ __device__ __forceinline__ void carve_affine(const CarveParams &p, CamAffine *ou
   for (int e = bid * blockDim.x + threadIdx.x; e < n; e += nblocks * blockDim.x) {
     cam_affine(p.cams[e % p.ncam], p.gt->grids[e / p.ncam], out[e]);
     out[e].sil_off = (int)p.sil_off[e % p.ncam];  // (< 2^31 words: checked in carve_batch)
+    out[e].sil_stride = p.sil_stride[e % p.ncam];
   }
 }
 
@@ -341,7 +342,7 @@ __device__ __forceinline__ int carve_voxels(const CarveParams &p, const CamAffin
       }
       ++seen;
       const CamAffine &a = aff[c];  // (32-bit word index: planes < 2^31 words)
-      const uint32_t wi = (uint32_t)a.sil_off + (uint32_t)py * (uint32_t)((a.w + 31) >> 5) +
+      const uint32_t wi = (uint32_t)a.sil_off + (uint32_t)py * (uint32_t)a.sil_stride +
                           ((uint32_t)px >> 5);
       if (!((__ldg(p.sil + wi) >> (px & 31)) & 1u)) {
         off = true;
