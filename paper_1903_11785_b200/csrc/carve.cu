@@ -224,8 +224,8 @@ __device__ int tile_camera(const CarveParams &p, const CamAffine *aff, int c, in
       }
     }
   } else if (query) {
-    const uint32_t *plane = p.sil + p.sil_off[c];
-    const int stride = p.sil_stride[c];
+    const uint32_t *plane = p.sil + aff[c].sil_off;
+    const int stride = aff[c].sil_stride;
     const int w0 = x0 >> 5, w1 = x1 >> 5;
     const uint32_t mlo = 0xffffffffu << (x0 & 31), mhi = 0xffffffffu >> (31 - (x1 & 31));
     // rows g8, g8 + 8, ...; four rows' words in flight per step
