@@ -23,6 +23,7 @@
 // Integer-only and order independent; results are bit-identical to the
 // reference for every launch configuration (its block_dims independence,
 // tests/test_hull.py:159-168, holds trivially).
+#include <cooperative_groups.h>
 #include <cstring>
 
 #include "scan.cuh"
@@ -42,6 +43,8 @@ struct CclWs {
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
+constexpr int kMaxFusedGrid = 4096;  // blocks of ccl_fused_kernel (sums capacity)
+
 // Most components a 26-connected grid can hold: one per 2x2x2 block.
 static int64_t max_components(const int64_t *dims) {
   return ((dims[0] + 1) / 2) * ((dims[1] + 1) / 2) * ((dims[2] + 1) / 2);
@@ -56,8 +59,10 @@ static CclWs ccl_layout(void *base, const int64_t *dims) {
   w.comp_cap = max_components(dims);
   w.counts = (int64_t *)p;  // (first: the frame executor reads n_on / ncomp here in place)
   p += align256(4 * sizeof(int64_t));
-  w.sums = (int64_t *)p;
-  p += align256(onepass_bytes<int64_t>(nvox > w.words ? nvox : w.words));
+  w.sums = (int64_t *)p;  // scan statuses, or the fused kernel's 2 x grid block sums
+  const size_t scan_ws = onepass_bytes<int64_t>(nvox > w.words ? nvox : w.words);
+  const size_t fused_ws = 2 * sizeof(int64_t) * kMaxFusedGrid;
+  p += align256(scan_ws > fused_ws ? scan_ws : fused_ws);
   w.word_prefix = (int32_t *)p;
   p += align256(sizeof(int32_t) * w.words);
   w.on_list = (int32_t *)p;
@@ -398,6 +403,235 @@ __global__ void dense_filter_kernel(const int32_t *__restrict__ in, int64_t nvox
 
 constexpr int kCclGrid = 148 * 8;
 
+// ---- all of B-2 in one cooperative launch -----------------------------------
+// The separate launches above are latency chains over a few thousand ON
+// voxels (C3: ~12k in a 10M-voxel stage grid): seven launches whose ramps
+// and drains dominate. Here one co-resident grid runs the same steps with
+// grid-wide barriers in between, in the same order and with the same
+// integer operations, so the numbering is unchanged: rank scan (block
+// ranges of words, block sums, grid barrier, block prefixes), union over
+// runs, root scan over ranks, per-component stats, component table. Values
+// written in one step are read in later ones through L2 (ld.cg), never
+// through a possibly stale L1 line.
+constexpr int kFusedThreads = 256;
+
+// exclusive prefix of this block's `mine` over blocks 0 .. blockIdx.x - 1,
+// from the per-block sums written before the last grid barrier
+__device__ __forceinline__ int64_t block_offset(const int64_t *sums, int64_t *total) {
+  __shared__ int64_t part[kFusedThreads / 32];
+  int64_t acc = 0, all = 0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+    const int64_t v = __ldcg(sums + b);
+    if (b < (int)blockIdx.x) acc += v;
+    all += v;
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    all += __shfl_xor_sync(0xffffffffu, all, o);
+  }
+  __shared__ int64_t part_all[kFusedThreads / 32];
+  if ((threadIdx.x & 31) == 0) {
+    part[threadIdx.x >> 5] = acc;
+    part_all[threadIdx.x >> 5] = all;
+  }
+  __syncthreads();
+  int64_t off = 0, tot = 0;
+  for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+    off += part[k];
+    tot += part_all[k];
+  }
+  __syncthreads();
+  *total = tot;
+  return off;
+}
+
+__global__ void __launch_bounds__(kFusedThreads)
+    ccl_fused_kernel(const uint32_t *__restrict__ occ, CclWs w, int64_t nx, int64_t ny, int64_t nz,
+                     fvv_component *out, int64_t cap) {
+  namespace cg = cooperative_groups;
+  pdl_wait();
+  cg::grid_group grid = cg::this_grid();
+  using Scan = cub::BlockScan<int, kFusedThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int64_t s_run;
+  const int G = (int)gridDim.x, b = (int)blockIdx.x;
+  const int64_t gtid = b * (int64_t)blockDim.x + threadIdx.x, gstride = (int64_t)G * blockDim.x;
+  const WordRank wr{occ, w.word_prefix, w.on_list, w.parent, w.words, w.nvox};
+
+  // 1. ranks: block b owns words [w0, w1)
+  const int64_t w0 = w.words * b / G, w1 = w.words * (b + 1) / G;
+  {
+    int64_t mine = 0;
+    for (int64_t q = w0 + threadIdx.x; q < w1; q += blockDim.x) mine += __popc(wr.word(q));
+    mine = __reduce_add_sync(0xffffffffu, (unsigned)mine);
+    __shared__ int64_t bsum;
+    if (threadIdx.x == 0) bsum = 0;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) atomicAdd((unsigned long long *)&bsum, (unsigned long long)mine);
+    __syncthreads();
+    if (threadIdx.x == 0) w.sums[b] = bsum;
+  }
+  grid.sync();
+  {
+    int64_t n_on;
+    const int64_t off = block_offset(w.sums, &n_on);
+    if (b == 0 && threadIdx.x == 0) w.counts[0] = n_on;
+    if (threadIdx.x == 0) s_run = off;
+    __syncthreads();
+    for (int64_t c0 = w0; c0 < w1; c0 += blockDim.x) {
+      const int64_t q = c0 + threadIdx.x;
+      const uint32_t v = q < w1 ? wr.word(q) : 0u;
+      int ex, agg;
+      Scan(tmp).ExclusiveSum((int)__popc(v), ex, agg);
+      if (q < w1) wr.emit(q, s_run + ex, v);
+      __syncthreads();
+      if (threadIdx.x == 0) s_run += agg;
+      __syncthreads();
+    }
+  }
+  grid.sync();
+  const int64_t n_on = __ldcg(w.counts);
+
+  // 2. union over runs (ccl_union_kernel's step, values through L2)
+  {
+    const uint32_t ux = (uint32_t)nx, uy = (uint32_t)ny;
+    const int djs[4] = {-1, -1, 0, 1}, dks[4] = {0, -1, -1, -1};
+    for (int64_t e = gtid; e < 4 * n_on; e += gstride) {
+      const int64_t r = e >> 2;
+      const int n = (int)(e & 3);
+      const uint32_t l = (uint32_t)__ldcg(w.on_list + r);
+      const uint32_t q = l / ux, k = q / uy;
+      const uint32_t i = l - q * ux, j = q - k * uy;
+      const int64_t row0 = (int64_t)l - i;
+      const int64_t first = run_first(occ, row0, l);
+      if (first != (int64_t)l) {
+        if (n == 0) __stcg(w.parent + r, (int32_t)(r - ((int64_t)l - first)));
+        continue;
+      }
+      const int64_t jj = (int64_t)j + djs[n], kk = (int64_t)k + dks[n];
+      if (jj < 0 || jj >= ny || kk < 0) continue;
+      const int64_t last = run_last(occ, row0 + nx, l);
+      const int64_t a = i > 0 ? i - 1 : 0, i1 = last - row0, bb = i1 + 1 < nx ? i1 + 1 : nx - 1;
+      const int64_t nrow = nx * (jj + ny * kk);
+      int64_t p = nrow + a;
+      const int64_t pe = nrow + bb;
+      while (p <= pe) {
+        const int64_t s = next_on(occ, p, pe);
+        if (s < 0) break;
+        const int64_t sf = run_first(occ, nrow, s);
+        const uint32_t wv = __ldg(occ + (sf >> 5));
+        const int32_t rs = __ldcg(w.word_prefix + (sf >> 5)) + __popc(wv & ((1u << (sf & 31)) - 1u));
+        uf_unite(w.parent, (int32_t)r, rs);
+        p = run_last(occ, nrow + nx, s) + 2;
+      }
+    }
+  }
+  grid.sync();
+
+  // 3. root labels: block b owns ranks [r0, r1)
+  const int64_t r0 = n_on * b / G, r1 = n_on * (b + 1) / G;
+  {
+    int64_t mine = 0;
+    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) mine += __ldcg(w.parent + r) == (int32_t)r;
+    mine = __reduce_add_sync(0xffffffffu, (unsigned)mine);
+    __shared__ int64_t bsum2;
+    if (threadIdx.x == 0) bsum2 = 0;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) atomicAdd((unsigned long long *)&bsum2, (unsigned long long)mine);
+    __syncthreads();
+    if (threadIdx.x == 0) w.sums[G + b] = bsum2;
+  }
+  grid.sync();
+  {
+    int64_t ncomp;
+    const int64_t off = block_offset(w.sums + G, &ncomp);
+    if (b == 0 && threadIdx.x == 0) w.counts[1] = ncomp;
+    if (threadIdx.x == 0) s_run = off;
+    __syncthreads();
+    for (int64_t c0 = r0; c0 < r1; c0 += blockDim.x) {
+      const int64_t r = c0 + threadIdx.x;
+      const int root = r < r1 && __ldcg(w.parent + r) == (int32_t)r;
+      int ex, agg;
+      Scan(tmp).ExclusiveSum(root, ex, agg);
+      if (root) {
+        const int64_t lab = s_run + ex;
+        w.rank_label[r] = (int32_t)(lab + 1);
+        int32_t *st = w.stats + 8 * lab;
+        st[0] = 0;
+        st[1] = st[2] = st[3] = 0x7fffffff;
+        st[4] = st[5] = st[6] = -1;
+        st[7] = 0;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) s_run += agg;
+      __syncthreads();
+    }
+  }
+  grid.sync();
+
+  // 4. labels and component stats (ccl_stats_kernel's step)
+  {
+    const int lane = threadIdx.x & 31;
+    for (int64_t q0 = gtid & ~31ll; q0 < n_on; q0 += gstride) {
+      const int64_t r = q0 + lane;
+      const bool act = r < n_on;
+      int32_t lab = 0;
+      unsigned i = 0, j = 0, k = 0;
+      if (act) {
+        const int32_t root = uf_find(w.parent, (int32_t)r);
+        lab = __ldcg(w.rank_label + root);
+        if (root != (int32_t)r) w.rank_label[r] = lab;
+        const uint32_t l = (uint32_t)__ldcg(w.on_list + r);
+        const uint32_t q = l / (uint32_t)nx;
+        k = q / (uint32_t)ny;
+        i = l - q * (uint32_t)nx;
+        j = q - k * (uint32_t)ny;
+      }
+      const unsigned grp = __match_any_sync(0xffffffffu, act ? lab : -1);
+      const unsigned mn_i = __reduce_min_sync(grp, i), mx_i = __reduce_max_sync(grp, i);
+      const unsigned mn_j = __reduce_min_sync(grp, j), mx_j = __reduce_max_sync(grp, j);
+      const unsigned mn_k = __reduce_min_sync(grp, k), mx_k = __reduce_max_sync(grp, k);
+      if (act && lane == __ffs(grp) - 1) {
+        int32_t *st = w.stats + 8 * (int64_t)(lab - 1);
+        atomicAdd(st + 0, __popc(grp));
+        atomicMin(st + 1, (int32_t)mn_i);
+        atomicMin(st + 2, (int32_t)mn_j);
+        atomicMin(st + 3, (int32_t)mn_k);
+        atomicMax(st + 4, (int32_t)mx_i);
+        atomicMax(st + 5, (int32_t)mx_j);
+        atomicMax(st + 6, (int32_t)mx_k);
+      }
+    }
+  }
+  if (out == nullptr) return;
+  grid.sync();
+  export_components(w, out, cap, gtid, gstride);
+}
+
+// blocks of ccl_fused_kernel that are co-resident on every SM (cooperative launch)
+static int ccl_fused_grid() {
+  static const int g = [] {
+    int nb = 0, dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, ccl_fused_kernel, kFusedThreads, 0) !=
+            cudaSuccess || nb < 1)
+      return 0;
+    const int g = sms * (nb < 2 ? nb : 2);
+    return g < kMaxFusedGrid ? g : kMaxFusedGrid;
+  }();
+  return g;
+}
+
+static bool ccl_fused_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("FVV_CCL_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 }  // namespace fvv
 
 using namespace fvv;
@@ -420,6 +654,25 @@ int fvv_ccl26(const uint32_t *occ_dev, const fvv_grid *grid, void *ws_dev, size_
   }
   cudaStream_t st = (cudaStream_t)stream;
   CclWs w = ccl_layout(ws_dev, grid->dims);
+  const int fg = ccl_fused_enabled() ? ccl_fused_grid() : 0;
+  if (fg > 0) {  // one cooperative launch (w.sums holds its 2 x grid block sums)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = fg;
+    cfg.blockDim = kFusedThreads;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    cudaLaunchKernelEx(&cfg, ccl_fused_kernel, occ_dev, w, nx, ny, nz, comps_dev, comp_cap);
+    note_launches(1);
+    if (counts_dev) cudaMemcpyAsync(counts_dev, w.counts, 2 * sizeof(int64_t),
+                                    cudaMemcpyDeviceToDevice, st);
+    return cuda_check("fvv_ccl26");
+  }
   fill_async(w.counts, 0, 4 * sizeof(int64_t), st);
   WordRank wr{occ_dev, w.word_prefix, w.on_list, w.parent, w.words, nvox};
   onepass_scan(wr, nullptr, w.words, w.words, (void *)w.sums, w.counts + 0, st);
