@@ -268,3 +268,37 @@ def test_non_bool_silhouettes_are_coerced_like_reference(gpu, dtype):
     b = run_frame(cfg, rig, frames, sils=stacked.cuda())
     assert a.stats == b.stats
     assert np.array_equal(a.merged_mesh.triangles, b.merged_mesh.triangles)
+
+
+def test_ccl_separate_launches_match_oracle(gpu):
+    """B-2 runs as one cooperative launch (ccl_fused_kernel); FVV_CCL_FUSED=0
+    keeps the separate scan / union / scan / stats launches. Both numberings
+    equal the oracle's (the separate path runs in a child process: the switch
+    is read once per process)."""
+    import os
+    import subprocess
+    import sys
+
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, "tests")
+import oracle as O
+from paper_1903_11785_b200.hull import label_components
+from paper_1903_11785_b200.voxels import GridSpec, VoxelGrid
+rng = np.random.default_rng(7)
+for _ in range(6):
+    dims = tuple(int(d) for d in rng.integers(1, 60, 3))
+    dens = float(rng.choice([0.05, 0.3, 0.7]))
+    spec = GridSpec(origin=(0, 0, 0), spacing=1.0, dims=dims)
+    occ = rng.random(spec.num_voxels) < dens
+    lab = label_components(VoxelGrid(spec, occ))
+    ref_labels, ref_comps = O.label(occ, dims)
+    assert np.array_equal(lab.labels, ref_labels), (dims, dens)
+    assert len(lab.components) == len(ref_comps)
+print("ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FVV_CCL_FUSED="0")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
