@@ -43,7 +43,10 @@ struct CclWs {
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
-constexpr int kMaxFusedGrid = 4096;  // blocks of ccl_fused_kernel (sums capacity)
+constexpr int kMaxFusedGrid = 4096;
+#ifndef FVV_CCL_BPS
+#define FVV_CCL_BPS 2  // blocks per SM of the cooperative CCL grid
+#endif  // blocks of ccl_fused_kernel (sums capacity)
 
 // Most components a 26-connected grid can hold: one per 2x2x2 block.
 static int64_t max_components(const int64_t *dims) {
@@ -618,7 +621,7 @@ static int ccl_fused_grid() {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, ccl_fused_kernel, kFusedThreads, 0) !=
             cudaSuccess || nb < 1)
       return 0;
-    const int g = sms * (nb < 2 ? nb : 2);
+    const int g = sms * (nb < FVV_CCL_BPS ? nb : FVV_CCL_BPS);
     return g < kMaxFusedGrid ? g : kMaxFusedGrid;
   }();
   return g;
