@@ -657,10 +657,11 @@ def attach_executed(roof_stages, stage_ms):
     if "noise_filter_roi" in roof_stages:
         r = roof_stages["noise_filter_roi"]
         r.update({"bound": "latency", "ms": round(stage_ms["noise_filter_roi"], 4),
-                  "note": "launch / dependency-latency bound: a few thousand ON voxels "
-                          "through a rank scan, a run-based union-find, a root scan, "
-                          "stats and the ROI planner; its HBM fraction (algorithmic "
-                          "bytes / time) is kept in 'frac'"})
+                  "note": "dependency-latency bound: a few thousand ON voxels through a "
+                          "rank scan, a run-based union-find, a root scan and stats in one "
+                          "cooperative launch with grid barriers (ccl_fused_kernel), then "
+                          "the ROI planner; its HBM fraction (algorithmic bytes / time) is "
+                          "kept in 'frac'"})
 
 
 # ---------------------------------------------------------------- CPU arm

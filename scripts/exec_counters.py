@@ -43,7 +43,7 @@ def stage_of(names):
         elif n.startswith("carve_prep"):
             carves += 1
             stage = "B-1" if carves == 1 else "B-3"
-        elif "WordRank" in n:
+        elif "WordRank" in n or n.startswith("ccl_fused"):
             stage = "B-2"
         elif n.startswith("mesh_transpose"):
             stage = "C"
