@@ -12,7 +12,12 @@ namespace fvv {
 static thread_local char g_err[512] = "";
 static std::atomic<long long> g_launches{0};
 
-void note_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+static thread_local long long t_launches = 0;  // this thread's (graph capture counts its own)
+void note_launches(long long n) {
+  g_launches.fetch_add(n, std::memory_order_relaxed);
+  t_launches += n;
+}
+long long thread_launch_count() { return t_launches; }
 
 // cudaMemsetAsync as a kernel launched with programmatic serialisation:
 // inside a frame graph a memset node would break the chain of early-launched

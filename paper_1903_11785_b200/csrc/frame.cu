@@ -1202,7 +1202,7 @@ static int run_device_planned(fvv_frame *f, const uint8_t *masks_dev, const fvv_
     if (f->graph) cudaGraphExecDestroy(f->graph);
     f->graph = nullptr;
     f->graph_key.clear();
-    const long long n0 = fvv_launch_count();
+    const long long n0 = thread_launch_count();
     if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
       return cuda_check("fvv_frame_run capture");
     const int rc = enqueue_device_planned(f, masks_dev, virt, rank_pos, frames_dev, frame_off,
@@ -1220,7 +1220,7 @@ static int run_device_planned(fvv_frame *f, const uint8_t *masks_dev, const fvv_
     }
     cudaGraphDestroy(g);
     f->graph_key = key;
-    f->graph_launches = fvv_launch_count() - n0;
+    f->graph_launches = thread_launch_count() - n0;
     if (cudaGraphLaunch(f->graph, st) != cudaSuccess) return cuda_check("fvv_frame_run graph");
   } else {
     FVV_TRY(0, enqueue_device_planned(f, masks_dev, virt, rank_pos, frames_dev, frame_off,

@@ -19,6 +19,9 @@ void set_error(const char *fmt, ...);
 int cuda_check(const char *what);
 // kernels launched by this library (bench.py reports the timed-region delta)
 void note_launches(long long n);
+// kernels this host thread has launched (lanes capture their frame graphs
+// concurrently: a capture counts its own launches with this)
+long long thread_launch_count();
 
 // Programmatic dependent launch: every kernel is launched with the
 // programmatic-serialisation attribute and waits for its predecessor's
