@@ -189,6 +189,19 @@ def frame_config(cfg, budget) -> np.ndarray:
     return conf
 
 
+_FALLBACK_PTR = []
+
+
+def _fallback_ptr():
+    """Pointer to render.py's fallback colour (built once)."""
+    if not _FALLBACK_PTR:
+        from .render import FALLBACK_COLOR
+
+        _FALLBACK_PTR.append(_lib.host_ptr(np.ascontiguousarray(
+            np.asarray(FALLBACK_COLOR, dtype=np.uint8).reshape(3))))
+    return _FALLBACK_PTR[0]
+
+
 class FrameExecutor:
     """fvv_frame handle for one rig + PipelineConfig."""
 
@@ -217,17 +230,26 @@ class FrameExecutor:
                 pass
             self._h = None
 
-    def _rank_pos(self, virtual):
+    def _virtual_args(self, virtual):
+        """(fvv_camera record, rank positions) of a virtual camera and their
+        pointers, memoised on its parameter values: cam_table returns the
+        same record object for equal values, so a camera mutated in place
+        between frames gets a fresh ranking."""
         from .render import rank_cameras
 
-        key = id(virtual)
-        hit = self._ranks.get(key)
-        if hit is None or hit[0] is not virtual:
+        vt = cam_table([virtual])
+        hit = self._ranks.get(id(vt))
+        if hit is None or hit[0] is not vt:
             pos = {c.id: i for i, c in enumerate(self.cams)}
             arr = np.array([pos[i] for i in rank_cameras(virtual, self.cams)], dtype=np.int32)
-            hit = (virtual, arr)
-            self._ranks[key] = hit
-        return hit[1]
+            if len(self._ranks) > 64:
+                self._ranks.clear()
+            hit = (vt, arr, _lib.host_ptr(vt), _lib.host_ptr(arr))
+            self._ranks[id(vt)] = hit
+        return hit
+
+    def _rank_pos(self, virtual):
+        return self._virtual_args(virtual)[1]
 
     @property
     def last_mode(self) -> int:
@@ -240,40 +262,37 @@ class FrameExecutor:
         colour pass, frames_buf (uint8 CUDA tensor, or the int base address of
         mapped pinned host frames, see fvv_host_mapped) + frame_off (int64
         byte offset of each camera's (H, W, 3) frame from that base)."""
-        from .pipeline import StageError
-        from .render import FALLBACK_COLOR
-
         masks = mask_bytes(masks).reshape(-1)
         stats = np.zeros(1, dtype=_lib.FRAME_STATS_DTYPE)
         stage = ctypes.c_int(0)
         if virtual is not None:
             if frames_buf is None:
                 raise ValueError("the colour pass needs frames_buf/frame_off")
-            vt = cam_table([virtual])
-            rank = self._rank_pos(virtual)
-            fb = np.ascontiguousarray(np.asarray(
-                FALLBACK_COLOR if fallback is None else fallback, dtype=np.uint8).reshape(3))
+            _, _, vt_p, rank_p = self._virtual_args(virtual)
+            fb_p = _fallback_ptr() if fallback is None else _lib.host_ptr(np.ascontiguousarray(
+                np.asarray(fallback, dtype=np.uint8).reshape(3)))
             fptr = ctypes.c_void_p(int(frames_buf)) if isinstance(frames_buf, int) else \
                 _lib.dev_ptr(frames_buf)
-            args = (_lib.host_ptr(vt), _lib.host_ptr(rank), fptr,
-                    _lib.host_ptr(np.ascontiguousarray(frame_off, dtype=np.int64)),
-                    _lib.host_ptr(fb))
+            args = (vt_p, rank_p, fptr,
+                    _lib.host_ptr(np.ascontiguousarray(frame_off, dtype=np.int64)), fb_p)
         else:
             args = (ctypes.c_void_p(0),) * 5
         rc = _lib.load().fvv_frame_run(self._h, _lib.dev_ptr(masks), *args, stream_handle(),
                                        _lib.host_ptr(stats), ctypes.byref(stage))
         if rc != 0:
+            from .pipeline import StageError
+
             msg = _lib.load().fvv_last_error().decode(errors="replace")
             cause = ValueError(msg) if rc in (_lib.FVV_E_ARG, _lib.FVV_E_LIMIT) else \
                 _lib.FvvError(msg)
             raise StageError(STAGE_NAMES.get(stage.value, "B-1 sparse carve"), cause)
         outs = _lib.FrameOutputs()
         _lib.load().fvv_frame_get_outputs(self._h, ctypes.byref(outs))
-        n = int(outs.n_rois)
-        cid = np.zeros(max(n, 1), dtype=np.int64)
-        boxes = np.zeros((max(n, 1), 6))
-        grids = np.zeros(max(n, 1), dtype=_lib.GRID_DTYPE)
-        info = np.zeros((max(n, 1), 8), dtype=np.int64)
+        n = int(outs.n_rois)  # (fvv_frame_get_rois writes all n entries)
+        cid = np.empty(max(n, 1), dtype=np.int64)
+        boxes = np.empty((max(n, 1), 6))
+        grids = np.empty(max(n, 1), dtype=_lib.GRID_DTYPE)
+        info = np.empty((max(n, 1), 8), dtype=np.int64)
         _lib.load().fvv_frame_get_rois(self._h, _lib.host_ptr(cid), _lib.host_ptr(boxes),
                                        _lib.host_ptr(grids), _lib.host_ptr(info))
         return FrameOutput(stats[0], outs, (cid[:n], boxes[:n], grids[:n], info[:n]),
