@@ -331,6 +331,11 @@ typedef struct fvv_frame_stats {
  * graph capture + launch, 3 graph replay. */
 int fvv_frame_last_mode(const fvv_frame *f);
 
+/* Whether device-planned frames read their per-stage device times back into
+ * fvv_frame_stats.ms (default 1; the readout costs ~22 us of host time per
+ * frame). 0: ms is zero-filled. */
+int fvv_frame_set_stage_times(fvv_frame *f, int on);
+
 /* Device outputs of the last fvv_frame_run (valid until the next run):
  * merged-order triangles indexing verts (per-ROI slices via fvv_frame_rois),
  * visibility bits (ncam x vis_stride words), depth planes (rig order,

@@ -48,6 +48,7 @@ SYMBOLS = (
     "fvv_render_ellipsoids",
     "fvv_frame_create", "fvv_frame_destroy", "fvv_frame_run", "fvv_frame_get_outputs",
     "fvv_frame_last_mode",
+    "fvv_frame_set_stage_times",
     "fvv_frame_get_rois", "fvv_frame_readback_layout", "fvv_frame_readback",
     "fvv_synth_render", "fvv_erode_cross", "fvv_distance_map", "fvv_background",
     "fvv_extract_silhouette",

@@ -392,6 +392,7 @@ struct fvv_frame {
   std::vector<char> graph_key, pending_key;
   long long graph_launches = 0;
   int last_mode = 0;  // fvv_frame_last_mode
+  bool stage_times = true;  // fvv_frame_set_stage_times
 };
 
 // B-2's ON-voxel and component counts: the first words of the CCL workspace
@@ -1061,8 +1062,10 @@ static bool finish_device_planned(fvv_frame *f, bool colour) {
     S.covered_px = rcn[0];
     for (int c = 0; c < f->ncam; ++c) S.sourced_px += rcn[1 + c];
   }
+  // (eight cudaEventElapsedTime calls cost ~22 us of host time per frame)
   for (int e = 0; e < 8; ++e)
-    if (cudaEventElapsedTime(&S.ms[e], f->ev[e], f->ev[e + 1]) != cudaSuccess) S.ms[e] = 0.0f;
+    if (!f->stage_times || cudaEventElapsedTime(&S.ms[e], f->ev[e], f->ev[e + 1]) != cudaSuccess)
+      S.ms[e] = 0.0f;
   cudaGetLastError();
   return true;
 }
@@ -1266,6 +1269,12 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
 
 
 int fvv_frame_last_mode(const fvv_frame *f) { return f ? f->last_mode : -1; }
+
+int fvv_frame_set_stage_times(fvv_frame *f, int on) {
+  if (!f) return FVV_E_ARG;
+  f->stage_times = on != 0;
+  return FVV_OK;
+}
 
 int fvv_frame_get_outputs(const fvv_frame *f, fvv_frame_outputs *o) {
   memset(o, 0, sizeof(*o));

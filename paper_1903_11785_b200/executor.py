@@ -252,6 +252,17 @@ class FrameExecutor:
         return self._virtual_args(virtual)[1]
 
     @property
+    def stage_times(self) -> bool:
+        return getattr(self, "_stage_times", True)
+
+    @stage_times.setter
+    def stage_times(self, on: bool) -> None:
+        """Per-stage device times in each run's stats (ms); off saves ~22 us
+        of host time per device-planned frame (fvv_frame_set_stage_times)."""
+        _lib.load().fvv_frame_set_stage_times(self._h, ctypes.c_int(1 if on else 0))
+        self._stage_times = bool(on)
+
+    @property
     def last_mode(self) -> int:
         """How the last run went: 0 host-planned, 1 device-planned, 2 captured
         as a CUDA graph, 3 graph replay (fvv_frame_last_mode)."""

@@ -18,12 +18,15 @@ from paper_1903_11785_b200.executor import executor_for  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--frames", type=int, default=200)
+ap.add_argument("--no-stage-times", action="store_true",
+                help="skip the per-stage event readout (FrameExecutor.stage_times)")
 args = ap.parse_args()
 wl = workloads.get("C3")
 masks, frames = S.render_scene_device(wl.rig, wl.objects(1))
 fb = frames.reshape(-1)
 foff = np.arange(len(wl.rig), dtype=np.int64) * (frames.shape[1] * frames.shape[2] * 3)
 ex = executor_for(wl.cfg, wl.rig)
+ex.stage_times = not args.no_stage_times
 lib = _lib.load()
 native = {"t": 0.0}
 orig = lib.fvv_frame_run
@@ -48,6 +51,6 @@ with torch.cuda.stream(side):
     torch.cuda.synchronize()
     wall = (time.perf_counter() - t0) / args.frames * 1e6
 lib.fvv_frame_run = orig
-ms = float(np.sum(out.stats_raw["ms"][:7]))
+ms = float(np.sum(out.stats_raw["ms"][:7]))  # (0 without stage times)
 print(f"wall {wall:.1f} us/frame, native call {native['t'] / args.frames * 1e6:.1f} us, "
       f"python {wall - native['t'] / args.frames * 1e6:.1f} us, device stages {ms * 1e3:.1f} us")
