@@ -393,6 +393,20 @@ struct fvv_frame {
   long long graph_launches = 0;
   int last_mode = 0;  // fvv_frame_last_mode
   bool stage_times = true;  // fvv_frame_set_stage_times
+  // a graph replay begun by frame_begin and not yet ended: its inputs (for a
+  // host-planned redo) and the event recorded after its launch
+  struct Pending {
+    bool active = false;
+    const uint8_t *masks = nullptr, *frames = nullptr;
+    bool has_virt = false, has_off = false;
+    fvv_camera virt{};
+    int32_t rank_pos[FVV_MAX_CAMS] = {};
+    int64_t frame_off[FVV_MAX_CAMS] = {};
+    uint8_t fallback[3] = {0, 0, 0};
+    bool has_fallback = false;
+    cudaStream_t st = nullptr;
+  } pend;
+  cudaEvent_t launched = nullptr;
 };
 
 // B-2's ON-voxel and component counts: the first words of the CCL workspace
@@ -551,6 +565,7 @@ void fvv_frame_destroy(fvv_frame *f) {
   if (f->side) cudaStreamDestroy(f->side);
   if (f->fork) cudaEventDestroy(f->fork);
   if (f->join) cudaEventDestroy(f->join);
+  if (f->launched) cudaEventDestroy(f->launched);
   for (int e = 0; e < 9; ++e) cudaEventDestroy(f->ev[e]);
   if (f->host_small) cudaFreeHost(f->host_small);
   delete f;
@@ -1122,6 +1137,19 @@ static void reserve_buffers(fvv_frame *f) {
   f->caps_grown = false;
 }
 
+// A device-planned frame that has completed: its counts and tables, and the
+// capacities for the next ones. False: the frame must be redone host-planned.
+static bool finish_after_sync(fvv_frame *f, bool colour) {
+  const bool done = finish_device_planned(f, colour);
+  if (done) {
+    const int64_t *h = (const int64_t *)((const char *)f->host_small + kDs);
+    // (tiles / k-row words of this frame are not read back: their
+    // capacities grow through a host-planned frame when the planner reports one)
+    update_caps(f, h[7], 0, 0, h[8], h[9]);
+  }
+  return done;
+}
+
 // What a captured frame graph bakes in: the virtual camera, ranks, fallback
 // colour, stream, capacities and the masks' alignment class (the masks and
 // frame pointers are bound per frame through FrameInputs).
@@ -1166,18 +1194,29 @@ static bool device_planning_enabled() {
 
 // One device-planned frame: a plain enqueue, a graph capture (the second
 // frame with the same bindings) or a graph replay. True when it completed.
+// begin_only: launch a graph replay and return without waiting (done stays
+// false, *replayed tells whether it was launched); a frame that would not
+// replay is left untouched.
 static int run_device_planned(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt,
                               const int32_t *rank_pos, const uint8_t *frames_dev,
                               const int64_t *frame_off, const uint8_t *fallback, cudaStream_t st,
-                              int *out_stage, bool &done) {
+                              int *out_stage, bool &done, bool begin_only = false,
+                              bool *replayed = nullptr) {
   done = false;
-  memset(&f->stats, 0, sizeof(f->stats));
-  if (out_stage) *out_stage = 0;
-  if (f->caps_grown) reserve_buffers(f);
   const bool graphs = graphs_enabled() && st != nullptr && st != cudaStreamLegacy &&
                       st != cudaStreamPerThread;
   std::vector<char> key;
-  if (graphs) key = graph_key(f, masks_dev, virt, rank_pos, frames_dev, frame_off, fallback, st);
+  if (begin_only) {
+    *replayed = false;
+    if (!graphs || f->caps_grown || !f->graph) return FVV_OK;
+    key = graph_key(f, masks_dev, virt, rank_pos, frames_dev, frame_off, fallback, st);
+    if (key != f->graph_key) return FVV_OK;
+  }
+  memset(&f->stats, 0, sizeof(f->stats));
+  if (out_stage) *out_stage = 0;
+  if (f->caps_grown) reserve_buffers(f);
+  if (graphs && !begin_only)
+    key = graph_key(f, masks_dev, virt, rank_pos, frames_dev, frame_off, fallback, st);
   {  // this frame's input pointers, read by the pack and colour kernels
     if (f->inputs.ensure(sizeof(FrameInputs))) return FVV_E_CUDA;
     static thread_local FrameInputs in;
@@ -1198,6 +1237,12 @@ static int run_device_planned(fvv_frame *f, const uint8_t *masks_dev, const fvv_
     f->vis_stride = (nt_ub + 31) / 32 > 0 ? (nt_ub + 31) / 32 : 1;
     if (cudaGraphLaunch(f->graph, st) != cudaSuccess) return cuda_check("fvv_frame_run graph");
     note_launches(f->graph_launches);
+    if (begin_only) {
+      if (!f->launched) cudaEventCreateWithFlags(&f->launched, cudaEventDisableTiming);
+      cudaEventRecord(f->launched, st);
+      *replayed = true;
+      return cuda_check("fvv_frame_run graph");
+    }
   } else if (graphs && key == f->pending_key) {
     f->last_mode = 2;  // graph capture + launch
     // second frame with these bindings (buffers and dirty maps settled by the
@@ -1234,13 +1279,7 @@ static int run_device_planned(fvv_frame *f, const uint8_t *masks_dev, const fvv_
     if (out_stage) *out_stage = 8;
     return cuda_check("fvv_frame_run");
   }
-  done = finish_device_planned(f, virt != nullptr);
-  if (done) {
-    const int64_t *h = (const int64_t *)((const char *)f->host_small + kDs);
-    // (tiles / k-row words of this frame are not read back: their
-    // capacities grow through a host-planned frame when the planner reports one)
-    update_caps(f, h[7], 0, 0, h[8], h[9]);
-  }
+  done = finish_after_sync(f, virt != nullptr);
   return cuda_check("fvv_frame_run");
 }
 
@@ -1267,6 +1306,81 @@ int fvv_frame_run(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt
   return rc;
 }
 
+
+}  // extern "C"
+
+// fvv_frame_run in two halves for the sequence runner's lanes: a frame that
+// replays its graph is launched and left running (*async), so the lane can
+// finish its previous frame while this one runs; frame_end waits for it
+// (the event recorded after its launch, not the whole stream) and reads its
+// results back, or redoes it host-planned when the device planner handed it
+// back. Any other frame runs to completion in frame_begin.
+int fvv::frame_begin(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt,
+                     const int32_t *rank_pos, const uint8_t *frames_dev, const int64_t *frame_off,
+                     const uint8_t *fallback, void *stream, fvv_frame_stats *out_stats,
+                     int *out_stage, bool *async) {
+  *async = false;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (f->pend.active) {
+    set_error("fvv_frame: a begun frame was not ended");
+    return FVV_E_ARG;
+  }
+  if (f->caps.ready && device_planning_enabled()) {
+    bool done = false, replayed = false;
+    const int rc = run_device_planned(f, masks_dev, virt, rank_pos, frames_dev, frame_off,
+                                      fallback, st, out_stage, done, true, &replayed);
+    if (rc != FVV_OK) return rc;
+    if (replayed) {
+      fvv_frame::Pending &P = f->pend;
+      P.active = true;
+      P.masks = masks_dev;
+      P.frames = frames_dev;
+      P.has_virt = virt != nullptr;
+      if (virt) P.virt = *virt;
+      for (int c = 0; c < f->ncam && rank_pos; ++c) P.rank_pos[c] = rank_pos[c];
+      P.has_off = frame_off != nullptr;
+      for (int c = 0; c < f->ncam && frame_off; ++c) P.frame_off[c] = frame_off[c];
+      P.has_fallback = fallback != nullptr;
+      if (fallback) memcpy(P.fallback, fallback, 3);
+      P.st = st;
+      *async = true;
+      return FVV_OK;
+    }
+  }
+  return fvv_frame_run(f, masks_dev, virt, rank_pos, frames_dev, frame_off, fallback, stream,
+                       out_stats, out_stage);
+}
+
+int fvv::frame_end(fvv_frame *f, fvv_frame_stats *out_stats, int *out_stage) {
+  fvv_frame::Pending &P = f->pend;
+  if (!P.active) {
+    set_error("fvv_frame: no begun frame");
+    return FVV_E_ARG;
+  }
+  P.active = false;
+  if (out_stage) *out_stage = 0;
+  if (cudaEventSynchronize(f->launched) != cudaSuccess) {
+    if (out_stage) *out_stage = 8;
+    return cuda_check("fvv_frame_run");
+  }
+  if (finish_after_sync(f, P.has_virt)) {
+    if (out_stats) *out_stats = f->stats;
+    return cuda_check("fvv_frame_run");
+  }
+  f->last_mode = 0;  // handed back by the device planner: host-planned
+  const fvv_camera *virt = P.has_virt ? &P.virt : nullptr;
+  const int rc = run_host_planned(f, P.masks, virt, P.rank_pos, P.frames,
+                                  P.has_off ? P.frame_off : nullptr,
+                                  P.has_fallback ? P.fallback : nullptr, P.st, out_stats,
+                                  out_stage);
+  if (rc == FVV_OK && f->seen_plannable)
+    update_caps(f, f->seen_words, f->seen_tiles, f->seen_tw, f->seen_v, f->seen_s);
+  return rc;
+}
+
+cudaEvent_t fvv::frame_launched_event(const fvv_frame *f) { return f->launched; }
+
+extern "C" {
 
 int fvv_frame_last_mode(const fvv_frame *f) { return f ? f->last_mode : -1; }
 

@@ -32,6 +32,17 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 
 bool pdl_enabled();
 
+// fvv_frame_run split for pipelined callers (frame.cu): frame_begin launches
+// a graph replay without waiting (*async) or runs the frame to completion;
+// frame_end completes a begun frame; frame_launched_event is the event
+// recorded after the begun frame's launch.
+int frame_begin(fvv_frame *f, const uint8_t *masks_dev, const fvv_camera *virt,
+                const int32_t *rank_pos, const uint8_t *frames_dev, const int64_t *frame_off,
+                const uint8_t *fallback, void *stream, fvv_frame_stats *out_stats, int *out_stage,
+                bool *async);
+int frame_end(fvv_frame *f, fvv_frame_stats *out_stats, int *out_stage);
+cudaEvent_t frame_launched_event(const fvv_frame *f);
+
 // cudaMemsetAsync(p, value, bytes, st) as a programmatic-dependent kernel (api.cu)
 void fill_async(void *p, int value, size_t bytes, cudaStream_t st);
 

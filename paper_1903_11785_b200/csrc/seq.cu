@@ -135,6 +135,10 @@ struct Lane {
   std::mutex m;
   std::condition_variable cv_in, cv_out;
   int64_t n_run = 0;
+  // a frame begun on ex[pend_slot] (its graph replay running) whose results
+  // are read back after the lane has launched its next frame
+  fvv_seq_result *pend = nullptr;
+  int pend_slot = 0;
 };
 
 struct fvv_seq {
@@ -151,6 +155,15 @@ struct fvv_seq {
 };
 
 namespace {
+
+// FVV_SEQ_ASYNC=0: every frame completes before the lane takes the next
+bool async_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("FVV_SEQ_ASYNC");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 cudaEvent_t take_event(fvv_seq *s) {
   std::lock_guard<std::mutex> g(s->ev_m);
@@ -257,6 +270,102 @@ const uint8_t *stage_masks(fvv_seq *s, Lane &L, int slot, const Input &in, fvv_s
   return (const uint8_t *)L.masks[slot];
 }
 
+// After a lane's frame has completed on ex[slot]: ROI tables, the export
+// payload, and its readback queued on the readback stream behind `ran`.
+void finish_one(fvv_seq *s, Lane &L, int slot, fvv_seq_result *R, cudaEvent_t ran) {
+  fvv_frame *ex = L.ex[slot];
+  fvv_frame_outputs o;
+  fvv_frame_get_outputs(ex, &o);
+  R->nv = o.nv;
+  R->nt = o.nt;
+  R->vis_stride = o.vis_stride;
+  R->n_rois = o.n_rois;
+  const size_t nr = (size_t)o.n_rois;
+  R->comp.resize(nr);
+  R->boxes.resize(6 * nr);
+  R->grids.resize(nr);
+  R->info.resize(8 * nr);
+  fvv_frame_get_rois(ex, R->comp.data(), R->boxes.data(), R->grids.data(), R->info.data());
+  // 3. export payload (device) for a frame-sharded rank, behind the frame
+  if (s->cfg.export_payload) {
+    int64_t off[3], sz[3];
+    const int64_t tot = payload_layout(o.nv, o.nt, s->ncam, o.vis_stride, off, sz);
+    R->payload = s->dev_pool.acquire((size_t)(tot > 0 ? tot : 1));
+    if (!R->payload) {
+      R->status = FVV_E_CUDA;
+      R->stage = 8;
+      R->err = "fvv_seq: payload allocation failed";
+      return;
+    }
+    cudaStreamWaitEvent(L.readback, ran, 0);
+    const void *src[3] = {o.verts, o.tris, o.vis};
+    for (int i = 0; i < 3; ++i)
+      if (sz[i]) cudaMemcpyAsync((char *)R->payload->p + off[i], src[i], (size_t)sz[i],
+                                 cudaMemcpyDeviceToDevice, L.readback);
+    R->payload_bytes = tot;
+  }
+  // 4. readback into a pinned block
+  const int flags = s->cfg.readback_flags | (s->cfg.export_payload ? 4 : 0);
+  const int64_t total = fvv_frame_readback_layout(ex, flags, R->layout);
+  R->block = s->host_pool.acquire((size_t)(total > 0 ? total : 1));
+  if (!R->block) {
+    R->status = FVV_E_CUDA;
+    R->stage = 8;
+    R->err = "fvv_seq: pinned block allocation failed";
+    return;
+  }
+  cudaStreamWaitEvent(L.readback, ran, 0);
+  fvv_frame_readback(ex, R->block->p, flags, L.readback);
+  R->done = take_event(s);
+  cudaEventRecord(R->done, L.readback);
+  cudaEventRecord(L.slot_free[slot], L.readback);
+  L.slot_used[slot] = true;
+  const int e = fvv::cuda_check("fvv_seq lane");
+  if (e != FVV_OK) {
+    R->status = e;
+    R->stage = 8;
+    R->err = fvv_last_error();
+  }
+}
+
+void push_result(Lane &L, fvv_seq_result *R) {
+  {
+    std::lock_guard<std::mutex> g(L.m);
+    L.out.push_back(R);
+  }
+  L.cv_out.notify_all();
+}
+
+// The lane's begun frame: wait for it (not for the frame launched after
+// it), read it back, hand the result out.
+void end_pending(fvv_seq *s, Lane &L) {
+  fvv_seq_result *R = L.pend;
+  if (!R) return;
+  L.pend = nullptr;
+  const int slot = L.pend_slot;
+  int stage = 0;
+  const int rc = fvv::frame_end(L.ex[slot], &R->stats, &stage);
+  if (rc != FVV_OK) {
+    R->status = rc;
+    R->stage = stage;
+    R->err = fvv_last_error();
+    cudaGetLastError();
+  } else {
+    // (a frame redone host-planned ran after the lane's next frame on the
+    // compute stream: read it back behind everything queued there so far)
+    cudaEvent_t ran = fvv_frame_last_mode(L.ex[slot]) == 0 ? nullptr : fvv::frame_launched_event(L.ex[slot]);
+    cudaEvent_t own = nullptr;
+    if (!ran) {
+      own = take_event(s);
+      cudaEventRecord(own, L.compute);
+      ran = own;
+    }
+    finish_one(s, L, slot, R, ran);
+    if (own) give_event(s, own);
+  }
+  push_result(L, R);
+}
+
 void run_one(fvv_seq *s, Lane &L, Input &in, fvv_seq_result *R, const Input *next_in) {
   const int slot = (int)(L.n_run++ & 1);
   fvv_frame *ex = L.ex[slot];
@@ -264,14 +373,13 @@ void run_one(fvv_seq *s, Lane &L, Input &in, fvv_seq_result *R, const Input *nex
   if (L.slot_used[slot]) cudaStreamWaitEvent(st, L.slot_free[slot], 0);  // readback drained
   // 1. inputs (normally uploaded while the lane's previous frame ran)
   const uint8_t *masks = stage_masks(s, L, slot, in, R);
-  if (!masks) return;
+  if (!masks) {
+    end_pending(s, L);
+    push_result(L, R);
+    return;
+  }
   if (L.staged_id[slot] == in.id) cudaStreamWaitEvent(st, L.copied[slot], 0);
   L.staged_id[slot] = -1;  // consumed: the buffer is this frame's until it has run
-  if (next_in && !next_in->stop) {
-    // the other slot's previous frame has fully run (fvv_frame_run ends with a
-    // synchronisation), so its mask buffer can take the next frame's upload now
-    stage_masks(s, L, slot ^ 1, *next_in, nullptr);
-  }
   const bool colour = s->cfg.has_virtual && !in.frame_src.empty();
   const uint8_t *fbase = nullptr;
   int64_t foff[FVV_MAX_CAMS] = {};
@@ -290,6 +398,8 @@ void run_one(fvv_seq *s, Lane &L, Input &in, fvv_seq_result *R, const Input *nex
         R->status = FVV_E_CUDA;
         R->stage = 7;
         R->err = fvv_last_error();
+        end_pending(s, L);
+        push_result(L, R);
         return;
       }
       int64_t o = 0;
@@ -302,72 +412,43 @@ void run_one(fvv_seq *s, Lane &L, Input &in, fvv_seq_result *R, const Input *nex
       fbase = (const uint8_t *)L.frames[slot];
     }
   }
-  // 2. the frame
+  // 2. the frame: a graph replay is launched and left running while the
+  // lane finishes its previous frame; any other frame completes here
   int stage = 0;
-  const int rc = fvv_frame_run(ex, masks, colour ? &s->cfg.virt : nullptr, s->cfg.rank_pos, fbase,
-                               foff, s->cfg.fallback, st, &R->stats, &stage);
+  bool async = false;
+  const int rc = fvv::frame_begin(ex, masks, colour ? &s->cfg.virt : nullptr, s->cfg.rank_pos,
+                                  fbase, foff, s->cfg.fallback, st, &R->stats, &stage, &async);
+  end_pending(s, L);  // (in order: the previous frame's result first)
+  if (next_in && !next_in->stop) {
+    // the other slot's previous frame has completed (end_pending / a
+    // synchronous run), so its mask buffer can take the next frame's upload
+    stage_masks(s, L, slot ^ 1, *next_in, nullptr);
+  }
   if (rc != FVV_OK) {
     R->status = rc;
     R->stage = stage;
     R->err = fvv_last_error();
     cudaStreamSynchronize(st);
     cudaGetLastError();
+    push_result(L, R);
     return;
   }
-  fvv_frame_outputs o;
-  fvv_frame_get_outputs(ex, &o);
-  R->nv = o.nv;
-  R->nt = o.nt;
-  R->vis_stride = o.vis_stride;
-  R->n_rois = o.n_rois;
-  const size_t nr = (size_t)o.n_rois;
-  R->comp.resize(nr);
-  R->boxes.resize(6 * nr);
-  R->grids.resize(nr);
-  R->info.resize(8 * nr);
-  fvv_frame_get_rois(ex, R->comp.data(), R->boxes.data(), R->grids.data(), R->info.data());
-  // 3. export payload (device) for a frame-sharded rank
-  if (s->cfg.export_payload) {
-    int64_t off[3], sz[3];
-    const int64_t tot = payload_layout(o.nv, o.nt, s->ncam, o.vis_stride, off, sz);
-    R->payload = s->dev_pool.acquire((size_t)(tot > 0 ? tot : 1));
-    if (!R->payload) {
-      R->status = FVV_E_CUDA;
-      R->stage = 8;
-      R->err = "fvv_seq: payload allocation failed";
-      return;
-    }
-    const void *src[3] = {o.verts, o.tris, o.vis};
-    for (int i = 0; i < 3; ++i)
-      if (sz[i]) cudaMemcpyAsync((char *)R->payload->p + off[i], src[i], (size_t)sz[i],
-                                 cudaMemcpyDeviceToDevice, st);
-    R->payload_bytes = tot;
+  if (async && async_enabled()) {
+    L.pend = R;
+    L.pend_slot = slot;
+    return;
   }
-  // 4. readback into a pinned block
-  const int flags = s->cfg.readback_flags | (s->cfg.export_payload ? 4 : 0);
-  const int64_t total = fvv_frame_readback_layout(ex, flags, R->layout);
-  R->block = s->host_pool.acquire((size_t)(total > 0 ? total : 1));
-  if (!R->block) {
-    R->status = FVV_E_CUDA;
-    R->stage = 8;
-    R->err = "fvv_seq: pinned block allocation failed";
+  if (async) {  // (FVV_SEQ_ASYNC=0: complete it now)
+    L.pend = R;
+    L.pend_slot = slot;
+    end_pending(s, L);
     return;
   }
   cudaEvent_t ran = take_event(s);
   cudaEventRecord(ran, st);
-  cudaStreamWaitEvent(L.readback, ran, 0);
-  fvv_frame_readback(ex, R->block->p, flags, L.readback);
-  R->done = take_event(s);
-  cudaEventRecord(R->done, L.readback);
-  cudaEventRecord(L.slot_free[slot], L.readback);
-  L.slot_used[slot] = true;
+  finish_one(s, L, slot, R, ran);
   give_event(s, ran);  // (an event may be re-recorded once its waits are queued)
-  const int e = fvv::cuda_check("fvv_seq lane");
-  if (e != FVV_OK) {
-    R->status = e;
-    R->stage = 8;
-    R->err = fvv_last_error();
-  }
+  push_result(L, R);
 }
 
 void lane_main(fvv_seq *s, int k) {
@@ -377,12 +458,20 @@ void lane_main(fvv_seq *s, int k) {
     Input in;
     {
       std::unique_lock<std::mutex> g(L.m);
+      if (L.in.empty() && L.pend) {  // nothing queued: finish the running frame first
+        g.unlock();
+        end_pending(s, L);
+        g.lock();
+      }
       L.cv_in.wait(g, [&] { return !L.in.empty(); });
       in = std::move(L.in.front());
       L.in.pop_front();
     }
     L.cv_in.notify_all();  // room for the next submit
-    if (in.stop) return;
+    if (in.stop) {
+      end_pending(s, L);
+      return;
+    }
     fvv_seq_result *R = new fvv_seq_result();
     R->id = in.id;
     R->owner = s;
@@ -395,12 +484,7 @@ void lane_main(fvv_seq *s, int k) {
         have_next = true;
       }
     }
-    run_one(s, L, in, R, have_next ? &next_copy : nullptr);
-    {
-      std::lock_guard<std::mutex> g(L.m);
-      L.out.push_back(R);
-    }
-    L.cv_out.notify_all();
+    run_one(s, L, in, R, have_next ? &next_copy : nullptr);  // (it hands results out)
   }
 }
 
