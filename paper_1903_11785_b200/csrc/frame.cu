@@ -390,6 +390,7 @@ struct fvv_frame {
   // one CUDA graph of the device-planned frame per input binding
   cudaGraphExec_t graph = nullptr;
   std::vector<char> graph_key, pending_key;
+  std::vector<const void *> graph_bufs;  // the device buffers the graph was captured on
   long long graph_launches = 0;
   int last_mode = 0;  // fvv_frame_last_mode
   bool stage_times = true;  // fvv_frame_set_stage_times
@@ -1150,6 +1151,23 @@ static bool finish_after_sync(fvv_frame *f, bool colour) {
   return done;
 }
 
+// Every device buffer a captured frame graph may address: a host-planned
+// frame (redone or not plannable) can reallocate some of them without
+// growing the capacities, and the graph must then not replay.
+static std::vector<const void *> bound_buffers(const fvv_frame *f) {
+  const DevBuf *b[] = {&f->carve_ws, &f->code, &f->sil, &f->occ_c, &f->cnt_c, &f->ccl_ws,
+                       &f->comps, &f->occ_f, &f->cnt_f, &f->mesh_ws, &f->mesh_scratch,
+                       &f->mesh_totals, &f->mesh_info, &f->verts, &f->tris, &f->ntri,
+                       &f->raster_ws, &f->depth, &f->vis, &f->vplane_d, &f->vplane_id,
+                       &f->vraster_ws, &f->src, &f->rcounts, &f->color, &f->source,
+                       &f->covered, &f->dirty, &f->vdirty, &f->plan, &f->inputs};
+  std::vector<const void *> v;
+  v.reserve(sizeof(b) / sizeof(b[0]) + 1);
+  for (const DevBuf *d : b) v.push_back(d->p);
+  v.push_back(f->host_small_dev);
+  return v;
+}
+
 // What a captured frame graph bakes in: the virtual camera, ranks, fallback
 // colour, stream, capacities and the masks' alignment class (the masks and
 // frame pointers are bound per frame through FrameInputs).
@@ -1208,7 +1226,7 @@ static int run_device_planned(fvv_frame *f, const uint8_t *masks_dev, const fvv_
   std::vector<char> key;
   if (begin_only) {
     *replayed = false;
-    if (!graphs || f->caps_grown || !f->graph) return FVV_OK;
+    if (!graphs || f->caps_grown || !f->graph || bound_buffers(f) != f->graph_bufs) return FVV_OK;
     key = graph_key(f, masks_dev, virt, rank_pos, frames_dev, frame_off, fallback, st);
     if (key != f->graph_key) return FVV_OK;
   }
@@ -1229,6 +1247,11 @@ static int run_device_planned(fvv_frame *f, const uint8_t *masks_dev, const fvv_
     note_launches(1);
   }
   f->last_mode = 1;  // device-planned, enqueued
+  if (f->graph && bound_buffers(f) != f->graph_bufs) {  // a buffer moved under the graph
+    cudaGraphExecDestroy(f->graph);
+    f->graph = nullptr;
+    f->graph_key.clear();
+  }
   if (graphs && f->graph && key == f->graph_key) {
     f->last_mode = 3;  // graph replay
     f->stats.sparse_tests = f->coarse.dims[0] * f->coarse.dims[1] * f->coarse.dims[2];
@@ -1268,6 +1291,7 @@ static int run_device_planned(fvv_frame *f, const uint8_t *masks_dev, const fvv_
     }
     cudaGraphDestroy(g);
     f->graph_key = key;
+    f->graph_bufs = bound_buffers(f);
     f->graph_launches = thread_launch_count() - n0;
     if (cudaGraphLaunch(f->graph, st) != cudaSuccess) return cuda_check("fvv_frame_run graph");
   } else {

@@ -374,3 +374,35 @@ def test_device_planner_falls_back_to_host_planning(gpu):
         assert np.array_equal(bundle.merged_mesh.triangles, mt)
         for c in rig:
             assert np.array_equal(bundle.visibility[c.id], ref["visibility"][c.id]), c.id
+
+
+def test_sequence_lanes_redo_handed_back_frames(gpu):
+    """run_sequence's lanes launch a frame's graph replay and read the
+    previous frame back while it runs (frame_begin / frame_end); a replayed
+    frame the device planner hands back (more ROIs than a planned batch
+    holds, or ROIs beyond the capacities) is redone host-planned in
+    frame_end. Every frame of such a sequence equals run_frame's."""
+    from paper_1903_11785_b200 import synthetic as S
+    from paper_1903_11785_b200.pipeline import PipelineConfig, run_frame, run_sequence
+
+    rig = S.ring_rig(8, (0, 0, 300), 6000, 5000, 640, 480, 700)
+    cfg = PipelineConfig(stage_lo=(-3000, -3000, 0), stage_hi=(3000, 3000, 600),
+                         coarse_spacing=50.0, fine_spacing=25.0, t_small=1)
+    few = [S.Ellipsoid(center=(x, 0.0, 150.0), semi_axes=(60.0, 60.0, 150.0))
+           for x in (-1500.0, 0.0, 1500.0)]
+    many = [S.Ellipsoid(center=(x, y, 150.0), semi_axes=(60.0, 60.0, 150.0))
+            for x in np.linspace(-2600, 2600, 14) for y in np.linspace(-2600, 2600, 14)]
+    big = [S.Ellipsoid(center=(x, 0.0, 250.0), semi_axes=(400.0, 400.0, 250.0))
+           for x in (-1500.0, 0.0, 1500.0)]
+    scenes = [few] * 8 + [many, big, many, big] + [few] * 4
+    masks = [S.render_scene_device(rig, objs)[0] for objs in scenes]
+    frames = [{c.id: None for c in rig}] * len(scenes)
+    got = [b for b, _ in run_sequence(cfg, rig, frames, masks, None, lanes=1)]
+    assert len(got) == len(scenes)
+    for i, (m, b) in enumerate(zip(masks, got)):
+        ref = run_frame(cfg, rig, {c.id: None for c in rig}, sils=m)
+        assert b.stats == ref.stats, i
+        assert np.array_equal(b.merged_mesh.vertices, ref.merged_mesh.vertices), i
+        assert np.array_equal(b.merged_mesh.triangles, ref.merged_mesh.triangles), i
+        for c in rig:
+            assert np.array_equal(b.visibility[c.id], ref.visibility[c.id]), (i, c.id)
