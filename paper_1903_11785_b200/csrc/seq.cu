@@ -353,7 +353,9 @@ void end_pending(fvv_seq *s, Lane &L) {
   } else {
     // (a frame redone host-planned ran after the lane's next frame on the
     // compute stream: read it back behind everything queued there so far)
-    cudaEvent_t ran = fvv_frame_last_mode(L.ex[slot]) == 0 ? nullptr : fvv::frame_launched_event(L.ex[slot]);
+    cudaEvent_t ran = fvv_frame_last_mode(L.ex[slot]) == 0
+                          ? nullptr
+                          : fvv::frame_launched_event(L.ex[slot]);
     cudaEvent_t own = nullptr;
     if (!ran) {
       own = take_event(s);
