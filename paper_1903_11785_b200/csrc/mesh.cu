@@ -95,6 +95,11 @@ __device__ __forceinline__ uint32_t row_next(const uint32_t *tw, const MeshGridI
 __global__ void mesh_transpose_kernel(const MeshGrids *__restrict__ Gp, MeshBufs B) {
   pdl_wait();
   const MeshGrids &G = *Gp;
+  if (blockIdx.x == 0)  // the isovalue pass's per-grid counters (device-planned C has
+    for (int g = threadIdx.x; g < G.ngrid; g += blockDim.x) {  // no grid-counts launch)
+      B.info[8 * g + kInfoFallback] = 0;
+      B.info[8 * g + kInfoIncons] = 0;
+    }
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t total = G.tr_total;
@@ -233,15 +238,23 @@ struct CellFlags {
 };
 
 // per-grid vertex / surface-cell bases and counts (prefix at grid starts)
+// grid g's vertex range [vb, ve) and surface-cell range [sb, se) from the
+// scans' prefixes (the totals past the last grid)
+__device__ __forceinline__ void grid_ranges(const MeshGrids &G, const MeshBufs &B, int g,
+                                            int64_t &vb, int64_t &ve, int64_t &sb, int64_t &se) {
+  const int64_t s0 = G.tw_start[g], s1 = G.tw_start[g + 1];
+  vb = (s0 < G.tw_total) ? __ldcg(B.vprefix + 3 * s0) : __ldcg(B.totals + 0);
+  ve = (s1 < G.tw_total) ? __ldcg(B.vprefix + 3 * s1) : __ldcg(B.totals + 0);
+  sb = (s0 < G.tw_total) ? __ldcg(B.sprefix + s0) : __ldcg(B.totals + 1);
+  se = (s1 < G.tw_total) ? __ldcg(B.sprefix + s1) : __ldcg(B.totals + 1);
+}
+
 __global__ void mesh_grid_counts_kernel(const MeshGrids *__restrict__ Gp, MeshBufs B) {
   pdl_wait();
   const MeshGrids &G = *Gp;
   for (int g = threadIdx.x; g < G.ngrid; g += blockDim.x) {
-    const int64_t s0 = G.tw_start[g], s1 = G.tw_start[g + 1];
-    const int64_t vb = (3 * s0 < 3 * G.tw_total) ? B.vprefix[3 * s0] : B.totals[0];
-    const int64_t ve = (3 * s1 < 3 * G.tw_total) ? B.vprefix[3 * s1] : B.totals[0];
-    const int64_t sb = (s0 < G.tw_total) ? B.sprefix[s0] : B.totals[1];
-    const int64_t se = (s1 < G.tw_total) ? B.sprefix[s1] : B.totals[1];
+    int64_t vb, ve, sb, se;
+    grid_ranges(G, B, g, vb, ve, sb, se);
     int64_t *inf = B.info + 8 * g;
     inf[kInfoVbase] = vb;
     inf[kInfoV] = ve - vb;
@@ -439,7 +452,12 @@ __global__ void __launch_bounds__(128)
     const double *pon = on ? p0 : p1, *poff = on ? p1 : p0;
     double lam;
     if (exact) {
-      const bool gemv = B.info[8 * g + kInfoV] == 1;  // one-edge batch: numpy gemv order
+      // one-edge batch (numpy's gemv order): the grid's vertex range is this
+      // vertex alone, i.e. its neighbours in the (ordered) vertex list lie in
+      // other grids' V-element ranges
+      const int64_t lo_e = 3 * G.tw_start[g], hi_e = 3 * G.tw_start[g + 1];
+      const bool gemv = (v == 0 || (B.vert_key[v - 1] >> 5) < lo_e) &&
+                        (v + 1 >= nv || (B.vert_key[v + 1] >> 5) >= hi_e);
       int sel, incons;
       lam = edge_lambda(C, sil, pon, poff, gemv, sel, incons);
       if (sel < 0)
@@ -648,8 +666,13 @@ __global__ void mesh_slot_bases_kernel(const MeshGrids *__restrict__ Gp, MeshBuf
     const int g = g0 + lane;
     int64_t p0[5], p1[5], cnt = 0;
     if (g < G.ngrid) {
-      const int64_t *inf = B.info + 8 * g;
-      const int64_t s0 = inf[kInfoSbase], s1 = s0 + inf[kInfoS];
+      int64_t *inf = B.info + 8 * g;
+      int64_t vb, ve, s0, s1;
+      grid_ranges(G, B, g, vb, ve, s0, s1);
+      inf[kInfoVbase] = vb;
+      inf[kInfoV] = ve - vb;
+      inf[kInfoSbase] = s0;
+      inf[kInfoS] = s1 - s0;
       for (int t = 0; t < 5; ++t) {
         p0[t] = s0 < S ? B.cprefix[5 * s0 + t] : total->v[t];
         p1[t] = s1 < S ? B.cprefix[5 * s1 + t] : total->v[t];
@@ -884,8 +907,10 @@ int fvv::mesh_prepare_batch(const MeshGrids *G_dev, int64_t tw_cap, int ngrid_ma
     onepass_scan(ef, &G_dev->tw3, 0, 3 * tw_cap, (void *)B.sums, B.totals + 0, st);
     if (side) cudaStreamWaitEvent(st, join, 0);
   }
-  launch_k(mesh_grid_counts_kernel, 1, 128, 0, st, G_dev, B);
-  note_launches(1);
+  if (!scratch_dev) {  // (fvv_mesh_counts reads them; device-planned C: the slot-bases launch)
+    launch_k(mesh_grid_counts_kernel, 1, 128, 0, st, G_dev, B);
+    note_launches(1);
+  }
   return cuda_check("fvv_mesh_prepare");
 }
 
