@@ -1006,7 +1006,7 @@ static int enqueue_device_planned(fvv_frame *f, const uint8_t *masks_dev, const 
                              f->word_off_by_id.data(), &P->mesh, K.tw, FVV_MAX_GRIDS, cfg.exact,
                              cfg.fixed_isovalue, f->mesh_ws.p, f->mesh_ws.cap, K.v, K.s,
                              f->mesh_scratch.p, f->mesh_scratch.cap, f->verts.as<double>(),
-                             f->tris.as<int32_t>(), st, true));
+                             f->tris.as<int32_t>(), st, true, side_stream(f) != nullptr));
   stage_mark(f, 4, st);
   int64_t *totals = mesh_ws_totals(f->mesh_ws.p, K.tw, FVV_MAX_GRIDS);  // V, S, T
   const int64_t nt_ub = 5 * K.s;

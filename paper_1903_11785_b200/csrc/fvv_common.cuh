@@ -354,6 +354,8 @@ int mesh_emit_batch(const fvv_camera *cams_by_id, int ncam, const uint32_t *sil_
                     int ngrid_max, int exact, double fixed_iso, void *ws_dev, size_t ws_bytes,
                     int64_t cap_v, int64_t cap_s, void *scratch_dev, size_t scratch_bytes,
                     double *verts_dev, int32_t *tris_dev, cudaStream_t st,
-                    bool fused = false);  // fused: prepare wrote the vertex / cell lists
+                    bool fused = false,  // fused: prepare wrote the vertex / cell lists
+                    bool side_cleared = false);  // prepare (with a side stream) cleared the
+                                                 // triangle scan's status words
 
 }  // namespace fvv

@@ -887,7 +887,13 @@ int fvv::mesh_prepare_batch(const MeshGrids *G_dev, int64_t tw_cap, int ngrid_ma
   }
   MeshBufs B = bufs_from(ws_dev, L);
   B.occ = occ_dev;
-  fill_async(B.totals, 0, 32, st);
+  // one fill clears both scans' status words and the totals (contiguous:
+  // sums, sums2, totals) when the two scans run side by side
+  const bool one_fill = side && tw_cap > 0;
+  if (one_fill)
+    fill_async(B.sums, 0, (size_t)((char *)B.totals - (char *)B.sums) + 32, st);
+  else
+    fill_async(B.totals, 0, 32, st);
   if (tw_cap > 0) {
     launch_k(mesh_transpose_kernel, kMeshGrid, 256, 0, st, G_dev, B);
     note_launches(1);
@@ -899,12 +905,14 @@ int fvv::mesh_prepare_batch(const MeshGrids *G_dev, int64_t tw_cap, int ngrid_ma
     }
     // with a phase-B scratch, the scans also write the vertex and cell lists
     const ScratchLayout SL = scratch_layout(scratch_dev, cap_v, cap_s);
+    if (side && scratch_dev && cap_s > 0)  // the triangle scan's status words, off the main chain
+      fill_async(SL.cell_sums, 0, onepass_bytes<Slot5>(cap_s + 1), side);
     CellFlags cf{G_dev, B.tw, B.sflags, B.sprefix, scratch_dev ? SL.cell_key : nullptr, cap_s};
     onepass_scan(cf, &G_dev->tw_total, 0, tw_cap, (void *)(side ? B.sums2 : B.sums),
-                 B.totals + 1, side ? side : st);
+                 B.totals + 1, side ? side : st, one_fill);
     if (side) cudaEventRecord(join, side);
     EdgeFlags ef{G_dev, B.tw, B.eflags, B.vprefix, scratch_dev ? SL.vert_key : nullptr, cap_v};
-    onepass_scan(ef, &G_dev->tw3, 0, 3 * tw_cap, (void *)B.sums, B.totals + 0, st);
+    onepass_scan(ef, &G_dev->tw3, 0, 3 * tw_cap, (void *)B.sums, B.totals + 0, st, one_fill);
     if (side) cudaStreamWaitEvent(st, join, 0);
   }
   if (!scratch_dev) {  // (fvv_mesh_counts reads them; device-planned C: the slot-bases launch)
@@ -923,7 +931,7 @@ int fvv::mesh_emit_batch(const fvv_camera *cams_by_id, int ncam, const uint32_t 
                          int ngrid_max, int exact, double fixed_iso, void *ws_dev,
                          size_t ws_bytes, int64_t cap_v, int64_t cap_s, void *scratch_dev,
                          size_t scratch_bytes, double *verts_dev, int32_t *tris_dev,
-                         cudaStream_t st, bool fused) {
+                         cudaStream_t st, bool fused, bool side_cleared) {
   int rc = ensure_tables();
   if (rc) return rc;
   if (exact && (ncam < 1 || ncam > FVV_MAX_CAMS)) {
@@ -968,7 +976,9 @@ int fvv::mesh_emit_batch(const fvv_camera *cams_by_id, int ncam, const uint32_t 
   }
   if (cap_s > 0 && fused) {  // the cells evaluated inside the triangle scan
     TriCells tc{G_dev, B};
-    onepass_scan(tc, B.totals + 3, 0, cap_s, (void *)cell_sums, d_total, st);
+    // (status words cleared on the side stream during C's scans when
+    // mesh_prepare_batch ran with one)
+    onepass_scan(tc, B.totals + 3, 0, cap_s, (void *)cell_sums, d_total, st, side_cleared);
   } else if (cap_s > 0) {
     const int64_t cell_blocks = std::min<int64_t>(tw_cap / 256 + 1, 148 * 64);
     launch_k(mesh_cells_kernel, (unsigned)std::max<int64_t>(cell_blocks, kMeshGrid), 256, 0, st, G_dev,

@@ -303,9 +303,9 @@ inline size_t onepass_bytes(int64_t n_max) {
 
 template <class F, typename T>
 inline void onepass_scan(const F &f, const int64_t *n_dev, int64_t n_host, int64_t n_max,
-                         void *ws, T *total, cudaStream_t st) {
+                         void *ws, T *total, cudaStream_t st, bool zeroed = false) {
   const size_t sbytes = onepass_status_bytes<T>(n_max);
-  fill_async(ws, 0, sbytes + 64, st);
+  if (!zeroed) fill_async(ws, 0, sbytes + 64, st);  // (zeroed: the caller cleared ws)
   launch_k(onepass_scan_kernel<F, T>, kScanGrid, kScanThreads, 0, st, f, n_dev, n_host, (ScanStatus<T> *)ws, (unsigned long long *)((char *)ws + sbytes),
       total);
   note_launches(1);
