@@ -56,6 +56,8 @@ struct MeshBufs {
   double *verts;       // [V][3]
   int32_t *tris;       // [T][3] global vertex indices
   int64_t cap_v, cap_s;  // phase-B capacities (emit kernels skip a batch that exceeds them)
+  uint4 *zero;           // optional: cleared by the transpose kernel (scan status, totals)
+  int64_t zero_n;        // its 16-byte words
 };
 
 // phase B runs only when the counts fit the buffers it was given
@@ -100,6 +102,9 @@ __global__ void mesh_transpose_kernel(const MeshGrids *__restrict__ Gp, MeshBufs
       B.info[8 * g + kInfoFallback] = 0;
       B.info[8 * g + kInfoIncons] = 0;
     }
+  for (int64_t z = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; z < B.zero_n;
+       z += (int64_t)gridDim.x * blockDim.x)
+    B.zero[z] = make_uint4(0u, 0u, 0u, 0u);
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t total = G.tr_total;
@@ -889,11 +894,16 @@ int fvv::mesh_prepare_batch(const MeshGrids *G_dev, int64_t tw_cap, int ngrid_ma
   B.occ = occ_dev;
   // one fill clears both scans' status words and the totals (contiguous:
   // sums, sums2, totals) when the two scans run side by side
+  // with the scans side by side, the transpose kernel clears both scans'
+  // status words and the totals (contiguous: sums, sums2, totals; no fill
+  // launch on the chain)
   const bool one_fill = side && tw_cap > 0;
-  if (one_fill)
-    fill_async(B.sums, 0, (size_t)((char *)B.totals - (char *)B.sums) + 32, st);
-  else
+  if (one_fill) {
+    B.zero = (uint4 *)B.sums;
+    B.zero_n = (int64_t)(((char *)B.totals - (char *)B.sums) + 32 + 15) / 16;
+  } else {
     fill_async(B.totals, 0, 32, st);
+  }
   if (tw_cap > 0) {
     launch_k(mesh_transpose_kernel, kMeshGrid, 256, 0, st, G_dev, B);
     note_launches(1);
