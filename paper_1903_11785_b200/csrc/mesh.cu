@@ -658,12 +658,13 @@ struct TriCells {
 };
 
 // ---- B4: per-grid slot bases (one warp, a lane per grid) ---------------------
-__global__ void mesh_slot_bases_kernel(const MeshGrids *__restrict__ Gp, MeshBufs B,
-                                       const Slot5 *total) {
-  pdl_wait();
-  const MeshGrids &G = *Gp;
-  if (!emit_fits(B)) return;
-  if (blockIdx.x != 0) return;
+// slot_base[g][t] = first triangle index of slot t of grid g minus the slot
+// prefix at the grid's start (grids in order, slots in order inside a grid).
+// With `info`, also the per-grid vertex / cell / triangle ranges and the
+// triangle total (B.info, B.totals[2]).
+__device__ __forceinline__ void slot_bases_warp(const MeshGrids &G, const MeshBufs &B,
+                                                const Slot5 *total, int64_t *slot_base,
+                                                bool info) {
   const int lane = threadIdx.x & 31;
   const int64_t S = B.totals[1];
   int64_t carry = 0;  // triangles of the grids before this chunk of 32
@@ -671,13 +672,15 @@ __global__ void mesh_slot_bases_kernel(const MeshGrids *__restrict__ Gp, MeshBuf
     const int g = g0 + lane;
     int64_t p0[5], p1[5], cnt = 0;
     if (g < G.ngrid) {
-      int64_t *inf = B.info + 8 * g;
       int64_t vb, ve, s0, s1;
       grid_ranges(G, B, g, vb, ve, s0, s1);
-      inf[kInfoVbase] = vb;
-      inf[kInfoV] = ve - vb;
-      inf[kInfoSbase] = s0;
-      inf[kInfoS] = s1 - s0;
+      if (info) {
+        int64_t *inf = B.info + 8 * g;
+        inf[kInfoVbase] = vb;
+        inf[kInfoV] = ve - vb;
+        inf[kInfoSbase] = s0;
+        inf[kInfoS] = s1 - s0;
+      }
       for (int t = 0; t < 5; ++t) {
         p0[t] = s0 < S ? B.cprefix[5 * s0 + t] : total->v[t];
         p1[t] = s1 < S ? B.cprefix[5 * s1 + t] : total->v[t];
@@ -691,25 +694,46 @@ __global__ void mesh_slot_bases_kernel(const MeshGrids *__restrict__ Gp, MeshBuf
     }
     const int64_t tbase = carry + incl - cnt;
     if (g < G.ngrid) {
-      int64_t *inf = B.info + 8 * g;
-      inf[kInfoTbase] = tbase;
       int64_t run = tbase;
       for (int t = 0; t < 5; ++t) {
-        // slot_base[g][t] = first triangle index of slot t minus the prefix at the grid start
-        B.slot_base[5 * g + t] = run - p0[t];
+        slot_base[5 * g + t] = run - p0[t];
         run += p1[t] - p0[t];
       }
-      inf[kInfoT] = run - tbase;
+      if (info) {
+        B.info[8 * g + kInfoTbase] = tbase;
+        B.info[8 * g + kInfoT] = run - tbase;
+      }
     }
     carry += __shfl_sync(0xffffffffu, incl, 31);
   }
-  if (lane == 0) B.totals[2] = carry;
+  if (info && lane == 0) B.totals[2] = carry;
+}
+
+__global__ void mesh_slot_bases_kernel(const MeshGrids *__restrict__ Gp, MeshBufs B,
+                                       const Slot5 *total) {
+  pdl_wait();
+  const MeshGrids &G = *Gp;
+  if (!emit_fits(B)) return;
+  if (blockIdx.x != 0 || threadIdx.x >= 32) return;
+  slot_bases_warp(G, B, total, B.slot_base, true);
 }
 
 // ---- B5: triangle emission ----------------------------------------------------
-__global__ void mesh_emit_kernel(const MeshGrids *__restrict__ Gp, MeshBufs B) {
+// kSlots: each block first computes the slot bases itself into shared memory
+// (warp 0; block 0 also writes the per-grid ranges and the triangle total),
+// so no separate slot-bases launch runs between the triangle scan and here.
+template <bool kSlots>
+__global__ void mesh_emit_kernel(const MeshGrids *__restrict__ Gp, MeshBufs B,
+                                 const Slot5 *total) {
   pdl_wait();
   if (!emit_fits(B)) return;
+  __shared__ int64_t sbase[kSlots ? 5 * FVV_MAX_GRIDS : 1];
+  const int64_t *slot_base = B.slot_base;
+  if (kSlots) {
+    if (threadIdx.x < 32) slot_bases_warp(*Gp, B, total, sbase, blockIdx.x == 0);
+    __syncthreads();
+    slot_base = sbase;
+  }
   const int64_t S = __ldcg(B.totals + 1);
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < S;
        c += (int64_t)gridDim.x * blockDim.x) {
@@ -720,7 +744,7 @@ __global__ void mesh_emit_kernel(const MeshGrids *__restrict__ Gp, MeshBufs B) {
     const int32_t *tv = B.cell_tri + 15 * c;
     for (int t = 0; t < 5; ++t) {
       if (!((keep >> t) & 1)) continue;
-      const int64_t idx = B.slot_base[5 * g + t] + B.cprefix[5 * c + t];
+      const int64_t idx = slot_base[5 * g + t] + B.cprefix[5 * c + t];
       B.tris[3 * idx] = tv[3 * t];
       B.tris[3 * idx + 1] = tv[3 * t + 1];
       B.tris[3 * idx + 2] = tv[3 * t + 2];
@@ -999,9 +1023,15 @@ int fvv::mesh_emit_batch(const fvv_camera *cams_by_id, int ncam, const uint32_t 
   } else {
     fill_async(d_total, 0, sizeof(Slot5), st);
   }
-  launch_k(mesh_slot_bases_kernel, 1, 32, 0, st, G_dev, B, d_total);
-  if (cap_s > 0) launch_k(mesh_emit_kernel, kMeshGrid, 256, 0, st, G_dev, B);
-  note_launches(1 + (cap_s > 0 ? 1 : 0));
+  if (cap_s > 0 && fused) {  // the emit blocks compute the slot bases themselves
+    launch_k(mesh_emit_kernel<true>, kMeshGrid, 256, 0, st, G_dev, B, (const Slot5 *)d_total);
+    note_launches(1);
+  } else {
+    launch_k(mesh_slot_bases_kernel, 1, 32, 0, st, G_dev, B, (const Slot5 *)d_total);
+    if (cap_s > 0) launch_k(mesh_emit_kernel<false>, kMeshGrid, 256, 0, st, G_dev, B,
+                            (const Slot5 *)d_total);
+    note_launches(1 + (cap_s > 0 ? 1 : 0));
+  }
   return cuda_check("fvv_mesh_emit");
 }
 
