@@ -426,7 +426,7 @@ def run_b200(args):
         # (>= 6 frames per executor, two executors per lane: host-planned,
         # device-planned, graph capture, and capacity growth over the cycled
         # frames all happen before the timed region)
-        run_e2e(max(args.warmup, 2 * len(host) + 2, 12 * lanes + 2))
+        run_e2e(max(args.warmup, 4 * len(host) + 2, 24 * lanes + 2))
         torch.cuda.synchronize()
         barrier(world)
         R.H2D_BYTES["frames"] = R.H2D_BYTES["masks"] = 0

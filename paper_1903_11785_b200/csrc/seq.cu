@@ -68,7 +68,9 @@ class Pool {
       if (best->p) device_ ? cudaFree(best->p) : cudaFreeHost(best->p);
       best->p = nullptr;
       best->cap = 0;
-      const size_t want = bytes + bytes / 4 + 4096;
+      // generous headroom: a block re-pinned later (frames vary in size)
+      // costs a device-wide synchronisation in cudaFreeHost and ms of pinning
+      const size_t want = bytes + bytes / 2 + 4096;
       const cudaError_t e = device_ ? cudaMalloc(&best->p, want) : cudaHostAlloc(&best->p, want, 0);
       if (e != cudaSuccess) {
         cudaGetLastError();
