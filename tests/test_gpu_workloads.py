@@ -406,3 +406,56 @@ def test_sequence_lanes_redo_handed_back_frames(gpu):
         assert np.array_equal(b.merged_mesh.triangles, ref.merged_mesh.triangles), i
         for c in rig:
             assert np.array_equal(b.visibility[c.id], ref.visibility[c.id]), (i, c.id)
+
+
+def test_executor_with_moving_viewpoint_and_stage_times_off(gpu):
+    """One executor, the virtual viewpoint alternating A, B, A, B, A, A, A
+    (the captured graph's key changes with the viewpoint: plain enqueues,
+    a capture and replays of A), per-stage times switched off: every
+    frame's virtual view, mesh and stats equal a fresh executor's; stage
+    times are zero-filled while off and present again when switched on."""
+    import torch
+
+    from paper_1903_11785_b200 import synthetic as S, workloads
+    from paper_1903_11785_b200.executor import FrameExecutor
+    from paper_1903_11785_b200.workloads import _virtual_on_ring
+
+    wl = workloads.get("C3")
+    masks, frames = S.render_scene_device(wl.rig, wl.objects(3))
+    fb = frames.reshape(-1)
+    foff = np.arange(len(wl.rig), dtype=np.int64) * (frames.shape[1] * frames.shape[2] * 3)
+    view_a = wl.virtual
+    view_b = _virtual_on_ring(100, (0, 0, 1000), 15000, 4000, 1920, 1080, 1600, 40.0)
+
+    def run(ex, view):
+        out = ex.run(masks, view, fb, foff)
+        host = out.to_host(wl.rig, keep_depths=False)
+        torch.cuda.synchronize()
+        return out.stats(), {k: np.array(v) for k, v in host.items()}, np.array(out.stats_raw["ms"])
+
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        ref = {}
+        for name, view in (("a", view_a), ("b", view_b)):
+            s, h, _ = run(FrameExecutor(wl.cfg, wl.rig), view)
+            ref[name] = (s, h)
+        ex = FrameExecutor(wl.cfg, wl.rig)
+        ex.stage_times = False
+        modes = []
+        for name in "ababaaa":
+            s, h, ms = run(ex, view_a if name == "a" else view_b)
+            modes.append(ex.last_mode)
+            s_ref, h_ref = ref[name]
+            assert s == s_ref, name
+            words = (s["triangles"] + 31) // 32
+            for k in h_ref:
+                a, b = h[k], h_ref[k]
+                if k == "vis":
+                    a, b = a[:, :words], b[:, :words]
+                assert np.array_equal(a, b), (name, k)
+            if modes[-1] != 0:  # (host-planned frames time their stages on the host path)
+                assert not ms.any(), (name, ms)
+        assert modes[-1] == 3, modes  # viewpoint A replayed from its graph
+        ex.stage_times = True
+        _, _, ms = run(ex, view_a)
+        assert ms[:7].sum() > 0
