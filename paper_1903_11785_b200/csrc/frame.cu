@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(kPlanThreads)
   // per-grid prefixes (one warp, 32 grids per step): occupancy words, tiles, k-row words
   if (warp == 0) {
     int64_t cw = 0, ct = 0, ck = 0, dense = 0, cr = 0;
-    for (int g0 = 0; g0 < FVV_MAX_GRIDS; g0 += 32) {
+    for (int g0 = 0; g0 < nroi; g0 += 32) {  // (grids past nroi add nothing)
       const int g = g0 + lane;
       const bool live = g < nroi;
       int64_t w = live ? s_words[g] : 0, t = live ? s_tiles[g] : 0, k = 0, vox = 0;
@@ -311,12 +311,16 @@ __global__ void __launch_bounds__(kPlanThreads)
       dense += __shfl_sync(0xffffffffu, iv, 31);
       cr += __shfl_sync(0xffffffffu, ir, 31);
     }
+    int st = s_status;
+    if (cw > a.cap_words || ct > a.cap_tiles || ck > a.cap_tw) st |= kPlanCapacity;
+    if (3 * ck >= ((int64_t)1 << 31)) st |= kPlanError;
+    const bool run = st == 0;  // otherwise the device stages find nothing to do
+    const int ng = run ? nroi : 0;
+    for (int g = ng + lane; g <= FVV_MAX_GRIDS; g += 32) {  // the tables' tails, lane-parallel
+      plan->carve.blk_start[g] = run ? ct : 0;
+      plan->mesh.tw_start[g] = run ? ck : 0;
+    }
     if (lane == 0) {
-      int st = s_status;
-      if (cw > a.cap_words || ct > a.cap_tiles || ck > a.cap_tw) st |= kPlanCapacity;
-      if (3 * ck >= ((int64_t)1 << 31)) st |= kPlanError;
-      const bool run = st == 0;  // otherwise the device stages find nothing to do
-      const int ng = run ? nroi : 0;
       plan->status = st;
       plan->nroi = nroi_all;
       plan->dense_tests = dense;
@@ -324,12 +328,10 @@ __global__ void __launch_bounds__(kPlanThreads)
       plan->carve.ngrid = ng;
       plan->carve.tile_log2 = 4;
       plan->carve.total_tiles = run ? ct : 0;
-      for (int g = ng; g <= FVV_MAX_GRIDS; ++g) plan->carve.blk_start[g] = run ? ct : 0;
       plan->mesh.ngrid = ng;
       plan->mesh.tw_total = run ? ck : 0;
       plan->mesh.tw3 = run ? 3 * ck : 0;
       plan->mesh.tr_total = run ? cr : 0;
-      for (int g = ng; g <= FVV_MAX_GRIDS; ++g) plan->mesh.tw_start[g] = run ? ck : 0;
     }
   }
 }

@@ -426,6 +426,7 @@ def test_executor_with_moving_viewpoint_and_stage_times_off(gpu):
     foff = np.arange(len(wl.rig), dtype=np.int64) * (frames.shape[1] * frames.shape[2] * 3)
     view_a = wl.virtual
     view_b = _virtual_on_ring(100, (0, 0, 1000), 15000, 4000, 1920, 1080, 1600, 40.0)
+    torch.cuda.synchronize()  # (rendered on the default stream; the runs use `side`)
 
     def run(ex, view):
         out = ex.run(masks, view, fb, foff)
