@@ -122,12 +122,11 @@ __global__ void pack_wide_kernel(const __grid_constant__ PackParams p) {
     uint32_t bits = 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      // byte j of q[k] nonzero -> bit 4k + j
-      const uint32_t v = q[k];
-      bits |= (uint32_t)((v & 0x000000ffu) != 0) << (4 * k);
-      bits |= (uint32_t)((v & 0x0000ff00u) != 0) << (4 * k + 1);
-      bits |= (uint32_t)((v & 0x00ff0000u) != 0) << (4 * k + 2);
-      bits |= (uint32_t)((v & 0xff000000u) != 0) << (4 * k + 3);
+      // byte j of q[k] nonzero -> bit 4k + j: 0xff per nonzero byte, its top
+      // bits gathered into bits 28..31 by one multiply (the four partial
+      // products land on distinct bits, so nothing carries)
+      const uint32_t ne = __vcmpne4(q[k], 0u) & 0x80808080u;
+      bits |= ((ne * 0x00204081u) >> 28) << (4 * k);
     }
     p.sil[p.sil_off[c] + local] = bits;
   }
