@@ -380,15 +380,21 @@ def run_b200(args):
             on rank f mod N; at N > 1 every frame's mesh + visibility is
             gathered to rank 0 over NCCL (run_sequence_sharded)."""
             if world == 1:
-                fr = [host[(i + i // lanes) % len(host)][1] for i in range(nsteps)]
-                ms_ = [host[(i + i // lanes) % len(host)][0] for i in range(nsteps)]
+                # input (i + i // 2 lanes) mod F: each lane runs its frames on two
+                # executors in turn, and this way both of them meet every input
+                # within 2 F rounds (the warm-up covers that: no executor sees a
+                # new input, i.e. no capacity growth or graph capture, in the
+                # timed run whatever lane the sequence runner starts it on)
+                idx = [(i + i // (2 * lanes)) % len(host) for i in range(nsteps)]
+                fr = [host[k][1] for k in idx]
+                ms_ = [host[k][0] for k in idx]
                 for bundle, img in run_sequence(cfg, rig, fr, ms_, virt, lanes=lanes):
                     yield bundle, img
                 return
 
             def source(f):  # the j-th frame of this rank is global frame rank + j * N
                 j = f // world
-                m_h, fr_h = host[(j + j // lanes) % len(host)]
+                m_h, fr_h = host[(j + j // (2 * lanes)) % len(host)]
                 return fr_h, m_h
 
             for _, bundle, img in run_sequence_sharded(cfg, rig, source, nsteps * world, virt,
