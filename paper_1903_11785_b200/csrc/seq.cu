@@ -42,6 +42,7 @@ struct Block {
 // the lane's acquire until the caller frees the result that owns it.
 class Pool {
  public:
+  static constexpr size_t kMaxBlocks = 96;
   explicit Pool(bool device) : device_(device) {}
   ~Pool() {
     for (Block *b : blocks_) {
@@ -55,11 +56,15 @@ class Pool {
     for (Block *b : blocks_)
       if (!b->busy && b->cap >= bytes && (!best || b->cap < best->cap)) best = b;
     if (!best) {
-      for (Block *b : blocks_)  // grow a free block rather than adding one
-        if (!b->busy) {
-          best = b;
-          break;
-        }
+      // add a block while the pool is small: re-sizing a free one frees it
+      // first, and cudaFree / cudaFreeHost wait for the whole device (every
+      // lane stalls); past kMaxBlocks a free block is re-sized
+      if (blocks_.size() >= kMaxBlocks)
+        for (Block *b : blocks_)
+          if (!b->busy) {
+            best = b;
+            break;
+          }
       if (!best) {
         best = new Block();
         best->device = device_;
